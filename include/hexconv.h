@@ -1,0 +1,215 @@
+/*
+ * hexconv.h -- C ABI of the B200-native hexagonal convolution / pooling
+ * library (libhexconv.so), after HexagDLy (Steppa & Holch, arXiv 1903.01814).
+ *
+ * Data model (Sec. 2.1 "Input Format"): a hexagonally
+ * sampled image is stored in a square tensor by "shifting every second column
+ * upwards by half the distance between neighbouring pixels"; rows are counted
+ * top->bottom and columns left->right.  `parity` selects which columns were
+ * shifted: HEX_PARITY_ODD_LOW (0, the paper's default reading, A1)
+ * means odd tensor columns are physically half a pitch lower.  Cells without a
+ * hexagonal pixel hold arbitrary values and are treated as ordinary data.
+ *
+ * Kernel of size n (Sec. 2.2): all pixels within n layers
+ * of neighbours of the centre, T(n) = 3n(n+1)+1 taps.  Weights are indexed
+ * [Cout][Cin][T] with taps in canonical order: column-major left->right,
+ * top->bottom (A2).
+ *
+ * Stride s: kernel centres form the lattice
+ * anchored at pixel (0,0) with s equal steps along the three hex axes; output
+ * column C is input column s*C, its rows are rho(C)+s*R with
+ * rho(C) = floor((s*C+parity)/2) mod s, and every column is truncated to the
+ * shortest one ("steps that would lead to an output with columns of unequal
+ * length are neglected", A6).  Wo = floor((W-1)/s)+1,
+ * Ho = min_C floor((H-1-rho(C))/s)+1.
+ *
+ * Conventions (all entry points):
+ *  - Every tensor pointer is a caller-owned CUDA DEVICE pointer unless the
+ *    argument says "host".  Tensors are dense and contiguous in the declared
+ *    layout: HEX_NCHW = [B][C][H][W], HEX_NHWC = [B][H][W][C].
+ *  - Argument validation is synchronous; on error nothing is launched and a
+ *    status other than HEX_OK is returned.  Kernels run asynchronously on
+ *    `stream` (a cudaStream_t; NULL = legacy default stream).  A launch
+ *    failure returns HEX_ERR_CUDA; device faults surface at the caller's next
+ *    synchronisation.
+ *  - No device memory is allocated inside a call: scratch space is passed in
+ *    `ws` (device) of `ws_bytes`, sized by hex_conv2d_workspace_size().
+ *  - Thread-safe and re-entrant.  Results are deterministic (no floating
+ *    point atomics): the same inputs give bitwise identical outputs.
+ *  - HEX_BF16 tensors use round-to-nearest-even from fp32 accumulators.
+ *    Weight/bias gradients are always fp32.  Bias is always fp32.
+ *  - There is no CPU path: every entry point that touches tensor data runs
+ *    CUDA kernels for sm_100a.
+ */
+#ifndef HEXCONV_H_
+#define HEXCONV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define HEX_API __attribute__((visibility("default")))
+#else
+#define HEX_API
+#endif
+
+/* Same type as cudaStream_t (driver_types.h: typedef struct CUstream_st* cudaStream_t). */
+typedef struct CUstream_st* hex_stream_t;
+
+typedef enum {
+    HEX_OK = 0,
+    HEX_ERR_INVALID_ARG = 1,   /* null pointer, n < 0, stride < 1, bad enum, ... */
+    HEX_ERR_SHAPE = 2,         /* non-positive dimension, channel mismatch        */
+    HEX_ERR_EMPTY_LATTICE = 3, /* Ho or Wo would be 0 (A7)              */
+    HEX_ERR_DTYPE = 4,
+    HEX_ERR_LAYOUT = 5,
+    HEX_ERR_ALIGNMENT = 6,     /* pointer not 16-byte aligned where required      */
+    HEX_ERR_WORKSPACE = 7,     /* ws too small or NULL when required              */
+    HEX_ERR_UNSUPPORTED = 8,   /* valid but unsupported (e.g. n > HEX_MAX_N)      */
+    HEX_ERR_CUDA = 9           /* a CUDA runtime call failed                      */
+} hex_status_t;
+
+typedef enum { HEX_F32 = 0, HEX_BF16 = 1 } hex_dtype_t;
+typedef enum { HEX_NCHW = 0, HEX_NHWC = 1 } hex_layout_t;
+typedef enum { HEX_PARITY_ODD_LOW = 0, HEX_PARITY_EVEN_LOW = 1 } hex_parity_t;
+typedef enum { HEX_POOL_MAX = 0, HEX_POOL_AVG = 1 } hex_pool_mode_t;
+
+#define HEX_MAX_N 7   /* largest supported kernel size (T = 169) */
+
+typedef struct {
+    int32_t batch, in_channels, out_channels, height, width;
+    int32_t kernel_size; /* n >= 0; T(n) = 3n(n+1)+1 taps                          */
+    int32_t stride;      /* s >= 1                                                 */
+    int32_t parity;      /* hex_parity_t of the input grid                         */
+    int32_t dtype;       /* hex_dtype_t of x, y, w, dy, dx                         */
+    int32_t layout;      /* hex_layout_t of x, y, dy, dx                           */
+} hex_conv2d_desc_t;
+
+typedef struct {
+    int32_t batch, channels, height, width;
+    int32_t kernel_size; /* n >= 1 */
+    int32_t stride;      /* s >= 1 */
+    int32_t parity, dtype, layout;
+    int32_t mode;        /* hex_pool_mode_t */
+} hex_pool2d_desc_t;
+
+/* ---------------------------------------------------------------- geometry */
+
+/* T(n) = 3n(n+1)+1, or -1 if n < 0. */
+HEX_API int32_t hex_num_taps(int32_t n);
+
+/* Output grid of the stride lattice.  Ho, Wo,
+ * parity_out are host pointers.  parity_out is the parity convention of the
+ * output grid (pitch s): which output columns are physically lower.
+ * Errors: HEX_ERR_INVALID_ARG (s < 1, bad parity, NULL), HEX_ERR_SHAPE
+ * (H or W < 1), HEX_ERR_EMPTY_LATTICE (Ho == 0). */
+HEX_API hex_status_t hex_output_shape(int32_t H, int32_t W, int32_t stride, int32_t parity,
+                              int32_t* Ho, int32_t* Wo, int32_t* parity_out);
+
+/* Test hook: the offset displacement of every tap for a centre whose column
+ * has parity p = (col + parity) mod 2.  dc_dr (host, 2*T int32) receives
+ * (dc, drow) pairs in canonical order.  (A2) */
+HEX_API hex_status_t hex_tap_offsets(int32_t n, int32_t centre_col_parity, int32_t* dc_dr);
+
+/* Test hook: device int32 map [Ho][Wo][T], entry = r*W + c of tap t of
+ * output (R,C), or -1 when that neighbour lies outside the grid.  Uses
+ * desc->height/width/kernel_size/stride/parity only. */
+HEX_API hex_status_t hex_conv2d_gather_map(const hex_conv2d_desc_t* desc, int32_t* map, hex_stream_t stream);
+
+/* ---------------------------------------------------------------- convolution */
+
+/* Workspace bytes needed by pass 0 = fwd, 1 = bwd_data, 2 = bwd_weight.
+ * bytes is a host pointer.  0 means ws may be NULL. */
+HEX_API hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* desc, int32_t pass, size_t* bytes);
+
+/* Forward (A3 cross-correlation,
+ * A4 zero contribution of off-grid neighbours):
+ *   y[b,co,R,C] = bias[co] + sum_ci sum_t w[co,ci,t] * x[b,ci, centre(R,C)+off_t]
+ * then y = max(y, 0) if fuse_relu.
+ * x: [B,Cin,H,W] in desc layout/dtype.  w: [Cout][Cin][T] in desc dtype.
+ * bias: fp32 [Cout] or NULL.  y: [B,Cout,Ho,Wo] in desc layout/dtype.
+ * bf16 + NHWC with Cin, Cout multiples of 16 and s == 1 runs on the
+ * tcgen05 tensor-core path; everything else on the CUDA-core stencil path. */
+HEX_API hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* desc, const void* x, const void* w,
+                            const float* bias, int32_t fuse_relu, void* y,
+                            void* ws, size_t ws_bytes, hex_stream_t stream);
+
+/* Backward w.r.t. the input: the adjoint of the forward map,
+ *   dx[b,ci,p] = sum_co sum_{(o,t): centre(o)+off_t = p} w[co,ci,t] * dy[b,co,o].
+ * dy: [B,Cout,Ho,Wo]; dx: [B,Cin,H,W] (overwritten).
+ * relu_y (optional, may be NULL): a tensor shaped like dx (the ReLU output
+ * that was this layer's input); when given, dx is multiplied by (relu_y > 0)
+ * -- the fused ReLU backward of the previous layer. */
+HEX_API hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* desc, const void* dy, const void* w,
+                                 const void* relu_y, void* dx,
+                                 void* ws, size_t ws_bytes, hex_stream_t stream);
+
+/* Backward w.r.t. weights and bias:
+ *   dw[co,ci,t] = sum_{b,o} dy[b,co,o] * x[b,ci,centre(o)+off_t]   (off-grid -> 0)
+ *   dbias[co]   = sum_{b,o} dy[b,co,o]
+ * dw: fp32 [Cout][Cin][T]; dbias fp32 [Cout] or NULL.  accumulate != 0 adds
+ * into dw/dbias instead of overwriting.  Deterministic two-stage reduction. */
+HEX_API hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* desc, const void* x, const void* dy,
+                                   float* dw, float* dbias, int32_t accumulate,
+                                   void* ws, size_t ws_bytes, hex_stream_t stream);
+
+/* ---------------------------------------------------------------- pooling */
+
+/* Pooling (the sub-convolutions are replaced by pooling
+ * and "combined with aggregation functions", same padding/striding scheme).
+ * HEX_POOL_MAX: y = x at the first strict maximum over the in-grid
+ * neighbourhood in canonical tap order (A8, A9); argmax_tap
+ * (uint8 [B,C,Ho,Wo] in desc layout, may be NULL) receives that tap index.
+ * HEX_POOL_AVG: y = in-grid sum / in-grid count (A8). */
+HEX_API hex_status_t hex_pool2d_fwd(const hex_pool2d_desc_t* desc, const void* x, void* y,
+                            uint8_t* argmax_tap, hex_stream_t stream);
+
+/* Pool backward (gather form, no atomics).  MAX: dx[p] = sum of dy[o] over
+ * outputs whose argmax tap points at p (argmax_tap required).  AVG:
+ * dx[p] = sum_{o: p in N(o)} dy[o] / count(o).  dx is overwritten. */
+HEX_API hex_status_t hex_pool2d_bwd(const hex_pool2d_desc_t* desc, const void* dy,
+                            const uint8_t* argmax_tap, void* dx, hex_stream_t stream);
+
+/* ---------------------------------------------------------------- training helpers
+ * Used by the data-parallel training step (BASELINE config 5).  Not part of
+ * the paper's method; plain elementwise / reduction kernels. */
+
+/* Head of the C5 network, forward + backward in one launch:
+ * feat bf16 NHWC [B][HW][C] (ReLU output) -> global average pool -> logits
+ * [B][K] = gap @ wl^T + bl (wl fp32 [K][C], bl fp32 [K]) -> mean softmax
+ * cross-entropy against labels (int32 [B]).  Writes loss (fp32 scalar),
+ * dfeat (bf16 NHWC, = d loss / d feat masked by feat > 0), dwl, dbl (fp32).
+ * ws must hold hex_head_workspace_size(B, K, C) bytes. */
+HEX_API size_t hex_head_workspace_size(int32_t B, int32_t K, int32_t C);
+HEX_API hex_status_t hex_head_fwd_bwd(int32_t B, int32_t HW, int32_t C, int32_t K,
+                              const void* feat, const float* wl, const float* bl,
+                              const int32_t* labels, float* loss, void* dfeat,
+                              float* dwl, float* dbl, void* ws, size_t ws_bytes,
+                              hex_stream_t stream);
+
+/* SGD with momentum over a flat fp32 parameter vector:
+ *   g = grad * grad_scale;  mom = mu * mom + g;  param -= lr * mom;
+ * and, if param_bf16 != NULL, param_bf16 = bf16(param). */
+HEX_API hex_status_t hex_sgd_momentum(int64_t count, float* param, const float* grad, float* mom,
+                              float lr, float mu, float grad_scale, void* param_bf16,
+                              hex_stream_t stream);
+
+/* Elementwise fp32 -> bf16 (RNE) conversion of count values. */
+HEX_API hex_status_t hex_cast_f32_bf16(int64_t count, const float* src, void* dst, hex_stream_t stream);
+
+/* ---------------------------------------------------------------- misc */
+HEX_API const char* hex_status_string(hex_status_t status);
+/* Library version, e.g. 0x000100 for 0.1.0. */
+HEX_API int32_t hex_version(void);
+/* Number of kernels this library has launched since load (host counter,
+ * used by bench.py to report gpu_launches). */
+HEX_API int64_t hex_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEXCONV_H_ */

@@ -1,0 +1,308 @@
+// abi.cu -- the C ABI of libhexconv (include/hexconv.h): argument validation,
+// path selection (tcgen05 implicit GEMM vs CUDA-core stencil) and launch.
+// Validation is synchronous and never launches on error.  There is no CPU
+// fallback: every data-touching call runs CUDA kernels.
+#include <mutex>
+
+#include "common.cuh"
+#include "geometry.cuh"
+#include "kernels.h"
+
+namespace hexconv {
+std::atomic<int64_t> g_launches{0};
+size_t head_ws_bytes(int B, int K, int C);
+hex_status_t head_fwd_bwd(int B, int HW, int C, int K, const void* feat, const float* wl, const float* bl,
+                          const int32_t* labels, float* loss, void* dfeat, float* dwl, float* dbl, void* ws,
+                          cudaStream_t st);
+hex_status_t sgd_momentum(int64_t n, float* p, const float* g, float* m, float lr, float mu, float gs, void* pb,
+                          cudaStream_t st);
+hex_status_t cast_f32_bf16(int64_t n, const float* s, void* d, cudaStream_t st);
+}  // namespace hexconv
+
+using namespace hexconv;
+
+namespace {
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+hex_status_t check_common(int B, int C, int H, int W, int n, int s, int parity, int dtype, int layout) {
+    if (n < 0 || s < 1) return HEX_ERR_INVALID_ARG;
+    if (parity != 0 && parity != 1) return HEX_ERR_INVALID_ARG;
+    if (B < 1 || C < 1 || H < 1 || W < 1) return HEX_ERR_SHAPE;
+    if (dtype != HEX_F32 && dtype != HEX_BF16) return HEX_ERR_DTYPE;
+    if (layout != HEX_NCHW && layout != HEX_NHWC) return HEX_ERR_LAYOUT;
+    if (n > HEX_MAX_N) return HEX_ERR_UNSUPPORTED;
+    return HEX_OK;
+}
+
+hex_status_t conv_geom(const hex_conv2d_desc_t* d, Geom* g) {
+    if (!d) return HEX_ERR_INVALID_ARG;
+    hex_status_t st = check_common(d->batch, d->in_channels, d->height, d->width, d->kernel_size, d->stride,
+                                   d->parity, d->dtype, d->layout);
+    if (st != HEX_OK) return st;
+    if (d->out_channels < 1) return HEX_ERR_SHAPE;
+    g->B = d->batch; g->H = d->height; g->W = d->width;
+    g->n = d->kernel_size; g->s = d->stride; g->parity = d->parity; g->T = hex_taps(d->kernel_size);
+    if (!out_shape(g->H, g->W, g->s, g->parity, &g->Ho, &g->Wo, nullptr)) return HEX_ERR_EMPTY_LATTICE;
+    return HEX_OK;
+}
+
+// The tensor-core path: bf16, NHWC, stride 1 and channel counts that tile.
+bool use_tc_fwd(const hex_conv2d_desc_t* d, const Geom& g) {
+    return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_conv_supported(g, d->in_channels, d->out_channels);
+}
+bool use_tc_bwd_data(const hex_conv2d_desc_t* d, const Geom& g) {
+    return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_conv_supported(g, d->out_channels, d->in_channels);
+}
+bool use_tc_wgrad(const hex_conv2d_desc_t* d, const Geom& g) {
+    return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_wgrad_supported(g, d->in_channels, d->out_channels);
+}
+
+size_t packed_weight_bytes(const hex_conv2d_desc_t* d, const Geom& g) {
+    return (size_t)g.T * d->out_channels * d->in_channels * 2 + 1024;
+}
+
+DirectConvArgs make_direct(const hex_conv2d_desc_t* d, const Geom& g) {
+    DirectConvArgs a{};
+    a.g = g;
+    a.Cin = d->in_channels;
+    a.Cout = d->out_channels;
+    a.dtype = d->dtype;
+    a.sx = make_strides(d->layout, d->in_channels, g.H, g.W);
+    a.sy = make_strides(d->layout, d->out_channels, g.Ho, g.Wo);
+    return a;
+}
+
+void* align_up(void* p, size_t a) { return (void*)(((uintptr_t)p + a - 1) & ~(uintptr_t)(a - 1)); }
+
+}  // namespace
+
+extern "C" {
+
+int32_t hex_num_taps(int32_t n) { return n < 0 ? -1 : hex_taps(n); }
+
+int32_t hex_version(void) { return 0x000100; }
+
+int64_t hex_launch_count(void) { return g_launches.load(); }
+
+const char* hex_status_string(hex_status_t s) {
+    switch (s) {
+        case HEX_OK: return "ok";
+        case HEX_ERR_INVALID_ARG: return "invalid argument";
+        case HEX_ERR_SHAPE: return "shape mismatch";
+        case HEX_ERR_EMPTY_LATTICE: return "empty lattice";
+        case HEX_ERR_DTYPE: return "unsupported dtype";
+        case HEX_ERR_LAYOUT: return "unsupported layout";
+        case HEX_ERR_ALIGNMENT: return "misaligned pointer";
+        case HEX_ERR_WORKSPACE: return "workspace too small";
+        case HEX_ERR_UNSUPPORTED: return "unsupported configuration";
+        case HEX_ERR_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}
+
+hex_status_t hex_output_shape(int32_t H, int32_t W, int32_t stride, int32_t parity, int32_t* Ho, int32_t* Wo,
+                              int32_t* parity_out) {
+    if (!Ho || !Wo || !parity_out) return HEX_ERR_INVALID_ARG;
+    if (stride < 1 || (parity != 0 && parity != 1)) return HEX_ERR_INVALID_ARG;
+    if (H < 1 || W < 1) return HEX_ERR_SHAPE;
+    int ho, wo, po;
+    bool ok = out_shape(H, W, stride, parity, &ho, &wo, &po);
+    *Ho = ho < 0 ? 0 : ho;
+    *Wo = wo;
+    *parity_out = po;
+    return ok ? HEX_OK : HEX_ERR_EMPTY_LATTICE;
+}
+
+hex_status_t hex_tap_offsets(int32_t n, int32_t p, int32_t* dc_dr) {
+    if (n < 0 || (p != 0 && p != 1) || !dc_dr) return HEX_ERR_INVALID_ARG;
+    if (n > HEX_MAX_N) return HEX_ERR_UNSUPPORTED;
+    const int T = hex_taps(n);
+    for (int t = 0; t < T; ++t) tap_offset(n, p, t, &dc_dr[2 * t], &dc_dr[2 * t + 1]);
+    return HEX_OK;
+}
+
+hex_status_t hex_conv2d_gather_map(const hex_conv2d_desc_t* d, int32_t* map, hex_stream_t stream) {
+    if (!d || !map) return HEX_ERR_INVALID_ARG;
+    if (d->kernel_size < 0 || d->stride < 1 || (d->parity != 0 && d->parity != 1)) return HEX_ERR_INVALID_ARG;
+    if (d->height < 1 || d->width < 1) return HEX_ERR_SHAPE;
+    if (d->kernel_size > HEX_MAX_N) return HEX_ERR_UNSUPPORTED;
+    Geom g{};
+    g.B = 1; g.H = d->height; g.W = d->width; g.n = d->kernel_size; g.s = d->stride; g.parity = d->parity;
+    g.T = hex_taps(g.n);
+    if (!out_shape(g.H, g.W, g.s, g.parity, &g.Ho, &g.Wo, nullptr)) return HEX_ERR_EMPTY_LATTICE;
+    return launch_gather_map(map, g, (cudaStream_t)stream);
+}
+
+hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* d, int32_t pass, size_t* bytes) {
+    if (!bytes) return HEX_ERR_INVALID_ARG;
+    Geom g;
+    hex_status_t st = conv_geom(d, &g);
+    if (st != HEX_OK) return st;
+    switch (pass) {
+        case 0: *bytes = use_tc_fwd(d, g) ? packed_weight_bytes(d, g) : 0; return HEX_OK;
+        case 1: *bytes = use_tc_bwd_data(d, g) ? packed_weight_bytes(d, g) : 0; return HEX_OK;
+        case 2:
+            *bytes = use_tc_wgrad(d, g) ? tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
+                                        : direct_wgrad_ws_bytes(g, d->in_channels, d->out_channels);
+            return HEX_OK;
+        default: return HEX_ERR_INVALID_ARG;
+    }
+}
+
+hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* d, const void* x, const void* w, const float* bias,
+                            int32_t fuse_relu, void* y, void* ws, size_t ws_bytes, hex_stream_t stream) {
+    Geom g;
+    hex_status_t st = conv_geom(d, &g);
+    if (st != HEX_OK) return st;
+    if (!x || !w || !y) return HEX_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (use_tc_fwd(d, g)) {
+        if (!aligned16(x) || !aligned16(y) || !aligned16(w)) return HEX_ERR_ALIGNMENT;
+        const size_t need = packed_weight_bytes(d, g);
+        if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
+        void* wp = align_up(ws, 1024);
+        st = tc_pack_weights(w, wp, d->out_channels, d->in_channels, g.T, 0, s);
+        if (st != HEX_OK) return st;
+        TcConvArgs a{};
+        a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
+        a.x = x; a.wpack = wp; a.bias = bias; a.y = y; a.relu_y = nullptr; a.relu = fuse_relu;
+        return tc_conv_fwd(a, s);
+    }
+    DirectConvArgs a = make_direct(d, g);
+    a.x = x; a.w = w; a.bias = bias; a.y = y; a.relu = fuse_relu;
+    return direct_conv_fwd(a, s);
+}
+
+hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* d, const void* dy, const void* w, const void* relu_y,
+                                 void* dx, void* ws, size_t ws_bytes, hex_stream_t stream) {
+    Geom g;
+    hex_status_t st = conv_geom(d, &g);
+    if (st != HEX_OK) return st;
+    if (!dy || !w || !dx) return HEX_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (use_tc_bwd_data(d, g)) {
+        if (!aligned16(dy) || !aligned16(dx) || !aligned16(w) || (relu_y && !aligned16(relu_y)))
+            return HEX_ERR_ALIGNMENT;
+        const size_t need = packed_weight_bytes(d, g);
+        if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
+        void* wp = align_up(ws, 1024);
+        // stride 1: dx = fwd conv of dy with W'[ci][co][t] = W[co][ci][T-1-t] (P18)
+        st = tc_pack_weights(w, wp, d->out_channels, d->in_channels, g.T, 1, s);
+        if (st != HEX_OK) return st;
+        TcConvArgs a{};
+        a.g = g; a.Cin = d->out_channels; a.Cout = d->in_channels;
+        a.x = dy; a.wpack = wp; a.bias = nullptr; a.y = dx; a.relu_y = relu_y; a.relu = 0;
+        return tc_conv_fwd(a, s);
+    }
+    DirectConvArgs a = make_direct(d, g);
+    a.dy = dy; a.w = w; a.relu_y = relu_y; a.dx = dx;
+    return direct_conv_bwd_data(a, s);
+}
+
+hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* d, const void* x, const void* dy, float* dw,
+                                   float* dbias, int32_t accumulate, void* ws, size_t ws_bytes,
+                                   hex_stream_t stream) {
+    Geom g;
+    hex_status_t st = conv_geom(d, &g);
+    if (st != HEX_OK) return st;
+    if (!x || !dy || !dw) return HEX_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (use_tc_wgrad(d, g)) {
+        if (!aligned16(x) || !aligned16(dy)) return HEX_ERR_ALIGNMENT;
+        const size_t need = tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels);
+        if (need && (!ws || ws_bytes < need)) return HEX_ERR_WORKSPACE;
+        TcWgradArgs a{};
+        a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
+        a.x = x; a.dy = dy; a.dw = dw; a.dbias = dbias; a.accumulate = accumulate;
+        return tc_conv_wgrad(a, ws, ws_bytes, s);
+    }
+    const size_t need = direct_wgrad_ws_bytes(g, d->in_channels, d->out_channels);
+    if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
+    DirectConvArgs a = make_direct(d, g);
+    a.x = x; a.dy = dy; a.dw = dw; a.dbias = dbias; a.accumulate = accumulate;
+    return direct_conv_bwd_weight(a, ws, s);
+}
+
+static hex_status_t pool_geom(const hex_pool2d_desc_t* d, Geom* g) {
+    if (!d) return HEX_ERR_INVALID_ARG;
+    hex_status_t st = check_common(d->batch, d->channels, d->height, d->width, d->kernel_size, d->stride,
+                                   d->parity, d->dtype, d->layout);
+    if (st != HEX_OK) return st;
+    if (d->kernel_size < 1) return HEX_ERR_INVALID_ARG;
+    if (d->mode != HEX_POOL_MAX && d->mode != HEX_POOL_AVG) return HEX_ERR_INVALID_ARG;
+    g->B = d->batch; g->H = d->height; g->W = d->width;
+    g->n = d->kernel_size; g->s = d->stride; g->parity = d->parity; g->T = hex_taps(d->kernel_size);
+    if (g->T > 255) return HEX_ERR_UNSUPPORTED;  // argmax is a uint8 tap index
+    if (!out_shape(g->H, g->W, g->s, g->parity, &g->Ho, &g->Wo, nullptr)) return HEX_ERR_EMPTY_LATTICE;
+    return HEX_OK;
+}
+
+static PoolArgs make_pool(const hex_pool2d_desc_t* d, const Geom& g) {
+    PoolArgs a{};
+    a.g = g;
+    a.C = d->channels; a.dtype = d->dtype; a.layout = d->layout; a.mode = d->mode;
+    a.sx = make_strides(d->layout, d->channels, g.H, g.W);
+    a.sy = make_strides(d->layout, d->channels, g.Ho, g.Wo);
+    return a;
+}
+
+hex_status_t hex_pool2d_fwd(const hex_pool2d_desc_t* d, const void* x, void* y, uint8_t* argmax_tap,
+                            hex_stream_t stream) {
+    Geom g;
+    hex_status_t st = pool_geom(d, &g);
+    if (st != HEX_OK) return st;
+    if (!x || !y) return HEX_ERR_INVALID_ARG;
+    PoolArgs a = make_pool(d, g);
+    if (d->dtype == HEX_BF16 && d->layout == HEX_NHWC && d->channels % 8 == 0) {
+        if (!aligned16(x) || !aligned16(y) || (argmax_tap && ((uintptr_t)argmax_tap & 7))) return HEX_ERR_ALIGNMENT;
+    }
+    a.x = x; a.y = y; a.argmax = argmax_tap;
+    return pool_fwd(a, (cudaStream_t)stream);
+}
+
+hex_status_t hex_pool2d_bwd(const hex_pool2d_desc_t* d, const void* dy, const uint8_t* argmax_tap, void* dx,
+                            hex_stream_t stream) {
+    Geom g;
+    hex_status_t st = pool_geom(d, &g);
+    if (st != HEX_OK) return st;
+    if (!dy || !dx) return HEX_ERR_INVALID_ARG;
+    if (d->mode == HEX_POOL_MAX && !argmax_tap) return HEX_ERR_INVALID_ARG;
+    PoolArgs a = make_pool(d, g);
+    if (d->dtype == HEX_BF16 && d->layout == HEX_NHWC && d->channels % 8 == 0) {
+        if (!aligned16(dy) || !aligned16(dx) || (argmax_tap && ((uintptr_t)argmax_tap & 7))) return HEX_ERR_ALIGNMENT;
+    }
+    a.dy = dy; a.argmax_in = argmax_tap; a.dx = dx;
+    return pool_bwd(a, (cudaStream_t)stream);
+}
+
+size_t hex_head_workspace_size(int32_t B, int32_t K, int32_t C) {
+    if (B < 1 || K < 1 || C < 1) return 0;
+    return head_ws_bytes(B, K, C);
+}
+
+hex_status_t hex_head_fwd_bwd(int32_t B, int32_t HW, int32_t C, int32_t K, const void* feat, const float* wl,
+                              const float* bl, const int32_t* labels, float* loss, void* dfeat, float* dwl,
+                              float* dbl, void* ws, size_t ws_bytes, hex_stream_t stream) {
+    if (B < 1 || HW < 1 || C < 1 || K < 1) return HEX_ERR_SHAPE;
+    if (K > 8 || C % 8 != 0) return HEX_ERR_UNSUPPORTED;
+    if (!feat || !wl || !bl || !labels || !loss || !dfeat || !dwl || !dbl) return HEX_ERR_INVALID_ARG;
+    if (!aligned16(feat) || !aligned16(dfeat)) return HEX_ERR_ALIGNMENT;
+    if (!ws || ws_bytes < head_ws_bytes(B, K, C)) return HEX_ERR_WORKSPACE;
+    return head_fwd_bwd(B, HW, C, K, feat, wl, bl, labels, loss, dfeat, dwl, dbl, ws, (cudaStream_t)stream);
+}
+
+hex_status_t hex_sgd_momentum(int64_t count, float* param, const float* grad, float* mom, float lr, float mu,
+                              float grad_scale, void* param_bf16, hex_stream_t stream) {
+    if (count < 0) return HEX_ERR_SHAPE;
+    if (count > 0 && (!param || !grad || !mom)) return HEX_ERR_INVALID_ARG;
+    return sgd_momentum(count, param, grad, mom, lr, mu, grad_scale, param_bf16, (cudaStream_t)stream);
+}
+
+hex_status_t hex_cast_f32_bf16(int64_t count, const float* src, void* dst, hex_stream_t stream) {
+    if (count < 0) return HEX_ERR_SHAPE;
+    if (count > 0 && (!src || !dst)) return HEX_ERR_INVALID_ARG;
+    return cast_f32_bf16(count, src, dst, (cudaStream_t)stream);
+}
+
+}  // extern "C"

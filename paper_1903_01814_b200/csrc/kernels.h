@@ -1,0 +1,74 @@
+// kernels.h -- internal launcher interfaces between the C ABI (abi.cu) and the
+// kernel translation units.  Not installed; not part of the public ABI.
+#pragma once
+#include "common.cuh"
+#include "geometry.cuh"
+
+namespace hexconv {
+
+struct DirectConvArgs {
+    Geom g;
+    int Cin, Cout, dtype;
+    Strides4 sx, sy;  // sx: x / dx (input grid), sy: y / dy (output grid)
+    const void* x;
+    const void* w;
+    const float* bias;
+    void* y;
+    const void* dy;
+    const void* relu_y;
+    void* dx;
+    float* dw;
+    float* dbias;
+    int relu, accumulate;
+};
+
+hex_status_t direct_conv_fwd(const DirectConvArgs& a, cudaStream_t st);
+hex_status_t direct_conv_bwd_data(const DirectConvArgs& a, cudaStream_t st);
+hex_status_t direct_conv_bwd_weight(const DirectConvArgs& a, void* ws, cudaStream_t st);
+size_t direct_wgrad_ws_bytes(const Geom& g, int Cin, int Cout);
+hex_status_t launch_gather_map(int32_t* map, const Geom& g, cudaStream_t st);
+
+struct PoolArgs {
+    Geom g;
+    int C, dtype, layout, mode;
+    Strides4 sx, sy;
+    const void* x;
+    void* y;
+    uint8_t* argmax;
+    const void* dy;
+    const uint8_t* argmax_in;
+    void* dx;
+};
+hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st);
+hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st);
+
+// tcgen05 implicit-GEMM path (bf16 NHWC, stride 1).
+struct TcConvArgs {
+    Geom g;
+    int Cin, Cout;
+    const void* x;      // bf16 NHWC [B][H][W][Cin]
+    const void* wpack;  // bf16 [T][Cout][Cin] (tap-major, K-major rows)
+    const float* bias;
+    void* y;            // bf16 NHWC [B][H][W][Cout]
+    const void* relu_y; // optional bf16 NHWC [B][H][W][Cout] mask source
+    int relu;
+};
+bool tc_conv_supported(const Geom& g, int Cin, int Cout);
+hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st);
+hex_status_t tc_pack_weights(const void* w, void* wpack, int Cout, int Cin, int T, int transpose_reverse,
+                             cudaStream_t st);
+
+struct TcWgradArgs {
+    Geom g;
+    int Cin, Cout;
+    const void* x;   // bf16 NHWC input
+    const void* dy;  // bf16 NHWC output gradient
+    float* dw;       // fp32 [Cout][Cin][T]
+    float* dbias;    // fp32 [Cout] or NULL
+    int accumulate;
+};
+bool tc_wgrad_supported(const Geom& g, int Cin, int Cout);
+size_t tc_wgrad_ws_bytes(const Geom& g, int Cin, int Cout);
+hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace hexconv

@@ -1,0 +1,292 @@
+// pool.cu -- hexagonal max / average pooling, forward and backward.
+//
+// pooling replaces the sub-convolutions and the results are
+// "combined with aggregation functions, whereas the padding- and
+// striding-scheme is identical".  Readings: A8 max ignores
+// off-grid cells and avg divides by the in-grid count; A9 ties resolve to the
+// first maximal tap in canonical order (strict '>' scan), and the output bits
+// are a copy of x at that tap.
+//
+// HBM-bound stencils.  NHWC tensors with C % 8 == 0 use 16-byte vectors of 8
+// channels per thread; everything else one element per thread.  The backward
+// pass is a gather over the candidate centres of each input pixel (no
+// atomics, deterministic).
+#include "common.cuh"
+#include "geometry.cuh"
+#include "kernels.h"
+
+namespace hexconv {
+
+template <typename T>
+__global__ void pool_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, uint8_t* __restrict__ am, Geom g,
+                                int Cc, Strides4 sx, Strides4 sy, int mode, int chan_fast) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)g.B * Cc * g.Ho * g.Wo;
+    if (idx >= total) return;
+    int ch, C, R, b;
+    if (chan_fast) {
+        ch = (int)(idx % Cc);
+        int64_t q = idx / Cc;
+        C = (int)(q % g.Wo); q /= g.Wo;
+        R = (int)(q % g.Ho);
+        b = (int)(q / g.Ho);
+    } else {
+        C = (int)(idx % g.Wo);
+        int64_t q = idx / g.Wo;
+        R = (int)(q % g.Ho); q /= g.Ho;
+        ch = (int)(q % Cc);
+        b = (int)(q / Cc);
+    }
+    const int c = g.s * C;
+    const int r = hex_rho(C, g.s, g.parity) + g.s * R;
+    const int p = (c + g.parity) & 1;
+    const int n = g.n;
+    const T* xp = x + (int64_t)b * sx.b + (int64_t)ch * sx.c;
+    int t = 0, best = -1, cnt = 0;
+    float bv = 0.f, sum = 0.f;
+    T braw = from_f32<T>(0.f);
+    for (int dc = -n; dc <= n; ++dc) {
+        const int len = 2 * n + 1 - (dc < 0 ? -dc : dc);
+        const int cc = c + dc;
+        if (cc < 0 || cc >= g.W) { t += len; continue; }
+        int rr = r + tap_top(n, dc, p);
+        for (int k = 0; k < len; ++k, ++t, ++rr) {
+            if (rr < 0 || rr >= g.H) continue;
+            const T raw = xp[(int64_t)rr * sx.h + (int64_t)cc * sx.w];
+            const float v = to_f32(raw);
+            if (mode == HEX_POOL_MAX) {
+                if (best < 0 || v > bv) { best = t; bv = v; braw = raw; }
+            } else {
+                sum += v;
+                ++cnt;
+            }
+        }
+    }
+    const int64_t yo = (int64_t)b * sy.b + (int64_t)ch * sy.c + (int64_t)R * sy.h + (int64_t)C * sy.w;
+    if (mode == HEX_POOL_MAX) {
+        y[yo] = braw;
+        if (am) am[yo] = (uint8_t)best;
+    } else {
+        y[yo] = from_f32<T>(sum / (float)cnt);
+    }
+}
+
+// NHWC bf16, 8 channels per thread (16-byte loads/stores).
+__global__ void pool_fwd_nhwc_bf16x8_kernel(const uint4* __restrict__ x, uint4* __restrict__ y,
+                                            uint64_t* __restrict__ am, Geom g, int C8, int mode) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)g.B * C8 * g.Ho * g.Wo;
+    if (idx >= total) return;
+    const int ch8 = (int)(idx % C8);
+    int64_t q = idx / C8;
+    const int C = (int)(q % g.Wo); q /= g.Wo;
+    const int R = (int)(q % g.Ho);
+    const int b = (int)(q / g.Ho);
+    const int c = g.s * C;
+    const int r = hex_rho(C, g.s, g.parity) + g.s * R;
+    const int p = (c + g.parity) & 1;
+    const int n = g.n;
+    const uint4* xp = x + (int64_t)b * g.H * g.W * C8 + ch8;
+    float bv[8], sum[8];
+    int best[8];
+    __nv_bfloat16 braw[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { bv[j] = 0.f; sum[j] = 0.f; best[j] = -1; braw[j] = __float2bfloat16_rn(0.f); }
+    int t = 0, cnt = 0;
+    for (int dc = -n; dc <= n; ++dc) {
+        const int len = 2 * n + 1 - (dc < 0 ? -dc : dc);
+        const int cc = c + dc;
+        if (cc < 0 || cc >= g.W) { t += len; continue; }
+        int rr = r + tap_top(n, dc, p);
+        for (int k = 0; k < len; ++k, ++t, ++rr) {
+            if (rr < 0 || rr >= g.H) continue;
+            uint4 v4 = __ldg(xp + ((int64_t)rr * g.W + cc) * C8);
+            const __nv_bfloat16* v = reinterpret_cast<const __nv_bfloat16*>(&v4);
+            ++cnt;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float f = __bfloat162float(v[j]);
+                if (mode == HEX_POOL_MAX) {
+                    if (best[j] < 0 || f > bv[j]) { best[j] = t; bv[j] = f; braw[j] = v[j]; }
+                } else {
+                    sum[j] += f;
+                }
+            }
+        }
+    }
+    uint4 out;
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&out);
+    const int64_t yo = (((int64_t)b * g.Ho + R) * g.Wo + C) * C8 + ch8;
+    if (mode == HEX_POOL_MAX) {
+        uint64_t a = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { o[j] = braw[j]; a |= (uint64_t)(uint8_t)best[j] << (8 * j); }
+        if (am) am[yo] = a;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16_rn(sum[j] / (float)cnt);
+    }
+    y[yo] = out;
+}
+
+// Number of in-grid taps of the centre at (r, c).
+__device__ __forceinline__ int in_grid_count(const Geom& g, int r, int c) {
+    const int p = (c + g.parity) & 1;
+    int cnt = 0;
+    for (int dc = -g.n; dc <= g.n; ++dc) {
+        const int cc = c + dc;
+        if (cc < 0 || cc >= g.W) continue;
+        const int len = 2 * g.n + 1 - (dc < 0 ? -dc : dc);
+        const int top = r + tap_top(g.n, dc, p);
+        const int lo = max(top, 0), hi = min(top + len, g.H);
+        cnt += max(hi - lo, 0);
+    }
+    return cnt;
+}
+
+// Backward: one thread per input element (gather over candidate centres).
+template <typename T>
+__global__ void pool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am, T* __restrict__ dx,
+                                Geom g, int Cc, Strides4 sx, Strides4 sy, int mode, int chan_fast) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)g.B * Cc * g.H * g.W;
+    if (idx >= total) return;
+    int ch, c, r, b;
+    if (chan_fast) {
+        ch = (int)(idx % Cc);
+        int64_t q = idx / Cc;
+        c = (int)(q % g.W); q /= g.W;
+        r = (int)(q % g.H);
+        b = (int)(q / g.H);
+    } else {
+        c = (int)(idx % g.W);
+        int64_t q = idx / g.W;
+        r = (int)(q % g.H); q /= g.H;
+        ch = (int)(q % Cc);
+        b = (int)(q / Cc);
+    }
+    const int n = g.n, s = g.s;
+    const int64_t ybase = (int64_t)b * sy.b + (int64_t)ch * sy.c;
+    float acc = 0.f;
+    int t = 0;
+    for (int dc = -n; dc <= n; ++dc) {
+        const int len = 2 * n + 1 - (dc < 0 ? -dc : dc);
+        const int oc = c - dc;
+        if (oc < 0 || oc % s != 0 || oc / s >= g.Wo) { t += len; continue; }
+        const int Cq = oc / s;
+        const int po = (oc + g.parity) & 1;
+        const int rho = hex_rho(Cq, s, g.parity);
+        const int top = tap_top(n, dc, po);
+        for (int k = 0; k < len; ++k, ++t) {
+            const int d = r - (top + k) - rho;
+            if (d < 0 || d % s != 0) continue;
+            const int Rq = d / s;
+            if (Rq >= g.Ho) continue;
+            const int64_t yo = ybase + (int64_t)Rq * sy.h + (int64_t)Cq * sy.w;
+            if (mode == HEX_POOL_MAX) {
+                if (am[yo] == t) acc += to_f32(dy[yo]);
+            } else {
+                const int orow = rho + s * Rq;
+                acc += to_f32(dy[yo]) / (float)in_grid_count(g, orow, oc);
+            }
+        }
+    }
+    dx[(int64_t)b * sx.b + (int64_t)ch * sx.c + (int64_t)r * sx.h + (int64_t)c * sx.w] = from_f32<T>(acc);
+}
+
+// NHWC bf16 backward, 8 channels per thread.
+__global__ void pool_bwd_nhwc_bf16x8_kernel(const uint4* __restrict__ dy, const uint64_t* __restrict__ am,
+                                            uint4* __restrict__ dx, Geom g, int C8, int mode) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)g.B * C8 * g.H * g.W;
+    if (idx >= total) return;
+    const int ch8 = (int)(idx % C8);
+    int64_t q = idx / C8;
+    const int c = (int)(q % g.W); q /= g.W;
+    const int r = (int)(q % g.H);
+    const int b = (int)(q / g.H);
+    const int n = g.n, s = g.s;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    int t = 0;
+    for (int dc = -n; dc <= n; ++dc) {
+        const int len = 2 * n + 1 - (dc < 0 ? -dc : dc);
+        const int oc = c - dc;
+        if (oc < 0 || oc % s != 0 || oc / s >= g.Wo) { t += len; continue; }
+        const int Cq = oc / s;
+        const int po = (oc + g.parity) & 1;
+        const int rho = hex_rho(Cq, s, g.parity);
+        const int top = tap_top(n, dc, po);
+        for (int k = 0; k < len; ++k, ++t) {
+            const int d = r - (top + k) - rho;
+            if (d < 0 || d % s != 0) continue;
+            const int Rq = d / s;
+            if (Rq >= g.Ho) continue;
+            const int64_t yo = (((int64_t)b * g.Ho + Rq) * g.Wo + Cq) * C8 + ch8;
+            uint4 v4 = __ldg(dy + yo);
+            const __nv_bfloat16* v = reinterpret_cast<const __nv_bfloat16*>(&v4);
+            if (mode == HEX_POOL_MAX) {
+                const uint64_t a = __ldg(am + yo);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if ((int)((a >> (8 * j)) & 0xff) == t) acc[j] += __bfloat162float(v[j]);
+            } else {
+                const float inv = 1.f / (float)in_grid_count(g, rho + s * Rq, oc);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(v[j]) * inv;
+            }
+        }
+    }
+    uint4 out;
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&out);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16_rn(acc[j]);
+    dx[(((int64_t)b * g.H + r) * g.W + c) * C8 + ch8] = out;
+}
+
+static bool use_vec8(const PoolArgs& a) {
+    return a.dtype == HEX_BF16 && a.layout == HEX_NHWC && (a.C % 8) == 0;
+}
+
+hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
+    if (use_vec8(a)) {
+        const int C8 = a.C / 8;
+        const int64_t total = (int64_t)a.g.B * C8 * a.g.Ho * a.g.Wo;
+        pool_fwd_nhwc_bf16x8_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
+            (const uint4*)a.x, (uint4*)a.y, (uint64_t*)a.argmax, a.g, C8, a.mode);
+    } else {
+        const int64_t total = (int64_t)a.g.B * a.C * a.g.Ho * a.g.Wo;
+        const int cf = a.layout == HEX_NHWC;
+        if (a.dtype == HEX_F32)
+            pool_fwd_kernel<float><<<ceil_div(total, 256), 256, 0, st>>>(
+                (const float*)a.x, (float*)a.y, a.argmax, a.g, a.C, a.sx, a.sy, a.mode, cf);
+        else
+            pool_fwd_kernel<__nv_bfloat16><<<ceil_div(total, 256), 256, 0, st>>>(
+                (const __nv_bfloat16*)a.x, (__nv_bfloat16*)a.y, a.argmax, a.g, a.C, a.sx, a.sy, a.mode, cf);
+    }
+    count_launch();
+    return last_launch_status();
+}
+
+hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
+    if (use_vec8(a)) {
+        const int C8 = a.C / 8;
+        const int64_t total = (int64_t)a.g.B * C8 * a.g.H * a.g.W;
+        pool_bwd_nhwc_bf16x8_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
+            (const uint4*)a.dy, (const uint64_t*)a.argmax_in, (uint4*)a.dx, a.g, C8, a.mode);
+    } else {
+        const int64_t total = (int64_t)a.g.B * a.C * a.g.H * a.g.W;
+        const int cf = a.layout == HEX_NHWC;
+        if (a.dtype == HEX_F32)
+            pool_bwd_kernel<float><<<ceil_div(total, 256), 256, 0, st>>>(
+                (const float*)a.dy, a.argmax_in, (float*)a.dx, a.g, a.C, a.sx, a.sy, a.mode, cf);
+        else
+            pool_bwd_kernel<__nv_bfloat16><<<ceil_div(total, 256), 256, 0, st>>>(
+                (const __nv_bfloat16*)a.dy, a.argmax_in, (__nv_bfloat16*)a.dx, a.g, a.C, a.sx, a.sy, a.mode, cf);
+    }
+    count_launch();
+    return last_launch_status();
+}
+
+}  // namespace hexconv

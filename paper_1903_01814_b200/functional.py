@@ -1,0 +1,228 @@
+"""Torch-facing hexagonal conv / pool ops over the C ABI (libhexconv.so).
+
+PyTorch supplies device memory, streams and autograd bookkeeping only; each
+op is one (or a few) calls into the library's CUDA kernels.  Shapes follow
+the declared layout: "NCHW" tensors are (B, C, H, W), "NHWC" tensors are
+(B, H, W, C).  Weights are (Cout, Cin, T) with taps in canonical order
+(A2).  Parity 0 = odd columns physically lower
+(A1).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _abi as A
+
+_DTYPES = {torch.float32: A.F32, torch.bfloat16: A.BF16}
+_LAYOUTS = {"NCHW": A.NCHW, "NHWC": A.NHWC}
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _check_cuda(*ts):
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError("hexconv ops take CUDA tensors (there is no CPU path)")
+        if not t.is_contiguous():
+            raise ValueError("hexconv ops take contiguous tensors in the declared layout")
+
+
+def _dims(x, layout):
+    if layout == "NCHW":
+        B, C, H, W = x.shape
+    elif layout == "NHWC":
+        B, H, W, C = x.shape
+    else:
+        raise ValueError(f"unknown layout {layout}")
+    return B, C, H, W
+
+
+def _shape(layout, B, C, H, W):
+    return (B, C, H, W) if layout == "NCHW" else (B, H, W, C)
+
+
+def num_taps(n: int) -> int:
+    return A.num_taps(n)
+
+
+def output_shape(H: int, W: int, stride: int = 1, parity: int = 0):
+    return A.output_shape(H, W, stride, parity)
+
+
+def conv_desc(B, Cin, Cout, H, W, n, stride, parity, dtype, layout) -> A.ConvDesc:
+    return A.ConvDesc(B, Cin, Cout, H, W, n, stride, parity, _DTYPES[dtype], _LAYOUTS[layout])
+
+
+def _workspace(desc, pass_id, device):
+    nbytes = ctypes.c_size_t()
+    A.check(A.lib().hex_conv2d_workspace_size(ctypes.byref(desc), pass_id, ctypes.byref(nbytes)),
+            "hex_conv2d_workspace_size")
+    if nbytes.value == 0:
+        return None, 0
+    return torch.empty(nbytes.value, dtype=torch.uint8, device=device), nbytes.value
+
+
+# ------------------------------------------------------------------ convolution
+def conv2d_fwd(x, w, bias=None, n: int = 1, stride: int = 1, parity: int = 0, relu: bool = False,
+               layout: str = "NCHW", out=None):
+    """y = hexconv(x, w) + bias (then ReLU if relu)."""
+    _check_cuda(x, w, bias, out)
+    B, Cin, H, W = _dims(x, layout)
+    Cout, Ci2, T = w.shape
+    if Ci2 != Cin:
+        raise ValueError("channel mismatch")
+    if T != A.num_taps(n):
+        raise ValueError("weight tap count does not match kernel size")
+    if w.dtype != x.dtype:
+        raise ValueError("x and w must share a dtype")
+    if bias is not None and bias.dtype != torch.float32:
+        raise ValueError("bias is fp32")
+    Ho, Wo, _ = A.output_shape(H, W, stride, parity)
+    d = conv_desc(B, Cin, Cout, H, W, n, stride, parity, x.dtype, layout)
+    if out is None:
+        out = torch.empty(_shape(layout, B, Cout, Ho, Wo), dtype=x.dtype, device=x.device)
+    ws, nb = _workspace(d, 0, x.device)
+    A.check(A.lib().hex_conv2d_fwd(ctypes.byref(d), _ptr(x), _ptr(w), _ptr(bias), int(relu), _ptr(out),
+                                   _ptr(ws), nb, _stream()), "hex_conv2d_fwd")
+    return out
+
+
+def conv2d_bwd_data(dy, w, in_hw, n: int = 1, stride: int = 1, parity: int = 0, layout: str = "NCHW",
+                    relu_y=None, out=None):
+    """dx = adjoint of conv2d_fwd applied to dy; optionally masked by relu_y > 0."""
+    _check_cuda(dy, w, relu_y, out)
+    B, Cout, Ho, Wo = _dims(dy, layout)
+    Co2, Cin, T = w.shape
+    H, W = in_hw
+    if Co2 != Cout:
+        raise ValueError("channel mismatch")
+    d = conv_desc(B, Cin, Cout, H, W, n, stride, parity, dy.dtype, layout)
+    if out is None:
+        out = torch.empty(_shape(layout, B, Cin, H, W), dtype=dy.dtype, device=dy.device)
+    ws, nb = _workspace(d, 1, dy.device)
+    A.check(A.lib().hex_conv2d_bwd_data(ctypes.byref(d), _ptr(dy), _ptr(w), _ptr(relu_y), _ptr(out),
+                                        _ptr(ws), nb, _stream()), "hex_conv2d_bwd_data")
+    return out
+
+
+def conv2d_bwd_weight(x, dy, n: int = 1, stride: int = 1, parity: int = 0, layout: str = "NCHW",
+                      with_bias: bool = True, dw=None, dbias=None, accumulate: bool = False):
+    """(dw fp32 [Cout,Cin,T], dbias fp32 [Cout] or None)."""
+    _check_cuda(x, dy, dw, dbias)
+    B, Cin, H, W = _dims(x, layout)
+    Cout = _dims(dy, layout)[1]
+    T = A.num_taps(n)
+    d = conv_desc(B, Cin, Cout, H, W, n, stride, parity, x.dtype, layout)
+    if dw is None:
+        dw = torch.empty((Cout, Cin, T), dtype=torch.float32, device=x.device)
+    if with_bias and dbias is None:
+        dbias = torch.empty((Cout,), dtype=torch.float32, device=x.device)
+    ws, nb = _workspace(d, 2, x.device)
+    A.check(A.lib().hex_conv2d_bwd_weight(ctypes.byref(d), _ptr(x), _ptr(dy), _ptr(dw),
+                                          _ptr(dbias if with_bias else None), int(accumulate),
+                                          _ptr(ws), nb, _stream()), "hex_conv2d_bwd_weight")
+    return dw, (dbias if with_bias else None)
+
+
+def gather_map(H: int, W: int, n: int, stride: int = 1, parity: int = 0, device="cuda"):
+    Ho, Wo, _ = A.output_shape(H, W, stride, parity)
+    T = A.num_taps(n)
+    m = torch.empty((Ho, Wo, T), dtype=torch.int32, device=device)
+    d = A.ConvDesc(1, 1, 1, H, W, n, stride, parity, A.F32, A.NCHW)
+    A.check(A.lib().hex_conv2d_gather_map(ctypes.byref(d), _ptr(m), _stream()), "hex_conv2d_gather_map")
+    return m
+
+
+# ------------------------------------------------------------------ pooling
+def pool_desc(B, C, H, W, n, stride, parity, dtype, layout, mode) -> A.PoolDesc:
+    return A.PoolDesc(B, C, H, W, n, stride, parity, _DTYPES[dtype], _LAYOUTS[layout],
+                      A.POOL_MAX if mode == "max" else A.POOL_AVG)
+
+
+def pool2d_fwd(x, n: int = 1, stride: int = 1, parity: int = 0, mode: str = "max", layout: str = "NCHW",
+               need_argmax: bool = True, out=None):
+    """(y, argmax uint8 or None)."""
+    _check_cuda(x, out)
+    B, C, H, W = _dims(x, layout)
+    Ho, Wo, _ = A.output_shape(H, W, stride, parity)
+    d = pool_desc(B, C, H, W, n, stride, parity, x.dtype, layout, mode)
+    if out is None:
+        out = torch.empty(_shape(layout, B, C, Ho, Wo), dtype=x.dtype, device=x.device)
+    am = None
+    if mode == "max" and need_argmax:
+        am = torch.empty(_shape(layout, B, C, Ho, Wo), dtype=torch.uint8, device=x.device)
+    A.check(A.lib().hex_pool2d_fwd(ctypes.byref(d), _ptr(x), _ptr(out), _ptr(am), _stream()), "hex_pool2d_fwd")
+    return out, am
+
+
+def pool2d_bwd(dy, argmax, in_hw, n: int = 1, stride: int = 1, parity: int = 0, mode: str = "max",
+               layout: str = "NCHW", out=None):
+    _check_cuda(dy, argmax, out)
+    B, C, Ho, Wo = _dims(dy, layout)
+    H, W = in_hw
+    d = pool_desc(B, C, H, W, n, stride, parity, dy.dtype, layout, mode)
+    if out is None:
+        out = torch.empty(_shape(layout, B, C, H, W), dtype=dy.dtype, device=dy.device)
+    A.check(A.lib().hex_pool2d_bwd(ctypes.byref(d), _ptr(dy), _ptr(argmax), _ptr(out), _stream()),
+            "hex_pool2d_bwd")
+    return out
+
+
+# ------------------------------------------------------------------ autograd
+class HexConv2dFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, bias, n, stride, parity, relu, layout):
+        y = conv2d_fwd(x, w, bias, n, stride, parity, relu, layout)
+        ctx.save_for_backward(x, w, y if relu else None)
+        ctx.cfg = (n, stride, parity, relu, layout, bias is not None)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, w, y = ctx.saved_tensors
+        n, stride, parity, relu, layout, has_bias = ctx.cfg
+        gy = gy.contiguous()
+        if relu:
+            gy = gy * (y > 0).to(gy.dtype)
+        B, Cin, H, W = _dims(x, layout)
+        dx = conv2d_bwd_data(gy, w, (H, W), n, stride, parity, layout) if ctx.needs_input_grad[0] else None
+        dw, db = conv2d_bwd_weight(x, gy, n, stride, parity, layout, with_bias=has_bias)
+        return dx, dw.to(w.dtype), db, None, None, None, None, None
+
+
+class HexPool2dFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, n, stride, parity, mode, layout):
+        y, am = pool2d_fwd(x, n, stride, parity, mode, layout)
+        ctx.save_for_backward(am) if am is not None else ctx.save_for_backward()
+        B, C, H, W = _dims(x, layout)
+        ctx.cfg = (n, stride, parity, mode, layout, H, W)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        n, stride, parity, mode, layout, H, W = ctx.cfg
+        am = ctx.saved_tensors[0] if mode == "max" else None
+        return pool2d_bwd(gy.contiguous(), am, (H, W), n, stride, parity, mode, layout), None, None, None, None, None
+
+
+def hex_conv2d(x, w, bias=None, n=1, stride=1, parity=0, relu=False, layout="NCHW"):
+    return HexConv2dFn.apply(x, w, bias, n, stride, parity, relu, layout)
+
+
+def hex_max_pool2d(x, n=1, stride=1, parity=0, layout="NCHW"):
+    return HexPool2dFn.apply(x, n, stride, parity, "max", layout)
+
+
+def hex_avg_pool2d(x, n=1, stride=1, parity=0, layout="NCHW"):
+    return HexPool2dFn.apply(x, n, stride, parity, "avg", layout)

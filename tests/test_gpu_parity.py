@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle.
+
+Bars (BASELINE.json north_star):
+  * integer / index work (gather maps, argmax, output shapes): bit-exact
+  * fp32 path: normwise relative error max|gpu-ref| / max|ref| <= 1e-5
+  * bf16 path (inputs rounded to bf16 on both sides, fp32 accumulation,
+    bf16 output): normwise <= 2e-2
+  * max-pool values: bit-exact (a copy of the selected input)
+"""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-5
+TOL_BF16 = 2e-2
+
+
+@pytest.fixture(scope="module")
+def F():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1903_01814_b200 import functional
+    return functional
+
+
+def rel(gpu, ref):
+    ref = np.asarray(ref, dtype=np.float64)
+    gpu = np.asarray(gpu, dtype=np.float64)
+    den = max(np.abs(ref).max(), 1e-30)
+    return float(np.abs(gpu - ref).max() / den)
+
+
+def to_dev(a, dtype, layout="NCHW"):
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+    if layout == "NHWC" and t.dim() == 4:
+        t = t.permute(0, 2, 3, 1).contiguous()
+    return t.to(dtype).cuda()
+
+
+def to_np(t, layout="NCHW"):
+    t = t.detach().float().cpu()
+    if layout == "NHWC" and t.dim() == 4:
+        t = t.permute(0, 3, 1, 2).contiguous()
+    return t.numpy().astype(np.float64)
+
+
+def rnd(shape, seed, dtype):
+    a = np.random.default_rng(seed).standard_normal(shape)
+    if dtype == torch.bfloat16:
+        from synth import round_bf16
+        return round_bf16(a)
+    return a.astype(np.float32).astype(np.float64)
+
+
+GRIDS = [(1, 1), (1, 6), (5, 5), (6, 7), (12, 13), (11, 12), (9, 4)]
+
+
+# ------------------------------------------------------------------ geometry
+def test_gather_map_bit_exact(F, oracle):
+    for pi, n, s in itertools.product((0, 1), (0, 1, 2, 3), (1, 2, 3)):
+        for H, W in GRIDS + [(16, 16), (7, 13)]:
+            try:
+                ref = oracle.gather_map(H, W, n, s, pi)
+            except ValueError:
+                continue
+            got = F.gather_map(H, W, n, s, pi).cpu().numpy()
+            assert np.array_equal(got, ref), (pi, n, s, H, W)
+
+
+# ------------------------------------------------------------------ convolution, CUDA-core path
+ENVELOPE = [(pi, n, s, H, W) for pi in (0, 1) for n in (0, 1, 2, 3) for s in (1, 2, 3) for (H, W) in GRIDS]
+
+
+def _conv_case(F, oracle, pi, n, s, H, W, B, Cin, Cout, dtype, layout, seed):
+    try:
+        oracle.out_shape(H, W, s, pi)
+    except ValueError:
+        return
+    T = oracle.num_taps(n)
+    x = rnd((B, Cin, H, W), seed, dtype)
+    w = rnd((Cout, Cin, T), seed + 1, dtype) * 0.5
+    if dtype == torch.bfloat16:
+        from synth import round_bf16
+        w = round_bf16(w)
+    bias = np.random.default_rng(seed + 2).standard_normal(Cout).astype(np.float32).astype(np.float64)
+    tol = TOL_F32 if dtype == torch.float32 else TOL_BF16
+    xd, wd = to_dev(x, dtype, layout), torch.from_numpy(w.astype(np.float32)).to(dtype).cuda()
+    bd = torch.from_numpy(bias.astype(np.float32)).cuda()
+    # forward (+ bias)
+    y = F.conv2d_fwd(xd, wd, bd, n=n, stride=s, parity=pi, layout=layout)
+    yref = oracle.conv2d_fwd(x, w, bias, n=n, s=s, pi=pi)
+    assert rel(to_np(y, layout), yref) <= tol, ("fwd", pi, n, s, H, W)
+    # fused relu
+    yr = F.conv2d_fwd(xd, wd, bd, n=n, stride=s, parity=pi, relu=True, layout=layout)
+    assert rel(to_np(yr, layout), np.maximum(yref, 0)) <= tol
+    # backward
+    g = rnd(yref.shape, seed + 3, dtype)
+    gd = to_dev(g, dtype, layout)
+    dx = F.conv2d_bwd_data(gd, wd, (H, W), n=n, stride=s, parity=pi, layout=layout)
+    dw, db = F.conv2d_bwd_weight(xd, gd, n=n, stride=s, parity=pi, layout=layout)
+    dxr, dwr, dbr = oracle.conv2d_bwd(x, w, g, n=n, s=s, pi=pi)
+    assert rel(to_np(dx, layout), dxr) <= tol, ("dgrad", pi, n, s, H, W)
+    wtol = TOL_F32 if dtype == torch.float32 else 1e-4  # dw is fp32 accumulated from exact bf16 inputs
+    assert rel(dw.cpu().numpy(), dwr) <= wtol, ("wgrad", pi, n, s, H, W)
+    assert rel(db.cpu().numpy(), dbr) <= wtol, ("dbias", pi, n, s, H, W)
+
+
+@pytest.mark.parametrize("pi,n,s", [(pi, n, s) for pi in (0, 1) for n in (0, 1, 2, 3) for s in (1, 2, 3)])
+def test_conv_f32_nchw_envelope(F, oracle, pi, n, s):
+    for k, (H, W) in enumerate(GRIDS):
+        B, Cin, Cout = (1, 1, 3) if k % 2 else (2, 3, 1)
+        _conv_case(F, oracle, pi, n, s, H, W, B, Cin, Cout, torch.float32, "NCHW", 100 + k)
+
+
+@pytest.mark.parametrize("layout,dtype", [("NHWC", torch.float32), ("NHWC", torch.bfloat16),
+                                          ("NCHW", torch.bfloat16)])
+def test_conv_other_layouts(F, oracle, layout, dtype):
+    for pi, n, s in [(0, 1, 1), (1, 2, 2), (0, 3, 3), (0, 2, 1), (1, 0, 2)]:
+        for (H, W) in [(12, 13), (9, 4)]:
+            _conv_case(F, oracle, pi, n, s, H, W, 2, 5, 6, dtype, layout, 7)
+
+
+def test_conv_many_channels_f32(F, oracle):
+    # channel blocks > 1 and ragged tails (Cout 37 > 32, Cin 40 > 32), several pixel blocks
+    _conv_case(F, oracle, 0, 1, 1, 23, 21, 2, 40, 37, torch.float32, "NCHW", 11)
+    _conv_case(F, oracle, 0, 2, 2, 24, 30, 1, 17, 70, torch.float32, "NCHW", 12)
+
+
+def test_conv_deterministic(F):
+    x = torch.randn(4, 16, 20, 20, device="cuda")
+    w = torch.randn(32, 16, 19, device="cuda")
+    g = torch.randn(4, 32, 20, 20, device="cuda")
+    a = F.conv2d_bwd_weight(x, g, n=2)[0]
+    b = F.conv2d_bwd_weight(x, g, n=2)[0]
+    assert torch.equal(a, b)
+    assert torch.equal(F.conv2d_fwd(x, w, n=2), F.conv2d_fwd(x, w, n=2))
+
+
+def test_conv_fused_relu_mask_dgrad(F, oracle):
+    x = rnd((2, 4, 10, 11), 5, torch.float32)
+    w = rnd((3, 4, 7), 6, torch.float32)
+    g = rnd((2, 3, 10, 11), 7, torch.float32)
+    ry = rnd((2, 4, 10, 11), 8, torch.float32)
+    dx = F.conv2d_bwd_data(to_dev(g, torch.float32), to_dev(w, torch.float32), (10, 11), n=1,
+                           relu_y=to_dev(ry, torch.float32))
+    ref = oracle.conv2d_bwd(x, w, g, n=1)[0] * (ry > 0)
+    assert rel(to_np(dx), ref) <= TOL_F32
+
+
+# ------------------------------------------------------------------ pooling
+def _pool_case(F, oracle, pi, n, s, H, W, B, C, dtype, layout, mode, seed, data=None):
+    try:
+        oracle.out_shape(H, W, s, pi)
+    except ValueError:
+        return
+    x = rnd((B, C, H, W), seed, dtype) if data is None else data
+    xd = to_dev(x, dtype, layout)
+    y, am = F.pool2d_fwd(xd, n=n, stride=s, parity=pi, mode=mode, layout=layout)
+    yref, amref = oracle.pool2d_fwd(x, n=n, s=s, pi=pi, mode=mode)
+    if mode == "max":
+        assert np.array_equal(to_np(y, layout), yref), ("maxpool value", pi, n, s, H, W)
+        amg = am.cpu()
+        if layout == "NHWC":
+            amg = amg.permute(0, 3, 1, 2)
+        assert np.array_equal(amg.numpy(), amref), ("argmax", pi, n, s, H, W)
+    else:
+        tol = TOL_F32 if dtype == torch.float32 else TOL_BF16
+        assert rel(to_np(y, layout), yref) <= tol
+    g = rnd(yref.shape, seed + 1, dtype)
+    dx = F.pool2d_bwd(to_dev(g, dtype, layout), am, (H, W), n=n, stride=s, parity=pi, mode=mode, layout=layout)
+    dxr = oracle.pool2d_bwd(g, amref, H, W, n=n, s=s, pi=pi, mode=mode)
+    tol = TOL_F32 if dtype == torch.float32 else TOL_BF16
+    assert rel(to_np(dx, layout), dxr) <= tol, ("pool bwd", mode, pi, n, s, H, W)
+
+
+@pytest.mark.parametrize("mode", ["max", "avg"])
+@pytest.mark.parametrize("pi", [0, 1])
+def test_pool_envelope(F, oracle, mode, pi):
+    for n in (1, 2, 3):
+        for s in (1, 2, 3):
+            for k, (H, W) in enumerate(GRIDS):
+                _pool_case(F, oracle, pi, n, s, H, W, 2, 3, torch.float32, "NCHW", mode, 200 + k)
+
+
+@pytest.mark.parametrize("mode", ["max", "avg"])
+def test_pool_bf16_nhwc_vectorised(F, oracle, mode):
+    for pi, n, s in [(0, 1, 2), (1, 1, 1), (0, 2, 3)]:
+        for C in (8, 16, 3):
+            _pool_case(F, oracle, pi, n, s, 12, 13, 2, C, torch.bfloat16, "NHWC", mode, 300 + C)
+
+
+def test_maxpool_ties_first_in_canonical_order(F, oracle):
+    # ReLU-like data with many exact zeros: the first in-grid tap wins
+    x = np.maximum(rnd((2, 8, 11, 12), 9, torch.bfloat16), 0)
+    x[:, :, 3:6, 3:6] = 0.0
+    for layout in ("NCHW", "NHWC"):
+        _pool_case(F, oracle, 0, 1, 2, 11, 12, 2, 8, torch.bfloat16, layout, "max", 0, data=x)
+        _pool_case(F, oracle, 0, 1, 1, 11, 12, 2, 8, torch.bfloat16, layout, "max", 0, data=x)
+
+
+# ------------------------------------------------------------------ BASELINE configs 1 and 2 at full size
+def test_config1_full(F, oracle):
+    import synth
+    c = synth.CONFIGS["c1"]
+    x = synth.round_f32(synth.normal((c["B"], c["Cin"], c["H"], c["W"]), 0))
+    w = synth.round_f32(synth.normal((c["Cout"], c["Cin"], 7), 1, 0.1))
+    y = F.conv2d_fwd(to_dev(x, torch.float32), to_dev(w, torch.float32), torch.zeros(4, device="cuda"), n=1)
+    assert rel(to_np(y), oracle.conv2d_fwd(x, w, np.zeros(4), n=1)) <= TOL_F32
+    # the gather map of the config, bit-exact
+    assert np.array_equal(F.gather_map(16, 16, 1).cpu().numpy(), oracle.gather_map(16, 16, 1, 1))
+
+
+def test_config2_full(F, oracle):
+    import synth
+    c = synth.CONFIGS["c2"]
+    B, Ci, Co, H, W = c["B"], c["Cin"], c["Cout"], c["H"], c["W"]
+    x = synth.round_f32(synth.normal((B, Ci, H, W), 0))
+    w = synth.round_f32(synth.kaiming_uniform((Co, Ci, 19), 1))
+    xd, wd = to_dev(x, torch.float32), to_dev(w, torch.float32)
+    y = F.conv2d_fwd(xd, wd, None, n=2, stride=2)
+    yref = oracle.conv2d_fwd(x, w, None, n=2, s=2)
+    assert y.shape == (32, 32, 24, 24)
+    assert rel(to_np(y), yref) <= TOL_F32
+    # max pool n1 s2 on the GPU's own conv output (reading A17)
+    y64 = to_np(y)
+    p, am = F.pool2d_fwd(y, n=1, stride=2, mode="max")
+    pref, amref = oracle.pool2d_fwd(y64, n=1, s=2, mode="max")
+    assert p.shape == (32, 32, 12, 12)
+    assert np.array_equal(to_np(p), pref) and np.array_equal(am.cpu().numpy(), amref)
+    gp = synth.round_f32(synth.normal(pref.shape, 3))
+    gy = F.pool2d_bwd(to_dev(gp, torch.float32), am, (24, 24), n=1, stride=2, mode="max")
+    gyref = oracle.pool2d_bwd(gp, amref, 24, 24, n=1, s=2, mode="max")
+    assert rel(to_np(gy), gyref) <= TOL_F32
+    gy64 = to_np(gy)
+    dx = F.conv2d_bwd_data(gy, wd, (H, W), n=2, stride=2)
+    dw, db = F.conv2d_bwd_weight(xd, gy, n=2, stride=2)
+    dxr, dwr, dbr = oracle.conv2d_bwd(x, w, gy64, n=2, s=2)
+    assert rel(to_np(dx), dxr) <= TOL_F32
+    assert rel(dw.cpu().numpy(), dwr) <= TOL_F32
+    assert rel(db.cpu().numpy(), dbr) <= TOL_F32
