@@ -157,6 +157,11 @@ HEX_API hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* desc, const 
                                    float* dw, float* dbias, int32_t accumulate,
                                    void* ws, size_t ws_bytes, hex_stream_t stream);
 
+/* Which kernel family a call with this descriptor runs: *algo (host) = 0 for
+ * the CUDA-core stencil path, 1 for the tcgen05 tensor-core path.
+ * pass: 0 fwd, 1 bwd_data, 2 bwd_weight. */
+HEX_API hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* desc, int32_t pass, int32_t* algo);
+
 /* ---------------------------------------------------------------- pooling */
 
 /* Pooling (the sub-convolutions are replaced by pooling

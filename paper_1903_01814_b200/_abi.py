@@ -72,6 +72,7 @@ _SIGS = {
     "hex_tap_offsets": (_i32, [_i32, _i32, _i32p]),
     "hex_conv2d_gather_map": (_i32, [_CDP, _vp, _vp]),
     "hex_conv2d_workspace_size": (_i32, [_CDP, _i32, _szp]),
+    "hex_conv2d_algo": (_i32, [_CDP, _i32, _i32p]),
     "hex_conv2d_fwd": (_i32, [_CDP, _vp, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
     "hex_conv2d_bwd_data": (_i32, [_CDP, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "hex_conv2d_bwd_weight": (_i32, [_CDP, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),

@@ -150,6 +150,19 @@ hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* d, int32_t pass,
     }
 }
 
+hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* d, int32_t pass, int32_t* algo) {
+    if (!algo) return HEX_ERR_INVALID_ARG;
+    Geom g;
+    hex_status_t st = conv_geom(d, &g);
+    if (st != HEX_OK) return st;
+    switch (pass) {
+        case 0: *algo = use_tc_fwd(d, g) ? 1 : 0; return HEX_OK;
+        case 1: *algo = use_tc_bwd_data(d, g) ? 1 : 0; return HEX_OK;
+        case 2: *algo = use_tc_wgrad(d, g) ? 1 : 0; return HEX_OK;
+        default: return HEX_ERR_INVALID_ARG;
+    }
+}
+
 hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* d, const void* x, const void* w, const float* bias,
                             int32_t fuse_relu, void* y, void* ws, size_t ws_bytes, hex_stream_t stream) {
     Geom g;

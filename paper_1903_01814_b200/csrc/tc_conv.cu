@@ -1,17 +1,695 @@
-// tc_conv.cu -- tcgen05 implicit-GEMM hexagonal convolution (placeholder: the
-// tensor-core path is being brought up; until then every shape takes the
-// CUDA-core stencil path).
+// tc_conv.cu -- tcgen05 / TMEM / TMA implicit-GEMM hexagonal convolution for
+// sm_100a (bf16 NHWC activations, fp32 accumulation in tensor memory).
+//
+// Method: y = bias + sum_ci sum_t w[co,ci,t] x[nb_t].
+// The paper realises it as n+1 dilated rectangular sub-convolutions per
+// column parity; here it is ONE implicit GEMM per column-parity class:
+//
+//   M = 128 output pixels of one column parity P (a box of RB rows x JB
+//       sub-columns x BB images of the parity view P = tensor columns P::2),
+//   N = output channels (64/128/256 per tile),
+//   K = (tap t, input channel).
+//
+// For a tile of parity P every tap t = (dc, dr) reads ONE constant-offset box
+// of one input parity view P' = (P+dc) mod 2, at sub-column offset
+// floor((P+dc)/2) and row offset dr (the tap row offset depends only on the
+// centre parity, constant over the tile).  TMA loads that box (64 channels x
+// 128 pixels, SWIZZLE_128B, zero fill for off-grid neighbours = DESIGN.md A4)
+// straight into the K-major A operand layout; weights are pre-packed
+// tap-major [T][Cout][Cin] and loaded as the K-major B operand.
+//
+// Forward kernel: persistent, warp specialised (warp 0 TMA producer, warp 1
+// MMA issuer, warps 2-5 epilogue), 4-8 stage smem ring, two TMEM accumulators
+// so the epilogue of tile i overlaps the MMAs of tile i+1.  The epilogue adds
+// bias, applies ReLU or a ReLU-backward mask, rounds to bf16 (RNE) and stores
+// NHWC rows.  Backward-data at stride 1 is the same kernel on dy with
+// W'[ci][co][t] = W[co][ci][T-1-t] (pin P18).
+//
+// Weight-gradient kernel: per (Cout tile of 128, Cin tile N, tap group,
+// pixel chunk) accumulate dW_t = dy^T * shift_t(x) over the chunk with both
+// operands MN-major (pixels are K), then a fixed-order split-K reduction.
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "geometry.cuh"
 #include "kernels.h"
+#include "tc_ptx.cuh"
 
 namespace hexconv {
 
-bool tc_conv_supported(const Geom&, int, int) { return false; }
-bool tc_wgrad_supported(const Geom&, int, int) { return false; }
-size_t tc_wgrad_ws_bytes(const Geom&, int, int) { return 0; }
-hex_status_t tc_conv_fwd(const TcConvArgs&, cudaStream_t) { return HEX_ERR_UNSUPPORTED; }
-hex_status_t tc_conv_wgrad(const TcWgradArgs&, void*, size_t, cudaStream_t) { return HEX_ERR_UNSUPPORTED; }
-hex_status_t tc_pack_weights(const void*, void*, int, int, int, int, cudaStream_t) { return HEX_ERR_UNSUPPORTED; }
+constexpr int TC_BM = 128;  // output pixels per tile (UMMA M)
+constexpr int TC_BK = 64;   // channels per K block = one 128-byte swizzle row
+constexpr int TC_MAXT = 37; // taps supported on the tensor-core path (n <= 3)
+
+// ------------------------------------------------------------------ host: TMA descriptors
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+// NHWC bf16 tensor [B][H][W][C] viewed as parity view P (columns P, P+2, ...):
+// dims {C, H, ceil((W-P)/2), B}, box {64, RB, JB, BB}.
+static bool make_view_map(CUtensorMap* m, const void* base, int B, int H, int W, int C, int P, int RB, int JB,
+                          int BB) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    const int Wp = (W - P + 1) / 2;
+    if (Wp < 1) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)H, (cuuint64_t)Wp, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)W * C * 2, (cuuint64_t)2 * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {(cuuint32_t)TC_BK, (cuuint32_t)RB, (cuuint32_t)JB, (cuuint32_t)BB};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    void* addr = (void*)((const char*)base + (size_t)P * C * 2);
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, addr, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// packed weights [T][N][K] bf16, box {64, BN, 1}
+static bool make_weight_map(CUtensorMap* m, const void* base, int T, int N, int K, int BN) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)T};
+    cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)N * K * 2};
+    cuuint32_t box[3] = {(cuuint32_t)TC_BK, (cuuint32_t)BN, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// Pixel box (RB x JB x BB = npix) minimising the number of tiles over both views.
+static void choose_box(int B, int H, int W, int npix, int* RB, int* JB, int* BB) {
+    long best = -1;
+    for (int rb = 1; rb <= npix; rb *= 2)
+        for (int jb = 1; rb * jb <= npix; jb *= 2) {
+            const int bb = npix / (rb * jb);
+            if (rb > 256 || jb > 256 || bb > 256) continue;
+            long tiles = 0;
+            for (int P = 0; P < 2; ++P) {
+                const int Wp = (W - P + 1) / 2;
+                if (Wp < 1) continue;
+                tiles += (long)ceil_div(H, rb) * ceil_div(Wp, jb) * ceil_div(B, bb);
+            }
+            // prefer fewer tiles, then taller row boxes (vertical halo reuse in L2)
+            if (best < 0 || tiles < best || (tiles == best && rb > *RB)) {
+                best = tiles;
+                *RB = rb; *JB = jb; *BB = bb;
+            }
+        }
+}
+
+// ------------------------------------------------------------------ forward kernel
+struct TcFwdParams {
+    int B, H, W, Cin, Cout, T, parity;
+    int RB, JB, BB;
+    int rt, bt, jt0, jt1;  // tiles along rows, batch, and sub-columns of view 0 / view 1
+    int tiles0;            // m tiles of view 0
+    int n_tiles, total_tiles, kblocks;
+    int relu;
+    const float* bias;
+    __nv_bfloat16* y;
+    const __nv_bfloat16* relu_y;
+    int8_t tap_dc[2][TC_MAXT];
+    int8_t tap_dr[2][TC_MAXT];
+};
+
+struct TileCoord {
+    int P, r0, j0, b0, n0;
+};
+
+__device__ __forceinline__ TileCoord decode_fwd_tile(const TcFwdParams& p, int tile, int BN) {
+    TileCoord tc;
+    const int nt = tile % p.n_tiles;
+    int m = tile / p.n_tiles;
+    tc.n0 = nt * BN;
+    int jt;
+    if (m < p.tiles0) { tc.P = 0; jt = p.jt0; }
+    else { tc.P = 1; m -= p.tiles0; jt = p.jt1; }
+    const int rti = m % p.rt;
+    m /= p.rt;
+    const int jti = m % jt;
+    const int bti = m / jt;
+    tc.r0 = rti * p.RB;
+    tc.j0 = jti * p.JB;
+    tc.b0 = bti * p.BB;
+    return tc;
+}
+
+template <int BN>
+struct FwdCfg {
+    static constexpr int A_BYTES = TC_BM * 128;
+    static constexpr int B_BYTES = BN * 128;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+    static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
+                   const __grid_constant__ CUtensorMap map_w, const __grid_constant__ TcFwdParams p) {
+    using Cfg = FwdCfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE);
+    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* tfull = empty + Cfg::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < Cfg::STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4); }
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&map_x0);
+        ptx::prefetch_tmap(&map_x1);
+        ptx::prefetch_tmap(&map_w);
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int k_iters = p.T * p.kblocks;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+                const TileCoord tc = decode_fwd_tile(p, tile, BN);
+                const int pc = (tc.P + p.parity) & 1;
+                for (int t = 0; t < p.T; ++t) {
+                    const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
+                    const int Pv = (tc.P + dc) & 1;
+                    const int jsh = (tc.P + dc - Pv) / 2;
+                    const CUtensorMap* mx = Pv ? &map_x1 : &map_x0;
+                    for (int kb = 0; kb < p.kblocks; ++kb) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sa = smem + stage * Cfg::STAGE;
+                        ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
+                        ptx::tma_load_4d(mx, &full[stage], sa, kb * TC_BK, tc.r0 + dr, tc.j0 + jsh, tc.b0);
+                        ptx::tma_load_3d(&map_w, &full[stage], sa + Cfg::A_BYTES, kb * TC_BK, tc.n0, t);
+                        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(TC_BM, BN, 0, 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t aphase = 0;
+            for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+                ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int it = 0; it < k_iters; ++it) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(smem + stage * Cfg::STAGE);
+                    const uint32_t b0 = a0 + Cfg::A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < TC_BK / 16; ++k) {
+                        const uint64_t ad = ptx::smem_desc_sw128(a0 + k * 32, 16, 1024);
+                        const uint64_t bd = ptx::smem_desc_sw128(b0 + k * 32, 16, 1024);
+                        ptx::mma_bf16(d, ad, bd, idesc, (it | k) != 0);
+                    }
+                    ptx::mma_commit(&empty[stage]);
+                    if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) aphase ^= 1;
+            }
+        }
+    } else {
+        // epilogue: warps 2..5 own TMEM lane quadrants (warp % 4)
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+            const TileCoord tc = decode_fwd_tile(p, tile, BN);
+            const int rl = row % p.RB;
+            const int jl = (row / p.RB) % p.JB;
+            const int bl = row / (p.RB * p.JB);
+            const int r = tc.r0 + rl, c = 2 * (tc.j0 + jl) + tc.P, b = tc.b0 + bl;
+            const bool valid = r < p.H && c < p.W && b < p.B;
+            const int64_t off = valid ? ((((int64_t)b * p.H + r) * p.W + c) * p.Cout + tc.n0) : 0;
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t v[32];
+                ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, v);
+                ptx::tmem_ld_wait();
+                if (valid) {
+                    const int co = tc.n0 + ch * 32;
+                    uint32_t mask[16];
+                    if (p.relu_y) {
+                        const uint4* m4 = reinterpret_cast<const uint4*>(p.relu_y + off + ch * 32);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            uint4 mm = __ldg(m4 + i);
+                            mask[4 * i] = mm.x; mask[4 * i + 1] = mm.y; mask[4 * i + 2] = mm.z; mask[4 * i + 3] = mm.w;
+                        }
+                    }
+                    uint32_t packed[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        float f0 = __uint_as_float(v[2 * i]);
+                        float f1 = __uint_as_float(v[2 * i + 1]);
+                        if (p.bias) { f0 += __ldg(p.bias + co + 2 * i); f1 += __ldg(p.bias + co + 2 * i + 1); }
+                        if (p.relu) { f0 = fmaxf(f0, 0.f); f1 = fmaxf(f1, 0.f); }
+                        if (p.relu_y) {
+                            __nv_bfloat162 mm = *reinterpret_cast<__nv_bfloat162*>(&mask[i]);
+                            if (!(__low2float(mm) > 0.f)) f0 = 0.f;
+                            if (!(__high2float(mm) > 0.f)) f1 = 0.f;
+                        }
+                        __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
+                        packed[i] = *reinterpret_cast<uint32_t*>(&h);
+                    }
+                    uint4* dst = reinterpret_cast<uint4*>(p.y + off + ch * 32);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    }
+}
+
+// ------------------------------------------------------------------ weight packing
+__global__ void pack_weights_kernel(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wp, int Cout,
+                                    int Cin, int T, int tr) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)T * Cout * Cin;
+    if (idx >= total) return;
+    if (!tr) {
+        // wp[t][co][ci] = w[co][ci][t]
+        const int ci = (int)(idx % Cin);
+        const int64_t q = idx / Cin;
+        const int co = (int)(q % Cout);
+        const int t = (int)(q / Cout);
+        wp[idx] = w[((int64_t)co * Cin + ci) * T + t];
+    } else {
+        // wp[t][ci][co] = w[co][ci][T-1-t]
+        const int co = (int)(idx % Cout);
+        const int64_t q = idx / Cout;
+        const int ci = (int)(q % Cin);
+        const int t = (int)(q / Cin);
+        wp[idx] = w[((int64_t)co * Cin + ci) * T + (T - 1 - t)];
+    }
+}
+
+hex_status_t tc_pack_weights(const void* w, void* wpack, int Cout, int Cin, int T, int tr, cudaStream_t st) {
+    const int64_t total = (int64_t)T * Cout * Cin;
+    pack_weights_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)wpack, Cout,
+                                                              Cin, T, tr);
+    count_launch();
+    return last_launch_status();
+}
+
+// ------------------------------------------------------------------ forward host
+static int pick_bn(int Cout) {
+    if (Cout % 256 == 0) return 256;
+    if (Cout % 128 == 0) return 128;
+    if (Cout % 64 == 0) return 64;
+    return 0;
+}
+
+bool tc_conv_supported(const Geom& g, int Cin, int Cout) {
+    if (g.s != 1 || g.T > TC_MAXT) return false;
+    if (Cin % TC_BK != 0 || pick_bn(Cout) == 0) return false;
+    if (g.W < 2) return false;
+    if (getenv("HEXCONV_DISABLE_TC")) return false;
+    return get_encode() != nullptr;
+}
+
+template <int BN>
+static hex_status_t launch_fwd_bn(const CUtensorMap& mx0, const CUtensorMap& mx1, const CUtensorMap& mw,
+                                  const TcFwdParams& p, cudaStream_t st) {
+    using Cfg = FwdCfg<BN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(tc_conv_fwd_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) !=
+            cudaSuccess)
+            return HEX_ERR_CUDA;
+        attr_set = true;
+    }
+    const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+    tc_conv_fwd_kernel<BN><<<grid, 192, Cfg::SMEM, st>>>(mx0, mx1, mw, p);
+    count_launch();
+    return last_launch_status();
+}
+
+hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
+    const Geom& g = a.g;
+    TcFwdParams p{};
+    p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
+    choose_box(g.B, g.H, g.W, TC_BM, &p.RB, &p.JB, &p.BB);
+    p.rt = ceil_div(g.H, p.RB);
+    p.bt = ceil_div(g.B, p.BB);
+    p.jt0 = ceil_div((g.W + 1) / 2, p.JB);
+    p.jt1 = ceil_div(g.W / 2, p.JB);
+    p.tiles0 = p.rt * p.jt0 * p.bt;
+    const int BN = pick_bn(a.Cout);
+    p.n_tiles = a.Cout / BN;
+    p.total_tiles = (p.tiles0 + p.rt * p.jt1 * p.bt) * p.n_tiles;
+    p.kblocks = a.Cin / TC_BK;
+    p.relu = a.relu;
+    p.bias = a.bias;
+    p.y = (__nv_bfloat16*)a.y;
+    p.relu_y = (const __nv_bfloat16*)a.relu_y;
+    for (int pc = 0; pc < 2; ++pc)
+        for (int t = 0; t < g.T; ++t) {
+            int dc, dr;
+            tap_offset(g.n, pc, t, &dc, &dr);
+            p.tap_dc[pc][t] = (int8_t)dc;
+            p.tap_dr[pc][t] = (int8_t)dr;
+        }
+    CUtensorMap mx0, mx1, mw;
+    if (!make_view_map(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
+    if (!make_view_map(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
+    if (!make_weight_map(&mw, a.wpack, g.T, a.Cout, a.Cin, BN)) return HEX_ERR_CUDA;
+    switch (BN) {
+        case 256: return launch_fwd_bn<256>(mx0, mx1, mw, p, st);
+        case 128: return launch_fwd_bn<128>(mx0, mx1, mw, p, st);
+        default: return launch_fwd_bn<64>(mx0, mx1, mw, p, st);
+    }
+}
+
+// ------------------------------------------------------------------ weight-gradient kernel
+// Unit = (co tile of 128, ci tile of N, tap group of TG taps, pixel chunk).
+// Per pixel tile (64 pixels of one parity view, RB x JB x BB):
+//   A = dy box   [64 px rows][64 co] x 2      (MN-major, co contiguous)
+//   B = x_t box  [64 px rows][64 ci] x N/64   (MN-major, ci contiguous), one per tap
+//   D_t[co][ci] += A^T-contract-B over the 64 pixels, D_t in TMEM columns t*N.
+constexpr int WG_PIX = 64;
+constexpr int WG_STAGES = 2;
+constexpr int WG_BOX_BYTES = WG_PIX * 128;  // one 64-channel box: 8 KB
+constexpr int WG_STAGE_BYTES = 10 * WG_BOX_BYTES;  // 2 dy boxes + up to 8 x boxes (512 TMEM columns)
+
+struct TcWgParams {
+    int B, H, W, Cin, Cout, T, parity;
+    int RB, JB, BB;
+    int rt, bt, jt0, jt1, tiles0, ptiles;  // pixel tiles
+    int N, TG, groups, co_tiles, ci_tiles, chunks, tiles_per_chunk;
+    float* part;  // [chunks][T][Cout][Cin]
+    int8_t tap_dc[2][TC_MAXT];
+    int8_t tap_dr[2][TC_MAXT];
+};
+
+__device__ __forceinline__ void decode_ptile(const TcWgParams& p, int m, int* P, int* r0, int* j0, int* b0) {
+    int jt;
+    if (m < p.tiles0) { *P = 0; jt = p.jt0; }
+    else { *P = 1; m -= p.tiles0; jt = p.jt1; }
+    const int rti = m % p.rt;
+    m /= p.rt;
+    const int jti = m % jt;
+    const int bti = m / jt;
+    *r0 = rti * p.RB;
+    *j0 = jti * p.JB;
+    *b0 = bti * p.BB;
+}
+
+__global__ void __launch_bounds__(192, 1)
+tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
+                     const __grid_constant__ CUtensorMap map_dy0, const __grid_constant__ CUtensorMap map_dy1,
+                     const __grid_constant__ TcWgParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + WG_STAGES * WG_STAGE_BYTES);
+    uint64_t* empty = full + WG_STAGES;
+    uint64_t* tfull = empty + WG_STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+
+    // unit decode
+    int u = blockIdx.x;
+    const int chunk = u % p.chunks; u /= p.chunks;
+    const int grp = u % p.groups; u /= p.groups;
+    const int cit = u % p.ci_tiles;
+    const int cot = u / p.ci_tiles;
+    const int t0 = grp * p.TG;
+    const int ntaps = min(p.TG, p.T - t0);
+    const int co0 = cot * 128, ci0 = cit * p.N;
+    const int pt_begin = chunk * p.tiles_per_chunk;
+    const int pt_end = min(p.ptiles, pt_begin + p.tiles_per_chunk);
+    const int nbx = p.N / 64;  // x boxes per tap
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < WG_STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        ptx::mbar_init(tfull, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t stage_bytes = (2 + ntaps * nbx) * WG_BOX_BYTES;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int pt = pt_begin; pt < pt_end; ++pt) {
+                int P, r0, j0, b0;
+                decode_ptile(p, pt, &P, &r0, &j0, &b0);
+                const int pc = (P + p.parity) & 1;
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* s = smem + stage * WG_STAGE_BYTES;
+                ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
+                const CUtensorMap* mdy = P ? &map_dy1 : &map_dy0;
+                ptx::tma_load_4d(mdy, &full[stage], s, co0, r0, j0, b0);
+                ptx::tma_load_4d(mdy, &full[stage], s + WG_BOX_BYTES, co0 + 64, r0, j0, b0);
+                for (int tl = 0; tl < ntaps; ++tl) {
+                    const int t = t0 + tl;
+                    const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
+                    const int Pv = (P + dc) & 1;
+                    const int jsh = (P + dc - Pv) / 2;
+                    const CUtensorMap* mx = Pv ? &map_x1 : &map_x0;
+                    for (int i = 0; i < nbx; ++i)
+                        ptx::tma_load_4d(mx, &full[stage], s + (2 + tl * nbx + i) * WG_BOX_BYTES, ci0 + 64 * i,
+                                         r0 + dr, j0 + jsh, b0);
+                }
+                if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = ptx::idesc_bf16(128, p.N, 1, 1);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int pt = pt_begin; pt < pt_end; ++pt) {
+                ptx::mbar_wait(&full[stage], phase);
+                ptx::tc_fence_after();
+                const uint32_t s = ptx::smem_u32(smem + stage * WG_STAGE_BYTES);
+                for (int tl = 0; tl < ntaps; ++tl) {
+                    const uint32_t bx = s + (2 + tl * nbx) * WG_BOX_BYTES;
+#pragma unroll
+                    for (int k = 0; k < WG_PIX / 16; ++k) {
+                        // MN-major SW128: 8-row K groups 1024 B apart, 64-element MN blocks one box apart
+                        const uint64_t ad = ptx::smem_desc_sw128(s + k * 2048, WG_BOX_BYTES, 1024);
+                        const uint64_t bd = ptx::smem_desc_sw128(bx + k * 2048, WG_BOX_BYTES, 1024);
+                        ptx::mma_bf16(tmem_base + tl * p.N, ad, bd, idesc, (pt != pt_begin) || (k != 0));
+                    }
+                }
+                ptx::mma_commit(&empty[stage]);
+                if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
+            }
+            ptx::mma_commit(tfull);
+        }
+    } else {
+        const int q = warp & 3;
+        const int row = q * 32 + lane;  // co local
+        ptx::mbar_wait(tfull, 0);
+        ptx::tc_fence_after();
+        const int co = co0 + row;
+        for (int tl = 0; tl < ntaps; ++tl) {
+            float* dst = p.part + (((int64_t)chunk * p.T + (t0 + tl)) * p.Cout + co) * p.Cin + ci0;
+#pragma unroll 1
+            for (int ch = 0; ch < p.N / 32; ++ch) {
+                uint32_t v[32];
+                ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + tl * p.N + ch * 32, v);
+                ptx::tmem_ld_wait();
+                const bool empty_chunk = pt_end <= pt_begin;
+                float4* d4 = reinterpret_cast<float4*>(dst + ch * 32);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    float4 f;
+                    f.x = empty_chunk ? 0.f : __uint_as_float(v[4 * i]);
+                    f.y = empty_chunk ? 0.f : __uint_as_float(v[4 * i + 1]);
+                    f.z = empty_chunk ? 0.f : __uint_as_float(v[4 * i + 2]);
+                    f.w = empty_chunk ? 0.f : __uint_as_float(v[4 * i + 3]);
+                    d4[i] = f;
+                }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, 512);
+    }
+}
+
+// dw[co][ci][t] (+)= sum_chunk part[chunk][t][co][ci]   (fixed chunk order)
+__global__ void wgrad_tc_reduce_kernel(const float* __restrict__ part, int chunks, int T, int Cout, int Cin,
+                                       float* __restrict__ dw, int accumulate) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)T * Cout * Cin;
+    if (idx >= total) return;
+    // idx enumerates (t, co, ci) with ci fastest (coalesced partial reads)
+    const int ci = (int)(idx % Cin);
+    const int64_t q = idx / Cin;
+    const int co = (int)(q % Cout);
+    const int t = (int)(q / Cout);
+    float s = 0.f;
+    for (int c = 0; c < chunks; ++c) s += part[(int64_t)c * total + idx];
+    float* d = dw + ((int64_t)co * Cin + ci) * T + t;
+    *d = accumulate ? *d + s : s;
+}
+
+// dbias partials: part[chunk][co] = sum over the chunk's pixels of dy (NHWC bf16)
+__global__ void dbias_partial_kernel(const __nv_bfloat16* __restrict__ dy, int64_t npix, int Cout, int64_t chunk_len,
+                                     float* __restrict__ part) {
+    const int chunk = blockIdx.x;
+    const int64_t p0 = chunk * chunk_len;
+    const int64_t p1 = min(npix, p0 + chunk_len);
+    for (int co = threadIdx.x; co < Cout; co += blockDim.x) {
+        float s = 0.f;
+        for (int64_t px = p0; px < p1; ++px) s += __bfloat162float(dy[px * Cout + co]);
+        part[(int64_t)chunk * Cout + co] = s;
+    }
+}
+__global__ void dbias_reduce_kernel(const float* __restrict__ part, int chunks, int Cout, float* __restrict__ db,
+                                    int accumulate) {
+    const int co = blockIdx.x * blockDim.x + threadIdx.x;
+    if (co >= Cout) return;
+    float s = 0.f;
+    for (int c = 0; c < chunks; ++c) s += part[(int64_t)c * Cout + co];
+    db[co] = accumulate ? db[co] + s : s;
+}
+
+constexpr int DB_CHUNKS = 256;
+
+struct WgPlan {
+    int RB, JB, BB, rt, bt, jt0, jt1, tiles0, ptiles;
+    int N, TG, groups, co_tiles, ci_tiles, chunks, tiles_per_chunk;
+};
+
+static WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
+    WgPlan w{};
+    choose_box(g.B, g.H, g.W, WG_PIX, &w.RB, &w.JB, &w.BB);
+    w.rt = ceil_div(g.H, w.RB);
+    w.bt = ceil_div(g.B, w.BB);
+    w.jt0 = ceil_div((g.W + 1) / 2, w.JB);
+    w.jt1 = ceil_div(g.W / 2, w.JB);
+    w.tiles0 = w.rt * w.jt0 * w.bt;
+    w.ptiles = w.tiles0 + w.rt * w.jt1 * w.bt;
+    w.N = Cin % 256 == 0 ? 256 : (Cin % 128 == 0 ? 128 : 64);
+    w.TG = 512 / w.N;
+    if (w.TG > g.T) w.TG = g.T;
+    w.groups = ceil_div(g.T, w.TG);
+    w.co_tiles = Cout / 128;
+    w.ci_tiles = Cin / w.N;
+    const int base_units = w.co_tiles * w.ci_tiles * w.groups;
+    int chunks = ceil_div(2 * 148, base_units);
+    if (chunks > w.ptiles) chunks = w.ptiles;
+    if (chunks < 1) chunks = 1;
+    w.tiles_per_chunk = ceil_div(w.ptiles, chunks);
+    w.chunks = ceil_div(w.ptiles, w.tiles_per_chunk);
+    return w;
+}
+
+bool tc_wgrad_supported(const Geom& g, int Cin, int Cout) {
+    if (g.s != 1 || g.T > TC_MAXT || g.W < 2) return false;
+    if (Cout % 128 != 0 || Cin % 64 != 0) return false;
+    if (getenv("HEXCONV_DISABLE_TC")) return false;
+    return get_encode() != nullptr;
+}
+
+size_t tc_wgrad_ws_bytes(const Geom& g, int Cin, int Cout) {
+    const WgPlan w = wg_plan(g, Cin, Cout);
+    return (size_t)w.chunks * g.T * Cout * Cin * sizeof(float) + (size_t)DB_CHUNKS * Cout * sizeof(float) + 256;
+}
+
+hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
+    const Geom& g = a.g;
+    const WgPlan w = wg_plan(g, a.Cin, a.Cout);
+    if (ws_bytes < tc_wgrad_ws_bytes(g, a.Cin, a.Cout)) return HEX_ERR_WORKSPACE;
+    TcWgParams p{};
+    p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
+    p.RB = w.RB; p.JB = w.JB; p.BB = w.BB; p.rt = w.rt; p.bt = w.bt; p.jt0 = w.jt0; p.jt1 = w.jt1;
+    p.tiles0 = w.tiles0; p.ptiles = w.ptiles;
+    p.N = w.N; p.TG = w.TG; p.groups = w.groups; p.co_tiles = w.co_tiles; p.ci_tiles = w.ci_tiles;
+    p.chunks = w.chunks; p.tiles_per_chunk = w.tiles_per_chunk;
+    p.part = (float*)ws;
+    for (int pc = 0; pc < 2; ++pc)
+        for (int t = 0; t < g.T; ++t) {
+            int dc, dr;
+            tap_offset(g.n, pc, t, &dc, &dr);
+            p.tap_dc[pc][t] = (int8_t)dc;
+            p.tap_dr[pc][t] = (int8_t)dr;
+        }
+    CUtensorMap mx0, mx1, md0, md1;
+    if (!make_view_map(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
+    if (!make_view_map(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
+    if (!make_view_map(&md0, a.dy, g.B, g.H, g.W, a.Cout, 0, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
+    if (!make_view_map(&md1, a.dy, g.B, g.H, g.W, a.Cout, 1, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
+    const int smem = WG_STAGES * WG_STAGE_BYTES + 1024 + 128;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(tc_conv_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return HEX_ERR_CUDA;
+        attr_set = true;
+    }
+    const int units = w.co_tiles * w.ci_tiles * w.groups * w.chunks;
+    tc_conv_wgrad_kernel<<<units, 192, smem, st>>>(mx0, mx1, md0, md1, p);
+    count_launch();
+    const int64_t total = (int64_t)g.T * a.Cout * a.Cin;
+    wgrad_tc_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const float*)ws, w.chunks, g.T, a.Cout, a.Cin,
+                                                                 a.dw, a.accumulate);
+    count_launch();
+    if (a.dbias) {
+        float* dbp = (float*)ws + (size_t)w.chunks * g.T * a.Cout * a.Cin;
+        const int64_t npix = (int64_t)g.B * g.H * g.W;
+        const int64_t len = (npix + DB_CHUNKS - 1) / DB_CHUNKS;
+        dbias_partial_kernel<<<DB_CHUNKS, 256, 0, st>>>((const __nv_bfloat16*)a.dy, npix, a.Cout, len, dbp);
+        dbias_reduce_kernel<<<ceil_div(a.Cout, 256), 256, 0, st>>>(dbp, DB_CHUNKS, a.Cout, a.dbias, a.accumulate);
+        count_launch(2);
+    }
+    return last_launch_status();
+}
 
 }  // namespace hexconv

@@ -63,6 +63,14 @@ def conv_desc(B, Cin, Cout, H, W, n, stride, parity, dtype, layout) -> A.ConvDes
     return A.ConvDesc(B, Cin, Cout, H, W, n, stride, parity, _DTYPES[dtype], _LAYOUTS[layout])
 
 
+def conv_algo(B, Cin, Cout, H, W, n, stride, parity, dtype, layout, pass_id=0) -> str:
+    """'tcgen05' or 'stencil': the kernel family the library picks for this call."""
+    d = conv_desc(B, Cin, Cout, H, W, n, stride, parity, dtype, layout)
+    a = ctypes.c_int32()
+    A.check(A.lib().hex_conv2d_algo(ctypes.byref(d), pass_id, ctypes.byref(a)), "hex_conv2d_algo")
+    return "tcgen05" if a.value == 1 else "stencil"
+
+
 def _workspace(desc, pass_id, device):
     nbytes = ctypes.c_size_t()
     A.check(A.lib().hex_conv2d_workspace_size(ctypes.byref(desc), pass_id, ctypes.byref(nbytes)),

@@ -1,0 +1,101 @@
+"""GPU parity of the tcgen05 tensor-core path (bf16 NHWC, stride 1) against the
+fp64 oracle fed the same bf16-rounded inputs.  Tolerance 2e-2 normwise for
+bf16 outputs (north_star); weight gradients are fp32 sums of exact bf16
+products, checked at 1e-3 normwise (fp32 accumulation over up to ~1e5 terms).
+Each case asserts the library actually routed it to the tensor-core kernels.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-2
+TOL_WGRAD = 1e-3
+
+
+@pytest.fixture(scope="module")
+def F():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1903_01814_b200 import functional
+    return functional
+
+
+def rel(gpu, ref):
+    return float(np.abs(np.asarray(gpu, np.float64) - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def nhwc(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).permute(0, 2, 3, 1).contiguous().to(
+        torch.bfloat16).cuda()
+
+
+def back(t):
+    return t.float().permute(0, 3, 1, 2).cpu().numpy().astype(np.float64)
+
+
+def case(F, oracle, B, Cin, Cout, H, W, n, pi, seed, relu=False, bias=True):
+    import synth
+    T = oracle.num_taps(n)
+    x = synth.round_bf16(synth.normal((B, Cin, H, W), seed))
+    w = synth.round_bf16(synth.normal((Cout, Cin, T), seed + 1, 1.0 / np.sqrt(Cin * T)))
+    b = synth.round_f32(synth.normal((Cout,), seed + 2)) if bias else None
+    g = synth.round_bf16(synth.normal((B, Cout, H, W), seed + 3))
+    for pass_id in (0, 1, 2):
+        assert F.conv_algo(B, Cin, Cout, H, W, n, 1, pi, torch.bfloat16, "NHWC", pass_id) == "tcgen05"
+    xd, gd = nhwc(x), nhwc(g)
+    wd = torch.from_numpy(w.astype(np.float32)).to(torch.bfloat16).cuda()
+    bd = None if b is None else torch.from_numpy(b.astype(np.float32)).cuda()
+    y = F.conv2d_fwd(xd, wd, bd, n=n, parity=pi, relu=relu, layout="NHWC")
+    yref = oracle.conv2d_fwd(x, w, b, n=n, pi=pi)
+    if relu:
+        yref = np.maximum(yref, 0)
+    assert rel(back(y), yref) <= TOL_BF16, ("fwd", B, Cin, Cout, H, W, n, pi)
+    dxr, dwr, dbr = oracle.conv2d_bwd(x, w, g, n=n, pi=pi)
+    dx = F.conv2d_bwd_data(gd, wd, (H, W), n=n, parity=pi, layout="NHWC")
+    assert rel(back(dx), dxr) <= TOL_BF16, ("dgrad", B, Cin, Cout, H, W, n, pi)
+    # fused ReLU-backward mask in the dgrad epilogue
+    dxm = F.conv2d_bwd_data(gd, wd, (H, W), n=n, parity=pi, layout="NHWC", relu_y=xd)
+    assert rel(back(dxm), dxr * (x > 0)) <= TOL_BF16
+    dw, db = F.conv2d_bwd_weight(xd, gd, n=n, parity=pi, layout="NHWC")
+    assert rel(dw.cpu().numpy(), dwr) <= TOL_WGRAD, ("wgrad", B, Cin, Cout, H, W, n, pi)
+    assert rel(db.cpu().numpy(), dbr) <= TOL_WGRAD
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+@pytest.mark.parametrize("pi", [0, 1])
+def test_tc_small_ragged(F, oracle, n, pi):
+    # ragged tiles in every direction: odd W (views of unequal width), H not a box multiple
+    case(F, oracle, 3, 64, 128, 13, 11, n, pi, 10 * n + pi)
+
+
+@pytest.mark.parametrize("Cin,Cout", [(64, 64), (128, 256), (256, 128), (64, 512)])
+def test_tc_channel_tiles(F, oracle, Cin, Cout):
+    case(F, oracle, 2, Cin, Cout, 10, 12, 1, 0, Cin + Cout, relu=True)
+
+
+def test_tc_c5_like_shapes(F, oracle):
+    # the C5 layer shapes at a small batch (96x96 / 48x48 / 24x24 grids)
+    case(F, oracle, 1, 64, 128, 24, 24, 1, 0, 1)
+    case(F, oracle, 2, 128, 128, 16, 16, 2, 0, 2)
+
+
+def test_tc_deterministic(F):
+    x = torch.randn(4, 16, 16, 128, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(128, 128, 19, device="cuda") * 0.02).to(torch.bfloat16)
+    g = torch.randn(4, 16, 16, 128, device="cuda").to(torch.bfloat16)
+    assert torch.equal(F.conv2d_fwd(x, w, n=2, layout="NHWC"), F.conv2d_fwd(x, w, n=2, layout="NHWC"))
+    a = F.conv2d_bwd_weight(x, g, n=2, layout="NHWC")[0]
+    b = F.conv2d_bwd_weight(x, g, n=2, layout="NHWC")[0]
+    assert torch.equal(a, b)
+
+
+def test_tc_matches_stencil_path(F, monkeypatch):
+    # same bf16 inputs through both kernel families (fp32 accumulation in both)
+    x = torch.randn(2, 12, 14, 64, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(64, 64, 7, device="cuda") * 0.05).to(torch.bfloat16)
+    y_tc = F.conv2d_fwd(x, w, n=1, layout="NHWC").float()
+    xs = x.permute(0, 3, 1, 2).contiguous()
+    y_st = F.conv2d_fwd(xs, w, n=1, layout="NCHW").float().permute(0, 2, 3, 1)
+    assert (y_tc - y_st).abs().max().item() <= 2e-2 * y_st.abs().max().item()
