@@ -1,0 +1,347 @@
+"""bench.py -- BASELINE config 5: data-parallel training step of the 6-layer
+hexagonal CNN (256 images per GPU, 96x96 offset-column grid, bf16 NHWC, fp32
+master weights, weight-gradient allreduce over NCCL), reported as images/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1, one rank per GPU)
+
+One JSON line on rank 0:
+  value     images/s of the whole job with inputs resident in HBM (device timed,
+            CUDA events, barrier + synchronize on both sides, max over ranks)
+  e2e       the same metric through the public API with each step's batch
+            copied from pinned host memory and the loss read back
+  roofline  the dominant kernel family (tcgen05 implicit-GEMM conv) against the
+            measured sustained bf16 tensor-core peak, from live CUDA events
+  cpu_baseline  the fp64 oracle (test infrastructure) on a bounded sample
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "hex-conv TFLOP/s (valid taps) & pool/conv HBM GB/s vs B200 roofline; images/s 1–8 GPU"
+WORKLOAD = "c5: 6-layer hex CNN (1-64-128-128-256-256-256, n=2,1,2,1,2,1, maxpool n1 s2 after L2/L4, GAP, linear->2, CE) DP train step, 256 img/GPU, 96x96"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        loaded = [v for v in sm if v > 0.5 * (mx or max(sm))] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ data
+def make_batches(nb, B, H, W, R, seed):
+    import numpy as np
+
+    import synth
+    xs, ys = [], []
+    for i in range(nb):
+        img = synth.shower_images(B, H, W, R, seed + i)            # [B,1,H,W] float32
+        xs.append(np.ascontiguousarray(img.transpose(0, 2, 3, 1)))  # NHWC, C = 1
+        ys.append(synth.labels(B, seed + 100 + i))
+    return xs, ys
+
+
+# ------------------------------------------------------------------ oracle legs (test infrastructure)
+def oracle_train_sample(n_images: int, seed: int = 0):
+    """One C5 training step of the fp64 oracle on n_images (a bounded sample of
+    the workload): convs + ReLU + max pools forward, GAP/linear/CE head, full
+    backward (dgrad, wgrad, pool bwd) and the SGD-momentum update.  Returns
+    (seconds, threads)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    ch = (1, 64, 128, 128, 256, 256, 256)
+    ns = (2, 1, 2, 1, 2, 1)
+    rng = np.random.default_rng(seed)
+    Ws = [rng.uniform(-1, 1, size=(ch[l + 1], ch[l], oracle.num_taps(ns[l]))) * (6.0 / (ch[l] * oracle.num_taps(ns[l]))) ** 0.5
+          for l in range(6)]
+    bs = [np.zeros(ch[l + 1]) for l in range(6)]
+    wl = rng.uniform(-1, 1, size=(2, 256)) / 16.0
+    bl = np.zeros(2)
+    x = synth.round_bf16(synth.shower_images(n_images, 96, 96, 47, seed + 7).astype(np.float64))
+    lab = synth.labels(n_images, seed + 8)
+    t0 = time.perf_counter()
+    acts, inputs, pools = [], [], {}
+    h = x
+    for l in range(6):
+        inputs.append(h)
+        a = np.maximum(oracle.conv2d_fwd(h, Ws[l], bs[l], n=ns[l]), 0.0)
+        acts.append(a)
+        h = a
+        if l in (1, 3):
+            p, am = oracle.pool2d_fwd(a, n=1, s=2, mode="max")
+            pools[l] = (p, am, a.shape[-2:])
+            h = p
+    gap = h.mean(axis=(2, 3))
+    logits = gap @ wl.T + bl
+    z = logits - logits.max(1, keepdims=True)
+    pr = np.exp(z) / np.exp(z).sum(1, keepdims=True)
+    dlog = (pr - np.eye(2)[lab]) / n_images
+    dwl, dbl = dlog.T @ gap, dlog.sum(0)
+    g = (dlog @ wl)[:, :, None, None] / (h.shape[2] * h.shape[3]) * np.ones_like(h)
+    for l in reversed(range(6)):
+        g = g * (acts[l] > 0) if l not in (1, 3) else g
+        if l in (1, 3):
+            p, am, (H, W) = pools[l]
+            g = oracle.pool2d_bwd(g, am, H, W, n=1, s=2, mode="max") * (acts[l] > 0)
+        dx, dw, db = oracle.conv2d_bwd(inputs[l], Ws[l], g, n=ns[l], need=("dx", "dw", "db") if l else ("dw", "db"))
+        Ws[l] -= 0.01 * dw
+        bs[l] -= 0.01 * db
+        g = dx
+    wl -= 0.01 * dwl
+    bl -= 0.01 * dbl
+    return time.perf_counter() - t0, oracle.max_threads()
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the fp64 oracle on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    n_img = 1
+    for _ in range(args.warmup):
+        oracle_train_sample(n_img)
+    ts = []
+    for _ in range(args.steps):
+        dt, threads = oracle_train_sample(n_img)
+        ts.append(dt)
+    tot = sum(ts)
+    value = n_img * len(ts) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(ts) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": 256 * args.gpus, "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{n_img} image per step through the full C5 fwd+bwd+SGD in fp64 "
+                                   f"(bounded sample of the 256-image batch)"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1903_01814_b200 import _abi
+    from paper_1903_01814_b200.hexcnn import HexCNN
+
+    B = args.batch
+    model = HexCNN(batch=B, device=dev, seed=0)
+    NB = 4
+    xs_np, ys_np = make_batches(NB, B, 96, 96, 47, seed=1000 + 17 * rank)
+    xs = [torch.from_numpy(a).to(dev).to(torch.bfloat16) for a in xs_np]
+    ys = [torch.from_numpy(a).to(dev) for a in ys_np]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    # warm-up
+    for i in range(args.warmup):
+        model.step(xs[i % NB], ys[i % NB])
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region (with per-conv events for the roofline)
+    model.timer = []
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = _abi.launch_count()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for i in range(args.steps):
+        model.step(xs[i % NB], ys[i % NB])
+    t_end.record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = _abi.launch_count() - l0
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end)
+    ms = max_over_ranks(ms)
+    ms_step = ms / args.steps
+    value = world * B * args.steps / (ms / 1e3)
+    events = model.timer
+    model.timer = None
+
+    # roofline: tcgen05 implicit-GEMM conv kernel family (fwd + dgrad of L2..L6)
+    flops_img, per_layer = model.flops_per_image()
+    tc_ms = 0.0
+    tc_flops = 0.0
+    tc_launches = 0
+    share = {}
+    for kind, l, e0, e1 in events:
+        dt = e0.elapsed_time(e1)
+        share[kind] = share.get(kind, 0.0) + dt
+        if l > 0 and kind in ("fwd", "dgrad"):
+            tc_ms += dt
+            tc_flops += per_layer[l][0] * B
+            tc_launches += 1
+    peaks, peak_src = load_peaks()
+    peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    achieved = tc_flops / (tc_ms / 1e3) / 1e12 if tc_ms > 0 else None
+    total_tf = flops_img * B / (ms_step / 1e3) / 1e12
+
+    # ---- end-to-end through the public API with host buffers
+    pin_x = [torch.from_numpy(a.astype(np.float32)).to(torch.bfloat16).pin_memory() for a in xs_np]
+    pin_y = [torch.from_numpy(a).pin_memory() for a in ys_np]
+    xd = torch.empty_like(xs[0])
+    yd = torch.empty_like(ys[0])
+    loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        xd.copy_(pin_x[i % NB], non_blocking=True)
+        yd.copy_(pin_y[i % NB], non_blocking=True)
+        loss = model.step(xd, yd)
+        loss_h.copy_(loss, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_value = world * B * args.steps / (e2e_ms / 1e3)
+    h2d = pin_x[0].numel() * pin_x[0].element_size() + pin_y[0].numel() * pin_y[0].element_size()
+
+    # ---- oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        dt, threads = oracle_train_sample(1)
+        cpu = {"value": 1.0 / dt, "unit": "images/s", "cores": threads, "kind": "oracle",
+               "sample": "1 image through the full C5 fwd+bwd+SGD step in fp64 (bounded sample of the "
+                         "256-image batch)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "global_batch": B * world, "per_gpu_batch": B, "grid": "96x96",
+                       "parallelism": f"dp{world}", "l2": "working set > L2 (activations ~2.5 GB/step)"},
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+            "roofline": {"bound": "tensor", "kernel": "tc_conv_fwd_kernel (tcgen05 implicit-GEMM hex conv; "
+                                                      "fwd + bwd-data of L2-L6)",
+                         "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": (achieved / peak_tf) if achieved else None, "traffic": None,
+                         "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+                         "launches_per_step": tc_launches // max(args.steps, 1)},
+            "step_tflops": total_tf,
+            "step_share_ms": {k: v / args.steps for k, v in share.items()},
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

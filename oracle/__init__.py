@@ -56,6 +56,9 @@ def lib():
         L.oracle_conv2d_bwd.argtypes = [ctypes.c_int] * 8 + [ctypes.c_void_p] * 6
         L.oracle_pool2d_fwd.argtypes = [ctypes.c_int] * 8 + [ctypes.c_void_p] * 3
         L.oracle_pool2d_bwd.argtypes = [ctypes.c_int] * 8 + [ctypes.c_void_p] * 3
+        L.oracle_conv2d_bwd_weight_at.argtypes = [ctypes.c_int] * 6 + [
+            ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+            ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -200,3 +203,36 @@ def pool2d_bwd(dy, argmax, H: int, W: int, n: int = 1, s: int = 1, pi: int = 0, 
 
 def max_threads() -> int:
     return int(lib().oracle_max_threads())
+
+
+def _storage(a):
+    """(contiguous array, fmt) for float32 arrays or bf16 bit patterns (uint16)."""
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.float32:
+        return a, 0
+    if a.dtype == np.uint16:
+        return a, 1
+    raise TypeError("x / dy must be float32 or uint16 (bf16 bits)")
+
+
+def conv2d_bwd_weight_at(x, dy, pts, n: int = 1, s: int = 1, pi: int = 0, layout: str = "NCHW"):
+    """dw[co, ci, t] at the listed (co, ci, t) points; x, dy in storage format
+    (float32, or uint16 bf16 bits) and `layout` ("NCHW" (B,C,H,W) / "NHWC" (B,H,W,C))."""
+    x, xf = _storage(x)
+    dy, df = _storage(dy)
+    if layout == "NCHW":
+        B, _, H, W = x.shape
+        xs = [x.strides[i] // x.itemsize for i in (0, 1, 2, 3)]
+        dys = [dy.strides[i] // dy.itemsize for i in (0, 1, 2, 3)]
+    else:
+        B, H, W, _ = x.shape
+        xs = [x.strides[i] // x.itemsize for i in (0, 3, 1, 2)]
+        dys = [dy.strides[i] // dy.itemsize for i in (0, 3, 1, 2)]
+    pts = np.ascontiguousarray(pts, dtype=np.int32).reshape(-1, 3)
+    out = np.empty(len(pts), dtype=np.float64)
+    xs = np.array(xs, dtype=np.int64)
+    dys = np.array(dys, dtype=np.int64)
+    st = lib().oracle_conv2d_bwd_weight_at(B, H, W, n, s, pi, _ptr(x), xf, _ptr(xs), _ptr(dy), df, _ptr(dys),
+                                           len(pts), _ptr(pts), _ptr(out))
+    assert st == 0
+    return out

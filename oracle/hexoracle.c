@@ -400,3 +400,45 @@ int oracle_max_threads(void) {
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------ */
+/* Point evaluation of the weight gradient (same definition as          */
+/* oracle_conv2d_bwd, evaluated only at listed (co, ci, t)) for full-   */
+/* size checks where the dense fp64 oracle would not fit in memory.     */
+/* x / dy are given in their storage format (fmt 0 = float32, 1 = bf16  */
+/* bit patterns; both convert exactly to double) with element strides   */
+/* (b, c, h, w).  pts = npts triples (co, ci, t); out[npts].             */
+/* ------------------------------------------------------------------ */
+static double load_any(const void* p, int fmt, int64_t i) {
+    if (fmt == 0) return (double)((const float*)p)[i];
+    uint32_t u = (uint32_t)((const uint16_t*)p)[i] << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+int oracle_conv2d_bwd_weight_at(int B, int H, int W, int n, int s, int pi,
+                                const void* x, int x_fmt, const int64_t* xs,
+                                const void* dy, int dy_fmt, const int64_t* dys,
+                                int npts, const int32_t* pts, double* out) {
+    int Ho, Wo, T;
+    int32_t* map = build_map(H, W, n, s, pi, &Ho, &Wo, &T);
+    if (!map) return 1;
+    #pragma omp parallel for schedule(dynamic)
+    for (int k = 0; k < npts; ++k) {
+        const int co = pts[3 * k], ci = pts[3 * k + 1], t = pts[3 * k + 2];
+        double acc = 0.0;
+        for (int b = 0; b < B; ++b)
+            for (int R = 0; R < Ho; ++R)
+                for (int C = 0; C < Wo; ++C) {
+                    int32_t m = map[((int64_t)R * Wo + C) * T + t];
+                    if (m < 0) continue;
+                    const int r = m / W, c = m % W;
+                    double g = load_any(dy, dy_fmt, b * dys[0] + co * dys[1] + R * dys[2] + C * dys[3]);
+                    acc += g * load_any(x, x_fmt, b * xs[0] + ci * xs[1] + r * xs[2] + c * xs[3]);
+                }
+        out[k] = acc;
+    }
+    free(map);
+    return 0;
+}

@@ -43,6 +43,8 @@ def case(F, oracle, B, Cin, Cout, H, W, n, pi, seed, relu=False, bias=True):
     b = synth.round_f32(synth.normal((Cout,), seed + 2)) if bias else None
     g = synth.round_bf16(synth.normal((B, Cout, H, W), seed + 3))
     for pass_id in (0, 1, 2):
+        if pass_id == 2 and Cout % 128:
+            continue  # the tcgen05 weight-gradient kernel tiles Cout by 128 (stencil path otherwise)
         assert F.conv_algo(B, Cin, Cout, H, W, n, 1, pi, torch.bfloat16, "NHWC", pass_id) == "tcgen05"
     xd, gd = nhwc(x), nhwc(g)
     wd = torch.from_numpy(w.astype(np.float32)).to(torch.bfloat16).cuda()

@@ -634,3 +634,24 @@ def test_errors(oracle):
         oracle.conv2d_fwd(np.zeros((1, 2, 4, 4)), np.zeros((1, 3, 7)), n=1)  # channel mismatch
     with pytest.raises(ValueError):
         oracle.pool2d_fwd(np.zeros((1, 1, 4, 4)), n=0)
+
+
+def test_wgrad_point_evaluation_matches_dense(oracle):
+    # the point-evaluation entry used for full-size checks equals the dense adjoint
+    for layout in ("NCHW", "NHWC"):
+        for n, s, pi in [(1, 1, 0), (2, 2, 1), (3, 1, 1)]:
+            x = rand((2, 3, 9, 10), 130).astype(np.float32)
+            w = rand((4, 3, oracle.num_taps(n)), 131)
+            Ho, Wo, _ = oracle.out_shape(9, 10, s, pi)
+            g = rand((2, 4, Ho, Wo), 132).astype(np.float32)
+            _, dw, _ = oracle.conv2d_bwd(x, w, g, n=n, s=s, pi=pi)
+            pts = [(co, ci, t) for co in range(4) for ci in range(3) for t in range(oracle.num_taps(n))]
+            xx, gg = (x, g) if layout == "NCHW" else (x.transpose(0, 2, 3, 1).copy(), g.transpose(0, 2, 3, 1).copy())
+            got = oracle.conv2d_bwd_weight_at(xx, gg, pts, n=n, s=s, pi=pi, layout=layout)
+            np.testing.assert_allclose(got, [dw[p] for p in pts], atol=1e-10)
+            # bf16 storage: the bit patterns of bf16-representable values convert exactly
+            xb = (xx.view(np.uint32) >> 16).astype(np.uint16)
+            x_trunc = (xb.astype(np.uint32) << 16).view(np.float32)
+            got_b = oracle.conv2d_bwd_weight_at(xb, gg, pts, n=n, s=s, pi=pi, layout=layout)
+            ref_b = oracle.conv2d_bwd_weight_at(x_trunc, gg, pts, n=n, s=s, pi=pi, layout=layout)
+            np.testing.assert_allclose(got_b, ref_b, atol=1e-12)
