@@ -54,6 +54,9 @@ bool use_tc_fwd(const hex_conv2d_desc_t* d, const Geom& g) {
 bool use_tc_bwd_data(const hex_conv2d_desc_t* d, const Geom& g) {
     return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_conv_supported(g, d->out_channels, d->in_channels);
 }
+bool use_smallc(const hex_conv2d_desc_t* d, const Geom& g) {
+    return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && smallc_supported(g, d->in_channels, d->out_channels);
+}
 bool use_tc_wgrad(const hex_conv2d_desc_t* d, const Geom& g) {
     return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_wgrad_supported(g, d->in_channels, d->out_channels);
 }
@@ -143,7 +146,8 @@ hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* d, int32_t pass,
         case 0: *bytes = use_tc_fwd(d, g) ? packed_weight_bytes(d, g) : 0; return HEX_OK;
         case 1: *bytes = use_tc_bwd_data(d, g) ? packed_weight_bytes(d, g) : 0; return HEX_OK;
         case 2:
-            *bytes = use_tc_wgrad(d, g) ? tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
+            *bytes = use_tc_wgrad(d, g)  ? tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
+                     : use_smallc(d, g) ? smallc_wgrad_ws_bytes(g, d->out_channels)
                                         : direct_wgrad_ws_bytes(g, d->in_channels, d->out_channels);
             return HEX_OK;
         default: return HEX_ERR_INVALID_ARG;
@@ -181,6 +185,10 @@ hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* d, const void* x, const voi
         a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
         a.x = x; a.wpack = wp; a.bias = bias; a.y = y; a.relu_y = nullptr; a.relu = fuse_relu;
         return tc_conv_fwd(a, s);
+    }
+    if (use_smallc(d, g)) {
+        if (((uintptr_t)y & 3) != 0) return HEX_ERR_ALIGNMENT;
+        return smallc_fwd(x, w, bias, y, g, d->out_channels, fuse_relu, s);
     }
     DirectConvArgs a = make_direct(d, g);
     a.x = x; a.w = w; a.bias = bias; a.y = y; a.relu = fuse_relu;
@@ -229,6 +237,12 @@ hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* d, const void* x, co
         a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
         a.x = x; a.dy = dy; a.dw = dw; a.dbias = dbias; a.accumulate = accumulate;
         return tc_conv_wgrad(a, ws, ws_bytes, s);
+    }
+    if (use_smallc(d, g)) {
+        const size_t need = smallc_wgrad_ws_bytes(g, d->out_channels);
+        if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
+        if (((uintptr_t)dy & 3) != 0) return HEX_ERR_ALIGNMENT;
+        return smallc_wgrad(x, dy, dw, dbias, accumulate, g, d->out_channels, ws, s);
     }
     const size_t need = direct_wgrad_ws_bytes(g, d->in_channels, d->out_channels);
     if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;

@@ -71,4 +71,12 @@ bool tc_wgrad_supported(const Geom& g, int Cin, int Cout);
 size_t tc_wgrad_ws_bytes(const Geom& g, int Cin, int Cout);
 hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
 
+// single-input-channel bf16 NHWC stencil (config 5 layer 1)
+bool smallc_supported(const Geom& g, int Cin, int Cout);
+size_t smallc_wgrad_ws_bytes(const Geom& g, int Cout);
+hex_status_t smallc_fwd(const void* x, const void* w, const float* bias, void* y, const Geom& g, int Cout, int relu,
+                        cudaStream_t st);
+hex_status_t smallc_wgrad(const void* x, const void* dy, float* dw, float* dbias, int accumulate, const Geom& g,
+                          int Cout, void* ws, cudaStream_t st);
+
 }  // namespace hexconv

@@ -245,12 +245,177 @@ __global__ void pool_bwd_nhwc_bf16x8_kernel(const uint4* __restrict__ dy, const 
     dx[(((int64_t)b * g.H + r) * g.W + c) * C8 + ch8] = out;
 }
 
+// ---------------------------------------------------------------------------
+// Specialised NHWC bf16 x8 kernels: compile-time kernel size N and stride S,
+// batch on blockIdx.y, 32-bit index math (no 64-bit division on the hot path).
+// ---------------------------------------------------------------------------
+template <int N, int S>
+__global__ void __launch_bounds__(256)
+pool_fwd_nhwc_x8_spec(const uint4* __restrict__ x, uint4* __restrict__ y, uint64_t* __restrict__ am, Geom g, int C8,
+                      int mode) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int per_img = g.Ho * g.Wo * C8;
+    if (idx >= per_img) return;
+    const int b = blockIdx.y;
+    const int ch8 = idx % C8;
+    const int o = idx / C8;
+    const int R = o / g.Wo, C = o - R * g.Wo;
+    const int c = S * C;
+    const int r = ((S * C + g.parity) >> 1) % S + S * R;
+    const int p = (c + g.parity) & 1;
+    const uint4* xp = x + (size_t)b * g.H * g.W * C8 + ch8;
+    float bv[8], sum[8];
+    int best[8];
+    uint32_t braw[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { bv[j] = -INFINITY; sum[j] = 0.f; best[j] = -1; }
+    int t = 0, cnt = 0;
+#pragma unroll
+    for (int dc = -N; dc <= N; ++dc) {
+        const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
+        const int cc = c + dc;
+        const bool colok = cc >= 0 && cc < g.W;
+        const int top = r - N + (((dc < 0 ? -dc : dc) + p) >> 1);
+#pragma unroll
+        for (int k = 0; k < len; ++k, ++t) {
+            const int rr = top + k;
+            if (!colok || rr < 0 || rr >= g.H) continue;
+            const uint4 v4 = __ldg(xp + (rr * g.W + cc) * C8);
+            const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+            ++cnt;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t bits = (j & 1) ? (w[j >> 1] & 0xffff0000u) : (w[j >> 1] << 16);
+                const float f = __uint_as_float(bits);
+                if (mode == HEX_POOL_MAX) {
+                    if (best[j] < 0 || f > bv[j]) {
+                        best[j] = t;
+                        bv[j] = f;
+                        const uint32_t h = (j & 1) ? (w[j >> 1] & 0xffff0000u) : (w[j >> 1] & 0xffffu);
+                        braw[j >> 1] = (j & 1) ? ((braw[j >> 1] & 0xffffu) | h) : ((braw[j >> 1] & 0xffff0000u) | h);
+                    }
+                } else {
+                    sum[j] += f;
+                }
+            }
+        }
+    }
+    const size_t yo = ((size_t)b * g.Ho * g.Wo + o) * C8 + ch8;
+    if (mode == HEX_POOL_MAX) {
+        uint64_t a = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a |= (uint64_t)(uint8_t)best[j] << (8 * j);
+        y[yo] = make_uint4(braw[0], braw[1], braw[2], braw[3]);
+        if (am) am[yo] = a;
+    } else {
+        uint4 out;
+        __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&out);
+        const float inv = 1.f / (float)cnt;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ob[j] = __float2bfloat16_rn(sum[j] * inv);
+        y[yo] = out;
+    }
+}
+
+template <int N, int S>
+__global__ void __launch_bounds__(256)
+pool_bwd_nhwc_x8_spec(const uint4* __restrict__ dy, const uint64_t* __restrict__ am, uint4* __restrict__ dx, Geom g,
+                      int C8, int mode) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int per_img = g.H * g.W * C8;
+    if (idx >= per_img) return;
+    const int b = blockIdx.y;
+    const int ch8 = idx % C8;
+    const int q = idx / C8;
+    const int r = q / g.W, c = q - r * g.W;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    const size_t ybase = (size_t)b * g.Ho * g.Wo * C8 + ch8;
+    int t = 0;
+#pragma unroll
+    for (int dc = -N; dc <= N; ++dc) {
+        const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
+        const int oc = c - dc;
+        const bool colok = oc >= 0 && (oc % S) == 0 && oc / S < g.Wo;
+        const int Cq = oc / S;
+        const int po = (oc + g.parity) & 1;
+        const int rho = ((S * Cq + g.parity) >> 1) % S;
+        const int top = -N + (((dc < 0 ? -dc : dc) + po) >> 1);
+#pragma unroll
+        for (int k = 0; k < len; ++k, ++t) {
+            if (!colok) continue;
+            const int d = r - (top + k) - rho;
+            if (d < 0 || (d % S) != 0) continue;
+            const int Rq = d / S;
+            if (Rq >= g.Ho) continue;
+            const size_t yo = ybase + (size_t)(Rq * g.Wo + Cq) * C8;
+            const uint4 v4 = __ldg(dy + yo);
+            const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+            if (mode == HEX_POOL_MAX) {
+                const uint64_t a = __ldg(am + yo);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t bits = (j & 1) ? (w[j >> 1] & 0xffff0000u) : (w[j >> 1] << 16);
+                    if ((int)((a >> (8 * j)) & 0xff) == t) acc[j] += __uint_as_float(bits);
+                }
+            } else {
+                // in-grid count of the centre (oc, rho + S*Rq)
+                const int orow = rho + S * Rq;
+                int cnt = 0;
+#pragma unroll
+                for (int e = -N; e <= N; ++e) {
+                    const int ccol = oc + e;
+                    if (ccol < 0 || ccol >= g.W) continue;
+                    const int l2 = 2 * N + 1 - (e < 0 ? -e : e);
+                    const int tp = orow - N + (((e < 0 ? -e : e) + po) >> 1);
+                    cnt += max(min(tp + l2, g.H) - max(tp, 0), 0);
+                }
+                const float inv = 1.f / (float)cnt;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t bits = (j & 1) ? (w[j >> 1] & 0xffff0000u) : (w[j >> 1] << 16);
+                    acc[j] += __uint_as_float(bits) * inv;
+                }
+            }
+        }
+    }
+    uint4 out;
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&out);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16_rn(acc[j]);
+    dx[(size_t)b * per_img + idx] = out;
+}
+
 static bool use_vec8(const PoolArgs& a) {
     return a.dtype == HEX_BF16 && a.layout == HEX_NHWC && (a.C % 8) == 0;
 }
 
+static bool use_spec(const PoolArgs& a) {
+    return use_vec8(a) && (a.g.n == 1 || a.g.n == 2) && (a.g.s == 1 || a.g.s == 2) && a.g.B <= 65535 &&
+           (int64_t)a.g.H * a.g.W * (a.C / 8) < (1ll << 31);
+}
+
+template <int N, int S>
+static void launch_spec_fwd(const PoolArgs& a, cudaStream_t st) {
+    const int C8 = a.C / 8;
+    dim3 grid(ceil_div((int64_t)a.g.Ho * a.g.Wo * C8, 256), a.g.B);
+    pool_fwd_nhwc_x8_spec<N, S><<<grid, 256, 0, st>>>((const uint4*)a.x, (uint4*)a.y, (uint64_t*)a.argmax, a.g, C8,
+                                                      a.mode);
+}
+template <int N, int S>
+static void launch_spec_bwd(const PoolArgs& a, cudaStream_t st) {
+    const int C8 = a.C / 8;
+    dim3 grid(ceil_div((int64_t)a.g.H * a.g.W * C8, 256), a.g.B);
+    pool_bwd_nhwc_x8_spec<N, S><<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint64_t*)a.argmax_in, (uint4*)a.dx,
+                                                      a.g, C8, a.mode);
+}
+
 hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
-    if (use_vec8(a)) {
+    if (use_spec(a)) {
+        if (a.g.n == 1) { if (a.g.s == 1) launch_spec_fwd<1, 1>(a, st); else launch_spec_fwd<1, 2>(a, st); }
+        else { if (a.g.s == 1) launch_spec_fwd<2, 1>(a, st); else launch_spec_fwd<2, 2>(a, st); }
+    } else if (use_vec8(a)) {
         const int C8 = a.C / 8;
         const int64_t total = (int64_t)a.g.B * C8 * a.g.Ho * a.g.Wo;
         pool_fwd_nhwc_bf16x8_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
@@ -270,7 +435,10 @@ hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
 }
 
 hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
-    if (use_vec8(a)) {
+    if (use_spec(a)) {
+        if (a.g.n == 1) { if (a.g.s == 1) launch_spec_bwd<1, 1>(a, st); else launch_spec_bwd<1, 2>(a, st); }
+        else { if (a.g.s == 1) launch_spec_bwd<2, 1>(a, st); else launch_spec_bwd<2, 2>(a, st); }
+    } else if (use_vec8(a)) {
         const int C8 = a.C / 8;
         const int64_t total = (int64_t)a.g.B * C8 * a.g.H * a.g.W;
         pool_bwd_nhwc_bf16x8_kernel<<<ceil_div(total, 256), 256, 0, st>>>(

@@ -1,0 +1,193 @@
+// smallc_conv.cu -- single-input-channel hexagonal convolution, bf16 NHWC
+// (BASELINE config 5 layer 1: 1 -> 64 channels, n = 2, on 96x96 camera
+// images).  With Cin = 1 the layer has no channel contraction, so it is a
+// stencil, not a GEMM: each warp owns one output pixel at a time and each lane
+// two output channels (bf16x2), the lane's weights live in registers, and the
+// T neighbour values are warp-uniform loads.  Stores / dy loads are one
+// coalesced 128-byte row per warp per pixel.
+//
+// Forward:  y[p][co] = relu?(bias[co] + sum_t w[co][t] * x[p + off_t])
+// Weight gradient: dw[co][t] = sum_p dy[p][co] * x[p + off_t],
+//                  dbias[co] = sum_p dy[p][co]
+// (off-grid neighbours contribute 0, A4).  The
+// weight gradient reduces per block in a fixed warp order and then across
+// blocks in a fixed order: deterministic.
+#include "common.cuh"
+#include "geometry.cuh"
+#include "kernels.h"
+
+namespace hexconv {
+
+constexpr int SC_WARPS = 8;
+constexpr int SC_WG_BLOCKS = 592;  // 4 x 148 SMs
+
+template <int N>
+struct TapsOf {
+    static constexpr int T = 3 * N * (N + 1) + 1;
+};
+
+// Neighbour value of tap t for a centre (r, c) with column parity p; 0 when off-grid.
+template <int N>
+__device__ __forceinline__ void gather_taps(const __nv_bfloat16* __restrict__ xb, int H, int W, int r, int c, int p,
+                                            float* v) {
+    int t = 0;
+#pragma unroll
+    for (int dc = -N; dc <= N; ++dc) {
+        const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
+        const int cc = c + dc;
+        const bool colok = cc >= 0 && cc < W;
+        const int top = r - N + (((dc < 0 ? -dc : dc) + p) >> 1);
+#pragma unroll
+        for (int k = 0; k < len; ++k, ++t) {
+            const int rr = top + k;
+            v[t] = (colok && rr >= 0 && rr < H) ? __bfloat162float(xb[rr * W + cc]) : 0.f;
+        }
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(SC_WARPS * 32)
+smallc_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+                  const float* __restrict__ bias, __nv_bfloat16* __restrict__ y, Geom g, int Cout, int relu) {
+    constexpr int T = TapsOf<N>::T;
+    const int lane = threadIdx.x & 31;
+    const int co = blockIdx.y * 64 + 2 * lane;
+    float w0[T], w1[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        w0[t] = __bfloat162float(w[(int64_t)co * T + t]);
+        w1[t] = __bfloat162float(w[(int64_t)(co + 1) * T + t]);
+    }
+    const float b0 = bias ? bias[co] : 0.f, b1 = bias ? bias[co + 1] : 0.f;
+    const int npix_img = g.Ho * g.Wo;
+    const int64_t npix = (int64_t)g.B * npix_img;
+    const int64_t warp_g = (int64_t)blockIdx.x * SC_WARPS + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * SC_WARPS;
+    for (int64_t pix = warp_g; pix < npix; pix += nwarps) {
+        const int b = (int)(pix / npix_img);
+        const int o = (int)(pix - (int64_t)b * npix_img);
+        const int R = o / g.Wo, C = o - (o / g.Wo) * g.Wo;
+        const int c = g.s * C;
+        const int r = hex_rho(C, g.s, g.parity) + g.s * R;
+        float v[T];
+        gather_taps<N>(x + (int64_t)b * g.H * g.W, g.H, g.W, r, c, (c + g.parity) & 1, v);
+        float a0 = b0, a1 = b1;
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            a0 = fmaf(w0[t], v[t], a0);
+            a1 = fmaf(w1[t], v[t], a1);
+        }
+        if (relu) { a0 = fmaxf(a0, 0.f); a1 = fmaxf(a1, 0.f); }
+        *reinterpret_cast<__nv_bfloat162*>(y + pix * Cout + co) = __floats2bfloat162_rn(a0, a1);
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(SC_WARPS * 32)
+smallc_wgrad_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
+                    float* __restrict__ part, Geom g, int Cout) {
+    constexpr int T = TapsOf<N>::T;
+    constexpr int NA = T + 1;  // taps + bias column
+    __shared__ float red[SC_WARPS][64][NA];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int co = blockIdx.y * 64 + 2 * lane;
+    float a0[NA], a1[NA];
+#pragma unroll
+    for (int t = 0; t < NA; ++t) { a0[t] = 0.f; a1[t] = 0.f; }
+    const int npix_img = g.Ho * g.Wo;
+    const int64_t npix = (int64_t)g.B * npix_img;
+    const int64_t warp_g = (int64_t)blockIdx.x * SC_WARPS + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * SC_WARPS;
+    for (int64_t pix = warp_g; pix < npix; pix += nwarps) {
+        const int b = (int)(pix / npix_img);
+        const int o = (int)(pix - (int64_t)b * npix_img);
+        const int R = o / g.Wo, C = o - (o / g.Wo) * g.Wo;
+        const int c = g.s * C;
+        const int r = hex_rho(C, g.s, g.parity) + g.s * R;
+        const __nv_bfloat162 d2 = *reinterpret_cast<const __nv_bfloat162*>(dy + pix * Cout + co);
+        const float d0 = __low2float(d2), d1 = __high2float(d2);
+        float v[T];
+        gather_taps<N>(x + (int64_t)b * g.H * g.W, g.H, g.W, r, c, (c + g.parity) & 1, v);
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            a0[t] = fmaf(d0, v[t], a0[t]);
+            a1[t] = fmaf(d1, v[t], a1[t]);
+        }
+        a0[T] += d0;
+        a1[T] += d1;
+    }
+#pragma unroll
+    for (int t = 0; t < NA; ++t) {
+        red[warp][2 * lane][t] = a0[t];
+        red[warp][2 * lane + 1][t] = a1[t];
+    }
+    __syncthreads();
+    // fixed-order reduction over the block's warps; part[block][co][t]
+    for (int i = threadIdx.x; i < 64 * NA; i += blockDim.x) {
+        const int cl = i / NA, t = i % NA;
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < SC_WARPS; ++k) s += red[k][cl][t];
+        part[((int64_t)blockIdx.x * Cout + blockIdx.y * 64 + cl) * NA + t] = s;
+    }
+}
+
+__global__ void smallc_wgrad_reduce_kernel(const float* __restrict__ part, int nblocks, int Cout, int NA,
+                                           float* __restrict__ dw, float* __restrict__ dbias, int accumulate) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Cout * NA) return;
+    float s = 0.f;
+    for (int k = 0; k < nblocks; ++k) s += part[(int64_t)k * Cout * NA + i];
+    const int co = i / NA, t = i % NA;
+    if (t == NA - 1) {
+        if (dbias) dbias[co] = accumulate ? dbias[co] + s : s;
+    } else {
+        float* d = dw + (int64_t)co * (NA - 1) + t;
+        *d = accumulate ? *d + s : s;
+    }
+}
+
+bool smallc_supported(const Geom& g, int Cin, int Cout) {
+    return Cin == 1 && Cout % 64 == 0 && g.n >= 1 && g.n <= 2;
+}
+
+size_t smallc_wgrad_ws_bytes(const Geom& g, int Cout) {
+    return (size_t)SC_WG_BLOCKS * Cout * (g.T + 1) * sizeof(float);
+}
+
+hex_status_t smallc_fwd(const void* x, const void* w, const float* bias, void* y, const Geom& g, int Cout, int relu,
+                        cudaStream_t st) {
+    const int64_t npix = (int64_t)g.B * g.Ho * g.Wo;
+    int blocks = (int)((npix + SC_WARPS * 8 - 1) / (SC_WARPS * 8));  // ~8 pixels per warp
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    dim3 grid(blocks, Cout / 64);
+    const auto* xb = (const __nv_bfloat16*)x;
+    const auto* wb = (const __nv_bfloat16*)w;
+    auto* yb = (__nv_bfloat16*)y;
+    switch (g.n) {
+        case 1: smallc_fwd_kernel<1><<<grid, SC_WARPS * 32, 0, st>>>(xb, wb, bias, yb, g, Cout, relu); break;
+        default: smallc_fwd_kernel<2><<<grid, SC_WARPS * 32, 0, st>>>(xb, wb, bias, yb, g, Cout, relu); break;
+    }
+    count_launch();
+    return last_launch_status();
+}
+
+hex_status_t smallc_wgrad(const void* x, const void* dy, float* dw, float* dbias, int accumulate, const Geom& g,
+                          int Cout, void* ws, cudaStream_t st) {
+    dim3 grid(SC_WG_BLOCKS, Cout / 64);
+    const auto* xb = (const __nv_bfloat16*)x;
+    const auto* db = (const __nv_bfloat16*)dy;
+    float* part = (float*)ws;
+    switch (g.n) {
+        case 1: smallc_wgrad_kernel<1><<<grid, SC_WARPS * 32, 0, st>>>(xb, db, part, g, Cout); break;
+        default: smallc_wgrad_kernel<2><<<grid, SC_WARPS * 32, 0, st>>>(xb, db, part, g, Cout); break;
+    }
+    count_launch();
+    const int NA = g.T + 1;
+    smallc_wgrad_reduce_kernel<<<ceil_div(Cout * NA, 256), 256, 0, st>>>(part, SC_WG_BLOCKS, Cout, NA, dw, dbias,
+                                                                         accumulate);
+    count_launch();
+    return last_launch_status();
+}
+
+}  // namespace hexconv

@@ -242,3 +242,10 @@ def test_config2_full(F, oracle):
     assert rel(to_np(dx), dxr) <= TOL_F32
     assert rel(dw.cpu().numpy(), dwr) <= TOL_F32
     assert rel(db.cpu().numpy(), dbr) <= TOL_F32
+
+
+def test_single_input_channel_bf16_nhwc(F, oracle):
+    # the Cin = 1 stencil kernels (config 5 layer 1): both n, both parities, strides 1 and 2, ragged grids
+    for pi, n, s, (H, W), Cout in [(0, 2, 1, (13, 11), 64), (1, 1, 1, (9, 12), 128), (0, 2, 2, (12, 13), 64),
+                                   (1, 2, 2, (11, 10), 64)]:
+        _conv_case(F, oracle, pi, n, s, H, W, 3, 1, Cout, torch.bfloat16, "NHWC", 40 + n)
