@@ -45,40 +45,72 @@ __device__ __forceinline__ void gather_taps(const __nv_bfloat16* __restrict__ xb
     }
 }
 
+// Each warp walks its pixels in batches of 32: lane j computes pixel j's centre
+// and gathers its T neighbour values once into shared memory; then the warp
+// sweeps the 32 pixels with lanes owning output-channel pairs (uniform LDS of
+// the gathered values, one coalesced 128-byte dy load / y store per pixel).
+template <int N>
+__device__ __forceinline__ void stage_batch(const __nv_bfloat16* __restrict__ x, const Geom& g, int64_t pix0,
+                                            int64_t npix, float* sv) {
+    constexpr int T = TapsOf<N>::T;
+    const int lane = threadIdx.x & 31;
+    const int64_t pix = pix0 + lane;
+    float v[T + 1];
+    if (pix < npix) {
+        const int npix_img = g.Ho * g.Wo;
+        const int b = (int)(pix / npix_img);
+        const int o = (int)(pix - (int64_t)b * npix_img);
+        const int R = o / g.Wo, C = o - R * g.Wo;
+        const int c = g.s * C;
+        const int r = hex_rho(C, g.s, g.parity) + g.s * R;
+        gather_taps<N>(x + (int64_t)b * g.H * g.W, g.H, g.W, r, c, (c + g.parity) & 1, v);
+        v[T] = 1.f;
+    } else {
+#pragma unroll
+        for (int t = 0; t <= T; ++t) v[t] = 0.f;
+    }
+#pragma unroll
+    for (int t = 0; t <= T; ++t) sv[lane * (T + 1) + t] = v[t];
+    __syncwarp();
+}
+
 template <int N>
 __global__ void __launch_bounds__(SC_WARPS * 32)
 smallc_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
                   const float* __restrict__ bias, __nv_bfloat16* __restrict__ y, Geom g, int Cout, int relu) {
     constexpr int T = TapsOf<N>::T;
-    const int lane = threadIdx.x & 31;
+    constexpr int NA = T + 1;
+    __shared__ float sv_all[SC_WARPS][32 * NA];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float* sv = sv_all[warp];
     const int co = blockIdx.y * 64 + 2 * lane;
-    float w0[T], w1[T];
+    float w0[NA], w1[NA];
 #pragma unroll
     for (int t = 0; t < T; ++t) {
         w0[t] = __bfloat162float(w[(int64_t)co * T + t]);
         w1[t] = __bfloat162float(w[(int64_t)(co + 1) * T + t]);
     }
-    const float b0 = bias ? bias[co] : 0.f, b1 = bias ? bias[co + 1] : 0.f;
-    const int npix_img = g.Ho * g.Wo;
-    const int64_t npix = (int64_t)g.B * npix_img;
-    const int64_t warp_g = (int64_t)blockIdx.x * SC_WARPS + (threadIdx.x >> 5);
-    const int64_t nwarps = (int64_t)gridDim.x * SC_WARPS;
-    for (int64_t pix = warp_g; pix < npix; pix += nwarps) {
-        const int b = (int)(pix / npix_img);
-        const int o = (int)(pix - (int64_t)b * npix_img);
-        const int R = o / g.Wo, C = o - (o / g.Wo) * g.Wo;
-        const int c = g.s * C;
-        const int r = hex_rho(C, g.s, g.parity) + g.s * R;
-        float v[T];
-        gather_taps<N>(x + (int64_t)b * g.H * g.W, g.H, g.W, r, c, (c + g.parity) & 1, v);
-        float a0 = b0, a1 = b1;
+    w0[T] = bias ? bias[co] : 0.f;   // the ones column carries the bias
+    w1[T] = bias ? bias[co + 1] : 0.f;
+    const int64_t npix = (int64_t)g.B * g.Ho * g.Wo;
+    const int64_t nbatch = (npix + 31) / 32;
+    for (int64_t bt = (int64_t)blockIdx.x * SC_WARPS + warp; bt < nbatch; bt += (int64_t)gridDim.x * SC_WARPS) {
+        const int64_t pix0 = bt * 32;
+        stage_batch<N>(x, g, pix0, npix, sv);
+        const int cnt = (int)min((int64_t)32, npix - pix0);
+        for (int j = 0; j < cnt; ++j) {
+            const float* vj = sv + j * NA;
+            float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-            a0 = fmaf(w0[t], v[t], a0);
-            a1 = fmaf(w1[t], v[t], a1);
+            for (int t = 0; t < NA; ++t) {
+                const float vt = vj[t];
+                a0 = fmaf(w0[t], vt, a0);
+                a1 = fmaf(w1[t], vt, a1);
+            }
+            if (relu) { a0 = fmaxf(a0, 0.f); a1 = fmaxf(a1, 0.f); }
+            *reinterpret_cast<__nv_bfloat162*>(y + (pix0 + j) * Cout + co) = __floats2bfloat162_rn(a0, a1);
         }
-        if (relu) { a0 = fmaxf(a0, 0.f); a1 = fmaxf(a1, 0.f); }
-        *reinterpret_cast<__nv_bfloat162*>(y + pix * Cout + co) = __floats2bfloat162_rn(a0, a1);
+        __syncwarp();
     }
 }
 
@@ -87,47 +119,58 @@ __global__ void __launch_bounds__(SC_WARPS * 32)
 smallc_wgrad_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
                     float* __restrict__ part, Geom g, int Cout) {
     constexpr int T = TapsOf<N>::T;
-    constexpr int NA = T + 1;  // taps + bias column
-    __shared__ float red[SC_WARPS][64][NA];
+    constexpr int NA = T + 1;  // taps + bias column (ones)
+    __shared__ float sv_all[SC_WARPS][32 * NA];
+    __shared__ float red[SC_WARPS / 2][NA][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float* sv = sv_all[warp];
     const int co = blockIdx.y * 64 + 2 * lane;
     float a0[NA], a1[NA];
 #pragma unroll
     for (int t = 0; t < NA; ++t) { a0[t] = 0.f; a1[t] = 0.f; }
-    const int npix_img = g.Ho * g.Wo;
-    const int64_t npix = (int64_t)g.B * npix_img;
-    const int64_t warp_g = (int64_t)blockIdx.x * SC_WARPS + warp;
-    const int64_t nwarps = (int64_t)gridDim.x * SC_WARPS;
-    for (int64_t pix = warp_g; pix < npix; pix += nwarps) {
-        const int b = (int)(pix / npix_img);
-        const int o = (int)(pix - (int64_t)b * npix_img);
-        const int R = o / g.Wo, C = o - (o / g.Wo) * g.Wo;
-        const int c = g.s * C;
-        const int r = hex_rho(C, g.s, g.parity) + g.s * R;
-        const __nv_bfloat162 d2 = *reinterpret_cast<const __nv_bfloat162*>(dy + pix * Cout + co);
-        const float d0 = __low2float(d2), d1 = __high2float(d2);
-        float v[T];
-        gather_taps<N>(x + (int64_t)b * g.H * g.W, g.H, g.W, r, c, (c + g.parity) & 1, v);
+    const int64_t npix = (int64_t)g.B * g.Ho * g.Wo;
+    const int64_t nbatch = (npix + 31) / 32;
+    for (int64_t bt = (int64_t)blockIdx.x * SC_WARPS + warp; bt < nbatch; bt += (int64_t)gridDim.x * SC_WARPS) {
+        const int64_t pix0 = bt * 32;
+        stage_batch<N>(x, g, pix0, npix, sv);
+        const int cnt = (int)min((int64_t)32, npix - pix0);
+        for (int j = 0; j < cnt; ++j) {
+            const __nv_bfloat162 d2 = *reinterpret_cast<const __nv_bfloat162*>(dy + (pix0 + j) * Cout + co);
+            const float d0 = __low2float(d2), d1 = __high2float(d2);
+            const float* vj = sv + j * NA;
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-            a0[t] = fmaf(d0, v[t], a0[t]);
-            a1[t] = fmaf(d1, v[t], a1[t]);
+            for (int t = 0; t < NA; ++t) {
+                const float vt = vj[t];
+                a0[t] = fmaf(d0, vt, a0[t]);
+                a1[t] = fmaf(d1, vt, a1[t]);
+            }
         }
-        a0[T] += d0;
-        a1[T] += d1;
+        __syncwarp();
     }
+    // fixed-order reduction over the block's warps: red[k] = acc(warp k+4) + acc(warp k), then sum k
+    constexpr int HW_ = SC_WARPS / 2;
+    if (warp >= HW_) {
 #pragma unroll
-    for (int t = 0; t < NA; ++t) {
-        red[warp][2 * lane][t] = a0[t];
-        red[warp][2 * lane + 1][t] = a1[t];
+        for (int t = 0; t < NA; ++t) {
+            red[warp - HW_][t][2 * lane] = a0[t];
+            red[warp - HW_][t][2 * lane + 1] = a1[t];
+        }
     }
     __syncthreads();
-    // fixed-order reduction over the block's warps; part[block][co][t]
+    if (warp < HW_) {
+#pragma unroll
+        for (int t = 0; t < NA; ++t) {
+            red[warp][t][2 * lane] += a0[t];
+            red[warp][t][2 * lane + 1] += a1[t];
+        }
+    }
+    __syncthreads();
+    // part[block][co][t]
     for (int i = threadIdx.x; i < 64 * NA; i += blockDim.x) {
         const int cl = i / NA, t = i % NA;
         float s = 0.f;
 #pragma unroll
-        for (int k = 0; k < SC_WARPS; ++k) s += red[k][cl][t];
+        for (int k = 0; k < HW_; ++k) s += red[k][t][cl];
         part[((int64_t)blockIdx.x * Cout + blockIdx.y * 64 + cl) * NA + t] = s;
     }
 }
@@ -158,8 +201,9 @@ size_t smallc_wgrad_ws_bytes(const Geom& g, int Cout) {
 hex_status_t smallc_fwd(const void* x, const void* w, const float* bias, void* y, const Geom& g, int Cout, int relu,
                         cudaStream_t st) {
     const int64_t npix = (int64_t)g.B * g.Ho * g.Wo;
-    int blocks = (int)((npix + SC_WARPS * 8 - 1) / (SC_WARPS * 8));  // ~8 pixels per warp
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    int blocks = (int)((npix + SC_WARPS * 32 * 4 - 1) / (SC_WARPS * 32 * 4));  // ~4 pixel batches per warp
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
     dim3 grid(blocks, Cout / 64);
     const auto* xb = (const __nv_bfloat16*)x;
     const auto* wb = (const __nv_bfloat16*)w;

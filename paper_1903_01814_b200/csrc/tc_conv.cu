@@ -406,21 +406,27 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ weight-gradient kernel
-// Unit = (co tile of 128, ci tile of N, tap group of TG taps, pixel chunk).
-// Per pixel tile (64 pixels of one parity view, RB x JB x BB):
-//   A = dy box   [64 px rows][64 co] x 2      (MN-major, co contiguous)
-//   B = x_t box  [64 px rows][64 ci] x N/64   (MN-major, ci contiguous), one per tap
-//   D_t[co][ci] += A^T-contract-B over the 64 pixels, D_t in TMEM columns t*N.
+// dW[t][co][ci] = sum_pixels dy[px][co] * x[px + off_t][ci]  (pixels are K).
+// The (tap, 64-input-channel chunk) pairs are "atoms"; one unit of work is
+// (Cout tile of 128, a group of up to 8 atoms = 512 TMEM columns, a chunk of
+// pixel tiles).  Per pixel tile (64 pixels of one parity view, RB x JB x BB):
+//   A   = dy box  [64 px rows][64 co] x 2          (MN-major: co contiguous)
+//   B_a = x box of atom a, shifted by tap t        (MN-major: ci contiguous)
+// Up to four atom boxes sit one LBO (8 KB) apart and form one N = 256 MMA, so
+// a full group is two 128x256x16 MMAs per 16 pixels; atom a accumulates in
+// TMEM columns [64a, 64a+64).  Partial sums per pixel chunk go to a workspace
+// and are reduced in a fixed order (deterministic).
 constexpr int WG_PIX = 64;
 constexpr int WG_STAGES = 2;
-constexpr int WG_BOX_BYTES = WG_PIX * 128;  // one 64-channel box: 8 KB
-constexpr int WG_STAGE_BYTES = 10 * WG_BOX_BYTES;  // 2 dy boxes + up to 8 x boxes (512 TMEM columns)
+constexpr int WG_BOX_BYTES = WG_PIX * 128;         // one 64-channel box: 8 KB
+constexpr int WG_ATOMS = 8;                        // atoms per unit (512 TMEM columns)
+constexpr int WG_STAGE_BYTES = (2 + WG_ATOMS) * WG_BOX_BYTES;
 
 struct TcWgParams {
     int B, H, W, Cin, Cout, T, parity;
     int RB, JB, BB;
     int rt, bt, jt0, jt1, tiles0, ptiles;  // pixel tiles
-    int N, TG, groups, co_tiles, ci_tiles, chunks, tiles_per_chunk;
+    int kchunks, n_atoms, groups, co_tiles, chunks, tiles_per_chunk;
     float* part;  // [chunks][T][Cout][Cin]
     int8_t tap_dc[2][TC_MAXT];
     int8_t tap_dr[2][TC_MAXT];
@@ -453,15 +459,13 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
     // unit decode
     int u = blockIdx.x;
     const int chunk = u % p.chunks; u /= p.chunks;
-    const int grp = u % p.groups; u /= p.groups;
-    const int cit = u % p.ci_tiles;
-    const int cot = u / p.ci_tiles;
-    const int t0 = grp * p.TG;
-    const int ntaps = min(p.TG, p.T - t0);
-    const int co0 = cot * 128, ci0 = cit * p.N;
+    const int grp = u % p.groups;
+    const int cot = u / p.groups;
+    const int a0 = grp * WG_ATOMS;
+    const int na = min(WG_ATOMS, p.n_atoms - a0);
+    const int co0 = cot * 128;
     const int pt_begin = chunk * p.tiles_per_chunk;
     const int pt_end = min(p.ptiles, pt_begin + p.tiles_per_chunk);
-    const int nbx = p.N / 64;  // x boxes per tap
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
@@ -474,7 +478,7 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t stage_bytes = (2 + ntaps * nbx) * WG_BOX_BYTES;
+    const uint32_t stage_bytes = (2 + na) * WG_BOX_BYTES;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -490,37 +494,40 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
                 const CUtensorMap* mdy = P ? &map_dy1 : &map_dy0;
                 ptx::tma_load_4d(mdy, &full[stage], s, co0, r0, j0, b0);
                 ptx::tma_load_4d(mdy, &full[stage], s + WG_BOX_BYTES, co0 + 64, r0, j0, b0);
-                for (int tl = 0; tl < ntaps; ++tl) {
-                    const int t = t0 + tl;
+                for (int i = 0; i < na; ++i) {
+                    const int a = a0 + i;
+                    const int t = a / p.kchunks, kc = a - t * p.kchunks;
                     const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
                     const int Pv = (P + dc) & 1;
                     const int jsh = (P + dc - Pv) / 2;
-                    const CUtensorMap* mx = Pv ? &map_x1 : &map_x0;
-                    for (int i = 0; i < nbx; ++i)
-                        ptx::tma_load_4d(mx, &full[stage], s + (2 + tl * nbx + i) * WG_BOX_BYTES, ci0 + 64 * i,
-                                         r0 + dr, j0 + jsh, b0);
+                    ptx::tma_load_4d(Pv ? &map_x1 : &map_x0, &full[stage], s + (2 + i) * WG_BOX_BYTES, kc * 64,
+                                     r0 + dr, j0 + jsh, b0);
                 }
                 if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = ptx::idesc_bf16(128, p.N, 1, 1);
+            const int n0 = min(na, 4), n1 = na - n0;
+            const uint32_t idesc0 = ptx::idesc_bf16(128, 64 * n0, 1, 1);
+            const uint32_t idesc1 = ptx::idesc_bf16(128, 64 * (n1 > 0 ? n1 : 1), 1, 1);
             int stage = 0;
             uint32_t phase = 0;
             for (int pt = pt_begin; pt < pt_end; ++pt) {
                 ptx::mbar_wait(&full[stage], phase);
                 ptx::tc_fence_after();
                 const uint32_t s = ptx::smem_u32(smem + stage * WG_STAGE_BYTES);
-                for (int tl = 0; tl < ntaps; ++tl) {
-                    const uint32_t bx = s + (2 + tl * nbx) * WG_BOX_BYTES;
+                const uint32_t bx = s + 2 * WG_BOX_BYTES;
 #pragma unroll
-                    for (int k = 0; k < WG_PIX / 16; ++k) {
-                        // MN-major SW128: 8-row K groups 1024 B apart, 64-element MN blocks one box apart
-                        const uint64_t ad = ptx::smem_desc_sw128(s + k * 2048, WG_BOX_BYTES, 1024);
-                        const uint64_t bd = ptx::smem_desc_sw128(bx + k * 2048, WG_BOX_BYTES, 1024);
-                        ptx::mma_bf16(tmem_base + tl * p.N, ad, bd, idesc, (pt != pt_begin) || (k != 0));
-                    }
+                for (int k = 0; k < WG_PIX / 16; ++k) {
+                    // MN-major SW128: 8-row K groups 1024 B apart, 64-element MN blocks one box (LBO) apart
+                    const uint64_t ad = ptx::smem_desc_sw128(s + k * 2048, WG_BOX_BYTES, 1024);
+                    const uint32_t acc = (pt != pt_begin) || (k != 0);
+                    ptx::mma_bf16(tmem_base, ad, ptx::smem_desc_sw128(bx + k * 2048, WG_BOX_BYTES, 1024), idesc0, acc);
+                    if (n1 > 0)
+                        ptx::mma_bf16(tmem_base + 256, ad,
+                                      ptx::smem_desc_sw128(bx + 4 * WG_BOX_BYTES + k * 2048, WG_BOX_BYTES, 1024),
+                                      idesc1, acc);
                 }
                 ptx::mma_commit(&empty[stage]);
                 if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
@@ -533,23 +540,25 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
         ptx::mbar_wait(tfull, 0);
         ptx::tc_fence_after();
         const int co = co0 + row;
-        for (int tl = 0; tl < ntaps; ++tl) {
-            float* dst = p.part + (((int64_t)chunk * p.T + (t0 + tl)) * p.Cout + co) * p.Cin + ci0;
+        const bool empty_chunk = pt_end <= pt_begin;
+        for (int i = 0; i < na; ++i) {
+            const int a = a0 + i;
+            const int t = a / p.kchunks, kc = a - t * p.kchunks;
+            float* dst = p.part + (((int64_t)chunk * p.T + t) * p.Cout + co) * p.Cin + kc * 64;
 #pragma unroll 1
-            for (int ch = 0; ch < p.N / 32; ++ch) {
+            for (int ch = 0; ch < 2; ++ch) {
                 uint32_t v[32];
-                ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + tl * p.N + ch * 32, v);
+                ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + i * 64 + ch * 32, v);
                 ptx::tmem_ld_wait();
-                const bool empty_chunk = pt_end <= pt_begin;
                 float4* d4 = reinterpret_cast<float4*>(dst + ch * 32);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int j = 0; j < 8; ++j) {
                     float4 f;
-                    f.x = empty_chunk ? 0.f : __uint_as_float(v[4 * i]);
-                    f.y = empty_chunk ? 0.f : __uint_as_float(v[4 * i + 1]);
-                    f.z = empty_chunk ? 0.f : __uint_as_float(v[4 * i + 2]);
-                    f.w = empty_chunk ? 0.f : __uint_as_float(v[4 * i + 3]);
-                    d4[i] = f;
+                    f.x = empty_chunk ? 0.f : __uint_as_float(v[4 * j]);
+                    f.y = empty_chunk ? 0.f : __uint_as_float(v[4 * j + 1]);
+                    f.z = empty_chunk ? 0.f : __uint_as_float(v[4 * j + 2]);
+                    f.w = empty_chunk ? 0.f : __uint_as_float(v[4 * j + 3]);
+                    d4[j] = f;
                 }
             }
         }
@@ -604,7 +613,7 @@ constexpr int DB_CHUNKS = 256;
 
 struct WgPlan {
     int RB, JB, BB, rt, bt, jt0, jt1, tiles0, ptiles;
-    int N, TG, groups, co_tiles, ci_tiles, chunks, tiles_per_chunk;
+    int kchunks, n_atoms, groups, co_tiles, chunks, tiles_per_chunk;
 };
 
 static WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
@@ -616,13 +625,11 @@ static WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
     w.jt1 = ceil_div(g.W / 2, w.JB);
     w.tiles0 = w.rt * w.jt0 * w.bt;
     w.ptiles = w.tiles0 + w.rt * w.jt1 * w.bt;
-    w.N = Cin % 256 == 0 ? 256 : (Cin % 128 == 0 ? 128 : 64);
-    w.TG = 512 / w.N;
-    if (w.TG > g.T) w.TG = g.T;
-    w.groups = ceil_div(g.T, w.TG);
+    w.kchunks = Cin / 64;
+    w.n_atoms = g.T * w.kchunks;
+    w.groups = ceil_div(w.n_atoms, WG_ATOMS);
     w.co_tiles = Cout / 128;
-    w.ci_tiles = Cin / w.N;
-    const int base_units = w.co_tiles * w.ci_tiles * w.groups;
+    const int base_units = w.co_tiles * w.groups;
     int chunks = ceil_div(2 * 148, base_units);
     if (chunks > w.ptiles) chunks = w.ptiles;
     if (chunks < 1) chunks = 1;
@@ -651,7 +658,7 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
     p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
     p.RB = w.RB; p.JB = w.JB; p.BB = w.BB; p.rt = w.rt; p.bt = w.bt; p.jt0 = w.jt0; p.jt1 = w.jt1;
     p.tiles0 = w.tiles0; p.ptiles = w.ptiles;
-    p.N = w.N; p.TG = w.TG; p.groups = w.groups; p.co_tiles = w.co_tiles; p.ci_tiles = w.ci_tiles;
+    p.kchunks = w.kchunks; p.n_atoms = w.n_atoms; p.groups = w.groups; p.co_tiles = w.co_tiles;
     p.chunks = w.chunks; p.tiles_per_chunk = w.tiles_per_chunk;
     p.part = (float*)ws;
     for (int pc = 0; pc < 2; ++pc)
@@ -674,7 +681,7 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
             return HEX_ERR_CUDA;
         attr_set = true;
     }
-    const int units = w.co_tiles * w.ci_tiles * w.groups * w.chunks;
+    const int units = w.co_tiles * w.groups * w.chunks;
     tc_conv_wgrad_kernel<<<units, 192, smem, st>>>(mx0, mx1, md0, md1, p);
     count_launch();
     const int64_t total = (int64_t)g.T * a.Cout * a.Cin;
