@@ -416,9 +416,9 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
 // a full group is two 128x256x16 MMAs per 16 pixels; atom a accumulates in
 // TMEM columns [64a, 64a+64).  Partial sums per pixel chunk go to a workspace
 // and are reduced in a fixed order (deterministic).
-constexpr int WG_PIX = 64;
-constexpr int WG_STAGES = 2;
-constexpr int WG_BOX_BYTES = WG_PIX * 128;         // one 64-channel box: 8 KB
+constexpr int WG_PIX = 32;
+constexpr int WG_STAGES = 5;
+constexpr int WG_BOX_BYTES = WG_PIX * 128;         // one 64-channel box: 4 KB
 constexpr int WG_ATOMS = 8;                        // atoms per unit (512 TMEM columns)
 constexpr int WG_STAGE_BYTES = (2 + WG_ATOMS) * WG_BOX_BYTES;
 
@@ -427,7 +427,8 @@ struct TcWgParams {
     int RB, JB, BB;
     int rt, bt, jt0, jt1, tiles0, ptiles;  // pixel tiles
     int kchunks, n_atoms, groups, co_tiles, chunks, tiles_per_chunk;
-    float* part;  // [chunks][T][Cout][Cin]
+    float* part;     // [chunks][T][Cout][Cin]
+    float* db_part;  // [chunks][Cout] or NULL (no bias gradient)
     int8_t tap_dc[2][TC_MAXT];
     int8_t tap_dr[2][TC_MAXT];
 };
@@ -467,9 +468,14 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
     const int pt_begin = chunk * p.tiles_per_chunk;
     const int pt_end = min(p.ptiles, pt_begin + p.tiles_per_chunk);
 
+    // units of atom group 0 also reduce dbias from the dy tiles in shared memory
+    const bool do_db = p.db_part != nullptr && grp == 0;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < WG_STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        for (int s = 0; s < WG_STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], do_db ? 5 : 1);  // MMA commit (+ 4 epilogue warps reading dy)
+        }
         ptx::mbar_init(tfull, 1);
         ptx::fence_barrier_init();
     }
@@ -537,6 +543,28 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
     } else {
         const int q = warp & 3;
         const int row = q * 32 + lane;  // co local
+        if (do_db) {
+            // dbias[co] partial: column sums of the dy tiles (SW128 layout: 16-byte chunk j of
+            // pixel row px sits at chunk j ^ (px & 7))
+            const int box = row >> 6, e = row & 63, j = e >> 3, sub = e & 7;
+            float dsum = 0.f;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int pt = pt_begin; pt < pt_end; ++pt) {
+                ptx::mbar_wait(&full[stage], phase);
+                const uint8_t* sdy = smem + stage * WG_STAGE_BYTES + box * WG_BOX_BYTES;
+#pragma unroll 8
+                for (int px = 0; px < WG_PIX; ++px) {
+                    const __nv_bfloat16 v =
+                        *reinterpret_cast<const __nv_bfloat16*>(sdy + px * 128 + ((j ^ (px & 7)) << 4) + sub * 2);
+                    dsum += __bfloat162float(v);
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+                if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
+            }
+            p.db_part[(int64_t)chunk * p.Cout + co0 + row] = dsum;
+        }
         ptx::mbar_wait(tfull, 0);
         ptx::tc_fence_after();
         const int co = co0 + row;
@@ -588,18 +616,6 @@ __global__ void wgrad_tc_reduce_kernel(const float* __restrict__ part, int chunk
     *d = accumulate ? *d + s : s;
 }
 
-// dbias partials: part[chunk][co] = sum over the chunk's pixels of dy (NHWC bf16)
-__global__ void dbias_partial_kernel(const __nv_bfloat16* __restrict__ dy, int64_t npix, int Cout, int64_t chunk_len,
-                                     float* __restrict__ part) {
-    const int chunk = blockIdx.x;
-    const int64_t p0 = chunk * chunk_len;
-    const int64_t p1 = min(npix, p0 + chunk_len);
-    for (int co = threadIdx.x; co < Cout; co += blockDim.x) {
-        float s = 0.f;
-        for (int64_t px = p0; px < p1; ++px) s += __bfloat162float(dy[px * Cout + co]);
-        part[(int64_t)chunk * Cout + co] = s;
-    }
-}
 __global__ void dbias_reduce_kernel(const float* __restrict__ part, int chunks, int Cout, float* __restrict__ db,
                                     int accumulate) {
     const int co = blockIdx.x * blockDim.x + threadIdx.x;
@@ -608,8 +624,6 @@ __global__ void dbias_reduce_kernel(const float* __restrict__ part, int chunks, 
     for (int c = 0; c < chunks; ++c) s += part[(int64_t)c * Cout + co];
     db[co] = accumulate ? db[co] + s : s;
 }
-
-constexpr int DB_CHUNKS = 256;
 
 struct WgPlan {
     int RB, JB, BB, rt, bt, jt0, jt1, tiles0, ptiles;
@@ -647,7 +661,7 @@ bool tc_wgrad_supported(const Geom& g, int Cin, int Cout) {
 
 size_t tc_wgrad_ws_bytes(const Geom& g, int Cin, int Cout) {
     const WgPlan w = wg_plan(g, Cin, Cout);
-    return (size_t)w.chunks * g.T * Cout * Cin * sizeof(float) + (size_t)DB_CHUNKS * Cout * sizeof(float) + 256;
+    return (size_t)w.chunks * g.T * Cout * Cin * sizeof(float) + (size_t)w.chunks * Cout * sizeof(float) + 256;
 }
 
 hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -661,6 +675,7 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
     p.kchunks = w.kchunks; p.n_atoms = w.n_atoms; p.groups = w.groups; p.co_tiles = w.co_tiles;
     p.chunks = w.chunks; p.tiles_per_chunk = w.tiles_per_chunk;
     p.part = (float*)ws;
+    p.db_part = a.dbias ? (float*)ws + (size_t)w.chunks * g.T * a.Cout * a.Cin : nullptr;
     for (int pc = 0; pc < 2; ++pc)
         for (int t = 0; t < g.T; ++t) {
             int dc, dr;
@@ -689,12 +704,9 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
                                                                  a.dw, a.accumulate);
     count_launch();
     if (a.dbias) {
-        float* dbp = (float*)ws + (size_t)w.chunks * g.T * a.Cout * a.Cin;
-        const int64_t npix = (int64_t)g.B * g.H * g.W;
-        const int64_t len = (npix + DB_CHUNKS - 1) / DB_CHUNKS;
-        dbias_partial_kernel<<<DB_CHUNKS, 256, 0, st>>>((const __nv_bfloat16*)a.dy, npix, a.Cout, len, dbp);
-        dbias_reduce_kernel<<<ceil_div(a.Cout, 256), 256, 0, st>>>(dbp, DB_CHUNKS, a.Cout, a.dbias, a.accumulate);
-        count_launch(2);
+        dbias_reduce_kernel<<<ceil_div(a.Cout, 256), 256, 0, st>>>(p.db_part, w.chunks, a.Cout, a.dbias,
+                                                                   a.accumulate);
+        count_launch();
     }
     return last_launch_status();
 }
