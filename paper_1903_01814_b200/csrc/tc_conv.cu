@@ -416,11 +416,15 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
 // a full group is two 128x256x16 MMAs per 16 pixels; atom a accumulates in
 // TMEM columns [64a, 64a+64).  Partial sums per pixel chunk go to a workspace
 // and are reduced in a fixed order (deterministic).
-constexpr int WG_PIX = 32;
-constexpr int WG_STAGES = 5;
-constexpr int WG_BOX_BYTES = WG_PIX * 128;         // one 64-channel box: 4 KB
+// Pixels per pipeline stage: 32 (5 stages) for Cin = 64, 64 (2 stages) otherwise.
+template <int PIX>
+struct WgCfg {
+    static constexpr int STAGES = PIX == 32 ? 5 : 2;
+    static constexpr int BOX = PIX * 128;          // one 64-channel box
+    static constexpr int STAGE_BYTES = (2 + 8) * BOX;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 128;
+};
 constexpr int WG_ATOMS = 8;                        // atoms per unit (512 TMEM columns)
-constexpr int WG_STAGE_BYTES = (2 + WG_ATOMS) * WG_BOX_BYTES;
 
 struct TcWgParams {
     int B, H, W, Cin, Cout, T, parity;
@@ -446,15 +450,17 @@ __device__ __forceinline__ void decode_ptile(const TcWgParams& p, int m, int* P,
     *b0 = bti * p.BB;
 }
 
+template <int PIX>
 __global__ void __launch_bounds__(192, 1)
 tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                      const __grid_constant__ CUtensorMap map_dy0, const __grid_constant__ CUtensorMap map_dy1,
                      const __grid_constant__ TcWgParams p) {
+    using Cfg = WgCfg<PIX>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = (uint64_t*)(smem + WG_STAGES * WG_STAGE_BYTES);
-    uint64_t* empty = full + WG_STAGES;
-    uint64_t* tfull = empty + WG_STAGES;
+    uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* tfull = empty + Cfg::STAGES;
     uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
 
     // unit decode
@@ -472,7 +478,7 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
     const bool do_db = p.db_part != nullptr && grp == 0;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < WG_STAGES; ++s) {
+        for (int s = 0; s < Cfg::STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], do_db ? 5 : 1);  // MMA commit (+ 4 epilogue warps reading dy)
         }
@@ -484,7 +490,7 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t stage_bytes = (2 + na) * WG_BOX_BYTES;
+    const uint32_t stage_bytes = (2 + na) * Cfg::BOX;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -495,21 +501,21 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
                 decode_ptile(p, pt, &P, &r0, &j0, &b0);
                 const int pc = (P + p.parity) & 1;
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
-                uint8_t* s = smem + stage * WG_STAGE_BYTES;
+                uint8_t* s = smem + stage * Cfg::STAGE_BYTES;
                 ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
                 const CUtensorMap* mdy = P ? &map_dy1 : &map_dy0;
                 ptx::tma_load_4d(mdy, &full[stage], s, co0, r0, j0, b0);
-                ptx::tma_load_4d(mdy, &full[stage], s + WG_BOX_BYTES, co0 + 64, r0, j0, b0);
+                ptx::tma_load_4d(mdy, &full[stage], s + Cfg::BOX, co0 + 64, r0, j0, b0);
                 for (int i = 0; i < na; ++i) {
                     const int a = a0 + i;
                     const int t = a / p.kchunks, kc = a - t * p.kchunks;
                     const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
                     const int Pv = (P + dc) & 1;
                     const int jsh = (P + dc - Pv) / 2;
-                    ptx::tma_load_4d(Pv ? &map_x1 : &map_x0, &full[stage], s + (2 + i) * WG_BOX_BYTES, kc * 64,
+                    ptx::tma_load_4d(Pv ? &map_x1 : &map_x0, &full[stage], s + (2 + i) * Cfg::BOX, kc * 64,
                                      r0 + dr, j0 + jsh, b0);
                 }
-                if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
             }
         }
     } else if (warp == 1) {
@@ -522,21 +528,21 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
             for (int pt = pt_begin; pt < pt_end; ++pt) {
                 ptx::mbar_wait(&full[stage], phase);
                 ptx::tc_fence_after();
-                const uint32_t s = ptx::smem_u32(smem + stage * WG_STAGE_BYTES);
-                const uint32_t bx = s + 2 * WG_BOX_BYTES;
+                const uint32_t s = ptx::smem_u32(smem + stage * Cfg::STAGE_BYTES);
+                const uint32_t bx = s + 2 * Cfg::BOX;
 #pragma unroll
-                for (int k = 0; k < WG_PIX / 16; ++k) {
+                for (int k = 0; k < PIX / 16; ++k) {
                     // MN-major SW128: 8-row K groups 1024 B apart, 64-element MN blocks one box (LBO) apart
-                    const uint64_t ad = ptx::smem_desc_sw128(s + k * 2048, WG_BOX_BYTES, 1024);
+                    const uint64_t ad = ptx::smem_desc_sw128(s + k * 2048, Cfg::BOX, 1024);
                     const uint32_t acc = (pt != pt_begin) || (k != 0);
-                    ptx::mma_bf16(tmem_base, ad, ptx::smem_desc_sw128(bx + k * 2048, WG_BOX_BYTES, 1024), idesc0, acc);
+                    ptx::mma_bf16(tmem_base, ad, ptx::smem_desc_sw128(bx + k * 2048, Cfg::BOX, 1024), idesc0, acc);
                     if (n1 > 0)
                         ptx::mma_bf16(tmem_base + 256, ad,
-                                      ptx::smem_desc_sw128(bx + 4 * WG_BOX_BYTES + k * 2048, WG_BOX_BYTES, 1024),
+                                      ptx::smem_desc_sw128(bx + 4 * Cfg::BOX + k * 2048, Cfg::BOX, 1024),
                                       idesc1, acc);
                 }
                 ptx::mma_commit(&empty[stage]);
-                if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
             }
             ptx::mma_commit(tfull);
         }
@@ -552,16 +558,16 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
             uint32_t phase = 0;
             for (int pt = pt_begin; pt < pt_end; ++pt) {
                 ptx::mbar_wait(&full[stage], phase);
-                const uint8_t* sdy = smem + stage * WG_STAGE_BYTES + box * WG_BOX_BYTES;
+                const uint8_t* sdy = smem + stage * Cfg::STAGE_BYTES + box * Cfg::BOX;
 #pragma unroll 8
-                for (int px = 0; px < WG_PIX; ++px) {
+                for (int px = 0; px < PIX; ++px) {
                     const __nv_bfloat16 v =
                         *reinterpret_cast<const __nv_bfloat16*>(sdy + px * 128 + ((j ^ (px & 7)) << 4) + sub * 2);
                     dsum += __bfloat162float(v);
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&empty[stage]);
-                if (++stage == WG_STAGES) { stage = 0; phase ^= 1; }
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
             }
             p.db_part[(int64_t)chunk * p.Cout + co0 + row] = dsum;
         }
@@ -630,9 +636,11 @@ struct WgPlan {
     int kchunks, n_atoms, groups, co_tiles, chunks, tiles_per_chunk;
 };
 
+static int wg_pix(int Cin) { return Cin == 64 ? 32 : 64; }
+
 static WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
     WgPlan w{};
-    choose_box(g.B, g.H, g.W, WG_PIX, &w.RB, &w.JB, &w.BB);
+    choose_box(g.B, g.H, g.W, wg_pix(Cin), &w.RB, &w.JB, &w.BB);
     w.rt = ceil_div(g.H, w.RB);
     w.bt = ceil_div(g.B, w.BB);
     w.jt0 = ceil_div((g.W + 1) / 2, w.JB);
@@ -664,6 +672,20 @@ size_t tc_wgrad_ws_bytes(const Geom& g, int Cin, int Cout) {
     return (size_t)w.chunks * g.T * Cout * Cin * sizeof(float) + (size_t)w.chunks * Cout * sizeof(float) + 256;
 }
 
+template <int PIX>
+static hex_status_t launch_wgrad_pix(const CUtensorMap& mx0, const CUtensorMap& mx1, const CUtensorMap& md0,
+                                     const CUtensorMap& md1, const TcWgParams& p, int units, cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(tc_conv_wgrad_kernel<PIX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 WgCfg<PIX>::SMEM) != cudaSuccess)
+            return HEX_ERR_CUDA;
+        attr_set = true;
+    }
+    tc_conv_wgrad_kernel<PIX><<<units, 192, WgCfg<PIX>::SMEM, st>>>(mx0, mx1, md0, md1, p);
+    return HEX_OK;
+}
+
 hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
     const Geom& g = a.g;
     const WgPlan w = wg_plan(g, a.Cin, a.Cout);
@@ -688,16 +710,12 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
     if (!make_view_map(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
     if (!make_view_map(&md0, a.dy, g.B, g.H, g.W, a.Cout, 0, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
     if (!make_view_map(&md1, a.dy, g.B, g.H, g.W, a.Cout, 1, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
-    const int smem = WG_STAGES * WG_STAGE_BYTES + 1024 + 128;
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(tc_conv_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
-            return HEX_ERR_CUDA;
-        attr_set = true;
-    }
     const int units = w.co_tiles * w.groups * w.chunks;
-    tc_conv_wgrad_kernel<<<units, 192, smem, st>>>(mx0, mx1, md0, md1, p);
+    if (wg_pix(a.Cin) == 32) {
+        if (launch_wgrad_pix<32>(mx0, mx1, md0, md1, p, units, st) != HEX_OK) return HEX_ERR_CUDA;
+    } else {
+        if (launch_wgrad_pix<64>(mx0, mx1, md0, md1, p, units, st) != HEX_OK) return HEX_ERR_CUDA;
+    }
     count_launch();
     const int64_t total = (int64_t)g.T * a.Cout * a.Cin;
     wgrad_tc_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const float*)ws, w.chunks, g.T, a.Cout, a.Cin,
