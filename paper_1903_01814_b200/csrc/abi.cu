@@ -175,7 +175,7 @@ hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* d, const void* x, const voi
     if (!x || !w || !y) return HEX_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     if (use_tc_fwd(d, g)) {
-        if (!aligned16(x) || !aligned16(y) || !aligned16(w)) return HEX_ERR_ALIGNMENT;
+        if (!aligned16(x) || !aligned16(y) || !aligned16(w) || (bias && !aligned16(bias))) return HEX_ERR_ALIGNMENT;
         const size_t need = packed_weight_bytes(d, g);
         if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
         void* wp = align_up(ws, 1024);

@@ -115,10 +115,8 @@ struct TcFwdParams {
     int rt, bt, jt0, jt1;  // tiles along rows, batch, and sub-columns of view 0 / view 1
     int tiles0;            // m tiles of view 0
     int n_tiles, total_tiles, kblocks;
-    int relu;
+    int relu, has_mask;
     const float* bias;
-    __nv_bfloat16* y;
-    const __nv_bfloat16* relu_y;
     int8_t tap_dc[2][TC_MAXT];
     int8_t tap_dr[2][TC_MAXT];
 };
@@ -150,32 +148,43 @@ struct FwdCfg {
     static constexpr int A_BYTES = TC_BM * 128;
     static constexpr int B_BYTES = BN * 128;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+    static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 5 : 7);
+    static constexpr int OUT_BYTES = TC_BM * 128;  // one 64-channel output chunk, SW128 staging
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-    static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+    static constexpr int SMEM = STAGES * STAGE + 2 * OUT_BYTES + 1024 + 256;
 };
 
 template <int BN>
 __global__ void __launch_bounds__(192, 1)
 tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
-                   const __grid_constant__ CUtensorMap map_w, const __grid_constant__ TcFwdParams p) {
+                   const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
+                   const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
+                   const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ TcFwdParams p) {
     using Cfg = FwdCfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE);
+    uint8_t* obuf = smem + Cfg::STAGES * Cfg::STAGE;
+    uint64_t* full = (uint64_t*)(obuf + 2 * Cfg::OUT_BYTES);
     uint64_t* empty = full + Cfg::STAGES;
     uint64_t* tfull = empty + Cfg::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    uint64_t* mbar = tempty + 2;  // mask-tile loads into the two staging buffers
+    uint32_t* tmem_slot = (uint32_t*)(mbar + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < Cfg::STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4); }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 4);
+            ptx::mbar_init(&mbar[a], 1);
+        }
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&map_x0);
         ptx::prefetch_tmap(&map_x1);
         ptx::prefetch_tmap(&map_w);
+        ptx::prefetch_tmap(&map_y0);
+        ptx::prefetch_tmap(&map_y1);
     }
     if (warp == 1) ptx::tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
     ptx::tc_fence_before();
@@ -238,57 +247,82 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
             }
         }
     } else {
-        // epilogue: warps 2..5 own TMEM lane quadrants (warp % 4)
+        // Epilogue: warps 2..5 own TMEM lane quadrants (warp % 4); tile row m = TMEM lane.
+        // Per 64-channel chunk: TMEM -> registers -> (bias, ReLU | ReLU-backward mask) -> bf16
+        // -> SW128 staging row m (16-byte chunk i at i ^ (m & 7)) -> one TMA store of the box.
         const int q = warp & 3;
         const int row = q * 32 + lane;
+        const int et = threadIdx.x - 64;  // 0..127
         int acc = 0;
         uint32_t aphase = 0;
+        int ob = 0;
+        uint32_t mphase0 = 0, mphase1 = 0;
         for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
             const TileCoord tc = decode_fwd_tile(p, tile, BN);
-            const int rl = row % p.RB;
-            const int jl = (row / p.RB) % p.JB;
-            const int bl = row / (p.RB * p.JB);
-            const int r = tc.r0 + rl, c = 2 * (tc.j0 + jl) + tc.P, b = tc.b0 + bl;
-            const bool valid = r < p.H && c < p.W && b < p.B;
-            const int64_t off = valid ? ((((int64_t)b * p.H + r) * p.W + c) * p.Cout + tc.n0) : 0;
+            const CUtensorMap* my = tc.P ? &map_y1 : &map_y0;
+            const CUtensorMap* mm = tc.P ? &map_m1 : &map_m0;
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
 #pragma unroll 1
-            for (int ch = 0; ch < BN / 32; ++ch) {
-                uint32_t v[32];
-                ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 32, v);
-                ptx::tmem_ld_wait();
-                if (valid) {
-                    const int co = tc.n0 + ch * 32;
-                    uint32_t mask[16];
-                    if (p.relu_y) {
-                        const uint4* m4 = reinterpret_cast<const uint4*>(p.relu_y + off + ch * 32);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            uint4 mm = __ldg(m4 + i);
-                            mask[4 * i] = mm.x; mask[4 * i + 1] = mm.y; mask[4 * i + 2] = mm.z; mask[4 * i + 3] = mm.w;
-                        }
+            for (int ch = 0; ch < BN / 64; ++ch) {
+                uint8_t* buf = obuf + ob * Cfg::OUT_BYTES;
+                const int c0 = tc.n0 + ch * 64;
+                if (et == 0) ptx::bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago
+                ptx::named_bar(1, 128);
+                if (p.has_mask) {
+                    if (et == 0) {
+                        ptx::mbar_arrive_expect_tx(&mbar[ob], Cfg::OUT_BYTES);
+                        ptx::tma_load_4d(mm, &mbar[ob], buf, c0, tc.r0, tc.j0, tc.b0);
                     }
-                    uint32_t packed[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        float f0 = __uint_as_float(v[2 * i]);
-                        float f1 = __uint_as_float(v[2 * i + 1]);
-                        if (p.bias) { f0 += __ldg(p.bias + co + 2 * i); f1 += __ldg(p.bias + co + 2 * i + 1); }
-                        if (p.relu) { f0 = fmaxf(f0, 0.f); f1 = fmaxf(f1, 0.f); }
-                        if (p.relu_y) {
-                            __nv_bfloat162 mm = *reinterpret_cast<__nv_bfloat162*>(&mask[i]);
-                            if (!(__low2float(mm) > 0.f)) f0 = 0.f;
-                            if (!(__high2float(mm) > 0.f)) f1 = 0.f;
-                        }
-                        __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
-                        packed[i] = *reinterpret_cast<uint32_t*>(&h);
-                    }
-                    uint4* dst = reinterpret_cast<uint4*>(p.y + off + ch * 32);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+                    ptx::mbar_wait(&mbar[ob], ob ? mphase1 : mphase0);
+                    if (ob) mphase1 ^= 1; else mphase0 ^= 1;
                 }
+                uint32_t v[64];
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 64;
+                ptx::tmem_ld32(taddr, v);
+                ptx::tmem_ld32(taddr + 32, v + 32);
+                ptx::tmem_ld_wait();
+                uint8_t* rowp = buf + row * 128;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    uint4* slot = reinterpret_cast<uint4*>(rowp + ((i ^ (row & 7)) << 4));
+                    float f[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) f[k] = __uint_as_float(v[8 * i + k]);
+                    if (p.bias) {
+                        const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i));
+                        const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i + 4));
+                        f[0] += b0.x; f[1] += b0.y; f[2] += b0.z; f[3] += b0.w;
+                        f[4] += b1.x; f[5] += b1.y; f[6] += b1.z; f[7] += b1.w;
+                    }
+                    if (p.relu) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) f[k] = fmaxf(f[k], 0.f);
+                    }
+                    if (p.has_mask) {
+                        const uint4 m4 = *slot;
+                        const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t bits = (k & 1) ? (mw[k >> 1] & 0xffff0000u) : (mw[k >> 1] << 16);
+                            if (!(__uint_as_float(bits) > 0.f)) f[k] = 0.f;
+                        }
+                    }
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * k], f[2 * k + 1]);
+                        pk[k] = *reinterpret_cast<uint32_t*>(&h);
+                    }
+                    *slot = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA store
+                ptx::named_bar(1, 128);
+                if (et == 0) {
+                    ptx::tma_store_4d(my, buf, c0, tc.r0, tc.j0, tc.b0);
+                    ptx::bulk_commit();
+                }
+                ob ^= 1;
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -296,6 +330,7 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
+        if (et == 0) ptx::bulk_wait<0>();
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -354,7 +389,8 @@ bool tc_conv_supported(const Geom& g, int Cin, int Cout) {
 
 template <int BN>
 static hex_status_t launch_fwd_bn(const CUtensorMap& mx0, const CUtensorMap& mx1, const CUtensorMap& mw,
-                                  const TcFwdParams& p, cudaStream_t st) {
+                                  const CUtensorMap& my0, const CUtensorMap& my1, const CUtensorMap& mm0,
+                                  const CUtensorMap& mm1, const TcFwdParams& p, cudaStream_t st) {
     using Cfg = FwdCfg<BN>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -364,7 +400,7 @@ static hex_status_t launch_fwd_bn(const CUtensorMap& mx0, const CUtensorMap& mx1
         attr_set = true;
     }
     const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
-    tc_conv_fwd_kernel<BN><<<grid, 192, Cfg::SMEM, st>>>(mx0, mx1, mw, p);
+    tc_conv_fwd_kernel<BN><<<grid, 192, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
     count_launch();
     return last_launch_status();
 }
@@ -384,9 +420,8 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     p.total_tiles = (p.tiles0 + p.rt * p.jt1 * p.bt) * p.n_tiles;
     p.kblocks = a.Cin / TC_BK;
     p.relu = a.relu;
+    p.has_mask = a.relu_y != nullptr;
     p.bias = a.bias;
-    p.y = (__nv_bfloat16*)a.y;
-    p.relu_y = (const __nv_bfloat16*)a.relu_y;
     for (int pc = 0; pc < 2; ++pc)
         for (int t = 0; t < g.T; ++t) {
             int dc, dr;
@@ -398,10 +433,20 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     if (!make_view_map(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
     if (!make_view_map(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
     if (!make_weight_map(&mw, a.wpack, g.T, a.Cout, a.Cin, BN)) return HEX_ERR_CUDA;
+    CUtensorMap my0, my1, mm0, mm1;
+    if (!make_view_map(&my0, a.y, g.B, g.H, g.W, a.Cout, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
+    if (!make_view_map(&my1, a.y, g.B, g.H, g.W, a.Cout, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
+    if (a.relu_y) {
+        if (!make_view_map(&mm0, a.relu_y, g.B, g.H, g.W, a.Cout, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
+        if (!make_view_map(&mm1, a.relu_y, g.B, g.H, g.W, a.Cout, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
+    } else {
+        mm0 = my0;
+        mm1 = my1;
+    }
     switch (BN) {
-        case 256: return launch_fwd_bn<256>(mx0, mx1, mw, p, st);
-        case 128: return launch_fwd_bn<128>(mx0, mx1, mw, p, st);
-        default: return launch_fwd_bn<64>(mx0, mx1, mw, p, st);
+        case 256: return launch_fwd_bn<256>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
+        case 128: return launch_fwd_bn<128>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
+        default: return launch_fwd_bn<64>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
     }
 }
 
