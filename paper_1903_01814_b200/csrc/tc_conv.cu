@@ -115,6 +115,7 @@ struct TcFwdParams {
     int rt, bt, jt0, jt1;  // tiles along rows, batch, and sub-columns of view 0 / view 1
     int tiles0;            // m tiles of view 0
     int n_tiles, total_tiles, kblocks;
+    int m_total, pair_tiles;  // m tiles over both views; (n tile, m-tile pair) work items of the 2-CTA kernel
     int relu, has_mask;
     const float* bias;
     int8_t tap_dc[2][TC_MAXT];
@@ -143,6 +144,21 @@ __device__ __forceinline__ TileCoord decode_fwd_tile(const TcFwdParams& p, int t
     return tc;
 }
 
+// 2-CTA kernel: work item = (n tile, pair of consecutive m tiles); CTA `rank` of the
+// pair takes m tile 2*mpair + rank.  A missing odd tile gets r0 = H: its loads are
+// out of bounds (zero fill) and its TMA stores are clipped entirely.
+__device__ __forceinline__ TileCoord decode_pair_tile(const TcFwdParams& p, int ptile, int BN, int rank) {
+    const int nt = ptile % p.n_tiles;
+    const int m = 2 * (ptile / p.n_tiles) + rank;
+    TileCoord tc;
+    if (m >= p.m_total) {
+        tc.P = 0; tc.r0 = p.H; tc.j0 = 0; tc.b0 = 0; tc.n0 = nt * BN;
+        return tc;
+    }
+    tc = decode_fwd_tile(p, m * p.n_tiles + nt, BN);
+    return tc;
+}
+
 template <int BN>
 struct FwdCfg {
     static constexpr int A_BYTES = TC_BM * 128;
@@ -153,6 +169,107 @@ struct FwdCfg {
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr int SMEM = STAGES * STAGE + 2 * OUT_BYTES + 1024 + 256;
 };
+
+// Epilogue shared by the 1-CTA and 2-CTA forward kernels (warps 2..5).
+template <int BN, bool PAIR>
+__device__ __forceinline__ void fwd_epilogue(const TcFwdParams& p, const CUtensorMap* map_y0,
+                                             const CUtensorMap* map_y1, const CUtensorMap* map_m0,
+                                             const CUtensorMap* map_m1, uint8_t* obuf, uint64_t* tfull,
+                                             uint64_t* tempty, uint64_t* mbar, uint32_t tmem_base, int first,
+                                             int step, int rank) {
+    using Cfg = FwdCfg<BN>;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    {
+        // Epilogue: warps 2..5 own TMEM lane quadrants (warp % 4); tile row m = TMEM lane.
+        // Per 64-channel chunk: TMEM -> registers -> (bias, ReLU | ReLU-backward mask) -> bf16
+        // -> SW128 staging row m (16-byte chunk i at i ^ (m & 7)) -> one TMA store of the box.
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int et = threadIdx.x - 64;  // 0..127
+        int acc = 0;
+        uint32_t aphase = 0;
+        int ob = 0;
+        uint32_t mphase0 = 0, mphase1 = 0;
+        const int ntiles = PAIR ? p.pair_tiles : p.total_tiles;
+        for (int tile = first; tile < ntiles; tile += step) {
+            const TileCoord tc = PAIR ? decode_pair_tile(p, tile, BN, rank) : decode_fwd_tile(p, tile, BN);
+            const CUtensorMap* my = tc.P ? map_y1 : map_y0;
+            const CUtensorMap* mm = tc.P ? map_m1 : map_m0;
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 64; ++ch) {
+                uint8_t* buf = obuf + ob * Cfg::OUT_BYTES;
+                const int c0 = tc.n0 + ch * 64;
+                if (et == 0) ptx::bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago
+                ptx::named_bar(1, 128);
+                if (p.has_mask) {
+                    if (et == 0) {
+                        ptx::mbar_arrive_expect_tx(&mbar[ob], Cfg::OUT_BYTES);
+                        ptx::tma_load_4d(mm, &mbar[ob], buf, c0, tc.r0, tc.j0, tc.b0);
+                    }
+                    ptx::mbar_wait(&mbar[ob], ob ? mphase1 : mphase0);
+                    if (ob) mphase1 ^= 1; else mphase0 ^= 1;
+                }
+                uint32_t v[64];
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 64;
+                ptx::tmem_ld32(taddr, v);
+                ptx::tmem_ld32(taddr + 32, v + 32);
+                ptx::tmem_ld_wait();
+                uint8_t* rowp = buf + row * 128;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    uint4* slot = reinterpret_cast<uint4*>(rowp + ((i ^ (row & 7)) << 4));
+                    float f[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) f[k] = __uint_as_float(v[8 * i + k]);
+                    if (p.bias) {
+                        const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i));
+                        const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i + 4));
+                        f[0] += b0.x; f[1] += b0.y; f[2] += b0.z; f[3] += b0.w;
+                        f[4] += b1.x; f[5] += b1.y; f[6] += b1.z; f[7] += b1.w;
+                    }
+                    if (p.relu) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) f[k] = fmaxf(f[k], 0.f);
+                    }
+                    if (p.has_mask) {
+                        const uint4 m4 = *slot;
+                        const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t bits = (k & 1) ? (mw[k >> 1] & 0xffff0000u) : (mw[k >> 1] << 16);
+                            if (!(__uint_as_float(bits) > 0.f)) f[k] = 0.f;
+                        }
+                    }
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * k], f[2 * k + 1]);
+                        pk[k] = *reinterpret_cast<uint32_t*>(&h);
+                    }
+                    *slot = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA store
+                ptx::named_bar(1, 128);
+                if (et == 0) {
+                    ptx::tma_store_4d(my, buf, c0, tc.r0, tc.j0, tc.b0);
+                    ptx::bulk_commit();
+                }
+                ob ^= 1;
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (PAIR) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+                else ptx::mbar_arrive(&tempty[acc]);
+            }
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+        if (et == 0) ptx::bulk_wait<0>();
+    }
+}
 
 template <int BN>
 __global__ void __launch_bounds__(192, 1)
@@ -247,96 +364,141 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
             }
         }
     } else {
-        // Epilogue: warps 2..5 own TMEM lane quadrants (warp % 4); tile row m = TMEM lane.
-        // Per 64-channel chunk: TMEM -> registers -> (bias, ReLU | ReLU-backward mask) -> bf16
-        // -> SW128 staging row m (16-byte chunk i at i ^ (m & 7)) -> one TMA store of the box.
-        const int q = warp & 3;
-        const int row = q * 32 + lane;
-        const int et = threadIdx.x - 64;  // 0..127
-        int acc = 0;
-        uint32_t aphase = 0;
-        int ob = 0;
-        uint32_t mphase0 = 0, mphase1 = 0;
-        for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-            const TileCoord tc = decode_fwd_tile(p, tile, BN);
-            const CUtensorMap* my = tc.P ? &map_y1 : &map_y0;
-            const CUtensorMap* mm = tc.P ? &map_m1 : &map_m0;
-            ptx::mbar_wait(&tfull[acc], aphase);
-            ptx::tc_fence_after();
-#pragma unroll 1
-            for (int ch = 0; ch < BN / 64; ++ch) {
-                uint8_t* buf = obuf + ob * Cfg::OUT_BYTES;
-                const int c0 = tc.n0 + ch * 64;
-                if (et == 0) ptx::bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago
-                ptx::named_bar(1, 128);
-                if (p.has_mask) {
-                    if (et == 0) {
-                        ptx::mbar_arrive_expect_tx(&mbar[ob], Cfg::OUT_BYTES);
-                        ptx::tma_load_4d(mm, &mbar[ob], buf, c0, tc.r0, tc.j0, tc.b0);
-                    }
-                    ptx::mbar_wait(&mbar[ob], ob ? mphase1 : mphase0);
-                    if (ob) mphase1 ^= 1; else mphase0 ^= 1;
-                }
-                uint32_t v[64];
-                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 64;
-                ptx::tmem_ld32(taddr, v);
-                ptx::tmem_ld32(taddr + 32, v + 32);
-                ptx::tmem_ld_wait();
-                uint8_t* rowp = buf + row * 128;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    uint4* slot = reinterpret_cast<uint4*>(rowp + ((i ^ (row & 7)) << 4));
-                    float f[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) f[k] = __uint_as_float(v[8 * i + k]);
-                    if (p.bias) {
-                        const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i));
-                        const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i + 4));
-                        f[0] += b0.x; f[1] += b0.y; f[2] += b0.z; f[3] += b0.w;
-                        f[4] += b1.x; f[5] += b1.y; f[6] += b1.z; f[7] += b1.w;
-                    }
-                    if (p.relu) {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) f[k] = fmaxf(f[k], 0.f);
-                    }
-                    if (p.has_mask) {
-                        const uint4 m4 = *slot;
-                        const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const uint32_t bits = (k & 1) ? (mw[k >> 1] & 0xffff0000u) : (mw[k >> 1] << 16);
-                            if (!(__uint_as_float(bits) > 0.f)) f[k] = 0.f;
-                        }
-                    }
-                    uint32_t pk[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * k], f[2 * k + 1]);
-                        pk[k] = *reinterpret_cast<uint32_t*>(&h);
-                    }
-                    *slot = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                }
-                ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA store
-                ptx::named_bar(1, 128);
-                if (et == 0) {
-                    ptx::tma_store_4d(my, buf, c0, tc.r0, tc.j0, tc.b0);
-                    ptx::bulk_commit();
-                }
-                ob ^= 1;
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-            acc ^= 1;
-            if (acc == 0) aphase ^= 1;
-        }
-        if (et == 0) ptx::bulk_wait<0>();
+        fwd_epilogue<BN, false>(p, &map_y0, &map_y1, &map_m0, &map_m1, obuf, tfull, tempty, mbar, tmem_base,
+                                blockIdx.x, gridDim.x, 0);
     }
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    }
+}
+
+
+// ------------------------------------------------------------------ 2-CTA (cta_group::2) forward kernel
+// A CTA pair computes an M = 256 tile (each CTA its own 128-pixel box) x N = BN:
+// each CTA loads its A box and HALF of the weight tile (BN/2 rows), the leader
+// issues tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' smem, and each
+// CTA's TMEM receives its own 128 rows.  Per SM this halves the weight traffic
+// and the B footprint per stage (so the ring is deeper) compared with the
+// 1-CTA kernel.
+template <int BN>
+struct Fwd2Cfg {
+    static constexpr int A_BYTES = TC_BM * 128;
+    static constexpr int B_BYTES = (BN / 2) * 128;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int STAGES = BN == 256 ? 6 : (BN == 128 ? 8 : 9);
+    static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr int SMEM = STAGES * STAGE + 2 * FwdCfg<BN>::OUT_BYTES + 1024 + 256;
+};
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+tc_conv_fwd2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
+                    const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
+                    const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
+                    const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ TcFwdParams p) {
+    using Cfg = Fwd2Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* obuf = smem + Cfg::STAGES * Cfg::STAGE;
+    uint64_t* full = (uint64_t*)(obuf + 2 * FwdCfg<BN>::OUT_BYTES);
+    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* tfull = empty + Cfg::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* mbar = tempty + 2;
+    uint32_t* tmem_slot = (uint32_t*)(mbar + 2);
+
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < Cfg::STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+            ptx::mbar_init(&mbar[a], 1);
+        }
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&map_x0);
+        ptx::prefetch_tmap(&map_x1);
+        ptx::prefetch_tmap(&map_w);
+        ptx::prefetch_tmap(&map_y0);
+        ptx::prefetch_tmap(&map_y1);
+    }
+    if (warp == 1) ptx::tmem_alloc_2sm(tmem_slot, Cfg::TMEM_COLS);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int k_iters = p.T * p.kblocks;
+    const int first = blockIdx.x / 2, step = gridDim.x / 2;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = first; tile < p.pair_tiles; tile += step) {
+                const TileCoord tc = decode_pair_tile(p, tile, BN, rank);
+                const int pc = (tc.P + p.parity) & 1;
+                for (int t = 0; t < p.T; ++t) {
+                    const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
+                    const int Pv = (tc.P + dc) & 1;
+                    const int jsh = (tc.P + dc - Pv) / 2;
+                    const CUtensorMap* mx = Pv ? &map_x1 : &map_x0;
+                    for (int kb = 0; kb < p.kblocks; ++kb) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sa = smem + stage * Cfg::STAGE;
+                        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
+                        ptx::tma_load_4d_2sm(mx, &full[stage], sa, kb * TC_BK, tc.r0 + dr, tc.j0 + jsh, tc.b0);
+                        ptx::tma_load_3d_2sm(&map_w, &full[stage], sa + Cfg::A_BYTES, kb * TC_BK,
+                                             tc.n0 + (int)rank * (BN / 2), t);
+                        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(2 * TC_BM, BN, 0, 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t aphase = 0;
+            for (int tile = first; tile < p.pair_tiles; tile += step) {
+                ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int it = 0; it < k_iters; ++it) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(smem + stage * Cfg::STAGE);
+                    const uint32_t b0 = a0 + Cfg::A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < TC_BK / 16; ++k) {
+                        const uint64_t ad = ptx::smem_desc_sw128(a0 + k * 32, 16, 1024);
+                        const uint64_t bd = ptx::smem_desc_sw128(b0 + k * 32, 16, 1024);
+                        ptx::mma_bf16_2sm(d, ad, bd, idesc, (it | k) != 0);
+                    }
+                    ptx::mma_commit_2sm(&empty[stage]);
+                    if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit_2sm(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) aphase ^= 1;
+            }
+        }
+    } else {
+        fwd_epilogue<BN, true>(p, &map_y0, &map_y1, &map_m0, &map_m1, obuf, tfull, tempty, mbar, tmem_base, first,
+                               step, rank);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();  // the peer's smem / TMEM must outlive the leader's last MMA
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_2sm(tmem_base, Cfg::TMEM_COLS);
     }
 }
 
@@ -405,6 +567,26 @@ static hex_status_t launch_fwd_bn(const CUtensorMap& mx0, const CUtensorMap& mx1
     return last_launch_status();
 }
 
+template <int BN>
+static hex_status_t launch_fwd2_bn(const CUtensorMap& mx0, const CUtensorMap& mx1, const CUtensorMap& mw,
+                                   const CUtensorMap& my0, const CUtensorMap& my1, const CUtensorMap& mm0,
+                                   const CUtensorMap& mm1, const TcFwdParams& p, cudaStream_t st) {
+    using Cfg = Fwd2Cfg<BN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(tc_conv_fwd2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) !=
+            cudaSuccess)
+            return HEX_ERR_CUDA;
+        attr_set = true;
+    }
+    const int pairs = p.pair_tiles < num_sms() / 2 ? p.pair_tiles : num_sms() / 2;
+    tc_conv_fwd2_kernel<BN><<<2 * pairs, 192, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
+    count_launch();
+    return last_launch_status();
+}
+
+static bool use_2sm() { return getenv("HEXCONV_NO_2SM") == nullptr; }
+
 hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
     TcFwdParams p{};
@@ -416,8 +598,11 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     p.jt1 = ceil_div(g.W / 2, p.JB);
     p.tiles0 = p.rt * p.jt0 * p.bt;
     const int BN = pick_bn(a.Cout);
+    const bool pair = use_2sm();
     p.n_tiles = a.Cout / BN;
-    p.total_tiles = (p.tiles0 + p.rt * p.jt1 * p.bt) * p.n_tiles;
+    p.m_total = p.tiles0 + p.rt * p.jt1 * p.bt;
+    p.total_tiles = p.m_total * p.n_tiles;
+    p.pair_tiles = ceil_div(p.m_total, 2) * p.n_tiles;
     p.kblocks = a.Cin / TC_BK;
     p.relu = a.relu;
     p.has_mask = a.relu_y != nullptr;
@@ -432,7 +617,7 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     CUtensorMap mx0, mx1, mw;
     if (!make_view_map(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
     if (!make_view_map(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
-    if (!make_weight_map(&mw, a.wpack, g.T, a.Cout, a.Cin, BN)) return HEX_ERR_CUDA;
+    if (!make_weight_map(&mw, a.wpack, g.T, a.Cout, a.Cin, pair ? BN / 2 : BN)) return HEX_ERR_CUDA;
     CUtensorMap my0, my1, mm0, mm1;
     if (!make_view_map(&my0, a.y, g.B, g.H, g.W, a.Cout, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
     if (!make_view_map(&my1, a.y, g.B, g.H, g.W, a.Cout, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
@@ -442,6 +627,13 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     } else {
         mm0 = my0;
         mm1 = my1;
+    }
+    if (pair) {
+        switch (BN) {
+            case 256: return launch_fwd2_bn<256>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
+            case 128: return launch_fwd2_bn<128>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
+            default: return launch_fwd2_bn<64>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
+        }
     }
     switch (BN) {
         case 256: return launch_fwd_bn<256>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
