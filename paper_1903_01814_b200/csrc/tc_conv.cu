@@ -195,21 +195,24 @@ __device__ __forceinline__ void fwd_epilogue(const TcFwdParams& p, const CUtenso
             const TileCoord tc = PAIR ? decode_pair_tile(p, tile, BN, rank) : decode_fwd_tile(p, tile, BN);
             const CUtensorMap* my = tc.P ? map_y1 : map_y0;
             const CUtensorMap* mm = tc.P ? map_m1 : map_m0;
+            // ReLU-backward mask of the first chunk: fetch before waiting for the accumulator
+            if (p.has_mask && et == 0) {
+                ptx::bulk_wait_read<1>();  // buffer ob: its last store (2 chunks ago) has been read
+                ptx::mbar_arrive_expect_tx(&mbar[ob], Cfg::OUT_BYTES);
+                ptx::tma_load_4d(mm, &mbar[ob], obuf + ob * Cfg::OUT_BYTES, tc.n0, tc.r0, tc.j0, tc.b0);
+            }
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int ch = 0; ch < BN / 64; ++ch) {
                 uint8_t* buf = obuf + ob * Cfg::OUT_BYTES;
                 const int c0 = tc.n0 + ch * 64;
-                if (et == 0) ptx::bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago
-                ptx::named_bar(1, 128);
                 if (p.has_mask) {
-                    if (et == 0) {
-                        ptx::mbar_arrive_expect_tx(&mbar[ob], Cfg::OUT_BYTES);
-                        ptx::tma_load_4d(mm, &mbar[ob], buf, c0, tc.r0, tc.j0, tc.b0);
-                    }
                     ptx::mbar_wait(&mbar[ob], ob ? mphase1 : mphase0);
                     if (ob) mphase1 ^= 1; else mphase0 ^= 1;
+                } else {
+                    if (et == 0) ptx::bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago
+                    ptx::named_bar(1, 128);
                 }
                 uint32_t v[64];
                 const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 64;
@@ -255,6 +258,12 @@ __device__ __forceinline__ void fwd_epilogue(const TcFwdParams& p, const CUtenso
                 if (et == 0) {
                     ptx::tma_store_4d(my, buf, c0, tc.r0, tc.j0, tc.b0);
                     ptx::bulk_commit();
+                    if (p.has_mask && ch + 1 < BN / 64) {  // prefetch the next chunk's mask
+                        ptx::bulk_wait_read<1>();
+                        ptx::mbar_arrive_expect_tx(&mbar[ob ^ 1], Cfg::OUT_BYTES);
+                        ptx::tma_load_4d(mm, &mbar[ob ^ 1], obuf + (ob ^ 1) * Cfg::OUT_BYTES, c0 + 64, tc.r0, tc.j0,
+                                         tc.b0);
+                    }
                 }
                 ob ^= 1;
             }
@@ -585,7 +594,15 @@ static hex_status_t launch_fwd2_bn(const CUtensorMap& mx0, const CUtensorMap& mx
     return last_launch_status();
 }
 
-static bool use_2sm() { return getenv("HEXCONV_NO_2SM") == nullptr; }
+// The CTA-pair kernel halves the per-SM weight traffic; it pays off when the
+// weight tile is the larger operand (BN = 256).  For BN <= 128 the A operand
+// dominates and the 1-CTA kernel's deeper per-CTA tiles are as fast or faster
+// (round-1 measurements).  HEXCONV_FORCE_2SM / _NO_2SM override.
+static bool use_2sm(int BN) {
+    if (getenv("HEXCONV_NO_2SM")) return false;
+    if (getenv("HEXCONV_FORCE_2SM")) return true;
+    return BN == 256;
+}
 
 hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
@@ -598,9 +615,9 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     p.jt1 = ceil_div(g.W / 2, p.JB);
     p.tiles0 = p.rt * p.jt0 * p.bt;
     const int BN = pick_bn(a.Cout);
-    const bool pair = use_2sm();
     p.n_tiles = a.Cout / BN;
     p.m_total = p.tiles0 + p.rt * p.jt1 * p.bt;
+    const bool pair = use_2sm(BN) && p.m_total >= 2;
     p.total_tiles = p.m_total * p.n_tiles;
     p.pair_tiles = ceil_div(p.m_total, 2) * p.n_tiles;
     p.kblocks = a.Cin / TC_BK;

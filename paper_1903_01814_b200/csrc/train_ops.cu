@@ -6,109 +6,143 @@
 
 namespace hexconv {
 
-// gap[b][c] = mean_hw feat[b][hw][c]   (feat bf16 NHWC)
-__global__ void gap_kernel(const __nv_bfloat16* __restrict__ feat, float* __restrict__ gap, int HW, int C) {
-    const int b = blockIdx.x;
-    for (int c = threadIdx.x; c < C; c += blockDim.x) {
-        const __nv_bfloat16* p = feat + (int64_t)b * HW * C + c;
-        float s = 0.f;
-        for (int i = 0; i < HW; ++i) s += __bfloat162float(p[(int64_t)i * C]);
-        gap[(int64_t)b * C + c] = s / (float)HW;
-    }
-}
+// Per-sample block: global average pool (8 channels per thread, HW split over
+// thread slices, fixed-order smem reduction), logits, softmax cross-entropy,
+// dlogits.  gap[b][C], dlog[b][K], loss_b[b].
+constexpr int HEAD_THREADS = 256;
 
-// One block: logits, softmax CE, dlogits, dwl, dbl, dgap.
-__global__ void head_kernel(const float* __restrict__ gap, const float* __restrict__ wl, const float* __restrict__ bl,
-                            const int32_t* __restrict__ labels, float* __restrict__ loss, float* __restrict__ dwl,
-                            float* __restrict__ dbl, float* __restrict__ dlog, float* __restrict__ dgap,
-                            int B, int C, int K) {
-    extern __shared__ float sh[];  // [B*K] dlogits, then [blockDim] reduction scratch
-    float* dl = sh;
-    float* red = sh + B * K;
-    // logits and per-sample loss
-    float my_loss = 0.f;
-    for (int b = threadIdx.x; b < B; b += blockDim.x) {
-        float lg[8];
-        float mx = -INFINITY;
-        for (int k = 0; k < K; ++k) {
-            float s = bl[k];
-            for (int c = 0; c < C; ++c) s = fmaf(gap[(int64_t)b * C + c], wl[(int64_t)k * C + c], s);
-            lg[k] = s;
-            mx = fmaxf(mx, s);
+__global__ void __launch_bounds__(HEAD_THREADS)
+head_sample_kernel(const uint4* __restrict__ feat, const float* __restrict__ wl, const float* __restrict__ bl,
+                   const int32_t* __restrict__ labels, float* __restrict__ gap, float* __restrict__ dlog,
+                   float* __restrict__ loss_b, int B, int HW, int C, int K) {
+    extern __shared__ float sh[];  // [slices][C] partial sums, then logits
+    const int b = blockIdx.x;
+    const int C8 = C / 8;
+    const int slices = HEAD_THREADS / C8 > 0 ? HEAD_THREADS / C8 : 1;
+    const int tid = threadIdx.x;
+    const int c8 = tid % C8, sl = tid / C8;
+    if (sl < slices && tid < slices * C8) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = sl; i < HW; i += slices) {
+            const uint4 v4 = feat[((int64_t)b * HW + i) * C8 + c8];
+            const __nv_bfloat16* v = reinterpret_cast<const __nv_bfloat16*>(&v4);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(v[j]);
         }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sh[sl * C + c8 * 8 + j] = acc[j];
+    }
+    // C8 > HEAD_THREADS: loop the remaining channel groups with one slice
+    for (int cc = HEAD_THREADS + tid; cc < C8; cc += HEAD_THREADS) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = 0; i < HW; ++i) {
+            const uint4 v4 = feat[((int64_t)b * HW + i) * C8 + cc];
+            const __nv_bfloat16* v = reinterpret_cast<const __nv_bfloat16*>(&v4);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(v[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sh[cc * 8 + j] = acc[j];
+    }
+    __syncthreads();
+    float* g = sh;  // reduce slices into row 0
+    for (int c = tid; c < C; c += HEAD_THREADS) {
+        float s = 0.f;
+        const int ns = (C8 <= HEAD_THREADS) ? slices : 1;
+        for (int k = 0; k < ns; ++k) s += sh[k * C + c];
+        g[c] = s / (float)HW;
+    }
+    __syncthreads();
+    for (int c = tid; c < C; c += HEAD_THREADS) gap[(int64_t)b * C + c] = g[c];
+    // logits: warp k computes logit k
+    float* lg = sh + C;
+    const int warp = tid / 32, lane = tid % 32;
+    for (int k = warp; k < K; k += HEAD_THREADS / 32) {
+        float s = 0.f;
+        for (int c = lane; c < C; c += 32) s = fmaf(g[c], wl[(int64_t)k * C + c], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) lg[k] = s + bl[k];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        float mx = -INFINITY;
+        for (int k = 0; k < K; ++k) mx = fmaxf(mx, lg[k]);
         float z = 0.f;
         for (int k = 0; k < K; ++k) z += expf(lg[k] - mx);
         const int y = labels[b];
-        my_loss += (logf(z) + mx - lg[y]);
-        for (int k = 0; k < K; ++k) {
-            const float pk = expf(lg[k] - mx) / z;
-            dl[b * K + k] = (pk - (k == y ? 1.f : 0.f)) / (float)B;
-        }
+        loss_b[b] = logf(z) + mx - lg[y];
+        for (int k = 0; k < K; ++k)
+            dlog[(int64_t)b * K + k] = (expf(lg[k] - mx) / z - (k == y ? 1.f : 0.f)) / (float)B;
     }
-    red[threadIdx.x] = my_loss;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float s = 0.f;
-        for (int i = 0; i < (int)blockDim.x; ++i) s += red[i];
-        *loss = s / (float)B;
-    }
-    // dwl[k][c] = sum_b dl[b][k] gap[b][c]; dbl[k] = sum_b dl[b][k]
-    for (int i = threadIdx.x; i < K * C; i += blockDim.x) {
-        const int k = i / C, c = i % C;
-        float s = 0.f;
-        for (int b = 0; b < B; ++b) s = fmaf(dl[b * K + k], gap[(int64_t)b * C + c], s);
-        dwl[i] = s;
-    }
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
-        float s = 0.f;
-        for (int b = 0; b < B; ++b) s += dl[b * K + k];
-        dbl[k] = s;
-    }
-    // dgap[b][c] = sum_k dl[b][k] wl[k][c]
-    for (int i = threadIdx.x; i < B * C; i += blockDim.x) {
-        const int b = i / C, c = i % C;
-        float s = 0.f;
-        for (int k = 0; k < K; ++k) s = fmaf(dl[b * K + k], wl[(int64_t)k * C + c], s);
-        dgap[i] = s;
-    }
-    for (int i = threadIdx.x; i < B * K; i += blockDim.x) dlog[i] = dl[i];
 }
 
-// dfeat[b][hw][c] = dgap[b][c] / HW * (feat > 0)   (8 channels per thread)
-__global__ void head_dfeat_kernel(const uint4* __restrict__ feat, const float* __restrict__ dgap,
-                                  uint4* __restrict__ dfeat, int B, int HW, int C8) {
+// dwl[k][c] = sum_b dlog[b][k] gap[b][c]; dbl[k] = sum_b dlog[b][k]; loss = mean_b loss_b (fixed order)
+__global__ void head_param_grad_kernel(const float* __restrict__ gap, const float* __restrict__ dlog,
+                                       const float* __restrict__ loss_b, float* __restrict__ dwl,
+                                       float* __restrict__ dbl, float* __restrict__ loss, int B, int C, int K) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < K * C) {
+        const int k = i / C, c = i % C;
+        float s = 0.f;
+        for (int b = 0; b < B; ++b) s = fmaf(dlog[(int64_t)b * K + k], gap[(int64_t)b * C + c], s);
+        dwl[i] = s;
+    } else if (i < K * C + K) {
+        const int k = i - K * C;
+        float s = 0.f;
+        for (int b = 0; b < B; ++b) s += dlog[(int64_t)b * K + k];
+        dbl[k] = s;
+    } else if (i == K * C + K) {
+        float s = 0.f;
+        for (int b = 0; b < B; ++b) s += loss_b[b];
+        *loss = s / (float)B;
+    }
+}
+
+// dfeat[b][hw][c] = (sum_k dlog[b][k] wl[k][c]) / HW * (feat > 0)   (8 channels per thread)
+__global__ void head_dfeat_kernel(const uint4* __restrict__ feat, const float* __restrict__ dlog,
+                                  const float* __restrict__ wl, uint4* __restrict__ dfeat, int B, int HW, int C8,
+                                  int K) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t total = (int64_t)B * HW * C8;
     if (idx >= total) return;
     const int c8 = (int)(idx % C8);
     const int b = (int)(idx / ((int64_t)HW * C8));
+    const int C = C8 * 8;
     uint4 f4 = feat[idx];
     const __nv_bfloat16* f = reinterpret_cast<const __nv_bfloat16*>(&f4);
     uint4 o4;
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&o4);
     const float inv = 1.f / (float)HW;
-    const float* dg = dgap + (int64_t)b * C8 * 8 + c8 * 8;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16_rn(__bfloat162float(f[j]) > 0.f ? dg[j] * inv : 0.f);
+    for (int j = 0; j < 8; ++j) {
+        float dg = 0.f;
+        for (int k = 0; k < K; ++k) dg = fmaf(dlog[(int64_t)b * K + k], wl[(int64_t)k * C + c8 * 8 + j], dg);
+        o[j] = __float2bfloat16_rn(__bfloat162float(f[j]) > 0.f ? dg * inv : 0.f);
+    }
     dfeat[idx] = o4;
 }
 
 size_t head_ws_bytes(int B, int K, int C) {
-    return (size_t)(B * C + B * C + B * K) * sizeof(float);
+    return (size_t)(B * C + B * K + B) * sizeof(float);
 }
 
 hex_status_t head_fwd_bwd(int B, int HW, int C, int K, const void* feat, const float* wl, const float* bl,
                           const int32_t* labels, float* loss, void* dfeat, float* dwl, float* dbl, void* ws,
                           cudaStream_t st) {
     float* gap = (float*)ws;
-    float* dgap = gap + (size_t)B * C;
-    float* dlog = dgap + (size_t)B * C;
-    gap_kernel<<<B, 256, 0, st>>>((const __nv_bfloat16*)feat, gap, HW, C);
-    const int threads = 256;
-    head_kernel<<<1, threads, (B * K + threads) * sizeof(float), st>>>(gap, wl, bl, labels, loss, dwl, dbl, dlog,
-                                                                         dgap, B, C, K);
-    const int64_t total = (int64_t)B * HW * (C / 8);
-    head_dfeat_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const uint4*)feat, dgap, (uint4*)dfeat, B, HW, C / 8);
+    float* dlog = gap + (size_t)B * C;
+    float* loss_b = dlog + (size_t)B * K;
+    const int C8 = C / 8;
+    const int slices = HEAD_THREADS / C8 > 0 ? HEAD_THREADS / C8 : 1;
+    const size_t smem = ((size_t)slices * C + 16) * sizeof(float);
+    if (smem > 48 * 1024) return HEX_ERR_UNSUPPORTED;
+    head_sample_kernel<<<B, HEAD_THREADS, smem, st>>>((const uint4*)feat, wl, bl, labels, gap, dlog, loss_b, B, HW,
+                                                      C, K);
+    head_param_grad_kernel<<<ceil_div(K * C + K + 1, 256), 256, 0, st>>>(gap, dlog, loss_b, dwl, dbl, loss, B, C, K);
+    const int64_t total = (int64_t)B * HW * C8;
+    head_dfeat_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const uint4*)feat, dlog, wl, (uint4*)dfeat, B, HW, C8,
+                                                            K);
     count_launch(3);
     return last_launch_status();
 }
