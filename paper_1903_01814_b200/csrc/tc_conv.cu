@@ -687,6 +687,7 @@ struct TcWgParams {
     int kchunks, n_atoms, groups, co_tiles, chunks, tiles_per_chunk;
     float* part;     // [chunks][T][Cout][Cin]
     float* db_part;  // [chunks][Cout] or NULL (no bias gradient)
+    int dbg;         // development: 1 = skip TMA loads, 2 = skip MMAs (results invalid)
     int8_t tap_dc[2][TC_MAXT];
     int8_t tap_dr[2][TC_MAXT];
 };
@@ -756,6 +757,11 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
                 const int pc = (P + p.parity) & 1;
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* s = smem + stage * Cfg::STAGE_BYTES;
+                if (p.dbg == 1) {
+                    ptx::mbar_arrive(&full[stage]);
+                    if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+                    continue;
+                }
                 ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
                 const CUtensorMap* mdy = P ? &map_dy1 : &map_dy0;
                 ptx::tma_load_4d(mdy, &full[stage], s, co0, r0, j0, b0);
@@ -789,6 +795,7 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
                     // MN-major SW128: 8-row K groups 1024 B apart, 64-element MN blocks one box (LBO) apart
                     const uint64_t ad = ptx::smem_desc_sw128(s + k * 2048, Cfg::BOX, 1024);
                     const uint32_t acc = (pt != pt_begin) || (k != 0);
+                    if (p.dbg == 2) continue;
                     ptx::mma_bf16(tmem_base, ad, ptx::smem_desc_sw128(bx + k * 2048, Cfg::BOX, 1024), idesc0, acc);
                     if (n1 > 0)
                         ptx::mma_bf16(tmem_base + 256, ad,
@@ -952,6 +959,7 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
     p.chunks = w.chunks; p.tiles_per_chunk = w.tiles_per_chunk;
     p.part = (float*)ws;
     p.db_part = a.dbias ? (float*)ws + (size_t)w.chunks * g.T * a.Cout * a.Cin : nullptr;
+    p.dbg = getenv("HEXCONV_WG_DEBUG") ? atoi(getenv("HEXCONV_WG_DEBUG")) : 0;
     for (int pc = 0; pc < 2; ++pc)
         for (int t = 0; t < g.T; ++t) {
             int dc, dr;
