@@ -739,6 +739,10 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
         }
         ptx::mbar_init(tfull, 1);
         ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&map_x0);
+        ptx::prefetch_tmap(&map_x1);
+        ptx::prefetch_tmap(&map_dy0);
+        ptx::prefetch_tmap(&map_dy1);
     }
     if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
     ptx::tc_fence_before();
