@@ -73,6 +73,40 @@ static bool make_view_map(CUtensorMap* m, const void* base, int B, int H, int W,
     return r == CUDA_SUCCESS;
 }
 
+// The same parity view with the channel axis split into 64-channel chunks as an
+// OUTER dimension: dims {64, H, Wp, B, C/64}, box {64, RB, JB, BB, KC}.  One TMA op
+// then fills KC consecutive canonical SW128 blocks (one per 64-channel chunk).
+static bool make_view_map5(CUtensorMap* m, const void* base, int B, int H, int W, int C, int P, int RB, int JB,
+                           int BB, int KC) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    const int Wp = (W - P + 1) / 2;
+    if (Wp < 1 || C % 64) return false;
+    cuuint64_t dims[5] = {64, (cuuint64_t)H, (cuuint64_t)Wp, (cuuint64_t)B, (cuuint64_t)(C / 64)};
+    cuuint64_t strides[4] = {(cuuint64_t)W * C * 2, (cuuint64_t)2 * C * 2, (cuuint64_t)H * W * C * 2, 128};
+    cuuint32_t box[5] = {64, (cuuint32_t)RB, (cuuint32_t)JB, (cuuint32_t)BB, (cuuint32_t)KC};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    void* addr = (void*)((const char*)base + (size_t)P * C * 2);
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, addr, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// packed weights [T][N][K] as dims {64, N, K/64, T}, box {64, BN, KC, 1}: KC blocks of [BN][64]
+static bool make_weight_map4(CUtensorMap* m, const void* base, int T, int N, int K, int BN, int KC) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {64, (cuuint64_t)N, (cuuint64_t)(K / 64), (cuuint64_t)T};
+    cuuint64_t strides[3] = {(cuuint64_t)K * 2, 128, (cuuint64_t)N * K * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)BN, (cuuint32_t)KC, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // packed weights [T][N][K] bf16, box {64, BN, 1}
 static bool make_weight_map(CUtensorMap* m, const void* base, int T, int N, int K, int BN) {
     auto enc = get_encode();
@@ -159,12 +193,14 @@ __device__ __forceinline__ TileCoord decode_pair_tile(const TcFwdParams& p, int 
     return tc;
 }
 
-template <int BN>
+// KC = 64-channel chunks per K iteration (one TMA op each for A and B).
+template <int BN, int KC = 1>
 struct FwdCfg {
-    static constexpr int A_BYTES = TC_BM * 128;
-    static constexpr int B_BYTES = BN * 128;
-    static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 5 : 7);
+    static constexpr int A_CHUNK = TC_BM * 128;
+    static constexpr int B_CHUNK = BN * 128;
+    static constexpr int A_BYTES = KC * A_CHUNK;
+    static constexpr int STAGE = KC * (A_CHUNK + B_CHUNK);
+    static constexpr int STAGES = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);
     static constexpr int OUT_BYTES = TC_BM * 128;  // one 64-channel output chunk, SW128 staging
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr int SMEM = STAGES * STAGE + 2 * OUT_BYTES + 1024 + 256;
@@ -280,13 +316,13 @@ __device__ __forceinline__ void fwd_epilogue(const TcFwdParams& p, const CUtenso
     }
 }
 
-template <int BN>
+template <int BN, int KC>
 __global__ void __launch_bounds__(192, 1)
 tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                    const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
                    const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
                    const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ TcFwdParams p) {
-    using Cfg = FwdCfg<BN>;
+    using Cfg = FwdCfg<BN, KC>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* obuf = smem + Cfg::STAGES * Cfg::STAGE;
@@ -317,7 +353,8 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int k_iters = p.T * p.kblocks;
+    const int kgroups = p.kblocks / KC;
+    const int k_iters = p.T * kgroups;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -331,12 +368,12 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
                     const int Pv = (tc.P + dc) & 1;
                     const int jsh = (tc.P + dc - Pv) / 2;
                     const CUtensorMap* mx = Pv ? &map_x1 : &map_x0;
-                    for (int kb = 0; kb < p.kblocks; ++kb) {
+                    for (int kg = 0; kg < kgroups; ++kg) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sa = smem + stage * Cfg::STAGE;
                         ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
-                        ptx::tma_load_4d(mx, &full[stage], sa, kb * TC_BK, tc.r0 + dr, tc.j0 + jsh, tc.b0);
-                        ptx::tma_load_3d(&map_w, &full[stage], sa + Cfg::A_BYTES, kb * TC_BK, tc.n0, t);
+                        ptx::tma_load_5d(mx, &full[stage], sa, 0, tc.r0 + dr, tc.j0 + jsh, tc.b0, kg * KC);
+                        ptx::tma_load_4d(&map_w, &full[stage], sa + Cfg::A_BYTES, 0, tc.n0, kg * KC, t);
                         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -359,11 +396,13 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
                     const uint32_t a0 = ptx::smem_u32(smem + stage * Cfg::STAGE);
                     const uint32_t b0 = a0 + Cfg::A_BYTES;
 #pragma unroll
-                    for (int k = 0; k < TC_BK / 16; ++k) {
-                        const uint64_t ad = ptx::smem_desc_sw128(a0 + k * 32, 16, 1024);
-                        const uint64_t bd = ptx::smem_desc_sw128(b0 + k * 32, 16, 1024);
-                        ptx::mma_bf16(d, ad, bd, idesc, (it | k) != 0);
-                    }
+                    for (int c = 0; c < KC; ++c)
+#pragma unroll
+                        for (int k = 0; k < TC_BK / 16; ++k) {
+                            const uint64_t ad = ptx::smem_desc_sw128(a0 + c * Cfg::A_CHUNK + k * 32, 16, 1024);
+                            const uint64_t bd = ptx::smem_desc_sw128(b0 + c * Cfg::B_CHUNK + k * 32, 16, 1024);
+                            ptx::mma_bf16(d, ad, bd, idesc, (it | c | k) != 0);
+                        }
                     ptx::mma_commit(&empty[stage]);
                     if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -392,23 +431,24 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
 // CTA's TMEM receives its own 128 rows.  Per SM this halves the weight traffic
 // and the B footprint per stage (so the ring is deeper) compared with the
 // 1-CTA kernel.
-template <int BN>
+template <int BN, int KC = 1>
 struct Fwd2Cfg {
-    static constexpr int A_BYTES = TC_BM * 128;
-    static constexpr int B_BYTES = (BN / 2) * 128;
-    static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = BN == 256 ? 6 : (BN == 128 ? 8 : 9);
+    static constexpr int A_CHUNK = TC_BM * 128;
+    static constexpr int B_CHUNK = (BN / 2) * 128;
+    static constexpr int A_BYTES = KC * A_CHUNK;
+    static constexpr int STAGE = KC * (A_CHUNK + B_CHUNK);
+    static constexpr int STAGES = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr int SMEM = STAGES * STAGE + 2 * FwdCfg<BN>::OUT_BYTES + 1024 + 256;
 };
 
-template <int BN>
+template <int BN, int KC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 tc_conv_fwd2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                     const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
                     const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
                     const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ TcFwdParams p) {
-    using Cfg = Fwd2Cfg<BN>;
+    using Cfg = Fwd2Cfg<BN, KC>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* obuf = smem + Cfg::STAGES * Cfg::STAGE;
@@ -441,7 +481,8 @@ tc_conv_fwd2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int k_iters = p.T * p.kblocks;
+    const int kgroups = p.kblocks / KC;
+    const int k_iters = p.T * kgroups;
     const int first = blockIdx.x / 2, step = gridDim.x / 2;
 
     if (warp == 0) {
@@ -456,13 +497,13 @@ tc_conv_fwd2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
                     const int Pv = (tc.P + dc) & 1;
                     const int jsh = (tc.P + dc - Pv) / 2;
                     const CUtensorMap* mx = Pv ? &map_x1 : &map_x0;
-                    for (int kb = 0; kb < p.kblocks; ++kb) {
+                    for (int kg = 0; kg < kgroups; ++kg) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sa = smem + stage * Cfg::STAGE;
                         if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
-                        ptx::tma_load_4d_2sm(mx, &full[stage], sa, kb * TC_BK, tc.r0 + dr, tc.j0 + jsh, tc.b0);
-                        ptx::tma_load_3d_2sm(&map_w, &full[stage], sa + Cfg::A_BYTES, kb * TC_BK,
-                                             tc.n0 + (int)rank * (BN / 2), t);
+                        ptx::tma_load_5d_2sm(mx, &full[stage], sa, 0, tc.r0 + dr, tc.j0 + jsh, tc.b0, kg * KC);
+                        ptx::tma_load_4d_2sm(&map_w, &full[stage], sa + Cfg::A_BYTES, 0, tc.n0 + (int)rank * (BN / 2),
+                                             kg * KC, t);
                         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -485,11 +526,13 @@ tc_conv_fwd2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
                     const uint32_t a0 = ptx::smem_u32(smem + stage * Cfg::STAGE);
                     const uint32_t b0 = a0 + Cfg::A_BYTES;
 #pragma unroll
-                    for (int k = 0; k < TC_BK / 16; ++k) {
-                        const uint64_t ad = ptx::smem_desc_sw128(a0 + k * 32, 16, 1024);
-                        const uint64_t bd = ptx::smem_desc_sw128(b0 + k * 32, 16, 1024);
-                        ptx::mma_bf16_2sm(d, ad, bd, idesc, (it | k) != 0);
-                    }
+                    for (int c = 0; c < KC; ++c)
+#pragma unroll
+                        for (int k = 0; k < TC_BK / 16; ++k) {
+                            const uint64_t ad = ptx::smem_desc_sw128(a0 + c * Cfg::A_CHUNK + k * 32, 16, 1024);
+                            const uint64_t bd = ptx::smem_desc_sw128(b0 + c * Cfg::B_CHUNK + k * 32, 16, 1024);
+                            ptx::mma_bf16_2sm(d, ad, bd, idesc, (it | c | k) != 0);
+                        }
                     ptx::mma_commit_2sm(&empty[stage]);
                     if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -558,49 +601,51 @@ bool tc_conv_supported(const Geom& g, int Cin, int Cout) {
     return get_encode() != nullptr;
 }
 
-template <int BN>
+template <int BN, int KC>
 static hex_status_t launch_fwd_bn(const CUtensorMap& mx0, const CUtensorMap& mx1, const CUtensorMap& mw,
                                   const CUtensorMap& my0, const CUtensorMap& my1, const CUtensorMap& mm0,
                                   const CUtensorMap& mm1, const TcFwdParams& p, cudaStream_t st) {
-    using Cfg = FwdCfg<BN>;
+    using Cfg = FwdCfg<BN, KC>;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(tc_conv_fwd_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(tc_conv_fwd_kernel<BN, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::SMEM) != cudaSuccess)
             return HEX_ERR_CUDA;
         attr_set = true;
     }
     const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
-    tc_conv_fwd_kernel<BN><<<grid, 192, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
+    tc_conv_fwd_kernel<BN, KC><<<grid, 192, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
     count_launch();
     return last_launch_status();
 }
 
-template <int BN>
+template <int BN, int KC>
 static hex_status_t launch_fwd2_bn(const CUtensorMap& mx0, const CUtensorMap& mx1, const CUtensorMap& mw,
                                    const CUtensorMap& my0, const CUtensorMap& my1, const CUtensorMap& mm0,
                                    const CUtensorMap& mm1, const TcFwdParams& p, cudaStream_t st) {
-    using Cfg = Fwd2Cfg<BN>;
+    using Cfg = Fwd2Cfg<BN, KC>;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(tc_conv_fwd2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(tc_conv_fwd2_kernel<BN, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::SMEM) != cudaSuccess)
             return HEX_ERR_CUDA;
         attr_set = true;
     }
     const int pairs = p.pair_tiles < num_sms() / 2 ? p.pair_tiles : num_sms() / 2;
-    tc_conv_fwd2_kernel<BN><<<2 * pairs, 192, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
+    tc_conv_fwd2_kernel<BN, KC><<<2 * pairs, 192, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
     count_launch();
     return last_launch_status();
 }
 
-// The CTA-pair kernel halves the per-SM weight traffic; it pays off when the
-// weight tile is the larger operand (BN = 256).  For BN <= 128 the A operand
-// dominates and the 1-CTA kernel's deeper per-CTA tiles are as fast or faster
-// (round-1 measurements).  HEXCONV_FORCE_2SM / _NO_2SM override.
+// Kernel choice (round-1 measurements).  Each TMA op costs
+// ~150 ns of issue time per SM almost independently of its size, so a K
+// iteration should carry >= ~512 MMA cycles per (A op, B op) pair: K iterations
+// span KC = 2 channel chunks whenever Cin allows, and BN = 256 tiles run as
+// CTA pairs (cta_group::2, M = 256) so each SM loads only half the weight tile.
+// HEXCONV_FORCE_2SM / HEXCONV_NO_2SM / HEXCONV_KC override for experiments.
 static bool use_2sm(int BN) {
     if (getenv("HEXCONV_NO_2SM")) return false;
-    if (getenv("HEXCONV_FORCE_2SM")) return true;
+    if (getenv("HEXCONV_FORCE_2SM")) return BN >= 128;
     return BN == 256;
 }
 
@@ -618,6 +663,9 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     p.n_tiles = a.Cout / BN;
     p.m_total = p.tiles0 + p.rt * p.jt1 * p.bt;
     const bool pair = use_2sm(BN) && p.m_total >= 2;
+    int KC = (a.Cin % 128 == 0 && !(BN == 256 && !pair)) ? 2 : 1;
+    if (getenv("HEXCONV_KC")) KC = atoi(getenv("HEXCONV_KC")) == 2 && a.Cin % 128 == 0 ? 2 : 1;
+    if (BN == 256 && !pair) KC = 1;  // a 1-CTA BN = 256 stage with KC = 2 would not fit twice in smem
     p.total_tiles = p.m_total * p.n_tiles;
     p.pair_tiles = ceil_div(p.m_total, 2) * p.n_tiles;
     p.kblocks = a.Cin / TC_BK;
@@ -632,9 +680,9 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
             p.tap_dr[pc][t] = (int8_t)dr;
         }
     CUtensorMap mx0, mx1, mw;
-    if (!make_view_map(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
-    if (!make_view_map(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
-    if (!make_weight_map(&mw, a.wpack, g.T, a.Cout, a.Cin, pair ? BN / 2 : BN)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, p.RB, p.JB, p.BB, KC)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, p.RB, p.JB, p.BB, KC)) return HEX_ERR_CUDA;
+    if (!make_weight_map4(&mw, a.wpack, g.T, a.Cout, a.Cin, pair ? BN / 2 : BN, KC)) return HEX_ERR_CUDA;
     CUtensorMap my0, my1, mm0, mm1;
     if (!make_view_map(&my0, a.y, g.B, g.H, g.W, a.Cout, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
     if (!make_view_map(&my1, a.y, g.B, g.H, g.W, a.Cout, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
@@ -645,18 +693,17 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
         mm0 = my0;
         mm1 = my1;
     }
+#define HEX_FWD_ARGS mx0, mx1, mw, my0, my1, mm0, mm1, p, st
     if (pair) {
-        switch (BN) {
-            case 256: return launch_fwd2_bn<256>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
-            case 128: return launch_fwd2_bn<128>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
-            default: return launch_fwd2_bn<64>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
-        }
+        if (BN == 256) return KC == 2 ? launch_fwd2_bn<256, 2>(HEX_FWD_ARGS) : launch_fwd2_bn<256, 1>(HEX_FWD_ARGS);
+        return KC == 2 ? launch_fwd2_bn<128, 2>(HEX_FWD_ARGS) : launch_fwd2_bn<128, 1>(HEX_FWD_ARGS);
     }
     switch (BN) {
-        case 256: return launch_fwd_bn<256>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
-        case 128: return launch_fwd_bn<128>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
-        default: return launch_fwd_bn<64>(mx0, mx1, mw, my0, my1, mm0, mm1, p, st);
+        case 256: return launch_fwd_bn<256, 1>(HEX_FWD_ARGS);
+        case 128: return KC == 2 ? launch_fwd_bn<128, 2>(HEX_FWD_ARGS) : launch_fwd_bn<128, 1>(HEX_FWD_ARGS);
+        default: return KC == 2 ? launch_fwd_bn<64, 2>(HEX_FWD_ARGS) : launch_fwd_bn<64, 1>(HEX_FWD_ARGS);
     }
+#undef HEX_FWD_ARGS
 }
 
 // ------------------------------------------------------------------ weight-gradient kernel
@@ -684,7 +731,7 @@ struct TcWgParams {
     int B, H, W, Cin, Cout, T, parity;
     int RB, JB, BB;
     int rt, bt, jt0, jt1, tiles0, ptiles;  // pixel tiles
-    int kchunks, n_atoms, groups, co_tiles, chunks, tiles_per_chunk;
+    int kchunks, cpo, n_atoms, groups, co_tiles, chunks, tiles_per_chunk;  // cpo: chunks per x op
     float* part;     // [chunks][T][Cout][Cin]
     float* db_part;  // [chunks][Cout] or NULL (no bias gradient)
     int dbg;         // development: 1 = skip TMA loads, 2 = skip MMAs (results invalid)
@@ -767,17 +814,15 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
                     continue;
                 }
                 ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
-                const CUtensorMap* mdy = P ? &map_dy1 : &map_dy0;
-                ptx::tma_load_4d(mdy, &full[stage], s, co0, r0, j0, b0);
-                ptx::tma_load_4d(mdy, &full[stage], s + Cfg::BOX, co0 + 64, r0, j0, b0);
-                for (int i = 0; i < na; ++i) {
-                    const int a = a0 + i;
-                    const int t = a / p.kchunks, kc = a - t * p.kchunks;
+                // one op for the two dy channel chunks, one op per tap for all its input-channel chunks
+                ptx::tma_load_5d(P ? &map_dy1 : &map_dy0, &full[stage], s, 0, r0, j0, b0, co0 / 64);
+                for (int i = 0; i < na; i += p.cpo) {
+                    const int t = (a0 + i) / p.kchunks, kc = (a0 + i) - t * p.kchunks;
                     const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
                     const int Pv = (P + dc) & 1;
                     const int jsh = (P + dc - Pv) / 2;
-                    ptx::tma_load_4d(Pv ? &map_x1 : &map_x0, &full[stage], s + (2 + i) * Cfg::BOX, kc * 64,
-                                     r0 + dr, j0 + jsh, b0);
+                    ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], s + (2 + i) * Cfg::BOX, 0, r0 + dr,
+                                     j0 + jsh, b0, kc);
                 }
                 if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
             }
@@ -898,10 +943,10 @@ __global__ void dbias_reduce_kernel(const float* __restrict__ part, int chunks, 
 
 struct WgPlan {
     int RB, JB, BB, rt, bt, jt0, jt1, tiles0, ptiles;
-    int kchunks, n_atoms, groups, co_tiles, chunks, tiles_per_chunk;
+    int kchunks, cpo, n_atoms, groups, co_tiles, chunks, tiles_per_chunk;
 };
 
-static int wg_pix(int Cin) { return Cin == 64 ? 32 : 64; }
+static int wg_pix(int) { return 64; }
 
 static WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
     WgPlan w{};
@@ -913,6 +958,8 @@ static WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
     w.tiles0 = w.rt * w.jt0 * w.bt;
     w.ptiles = w.tiles0 + w.rt * w.jt1 * w.bt;
     w.kchunks = Cin / 64;
+    w.cpo = 1;  // largest power of two dividing kchunks and the 8-atom group
+    while (w.cpo < 8 && w.kchunks % (2 * w.cpo) == 0) w.cpo *= 2;
     w.n_atoms = g.T * w.kchunks;
     w.groups = ceil_div(w.n_atoms, WG_ATOMS);
     w.co_tiles = Cout / 128;
@@ -959,7 +1006,7 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
     p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
     p.RB = w.RB; p.JB = w.JB; p.BB = w.BB; p.rt = w.rt; p.bt = w.bt; p.jt0 = w.jt0; p.jt1 = w.jt1;
     p.tiles0 = w.tiles0; p.ptiles = w.ptiles;
-    p.kchunks = w.kchunks; p.n_atoms = w.n_atoms; p.groups = w.groups; p.co_tiles = w.co_tiles;
+    p.kchunks = w.kchunks; p.cpo = w.cpo; p.n_atoms = w.n_atoms; p.groups = w.groups; p.co_tiles = w.co_tiles;
     p.chunks = w.chunks; p.tiles_per_chunk = w.tiles_per_chunk;
     p.part = (float*)ws;
     p.db_part = a.dbias ? (float*)ws + (size_t)w.chunks * g.T * a.Cout * a.Cin : nullptr;
@@ -972,10 +1019,10 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
             p.tap_dr[pc][t] = (int8_t)dr;
         }
     CUtensorMap mx0, mx1, md0, md1;
-    if (!make_view_map(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
-    if (!make_view_map(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
-    if (!make_view_map(&md0, a.dy, g.B, g.H, g.W, a.Cout, 0, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
-    if (!make_view_map(&md1, a.dy, g.B, g.H, g.W, a.Cout, 1, w.RB, w.JB, w.BB)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, w.RB, w.JB, w.BB, w.cpo)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, w.RB, w.JB, w.BB, w.cpo)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&md0, a.dy, g.B, g.H, g.W, a.Cout, 0, w.RB, w.JB, w.BB, 2)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&md1, a.dy, g.B, g.H, g.W, a.Cout, 1, w.RB, w.JB, w.BB, 2)) return HEX_ERR_CUDA;
     const int units = w.co_tiles * w.groups * w.chunks;
     if (wg_pix(a.Cin) == 32) {
         if (launch_wgrad_pix<32>(mx0, mx1, md0, md1, p, units, st) != HEX_OK) return HEX_ERR_CUDA;
