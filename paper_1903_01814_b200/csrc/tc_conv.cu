@@ -915,6 +915,184 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
     }
 }
 
+
+// ------------------------------------------------------------------ 2-CTA weight-gradient kernel
+// For Cout % 256 == 0 and Cin % 128 == 0.  A CTA pair owns 256 output channels
+// (M = 256, each CTA 128) and a group of up to 8 atoms; per 16 pixels the leader
+// issues up to two tcgen05.mma.cta_group::2 (M = 256, N = 64 q, q <= 4 atoms),
+// each CTA supplying q/2 atoms of B.  Per CTA and 64-pixel stage: one dy op
+// (its 128 channels) + one x op per MMA (2 chunks of one tap) = 48 KB, four
+// stages deep.  Atom 4m + j accumulates in TMEM columns 256 m + 64 j.
+struct Wg2Cfg {
+    static constexpr int PIX = 64;
+    static constexpr int BOX = PIX * 128;          // 8 KB per 64-channel box
+    static constexpr int STAGE_BYTES = 6 * BOX;    // dy (2 boxes) + x (2 ops x 2 boxes)
+    static constexpr int STAGES = 4;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 128;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+tc_conv_wgrad2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
+                      const __grid_constant__ CUtensorMap map_dy0, const __grid_constant__ CUtensorMap map_dy1,
+                      const __grid_constant__ TcWgParams p) {
+    using Cfg = Wg2Cfg;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* dbr = empty + Cfg::STAGES;  // per stage: MMAs done (multicast) -> dy tile readable for dbias
+    uint64_t* tfull = dbr + Cfg::STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    int u = blockIdx.x / 2;
+    const int chunk = u % p.chunks; u /= p.chunks;
+    const int grp = u % p.groups;
+    const int cop = u / p.groups;
+    const int a0 = grp * WG_ATOMS;
+    const int na = min(WG_ATOMS, p.n_atoms - a0);  // even
+    const int q0 = min(na, 4), q1 = na - q0;       // atoms of MMA 0 / MMA 1
+    const int co0 = cop * 256 + 128 * (int)rank;    // this CTA's channels
+    const int pt_begin = chunk * p.tiles_per_chunk;
+    const int pt_end = min(p.ptiles, pt_begin + p.tiles_per_chunk);
+    const bool do_db = p.db_part != nullptr && grp == 0;
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < Cfg::STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], do_db ? 5 : 1);
+            ptx::mbar_init(&dbr[s], 1);
+        }
+        ptx::mbar_init(tfull, 1);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&map_x0);
+        ptx::prefetch_tmap(&map_x1);
+        ptx::prefetch_tmap(&map_dy0);
+        ptx::prefetch_tmap(&map_dy1);
+    }
+    if (warp == 1) ptx::tmem_alloc_2sm(tmem_slot, 512);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t stage_bytes = (2 + (q1 > 0 ? 4 : 2)) * Cfg::BOX;  // per CTA
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int pt = pt_begin; pt < pt_end; ++pt) {
+                int P, r0, j0, b0;
+                decode_ptile(p, pt, &P, &r0, &j0, &b0);
+                const int pc = (P + p.parity) & 1;
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* s = smem + stage * Cfg::STAGE_BYTES;
+                if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
+                ptx::tma_load_5d_2sm(P ? &map_dy1 : &map_dy0, &full[stage], s, 0, r0, j0, b0, co0 / 64);
+                for (int m = 0; m < 2; ++m) {
+                    const int q = m ? q1 : q0;
+                    if (q == 0) break;
+                    const int a = a0 + 4 * m + (int)rank * (q / 2);
+                    const int t = a / p.kchunks, kc = a - t * p.kchunks;
+                    const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
+                    const int Pv = (P + dc) & 1;
+                    const int jsh = (P + dc - Pv) / 2;
+                    ptx::tma_load_5d_2sm(Pv ? &map_x1 : &map_x0, &full[stage], s + (2 + 2 * m) * Cfg::BOX, 0, r0 + dr,
+                                         j0 + jsh, b0, kc);
+                }
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            const uint32_t idesc0 = ptx::idesc_bf16(256, 64 * q0, 1, 1);
+            const uint32_t idesc1 = ptx::idesc_bf16(256, 64 * (q1 > 0 ? q1 : 2), 1, 1);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int pt = pt_begin; pt < pt_end; ++pt) {
+                ptx::mbar_wait(&full[stage], phase);
+                ptx::tc_fence_after();
+                const uint32_t s = ptx::smem_u32(smem + stage * Cfg::STAGE_BYTES);
+#pragma unroll
+                for (int k = 0; k < Cfg::PIX / 16; ++k) {
+                    const uint64_t ad = ptx::smem_desc_sw128(s + k * 2048, Cfg::BOX, 1024);
+                    const uint32_t acc = (pt != pt_begin) || (k != 0);
+                    ptx::mma_bf16_2sm(tmem_base, ad,
+                                      ptx::smem_desc_sw128(s + 2 * Cfg::BOX + k * 2048, Cfg::BOX, 1024), idesc0, acc);
+                    if (q1 > 0)
+                        ptx::mma_bf16_2sm(tmem_base + 256, ad,
+                                          ptx::smem_desc_sw128(s + 4 * Cfg::BOX + k * 2048, Cfg::BOX, 1024), idesc1,
+                                          acc);
+                }
+                ptx::mma_commit_2sm(&empty[stage]);
+                if (do_db) ptx::mma_commit_2sm(&dbr[stage]);
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+            }
+            ptx::mma_commit_2sm(tfull);
+        }
+    } else {
+        const int q = warp & 3;
+        const int row = q * 32 + lane;  // channel within this CTA's 128
+        if (do_db) {
+            const int box = row >> 6, e = row & 63, j = e >> 3, sub = e & 7;
+            float dsum = 0.f;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int pt = pt_begin; pt < pt_end; ++pt) {
+                ptx::mbar_wait(&dbr[stage], phase);  // both CTAs' tiles were consumed by the MMAs
+                const uint8_t* sdy = smem + stage * Cfg::STAGE_BYTES + box * Cfg::BOX;
+#pragma unroll 8
+                for (int px = 0; px < Cfg::PIX; ++px) {
+                    const __nv_bfloat16 v =
+                        *reinterpret_cast<const __nv_bfloat16*>(sdy + px * 128 + ((j ^ (px & 7)) << 4) + sub * 2);
+                    dsum += __bfloat162float(v);
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+            }
+            p.db_part[(int64_t)chunk * p.Cout + co0 + row] = dsum;
+        }
+        ptx::mbar_wait(tfull, 0);
+        ptx::tc_fence_after();
+        const int co = co0 + row;
+        const bool empty_chunk = pt_end <= pt_begin;
+        for (int m = 0; m < 2; ++m) {
+            const int qm = m ? q1 : q0;
+            for (int jj = 0; jj < qm; ++jj) {
+                const int a = a0 + 4 * m + jj;
+                const int t = a / p.kchunks, kc = a - t * p.kchunks;
+                float* dst = p.part + (((int64_t)chunk * p.T + t) * p.Cout + co) * p.Cin + kc * 64;
+#pragma unroll 1
+                for (int ch = 0; ch < 2; ++ch) {
+                    uint32_t v[32];
+                    ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + 256 * m + 64 * jj + ch * 32, v);
+                    ptx::tmem_ld_wait();
+                    float4* d4 = reinterpret_cast<float4*>(dst + ch * 32);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        float4 f;
+                        f.x = empty_chunk ? 0.f : __uint_as_float(v[4 * i]);
+                        f.y = empty_chunk ? 0.f : __uint_as_float(v[4 * i + 1]);
+                        f.z = empty_chunk ? 0.f : __uint_as_float(v[4 * i + 2]);
+                        f.w = empty_chunk ? 0.f : __uint_as_float(v[4 * i + 3]);
+                        d4[i] = f;
+                    }
+                }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_2sm(tmem_base, 512);
+    }
+}
+
 // dw[co][ci][t] (+)= sum_chunk part[chunk][t][co][ci]   (fixed chunk order)
 __global__ void wgrad_tc_reduce_kernel(const float* __restrict__ part, int chunks, int T, int Cout, int Cin,
                                        float* __restrict__ dw, int accumulate) {
@@ -944,7 +1122,13 @@ __global__ void dbias_reduce_kernel(const float* __restrict__ part, int chunks, 
 struct WgPlan {
     int RB, JB, BB, rt, bt, jt0, jt1, tiles0, ptiles;
     int kchunks, cpo, n_atoms, groups, co_tiles, chunks, tiles_per_chunk;
+    bool pair;  // 2-CTA kernel (co_tiles then counts 256-channel pairs)
 };
+
+static bool wg_use_pair(int Cin, int Cout) {
+    if (getenv("HEXCONV_NO_2SM")) return false;
+    return Cout % 256 == 0 && Cin % 128 == 0;
+}
 
 static int wg_pix(int) { return 64; }
 
@@ -962,9 +1146,12 @@ static WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
     while (w.cpo < 8 && w.kchunks % (2 * w.cpo) == 0) w.cpo *= 2;
     w.n_atoms = g.T * w.kchunks;
     w.groups = ceil_div(w.n_atoms, WG_ATOMS);
-    w.co_tiles = Cout / 128;
+    w.pair = wg_use_pair(Cin, Cout);
+    w.co_tiles = w.pair ? Cout / 256 : Cout / 128;
     const int base_units = w.co_tiles * w.groups;
-    int chunks = ceil_div(2 * 148, base_units);
+    // whole waves: the largest chunk count with base_units * chunks <= 2 x 148 SMs (one CTA per SM,
+    // a pair unit takes two).  A fixed SM count keeps the split-K summation order identical on every B200.
+    int chunks = (w.pair ? 148 : 2 * 148) / base_units;
     if (chunks > w.ptiles) chunks = w.ptiles;
     if (chunks < 1) chunks = 1;
     w.tiles_per_chunk = ceil_div(w.ptiles, chunks);
@@ -1019,12 +1206,22 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
             p.tap_dr[pc][t] = (int8_t)dr;
         }
     CUtensorMap mx0, mx1, md0, md1;
-    if (!make_view_map5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, w.RB, w.JB, w.BB, w.cpo)) return HEX_ERR_CUDA;
-    if (!make_view_map5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, w.RB, w.JB, w.BB, w.cpo)) return HEX_ERR_CUDA;
+    const int xbox = w.pair ? 2 : w.cpo;
+    if (!make_view_map5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, w.RB, w.JB, w.BB, xbox)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, w.RB, w.JB, w.BB, xbox)) return HEX_ERR_CUDA;
     if (!make_view_map5(&md0, a.dy, g.B, g.H, g.W, a.Cout, 0, w.RB, w.JB, w.BB, 2)) return HEX_ERR_CUDA;
     if (!make_view_map5(&md1, a.dy, g.B, g.H, g.W, a.Cout, 1, w.RB, w.JB, w.BB, 2)) return HEX_ERR_CUDA;
     const int units = w.co_tiles * w.groups * w.chunks;
-    if (wg_pix(a.Cin) == 32) {
+    if (w.pair) {
+        static bool attr2 = false;
+        if (!attr2) {
+            if (cudaFuncSetAttribute(tc_conv_wgrad2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Wg2Cfg::SMEM) != cudaSuccess)
+                return HEX_ERR_CUDA;
+            attr2 = true;
+        }
+        tc_conv_wgrad2_kernel<<<2 * units, 192, Wg2Cfg::SMEM, st>>>(mx0, mx1, md0, md1, p);
+    } else if (wg_pix(a.Cin) == 32) {
         if (launch_wgrad_pix<32>(mx0, mx1, md0, md1, p, units, st) != HEX_OK) return HEX_ERR_CUDA;
     } else {
         if (launch_wgrad_pix<64>(mx0, mx1, md0, md1, p, units, st) != HEX_OK) return HEX_ERR_CUDA;
