@@ -28,6 +28,13 @@ def main():
             F.conv2d_bwd_weight(x, g, n=n, layout="NHWC")
         elif op == "poolf":
             F.pool2d_fwd(x, 1, 2, 0, "max", "NHWC")
+        elif op == "l1fwd":
+            x1 = torch.randn(B, H, W, 1, device="cuda").to(torch.bfloat16)
+            w1 = (torch.randn(Co, 1, T, device="cuda") / T ** 0.5).to(torch.bfloat16)
+            F.conv2d_fwd(x1, w1, None, n=n, layout="NHWC")
+        elif op == "l1wgrad":
+            x1 = torch.randn(B, H, W, 1, device="cuda").to(torch.bfloat16)
+            F.conv2d_bwd_weight(x1, g, n=n, layout="NHWC")
         elif op == "poolb":
             y, am = F.pool2d_fwd(x, 1, 2, 0, "max", "NHWC")
             F.pool2d_bwd(torch.randn_like(y), am, (H, W), 1, 2, 0, "max", "NHWC")
