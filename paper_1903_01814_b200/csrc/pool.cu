@@ -411,8 +411,225 @@ static void launch_spec_bwd(const PoolArgs& a, cudaStream_t st) {
                                                       a.g, C8, a.mode);
 }
 
+
+// ---------------------------------------------------------------------------
+// Wide NHWC bf16 kernels: each thread owns V x 8 channels of one pixel, so the
+// per-pixel index math is shared by 8V channels.  Max pooling compares packed
+// bf16x2 pairs (__hgt2_mask, strict '>' keeps the first maximum) and keeps the
+// tap index as packed bytes; the backward selects the routed channels with
+// SIMD byte compares (__vcmpeq4) and byte-permuted masks.  Exactly the same
+// results as the scalar kernels (max: a copy of the selected input; avg and
+// backward: fp32 accumulation in canonical tap order).
+// ---------------------------------------------------------------------------
+template <int N, int S, int V>
+__global__ void __launch_bounds__(256)
+pool_fwd_nhwc_v(const uint4* __restrict__ x, uint4* __restrict__ y, uint2* __restrict__ am, Geom g, int CV,
+                int mode) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int per_img = g.Ho * g.Wo * CV;
+    if (idx >= per_img) return;
+    const int b = blockIdx.y;
+    const int cv = idx % CV;
+    const int o = idx / CV;
+    const int R = o / g.Wo, C = o - R * g.Wo;
+    const int c = S * C;
+    const int r = ((S * C + g.parity) >> 1) % S + S * R;
+    const int p = (c + g.parity) & 1;
+    const int C8 = CV * V;
+    const uint4* xp = x + (size_t)b * g.H * g.W * C8 + cv * V;
+    uint32_t best[4 * V], ix[4 * V];
+    float sum[8 * V];
+#pragma unroll
+    for (int i = 0; i < 4 * V; ++i) { best[i] = 0u; ix[i] = 0u; }
+#pragma unroll
+    for (int i = 0; i < 8 * V; ++i) sum[i] = 0.f;
+    int t = 0, cnt = 0;
+#pragma unroll
+    for (int dc = -N; dc <= N; ++dc) {
+        const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
+        const int cc = c + dc;
+        const bool colok = cc >= 0 && cc < g.W;
+        const int top = r - N + (((dc < 0 ? -dc : dc) + p) >> 1);
+#pragma unroll
+        for (int k = 0; k < len; ++k, ++t) {
+            const int rr = top + k;
+            if (!colok || rr < 0 || rr >= g.H) continue;
+            const uint4* src = xp + (size_t)(rr * g.W + cc) * C8;
+            const uint32_t tt = (uint32_t)t * 0x0101u;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const uint4 q = __ldg(src + v);
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const int i = 4 * v + kk;
+                    if (mode == HEX_POOL_MAX) {
+                        if (cnt == 0) {
+                            best[i] = w[kk];
+                            ix[i] = tt;
+                        } else {
+                            const unsigned m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&w[kk]),
+                                                           *reinterpret_cast<const __nv_bfloat162*>(&best[i]));
+                            best[i] = (w[kk] & m) | (best[i] & ~m);
+                            const uint32_t bm = __byte_perm(m, 0u, 0x4420);
+                            ix[i] = (tt & bm) | (ix[i] & ~bm);
+                        }
+                    } else {
+                        sum[2 * i] += __uint_as_float(w[kk] << 16);
+                        sum[2 * i + 1] += __uint_as_float(w[kk] & 0xffff0000u);
+                    }
+                }
+            }
+            ++cnt;
+        }
+    }
+    const size_t yo = ((size_t)b * g.Ho * g.Wo + o) * C8 + cv * V;
+    if (mode == HEX_POOL_MAX) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            y[yo + v] = make_uint4(best[4 * v], best[4 * v + 1], best[4 * v + 2], best[4 * v + 3]);
+            if (am) am[yo + v] = make_uint2(ix[4 * v] | (ix[4 * v + 1] << 16), ix[4 * v + 2] | (ix[4 * v + 3] << 16));
+        }
+    } else {
+        const float inv = 1.f / (float)cnt;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int i = 4 * v + kk;
+                __nv_bfloat162 h = __floats2bfloat162_rn(sum[2 * i] * inv, sum[2 * i + 1] * inv);
+                pk[kk] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            y[yo + v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+    }
+}
+
+template <int N, int S, int V>
+__global__ void __launch_bounds__(256)
+pool_bwd_nhwc_v(const uint4* __restrict__ dy, const uint2* __restrict__ am, uint4* __restrict__ dx, Geom g, int CV,
+                int mode) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int per_img = g.H * g.W * CV;
+    if (idx >= per_img) return;
+    const int b = blockIdx.y;
+    const int cv = idx % CV;
+    const int q = idx / CV;
+    const int r = q / g.W, c = q - r * g.W;
+    const int C8 = CV * V;
+    float acc[8 * V];
+#pragma unroll
+    for (int i = 0; i < 8 * V; ++i) acc[i] = 0.f;
+    const size_t ybase = (size_t)b * g.Ho * g.Wo * C8 + cv * V;
+    int t = 0;
+#pragma unroll
+    for (int dc = -N; dc <= N; ++dc) {
+        const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
+        const int oc = c - dc;
+        const bool colok = oc >= 0 && (oc % S) == 0 && oc / S < g.Wo;
+        const int Cq = oc / S;
+        const int po = (oc + g.parity) & 1;
+        const int rho = ((S * Cq + g.parity) >> 1) % S;
+        const int top = -N + (((dc < 0 ? -dc : dc) + po) >> 1);
+#pragma unroll
+        for (int k = 0; k < len; ++k, ++t) {
+            if (!colok) continue;
+            const int d = r - (top + k) - rho;
+            if (d < 0 || (d % S) != 0) continue;
+            const int Rq = d / S;
+            if (Rq >= g.Ho) continue;
+            const size_t yo = ybase + (size_t)(Rq * g.Wo + Cq) * C8;
+            float inv = 1.f;
+            if (mode != HEX_POOL_MAX) {
+                const int orow = rho + S * Rq;
+                int cntv = 0;
+#pragma unroll
+                for (int e = -N; e <= N; ++e) {
+                    const int ccol = oc + e;
+                    if (ccol < 0 || ccol >= g.W) continue;
+                    const int l2 = 2 * N + 1 - (e < 0 ? -e : e);
+                    const int tp = orow - N + (((e < 0 ? -e : e) + po) >> 1);
+                    cntv += max(min(tp + l2, g.H) - max(tp, 0), 0);
+                }
+                inv = 1.f / (float)cntv;
+            }
+            const uint32_t tt4 = (uint32_t)t * 0x01010101u;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const uint4 dq = __ldg(dy + yo + v);
+                uint32_t w[4] = {dq.x, dq.y, dq.z, dq.w};
+                if (mode == HEX_POOL_MAX) {
+                    const uint2 a = __ldg(am + yo + v);
+                    const uint32_t mlo = __vcmpeq4(a.x, tt4), mhi = __vcmpeq4(a.y, tt4);
+                    w[0] &= __byte_perm(mlo, 0u, 0x1100);
+                    w[1] &= __byte_perm(mlo, 0u, 0x3322);
+                    w[2] &= __byte_perm(mhi, 0u, 0x1100);
+                    w[3] &= __byte_perm(mhi, 0u, 0x3322);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        acc[8 * v + 2 * kk] += __uint_as_float(w[kk] << 16);
+                        acc[8 * v + 2 * kk + 1] += __uint_as_float(w[kk] & 0xffff0000u);
+                    }
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        acc[8 * v + 2 * kk] += __uint_as_float(w[kk] << 16) * inv;
+                        acc[8 * v + 2 * kk + 1] += __uint_as_float(w[kk] & 0xffff0000u) * inv;
+                    }
+                }
+            }
+        }
+    }
+    uint4* out = dx + (size_t)b * per_img * V + (size_t)q * C8 + cv * V;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(acc[8 * v + 2 * kk], acc[8 * v + 2 * kk + 1]);
+            pk[kk] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        out[v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+}
+
+static int pick_v(const PoolArgs& a) { return a.C % 32 == 0 ? 4 : (a.C % 16 == 0 ? 2 : 1); }
+
+template <int N, int S, int V>
+static void launch_v_fwd(const PoolArgs& a, cudaStream_t st) {
+    const int CV = a.C / (8 * V);
+    dim3 grid(ceil_div((int64_t)a.g.Ho * a.g.Wo * CV, 256), a.g.B);
+    pool_fwd_nhwc_v<N, S, V><<<grid, 256, 0, st>>>((const uint4*)a.x, (uint4*)a.y, (uint2*)a.argmax, a.g, CV, a.mode);
+}
+template <int N, int S, int V>
+static void launch_v_bwd(const PoolArgs& a, cudaStream_t st) {
+    const int CV = a.C / (8 * V);
+    dim3 grid(ceil_div((int64_t)a.g.H * a.g.W * CV, 256), a.g.B);
+    pool_bwd_nhwc_v<N, S, V><<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in, (uint4*)a.dx, a.g,
+                                                   CV, a.mode);
+}
+template <int V>
+static void dispatch_v(const PoolArgs& a, cudaStream_t st, bool fwd) {
+    if (a.g.n == 1) {
+        if (a.g.s == 1) { fwd ? launch_v_fwd<1, 1, V>(a, st) : launch_v_bwd<1, 1, V>(a, st); }
+        else { fwd ? launch_v_fwd<1, 2, V>(a, st) : launch_v_bwd<1, 2, V>(a, st); }
+    } else {
+        if (a.g.s == 1) { fwd ? launch_v_fwd<2, 1, V>(a, st) : launch_v_bwd<2, 1, V>(a, st); }
+        else { fwd ? launch_v_fwd<2, 2, V>(a, st) : launch_v_bwd<2, 2, V>(a, st); }
+    }
+}
+static bool dispatch_wide(const PoolArgs& a, cudaStream_t st, bool fwd) {
+    const int V = pick_v(a);
+    if (V == 1) return false;
+    if (V == 4) dispatch_v<4>(a, st, fwd);
+    else dispatch_v<2>(a, st, fwd);
+    return true;
+}
+
 hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
-    if (use_spec(a)) {
+    if (use_spec(a) && dispatch_wide(a, st, true)) {
+    } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_fwd<1, 1>(a, st); else launch_spec_fwd<1, 2>(a, st); }
         else { if (a.g.s == 1) launch_spec_fwd<2, 1>(a, st); else launch_spec_fwd<2, 2>(a, st); }
     } else if (use_vec8(a)) {
@@ -435,7 +652,8 @@ hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
 }
 
 hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
-    if (use_spec(a)) {
+    if (use_spec(a) && dispatch_wide(a, st, false)) {
+    } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_bwd<1, 1>(a, st); else launch_spec_bwd<1, 2>(a, st); }
         else { if (a.g.s == 1) launch_spec_bwd<2, 1>(a, st); else launch_spec_bwd<2, 2>(a, st); }
     } else if (use_vec8(a)) {

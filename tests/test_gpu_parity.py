@@ -188,8 +188,8 @@ def test_pool_envelope(F, oracle, mode, pi):
 
 @pytest.mark.parametrize("mode", ["max", "avg"])
 def test_pool_bf16_nhwc_vectorised(F, oracle, mode):
-    for pi, n, s in [(0, 1, 2), (1, 1, 1), (0, 2, 3)]:
-        for C in (8, 16, 3):
+    for pi, n, s in [(0, 1, 2), (1, 1, 1), (0, 2, 3), (1, 2, 2)]:
+        for C in (8, 16, 3, 32, 96):
             _pool_case(F, oracle, pi, n, s, 12, 13, 2, C, torch.bfloat16, "NHWC", mode, 300 + C)
 
 
