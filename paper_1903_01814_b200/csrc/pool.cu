@@ -11,6 +11,8 @@
 // channels per thread; everything else one element per thread.  The backward
 // pass is a gather over the candidate centres of each input pixel (no
 // atomics, deterministic).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "geometry.cuh"
 #include "kernels.h"
@@ -436,7 +438,7 @@ pool_fwd_nhwc_v(const uint4* __restrict__ x, uint4* __restrict__ y, uint2* __res
     const int r = ((S * C + g.parity) >> 1) % S + S * R;
     const int p = (c + g.parity) & 1;
     const int C8 = CV * V;
-    const uint4* xp = x + (size_t)b * g.H * g.W * C8 + cv;  // groups cv, cv + CV, ... (coalesced)
+    const uint4* xp = x + (size_t)b * g.H * g.W * C8 + cv * V;
     uint32_t best[4 * V], ix[4 * V];
     float sum[8 * V];
 #pragma unroll
@@ -458,7 +460,7 @@ pool_fwd_nhwc_v(const uint4* __restrict__ x, uint4* __restrict__ y, uint2* __res
             const uint32_t tt = (uint32_t)t * 0x0101u;
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-                const uint4 q = __ldg(src + v * CV);
+                const uint4 q = __ldg(src + v);
                 const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
@@ -483,12 +485,12 @@ pool_fwd_nhwc_v(const uint4* __restrict__ x, uint4* __restrict__ y, uint2* __res
             ++cnt;
         }
     }
-    const size_t yo = ((size_t)b * g.Ho * g.Wo + o) * C8 + cv;
+    const size_t yo = ((size_t)b * g.Ho * g.Wo + o) * C8 + cv * V;
     if (mode == HEX_POOL_MAX) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            y[yo + v * CV] = make_uint4(best[4 * v], best[4 * v + 1], best[4 * v + 2], best[4 * v + 3]);
-            if (am) am[yo + v * CV] = make_uint2(ix[4 * v] | (ix[4 * v + 1] << 16), ix[4 * v + 2] | (ix[4 * v + 3] << 16));
+            y[yo + v] = make_uint4(best[4 * v], best[4 * v + 1], best[4 * v + 2], best[4 * v + 3]);
+            if (am) am[yo + v] = make_uint2(ix[4 * v] | (ix[4 * v + 1] << 16), ix[4 * v + 2] | (ix[4 * v + 3] << 16));
         }
     } else {
         const float inv = 1.f / (float)cnt;
@@ -501,7 +503,7 @@ pool_fwd_nhwc_v(const uint4* __restrict__ x, uint4* __restrict__ y, uint2* __res
                 __nv_bfloat162 h = __floats2bfloat162_rn(sum[2 * i] * inv, sum[2 * i + 1] * inv);
                 pk[kk] = *reinterpret_cast<uint32_t*>(&h);
             }
-            y[yo + v * CV] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            y[yo + v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
     }
 }
@@ -521,7 +523,7 @@ pool_bwd_nhwc_v(const uint4* __restrict__ dy, const uint2* __restrict__ am, uint
     float acc[8 * V];
 #pragma unroll
     for (int i = 0; i < 8 * V; ++i) acc[i] = 0.f;
-    const size_t ybase = (size_t)b * g.Ho * g.Wo * C8 + cv;
+    const size_t ybase = (size_t)b * g.Ho * g.Wo * C8 + cv * V;
     int t = 0;
 #pragma unroll
     for (int dc = -N; dc <= N; ++dc) {
@@ -557,10 +559,10 @@ pool_bwd_nhwc_v(const uint4* __restrict__ dy, const uint2* __restrict__ am, uint
             const uint32_t tt4 = (uint32_t)t * 0x01010101u;
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-                const uint4 dq = __ldg(dy + yo + v * CV);
+                const uint4 dq = __ldg(dy + yo + v);
                 uint32_t w[4] = {dq.x, dq.y, dq.z, dq.w};
                 if (mode == HEX_POOL_MAX) {
-                    const uint2 a = __ldg(am + yo + v * CV);
+                    const uint2 a = __ldg(am + yo + v);
                     const uint32_t mlo = __vcmpeq4(a.x, tt4), mhi = __vcmpeq4(a.y, tt4);
                     w[0] &= __byte_perm(mlo, 0u, 0x1100);
                     w[1] &= __byte_perm(mlo, 0u, 0x3322);
@@ -581,7 +583,7 @@ pool_bwd_nhwc_v(const uint4* __restrict__ dy, const uint2* __restrict__ am, uint
             }
         }
     }
-    uint4* out = dx + (size_t)b * per_img * V + (size_t)q * C8 + cv;
+    uint4* out = dx + (size_t)b * per_img * V + (size_t)q * C8 + cv * V;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
         uint32_t pk[4];
@@ -590,7 +592,7 @@ pool_bwd_nhwc_v(const uint4* __restrict__ dy, const uint2* __restrict__ am, uint
             __nv_bfloat162 h = __floats2bfloat162_rn(acc[8 * v + 2 * kk], acc[8 * v + 2 * kk + 1]);
             pk[kk] = *reinterpret_cast<uint32_t*>(&h);
         }
-        out[v * CV] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        out[v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
 }
 
@@ -652,7 +654,9 @@ hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
 }
 
 hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
-    if (use_spec(a) && dispatch_wide(a, st, false)) {
+    // The 8-channel gather measured faster than the wide variant for the backward
+    // (round 1: 519 vs 577 us on config-5 pool 1); HEXCONV_POOL_WIDE_BWD selects it.
+    if (use_spec(a) && getenv("HEXCONV_POOL_WIDE_BWD") && dispatch_wide(a, st, false)) {
     } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_bwd<1, 1>(a, st); else launch_spec_bwd<1, 2>(a, st); }
         else { if (a.g.s == 1) launch_spec_bwd<2, 1>(a, st); else launch_spec_bwd<2, 2>(a, st); }
