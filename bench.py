@@ -267,23 +267,49 @@ def main():
     events = model.timer
     model.timer = None
 
-    # roofline: tcgen05 implicit-GEMM conv kernel family (fwd + dgrad of L2..L6)
+    # per kernel family, from CUDA events recorded around every call inside the timed region
     flops_img, per_layer = model.flops_per_image()
-    tc_ms = 0.0
-    tc_flops = 0.0
-    tc_launches = 0
+    fam = {}  # name -> [ms, algorithmic units, unit, launches]
+
+    def add(name, ms_, units, unit):
+        f = fam.setdefault(name, [0.0, 0.0, unit, 0])
+        f[0] += ms_
+        f[1] += units
+        f[3] += 1
+
     share = {}
     for kind, l, e0, e1 in events:
         dt = e0.elapsed_time(e1)
         share[kind] = share.get(kind, 0.0) + dt
-        if l > 0 and kind in ("fwd", "dgrad"):
-            tc_ms += dt
-            tc_flops += per_layer[l][0] * B
-            tc_launches += 1
+        if kind in ("fwd", "dgrad", "wgrad"):
+            fl = per_layer[l][0] * B
+            if l == 0:
+                add("stencil_cin1 (layer 1 fwd+wgrad, CUDA cores)", dt, fl, "TFLOP/s")
+            elif kind == "wgrad":
+                add("tc_conv_wgrad (tcgen05, layers 2-6)", dt, fl, "TFLOP/s")
+            else:
+                add("tc_conv_fwd (tcgen05 fwd + bwd-data, layers 2-6)", dt, fl, "TFLOP/s")
+        else:
+            add("pool (max n1 s2 fwd + bwd)", dt, model.pool_bytes(l, kind), "GB/s")
     peaks, peak_src = load_peaks()
     peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    achieved = tc_flops / (tc_ms / 1e3) / 1e12 if tc_ms > 0 else None
+    peak_gbs = peaks["hbm_gbs"]
+    kernels = {}
+    for name, (fms, units, unit, n) in fam.items():
+        ach = units / (fms / 1e3) / (1e12 if unit == "TFLOP/s" else 1e9)
+        pk = peak_gbs if unit == "GB/s" else (74.4 if "CUDA cores" in name else peak_tf)
+        kernels[name] = {"ms_per_step": fms / args.steps, "achieved": ach, "unit": unit, "peak": pk,
+                         "frac": ach / pk, "launches_per_step": n / args.steps}
+    dom = max(fam, key=lambda k: fam[k][0])
+    tc_name = "tc_conv_fwd (tcgen05 fwd + bwd-data, layers 2-6)"
+    achieved = kernels[tc_name]["achieved"]
     total_tf = flops_img * B / (ms_step / 1e3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "tc_conv_fwd_traffic.json")) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    except Exception:
+        pass
 
     # ---- end-to-end through the public API with host buffers
     pin_x = [torch.from_numpy(a.astype(np.float32)).to(torch.bfloat16).pin_memory() for a in xs_np]
@@ -326,12 +352,14 @@ def main():
             "config": {"workload": WORKLOAD, "global_batch": B * world, "per_gpu_batch": B, "grid": "96x96",
                        "parallelism": f"dp{world}", "l2": "working set > L2 (activations ~2.5 GB/step)"},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
-            "roofline": {"bound": "tensor", "kernel": "tc_conv_fwd_kernel (tcgen05 implicit-GEMM hex conv; "
-                                                      "fwd + bwd-data of L2-L6)",
+            "roofline": {"bound": "tensor", "kernel": "tc_conv_fwd_kernel / tc_conv_fwd2_kernel (tcgen05 "
+                                                      "implicit-GEMM hex conv; fwd + bwd-data of layers 2-6)",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": (achieved / peak_tf) if achieved else None, "traffic": None,
+                         "frac": achieved / peak_tf, "traffic": traffic,
                          "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
-                         "launches_per_step": tc_launches // max(args.steps, 1)},
+                         "launches_per_step": kernels[tc_name]["launches_per_step"],
+                         "dominant_by_time": dom == tc_name},
+            "kernels": kernels,
             "step_tflops": total_tf,
             "step_share_ms": {k: v / args.steps for k, v in share.items()},
             "cpu_baseline": cpu,

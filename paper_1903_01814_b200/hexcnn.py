@@ -200,8 +200,10 @@ class HexCNN:
                                      _p(self.act[l]), _p(ws), self.ws_sizes[l][0], stream), f"conv{l + 1} fwd")
             self._toc("fwd", l, e0)
             if l in self.pool_geo:
+                e0 = self._tic()
                 A.check(L.hex_pool2d_fwd(ctypes.byref(self.pdesc[l]), _p(self.act[l]), _p(self.pooled[l]),
                                          _p(self.argmax[l]), stream), f"pool{l + 1} fwd")
+                self._toc("pool_fwd", l, e0)
 
     def backward(self, x, labels, stream, hooks=None):
         """Head + backward of every layer.  `hooks(l)` is called after layer l's
@@ -235,8 +237,10 @@ class HexCNN:
                                               _p(self.pooled[prev]), _p(self.dpool[prev]), _p(self.ws[l][1]),
                                               self.ws_sizes[l][1], stream), f"conv{l + 1} dgrad")
                 self._toc("dgrad", l, e0)
+                e0 = self._tic()
                 A.check(L.hex_pool2d_bwd(ctypes.byref(self.pdesc[prev]), _p(self.dpool[prev]),
                                          _p(self.argmax[prev]), _p(self.dact[prev]), stream), f"pool{prev + 1} bwd")
+                self._toc("pool_bwd", prev, e0)
             else:
                 A.check(L.hex_conv2d_bwd_data(ctypes.byref(self.desc[l]), _p(dy), _p(self.weight(l)),
                                               _p(self.act[prev]), _p(self.dact[prev]), _p(self.ws[l][1]),
@@ -265,6 +269,14 @@ class HexCNN:
         return self.loss
 
     # ------------------------------------------------------------------ accounting
+    def pool_bytes(self, l, kind):
+        """Algorithmic HBM bytes of one pool call after layer l (read inputs + write outputs once)."""
+        h, w, ho, wo = self.pool_geo[l]
+        C = self.channels[l + 1]
+        full, pooled = self.B * h * w * C * 2, self.B * ho * wo * C * 2
+        am = self.B * ho * wo * C
+        return full + pooled + am  # fwd: read x, write y + argmax; bwd: read dy + argmax, write dx
+
     def flops_per_image(self):
         """Algorithmic FLOPs per image of fwd + dgrad (L2..L6) + wgrad, counting
         in-grid taps only (valid taps)."""
