@@ -166,7 +166,9 @@ __device__ __forceinline__ TileCoord decode_fwd_tile(const TcFwdParams& p, int t
     int m = tile / p.n_tiles;
     tc.n0 = nt * BN;
     int jt;
-    if (m < p.tiles0) { tc.P = 0; jt = p.jt0; }
+    if (p.jt0 == p.jt1) {  // interleave the two parity views: both passes over a region run together (L2 reuse)
+        tc.P = m & 1; m >>= 1; jt = p.jt0;
+    } else if (m < p.tiles0) { tc.P = 0; jt = p.jt0; }
     else { tc.P = 1; m -= p.tiles0; jt = p.jt1; }
     const int rti = m % p.rt;
     m /= p.rt;
@@ -741,7 +743,8 @@ struct TcWgParams {
 
 __device__ __forceinline__ void decode_ptile(const TcWgParams& p, int m, int* P, int* r0, int* j0, int* b0) {
     int jt;
-    if (m < p.tiles0) { *P = 0; jt = p.jt0; }
+    if (p.jt0 == p.jt1) { *P = m & 1; m >>= 1; jt = p.jt0; }  // views interleaved (see decode_fwd_tile)
+    else if (m < p.tiles0) { *P = 0; jt = p.jt0; }
     else { *P = 1; m -= p.tiles0; jt = p.jt1; }
     const int rti = m % p.rt;
     m /= p.rt;
