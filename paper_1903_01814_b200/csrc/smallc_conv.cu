@@ -80,9 +80,11 @@ smallc_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __re
                   const float* __restrict__ bias, __nv_bfloat16* __restrict__ y, Geom g, int Cout, int relu) {
     constexpr int T = TapsOf<N>::T;
     constexpr int NA = T + 1;
-    __shared__ float sv_all[SC_WARPS][32 * NA];
+    static_assert(NA % 4 == 0, "16-byte tap rows");
+    __shared__ __align__(16) float sv_all[SC_WARPS][33 * NA];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* sv = sv_all[warp];
+    if (lane < NA) sv[32 * NA + lane] = 0.f;
     const int co = blockIdx.y * 64 + 2 * lane;
     float w0[NA], w1[NA];
 #pragma unroll
@@ -98,17 +100,27 @@ smallc_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __re
         const int64_t pix0 = bt * 32;
         stage_batch<N>(x, g, pix0, npix, sv);
         const int cnt = (int)min((int64_t)32, npix - pix0);
-        for (int j = 0; j < cnt; ++j) {
-            const float* vj = sv + j * NA;
-            float a0 = 0.f, a1 = 0.f;
+        // two pixels per iteration (independent FMA chains), 16-byte broadcast smem loads
+        for (int j = 0; j < cnt; j += 2) {
+            const float4* v0 = reinterpret_cast<const float4*>(sv + j * NA);
+            const float4* v1 = reinterpret_cast<const float4*>(sv + (j + 1) * NA);  // row 32 exists (zeros)
+            float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
 #pragma unroll
-            for (int t = 0; t < NA; ++t) {
-                const float vt = vj[t];
-                a0 = fmaf(w0[t], vt, a0);
-                a1 = fmaf(w1[t], vt, a1);
+            for (int q = 0; q < NA / 4; ++q) {
+                const float4 u = v0[q], v = v1[q];
+                a0 = fmaf(w0[4 * q], u.x, a0); a1 = fmaf(w1[4 * q], u.x, a1);
+                b0 = fmaf(w0[4 * q], v.x, b0); b1 = fmaf(w1[4 * q], v.x, b1);
+                a0 = fmaf(w0[4 * q + 1], u.y, a0); a1 = fmaf(w1[4 * q + 1], u.y, a1);
+                b0 = fmaf(w0[4 * q + 1], v.y, b0); b1 = fmaf(w1[4 * q + 1], v.y, b1);
+                a0 = fmaf(w0[4 * q + 2], u.z, a0); a1 = fmaf(w1[4 * q + 2], u.z, a1);
+                b0 = fmaf(w0[4 * q + 2], v.z, b0); b1 = fmaf(w1[4 * q + 2], v.z, b1);
+                a0 = fmaf(w0[4 * q + 3], u.w, a0); a1 = fmaf(w1[4 * q + 3], u.w, a1);
+                b0 = fmaf(w0[4 * q + 3], v.w, b0); b1 = fmaf(w1[4 * q + 3], v.w, b1);
             }
-            if (relu) { a0 = fmaxf(a0, 0.f); a1 = fmaxf(a1, 0.f); }
+            if (relu) { a0 = fmaxf(a0, 0.f); a1 = fmaxf(a1, 0.f); b0 = fmaxf(b0, 0.f); b1 = fmaxf(b1, 0.f); }
             *reinterpret_cast<__nv_bfloat162*>(y + (pix0 + j) * Cout + co) = __floats2bfloat162_rn(a0, a1);
+            if (j + 1 < cnt)
+                *reinterpret_cast<__nv_bfloat162*>(y + (pix0 + j + 1) * Cout + co) = __floats2bfloat162_rn(b0, b1);
         }
         __syncwarp();
     }
@@ -120,7 +132,8 @@ smallc_wgrad_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __
                     float* __restrict__ part, Geom g, int Cout) {
     constexpr int T = TapsOf<N>::T;
     constexpr int NA = T + 1;  // taps + bias column (ones)
-    __shared__ float sv_all[SC_WARPS][32 * NA];
+    static_assert(NA % 4 == 0, "16-byte tap rows");
+    __shared__ __align__(16) float sv_all[SC_WARPS][32 * NA];
     __shared__ float red[SC_WARPS / 2][NA][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* sv = sv_all[warp];
@@ -137,12 +150,14 @@ smallc_wgrad_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __
         for (int j = 0; j < cnt; ++j) {
             const __nv_bfloat162 d2 = *reinterpret_cast<const __nv_bfloat162*>(dy + (pix0 + j) * Cout + co);
             const float d0 = __low2float(d2), d1 = __high2float(d2);
-            const float* vj = sv + j * NA;
+            const float4* vj = reinterpret_cast<const float4*>(sv + j * NA);
 #pragma unroll
-            for (int t = 0; t < NA; ++t) {
-                const float vt = vj[t];
-                a0[t] = fmaf(d0, vt, a0[t]);
-                a1[t] = fmaf(d1, vt, a1[t]);
+            for (int q = 0; q < NA / 4; ++q) {
+                const float4 v = vj[q];
+                a0[4 * q] = fmaf(d0, v.x, a0[4 * q]); a1[4 * q] = fmaf(d1, v.x, a1[4 * q]);
+                a0[4 * q + 1] = fmaf(d0, v.y, a0[4 * q + 1]); a1[4 * q + 1] = fmaf(d1, v.y, a1[4 * q + 1]);
+                a0[4 * q + 2] = fmaf(d0, v.z, a0[4 * q + 2]); a1[4 * q + 2] = fmaf(d1, v.z, a1[4 * q + 2]);
+                a0[4 * q + 3] = fmaf(d0, v.w, a0[4 * q + 3]); a1[4 * q + 3] = fmaf(d1, v.w, a1[4 * q + 3]);
             }
         }
         __syncwarp();
