@@ -147,17 +147,18 @@ smallc_wgrad_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __
         const int64_t pix0 = bt * 32;
         stage_batch<N>(x, g, pix0, npix, sv);
         const int cnt = (int)min((int64_t)32, npix - pix0);
+        // dy of the next pixel is loaded one iteration ahead (software pipelining)
+        __nv_bfloat162 dn = *reinterpret_cast<const __nv_bfloat162*>(dy + pix0 * Cout + co);
         for (int j = 0; j < cnt; ++j) {
-            const __nv_bfloat162 d2 = *reinterpret_cast<const __nv_bfloat162*>(dy + (pix0 + j) * Cout + co);
+            const __nv_bfloat162 d2 = dn;
+            if (j + 1 < cnt) dn = *reinterpret_cast<const __nv_bfloat162*>(dy + (pix0 + j + 1) * Cout + co);
             const float d0 = __low2float(d2), d1 = __high2float(d2);
-            const float4* vj = reinterpret_cast<const float4*>(sv + j * NA);
+            const float* vj = sv + j * NA;
 #pragma unroll
-            for (int q = 0; q < NA / 4; ++q) {
-                const float4 v = vj[q];
-                a0[4 * q] = fmaf(d0, v.x, a0[4 * q]); a1[4 * q] = fmaf(d1, v.x, a1[4 * q]);
-                a0[4 * q + 1] = fmaf(d0, v.y, a0[4 * q + 1]); a1[4 * q + 1] = fmaf(d1, v.y, a1[4 * q + 1]);
-                a0[4 * q + 2] = fmaf(d0, v.z, a0[4 * q + 2]); a1[4 * q + 2] = fmaf(d1, v.z, a1[4 * q + 2]);
-                a0[4 * q + 3] = fmaf(d0, v.w, a0[4 * q + 3]); a1[4 * q + 3] = fmaf(d1, v.w, a1[4 * q + 3]);
+            for (int t = 0; t < NA; ++t) {
+                const float vt = vj[t];
+                a0[t] = fmaf(d0, vt, a0[t]);
+                a1[t] = fmaf(d1, vt, a1[t]);
             }
         }
         __syncwarp();
