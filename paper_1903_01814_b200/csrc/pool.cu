@@ -596,6 +596,95 @@ pool_bwd_nhwc_v(const uint4* __restrict__ dy, const uint2* __restrict__ am, uint
     }
 }
 
+// ---------------------------------------------------------------------------
+// Max-pool backward for the config-5 case n = 1, s = 2 in closed form.  All
+// lattice centres sit in even columns 2C with centre parity p = parity & 1 and
+// rho(C) = C & 1.  An input pixel (r, c) is reached by:
+//   c even: the window of column c/2 -- its centre row r (tap 3) when r - rho is
+//           even, else the centres r+1 (tap 2) and r-1 (tap 4);
+//   c odd : one window on each side, centres in columns c+1 (taps 0,1; dc = -1)
+//           and c-1 (taps 5,6; dc = +1), whose row is the one of
+//           {r - top, r - top - 1} on the lattice (top = -1 + ((1 + p) >> 1)).
+// At most two candidates (their fp32 sum is order independent), each routed
+// per channel with SIMD byte compares of the argmax bytes.  8 channels/thread.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void route_add(const uint4* __restrict__ dy, const uint2* __restrict__ am, size_t yo,
+                                          int t, float* acc) {
+    const uint4 dq = __ldg(dy + yo);
+    const uint2 a = __ldg(am + yo);
+    const uint32_t tt4 = (uint32_t)t * 0x01010101u;
+    const uint32_t mlo = __vcmpeq4(a.x, tt4), mhi = __vcmpeq4(a.y, tt4);
+    const uint32_t w0 = dq.x & __byte_perm(mlo, 0u, 0x1100), w1 = dq.y & __byte_perm(mlo, 0u, 0x3322);
+    const uint32_t w2 = dq.z & __byte_perm(mhi, 0u, 0x1100), w3 = dq.w & __byte_perm(mhi, 0u, 0x3322);
+    acc[0] += __uint_as_float(w0 << 16); acc[1] += __uint_as_float(w0 & 0xffff0000u);
+    acc[2] += __uint_as_float(w1 << 16); acc[3] += __uint_as_float(w1 & 0xffff0000u);
+    acc[4] += __uint_as_float(w2 << 16); acc[5] += __uint_as_float(w2 & 0xffff0000u);
+    acc[6] += __uint_as_float(w3 << 16); acc[7] += __uint_as_float(w3 & 0xffff0000u);
+}
+
+__global__ void __launch_bounds__(256)
+maxpool_bwd_n1s2_kernel(const uint4* __restrict__ dy, const uint2* __restrict__ am, uint4* __restrict__ dx, Geom g,
+                        int C8) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int per_img = g.H * g.W * C8;
+    if (idx >= per_img) return;
+    const int b = blockIdx.y;
+    const int ch8 = idx % C8;
+    const int q = idx / C8;
+    const int r = q / g.W, c = q - r * g.W;
+    const size_t ybase = (size_t)b * g.Ho * g.Wo * C8 + ch8;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if ((c & 1) == 0) {
+        const int C = c >> 1;
+        if (C < g.Wo) {
+            const int rho = C & 1;
+            const int d = r - rho;
+            if ((d & 1) == 0) {
+                if (d >= 0 && (d >> 1) < g.Ho) route_add(dy, am, ybase + (size_t)((d >> 1) * g.Wo + C) * C8, 3, acc);
+            } else {
+                const int Ra = (d + 1) >> 1;  // centre r + 1, tap 2 (dr = -1)
+                if (d + 1 >= 0 && Ra < g.Ho) route_add(dy, am, ybase + (size_t)(Ra * g.Wo + C) * C8, 2, acc);
+                const int Rb = (d - 1) >> 1;  // centre r - 1, tap 4 (dr = +1)
+                if (d - 1 >= 0 && Rb < g.Ho) route_add(dy, am, ybase + (size_t)(Rb * g.Wo + C) * C8, 4, acc);
+            }
+        }
+    } else {
+        const int p = g.parity & 1;
+        const int top = -1 + ((1 + p) >> 1);
+        // right centre column c + 1 (dc = -1, taps 0, 1)
+        if (c + 1 < g.W) {
+            const int C = (c + 1) >> 1;
+            if (C < g.Wo) {
+                const int rho = C & 1;
+                const int k = ((r - top - rho) & 1);  // 0: dr = top is on the lattice, 1: dr = top + 1
+                const int ro = r - top - k;
+                const int d = ro - rho;
+                if (d >= 0 && (d >> 1) < g.Ho) route_add(dy, am, ybase + (size_t)((d >> 1) * g.Wo + C) * C8, k, acc);
+            }
+        }
+        // left centre column c - 1 (dc = +1, taps 5, 6)
+        {
+            const int C = (c - 1) >> 1;
+            if (C < g.Wo) {
+                const int rho = C & 1;
+                const int k = ((r - top - rho) & 1);
+                const int ro = r - top - k;
+                const int d = ro - rho;
+                if (d >= 0 && (d >> 1) < g.Ho)
+                    route_add(dy, am, ybase + (size_t)((d >> 1) * g.Wo + C) * C8, 5 + k, acc);
+            }
+        }
+    }
+    uint4 out;
+    uint32_t* o = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * k], acc[2 * k + 1]);
+        o[k] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    dx[(size_t)b * per_img + idx] = out;
+}
+
 static int pick_v(const PoolArgs& a) { return a.C % 32 == 0 ? 4 : (a.C % 16 == 0 ? 2 : 1); }
 
 template <int N, int S, int V>
@@ -656,7 +745,12 @@ hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
 hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
     // The 8-channel gather measured faster than the wide variant for the backward
     // (round 1: 519 vs 577 us on config-5 pool 1); HEXCONV_POOL_WIDE_BWD selects it.
-    if (use_spec(a) && getenv("HEXCONV_POOL_WIDE_BWD") && dispatch_wide(a, st, false)) {
+    if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC")) {
+        const int C8 = a.C / 8;
+        dim3 grid(ceil_div((int64_t)a.g.H * a.g.W * C8, 256), a.g.B);
+        maxpool_bwd_n1s2_kernel<<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in, (uint4*)a.dx,
+                                                      a.g, C8);
+    } else if (use_spec(a) && getenv("HEXCONV_POOL_WIDE_BWD") && dispatch_wide(a, st, false)) {
     } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_bwd<1, 1>(a, st); else launch_spec_bwd<1, 2>(a, st); }
         else { if (a.g.s == 1) launch_spec_bwd<2, 1>(a, st); else launch_spec_bwd<2, 2>(a, st); }

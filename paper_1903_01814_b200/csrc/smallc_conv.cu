@@ -147,11 +147,8 @@ smallc_wgrad_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __
         const int64_t pix0 = bt * 32;
         stage_batch<N>(x, g, pix0, npix, sv);
         const int cnt = (int)min((int64_t)32, npix - pix0);
-        // dy of the next pixel is loaded one iteration ahead (software pipelining)
-        __nv_bfloat162 dn = *reinterpret_cast<const __nv_bfloat162*>(dy + pix0 * Cout + co);
         for (int j = 0; j < cnt; ++j) {
-            const __nv_bfloat162 d2 = dn;
-            if (j + 1 < cnt) dn = *reinterpret_cast<const __nv_bfloat162*>(dy + (pix0 + j + 1) * Cout + co);
+            const __nv_bfloat162 d2 = *reinterpret_cast<const __nv_bfloat162*>(dy + (pix0 + j) * Cout + co);
             const float d0 = __low2float(d2), d1 = __high2float(d2);
             const float* vj = sv + j * NA;
 #pragma unroll

@@ -249,3 +249,11 @@ def test_single_input_channel_bf16_nhwc(F, oracle):
     for pi, n, s, (H, W), Cout in [(0, 2, 1, (13, 11), 64), (1, 1, 1, (9, 12), 128), (0, 2, 2, (12, 13), 64),
                                    (1, 2, 2, (11, 10), 64)]:
         _conv_case(F, oracle, pi, n, s, H, W, 3, 1, Cout, torch.bfloat16, "NHWC", 40 + n)
+
+
+def test_maxpool_n1s2_closed_form_backward(F, oracle):
+    # the specialised n=1, s=2 max-pool backward (config 5): both parities, odd/even grids, C % 8 == 0
+    for pi in (0, 1):
+        for (H, W) in [(12, 13), (13, 12), (9, 9), (2, 7)]:
+            for C in (8, 24):
+                _pool_case(F, oracle, pi, 1, 2, H, W, 2, C, torch.bfloat16, "NHWC", "max", 400 + H + C)
