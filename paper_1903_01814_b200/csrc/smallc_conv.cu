@@ -132,8 +132,7 @@ smallc_wgrad_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __
                     float* __restrict__ part, Geom g, int Cout) {
     constexpr int T = TapsOf<N>::T;
     constexpr int NA = T + 1;  // taps + bias column (ones)
-    static_assert(NA % 4 == 0, "16-byte tap rows");
-    __shared__ __align__(16) float sv_all[SC_WARPS][32 * NA];
+    __shared__ float sv_all[SC_WARPS][32 * NA];
     __shared__ float red[SC_WARPS / 2][NA][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* sv = sv_all[warp];

@@ -318,31 +318,42 @@ __device__ __forceinline__ void fwd_epilogue(const TcFwdParams& p, const CUtenso
     }
 }
 
-template <int BN, int KC>
+// RESB: the whole packed weight tensor ([T][kgroups][KC][BN][64] bf16, <= RES_MAX bytes) is
+// loaded once per CTA and stays resident in shared memory; the producer then
+// streams only the A operand (one TMA op per K iteration instead of two).
+constexpr int RES_MAX = 131072;
+
+template <int BN, int KC, bool RESB = false>
 __global__ void __launch_bounds__(192, 1)
 tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                    const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
                    const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
                    const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ TcFwdParams p) {
     using Cfg = FwdCfg<BN, KC>;
+    constexpr int STAGES = RESB ? 4 : Cfg::STAGES;
+    constexpr int STAGE = RESB ? Cfg::A_BYTES : Cfg::STAGE;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* obuf = smem + Cfg::STAGES * Cfg::STAGE;
+    uint8_t* smem_base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* resb = smem_base;                         // resident weights (RESB only)
+    uint8_t* smem = smem_base + (RESB ? RES_MAX : 0);  // stage ring
+    uint8_t* obuf = smem + STAGES * STAGE;
     uint64_t* full = (uint64_t*)(obuf + 2 * Cfg::OUT_BYTES);
-    uint64_t* empty = full + Cfg::STAGES;
-    uint64_t* tfull = empty + Cfg::STAGES;
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* mbar = tempty + 2;  // mask-tile loads into the two staging buffers
-    uint32_t* tmem_slot = (uint32_t*)(mbar + 2);
+    uint64_t* bres = mbar + 2;    // resident-weight load
+    uint32_t* tmem_slot = (uint32_t*)(bres + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < Cfg::STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
             ptx::mbar_init(&tempty[a], 4);
             ptx::mbar_init(&mbar[a], 1);
         }
+        ptx::mbar_init(bres, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&map_x0);
         ptx::prefetch_tmap(&map_x1);
@@ -358,8 +369,15 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
     const int kgroups = p.kblocks / KC;
     const int k_iters = p.T * kgroups;
 
+    constexpr int BLK = KC * BN * 128;  // one (tap, K group) weight block
     if (warp == 0) {
         if (lane == 0) {
+            if constexpr (RESB) {
+                ptx::mbar_arrive_expect_tx(bres, (uint32_t)(k_iters * BLK));
+                for (int t = 0; t < p.T; ++t)
+                    for (int kg = 0; kg < kgroups; ++kg)
+                        ptx::tma_load_4d(&map_w, bres, resb + (t * kgroups + kg) * BLK, 0, 0, kg * KC, t);
+            }
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
@@ -372,11 +390,12 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
                     const CUtensorMap* mx = Pv ? &map_x1 : &map_x0;
                     for (int kg = 0; kg < kgroups; ++kg) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
-                        uint8_t* sa = smem + stage * Cfg::STAGE;
-                        ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
+                        uint8_t* sa = smem + stage * STAGE;
+                        ptx::mbar_arrive_expect_tx(&full[stage], STAGE);
                         ptx::tma_load_5d(mx, &full[stage], sa, 0, tc.r0 + dr, tc.j0 + jsh, tc.b0, kg * KC);
-                        ptx::tma_load_4d(&map_w, &full[stage], sa + Cfg::A_BYTES, 0, tc.n0, kg * KC, t);
-                        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+                        if constexpr (!RESB)
+                            ptx::tma_load_4d(&map_w, &full[stage], sa + Cfg::A_BYTES, 0, tc.n0, kg * KC, t);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
             }
@@ -388,6 +407,7 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
             uint32_t phase = 0;
             int acc = 0;
             uint32_t aphase = 0;
+            if constexpr (RESB) ptx::mbar_wait(bres, 0);
             for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
                 ptx::mbar_wait(&tempty[acc], aphase ^ 1);
                 ptx::tc_fence_after();
@@ -395,8 +415,9 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
                 for (int it = 0; it < k_iters; ++it) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
-                    const uint32_t a0 = ptx::smem_u32(smem + stage * Cfg::STAGE);
-                    const uint32_t b0 = a0 + Cfg::A_BYTES;
+                    const uint32_t a0 = ptx::smem_u32(smem + stage * STAGE);
+                    // k iteration it = (tap t, K group kg) with it = t * kgroups + kg
+                    const uint32_t b0 = RESB ? ptx::smem_u32(resb + it * BLK) : a0 + Cfg::A_BYTES;
 #pragma unroll
                     for (int c = 0; c < KC; ++c)
 #pragma unroll
@@ -406,7 +427,7 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
                             ptx::mma_bf16(d, ad, bd, idesc, (it | c | k) != 0);
                         }
                     ptx::mma_commit(&empty[stage]);
-                    if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 ptx::mma_commit(&tfull[acc]);
                 acc ^= 1;
@@ -621,6 +642,24 @@ static hex_status_t launch_fwd_bn(const CUtensorMap& mx0, const CUtensorMap& mx1
     return last_launch_status();
 }
 
+template <int BN>
+static hex_status_t launch_fwd_res(const CUtensorMap& mx0, const CUtensorMap& mx1, const CUtensorMap& mw,
+                                   const CUtensorMap& my0, const CUtensorMap& my1, const CUtensorMap& mm0,
+                                   const CUtensorMap& mm1, const TcFwdParams& p, cudaStream_t st) {
+    constexpr int SMEM = RES_MAX + 4 * FwdCfg<BN, 1>::A_BYTES + 2 * FwdCfg<BN, 1>::OUT_BYTES + 1024 + 256;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(tc_conv_fwd_kernel<BN, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM) != cudaSuccess)
+            return HEX_ERR_CUDA;
+        attr_set = true;
+    }
+    const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+    tc_conv_fwd_kernel<BN, 1, true><<<grid, 192, SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
+    count_launch();
+    return last_launch_status();
+}
+
 template <int BN, int KC>
 static hex_status_t launch_fwd2_bn(const CUtensorMap& mx0, const CUtensorMap& mx1, const CUtensorMap& mw,
                                    const CUtensorMap& my0, const CUtensorMap& my1, const CUtensorMap& mm0,
@@ -665,7 +704,10 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     p.n_tiles = a.Cout / BN;
     p.m_total = p.tiles0 + p.rt * p.jt1 * p.bt;
     const bool pair = use_2sm(BN) && p.m_total >= 2;
-    int KC = (a.Cin % 128 == 0 && !(BN == 256 && !pair)) ? 2 : 1;
+    // resident weights: one n tile whose packed weights fit the resident region
+    const bool resident = !pair && p.n_tiles == 1 && BN <= 128 &&
+                          (size_t)g.T * a.Cout * a.Cin * 2 <= (size_t)RES_MAX && !getenv("HEXCONV_NO_RESB");
+    int KC = (a.Cin % 128 == 0 && !(BN == 256 && !pair) && !resident) ? 2 : 1;
     if (getenv("HEXCONV_KC")) KC = atoi(getenv("HEXCONV_KC")) == 2 && a.Cin % 128 == 0 ? 2 : 1;
     if (BN == 256 && !pair) KC = 1;  // a 1-CTA BN = 256 stage with KC = 2 would not fit twice in smem
     p.total_tiles = p.m_total * p.n_tiles;
@@ -700,6 +742,7 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
         if (BN == 256) return KC == 2 ? launch_fwd2_bn<256, 2>(HEX_FWD_ARGS) : launch_fwd2_bn<256, 1>(HEX_FWD_ARGS);
         return KC == 2 ? launch_fwd2_bn<128, 2>(HEX_FWD_ARGS) : launch_fwd2_bn<128, 1>(HEX_FWD_ARGS);
     }
+    if (resident) return BN == 128 ? launch_fwd_res<128>(HEX_FWD_ARGS) : launch_fwd_res<64>(HEX_FWD_ARGS);
     switch (BN) {
         case 256: return launch_fwd_bn<256, 1>(HEX_FWD_ARGS);
         case 128: return KC == 2 ? launch_fwd_bn<128, 2>(HEX_FWD_ARGS) : launch_fwd_bn<128, 1>(HEX_FWD_ARGS);
