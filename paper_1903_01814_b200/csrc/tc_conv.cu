@@ -40,6 +40,8 @@ namespace hexconv {
 constexpr int TC_BM = 128;  // output pixels per tile (UMMA M)
 constexpr int TC_BK = 64;   // channels per K block = one 128-byte swizzle row
 constexpr int TC_MAXT = 37; // taps supported on the tensor-core path (n <= 3)
+constexpr int TC_EPI_THREADS = 256;              // 8 epilogue warps (2 per TMEM lane quadrant)
+constexpr int TC_FWD_THREADS = 64 + TC_EPI_THREADS;
 
 // ------------------------------------------------------------------ host: TMA descriptors
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -218,12 +220,14 @@ __device__ __forceinline__ void fwd_epilogue(const TcFwdParams& p, const CUtenso
     using Cfg = FwdCfg<BN>;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     {
-        // Epilogue: warps 2..5 own TMEM lane quadrants (warp % 4); tile row m = TMEM lane.
-        // Per 64-channel chunk: TMEM -> registers -> (bias, ReLU | ReLU-backward mask) -> bf16
-        // -> SW128 staging row m (16-byte chunk i at i ^ (m & 7)) -> one TMA store of the box.
+        // Epilogue: warps 2..9; warp w owns TMEM lane quadrant w % 4 (tile row m = TMEM lane)
+        // and column half h of every 64-channel chunk.  Per chunk: TMEM -> registers ->
+        // (bias, ReLU | ReLU-backward mask) -> bf16 -> SW128 staging row m (16-byte chunk i
+        // at i ^ (m & 7)) -> one TMA store of the box.
         const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
         const int row = q * 32 + lane;
-        const int et = threadIdx.x - 64;  // 0..127
+        const int et = threadIdx.x - 64;  // 0..255
         int acc = 0;
         uint32_t aphase = 0;
         int ob = 0;
@@ -250,20 +254,20 @@ __device__ __forceinline__ void fwd_epilogue(const TcFwdParams& p, const CUtenso
                     if (ob) mphase1 ^= 1; else mphase0 ^= 1;
                 } else {
                     if (et == 0) ptx::bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago
-                    ptx::named_bar(1, 128);
+                    ptx::named_bar(1, TC_EPI_THREADS);
                 }
-                uint32_t v[64];
-                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 64;
+                uint32_t v[32];
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 64 + h * 32;
                 ptx::tmem_ld32(taddr, v);
-                ptx::tmem_ld32(taddr + 32, v + 32);
                 ptx::tmem_ld_wait();
                 uint8_t* rowp = buf + row * 128;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int ii = 0; ii < 4; ++ii) {
+                    const int i = 4 * h + ii;  // 16-byte unit (8 channels) within the 64-channel chunk
                     uint4* slot = reinterpret_cast<uint4*>(rowp + ((i ^ (row & 7)) << 4));
                     float f[8];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) f[k] = __uint_as_float(v[8 * i + k]);
+                    for (int k = 0; k < 8; ++k) f[k] = __uint_as_float(v[8 * ii + k]);
                     if (p.bias) {
                         const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i));
                         const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i + 4));
@@ -292,7 +296,7 @@ __device__ __forceinline__ void fwd_epilogue(const TcFwdParams& p, const CUtenso
                     *slot = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
                 ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA store
-                ptx::named_bar(1, 128);
+                ptx::named_bar(1, TC_EPI_THREADS);
                 if (et == 0) {
                     ptx::tma_store_4d(my, buf, c0, tc.r0, tc.j0, tc.b0);
                     ptx::bulk_commit();
@@ -324,7 +328,7 @@ __device__ __forceinline__ void fwd_epilogue(const TcFwdParams& p, const CUtenso
 constexpr int RES_MAX = 131072;
 
 template <int BN, int KC, bool RESB = false>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(TC_FWD_THREADS, 1)
 tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                    const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
                    const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
@@ -350,7 +354,7 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
         for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 4);
+            ptx::mbar_init(&tempty[a], TC_EPI_THREADS / 32);
             ptx::mbar_init(&mbar[a], 1);
         }
         ptx::mbar_init(bres, 1);
@@ -466,7 +470,7 @@ struct Fwd2Cfg {
 };
 
 template <int BN, int KC>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_FWD_THREADS, 1)
 tc_conv_fwd2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                     const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
                     const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
@@ -489,7 +493,7 @@ tc_conv_fwd2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
         for (int s = 0; s < Cfg::STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+            ptx::mbar_init(&tempty[a], 2 * TC_EPI_THREADS / 32);  // epilogue warps x 2 CTAs (leader's copy)
             ptx::mbar_init(&mbar[a], 1);
         }
         ptx::fence_barrier_init();
@@ -637,7 +641,7 @@ static hex_status_t launch_fwd_bn(const CUtensorMap& mx0, const CUtensorMap& mx1
         attr_set = true;
     }
     const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
-    tc_conv_fwd_kernel<BN, KC><<<grid, 192, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
+    tc_conv_fwd_kernel<BN, KC><<<grid, TC_FWD_THREADS, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
     count_launch();
     return last_launch_status();
 }
@@ -655,7 +659,7 @@ static hex_status_t launch_fwd_res(const CUtensorMap& mx0, const CUtensorMap& mx
         attr_set = true;
     }
     const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
-    tc_conv_fwd_kernel<BN, 1, true><<<grid, 192, SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
+    tc_conv_fwd_kernel<BN, 1, true><<<grid, TC_FWD_THREADS, SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
     count_launch();
     return last_launch_status();
 }
@@ -673,7 +677,7 @@ static hex_status_t launch_fwd2_bn(const CUtensorMap& mx0, const CUtensorMap& mx
         attr_set = true;
     }
     const int pairs = p.pair_tiles < num_sms() / 2 ? p.pair_tiles : num_sms() / 2;
-    tc_conv_fwd2_kernel<BN, KC><<<2 * pairs, 192, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
+    tc_conv_fwd2_kernel<BN, KC><<<2 * pairs, TC_FWD_THREADS, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
     count_launch();
     return last_launch_status();
 }
@@ -706,7 +710,7 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     const bool pair = use_2sm(BN) && p.m_total >= 2;
     // resident weights: one n tile whose packed weights fit the resident region
     const bool resident = !pair && p.n_tiles == 1 && BN <= 128 &&
-                          (size_t)g.T * a.Cout * a.Cin * 2 <= (size_t)RES_MAX && !getenv("HEXCONV_NO_RESB");
+                          (size_t)g.T * a.Cout * a.Cin * 2 <= (size_t)RES_MAX && getenv("HEXCONV_RESB");
     int KC = (a.Cin % 128 == 0 && !(BN == 256 && !pair) && !resident) ? 2 : 1;
     if (getenv("HEXCONV_KC")) KC = atoi(getenv("HEXCONV_KC")) == 2 && a.Cin % 128 == 0 ? 2 : 1;
     if (BN == 256 && !pair) KC = 1;  // a 1-CTA BN = 256 stage with KC = 2 would not fit twice in smem
