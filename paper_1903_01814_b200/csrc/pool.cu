@@ -426,14 +426,15 @@ static void launch_spec_bwd(const PoolArgs& a, cudaStream_t st) {
 template <int N, int S, int V>
 __global__ void __launch_bounds__(256)
 pool_fwd_nhwc_v(const uint4* __restrict__ x, uint4* __restrict__ y, uint2* __restrict__ am, Geom g, int CV,
-                int mode) {
+                int mode, int lgcv) {
+    // grid: x = (output column, channel group) within row R = blockIdx.y of image b = blockIdx.z
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    const int per_img = g.Ho * g.Wo * CV;
-    if (idx >= per_img) return;
-    const int b = blockIdx.y;
-    const int cv = idx % CV;
-    const int o = idx / CV;
-    const int R = o / g.Wo, C = o - R * g.Wo;
+    if (idx >= g.Wo * CV) return;
+    const int b = blockIdx.z;
+    const int R = blockIdx.y;
+    const int cv = lgcv >= 0 ? (idx & (CV - 1)) : idx % CV;
+    const int C = lgcv >= 0 ? (idx >> lgcv) : idx / CV;
+    const int o = R * g.Wo + C;
     const int c = S * C;
     const int r = ((S * C + g.parity) >> 1) % S + S * R;
     const int p = (c + g.parity) & 1;
@@ -624,14 +625,16 @@ __device__ __forceinline__ void route_add(const uint4* __restrict__ dy, const ui
 
 __global__ void __launch_bounds__(256)
 maxpool_bwd_n1s2_kernel(const uint4* __restrict__ dy, const uint2* __restrict__ am, uint4* __restrict__ dx, Geom g,
-                        int C8) {
+                        int C8, int lgc8) {
+    // grid: x = (input column, channel group) within row r = blockIdx.y of image b = blockIdx.z
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= g.W * C8) return;
+    const int b = blockIdx.z;
+    const int r = blockIdx.y;
+    const int ch8 = lgc8 >= 0 ? (idx & (C8 - 1)) : idx % C8;
+    const int c = lgc8 >= 0 ? (idx >> lgc8) : idx / C8;
     const int per_img = g.H * g.W * C8;
-    if (idx >= per_img) return;
-    const int b = blockIdx.y;
-    const int ch8 = idx % C8;
-    const int q = idx / C8;
-    const int r = q / g.W, c = q - r * g.W;
+    const int q = r * g.W + c;
     const size_t ybase = (size_t)b * g.Ho * g.Wo * C8 + ch8;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if ((c & 1) == 0) {
@@ -682,7 +685,14 @@ maxpool_bwd_n1s2_kernel(const uint4* __restrict__ dy, const uint2* __restrict__ 
         __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * k], acc[2 * k + 1]);
         o[k] = *reinterpret_cast<uint32_t*>(&h);
     }
-    dx[(size_t)b * per_img + idx] = out;
+    dx[(size_t)b * per_img + (size_t)q * C8 + ch8] = out;
+}
+
+static int ilog2_exact(int v) {  // log2(v) if v is a power of two, else -1
+    if (v <= 0 || (v & (v - 1))) return -1;
+    int l = 0;
+    while ((1 << l) < v) ++l;
+    return l;
 }
 
 static int pick_v(const PoolArgs& a) { return a.C % 32 == 0 ? 4 : (a.C % 16 == 0 ? 2 : 1); }
@@ -690,8 +700,9 @@ static int pick_v(const PoolArgs& a) { return a.C % 32 == 0 ? 4 : (a.C % 16 == 0
 template <int N, int S, int V>
 static void launch_v_fwd(const PoolArgs& a, cudaStream_t st) {
     const int CV = a.C / (8 * V);
-    dim3 grid(ceil_div((int64_t)a.g.Ho * a.g.Wo * CV, 256), a.g.B);
-    pool_fwd_nhwc_v<N, S, V><<<grid, 256, 0, st>>>((const uint4*)a.x, (uint4*)a.y, (uint2*)a.argmax, a.g, CV, a.mode);
+    dim3 grid(ceil_div((int64_t)a.g.Wo * CV, 256), a.g.Ho, a.g.B);
+    pool_fwd_nhwc_v<N, S, V><<<grid, 256, 0, st>>>((const uint4*)a.x, (uint4*)a.y, (uint2*)a.argmax, a.g, CV, a.mode,
+                                                   ilog2_exact(CV));
 }
 template <int N, int S, int V>
 static void launch_v_bwd(const PoolArgs& a, cudaStream_t st) {
@@ -747,9 +758,9 @@ hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
     // (round 1: 519 vs 577 us on config-5 pool 1); HEXCONV_POOL_WIDE_BWD selects it.
     if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC")) {
         const int C8 = a.C / 8;
-        dim3 grid(ceil_div((int64_t)a.g.H * a.g.W * C8, 256), a.g.B);
+        dim3 grid(ceil_div((int64_t)a.g.W * C8, 256), a.g.H, a.g.B);
         maxpool_bwd_n1s2_kernel<<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in, (uint4*)a.dx,
-                                                      a.g, C8);
+                                                      a.g, C8, ilog2_exact(C8));
     } else if (use_spec(a) && getenv("HEXCONV_POOL_WIDE_BWD") && dispatch_wide(a, st, false)) {
     } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_bwd<1, 1>(a, st); else launch_spec_bwd<1, 2>(a, st); }
