@@ -427,14 +427,13 @@ template <int N, int S, int V>
 __global__ void __launch_bounds__(256)
 pool_fwd_nhwc_v(const uint4* __restrict__ x, uint4* __restrict__ y, uint2* __restrict__ am, Geom g, int CV,
                 int mode, int lgcv) {
-    // grid: x = (output column, channel group) within row R = blockIdx.y of image b = blockIdx.z
+    // grid: x = (output pixel, channel group) of image b = blockIdx.y
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= g.Wo * CV) return;
-    const int b = blockIdx.z;
-    const int R = blockIdx.y;
+    if (idx >= g.Ho * g.Wo * CV) return;
+    const int b = blockIdx.y;
     const int cv = lgcv >= 0 ? (idx & (CV - 1)) : idx % CV;
-    const int C = lgcv >= 0 ? (idx >> lgcv) : idx / CV;
-    const int o = R * g.Wo + C;
+    const int o = lgcv >= 0 ? (idx >> lgcv) : idx / CV;
+    const int R = o / g.Wo, C = o - R * g.Wo;
     const int c = S * C;
     const int r = ((S * C + g.parity) >> 1) % S + S * R;
     const int p = (c + g.parity) & 1;
@@ -700,7 +699,7 @@ static int pick_v(const PoolArgs& a) { return a.C % 32 == 0 ? 4 : (a.C % 16 == 0
 template <int N, int S, int V>
 static void launch_v_fwd(const PoolArgs& a, cudaStream_t st) {
     const int CV = a.C / (8 * V);
-    dim3 grid(ceil_div((int64_t)a.g.Wo * CV, 256), a.g.Ho, a.g.B);
+    dim3 grid(ceil_div((int64_t)a.g.Ho * a.g.Wo * CV, 256), a.g.B);
     pool_fwd_nhwc_v<N, S, V><<<grid, 256, 0, st>>>((const uint4*)a.x, (uint4*)a.y, (uint2*)a.argmax, a.g, CV, a.mode,
                                                    ilog2_exact(CV));
 }
