@@ -694,7 +694,14 @@ static int ilog2_exact(int v) {  // log2(v) if v is a power of two, else -1
     return l;
 }
 
-static int pick_v(const PoolArgs& a) { return a.C % 32 == 0 ? 4 : (a.C % 16 == 0 ? 2 : 1); }
+static int pick_v(const PoolArgs& a) {
+    int v = a.C % 32 == 0 ? 4 : (a.C % 16 == 0 ? 2 : 1);
+    if (const char* e = getenv("HEXCONV_POOL_V")) {  // development override
+        const int want = atoi(e);
+        if (want >= 1 && want <= v && a.C % (8 * want) == 0) v = want;
+    }
+    return v;
+}
 
 template <int N, int S, int V>
 static void launch_v_fwd(const PoolArgs& a, cudaStream_t st) {
