@@ -622,32 +622,44 @@ __device__ __forceinline__ void route_add(const uint4* __restrict__ dy, const ui
     acc[6] += __uint_as_float(w3 << 16); acc[7] += __uint_as_float(w3 & 0xffff0000u);
 }
 
+template <int V>
+__device__ __forceinline__ void route_add_v(const uint4* __restrict__ dy, const uint2* __restrict__ am, size_t yo,
+                                            int t, float* acc) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) route_add(dy, am, yo + v, t, acc + 8 * v);
+}
+
+template <int V>
 __global__ void __launch_bounds__(256)
 maxpool_bwd_n1s2_kernel(const uint4* __restrict__ dy, const uint2* __restrict__ am, uint4* __restrict__ dx, Geom g,
-                        int C8, int lgc8) {
+                        int C8, int lgcv) {
     // grid: x = (input column, channel group) within row r = blockIdx.y of image b = blockIdx.z
+    const int CV = C8 / V;
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= g.W * C8) return;
+    if (idx >= g.W * CV) return;
     const int b = blockIdx.z;
     const int r = blockIdx.y;
-    const int ch8 = lgc8 >= 0 ? (idx & (C8 - 1)) : idx % C8;
-    const int c = lgc8 >= 0 ? (idx >> lgc8) : idx / C8;
+    const int cv = lgcv >= 0 ? (idx & (CV - 1)) : idx % CV;
+    const int c = lgcv >= 0 ? (idx >> lgcv) : idx / CV;
+    const int ch8 = cv * V;
     const int per_img = g.H * g.W * C8;
     const int q = r * g.W + c;
     const size_t ybase = (size_t)b * g.Ho * g.Wo * C8 + ch8;
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float acc[8 * V];
+#pragma unroll
+    for (int i = 0; i < 8 * V; ++i) acc[i] = 0.f;
     if ((c & 1) == 0) {
         const int C = c >> 1;
         if (C < g.Wo) {
             const int rho = C & 1;
             const int d = r - rho;
             if ((d & 1) == 0) {
-                if (d >= 0 && (d >> 1) < g.Ho) route_add(dy, am, ybase + (size_t)((d >> 1) * g.Wo + C) * C8, 3, acc);
+                if (d >= 0 && (d >> 1) < g.Ho) route_add_v<V>(dy, am, ybase + (size_t)((d >> 1) * g.Wo + C) * C8, 3, acc);
             } else {
                 const int Ra = (d + 1) >> 1;  // centre r + 1, tap 2 (dr = -1)
-                if (d + 1 >= 0 && Ra < g.Ho) route_add(dy, am, ybase + (size_t)(Ra * g.Wo + C) * C8, 2, acc);
+                if (d + 1 >= 0 && Ra < g.Ho) route_add_v<V>(dy, am, ybase + (size_t)(Ra * g.Wo + C) * C8, 2, acc);
                 const int Rb = (d - 1) >> 1;  // centre r - 1, tap 4 (dr = +1)
-                if (d - 1 >= 0 && Rb < g.Ho) route_add(dy, am, ybase + (size_t)(Rb * g.Wo + C) * C8, 4, acc);
+                if (d - 1 >= 0 && Rb < g.Ho) route_add_v<V>(dy, am, ybase + (size_t)(Rb * g.Wo + C) * C8, 4, acc);
             }
         }
     } else {
@@ -661,7 +673,7 @@ maxpool_bwd_n1s2_kernel(const uint4* __restrict__ dy, const uint2* __restrict__ 
                 const int k = ((r - top - rho) & 1);  // 0: dr = top is on the lattice, 1: dr = top + 1
                 const int ro = r - top - k;
                 const int d = ro - rho;
-                if (d >= 0 && (d >> 1) < g.Ho) route_add(dy, am, ybase + (size_t)((d >> 1) * g.Wo + C) * C8, k, acc);
+                if (d >= 0 && (d >> 1) < g.Ho) route_add_v<V>(dy, am, ybase + (size_t)((d >> 1) * g.Wo + C) * C8, k, acc);
             }
         }
         // left centre column c - 1 (dc = +1, taps 5, 6)
@@ -673,18 +685,21 @@ maxpool_bwd_n1s2_kernel(const uint4* __restrict__ dy, const uint2* __restrict__ 
                 const int ro = r - top - k;
                 const int d = ro - rho;
                 if (d >= 0 && (d >> 1) < g.Ho)
-                    route_add(dy, am, ybase + (size_t)((d >> 1) * g.Wo + C) * C8, 5 + k, acc);
+                    route_add_v<V>(dy, am, ybase + (size_t)((d >> 1) * g.Wo + C) * C8, 5 + k, acc);
             }
         }
     }
-    uint4 out;
-    uint32_t* o = reinterpret_cast<uint32_t*>(&out);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * k], acc[2 * k + 1]);
-        o[k] = *reinterpret_cast<uint32_t*>(&h);
+    for (int v = 0; v < V; ++v) {
+        uint4 out;
+        uint32_t* o = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(acc[8 * v + 2 * k], acc[8 * v + 2 * k + 1]);
+            o[k] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        dx[(size_t)b * per_img + (size_t)q * C8 + ch8 + v] = out;
     }
-    dx[(size_t)b * per_img + (size_t)q * C8 + ch8] = out;
 }
 
 static int ilog2_exact(int v) {  // log2(v) if v is a power of two, else -1
@@ -695,10 +710,10 @@ static int ilog2_exact(int v) {  // log2(v) if v is a power of two, else -1
 }
 
 static int pick_v(const PoolArgs& a) {
-    int v = a.C % 32 == 0 ? 4 : (a.C % 16 == 0 ? 2 : 1);
+    int v = a.C % 16 == 0 ? 2 : 1;  // 16 channels/thread measured best (occupancy vs index reuse)
     if (const char* e = getenv("HEXCONV_POOL_V")) {  // development override
         const int want = atoi(e);
-        if (want >= 1 && want <= v && a.C % (8 * want) == 0) v = want;
+        if ((want == 1 || want == 2 || want == 4) && a.C % (8 * want) == 0) v = want;
     }
     return v;
 }
@@ -764,9 +779,14 @@ hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
     // (round 1: 519 vs 577 us on config-5 pool 1); HEXCONV_POOL_WIDE_BWD selects it.
     if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC")) {
         const int C8 = a.C / 8;
-        dim3 grid(ceil_div((int64_t)a.g.W * C8, 256), a.g.H, a.g.B);
-        maxpool_bwd_n1s2_kernel<<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in, (uint4*)a.dx,
-                                                      a.g, C8, ilog2_exact(C8));
+        const int V = (C8 % 2 == 0 && !getenv("HEXCONV_POOL_BWD_V1")) ? 2 : 1;
+        dim3 grid(ceil_div((int64_t)a.g.W * (C8 / V), 256), a.g.H, a.g.B);
+        if (V == 2)
+            maxpool_bwd_n1s2_kernel<2><<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in,
+                                                             (uint4*)a.dx, a.g, C8, ilog2_exact(C8 / 2));
+        else
+            maxpool_bwd_n1s2_kernel<1><<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in,
+                                                             (uint4*)a.dx, a.g, C8, ilog2_exact(C8));
     } else if (use_spec(a) && getenv("HEXCONV_POOL_WIDE_BWD") && dispatch_wide(a, st, false)) {
     } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_bwd<1, 1>(a, st); else launch_spec_bwd<1, 2>(a, st); }
