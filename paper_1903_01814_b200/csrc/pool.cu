@@ -640,7 +640,10 @@ maxpool_bwd_n1s2_kernel(const uint4* __restrict__ dy, const uint2* __restrict__ 
     const int b = blockIdx.z;
     const int r = blockIdx.y;
     const int cv = lgcv >= 0 ? (idx & (CV - 1)) : idx % CV;
-    const int c = lgcv >= 0 ? (idx >> lgcv) : idx / CV;
+    const int ci = lgcv >= 0 ? (idx >> lgcv) : idx / CV;
+    // even columns first, then odd ones: a warp never mixes the two closed-form branches
+    const int half = (g.W + 1) >> 1;
+    const int c = ci < half ? 2 * ci : 2 * (ci - half) + 1;
     const int ch8 = cv * V;
     const int per_img = g.H * g.W * C8;
     const int q = r * g.W + c;
@@ -779,7 +782,7 @@ hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
     // (round 1: 519 vs 577 us on config-5 pool 1); HEXCONV_POOL_WIDE_BWD selects it.
     if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC")) {
         const int C8 = a.C / 8;
-        const int V = (C8 % 2 == 0 && !getenv("HEXCONV_POOL_BWD_V1")) ? 2 : 1;
+        const int V = (C8 % 2 == 0 && getenv("HEXCONV_POOL_BWD_V2")) ? 2 : 1;
         dim3 grid(ceil_div((int64_t)a.g.W * (C8 / V), 256), a.g.H, a.g.B);
         if (V == 2)
             maxpool_bwd_n1s2_kernel<2><<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in,
