@@ -190,6 +190,9 @@ hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* d, const void* x, const voi
         if (((uintptr_t)y & 3) != 0) return HEX_ERR_ALIGNMENT;
         return smallc_fwd(x, w, bias, y, g, d->out_channels, fuse_relu, s);
     }
+    if (tiled_supported(g, d->dtype, d->layout))
+        return tiled_conv((const float*)x, (const float*)w, bias, nullptr, (float*)y, g, d->in_channels,
+                          d->out_channels, fuse_relu, 0, s);
     DirectConvArgs a = make_direct(d, g);
     a.x = x; a.w = w; a.bias = bias; a.y = y; a.relu = fuse_relu;
     return direct_conv_fwd(a, s);
@@ -216,6 +219,9 @@ hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* d, const void* dy, con
         a.x = dy; a.wpack = wp; a.bias = nullptr; a.y = dx; a.relu_y = relu_y; a.relu = 0;
         return tc_conv_fwd(a, s);
     }
+    if (tiled_supported(g, d->dtype, d->layout))
+        return tiled_conv((const float*)dy, (const float*)w, nullptr, (const float*)relu_y, (float*)dx, g,
+                          d->out_channels, d->in_channels, 0, 1, s);
     DirectConvArgs a = make_direct(d, g);
     a.dy = dy; a.w = w; a.relu_y = relu_y; a.dx = dx;
     return direct_conv_bwd_data(a, s);

@@ -79,4 +79,9 @@ hex_status_t smallc_fwd(const void* x, const void* w, const float* bias, void* y
 hex_status_t smallc_wgrad(const void* x, const void* dy, float* dw, float* dbias, int accumulate, const Geom& g,
                           int Cout, void* ws, cudaStream_t st);
 
+// register-blocked fp32 NCHW stride-1 conv (forward / transposed backward-data)
+bool tiled_supported(const Geom& g, int dtype, int layout);
+hex_status_t tiled_conv(const float* x, const float* w, const float* bias, const float* relu_y, float* y,
+                        const Geom& g, int Cin, int Cout, int relu, int transpose, cudaStream_t st);
+
 }  // namespace hexconv
