@@ -79,6 +79,14 @@ hex_status_t smallc_fwd(const void* x, const void* w, const float* bias, void* y
 hex_status_t smallc_wgrad(const void* x, const void* dy, float* dw, float* dbias, int accumulate, const Geom& g,
                           int Cout, void* ws, cudaStream_t st);
 
+// the same layer on the warp-level tensor cores (stride 1)
+bool smallc_mma_supported(const Geom& g, int Cin, int Cout);
+size_t smallc_mma_wgrad_ws_bytes(const Geom& g, int Cout);
+hex_status_t smallc_mma_fwd(const void* x, const void* w, const float* bias, void* y, const Geom& g, int Cout,
+                            int relu, cudaStream_t st);
+hex_status_t smallc_mma_wgrad(const void* x, const void* dy, float* dw, float* dbias, int accumulate, const Geom& g,
+                              int Cout, void* ws, cudaStream_t st);
+
 // register-blocked fp32 NCHW stride-1 conv (forward / transposed backward-data)
 bool tiled_supported(const Geom& g, int dtype, int layout);
 hex_status_t tiled_conv(const float* x, const float* w, const float* bias, const float* relu_y, float* y,

@@ -12,6 +12,8 @@
 // (off-grid neighbours contribute 0, A4).  The
 // weight gradient reduces per block in a fixed warp order and then across
 // blocks in a fixed order: deterministic.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "geometry.cuh"
 #include "kernels.h"
@@ -206,12 +208,22 @@ bool smallc_supported(const Geom& g, int Cin, int Cout) {
     return Cin == 1 && Cout % 64 == 0 && g.n >= 1 && g.n <= 2;
 }
 
+// Stride 1 runs on the tensor-core kernels of smallc_mma.cu; the FFMA stencil
+// above remains for stride > 1 (HEXCONV_SMALLC_FFMA=1 forces it, for A/B runs).
+static bool use_mma(const Geom& g, int Cout) {
+    static const bool force_ffma = getenv("HEXCONV_SMALLC_FFMA") != nullptr;
+    return !force_ffma && smallc_mma_supported(g, 1, Cout);
+}
+
 size_t smallc_wgrad_ws_bytes(const Geom& g, int Cout) {
-    return (size_t)SC_WG_BLOCKS * Cout * (g.T + 1) * sizeof(float);
+    const size_t a = (size_t)SC_WG_BLOCKS * Cout * (g.T + 1) * sizeof(float);
+    const size_t b = smallc_mma_wgrad_ws_bytes(g, Cout);
+    return a > b ? a : b;
 }
 
 hex_status_t smallc_fwd(const void* x, const void* w, const float* bias, void* y, const Geom& g, int Cout, int relu,
                         cudaStream_t st) {
+    if (use_mma(g, Cout)) return smallc_mma_fwd(x, w, bias, y, g, Cout, relu, st);
     const int64_t npix = (int64_t)g.B * g.Ho * g.Wo;
     int blocks = (int)((npix + SC_WARPS * 32 * 4 - 1) / (SC_WARPS * 32 * 4));  // ~4 pixel batches per warp
     if (blocks > 148 * 8) blocks = 148 * 8;
@@ -230,6 +242,7 @@ hex_status_t smallc_fwd(const void* x, const void* w, const float* bias, void* y
 
 hex_status_t smallc_wgrad(const void* x, const void* dy, float* dw, float* dbias, int accumulate, const Geom& g,
                           int Cout, void* ws, cudaStream_t st) {
+    if (use_mma(g, Cout)) return smallc_mma_wgrad(x, dy, dw, dbias, accumulate, g, Cout, ws, st);
     dim3 grid(SC_WG_BLOCKS, Cout / 64);
     const auto* xb = (const __nv_bfloat16*)x;
     const auto* db = (const __nv_bfloat16*)dy;

@@ -251,6 +251,16 @@ def test_single_input_channel_bf16_nhwc(F, oracle):
         _conv_case(F, oracle, pi, n, s, H, W, 3, 1, Cout, torch.bfloat16, "NHWC", 40 + n)
 
 
+@pytest.mark.parametrize("pi,n", [(0, 2), (1, 2), (0, 1), (1, 1)])
+def test_single_input_channel_mma_bands(F, oracle, pi, n):
+    # the stride-1 Cin = 1 tensor-core kernels (smallc_mma.cu): several 16-row bands with a ragged
+    # last band, ragged 16-pixel items (W % 16 != 0), two 64-channel blocks, both parities
+    # (W % 8 == 0 takes the bulk-copy band staging; B * bands > 2 * 148 makes the persistent blocks loop)
+    for (H, W), Cout, B in [((37, 45), 128, 3), ((16, 16), 64, 2), ((5, 70), 64, 1), ((35, 40), 64, 2),
+                            ((40, 24), 64, 120)]:
+        _conv_case(F, oracle, pi, n, 1, H, W, B, 1, Cout, torch.bfloat16, "NHWC", 60 + n + H)
+
+
 def test_maxpool_n1s2_closed_form_backward(F, oracle):
     # the specialised n=1, s=2 max-pool backward (config 5): both parities, odd/even grids, C % 8 == 0
     for pi in (0, 1):
