@@ -705,6 +705,129 @@ maxpool_bwd_n1s2_kernel(const uint4* __restrict__ dy, const uint2* __restrict__ 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Max-pool backward, n = 1, s = 2, output-block form: one thread owns the 2x2
+// input block rows {2R', 2R'+1} x columns {2C, 2C+1} (8 channels).  All of
+// the block's candidate windows lie in window columns C, C+1 and rows
+// R'-1..R'+1; which (window, tap) reaches which pixel depends only on the
+// centre parity P = parity and rho(C) = C & 1 (lattice rho(C) =
+// floor((2C + parity) / 2) mod 2), so each of the four (P, rho) cases is a
+// compile-time table: every needed window is loaded once (dy 16 B + argmax
+// 8 B) and routed to its pixels with SIMD byte compares; a pixel reached by
+// two windows adds the two routed values (bf16x2 add = RNE of the exact sum,
+// the same value as the fp32 sum rounded once).  Columns are visited even C
+// first, then odd C, so rho is warp-uniform.
+// ---------------------------------------------------------------------------
+struct Cand {
+    int dC, dR, tap;  // window (C + dC, R' + dR), tap index; tap < 0: none
+};
+// candidate k (0/1) of pixel (row 2R' + pr, column 2C + pc) for centre parity P, rho(C) = RHO
+__host__ __device__ constexpr Cand blk_cand(int P, int RHO, int pc, int pr, int k) {
+    if (pc == 0) {  // column 2C: the window column's own taps 2, 3, 4 (dr = -1, 0, +1)
+        if (RHO == 0) {
+            if (pr == 0) return k == 0 ? Cand{0, 0, 3} : Cand{0, 0, -1};
+            return k == 0 ? Cand{0, 0, 4} : Cand{0, 1, 2};
+        }
+        if (pr == 0) return k == 0 ? Cand{0, -1, 4} : Cand{0, 0, 2};
+        return k == 0 ? Cand{0, 0, 3} : Cand{0, 0, -1};
+    }
+    // column 2C+1: k = 0 from window column C (dc = +1, taps 5, 6), k = 1 from C+1 (dc = -1, taps 0, 1)
+    if (P == 0) {
+        if (RHO == 0) {
+            if (pr == 0) return k == 0 ? Cand{0, 0, 6} : Cand{1, 0, 0};
+            return k == 0 ? Cand{0, 1, 5} : Cand{1, 0, 1};
+        }
+        if (pr == 0) return k == 0 ? Cand{0, 0, 5} : Cand{1, 0, 1};
+        return k == 0 ? Cand{0, 0, 6} : Cand{1, 1, 0};
+    }
+    if (RHO == 0) {
+        if (pr == 0) return k == 0 ? Cand{0, 0, 5} : Cand{1, -1, 1};
+        return k == 0 ? Cand{0, 0, 6} : Cand{1, 0, 0};
+    }
+    if (pr == 0) return k == 0 ? Cand{0, -1, 6} : Cand{1, 0, 0};
+    return k == 0 ? Cand{0, 0, 5} : Cand{1, 0, 1};
+}
+__host__ __device__ constexpr bool blk_uses(int P, int RHO, int dC, int dR) {
+    for (int pc = 0; pc < 2; ++pc)
+        for (int pr = 0; pr < 2; ++pr)
+            for (int k = 0; k < 2; ++k) {
+                const Cand c = blk_cand(P, RHO, pc, pr, k);
+                if (c.tap >= 0 && c.dC == dC && c.dR == dR) return true;
+            }
+    return false;
+}
+
+// dy masked to the channels whose argmax byte equals `tap`
+__device__ __forceinline__ uint4 route_mask(uint4 d, uint2 a, int tap) {
+    const uint32_t tt4 = (uint32_t)tap * 0x01010101u;
+    const uint32_t mlo = __vcmpeq4(a.x, tt4), mhi = __vcmpeq4(a.y, tt4);
+    return make_uint4(d.x & __byte_perm(mlo, 0u, 0x1100), d.y & __byte_perm(mlo, 0u, 0x3322),
+                      d.z & __byte_perm(mhi, 0u, 0x1100), d.w & __byte_perm(mhi, 0u, 0x3322));
+}
+__device__ __forceinline__ uint32_t badd2(uint32_t a, uint32_t b) {
+    __nv_bfloat162 r = __hadd2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+}
+
+template <int P, int RHO>
+__device__ __forceinline__ void maxpool_bwd_blk_body(const uint4* __restrict__ dyb, const uint2* __restrict__ amb,
+                                                     uint4* __restrict__ dxb, const Geom& g, int C8, int ch8, int Rp,
+                                                     int C) {
+    // windows (dC, dR) in {0,1} x {-1,0,1}; unused ones are compiled out
+    uint4 d[2][3];
+    uint2 a[2][3];
+#pragma unroll
+    for (int dC = 0; dC < 2; ++dC)
+#pragma unroll
+        for (int dR = -1; dR <= 1; ++dR) {
+            d[dC][dR + 1] = make_uint4(0u, 0u, 0u, 0u);
+            a[dC][dR + 1] = make_uint2(0xffffffffu, 0xffffffffu);  // no tap matches
+            if (blk_uses(P, RHO, dC, dR)) {
+                const int Cw = C + dC, Rw = Rp + dR;
+                if (Cw < g.Wo && Rw >= 0 && Rw < g.Ho) {
+                    const size_t o = (size_t)(Rw * g.Wo + Cw) * C8 + ch8;
+                    d[dC][dR + 1] = __ldg(dyb + o);
+                    a[dC][dR + 1] = __ldg(amb + o);
+                }
+            }
+        }
+#pragma unroll
+    for (int pc = 0; pc < 2; ++pc)
+#pragma unroll
+        for (int pr = 0; pr < 2; ++pr) {
+            const int r = 2 * Rp + pr, c = 2 * C + pc;
+            if (r >= g.H || c >= g.W) continue;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            const Cand c0 = blk_cand(P, RHO, pc, pr, 0), c1 = blk_cand(P, RHO, pc, pr, 1);
+            if (c0.tap >= 0) v = route_mask(d[c0.dC][c0.dR + 1], a[c0.dC][c0.dR + 1], c0.tap);
+            if (c1.tap >= 0) {
+                const uint4 u = route_mask(d[c1.dC][c1.dR + 1], a[c1.dC][c1.dR + 1], c1.tap);
+                v = make_uint4(badd2(v.x, u.x), badd2(v.y, u.y), badd2(v.z, u.z), badd2(v.w, u.w));
+            }
+            dxb[(size_t)(r * g.W + c) * C8 + ch8] = v;
+        }
+}
+
+template <int P>
+__global__ void __launch_bounds__(256)
+maxpool_bwd_n1s2_blk_kernel(const uint4* __restrict__ dy, const uint2* __restrict__ am, uint4* __restrict__ dx, Geom g,
+                            int C8, int lgc8) {
+    // grid: x = (block column in even-then-odd order, channel group), y = block row R', z = image
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nC = g.Wo;  // = ceil(W / 2) block columns
+    if (idx >= nC * C8) return;
+    const int ch8 = lgc8 >= 0 ? (idx & (C8 - 1)) : idx % C8;
+    const int ci = lgc8 >= 0 ? (idx >> lgc8) : idx / C8;
+    const int half = (nC + 1) >> 1;
+    const int C = ci < half ? 2 * ci : 2 * (ci - half) + 1;
+    const int b = blockIdx.z, Rp = blockIdx.y;
+    const size_t yimg = (size_t)b * g.Ho * g.Wo * C8, ximg = (size_t)b * g.H * g.W * C8;
+    if (C & 1)
+        maxpool_bwd_blk_body<P, 1>(dy + yimg, am + yimg, dx + ximg, g, C8, ch8, Rp, C);
+    else
+        maxpool_bwd_blk_body<P, 0>(dy + yimg, am + yimg, dx + ximg, g, C8, ch8, Rp, C);
+}
+
 static int ilog2_exact(int v) {  // log2(v) if v is a power of two, else -1
     if (v <= 0 || (v & (v - 1))) return -1;
     int l = 0;
@@ -780,7 +903,17 @@ hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
 hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
     // The 8-channel gather measured faster than the wide variant for the backward
     // (round 1: 519 vs 577 us on config-5 pool 1); HEXCONV_POOL_WIDE_BWD selects it.
-    if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC")) {
+    if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC") &&
+        !getenv("HEXCONV_POOL_PIXEL_BWD")) {
+        const int C8 = a.C / 8;
+        dim3 grid(ceil_div((int64_t)a.g.Wo * C8, 256), (a.g.H + 1) / 2, a.g.B);
+        if (a.g.parity & 1)
+            maxpool_bwd_n1s2_blk_kernel<1><<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in,
+                                                                 (uint4*)a.dx, a.g, C8, ilog2_exact(C8));
+        else
+            maxpool_bwd_n1s2_blk_kernel<0><<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in,
+                                                                 (uint4*)a.dx, a.g, C8, ilog2_exact(C8));
+    } else if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC")) {
         const int C8 = a.C / 8;
         const int V = (C8 % 2 == 0 && getenv("HEXCONV_POOL_BWD_V2")) ? 2 : 1;
         dim3 grid(ceil_div((int64_t)a.g.W * (C8 / V), 256), a.g.H, a.g.B);
