@@ -70,6 +70,11 @@ struct TcWgradArgs {
 bool tc_wgrad_supported(const Geom& g, int Cin, int Cout);
 size_t tc_wgrad_ws_bytes(const Geom& g, int Cin, int Cout);
 hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
+// tap-reuse variant (tc_wgrad_tr.cu); writes split-K partials, reduced by tc_conv_wgrad
+bool tc_wgrad_tr_supported(const Geom& g, int Cin, int Cout);
+size_t tc_wgrad_tr_ws_bytes(const Geom& g, int Cin, int Cout);
+hex_status_t tc_wgrad_tr(const TcWgradArgs& a, void* ws, size_t ws_bytes, int* chunks_out, float** db_part_out,
+                         cudaStream_t st);
 
 // single-input-channel bf16 NHWC stencil (config 5 layer 1)
 bool smallc_supported(const Geom& g, int Cin, int Cout);

@@ -1217,6 +1217,7 @@ bool tc_wgrad_supported(const Geom& g, int Cin, int Cout) {
 }
 
 size_t tc_wgrad_ws_bytes(const Geom& g, int Cin, int Cout) {
+    if (tc_wgrad_tr_supported(g, Cin, Cout)) return tc_wgrad_tr_ws_bytes(g, Cin, Cout);
     const WgPlan w = wg_plan(g, Cin, Cout);
     return (size_t)w.chunks * g.T * Cout * Cin * sizeof(float) + (size_t)w.chunks * Cout * sizeof(float) + 256;
 }
@@ -1237,6 +1238,22 @@ static hex_status_t launch_wgrad_pix(const CUtensorMap& mx0, const CUtensorMap& 
 
 hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
     const Geom& g = a.g;
+    if (tc_wgrad_tr_supported(g, a.Cin, a.Cout)) {  // tap-reuse kernel (tc_wgrad_tr.cu)
+        int chunks = 0;
+        float* db_part = nullptr;
+        const hex_status_t s = tc_wgrad_tr(a, ws, ws_bytes, &chunks, &db_part, st);
+        if (s != HEX_OK) return s;
+        const int64_t total = (int64_t)g.T * a.Cout * a.Cin;
+        wgrad_tc_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const float*)ws, chunks, g.T, a.Cout, a.Cin,
+                                                                     a.dw, a.accumulate);
+        count_launch();
+        if (a.dbias) {
+            dbias_reduce_kernel<<<ceil_div(a.Cout, 256), 256, 0, st>>>(db_part, chunks, a.Cout, a.dbias,
+                                                                       a.accumulate);
+            count_launch();
+        }
+        return last_launch_status();
+    }
     const WgPlan w = wg_plan(g, a.Cin, a.Cout);
     if (ws_bytes < tc_wgrad_ws_bytes(g, a.Cin, a.Cout)) return HEX_ERR_WORKSPACE;
     TcWgParams p{};

@@ -101,3 +101,17 @@ def test_tc_matches_stencil_path(F, monkeypatch):
     xs = x.permute(0, 3, 1, 2).contiguous()
     y_st = F.conv2d_fwd(xs, w, n=1, layout="NCHW").float().permute(0, 2, 3, 1)
     assert (y_tc - y_st).abs().max().item() <= 2e-2 * y_st.abs().max().item()
+
+
+@pytest.mark.parametrize("n", [1, 2])
+@pytest.mark.parametrize("pi", [0, 1])
+def test_tc_tap_reuse_wgrad_shapes(F, oracle, n, pi):
+    # shapes the tap-reuse weight-gradient kernel (tc_wgrad_tr.cu) takes: 16-row x 8-sub-column tiles
+    # at least 85% filled, here with a ragged last row tile (H = 30) and views of unequal width (W = 31)
+    case(F, oracle, 2, 64, 128, 30, 31, n, pi, 100 + 10 * n + pi)
+
+
+def test_tc_tap_reuse_wgrad_channel_tiles(F, oracle):
+    # two Cout tiles x two input-channel chunks (n = 1), and the three n = 2 column groups x two chunks
+    case(F, oracle, 1, 128, 256, 16, 16, 1, 0, 7)
+    case(F, oracle, 2, 128, 128, 16, 17, 2, 1, 8)

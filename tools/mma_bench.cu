@@ -1,0 +1,218 @@
+// mma_bench.cu -- development microbenchmark: issue rate of tcgen05.mma (kind::f16,
+// cta_group::1, M = 128) for the operand layouts the hexconv kernels use.  One CTA
+// per SM, one thread issues ITERS MMAs (data is whatever is in shared memory), and
+// the kernel reports cycles per MMA and MACs per cycle per SM.
+//
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1903_01814_b200/csrc \
+//        tools/mma_bench.cu -o /tmp/mma_bench -lcuda
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "tc_ptx.cuh"
+
+using namespace hexconv;
+
+struct Cfg {
+    int M, N, a_mn, b_mn, a_lbo, b_lbo, b_sbo, nmma;  // nmma: MMAs per k-step with distinct N blocks (D offsets)
+    const char* name;
+};
+
+__global__ void __launch_bounds__(128, 1) bench(Cfg c, int iters, long long* out) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t bar;
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bar, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(&slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = slot;
+    if (c.nmma == -3 && warp == 0) {  // whole warp runs the loop, one elected lane issues
+        const uint32_t s = ptx::smem_u32(smem);
+        const uint32_t idesc = ptx::idesc_bf16(c.M, c.N, c.a_mn, c.b_mn);
+        const uint64_t ad0 = ptx::smem_desc_sw128(s, 16, 1024);
+        const uint64_t bd0 = ptx::smem_desc_sw128(s + 65536, 16, 1024);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const uint64_t ad = ad0 + (uint64_t)((i & 7) * 2), bd = bd0 + (uint64_t)((i & 7) * 2);
+            const uint32_t d = tmem + (uint32_t)((i & 1) * c.N);
+            uint32_t pred;
+            asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+            if (pred) ptx::mma_bf16(d, ad, bd, idesc, 1);
+            __syncwarp();
+        }
+        if (threadIdx.x == 0) {
+            ptx::mma_commit(&bar);
+            ptx::mbar_wait(&bar, 0);
+            out[blockIdx.x] = clock64() - t0;
+        }
+    } else if (c.nmma == -2 && threadIdx.x == 0) {  // lane 0 alone, 64-bit descriptor adds per MMA
+        const uint32_t s = ptx::smem_u32(smem);
+        const uint32_t idesc = ptx::idesc_bf16(c.M, c.N, c.a_mn, c.b_mn);
+        const uint64_t ad0 = ptx::smem_desc_sw128(s, 16, 1024);
+        const uint64_t bd0 = ptx::smem_desc_sw128(s + 65536, 16, 1024);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const uint64_t ad = ad0 + (uint64_t)((i & 7) * 2), bd = bd0 + (uint64_t)((i & 7) * 2);
+            ptx::mma_bf16(tmem + (uint32_t)((i & 1) * c.N), ad, bd, idesc, 1);
+        }
+        ptx::mma_commit(&bar);
+        ptx::mbar_wait(&bar, 0);
+        out[blockIdx.x] = clock64() - t0;
+    } else if (c.nmma > -2 && threadIdx.x == 0) {
+        const uint32_t s = ptx::smem_u32(smem);
+        const uint32_t idesc = ptx::idesc_bf16(c.M, c.N, c.a_mn, c.b_mn);
+        if (c.nmma < 0) {  // lean issue loop: descriptors built once, 8 MMAs per iteration, 8 D tiles
+            const uint64_t ad = ptx::smem_desc_sw128(s, 16, 1024);
+            const uint64_t bd = ptx::smem_desc_sw128(s + 65536, 16, 1024);
+            const uint32_t step = (uint32_t)c.N;
+            const long long t0 = clock64();
+            for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) ptx::mma_bf16(tmem + ((j * step) & 511), ad, bd, idesc, 1);
+            }
+            ptx::mma_commit(&bar);
+            ptx::mbar_wait(&bar, 0);
+            out[blockIdx.x] = clock64() - t0;
+        } else {
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const int k = i & 7;
+            // A: MN-major -> 64-row blocks LBO apart, K groups 1024 B apart; K-major -> k*32 B advance
+            const uint64_t ad = c.a_mn ? ptx::smem_desc_sw128(s + k * 2048, c.a_lbo, 1024)
+                                       : ptx::smem_desc_sw128(s + (k & 3) * 32, 16, 1024);
+            const uint32_t bs = s + 65536;
+            const uint64_t bd = c.b_mn ? ptx::smem_desc_sw128(bs + k * 2048, c.b_lbo, c.b_sbo)
+                                       : ptx::smem_desc_sw128(bs + (k & 3) * 32, 16, 1024);
+            const int j = i % c.nmma;
+            ptx::mma_bf16(tmem + (uint32_t)(j * c.N), ad, bd, idesc, 1);
+        }
+        ptx::mma_commit(&bar);
+        ptx::mbar_wait(&bar, 0);
+        const long long t1 = clock64();
+        out[blockIdx.x] = t1 - t0;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
+// A fixed sequence of MMAs per k-step (MN-major A and B, B blocks 1024 B apart), lean issue.
+template <int N0, int N1, int N2, int N3>
+__global__ void __launch_bounds__(128, 1) bench_seq(int iters, long long* out) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t bar;
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bar, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(&slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        const uint32_t s = ptx::smem_u32(smem);
+        const uint64_t ad0 = ptx::smem_desc_sw128(s, 16384, 1024);
+        const uint64_t bd0 = ptx::smem_desc_sw128(s + 32768, 1024, 1024);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const uint64_t ad = ad0 + (uint64_t)((i & 7) * 128), bd = bd0 + (uint64_t)((i & 7) * 128);
+            ptx::mma_bf16(tmem, ad, bd, ptx::idesc_bf16(128, N0, 1, 1), 1);
+            if (N1) ptx::mma_bf16(tmem + N0, ad, bd + 1152, ptx::idesc_bf16(128, N1 ? N1 : 64, 1, 1), 1);
+            if (N2) ptx::mma_bf16(tmem + N0 + N1, ad, bd + 2304, ptx::idesc_bf16(128, N2 ? N2 : 64, 1, 1), 1);
+            if (N3) ptx::mma_bf16(tmem + N0 + N1 + N2, ad, bd + 3456, ptx::idesc_bf16(128, N3 ? N3 : 64, 1, 1), 1);
+        }
+        ptx::mma_commit(&bar);
+        ptx::mbar_wait(&bar, 0);
+        out[blockIdx.x] = clock64() - t0;
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
+template <int N0, int N1, int N2, int N3>
+static void run_seq(const char* name, long long* d_out) {
+    const int smem = 200 * 1024, iters = 4096;
+    cudaFuncSetAttribute(bench_seq<N0, N1, N2, N3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    bench_seq<N0, N1, N2, N3><<<148, 128, smem>>>(iters, d_out);
+    bench_seq<N0, N1, N2, N3><<<148, 128, smem>>>(iters, d_out);
+    cudaDeviceSynchronize();
+    long long h[148];
+    cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < 148; ++i) avg += h[i];
+    avg /= 148;
+    const double cyc = avg / iters;
+    const int N = N0 + N1 + N2 + N3;
+    printf("%-36s %7.1f cyc/step (ideal %5.1f)  %7.0f MAC/clk/SM\n", name, cyc, N / 2.0, 128.0 * N * 16 / cyc);
+}
+
+int main() {
+    Cfg cfgs[] = {
+        {128, 128, 0, 0, 16, 16, 1024, -2, "lane0 loop desc-add N=128"},
+        {128, 128, 0, 0, 16, 16, 1024, -3, "warp loop + elect N=128"},
+        {128, 256, 0, 0, 16, 16, 1024, -3, "warp loop + elect N=256"},
+        {128, 256, 0, 0, 16, 16, 1024, -1, "lean K-major N=256"},
+        {128, 128, 0, 0, 16, 16, 1024, -1, "lean K-major N=128"},
+        {128, 64, 0, 0, 16, 16, 1024, -1, "lean K-major N=64"},
+        {128, 32, 0, 0, 16, 16, 1024, -1, "lean K-major N=32"},
+        {64, 256, 0, 0, 16, 16, 1024, 1, "M=64 K-major A,B  N=256"},
+        {64, 128, 0, 0, 16, 16, 1024, 2, "M=64 K-major A,B  N=128"},
+        {128, 256, 0, 0, 16, 16, 1024, 1, "K-major A,B  N=256"},
+        {128, 128, 0, 0, 16, 16, 1024, 2, "K-major A,B  N=128 (2 D)"},
+        {128, 64, 0, 0, 16, 16, 1024, 4, "K-major A,B  N=64 (4 D)"},
+        {128, 256, 1, 1, 16384, 8192, 1024, 1, "MN-major A,B N=256 LBO 8K"},
+        {128, 192, 1, 1, 16384, 1024, 1024, 2, "MN-major A,B N=192 LBO 1K"},
+        {128, 128, 1, 1, 16384, 1024, 1024, 4, "MN-major A,B N=128 LBO 1K"},
+        {128, 64, 1, 1, 16384, 1024, 1024, 8, "MN-major A,B N=64"},
+        {128, 256, 1, 1, 16384, 1024, 1024, 2, "MN-major A,B N=256 LBO 1K"},
+        {128, 256, 1, 1, 16384, 1024, 3072, 2, "MN-major A,B N=256 LBO 1K SBO 3K"},
+        {128, 256, 1, 0, 16384, 16, 1024, 1, "MN-major A, K-major B N=256"},
+        {128, 256, 0, 1, 16, 8192, 1024, 1, "K-major A, MN-major B N=256"},
+    };
+    long long* d_out;
+    cudaMalloc(&d_out, 148 * sizeof(long long));
+    run_seq<128, 192, 128, 64>("seq n1: 128 192 128 64", d_out);
+    run_seq<128, 192, 128, 0>("seq n1: 128 192 128", d_out);
+    run_seq<192, 256, 64, 0>("seq n2 g0: 192 256 64", d_out);
+    run_seq<256, 64, 0, 0>("seq n2 g1: 256 64", d_out);
+    run_seq<256, 192, 0, 0>("seq n2 g2: 256 192", d_out);
+    run_seq<128, 128, 128, 128>("seq 4x128", d_out);
+    run_seq<192, 0, 0, 0>("seq 192", d_out);
+    run_seq<256, 256, 0, 0>("seq 256 256", d_out);
+    const int smem = 200 * 1024;
+    cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int iters = 8192;
+    for (const Cfg& c : cfgs) {
+        bench<<<148, 128, smem>>>(c, iters, d_out);
+        bench<<<148, 128, smem>>>(c, iters, d_out);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { printf("%s: %s\n", c.name, cudaGetErrorString(e)); return 1; }
+        long long h[148];
+        cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+        double avg = 0;
+        for (int i = 0; i < 148; ++i) avg += h[i];
+        avg /= 148;
+        const double cyc = avg / iters;
+        printf("%-36s %7.1f cyc/MMA  %7.0f MAC/clk/SM\n", c.name, cyc, (double)c.M * c.N * 16 / cyc);
+    }
+    return 0;
+}
