@@ -283,8 +283,8 @@ def main():
         share[kind] = share.get(kind, 0.0) + dt
         if kind in ("fwd", "dgrad", "wgrad"):
             fl = per_layer[l][0] * B
-            if l == 0:
-                add("stencil_cin1 (layer 1 fwd+wgrad, CUDA cores)", dt, fl, "TFLOP/s")
+            if l == 0:  # Cin = 1: warp-level tensor-core kernels bound by the y / dy stream (HBM bytes)
+                add("smallc_mma (layer 1 fwd + wgrad, mma.sync, HBM-bound)", dt, model.l1_bytes(kind), "GB/s")
             elif kind == "wgrad":
                 add("tc_conv_wgrad (tcgen05, layers 2-6)", dt, fl, "TFLOP/s")
             else:
@@ -297,7 +297,7 @@ def main():
     kernels = {}
     for name, (fms, units, unit, n) in fam.items():
         ach = units / (fms / 1e3) / (1e12 if unit == "TFLOP/s" else 1e9)
-        pk = peak_gbs if unit == "GB/s" else (74.4 if "CUDA cores" in name else peak_tf)
+        pk = peak_gbs if unit == "GB/s" else peak_tf
         kernels[name] = {"ms_per_step": fms / args.steps, "achieved": ach, "unit": unit, "peak": pk,
                          "frac": ach / pk, "launches_per_step": n / args.steps}
     dom = max(fam, key=lambda k: fam[k][0])

@@ -57,6 +57,12 @@ bool use_tc_bwd_data(const hex_conv2d_desc_t* d, const Geom& g) {
 bool use_smallc(const hex_conv2d_desc_t* d, const Geom& g) {
     return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && smallc_supported(g, d->in_channels, d->out_channels);
 }
+bool use_f32wg(const hex_conv2d_desc_t* d, const Geom& g) {
+    return f32_wgrad_supported(g, d->in_channels, d->out_channels, d->dtype, d->layout);
+}
+bool use_c1(const hex_conv2d_desc_t* d, const Geom& g) {
+    return c1_conv_supported(g, d->in_channels, d->out_channels, d->dtype, d->layout);
+}
 bool use_tc_wgrad(const hex_conv2d_desc_t* d, const Geom& g) {
     return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_wgrad_supported(g, d->in_channels, d->out_channels);
 }
@@ -148,6 +154,8 @@ hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* d, int32_t pass,
         case 2:
             *bytes = use_tc_wgrad(d, g)  ? tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
                      : use_smallc(d, g) ? smallc_wgrad_ws_bytes(g, d->out_channels)
+                     : use_c1(d, g)     ? c1_wgrad_ws_bytes(g, d->out_channels)
+                     : use_f32wg(d, g)  ? f32_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
                                         : direct_wgrad_ws_bytes(g, d->in_channels, d->out_channels);
             return HEX_OK;
         default: return HEX_ERR_INVALID_ARG;
@@ -190,6 +198,8 @@ hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* d, const void* x, const voi
         if (((uintptr_t)y & 3) != 0) return HEX_ERR_ALIGNMENT;
         return smallc_fwd(x, w, bias, y, g, d->out_channels, fuse_relu, s);
     }
+    if (use_c1(d, g)) return c1_conv_fwd((const float*)x, (const float*)w, bias, (float*)y, g, d->out_channels,
+                                         fuse_relu, s);
     if (tiled_supported(g, d->dtype, d->layout))
         return tiled_conv((const float*)x, (const float*)w, bias, nullptr, (float*)y, g, d->in_channels,
                           d->out_channels, fuse_relu, 0, s);
@@ -249,6 +259,15 @@ hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* d, const void* x, co
         if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
         if (((uintptr_t)dy & 3) != 0) return HEX_ERR_ALIGNMENT;
         return smallc_wgrad(x, dy, dw, dbias, accumulate, g, d->out_channels, ws, s);
+    }
+    if (use_c1(d, g)) {
+        if (!ws || ws_bytes < c1_wgrad_ws_bytes(g, d->out_channels)) return HEX_ERR_WORKSPACE;
+        return c1_conv_wgrad((const float*)x, (const float*)dy, dw, dbias, accumulate, g, d->out_channels, ws, s);
+    }
+    if (use_f32wg(d, g)) {
+        if (!ws || ws_bytes < f32_wgrad_ws_bytes(g, d->in_channels, d->out_channels)) return HEX_ERR_WORKSPACE;
+        return f32_wgrad((const float*)x, (const float*)dy, dw, dbias, accumulate, g, d->in_channels,
+                         d->out_channels, ws, s);
     }
     const size_t need = direct_wgrad_ws_bytes(g, d->in_channels, d->out_channels);
     if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;

@@ -40,6 +40,9 @@ struct PoolArgs {
     void* dx;
 };
 hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st);
+// NCHW plane-staged pools (plane_kernels.cu); return false when the shape is not covered
+bool pool_plane_fwd(const PoolArgs& a, cudaStream_t st);
+bool pool_plane_bwd(const PoolArgs& a, cudaStream_t st);
 hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st);
 
 // tcgen05 implicit-GEMM path (bf16 NHWC, stride 1).
@@ -91,6 +94,20 @@ hex_status_t smallc_mma_fwd(const void* x, const void* w, const float* bias, voi
                             int relu, cudaStream_t st);
 hex_status_t smallc_mma_wgrad(const void* x, const void* dy, float* dw, float* dbias, int accumulate, const Geom& g,
                               int Cout, void* ws, cudaStream_t st);
+
+// single-input-channel fp32 NCHW stride-1 conv (plane_kernels.cu)
+bool c1_conv_supported(const Geom& g, int Cin, int Cout, int dtype, int layout);
+size_t c1_wgrad_ws_bytes(const Geom& g, int Cout);
+hex_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, float* y, const Geom& g, int Cout,
+                         int relu, cudaStream_t st);
+hex_status_t c1_conv_wgrad(const float* x, const float* dy, float* dw, float* dbias, int accumulate, const Geom& g,
+                           int Cout, void* ws, cudaStream_t st);
+
+// fp32 NCHW weight gradient, column-walking sliding windows (f32_wgrad.cu)
+bool f32_wgrad_supported(const Geom& g, int Cin, int Cout, int dtype, int layout);
+size_t f32_wgrad_ws_bytes(const Geom& g, int Cin, int Cout);
+hex_status_t f32_wgrad(const float* x, const float* dy, float* dw, float* dbias, int accumulate, const Geom& g,
+                       int Cin, int Cout, void* ws, cudaStream_t st);
 
 // register-blocked fp32 NCHW stride-1 conv (forward / transposed backward-data)
 bool tiled_supported(const Geom& g, int dtype, int layout);

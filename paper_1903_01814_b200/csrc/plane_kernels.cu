@@ -1,0 +1,530 @@
+// plane_kernels.cu -- NCHW kernels that stage whole (image, channel) planes in
+// shared memory: hexagonal max / avg pooling (forward, backward) for any dtype,
+// and the single-input-channel fp32 convolution (forward, weight gradient) of
+// BASELINE config 3 (40x40 camera images, 1 -> 16 channels).
+//
+// These layers are HBM-bound: every input element is read once from HBM into
+// shared memory with coalesced 16-byte loads, every output element written
+// once, and the hexagonal neighbourhood gathers (pooling
+// PAPER.md:202-205) run against shared memory.  The per-element index work of
+// the generic kernels (div/mod decode, per-tap bounds checks against global
+// memory) is what kept them at a few percent of HBM bandwidth.
+//
+// Semantics are those of the generic kernels (A4, A8, A9): conv is a
+// cross-correlation with off-grid taps = 0; max pooling takes the first strict
+// maximum in canonical tap order and stores its tap index; average pooling
+// divides by the number of in-grid taps; backward passes gather over the
+// candidate centres (no atomics).
+#include <cstdlib>
+
+#include "common.cuh"
+#include "geometry.cuh"
+#include "kernels.h"
+#include "pool_tables.cuh"
+
+namespace hexconv {
+
+namespace {
+
+constexpr int PL_THREADS = 256;
+constexpr int PL_MAX_ELEMS = 12288;  // plane elements staged (48 KB of fp32)
+
+template <typename T>
+__device__ __forceinline__ void stage_plane(const T* __restrict__ src, float* dst, int n) {
+    if (sizeof(T) == 4 && (n & 3) == 0 && ((uintptr_t)src & 15) == 0) {
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        for (int i = threadIdx.x; i < (n >> 2); i += blockDim.x) reinterpret_cast<float4*>(dst)[i] = __ldg(s4 + i);
+    } else {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = to_f32(src[i]);
+    }
+}
+
+// number of in-grid taps of the window centred at (r, c)
+__device__ __forceinline__ int window_count(int n, int H, int W, int parity, int r, int c) {
+    const int p = (c + parity) & 1;
+    int cnt = 0;
+    for (int dc = -n; dc <= n; ++dc) {
+        const int cc = c + dc;
+        if (cc < 0 || cc >= W) continue;
+        const int len = 2 * n + 1 - (dc < 0 ? -dc : dc);
+        const int top = r + tap_top(n, dc, p);
+        cnt += max(min(top + len, H) - max(top, 0), 0);
+    }
+    return cnt;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Pool forward: grid-stride over planes; per plane the input is staged, every
+// thread computes output pixels from shared memory.
+// ---------------------------------------------------------------------------
+template <typename T, int N, int S>
+__global__ void __launch_bounds__(PL_THREADS)
+pool_fwd_plane_kernel(const T* __restrict__ x, T* __restrict__ y, uint8_t* __restrict__ am, Geom g, int planes,
+                      int pb, int mode) {
+    // pb consecutive planes are staged per iteration (more bytes in flight per block)
+    extern __shared__ float xs[];
+    const int HW = g.H * g.W, HoWo = g.Ho * g.Wo;
+    const int ngroups = (planes + pb - 1) / pb;
+    for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const int pl0 = grp * pb;
+        const int np = min(pb, planes - pl0);
+        __syncthreads();
+        stage_plane<T>(x + (int64_t)pl0 * HW, xs, np * HW);
+        __syncthreads();
+        for (int i = threadIdx.x; i < np * HoWo; i += blockDim.x) {
+            const int pp = i / HoWo, o = i - pp * HoWo;
+            const float* xp = xs + pp * HW;
+            const int R = o / g.Wo, C = o - R * g.Wo;
+            const int c = S * C;
+            const int r = hex_rho(C, S, g.parity) + S * R;
+            const int p = (c + g.parity) & 1;
+            int t = 0, best = -1, cnt = 0;
+            float bv = 0.f, sum = 0.f;
+#pragma unroll
+            for (int dc = -N; dc <= N; ++dc) {
+                const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
+                const int cc = c + dc;
+                const int top = r + tap_top(N, dc, p);
+#pragma unroll
+                for (int k = 0; k < len; ++k, ++t) {
+                    const int rr = top + k;
+                    if (cc < 0 || cc >= g.W || rr < 0 || rr >= g.H) continue;
+                    const float v = xp[rr * g.W + cc];
+                    if (mode == HEX_POOL_MAX) {
+                        if (best < 0 || v > bv) { best = t; bv = v; }
+                    } else {
+                        sum += v;
+                        ++cnt;
+                    }
+                }
+            }
+            const int64_t yo = (int64_t)pl0 * HoWo + i;
+            if (mode == HEX_POOL_MAX) {
+                y[yo] = from_f32<T>(bv);  // exact: staged values are the inputs (fp32 or widened bf16)
+                if (am) am[yo] = (uint8_t)best;
+            } else {
+                y[yo] = from_f32<T>(sum / (float)cnt);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pool backward: dy (avg: pre-divided by the window's in-grid count) and the
+// argmax plane are staged; every thread gathers its input pixels' candidates.
+// ---------------------------------------------------------------------------
+template <typename T, int N, int S>
+__global__ void __launch_bounds__(PL_THREADS)
+pool_bwd_plane_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am, T* __restrict__ dx, Geom g,
+                      int planes, int mode) {
+    extern __shared__ float ds[];
+    uint8_t* as = reinterpret_cast<uint8_t*>(ds + g.Ho * g.Wo);
+    const int HW = g.H * g.W, HoWo = g.Ho * g.Wo;
+    constexpr int s = S;
+    for (int pl = blockIdx.x; pl < planes; pl += gridDim.x) {
+        __syncthreads();
+        for (int o = threadIdx.x; o < HoWo; o += blockDim.x) {
+            float v = to_f32(dy[(int64_t)pl * HoWo + o]);
+            if (mode == HEX_POOL_MAX) {
+                as[o] = am[(int64_t)pl * HoWo + o];
+            } else {
+                const int R = o / g.Wo, C = o - R * g.Wo;
+                v = v / (float)window_count(N, g.H, g.W, g.parity, hex_rho(C, s, g.parity) + s * R, s * C);
+            }
+            ds[o] = v;
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < HW; q += blockDim.x) {
+            const int r = q / g.W, c = q - r * g.W;
+            float acc = 0.f;
+            int t = 0;
+#pragma unroll
+            for (int dc = -N; dc <= N; ++dc) {
+                const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
+                const int oc = c - dc;  // candidate centre column
+                const bool colok = oc >= 0 && oc % s == 0 && oc / s < g.Wo;
+                const int Cq = oc / s;
+                const int po = (oc + g.parity) & 1;
+                const int rho = colok ? hex_rho(Cq, s, g.parity) : 0;
+                const int top = tap_top(N, dc, po);
+#pragma unroll
+                for (int k = 0; k < len; ++k, ++t) {
+                    if (!colok) continue;
+                    const int d = r - (top + k) - rho;
+                    if (d < 0 || d % s != 0) continue;
+                    const int Rq = d / s;
+                    if (Rq >= g.Ho) continue;
+                    const int o = Rq * g.Wo + Cq;
+                    if (mode == HEX_POOL_MAX) {
+                        if (as[o] == t) acc += ds[o];
+                    } else {
+                        acc += ds[o];
+                    }
+                }
+            }
+            dx[(int64_t)pl * HW + q] = from_f32<T>(acc);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pool backward for n = 1, stride 2 (configs 2 and 3), NCHW: one thread per 2x2
+// input block of one plane; its candidate windows come from the compile-time
+// (parity, rho) tables of pool_tables.cuh and are read straight from global
+// memory (neighbouring threads read neighbouring windows: coalesced, L1 reuse).
+// max: routed where the stored argmax equals the tap; avg: dy / in-grid count.
+// ---------------------------------------------------------------------------
+template <typename T, int P, int RHO, bool MAX>
+__device__ __forceinline__ void pool_bwd_blk_nchw(const T* __restrict__ dyp, const uint8_t* __restrict__ amp,
+                                                  T* __restrict__ dxp, const Geom& g, int Rp, int C) {
+    float v[2][3];
+    int a[2][3];
+#pragma unroll
+    for (int dC = 0; dC < 2; ++dC)
+#pragma unroll
+        for (int dR = -1; dR <= 1; ++dR) {
+            v[dC][dR + 1] = 0.f;
+            a[dC][dR + 1] = -1;
+            if (blk_uses(P, RHO, dC, dR)) {
+                const int Cw = C + dC, Rw = Rp + dR;
+                if (Cw < g.Wo && Rw >= 0 && Rw < g.Ho) {
+                    const int o = Rw * g.Wo + Cw;
+                    float d = to_f32(dyp[o]);
+                    if (MAX) {
+                        a[dC][dR + 1] = amp[o];
+                    } else {
+                        const int rho = Cw & 1;  // = hex_rho(Cw, 2, parity) for parity in {0, 1}
+                        d = d / (float)window_count(1, g.H, g.W, g.parity, rho + 2 * Rw, 2 * Cw);
+                    }
+                    v[dC][dR + 1] = d;
+                }
+            }
+        }
+#pragma unroll
+    for (int pr = 0; pr < 2; ++pr) {
+        const int r = 2 * Rp + pr;
+        if (r >= g.H) continue;
+#pragma unroll
+        for (int pc = 0; pc < 2; ++pc) {
+            const int c = 2 * C + pc;
+            if (c >= g.W) continue;
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const Cand cd = blk_cand(P, RHO, pc, pr, k);
+                if (cd.tap < 0) continue;
+                const float d = v[cd.dC][cd.dR + 1];
+                if (!MAX || a[cd.dC][cd.dR + 1] == cd.tap) acc += d;
+            }
+            dxp[r * g.W + c] = from_f32<T>(acc);
+        }
+    }
+}
+
+template <typename T, int P, bool MAX>
+__global__ void __launch_bounds__(PL_THREADS)
+pool_bwd_n1s2_nchw_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am, T* __restrict__ dx, Geom g,
+                          int64_t planes) {
+    const int nC = g.Wo, nR = (g.H + 1) / 2;
+    const int half = (nC + 1) >> 1;  // block columns: even C first, then odd C (rho warp-uniform)
+    const int64_t per_plane = (int64_t)nR * nC;
+    const int64_t total = planes * per_plane;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pl = i / per_plane;
+        const int rem = (int)(i - pl * per_plane);
+        const int Rp = rem / nC, ci = rem - Rp * nC;
+        const int C = ci < half ? 2 * ci : 2 * (ci - half) + 1;
+        const T* dyp = dy + pl * g.Ho * g.Wo;
+        const uint8_t* amp = MAX ? am + pl * g.Ho * g.Wo : nullptr;
+        T* dxp = dx + pl * g.H * g.W;
+        if (C & 1) pool_bwd_blk_nchw<T, P, 1, MAX>(dyp, amp, dxp, g, Rp, C);
+        else pool_bwd_blk_nchw<T, P, 0, MAX>(dyp, amp, dxp, g, Rp, C);
+    }
+}
+
+template <typename T>
+static void launch_bwd_n1s2(const PoolArgs& a, cudaStream_t st) {
+    const int64_t planes = (int64_t)a.g.B * a.C;
+    const int64_t total = planes * ((a.g.H + 1) / 2) * a.g.Wo;
+    int blocks = (int)((total + PL_THREADS - 1) / PL_THREADS);
+    if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+    const bool mx = a.mode == HEX_POOL_MAX;
+    const T* dy = (const T*)a.dy;
+    T* dx = (T*)a.dx;
+    if (a.g.parity & 1) {
+        if (mx) pool_bwd_n1s2_nchw_kernel<T, 1, true><<<blocks, PL_THREADS, 0, st>>>(dy, a.argmax_in, dx, a.g, planes);
+        else pool_bwd_n1s2_nchw_kernel<T, 1, false><<<blocks, PL_THREADS, 0, st>>>(dy, nullptr, dx, a.g, planes);
+    } else {
+        if (mx) pool_bwd_n1s2_nchw_kernel<T, 0, true><<<blocks, PL_THREADS, 0, st>>>(dy, a.argmax_in, dx, a.g, planes);
+        else pool_bwd_n1s2_nchw_kernel<T, 0, false><<<blocks, PL_THREADS, 0, st>>>(dy, nullptr, dx, a.g, planes);
+    }
+}
+
+static bool plane_pool_ok(const PoolArgs& a) {
+    if (a.layout != HEX_NCHW || (a.g.n != 1 && a.g.n != 2) || (a.g.s != 1 && a.g.s != 2) || getenv("HEXCONV_NO_PLANE"))
+        return false;
+    const int64_t HW = (int64_t)a.g.H * a.g.W;
+    return HW <= PL_MAX_ELEMS;
+}
+
+static int plane_grid(int64_t planes) {
+    const int64_t cap = (int64_t)num_sms() * 8;
+    return (int)(planes < cap ? planes : cap);
+}
+
+template <typename T, int N, int S>
+static void launch_pool_fwd(const PoolArgs& a, cudaStream_t st) {
+    const int planes = a.g.B * a.C;
+    const int HW = a.g.H * a.g.W;
+    int pb = PL_MAX_ELEMS / HW;  // planes staged per iteration (<= 48 KB)
+    if (pb > 4) pb = 4;
+    if (pb < 1) pb = 1;
+    const size_t smem = (size_t)pb * HW * sizeof(float);
+    pool_fwd_plane_kernel<T, N, S><<<plane_grid((planes + pb - 1) / pb), PL_THREADS, smem, st>>>(
+        (const T*)a.x, (T*)a.y, a.argmax, a.g, planes, pb, a.mode);
+}
+
+template <typename T, int N, int S>
+static void launch_pool_bwd(const PoolArgs& a, cudaStream_t st) {
+    const int planes = a.g.B * a.C;
+    const size_t smem = (size_t)a.g.Ho * a.g.Wo * (sizeof(float) + 1) + 16;
+    pool_bwd_plane_kernel<T, N, S><<<plane_grid(planes), PL_THREADS, smem, st>>>(
+        (const T*)a.dy, a.argmax_in, (T*)a.dx, a.g, planes, a.mode);
+}
+
+template <typename T>
+static void dispatch_plane(const PoolArgs& a, cudaStream_t st, bool fwd) {
+#define HEX_PL(NN, SS) (fwd ? launch_pool_fwd<T, NN, SS>(a, st) : launch_pool_bwd<T, NN, SS>(a, st))
+    if (a.g.n == 1) {
+        if (a.g.s == 1) HEX_PL(1, 1); else HEX_PL(1, 2);
+    } else {
+        if (a.g.s == 1) HEX_PL(2, 1); else HEX_PL(2, 2);
+    }
+#undef HEX_PL
+}
+
+bool pool_plane_fwd(const PoolArgs& a, cudaStream_t st) {
+    if (!plane_pool_ok(a)) return false;
+    if (a.dtype == HEX_F32) dispatch_plane<float>(a, st, true);
+    else dispatch_plane<__nv_bfloat16>(a, st, true);
+    return true;
+}
+
+bool pool_plane_bwd(const PoolArgs& a, cudaStream_t st) {
+    if (!plane_pool_ok(a)) return false;
+    if (a.g.n == 1 && a.g.s == 2 && (a.g.parity == 0 || a.g.parity == 1)) {
+        if (a.dtype == HEX_F32) launch_bwd_n1s2<float>(a, st);
+        else launch_bwd_n1s2<__nv_bfloat16>(a, st);
+        return true;
+    }
+    if (a.dtype == HEX_F32) dispatch_plane<float>(a, st, false);
+    else dispatch_plane<__nv_bfloat16>(a, st, false);
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// Single-input-channel fp32 convolution, stride 1 (config 3 layer 1).
+// Forward: blocks of 128 threads own one band of C1_RB rows of one image and
+// COB output channels (weights + bias in registers); the zero-padded band of x
+// is staged in shared memory, each thread computes whole pixels, stores are
+// coalesced along each output channel plane.
+// ---------------------------------------------------------------------------
+constexpr int C1_RB = 8;
+constexpr int C1_THREADS = 128;
+
+template <int N, int COB>
+__global__ void __launch_bounds__(C1_THREADS)
+c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
+              float* __restrict__ y, int B, int H, int W, int parity, int Cout, int relu) {
+    constexpr int T = 3 * N * (N + 1) + 1;
+    extern __shared__ float xs[];  // [(C1_RB + 2N) x (W + 2N)]
+    const int Wp = W + 2 * N;
+    const int nb = (H + C1_RB - 1) / C1_RB;
+    const int b = blockIdx.x / nb, r0 = (blockIdx.x - b * nb) * C1_RB;
+    const int rows = min(C1_RB, H - r0);
+    const int co0 = blockIdx.y * COB;
+    float wr[T][COB], br[COB];
+#pragma unroll
+    for (int j = 0; j < COB; ++j) {
+        const bool ok = co0 + j < Cout;
+        br[j] = (bias && ok) ? __ldg(bias + co0 + j) : 0.f;
+#pragma unroll
+        for (int t = 0; t < T; ++t) wr[t][j] = ok ? __ldg(w + (int64_t)(co0 + j) * T + t) : 0.f;
+    }
+    for (int i = threadIdx.x; i < (rows + 2 * N) * Wp; i += blockDim.x) {
+        const int rr = i / Wp, cc = i - rr * Wp;
+        const int r = r0 - N + rr, c = cc - N;
+        xs[i] = (r >= 0 && r < H && c >= 0 && c < W) ? __ldg(x + ((int64_t)b * H + r) * W + c) : 0.f;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < rows * W; q += blockDim.x) {
+        const int rl = q / W, c = q - rl * W;
+        const int p = (c + parity) & 1;
+        float acc[COB];
+#pragma unroll
+        for (int j = 0; j < COB; ++j) acc[j] = br[j];
+        const float* xc = xs + (rl + N) * Wp + (c + N);
+        int t = 0;
+#pragma unroll
+        for (int dc = -N; dc <= N; ++dc) {
+            const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
+            const int top = tap_top(N, dc, p);
+#pragma unroll
+            for (int k = 0; k < len; ++k, ++t) {
+                const float v = xc[(top + k) * Wp + dc];
+#pragma unroll
+                for (int j = 0; j < COB; ++j) acc[j] = fmaf(v, wr[t][j], acc[j]);
+            }
+        }
+        float* yp = y + (((int64_t)b * Cout + co0) * H + r0 + rl) * W + c;
+#pragma unroll
+        for (int j = 0; j < COB; ++j)
+            if (co0 + j < Cout) yp[(int64_t)j * H * W] = relu ? fmaxf(acc[j], 0.f) : acc[j];
+    }
+}
+
+// Weight gradient: persistent blocks over (image, band); thread = (output channel,
+// pixel slice): per pixel one coalesced dy load and T shared-memory taps.  Fixed-
+// order reductions: slices of a block in slice order, then blocks in block order
+// (8 lanes per output, fixed shuffle tree).  part[block][co][T + 1].
+template <int N>
+__global__ void __launch_bounds__(PL_THREADS)
+c1_wgrad_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ part, int B, int H,
+                int W, int parity, int Cout, int slices) {
+    constexpr int T = 3 * N * (N + 1) + 1;
+    extern __shared__ float sm[];
+    const int Wp = W + 2 * N;
+    float* xs = sm;                                   // [(C1_RB + 2N) x Wp]
+    float* red = xs + (C1_RB + 2 * N) * Wp;           // [Cout][slices][T + 1]
+    const int co = threadIdx.x / slices, sl = threadIdx.x - co * slices;
+    const bool active = co < Cout;
+    const int nb = (H + C1_RB - 1) / C1_RB;
+    float acc[T + 1];
+#pragma unroll
+    for (int t = 0; t <= T; ++t) acc[t] = 0.f;
+    for (int band = blockIdx.x; band < B * nb; band += gridDim.x) {
+        const int b = band / nb, r0 = (band - b * nb) * C1_RB;
+        const int rows = min(C1_RB, H - r0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < (rows + 2 * N) * Wp; i += blockDim.x) {
+            const int rr = i / Wp, cc = i - rr * Wp;
+            const int r = r0 - N + rr, c = cc - N;
+            xs[i] = (r >= 0 && r < H && c >= 0 && c < W) ? __ldg(x + ((int64_t)b * H + r) * W + c) : 0.f;
+        }
+        __syncthreads();
+        if (!active) continue;
+        const float* dyp = dy + (((int64_t)b * Cout + co) * H + r0) * W;
+#pragma unroll 4
+        for (int q = sl; q < rows * W; q += slices) {
+            const int rl = q / W, c = q - rl * W;
+            const int p = (c + parity) & 1;
+            const float g = __ldg(dyp + q);
+            const float* xc = xs + (rl + N) * Wp + (c + N);
+            int t = 0;
+#pragma unroll
+            for (int dc = -N; dc <= N; ++dc) {
+                const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
+                const int top = tap_top(N, dc, p);
+#pragma unroll
+                for (int k = 0; k < len; ++k, ++t) acc[t] = fmaf(g, xc[(top + k) * Wp + dc], acc[t]);
+            }
+            acc[T] += g;
+        }
+    }
+    __syncthreads();
+    if (active)
+#pragma unroll
+        for (int t = 0; t <= T; ++t) red[(co * slices + sl) * (T + 1) + t] = acc[t];
+    __syncthreads();
+    for (int i = threadIdx.x; i < Cout * (T + 1); i += blockDim.x) {
+        const int c = i / (T + 1), t = i - c * (T + 1);
+        float s = 0.f;
+        for (int k = 0; k < slices; ++k) s += red[(c * slices + k) * (T + 1) + t];
+        part[(int64_t)blockIdx.x * Cout * (T + 1) + i] = s;
+    }
+}
+
+__global__ void c1_wgrad_reduce_kernel(const float* __restrict__ part, int nblocks, int Cout, int NA,
+                                       float* __restrict__ dw, float* __restrict__ dbias, int accumulate) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int o = gid >> 3, sub = gid & 7;
+    const int total = Cout * NA;
+    float s = 0.f;
+    if (o < total)
+        for (int k = sub; k < nblocks; k += 8) s += part[(int64_t)k * total + o];
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (o >= total || sub != 0) return;
+    const int co = o / NA, t = o - co * NA;
+    if (t == NA - 1) {
+        if (dbias) dbias[co] = accumulate ? dbias[co] + s : s;
+    } else {
+        float* d = dw + (int64_t)co * (NA - 1) + t;
+        *d = accumulate ? *d + s : s;
+    }
+}
+
+bool c1_conv_supported(const Geom& g, int Cin, int Cout, int dtype, int layout) {
+    if (getenv("HEXCONV_NO_PLANE")) return false;
+    if (dtype != HEX_F32 || layout != HEX_NCHW || Cin != 1 || g.s != 1 || (g.n != 1 && g.n != 2)) return false;
+    if (Cout > PL_THREADS || g.B > 65535 * 8) return false;
+    const int64_t band = (int64_t)(C1_RB + 2 * g.n) * (g.W + 2 * g.n);
+    return band * 4 + (int64_t)PL_THREADS * (g.T + 1) * 4 <= 200 * 1024;
+}
+
+static int c1_wgrad_blocks(const Geom& g) {
+    const int64_t bands = (int64_t)g.B * ((g.H + C1_RB - 1) / C1_RB);
+    const int64_t cap = (int64_t)num_sms() * 8;
+    return (int)(bands < cap ? bands : cap);
+}
+
+size_t c1_wgrad_ws_bytes(const Geom& g, int Cout) { return (size_t)c1_wgrad_blocks(g) * Cout * (g.T + 1) * 4; }
+
+hex_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, float* y, const Geom& g, int Cout,
+                         int relu, cudaStream_t st) {
+    const size_t smem = (size_t)(C1_RB + 2 * g.n) * (g.W + 2 * g.n) * 4;
+    const int nb = (g.H + C1_RB - 1) / C1_RB;
+    if (g.n == 1) {
+        constexpr int COB = 8;
+        dim3 grid(g.B * nb, ceil_div(Cout, COB));
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(c1_fwd_kernel<1, COB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        c1_fwd_kernel<1, COB><<<grid, C1_THREADS, smem, st>>>(x, w, bias, y, g.B, g.H, g.W, g.parity, Cout, relu);
+    } else {
+        constexpr int COB = 4;
+        dim3 grid(g.B * nb, ceil_div(Cout, COB));
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(c1_fwd_kernel<2, COB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        c1_fwd_kernel<2, COB><<<grid, C1_THREADS, smem, st>>>(x, w, bias, y, g.B, g.H, g.W, g.parity, Cout, relu);
+    }
+    count_launch();
+    return last_launch_status();
+}
+
+hex_status_t c1_conv_wgrad(const float* x, const float* dy, float* dw, float* dbias, int accumulate, const Geom& g,
+                           int Cout, void* ws, cudaStream_t st) {
+    const int nb = c1_wgrad_blocks(g);
+    const int slices = PL_THREADS / Cout;
+    const size_t smem = ((size_t)(C1_RB + 2 * g.n) * (g.W + 2 * g.n) + (size_t)PL_THREADS * (g.T + 1)) * 4;
+    float* part = (float*)ws;
+    if (g.n == 1) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(c1_wgrad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        c1_wgrad_kernel<1><<<nb, PL_THREADS, smem, st>>>(x, dy, part, g.B, g.H, g.W, g.parity, Cout, slices);
+    } else {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(c1_wgrad_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        c1_wgrad_kernel<2><<<nb, PL_THREADS, smem, st>>>(x, dy, part, g.B, g.H, g.W, g.parity, Cout, slices);
+    }
+    count_launch();
+    const int NA = g.T + 1;
+    c1_wgrad_reduce_kernel<<<ceil_div((int64_t)Cout * NA * 8, 256), 256, 0, st>>>(part, nb, Cout, NA, dw, dbias,
+                                                                                  accumulate);
+    count_launch();
+    return last_launch_status();
+}
+
+}  // namespace hexconv

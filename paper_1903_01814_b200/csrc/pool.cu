@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "geometry.cuh"
 #include "kernels.h"
+#include "pool_tables.cuh"
 
 namespace hexconv {
 
@@ -718,45 +719,6 @@ maxpool_bwd_n1s2_kernel(const uint4* __restrict__ dy, const uint2* __restrict__ 
 // the same value as the fp32 sum rounded once).  Columns are visited even C
 // first, then odd C, so rho is warp-uniform.
 // ---------------------------------------------------------------------------
-struct Cand {
-    int dC, dR, tap;  // window (C + dC, R' + dR), tap index; tap < 0: none
-};
-// candidate k (0/1) of pixel (row 2R' + pr, column 2C + pc) for centre parity P, rho(C) = RHO
-__host__ __device__ constexpr Cand blk_cand(int P, int RHO, int pc, int pr, int k) {
-    if (pc == 0) {  // column 2C: the window column's own taps 2, 3, 4 (dr = -1, 0, +1)
-        if (RHO == 0) {
-            if (pr == 0) return k == 0 ? Cand{0, 0, 3} : Cand{0, 0, -1};
-            return k == 0 ? Cand{0, 0, 4} : Cand{0, 1, 2};
-        }
-        if (pr == 0) return k == 0 ? Cand{0, -1, 4} : Cand{0, 0, 2};
-        return k == 0 ? Cand{0, 0, 3} : Cand{0, 0, -1};
-    }
-    // column 2C+1: k = 0 from window column C (dc = +1, taps 5, 6), k = 1 from C+1 (dc = -1, taps 0, 1)
-    if (P == 0) {
-        if (RHO == 0) {
-            if (pr == 0) return k == 0 ? Cand{0, 0, 6} : Cand{1, 0, 0};
-            return k == 0 ? Cand{0, 1, 5} : Cand{1, 0, 1};
-        }
-        if (pr == 0) return k == 0 ? Cand{0, 0, 5} : Cand{1, 0, 1};
-        return k == 0 ? Cand{0, 0, 6} : Cand{1, 1, 0};
-    }
-    if (RHO == 0) {
-        if (pr == 0) return k == 0 ? Cand{0, 0, 5} : Cand{1, -1, 1};
-        return k == 0 ? Cand{0, 0, 6} : Cand{1, 0, 0};
-    }
-    if (pr == 0) return k == 0 ? Cand{0, -1, 6} : Cand{1, 0, 0};
-    return k == 0 ? Cand{0, 0, 5} : Cand{1, 0, 1};
-}
-__host__ __device__ constexpr bool blk_uses(int P, int RHO, int dC, int dR) {
-    for (int pc = 0; pc < 2; ++pc)
-        for (int pr = 0; pr < 2; ++pr)
-            for (int k = 0; k < 2; ++k) {
-                const Cand c = blk_cand(P, RHO, pc, pr, k);
-                if (c.tap >= 0 && c.dC == dC && c.dR == dR) return true;
-            }
-    return false;
-}
-
 // dy masked to the channels whose argmax byte equals `tap`
 __device__ __forceinline__ uint4 route_mask(uint4 d, uint2 a, int tap) {
     const uint32_t tt4 = (uint32_t)tap * 0x01010101u;
@@ -881,6 +843,7 @@ hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
     } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_fwd<1, 1>(a, st); else launch_spec_fwd<1, 2>(a, st); }
         else { if (a.g.s == 1) launch_spec_fwd<2, 1>(a, st); else launch_spec_fwd<2, 2>(a, st); }
+    } else if (pool_plane_fwd(a, st)) {
     } else if (use_vec8(a)) {
         const int C8 = a.C / 8;
         const int64_t total = (int64_t)a.g.B * C8 * a.g.Ho * a.g.Wo;
@@ -927,6 +890,7 @@ hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
     } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_bwd<1, 1>(a, st); else launch_spec_bwd<1, 2>(a, st); }
         else { if (a.g.s == 1) launch_spec_bwd<2, 1>(a, st); else launch_spec_bwd<2, 2>(a, st); }
+    } else if (pool_plane_bwd(a, st)) {
     } else if (use_vec8(a)) {
         const int C8 = a.C / 8;
         const int64_t total = (int64_t)a.g.B * C8 * a.g.H * a.g.W;

@@ -337,7 +337,7 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
     constexpr int STAGES = RESB ? 4 : Cfg::STAGES;
     constexpr int STAGE = RESB ? Cfg::A_BYTES : Cfg::STAGE;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem_base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem_base = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned, shared space
     uint8_t* resb = smem_base;                         // resident weights (RESB only)
     uint8_t* smem = smem_base + (RESB ? RES_MAX : 0);  // stage ring
     uint8_t* obuf = smem + STAGES * STAGE;
@@ -477,7 +477,7 @@ tc_conv_fwd2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
                     const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ TcFwdParams p) {
     using Cfg = Fwd2Cfg<BN, KC>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned, shared space
     uint8_t* obuf = smem + Cfg::STAGES * Cfg::STAGE;
     uint64_t* full = (uint64_t*)(obuf + 2 * FwdCfg<BN>::OUT_BYTES);
     uint64_t* empty = full + Cfg::STAGES;
@@ -809,7 +809,7 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
                      const __grid_constant__ TcWgParams p) {
     using Cfg = WgCfg<PIX>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned, shared space
     uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
     uint64_t* empty = full + Cfg::STAGES;
     uint64_t* tfull = empty + Cfg::STAGES;
@@ -987,7 +987,7 @@ tc_conv_wgrad2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_c
                       const __grid_constant__ TcWgParams p) {
     using Cfg = Wg2Cfg;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned, shared space
     uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
     uint64_t* empty = full + Cfg::STAGES;
     uint64_t* dbr = empty + Cfg::STAGES;  // per stage: MMAs done (multicast) -> dy tile readable for dbias

@@ -150,7 +150,7 @@ tc_wgrad_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
                    const __grid_constant__ CUtensorMap map_dy0, const __grid_constant__ CUtensorMap map_dy1,
                    const __grid_constant__ TrParams p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned, shared space
     constexpr int TR_PIX = TR_JB * RB;
     constexpr int DY_BOX = TR_PIX * 128;  // one 64-channel dy box
     const int xbox = p.xrows * TR_JB * 128;

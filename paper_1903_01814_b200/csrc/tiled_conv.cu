@@ -21,16 +21,19 @@
 
 namespace hexconv {
 
-constexpr int TT_TR = 8, TT_TC = 32, TT_PR = 4, TT_CO = 8;
-constexpr int TT_THREADS = (TT_TR / TT_PR) * TT_TC * 4;  // 4 channel groups of TT_CO -> COB = 32
-constexpr int TT_COB = 4 * TT_CO;
+constexpr int TT_CO = 8;
 
-template <int N, bool TRANSPOSE>
-__global__ void __launch_bounds__(TT_THREADS)
+// Tile shapes: TT_TR rows x TT_TC columns, TT_PR rows per thread, NCG groups of 8 output
+// channels (COB = 8 NCG).  Chosen per call so the tiles cover the grid (and Cout) without
+// idle threads: 8x32 (default), 8x40 (40-wide grids), 20x20 (20x20 grids); NCG = 2 / 4.
+template <int N, bool TRANSPOSE, int TT_TR, int TT_TC, int TT_PR, int NCG>
+__global__ void __launch_bounds__((TT_TR / TT_PR) * TT_TC * NCG)
 tiled_conv_s1_kernel(const float* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
                      const float* __restrict__ relu_y, float* __restrict__ y, int B, int Cin, int Cout, int H, int W,
                      int parity, int relu) {
     constexpr int T = 3 * N * (N + 1) + 1;
+    constexpr int TT_THREADS = (TT_TR / TT_PR) * TT_TC * NCG;
+    constexpr int TT_COB = NCG * TT_CO;
     constexpr int TT_CIC = N >= 3 ? 4 : 8;  // input channels per staged chunk (static smem < 48 KB)
     constexpr int RH = TT_TR + 2 * N;  // staged rows
     constexpr int CW = TT_TC + 2 * N;  // staged columns
@@ -47,7 +50,7 @@ tiled_conv_s1_kernel(const float* __restrict__ x, const float* __restrict__ w, c
     const int tid = threadIdx.x;
     const int col = tid % TT_TC;                    // output column within the tile
     const int rg = (tid / TT_TC) % (TT_TR / TT_PR); // row group
-    const int cg = tid / (TT_TC * (TT_TR / TT_PR)); // channel group (0..3)
+    const int cg = tid / (TT_TC * (TT_TR / TT_PR)); // channel group (0..NCG-1)
     const int c = c0 + col;
     const int rbase = rg * TT_PR;                   // first output row (tile-relative)
     const int p = (c + parity) & 1;
@@ -137,19 +140,22 @@ bool tiled_supported(const Geom& g, int dtype, int layout) {
     return dtype == HEX_F32 && layout == HEX_NCHW && g.s == 1 && g.n <= 3 && !getenv("HEXCONV_NO_TILED");
 }
 
-// transpose = 0: forward (x, w[Cout][Cin][T]); 1: backward-data at stride 1 (x = dy,
-// Cin = original Cout, Cout = original Cin, w = the original weights).
-hex_status_t tiled_conv(const float* x, const float* w, const float* bias, const float* relu_y, float* y,
-                        const Geom& g, int Cin, int Cout, int relu, int transpose, cudaStream_t st) {
-    const int tiles = ceil_div(g.H, TT_TR) * ceil_div(g.W, TT_TC);
-    dim3 grid(tiles, ceil_div(Cout, TT_COB), g.B);
-#define HEX_TILED(NN)                                                                                         \
-    if (transpose)                                                                                            \
-        tiled_conv_s1_kernel<NN, true><<<grid, TT_THREADS, 0, st>>>(x, w, bias, relu_y, y, g.B, Cin, Cout, g.H, \
-                                                                    g.W, g.parity, relu);                    \
-    else                                                                                                      \
-        tiled_conv_s1_kernel<NN, false><<<grid, TT_THREADS, 0, st>>>(x, w, bias, relu_y, y, g.B, Cin, Cout,    \
-                                                                     g.H, g.W, g.parity, relu);
+namespace {
+template <int TR, int TC, int PR, int NCG>
+hex_status_t launch_tiled(const float* x, const float* w, const float* bias, const float* relu_y, float* y,
+                          const Geom& g, int Cin, int Cout, int relu, int transpose, cudaStream_t st) {
+    constexpr int threads = (TR / PR) * TC * NCG;
+    const int tiles = ceil_div(g.H, TR) * ceil_div(g.W, TC);
+    dim3 grid(tiles, ceil_div(Cout, NCG * TT_CO), g.B);
+#define HEX_TILED(NN)                                                                                          \
+    if (transpose)                                                                                             \
+        tiled_conv_s1_kernel<NN, true, TR, TC, PR, NCG><<<grid, threads, 0, st>>>(x, w, bias, relu_y, y, g.B,  \
+                                                                                  Cin, Cout, g.H, g.W,         \
+                                                                                  g.parity, relu);             \
+    else                                                                                                       \
+        tiled_conv_s1_kernel<NN, false, TR, TC, PR, NCG><<<grid, threads, 0, st>>>(x, w, bias, relu_y, y, g.B, \
+                                                                                   Cin, Cout, g.H, g.W,        \
+                                                                                   g.parity, relu);
     switch (g.n) {
         case 0: HEX_TILED(0); break;
         case 1: HEX_TILED(1); break;
@@ -159,6 +165,35 @@ hex_status_t tiled_conv(const float* x, const float* w, const float* bias, const
 #undef HEX_TILED
     count_launch();
     return last_launch_status();
+}
+
+// fraction of computed outputs that are real (tile padding of rows, columns and channels)
+double tile_fill(int H, int W, int Cout, int TR, int TC, int COB) {
+    return (double)H / (ceil_div(H, TR) * TR) * W / (ceil_div(W, TC) * TC) * Cout / (ceil_div(Cout, COB) * COB);
+}
+}  // namespace
+
+// transpose = 0: forward (x, w[Cout][Cin][T]); 1: backward-data at stride 1 (x = dy,
+// Cin = original Cout, Cout = original Cin, w = the original weights).
+hex_status_t tiled_conv(const float* x, const float* w, const float* bias, const float* relu_y, float* y,
+                        const Geom& g, int Cin, int Cout, int relu, int transpose, cudaStream_t st) {
+    // candidate shapes (rows, cols, channel groups); pick the best-filled, ties -> listed order
+    struct Shape { int tr, tc, ncg; };
+    const Shape cand[] = {{8, 32, 4}, {8, 40, 4}, {20, 20, 4}, {8, 32, 2}, {8, 40, 2}, {20, 20, 2}};
+    int best = 0;
+    double bf = -1.0;
+    for (int i = 0; i < 6; ++i) {
+        const double f = tile_fill(g.H, g.W, Cout, cand[i].tr, cand[i].tc, 8 * cand[i].ncg);
+        if (f > bf + 1e-9) { bf = f; best = i; }
+    }
+    switch (best) {
+        case 0: return launch_tiled<8, 32, 4, 4>(x, w, bias, relu_y, y, g, Cin, Cout, relu, transpose, st);
+        case 1: return launch_tiled<8, 40, 4, 4>(x, w, bias, relu_y, y, g, Cin, Cout, relu, transpose, st);
+        case 2: return launch_tiled<20, 20, 5, 4>(x, w, bias, relu_y, y, g, Cin, Cout, relu, transpose, st);
+        case 3: return launch_tiled<8, 32, 4, 2>(x, w, bias, relu_y, y, g, Cin, Cout, relu, transpose, st);
+        case 4: return launch_tiled<8, 40, 4, 2>(x, w, bias, relu_y, y, g, Cin, Cout, relu, transpose, st);
+        default: return launch_tiled<20, 20, 5, 2>(x, w, bias, relu_y, y, g, Cin, Cout, relu, transpose, st);
+    }
 }
 
 }  // namespace hexconv

@@ -277,6 +277,13 @@ class HexCNN:
         am = self.B * ho * wo * C
         return full + pooled + am  # fwd: read x, write y + argmax; bwd: read dy + argmax, write dx
 
+    def l1_bytes(self, kind):
+        """Algorithmic HBM bytes of a layer-1 (Cin = 1) call: fwd reads x and writes y;
+        wgrad reads x and dy (the weight gradient itself is 5 KB)."""
+        h, w = self.geo[0]
+        px = self.B * h * w
+        return px * 2 + px * self.channels[1] * 2
+
     def flops_per_image(self):
         """Algorithmic FLOPs per image of fwd + dgrad (L2..L6) + wgrad, counting
         in-grid taps only (valid taps)."""

@@ -261,6 +261,14 @@ def test_single_input_channel_mma_bands(F, oracle, pi, n):
         _conv_case(F, oracle, pi, n, 1, H, W, B, 1, Cout, torch.bfloat16, "NHWC", 60 + n + H)
 
 
+@pytest.mark.parametrize("pi,n", [(0, 1), (1, 1), (0, 2), (1, 2)])
+def test_f32_mid_channel_wgrad(F, oracle, pi, n):
+    # the column-walking fp32 weight gradient (f32_wgrad.cu): ragged 8-row bands (H = 13), odd W,
+    # one and two output-channel tiles, many bands per persistent block (B = 40)
+    for (B, Cin, Cout, H, W) in [(3, 16, 32, 13, 11), (2, 32, 64, 9, 10), (40, 8, 16, 16, 7)]:
+        _conv_case(F, oracle, pi, n, 1, H, W, B, Cin, Cout, torch.float32, "NCHW", 500 + Cin + H)
+
+
 def test_maxpool_n1s2_closed_form_backward(F, oracle):
     # the specialised n=1, s=2 max-pool backward (config 5): both parities, odd/even grids, C % 8 == 0
     for pi in (0, 1):

@@ -17,27 +17,60 @@ flush_buf = None
 
 
 def flush():
+    """Evict L2 by READING a 256 MB buffer: a write-based flush leaves ~126 MB of
+    dirty lines whose write-back would be charged to the next (timed) kernel."""
     global flush_buf
     if flush_buf is None:
-        flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    flush_buf.zero_()
+        flush_buf = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    flush_buf.sum()
 
 
-def timeit(fn, iters=10, warmup=3):
+def _graph(body):
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        body()
+    torch.cuda.current_stream().wait_stream(s)
+    with torch.cuda.graph(g):
+        body()
+    torch.cuda.synchronize()
+    return g
+
+
+def _time_graph(g, iters):
+    ts = []
+    for _ in range(iters):
+        s0, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        g.replay()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s0.elapsed_time(e))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def timeit(fn, iters=5, warmup=3, reps=10):
+    """Device time of one call with L2 flushed before it.  `reps` (flush, call)
+    pairs are captured in one CUDA graph and the same number of flushes alone in
+    another; the difference / reps is the call's time, free of host dispatch
+    (tens of us per call through Python/ctypes) and of the flush itself."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
-    ts = []
-    for _ in range(iters):
-        flush()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        fn()
-        e.record()
-        torch.cuda.synchronize()
-        ts.append(s.elapsed_time(e))
-    ts.sort()
-    return ts[len(ts) // 2]
+
+    def pairs():
+        for _ in range(reps):
+            flush()
+            fn()
+
+    def flushes():
+        for _ in range(reps):
+            flush()
+
+    gp, gf = _graph(pairs), _graph(flushes)
+    return max(_time_graph(gp, iters) - _time_graph(gf, iters), 0.0) / reps
 
 
 def valid_taps(H, W, n):
