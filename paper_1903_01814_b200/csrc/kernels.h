@@ -57,6 +57,8 @@ struct TcConvArgs {
     int relu;
 };
 bool tc_conv_supported(const Geom& g, int Cin, int Cout);
+bool tc_fwd_tr_supported(const Geom& g, int Cin, int Cout);  // tap-reuse forward (tc_fwd_tr.cu)
+hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st);
 hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st);
 hex_status_t tc_pack_weights(const void* w, void* wpack, int Cout, int Cin, int T, int transpose_reverse,
                              cudaStream_t st);

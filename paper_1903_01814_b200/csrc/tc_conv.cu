@@ -695,6 +695,7 @@ static bool use_2sm(int BN) {
 }
 
 hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
+    if (tc_fwd_tr_supported(a.g, a.Cin, a.Cout)) return tc_fwd_tr(a, st);  // tap-reuse kernel (tc_fwd_tr.cu)
     const Geom& g = a.g;
     TcFwdParams p{};
     p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;

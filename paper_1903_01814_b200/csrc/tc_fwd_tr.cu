@@ -1,0 +1,516 @@
+// tc_fwd_tr.cu -- tcgen05 hexagonal convolution forward (and stride-1
+// backward-data) with TAP REUSE of the A operand (bf16 NHWC, fp32 accumulation
+// in tensor memory).
+//
+//   y[px][co] = bias[co] + sum_t sum_ci x[px + off_t(parity(px))][ci] w[t][co][ci]
+// (the sum over the kernel footprint; off-grid taps
+// are TMA's zero fill, A4).  Backward-data at stride 1 is the same
+// computation on dy with W'[ci][co][t] = W[co][ci][T-1-t] (oracle pin P18).
+//
+// Output tiles are 16 rows x 8 sub-columns of one parity view of one image in
+// row-major order, so M = 128 pixels and one image row is one 1024-byte SW128
+// atom of the K-major A operand.  For a tile of view P the taps of kernel
+// column dc all read view P' = (P + dc) mod 2 at one sub-column shift and
+// differ only by their row: ONE A box of 16 + 2n rows per (column, 64-channel
+// chunk) serves every tap of the column, tap k being the 128-row window k atoms
+// into the box.  Per tile and chunk that is 2n+1 box loads of (16+2n)/16 tiles
+// instead of T = 3n(n+1)+1 tile loads (n = 1: 7 -> 3.4 tiles of traffic).
+// Weights are either resident in shared memory for the whole kernel (loaded
+// once per CTA when T x Cout x Cin fits) or streamed with each stage.
+//
+// Persistent, warp specialised: warp 0 TMA producer, warp 1 MMA issuer (all
+// shapes compile-time, descriptors advanced by 64-bit adds: see DESIGN.md
+// "MMA issue"), warps 2-9 the epilogue (bias, ReLU or the ReLU-backward mask,
+// bf16 RNE, SW128 staging, TMA store), two TMEM accumulators.
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "common.cuh"
+#include "geometry.cuh"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace hexconv {
+
+namespace {
+
+constexpr int FT_RB = 16, FT_JB = 8;  // output tile: 16 rows x 8 sub-columns = 128 pixels
+constexpr int FT_EPI = 256;           // epilogue threads (8 warps, two per TMEM lane quadrant)
+constexpr int FT_THREADS = 64 + FT_EPI;
+constexpr int FT_OUT = 128 * 128;     // one 64-channel output chunk staged (16 KB)
+constexpr int FT_SMEM_MAX = 227 * 1024;
+
+struct FtParams {
+    int B, H, W, Cin, Cout, T, parity;
+    int rt, jt0, jt1, tiles0, mtiles, n_tiles, total_tiles, kchunks, stages;
+    int relu, has_mask;
+    const float* bias;
+};
+
+__device__ __forceinline__ void ft_decode(const FtParams& p, int tile, int BN, int* P, int* r0, int* j0, int* b,
+                                          int* n0) {
+    const int nt = tile % p.n_tiles;
+    int m = tile / p.n_tiles;
+    *n0 = nt * BN;
+    int jt;
+    if (p.jt0 == p.jt1) { *P = m & 1; m >>= 1; jt = p.jt0; }  // views interleaved (L2 reuse across views)
+    else if (m < p.tiles0) { *P = 0; jt = p.jt0; }
+    else { *P = 1; m -= p.tiles0; jt = p.jt1; }
+    const int rti = m % p.rt;
+    m /= p.rt;
+    const int jti = m % jt;
+    *b = m / jt;
+    *r0 = rti * FT_RB;
+    *j0 = jti * FT_JB;
+}
+
+// Stage list of one 64-channel chunk: (kernel column, first tap, tap count), taps of a column split
+// into groups of <= TG (streamed weights: each stage also carries its taps' weight tiles).
+template <int N, int TG>
+struct StageList {
+    __host__ __device__ static constexpr int len(int dc) { return 2 * N + 1 - (dc < 0 ? -dc : dc); }
+    __host__ __device__ static constexpr int groups(int dc) { return (len(dc) + TG - 1) / TG; }
+    __host__ __device__ static constexpr int count() {
+        int c = 0;
+        for (int dc = -N; dc <= N; ++dc) c += groups(dc);
+        return c;
+    }
+    // stage s -> dc, g0 (first tap within the column), cnt, tb (canonical index of the column's tap 0)
+    __host__ __device__ static constexpr int dc_of(int s) {
+        for (int dc = -N; dc <= N; ++dc) {
+            if (s < groups(dc)) return dc;
+            s -= groups(dc);
+        }
+        return 0;
+    }
+    __host__ __device__ static constexpr int g0_of(int s) {
+        for (int dc = -N; dc <= N; ++dc) {
+            if (s < groups(dc)) return s * TG;
+            s -= groups(dc);
+        }
+        return 0;
+    }
+    __host__ __device__ static constexpr int cnt_of(int s) {
+        const int dc = dc_of(s), g0 = g0_of(s);
+        return len(dc) - g0 < TG ? len(dc) - g0 : TG;
+    }
+    __host__ __device__ static constexpr int tb_of(int s) {
+        const int dc = dc_of(s);
+        int t = 0;
+        for (int c = -N; c < dc; ++c) t += len(c);
+        return t;
+    }
+};
+
+// MMAs of one stage: taps g0 .. g0+CNT-1 of the column, 4 K-steps of 16 channels each.
+template <int BN, int CNT, bool RES>
+__device__ __forceinline__ void issue_stage(uint32_t d, uint64_t a_desc, uint64_t b_desc, int b_tap_stride16,
+                                            uint32_t first) {
+    constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 0, 0);
+#pragma unroll
+    for (int i = 0; i < CNT; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            ptx::mma_bf16(d, a_desc + (uint64_t)(i * 64 + k * 2), b_desc + (uint64_t)(i * b_tap_stride16 + k * 2),
+                          idesc, (i | k) ? 1u : first);
+}
+
+template <int BN, int N, int TG, bool RES, int S>
+__device__ __forceinline__ void issue_stages_from(uint32_t d, uint64_t a_ring, uint64_t b_ring, uint64_t res_desc,
+                                                  uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
+                                                  int nstages, uint32_t stage16, uint32_t a_bytes16, int kc,
+                                                  int kchunks, uint32_t first) {
+    using SL = StageList<N, TG>;
+    if constexpr (S < SL::count()) {
+        constexpr int g0 = SL::g0_of(S), cnt = SL::cnt_of(S), tb = SL::tb_of(S);
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint64_t soff = (uint64_t)stage * stage16;
+        const uint64_t ad = a_ring + soff + (uint64_t)(g0 * 64);  // tap g0 = g0 rows (1024 B) into the box
+        uint64_t bd;
+        int bstride;
+        if (RES) {  // resident weights: tile (t, kc) at ((t * kchunks + kc) * BN * 128) bytes
+            bd = res_desc + (uint64_t)(((tb + g0) * kchunks + kc) * (BN * 8));
+            bstride = kchunks * BN * 8;
+        } else {
+            bd = b_ring + soff + a_bytes16;
+            bstride = BN * 8;
+        }
+        issue_stage<BN, cnt, RES>(d, ad, bd, bstride, S == 0 ? first : 1u);
+        ptx::mma_commit(&empty[stage]);
+        if (++stage == nstages) { stage = 0; phase ^= 1; }
+        issue_stages_from<BN, N, TG, RES, S + 1>(d, a_ring, b_ring, res_desc, full, empty, stage, phase, nstages,
+                                                  stage16, a_bytes16, kc, kchunks, 1u);
+    }
+}
+
+}  // namespace
+
+template <int BN, int N, int TG, bool RES>
+__global__ void __launch_bounds__(FT_THREADS, 1)
+tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
+                 const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
+                 const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
+                 const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ FtParams p) {
+    using SL = StageList<N, TG>;
+    constexpr int A_BYTES = (FT_RB + 2 * N) * FT_JB * 128;   // one A box
+    constexpr int W_TILE = BN * 128;                          // one (tap, chunk) weight tile
+    constexpr int STAGE = RES ? A_BYTES : A_BYTES + TG * W_TILE;
+    constexpr int TMEM_COLS = 2 * BN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned
+    const int res_bytes = RES ? p.T * p.kchunks * W_TILE : 0;
+    uint8_t* resw = base;
+    uint8_t* ring = base + res_bytes;
+    uint8_t* obuf = ring + p.stages * STAGE;
+    uint64_t* full = (uint64_t*)(obuf + 2 * FT_OUT);
+    uint64_t* empty = full + p.stages;
+    uint64_t* tfull = empty + p.stages;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* mbar = tempty + 2;
+    uint64_t* bres = mbar + 2;
+    uint32_t* tmem_slot = (uint32_t*)(bres + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], FT_EPI / 32);
+            ptx::mbar_init(&mbar[a], 1);
+        }
+        ptx::mbar_init(bres, 1);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&map_x0);
+        ptx::prefetch_tmap(&map_x1);
+        ptx::prefetch_tmap(&map_w);
+        ptx::prefetch_tmap(&map_y0);
+        ptx::prefetch_tmap(&map_y1);
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            if constexpr (RES) {
+                ptx::mbar_arrive_expect_tx(bres, (uint32_t)res_bytes);
+                for (int t = 0; t < p.T; ++t)
+                    for (int kc = 0; kc < p.kchunks; ++kc)
+                        ptx::tma_load_4d(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0, 0, kc, t);
+            }
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+                int P, r0, j0, b, n0;
+                ft_decode(p, tile, BN, &P, &r0, &j0, &b, &n0);
+                const int pc = (P + p.parity) & 1;  // centre column parity
+                for (int kc = 0; kc < p.kchunks; ++kc) {
+#pragma unroll 1
+                    for (int s = 0; s < SL::count(); ++s) {
+                        const int dc = SL::dc_of(s), g0 = SL::g0_of(s), cnt = SL::cnt_of(s), tb = SL::tb_of(s);
+                        const int Pv = (P + dc) & 1;
+                        const int jsh = (P + dc - Pv) / 2;
+                        const int top = -N + (((dc < 0 ? -dc : dc) + pc) >> 1);
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sa = ring + stage * STAGE;
+                        ptx::mbar_arrive_expect_tx(&full[stage], RES ? A_BYTES : A_BYTES + cnt * W_TILE);
+                        ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top, b, kc);
+                        if constexpr (!RES)
+                            for (int i = 0; i < cnt; ++i)
+                                ptx::tma_load_4d(&map_w, &full[stage], sa + A_BYTES + i * W_TILE, 0, n0, kc,
+                                                 tb + g0 + i);
+                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint64_t a_ring = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
+            const uint64_t b_ring = a_ring;  // streamed weight tiles sit A_BYTES into the stage
+            const uint64_t res_desc = ptx::smem_desc_sw128(ptx::smem_u32(resw), 16, 1024);
+            const uint32_t stage16 = STAGE >> 4, a_bytes16 = A_BYTES >> 4;
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t aphase = 0;
+            if constexpr (RES) ptx::mbar_wait(bres, 0);
+            for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+                ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int kc = 0; kc < p.kchunks; ++kc)
+                    issue_stages_from<BN, N, TG, RES, 0>(d, a_ring, b_ring, res_desc, full, empty, stage, phase,
+                                                         p.stages, stage16, a_bytes16, kc, p.kchunks,
+                                                         kc == 0 ? 0u : 1u);
+                ptx::mma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) aphase ^= 1;
+            }
+        }
+    } else {
+        // Epilogue: warps 2..9; warp w owns TMEM lane quadrant w % 4 (tile row m = TMEM lane) and
+        // column half h of every 64-channel chunk.  Per chunk: TMEM -> registers -> (bias, ReLU |
+        // ReLU-backward mask) -> bf16 -> SW128 staging row m -> one TMA store of the 16 x 8 box.
+        const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
+        const int row = q * 32 + lane;
+        const int et = threadIdx.x - 64;
+        int acc = 0;
+        uint32_t aphase = 0;
+        int ob = 0;
+        uint32_t mphase0 = 0, mphase1 = 0;
+        for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+            int P, r0, j0, b, n0;
+            ft_decode(p, tile, BN, &P, &r0, &j0, &b, &n0);
+            const CUtensorMap* my = P ? &map_y1 : &map_y0;
+            const CUtensorMap* mm = P ? &map_m1 : &map_m0;
+            if (p.has_mask && et == 0) {
+                ptx::bulk_wait_read<1>();
+                ptx::mbar_arrive_expect_tx(&mbar[ob], FT_OUT);
+                ptx::tma_load_4d(mm, &mbar[ob], obuf + ob * FT_OUT, n0, j0, r0, b);
+            }
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 64; ++ch) {
+                uint8_t* buf = obuf + ob * FT_OUT;
+                const int c0 = n0 + ch * 64;
+                if (p.has_mask) {
+                    ptx::mbar_wait(&mbar[ob], ob ? mphase1 : mphase0);
+                    if (ob) mphase1 ^= 1; else mphase0 ^= 1;
+                } else {
+                    if (et == 0) ptx::bulk_wait_read<1>();
+                    ptx::named_bar(1, FT_EPI);
+                }
+                uint32_t v[32];
+                ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + ch * 64 + h * 32, v);
+                ptx::tmem_ld_wait();
+                uint8_t* rowp = buf + row * 128;
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    const int i = 4 * h + ii;  // 16-byte unit (8 channels) within the 64-channel chunk
+                    uint4* slot = reinterpret_cast<uint4*>(rowp + ((i ^ (row & 7)) << 4));
+                    float f[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) f[k] = __uint_as_float(v[8 * ii + k]);
+                    if (p.bias) {
+                        const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i));
+                        const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i + 4));
+                        f[0] += b0.x; f[1] += b0.y; f[2] += b0.z; f[3] += b0.w;
+                        f[4] += b1.x; f[5] += b1.y; f[6] += b1.z; f[7] += b1.w;
+                    }
+                    if (p.relu) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) f[k] = fmaxf(f[k], 0.f);
+                    }
+                    if (p.has_mask) {
+                        const uint4 m4 = *slot;
+                        const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t bits = (k & 1) ? (mw[k >> 1] & 0xffff0000u) : (mw[k >> 1] << 16);
+                            if (!(__uint_as_float(bits) > 0.f)) f[k] = 0.f;
+                        }
+                    }
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        __nv_bfloat162 hv = __floats2bfloat162_rn(f[2 * k], f[2 * k + 1]);
+                        pk[k] = *reinterpret_cast<uint32_t*>(&hv);
+                    }
+                    *slot = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                ptx::fence_proxy_async();
+                ptx::named_bar(1, FT_EPI);
+                if (et == 0) {
+                    ptx::tma_store_4d(my, buf, c0, j0, r0, b);
+                    ptx::bulk_commit();
+                    if (p.has_mask && ch + 1 < BN / 64) {
+                        ptx::bulk_wait_read<1>();
+                        ptx::mbar_arrive_expect_tx(&mbar[ob ^ 1], FT_OUT);
+                        ptx::tma_load_4d(mm, &mbar[ob ^ 1], obuf + (ob ^ 1) * FT_OUT, c0 + 64, j0, r0, b);
+                    }
+                }
+                ob ^= 1;
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+        if (et == 0) ptx::bulk_wait<0>();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 ft_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
+    }
+    return fn;
+}
+
+// parity view P, sub-columns before rows: dims {64, Wp, H, B, C/64}, box {64, 8, rows, 1, 1}
+static bool ft_view5(CUtensorMap* m, const void* base, int B, int H, int W, int C, int P, int rows) {
+    auto enc = ft_encode();
+    const int Wp = (W - P + 1) / 2;
+    if (!enc || Wp < 1 || C % 64) return false;
+    cuuint64_t dims[5] = {64, (cuuint64_t)Wp, (cuuint64_t)H, (cuuint64_t)B, (cuuint64_t)(C / 64)};
+    cuuint64_t strides[4] = {(cuuint64_t)2 * C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2, 128};
+    cuuint32_t box[5] = {64, (cuuint32_t)FT_JB, (cuuint32_t)rows, 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, (void*)((const char*)base + (size_t)P * C * 2), dims, strides,
+               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// output / mask tiles: dims {C, Wp, H, B}, box {64, 8, 16, 1}
+static bool ft_view4(CUtensorMap* m, const void* base, int B, int H, int W, int C, int P) {
+    auto enc = ft_encode();
+    const int Wp = (W - P + 1) / 2;
+    if (!enc || Wp < 1) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)Wp, (cuuint64_t)H, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)2 * C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)FT_JB, (cuuint32_t)FT_RB, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)((const char*)base + (size_t)P * C * 2), dims, strides,
+               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// packed weights [T][Cout][Cin]: dims {64, Cout, Cin/64, T}, box {64, BN, 1, 1}
+static bool ft_wmap(CUtensorMap* m, const void* base, int T, int Cout, int Cin, int BN) {
+    auto enc = ft_encode();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {64, (cuuint64_t)Cout, (cuuint64_t)(Cin / 64), (cuuint64_t)T};
+    cuuint64_t strides[3] = {(cuuint64_t)Cin * 2, 128, (cuuint64_t)Cout * Cin * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)BN, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace {
+struct FtPlan {
+    int BN, res, stages, smem;
+    bool ok;
+};
+
+constexpr int ft_tg(bool res, int n) { return res ? 2 * n + 1 : 3; }
+
+FtPlan ft_plan(const Geom& g, int Cin, int Cout) {
+    FtPlan pl{};
+    pl.BN = Cout % 128 == 0 ? 128 : (Cout % 64 == 0 ? 64 : 0);
+    if (!pl.BN || Cin % 64) return pl;
+    const int A = (FT_RB + 2 * g.n) * FT_JB * 128, WT = pl.BN * 128;
+    const int fixed = 2 * FT_OUT + 1024 + 512;
+    const int res_bytes = g.T * (Cin / 64) * WT;
+    // resident weights when they leave room for >= 4 A stages (the whole weight set of the call:
+    // only one Cout tile then, i.e. Cout == BN)
+    if (Cout == pl.BN && res_bytes + fixed + 4 * A <= FT_SMEM_MAX) {
+        pl.res = 1;
+        pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
+        if (pl.stages > 8) pl.stages = 8;
+        pl.smem = res_bytes + pl.stages * A + fixed;
+    } else {
+        const int st = A + ft_tg(false, g.n) * WT;
+        pl.stages = (FT_SMEM_MAX - fixed) / st;
+        if (pl.stages > 6) pl.stages = 6;
+        if (pl.stages < 2) return pl;
+        pl.smem = pl.stages * st + fixed;
+    }
+    pl.ok = true;
+    return pl;
+}
+}  // namespace
+
+// Taken for stride-1 bf16 NHWC layers whose 16 x 8 tiles fill >= 85% of both views and whose weights
+// stay resident in shared memory (n = 1, 2); HEXCONV_NO_FWD_TR disables it.
+bool tc_fwd_tr_supported(const Geom& g, int Cin, int Cout) {
+    if (getenv("HEXCONV_NO_FWD_TR")) return false;
+    if (g.s != 1 || (g.n != 1 && g.n != 2) || g.W < 2 || g.B > 65535) return false;
+    const double fill_c = (double)((g.W + 1) / 2) / (ceil_div((g.W + 1) / 2, FT_JB) * FT_JB);
+    const double fill_r = (double)g.H / (ceil_div(g.H, FT_RB) * FT_RB);
+    if (fill_c * fill_r < 0.85) return false;
+    const FtPlan pl = ft_plan(g, Cin, Cout);
+    if (!pl.ok) return false;
+    // streamed-weight plans measured slower than the CTA-pair kernel of tc_conv.cu (C5 L3/L4, round 1):
+    // only the resident-weight plan is taken unless HEXCONV_FWD_TR_STREAM is set
+    if (!pl.res && !getenv("HEXCONV_FWD_TR_STREAM")) return false;
+    return ft_encode() != nullptr;
+}
+
+template <int BN, int N, bool RES>
+static hex_status_t launch_ft(const CUtensorMap* maps, const FtParams& p, int smem, cudaStream_t st) {
+    constexpr int TG = ft_tg(RES, N);
+    if (cudaFuncSetAttribute(tc_fwd_tr_kernel<BN, N, TG, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+        return HEX_ERR_CUDA;
+    const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+    tc_fwd_tr_kernel<BN, N, TG, RES><<<grid, FT_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
+                                                                      maps[5], maps[6], p);
+    count_launch();
+    return last_launch_status();
+}
+
+hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
+    const Geom& g = a.g;
+    const FtPlan pl = ft_plan(g, a.Cin, a.Cout);
+    if (!pl.ok) return HEX_ERR_UNSUPPORTED;
+    FtParams p{};
+    p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
+    p.rt = ceil_div(g.H, FT_RB);
+    p.jt0 = ceil_div((g.W + 1) / 2, FT_JB);
+    p.jt1 = ceil_div(g.W / 2, FT_JB);
+    p.tiles0 = p.rt * p.jt0 * g.B;
+    p.mtiles = p.tiles0 + p.rt * p.jt1 * g.B;
+    p.n_tiles = a.Cout / pl.BN;
+    p.total_tiles = p.mtiles * p.n_tiles;
+    p.kchunks = a.Cin / 64;
+    p.stages = pl.stages;
+    p.relu = a.relu;
+    p.has_mask = a.relu_y != nullptr;
+    p.bias = a.bias;
+    CUtensorMap maps[7];
+    if (!ft_view5(&maps[0], a.x, g.B, g.H, g.W, a.Cin, 0, FT_RB + 2 * g.n)) return HEX_ERR_CUDA;
+    if (!ft_view5(&maps[1], a.x, g.B, g.H, g.W, a.Cin, 1, FT_RB + 2 * g.n)) return HEX_ERR_CUDA;
+    if (!ft_wmap(&maps[2], a.wpack, g.T, a.Cout, a.Cin, pl.BN)) return HEX_ERR_CUDA;
+    if (!ft_view4(&maps[3], a.y, g.B, g.H, g.W, a.Cout, 0)) return HEX_ERR_CUDA;
+    if (!ft_view4(&maps[4], a.y, g.B, g.H, g.W, a.Cout, 1)) return HEX_ERR_CUDA;
+    if (a.relu_y) {
+        if (!ft_view4(&maps[5], a.relu_y, g.B, g.H, g.W, a.Cout, 0)) return HEX_ERR_CUDA;
+        if (!ft_view4(&maps[6], a.relu_y, g.B, g.H, g.W, a.Cout, 1)) return HEX_ERR_CUDA;
+    } else {
+        maps[5] = maps[3];
+        maps[6] = maps[4];
+    }
+#define HEX_FT(BN_, N_, R_) return launch_ft<BN_, N_, R_>(maps, p, pl.smem, st)
+    if (pl.BN == 128) {
+        if (g.n == 1) { if (pl.res) HEX_FT(128, 1, true); else HEX_FT(128, 1, false); }
+        else { if (pl.res) HEX_FT(128, 2, true); else HEX_FT(128, 2, false); }
+    } else {
+        if (g.n == 1) { if (pl.res) HEX_FT(64, 1, true); else HEX_FT(64, 1, false); }
+        else { if (pl.res) HEX_FT(64, 2, true); else HEX_FT(64, 2, false); }
+    }
+#undef HEX_FT
+}
+
+}  // namespace hexconv
