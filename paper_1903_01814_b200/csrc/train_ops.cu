@@ -77,54 +77,69 @@ head_sample_kernel(const uint4* __restrict__ feat, const float* __restrict__ wl,
     }
 }
 
-// dwl[k][c] = sum_b dlog[b][k] gap[b][c]; dbl[k] = sum_b dlog[b][k]; loss = mean_b loss_b (fixed order)
+// dwl[k][c] = sum_b dlog[b][k] gap[b][c]; dbl[k] = sum_b dlog[b][k]; loss = mean_b loss_b.
+// One warp per output: lanes take a fixed strided subset of the samples, then a
+// fixed shuffle tree (deterministic).
 __global__ void head_param_grad_kernel(const float* __restrict__ gap, const float* __restrict__ dlog,
                                        const float* __restrict__ loss_b, float* __restrict__ dwl,
                                        float* __restrict__ dbl, float* __restrict__ loss, int B, int C, int K) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < K * C) {
-        const int k = i / C, c = i % C;
-        float s = 0.f;
-        for (int b = 0; b < B; ++b) s = fmaf(dlog[(int64_t)b * K + k], gap[(int64_t)b * C + c], s);
-        dwl[i] = s;
-    } else if (i < K * C + K) {
-        const int k = i - K * C;
-        float s = 0.f;
-        for (int b = 0; b < B; ++b) s += dlog[(int64_t)b * K + k];
-        dbl[k] = s;
-    } else if (i == K * C + K) {
-        float s = 0.f;
-        for (int b = 0; b < B; ++b) s += loss_b[b];
-        *loss = s / (float)B;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nout = K * C + K + 1;
+    if (w >= nout) return;
+    float s = 0.f;
+    if (w < K * C) {
+        const int k = w / C, c = w - k * C;
+        for (int b = lane; b < B; b += 32) s = fmaf(dlog[(int64_t)b * K + k], gap[(int64_t)b * C + c], s);
+    } else if (w < K * C + K) {
+        const int k = w - K * C;
+        for (int b = lane; b < B; b += 32) s += dlog[(int64_t)b * K + k];
+    } else {
+        for (int b = lane; b < B; b += 32) s += loss_b[b];
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane != 0) return;
+    if (w < K * C) dwl[w] = s;
+    else if (w < K * C + K) dbl[w - K * C] = s;
+    else *loss = s / (float)B;
 }
 
-// dfeat[b][hw][c] = (sum_k dlog[b][k] wl[k][c]) / HW * (feat > 0)   (8 channels per thread)
-__global__ void head_dfeat_kernel(const uint4* __restrict__ feat, const float* __restrict__ dlog,
-                                  const float* __restrict__ wl, uint4* __restrict__ dfeat, int B, int HW, int C8,
-                                  int K) {
+// dg[b][c] = (sum_k dlog[b][k] wl[k][c]) / HW: the gradient of every feature pixel of sample b
+__global__ void head_dg_kernel(const float* __restrict__ dlog, const float* __restrict__ wl, float* __restrict__ dg,
+                               int B, int C, int K, float inv_hw) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * C) return;
+    const int b = i / C, c = i - b * C;
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s = fmaf(dlog[(int64_t)b * K + k], wl[(int64_t)k * C + c], s);
+    dg[i] = s * inv_hw;
+}
+
+// dfeat[b][hw][c] = dg[b][c] * (feat > 0)   (8 channels per thread; ReLU backward of the last conv)
+__global__ void head_dfeat_kernel(const uint4* __restrict__ feat, const float* __restrict__ dg,
+                                  uint4* __restrict__ dfeat, int B, int HW, int C8) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t total = (int64_t)B * HW * C8;
     if (idx >= total) return;
     const int c8 = (int)(idx % C8);
     const int b = (int)(idx / ((int64_t)HW * C8));
-    const int C = C8 * 8;
-    uint4 f4 = feat[idx];
-    const __nv_bfloat16* f = reinterpret_cast<const __nv_bfloat16*>(&f4);
-    uint4 o4;
-    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&o4);
-    const float inv = 1.f / (float)HW;
+    const uint4 f4 = feat[idx];
+    const uint32_t fw[4] = {f4.x, f4.y, f4.z, f4.w};
+    const float4* g4 = reinterpret_cast<const float4*>(dg + ((int64_t)b * C8 + c8) * 8);
+    const float4 ga = __ldg(g4), gb = __ldg(g4 + 1);
+    const float g[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+    uint32_t o[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        float dg = 0.f;
-        for (int k = 0; k < K; ++k) dg = fmaf(dlog[(int64_t)b * K + k], wl[(int64_t)k * C + c8 * 8 + j], dg);
-        o[j] = __float2bfloat16_rn(__bfloat162float(f[j]) > 0.f ? dg * inv : 0.f);
+    for (int j = 0; j < 4; ++j) {
+        const float f0 = __uint_as_float(fw[j] << 16), f1 = __uint_as_float(fw[j] & 0xffff0000u);
+        __nv_bfloat162 h = __floats2bfloat162_rn(f0 > 0.f ? g[2 * j] : 0.f, f1 > 0.f ? g[2 * j + 1] : 0.f);
+        o[j] = *reinterpret_cast<uint32_t*>(&h);
     }
-    dfeat[idx] = o4;
+    dfeat[idx] = make_uint4(o[0], o[1], o[2], o[3]);
 }
 
 size_t head_ws_bytes(int B, int K, int C) {
-    return (size_t)(B * C + B * K + B) * sizeof(float);
+    return (size_t)(B * C + B * K + B + B * C) * sizeof(float) + 16;
 }
 
 hex_status_t head_fwd_bwd(int B, int HW, int C, int K, const void* feat, const float* wl, const float* bl,
@@ -133,17 +148,20 @@ hex_status_t head_fwd_bwd(int B, int HW, int C, int K, const void* feat, const f
     float* gap = (float*)ws;
     float* dlog = gap + (size_t)B * C;
     float* loss_b = dlog + (size_t)B * K;
+    float* dg = loss_b + B;
+    if (((uintptr_t)dg & 15) != 0) dg = (float*)(((uintptr_t)dg + 15) & ~(uintptr_t)15);
     const int C8 = C / 8;
     const int slices = HEAD_THREADS / C8 > 0 ? HEAD_THREADS / C8 : 1;
     const size_t smem = ((size_t)slices * C + 16) * sizeof(float);
     if (smem > 48 * 1024) return HEX_ERR_UNSUPPORTED;
     head_sample_kernel<<<B, HEAD_THREADS, smem, st>>>((const uint4*)feat, wl, bl, labels, gap, dlog, loss_b, B, HW,
                                                       C, K);
-    head_param_grad_kernel<<<ceil_div(K * C + K + 1, 256), 256, 0, st>>>(gap, dlog, loss_b, dwl, dbl, loss, B, C, K);
+    head_param_grad_kernel<<<ceil_div((int64_t)(K * C + K + 1) * 32, 256), 256, 0, st>>>(gap, dlog, loss_b, dwl, dbl,
+                                                                                        loss, B, C, K);
+    head_dg_kernel<<<ceil_div((int64_t)B * C, 256), 256, 0, st>>>(dlog, wl, dg, B, C, K, 1.f / (float)HW);
     const int64_t total = (int64_t)B * HW * C8;
-    head_dfeat_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const uint4*)feat, dlog, wl, (uint4*)dfeat, B, HW, C8,
-                                                            K);
-    count_launch(3);
+    head_dfeat_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const uint4*)feat, dg, (uint4*)dfeat, B, HW, C8);
+    count_launch(4);
     return last_launch_status();
 }
 
