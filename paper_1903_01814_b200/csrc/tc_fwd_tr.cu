@@ -44,6 +44,7 @@ constexpr int FT_SMEM_MAX = 227 * 1024;
 struct FtParams {
     int B, H, W, Cin, Cout, T, parity;
     int rt, jt0, jt1, tiles0, mtiles, n_tiles, total_tiles, kchunks, stages;
+    int pair_tiles;  // CTA-pair kernel: (n tile, pair of m tiles) work items
     int relu, has_mask;
     const float* bias;
 };
@@ -63,6 +64,19 @@ __device__ __forceinline__ void ft_decode(const FtParams& p, int tile, int BN, i
     *b = m / jt;
     *r0 = rti * FT_RB;
     *j0 = jti * FT_JB;
+}
+
+// CTA pairs: work item = (n tile, pair of consecutive m tiles); CTA `rank` takes m tile 2 mp + rank.
+// A missing odd tile gets r0 = H: its loads are zero fill and its stores are clipped.
+__device__ __forceinline__ void ft_decode_pair(const FtParams& p, int ptile, int BN, int rank, int* P, int* r0,
+                                               int* j0, int* b, int* n0) {
+    const int nt = ptile % p.n_tiles;
+    const int m = 2 * (ptile / p.n_tiles) + rank;
+    if (m >= p.mtiles) {
+        *P = 0; *r0 = p.H; *j0 = 0; *b = 0; *n0 = nt * BN;
+        return;
+    }
+    ft_decode(p, m * p.n_tiles + nt, BN, P, r0, j0, b, n0);
 }
 
 // Stage list of one 64-channel chunk: (kernel column, first tap, tap count), taps of a column split
@@ -116,7 +130,20 @@ __device__ __forceinline__ void issue_stage(uint32_t d, uint64_t a_desc, uint64_
                           idesc, (i | k) ? 1u : first);
 }
 
-template <int BN, int N, int TG, bool RES, int S>
+// the same for a CTA pair (M = 256, issued by the leader)
+template <int BN, int CNT>
+__device__ __forceinline__ void issue_stage_pair(uint32_t d, uint64_t a_desc, uint64_t b_desc, int b_tap_stride16,
+                                                 uint32_t first) {
+    constexpr uint32_t idesc = ptx::idesc_bf16(256, BN, 0, 0);
+#pragma unroll
+    for (int i = 0; i < CNT; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            ptx::mma_bf16_2sm(d, a_desc + (uint64_t)(i * 64 + k * 2), b_desc + (uint64_t)(i * b_tap_stride16 + k * 2),
+                              idesc, (i | k) ? 1u : first);
+}
+
+template <int BN, int N, int TG, bool RES, bool PAIR, int S>
 __device__ __forceinline__ void issue_stages_from(uint32_t d, uint64_t a_ring, uint64_t b_ring, uint64_t res_desc,
                                                   uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
                                                   int nstages, uint32_t stage16, uint32_t a_bytes16, int kc,
@@ -130,24 +157,30 @@ __device__ __forceinline__ void issue_stages_from(uint32_t d, uint64_t a_ring, u
         const uint64_t ad = a_ring + soff + (uint64_t)(g0 * 64);  // tap g0 = g0 rows (1024 B) into the box
         uint64_t bd;
         int bstride;
-        if (RES) {  // resident weights: tile (t, kc) at ((t * kchunks + kc) * BN * 128) bytes
-            bd = res_desc + (uint64_t)(((tb + g0) * kchunks + kc) * (BN * 8));
-            bstride = kchunks * BN * 8;
+        constexpr int BROWS = PAIR ? BN / 2 : BN;  // weight rows held per CTA
+        if (RES) {  // resident weights: tile (t, kc) at ((t * kchunks + kc) * BROWS * 128) bytes
+            bd = res_desc + (uint64_t)(((tb + g0) * kchunks + kc) * (BROWS * 8));
+            bstride = kchunks * BROWS * 8;
         } else {
             bd = b_ring + soff + a_bytes16;
-            bstride = BN * 8;
+            bstride = BROWS * 8;
         }
-        issue_stage<BN, cnt, RES>(d, ad, bd, bstride, S == 0 ? first : 1u);
-        ptx::mma_commit(&empty[stage]);
+        if constexpr (PAIR) {
+            issue_stage_pair<BN, cnt>(d, ad, bd, bstride, S == 0 ? first : 1u);
+            ptx::mma_commit_2sm(&empty[stage]);
+        } else {
+            issue_stage<BN, cnt, RES>(d, ad, bd, bstride, S == 0 ? first : 1u);
+            ptx::mma_commit(&empty[stage]);
+        }
         if (++stage == nstages) { stage = 0; phase ^= 1; }
-        issue_stages_from<BN, N, TG, RES, S + 1>(d, a_ring, b_ring, res_desc, full, empty, stage, phase, nstages,
+        issue_stages_from<BN, N, TG, RES, PAIR, S + 1>(d, a_ring, b_ring, res_desc, full, empty, stage, phase, nstages,
                                                   stage16, a_bytes16, kc, kchunks, 1u);
     }
 }
 
 }  // namespace
 
-template <int BN, int N, int TG, bool RES>
+template <int BN, int N, int TG, bool RES, bool PAIR>
 __global__ void __launch_bounds__(FT_THREADS, 1)
 tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                  const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
@@ -155,7 +188,7 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                  const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ FtParams p) {
     using SL = StageList<N, TG>;
     constexpr int A_BYTES = (FT_RB + 2 * N) * FT_JB * 128;   // one A box
-    constexpr int W_TILE = BN * 128;                          // one (tap, chunk) weight tile
+    constexpr int W_TILE = (PAIR ? BN / 2 : BN) * 128;         // one (tap, chunk) weight tile (this CTA's rows)
     constexpr int STAGE = RES ? A_BYTES : A_BYTES + TG * W_TILE;
     constexpr int TMEM_COLS = 2 * BN;
     extern __shared__ uint8_t smem_raw[];
@@ -173,11 +206,13 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
     uint32_t* tmem_slot = (uint32_t*)(bres + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], FT_EPI / 32);
+            ptx::mbar_init(&tempty[a], (PAIR ? 2 : 1) * FT_EPI / 32);  // pairs: both CTAs' epilogue warps
             ptx::mbar_init(&mbar[a], 1);
         }
         ptx::mbar_init(bres, 1);
@@ -188,9 +223,13 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
         ptx::prefetch_tmap(&map_y0);
         ptx::prefetch_tmap(&map_y1);
     }
-    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    if (warp == 1) {
+        if constexpr (PAIR) ptx::tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+        else ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) ptx::cluster_sync();
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -204,9 +243,11 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
             }
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+            for (int tile = PAIR ? blockIdx.x / 2 : blockIdx.x; tile < (PAIR ? p.pair_tiles : p.total_tiles);
+             tile += PAIR ? gridDim.x / 2 : gridDim.x) {
                 int P, r0, j0, b, n0;
-                ft_decode(p, tile, BN, &P, &r0, &j0, &b, &n0);
+                if (PAIR) ft_decode_pair(p, tile, BN, (int)rank, &P, &r0, &j0, &b, &n0);
+                else ft_decode(p, tile, BN, &P, &r0, &j0, &b, &n0);
                 const int pc = (P + p.parity) & 1;  // centre column parity
                 for (int kc = 0; kc < p.kchunks; ++kc) {
 #pragma unroll 1
@@ -217,19 +258,29 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                         const int top = -N + (((dc < 0 ? -dc : dc) + pc) >> 1);
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sa = ring + stage * STAGE;
-                        ptx::mbar_arrive_expect_tx(&full[stage], RES ? A_BYTES : A_BYTES + cnt * W_TILE);
-                        ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top, b, kc);
-                        if constexpr (!RES)
+                        const uint32_t bytes = RES ? A_BYTES : A_BYTES + cnt * W_TILE;
+                        if constexpr (PAIR) {  // both CTAs' bytes land on the leader's barrier
+                            if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * bytes);
+                            ptx::tma_load_5d_2sm(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top, b,
+                                                 kc);
                             for (int i = 0; i < cnt; ++i)
-                                ptx::tma_load_4d(&map_w, &full[stage], sa + A_BYTES + i * W_TILE, 0, n0, kc,
-                                                 tb + g0 + i);
+                                ptx::tma_load_4d_2sm(&map_w, &full[stage], sa + A_BYTES + i * W_TILE, 0,
+                                                     n0 + (int)rank * (BN / 2), kc, tb + g0 + i);
+                        } else {
+                            ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+                            ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top, b, kc);
+                            if constexpr (!RES)
+                                for (int i = 0; i < cnt; ++i)
+                                    ptx::tma_load_4d(&map_w, &full[stage], sa + A_BYTES + i * W_TILE, 0, n0, kc,
+                                                     tb + g0 + i);
+                        }
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && (!PAIR || leader)) {
             const uint64_t a_ring = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
             const uint64_t b_ring = a_ring;  // streamed weight tiles sit A_BYTES into the stage
             const uint64_t res_desc = ptx::smem_desc_sw128(ptx::smem_u32(resw), 16, 1024);
@@ -239,15 +290,17 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
             int acc = 0;
             uint32_t aphase = 0;
             if constexpr (RES) ptx::mbar_wait(bres, 0);
-            for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+            for (int tile = PAIR ? blockIdx.x / 2 : blockIdx.x; tile < (PAIR ? p.pair_tiles : p.total_tiles);
+                 tile += PAIR ? gridDim.x / 2 : gridDim.x) {
                 ptx::mbar_wait(&tempty[acc], aphase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
                 for (int kc = 0; kc < p.kchunks; ++kc)
-                    issue_stages_from<BN, N, TG, RES, 0>(d, a_ring, b_ring, res_desc, full, empty, stage, phase,
-                                                         p.stages, stage16, a_bytes16, kc, p.kchunks,
-                                                         kc == 0 ? 0u : 1u);
-                ptx::mma_commit(&tfull[acc]);
+                    issue_stages_from<BN, N, TG, RES, PAIR, 0>(d, a_ring, b_ring, res_desc, full, empty, stage, phase,
+                                                               p.stages, stage16, a_bytes16, kc, p.kchunks,
+                                                               kc == 0 ? 0u : 1u);
+                if constexpr (PAIR) ptx::mma_commit_2sm(&tfull[acc]);
+                else ptx::mma_commit(&tfull[acc]);
                 acc ^= 1;
                 if (acc == 0) aphase ^= 1;
             }
@@ -264,9 +317,11 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
         uint32_t aphase = 0;
         int ob = 0;
         uint32_t mphase0 = 0, mphase1 = 0;
-        for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+        for (int tile = PAIR ? blockIdx.x / 2 : blockIdx.x; tile < (PAIR ? p.pair_tiles : p.total_tiles);
+             tile += PAIR ? gridDim.x / 2 : gridDim.x) {
             int P, r0, j0, b, n0;
-            ft_decode(p, tile, BN, &P, &r0, &j0, &b, &n0);
+            if (PAIR) ft_decode_pair(p, tile, BN, (int)rank, &P, &r0, &j0, &b, &n0);
+            else ft_decode(p, tile, BN, &P, &r0, &j0, &b, &n0);
             const CUtensorMap* my = P ? &map_y1 : &map_y0;
             const CUtensorMap* mm = P ? &map_m1 : &map_m0;
             if (p.has_mask && et == 0) {
@@ -340,7 +395,10 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if (PAIR) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+                else ptx::mbar_arrive(&tempty[acc]);
+            }
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
@@ -348,9 +406,11 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) ptx::cluster_sync();  // the peer's smem / TMEM must outlive the leader's last MMA
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+        if constexpr (PAIR) ptx::tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+        else ptx::tmem_dealloc(tmem_base, TMEM_COLS);
     }
 }
 
@@ -410,40 +470,50 @@ static bool ft_wmap(CUtensorMap* m, const void* base, int T, int Cout, int Cin, 
 
 namespace {
 struct FtPlan {
-    int BN, res, stages, smem;
+    int BN, res, pair, tg, stages, smem;
     bool ok;
 };
 
-constexpr int ft_tg(bool res, int n) { return res ? 2 * n + 1 : 3; }
+// taps per stage: the whole column with resident weights; with streamed weight halves (CTA pairs) as
+// many as keep >= 3 stages in shared memory
+constexpr int ft_tg(bool res, int n, int BN) { return res ? 2 * n + 1 : (BN == 256 ? 2 : (n == 1 ? 3 : 5)); }
 
 FtPlan ft_plan(const Geom& g, int Cin, int Cout) {
     FtPlan pl{};
-    pl.BN = Cout % 128 == 0 ? 128 : (Cout % 64 == 0 ? 64 : 0);
-    if (!pl.BN || Cin % 64) return pl;
-    const int A = (FT_RB + 2 * g.n) * FT_JB * 128, WT = pl.BN * 128;
+    if (Cin % 64) return pl;
+    const int A = (FT_RB + 2 * g.n) * FT_JB * 128;
     const int fixed = 2 * FT_OUT + 1024 + 512;
-    const int res_bytes = g.T * (Cin / 64) * WT;
-    // resident weights when they leave room for >= 4 A stages (the whole weight set of the call:
-    // only one Cout tile then, i.e. Cout == BN)
-    if (Cout == pl.BN && res_bytes + fixed + 4 * A <= FT_SMEM_MAX) {
-        pl.res = 1;
-        pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
-        if (pl.stages > 8) pl.stages = 8;
-        pl.smem = res_bytes + pl.stages * A + fixed;
-    } else {
-        const int st = A + ft_tg(false, g.n) * WT;
-        pl.stages = (FT_SMEM_MAX - fixed) / st;
-        if (pl.stages > 6) pl.stages = 6;
-        if (pl.stages < 2) return pl;
-        pl.smem = pl.stages * st + fixed;
+    // 1) resident weights: one Cout tile (Cout = 64 or 128) whose packed weights leave >= 4 A stages
+    if (Cout == 64 || Cout == 128) {
+        const int res_bytes = g.T * (Cin / 64) * Cout * 128;
+        if (res_bytes + fixed + 4 * A <= FT_SMEM_MAX) {
+            pl.BN = Cout;
+            pl.res = 1;
+            pl.tg = ft_tg(true, g.n, Cout);
+            pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
+            if (pl.stages > 8) pl.stages = 8;
+            pl.smem = res_bytes + pl.stages * A + fixed;
+            pl.ok = true;
+            return pl;
+        }
     }
+    // 2) CTA pairs (M = 256) with streamed weights, each CTA loading half of every weight tile
+    pl.BN = Cout % 256 == 0 ? 256 : (Cout % 128 == 0 ? 128 : 0);
+    if (!pl.BN || getenv("HEXCONV_NO_FWD_TR_PAIR")) return pl;
+    pl.pair = 1;
+    pl.tg = ft_tg(false, g.n, pl.BN);
+    const int st = A + pl.tg * (pl.BN / 2) * 128;
+    pl.stages = (FT_SMEM_MAX - fixed) / st;
+    if (pl.stages > 6) pl.stages = 6;
+    if (pl.stages < 2) return pl;
+    pl.smem = pl.stages * st + fixed;
     pl.ok = true;
     return pl;
 }
 }  // namespace
 
-// Taken for stride-1 bf16 NHWC layers whose 16 x 8 tiles fill >= 85% of both views and whose weights
-// stay resident in shared memory (n = 1, 2); HEXCONV_NO_FWD_TR disables it.
+// Taken for stride-1 bf16 NHWC layers whose 16 x 8 tiles fill >= 85% of both views (n = 1, 2), with
+// resident weights or as CTA pairs; HEXCONV_NO_FWD_TR disables it.
 bool tc_fwd_tr_supported(const Geom& g, int Cin, int Cout) {
     if (getenv("HEXCONV_NO_FWD_TR")) return false;
     if (g.s != 1 || (g.n != 1 && g.n != 2) || g.W < 2 || g.B > 65535) return false;
@@ -452,21 +522,36 @@ bool tc_fwd_tr_supported(const Geom& g, int Cin, int Cout) {
     if (fill_c * fill_r < 0.85) return false;
     const FtPlan pl = ft_plan(g, Cin, Cout);
     if (!pl.ok) return false;
-    // streamed-weight plans measured slower than the CTA-pair kernel of tc_conv.cu (C5 L3/L4, round 1):
-    // only the resident-weight plan is taken unless HEXCONV_FWD_TR_STREAM is set
-    if (!pl.res && !getenv("HEXCONV_FWD_TR_STREAM")) return false;
     return ft_encode() != nullptr;
 }
 
-template <int BN, int N, bool RES>
+template <int BN, int N, bool RES, bool PAIR>
 static hex_status_t launch_ft(const CUtensorMap* maps, const FtParams& p, int smem, cudaStream_t st) {
-    constexpr int TG = ft_tg(RES, N);
-    if (cudaFuncSetAttribute(tc_fwd_tr_kernel<BN, N, TG, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
+    constexpr int TG = ft_tg(RES, N, BN);
+    auto kern = tc_fwd_tr_kernel<BN, N, TG, RES, PAIR>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return HEX_ERR_CUDA;
-    const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
-    tc_fwd_tr_kernel<BN, N, TG, RES><<<grid, FT_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
-                                                                      maps[5], maps[6], p);
+    if constexpr (PAIR) {
+        const int pairs = p.pair_tiles < num_sms() / 2 ? p.pair_tiles : num_sms() / 2;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * pairs);
+        cfg.blockDim = dim3(FT_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p) !=
+            cudaSuccess)
+            return HEX_ERR_CUDA;
+    } else {
+        const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+        kern<<<grid, FT_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
+    }
     count_launch();
     return last_launch_status();
 }
@@ -484,6 +569,7 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
     p.mtiles = p.tiles0 + p.rt * p.jt1 * g.B;
     p.n_tiles = a.Cout / pl.BN;
     p.total_tiles = p.mtiles * p.n_tiles;
+    p.pair_tiles = ceil_div(p.mtiles, 2) * p.n_tiles;
     p.kchunks = a.Cin / 64;
     p.stages = pl.stages;
     p.relu = a.relu;
@@ -492,7 +578,7 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
     CUtensorMap maps[7];
     if (!ft_view5(&maps[0], a.x, g.B, g.H, g.W, a.Cin, 0, FT_RB + 2 * g.n)) return HEX_ERR_CUDA;
     if (!ft_view5(&maps[1], a.x, g.B, g.H, g.W, a.Cin, 1, FT_RB + 2 * g.n)) return HEX_ERR_CUDA;
-    if (!ft_wmap(&maps[2], a.wpack, g.T, a.Cout, a.Cin, pl.BN)) return HEX_ERR_CUDA;
+    if (!ft_wmap(&maps[2], a.wpack, g.T, a.Cout, a.Cin, pl.pair ? pl.BN / 2 : pl.BN)) return HEX_ERR_CUDA;
     if (!ft_view4(&maps[3], a.y, g.B, g.H, g.W, a.Cout, 0)) return HEX_ERR_CUDA;
     if (!ft_view4(&maps[4], a.y, g.B, g.H, g.W, a.Cout, 1)) return HEX_ERR_CUDA;
     if (a.relu_y) {
@@ -502,15 +588,16 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
         maps[5] = maps[3];
         maps[6] = maps[4];
     }
-#define HEX_FT(BN_, N_, R_) return launch_ft<BN_, N_, R_>(maps, p, pl.smem, st)
-    if (pl.BN == 128) {
-        if (g.n == 1) { if (pl.res) HEX_FT(128, 1, true); else HEX_FT(128, 1, false); }
-        else { if (pl.res) HEX_FT(128, 2, true); else HEX_FT(128, 2, false); }
-    } else {
-        if (g.n == 1) { if (pl.res) HEX_FT(64, 1, true); else HEX_FT(64, 1, false); }
-        else { if (pl.res) HEX_FT(64, 2, true); else HEX_FT(64, 2, false); }
+    if (pl.res) {
+        if (pl.BN == 128) return g.n == 1 ? launch_ft<128, 1, true, false>(maps, p, pl.smem, st)
+                                          : launch_ft<128, 2, true, false>(maps, p, pl.smem, st);
+        return g.n == 1 ? launch_ft<64, 1, true, false>(maps, p, pl.smem, st)
+                        : launch_ft<64, 2, true, false>(maps, p, pl.smem, st);
     }
-#undef HEX_FT
+    if (pl.BN == 256) return g.n == 1 ? launch_ft<256, 1, false, true>(maps, p, pl.smem, st)
+                                      : launch_ft<256, 2, false, true>(maps, p, pl.smem, st);
+    return g.n == 1 ? launch_ft<128, 1, false, true>(maps, p, pl.smem, st)
+                    : launch_ft<128, 2, false, true>(maps, p, pl.smem, st);
 }
 
 }  // namespace hexconv

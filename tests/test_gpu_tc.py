@@ -115,3 +115,6 @@ def test_tc_tap_reuse_wgrad_channel_tiles(F, oracle):
     # two Cout tiles x two input-channel chunks (n = 1), and the three n = 2 column groups x two chunks
     case(F, oracle, 1, 128, 256, 16, 16, 1, 0, 7)
     case(F, oracle, 2, 128, 128, 16, 17, 2, 1, 8)
+    # CTA-pair forward with an odd number of 128-pixel tiles (the last pair's second tile is empty)
+    case(F, oracle, 1, 128, 128, 16, 17, 1, 0, 9)
+    case(F, oracle, 1, 256, 256, 16, 17, 2, 1, 10)
