@@ -24,9 +24,9 @@
 // Work unit = (Cout tile of 128, 64-channel input chunk, column group, pixel
 // chunk).  A column group is a set of kernel columns whose taps fit the 512
 // TMEM columns (n = 1: all three columns, 7 taps; n = 2: {-2,-1}, {0}, {1,2}).
-// Warp 0 issues TMA, warp 1 the MMAs, warps 2-5 reduce dbias from the staged
-// dy tiles (units of group 0 / chunk 0) and drain TMEM into a per-pixel-chunk
-// fp32 workspace, summed in a fixed order afterwards: deterministic.
+// Warp 0 issues TMA, warp 1 the MMAs (dbias as an extra block of ones), warps
+// 2-5 drain TMEM into a per-pixel-chunk fp32 workspace, summed in a fixed
+// order afterwards: deterministic.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -126,7 +126,7 @@ __device__ __forceinline__ void mma_loop(const MmaLoopArgs& m) {
         const uint64_t soff = (uint64_t)stage * m.stage16;
         const uint64_t ad0 = m.a_desc0 + soff, xd0 = m.x_desc0 + soff;
         if (m.dbg != 2) {
-#pragma unroll 1
+#pragma unroll
             for (int k = 0; k < KSTEPS; ++k) {
                 const uint64_t ad = ad0 + (uint64_t)(k * 128);  // 16 pixels = 2048 B
                 const uint64_t xk = xd0 + (uint64_t)(k * 128);
@@ -173,9 +173,12 @@ tc_wgrad_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
     uint64_t* tfull = empty + p.stages;
     uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
 
-    // dbias rides on the MMA: units of group 0 / chunk 0 add an N = 64 block of ones to B, whose
-    // accumulator columns are sum_px dy[px][co] (the group's taps use at most 448 of the 512 columns)
-    const bool do_db = p.db_part != nullptr && grp == 0 && kc == 0;
+    // dbias rides on the MMA: units of chunk 0 of one group add an N = 64 block of ones to B, whose
+    // accumulator columns are sum_px dy[px][co] (a group's taps use at most 448 of the 512 columns).
+    // n = 2: the centre-column group (5 taps + the block = 7 blocks like the two side groups, so every
+    // unit carries equal MMA work).  (Summing the staged dy tiles in the idle epilogue warps instead
+    // measured slower for n = 1: the stage release then waits for them.)
+    const bool do_db = p.db_part != nullptr && grp == (p.n == 1 ? 0 : 1) && kc == 0;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     for (int i = threadIdx.x; i < 512; i += blockDim.x) reinterpret_cast<uint32_t*>(ones)[i] = 0x3F803F80u;
     ptx::fence_proxy_async();  // generic smem writes -> visible to the tensor core (async proxy)
@@ -237,9 +240,9 @@ tc_wgrad_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
             switch (key) {
                 case 0: mma_loop<RB, 1, 0, false>(m); break;
                 case 1: mma_loop<RB, 1, 0, true>(m); break;
-                case 2: mma_loop<RB, 2, 0, false>(m); break;
-                case 3: mma_loop<RB, 2, 0, true>(m); break;
-                case 4: case 5: mma_loop<RB, 2, 1, false>(m); break;  // dbias only rides on group 0
+                case 2: case 3: mma_loop<RB, 2, 0, false>(m); break;
+                case 4: mma_loop<RB, 2, 1, false>(m); break;
+                case 5: mma_loop<RB, 2, 1, true>(m); break;  // dbias rides on the centre-column group
                 default: mma_loop<RB, 2, 2, false>(m); break;
             }
         }
