@@ -484,7 +484,7 @@ FtPlan ft_plan(const Geom& g, int Cin, int Cout) {
     const int A = (FT_RB + 2 * g.n) * FT_JB * 128;
     const int fixed = 2 * FT_OUT + 1024 + 512;
     // 1) resident weights: one Cout tile (Cout = 64 or 128) whose packed weights leave >= 4 A stages
-    if (Cout == 64 || Cout == 128) {
+    if ((Cout == 64 || Cout == 128) && !getenv("HEXCONV_FWD_TR_NORES")) {
         const int res_bytes = g.T * (Cin / 64) * Cout * 128;
         if (res_bytes + fixed + 4 * A <= FT_SMEM_MAX) {
             pl.BN = Cout;
@@ -498,7 +498,7 @@ FtPlan ft_plan(const Geom& g, int Cin, int Cout) {
         }
     }
     // 2) CTA pairs (M = 256) with streamed weights, each CTA loading half of every weight tile
-    pl.BN = Cout % 256 == 0 ? 256 : (Cout % 128 == 0 ? 128 : 0);
+    pl.BN = Cout % 256 == 0 ? 256 : (Cout % 128 == 0 ? 128 : (Cout % 64 == 0 ? 64 : 0));
     if (!pl.BN || getenv("HEXCONV_NO_FWD_TR_PAIR")) return pl;
     pl.pair = 1;
     pl.tg = ft_tg(false, g.n, pl.BN);
@@ -596,8 +596,10 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
     }
     if (pl.BN == 256) return g.n == 1 ? launch_ft<256, 1, false, true>(maps, p, pl.smem, st)
                                       : launch_ft<256, 2, false, true>(maps, p, pl.smem, st);
-    return g.n == 1 ? launch_ft<128, 1, false, true>(maps, p, pl.smem, st)
-                    : launch_ft<128, 2, false, true>(maps, p, pl.smem, st);
+    if (pl.BN == 128) return g.n == 1 ? launch_ft<128, 1, false, true>(maps, p, pl.smem, st)
+                                      : launch_ft<128, 2, false, true>(maps, p, pl.smem, st);
+    return g.n == 1 ? launch_ft<64, 1, false, true>(maps, p, pl.smem, st)
+                    : launch_ft<64, 2, false, true>(maps, p, pl.smem, st);
 }
 
 }  // namespace hexconv
