@@ -236,10 +236,18 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
     if (warp == 0) {
         if (lane == 0) {
             if constexpr (RES) {
-                ptx::mbar_arrive_expect_tx(bres, (uint32_t)res_bytes);
-                for (int t = 0; t < p.T; ++t)
-                    for (int kc = 0; kc < p.kchunks; ++kc)
-                        ptx::tma_load_4d(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0, 0, kc, t);
+                if constexpr (PAIR) {  // each CTA holds its half of every tile; bytes land on the leader
+                    if (leader) ptx::mbar_arrive_expect_tx(bres, (uint32_t)(2 * res_bytes));
+                    for (int t = 0; t < p.T; ++t)
+                        for (int kc = 0; kc < p.kchunks; ++kc)
+                            ptx::tma_load_4d_2sm(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0,
+                                                 (int)rank * (BN / 2), kc, t);
+                } else {
+                    ptx::mbar_arrive_expect_tx(bres, (uint32_t)res_bytes);
+                    for (int t = 0; t < p.T; ++t)
+                        for (int kc = 0; kc < p.kchunks; ++kc)
+                            ptx::tma_load_4d(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0, 0, kc, t);
+                }
             }
             int stage = 0;
             uint32_t phase = 0;
@@ -263,9 +271,10 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                             if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * bytes);
                             ptx::tma_load_5d_2sm(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top, b,
                                                  kc);
-                            for (int i = 0; i < cnt; ++i)
-                                ptx::tma_load_4d_2sm(&map_w, &full[stage], sa + A_BYTES + i * W_TILE, 0,
-                                                     n0 + (int)rank * (BN / 2), kc, tb + g0 + i);
+                            if constexpr (!RES)
+                                for (int i = 0; i < cnt; ++i)
+                                    ptx::tma_load_4d_2sm(&map_w, &full[stage], sa + A_BYTES + i * W_TILE, 0,
+                                                         n0 + (int)rank * (BN / 2), kc, tb + g0 + i);
                         } else {
                             ptx::mbar_arrive_expect_tx(&full[stage], bytes);
                             ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top, b, kc);
@@ -317,6 +326,18 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
         uint32_t aphase = 0;
         int ob = 0;
         uint32_t mphase0 = 0, mphase1 = 0;
+        // ReLU-backward mask tiles are TMA-loaded one chunk ahead -- across tile boundaries too, so
+        // the next tile's first mask chunk is in flight while the current tile's last chunk drains
+        if (p.has_mask && et == 0) {
+            const int t0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+            if (t0 < (PAIR ? p.pair_tiles : p.total_tiles)) {
+                int P, r0, j0, b, n0;
+                if (PAIR) ft_decode_pair(p, t0, BN, (int)rank, &P, &r0, &j0, &b, &n0);
+                else ft_decode(p, t0, BN, &P, &r0, &j0, &b, &n0);
+                ptx::mbar_arrive_expect_tx(&mbar[0], FT_OUT);
+                ptx::tma_load_4d(P ? &map_m1 : &map_m0, &mbar[0], obuf, n0, j0, r0, b);
+            }
+        }
         for (int tile = PAIR ? blockIdx.x / 2 : blockIdx.x; tile < (PAIR ? p.pair_tiles : p.total_tiles);
              tile += PAIR ? gridDim.x / 2 : gridDim.x) {
             int P, r0, j0, b, n0;
@@ -324,11 +345,6 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
             else ft_decode(p, tile, BN, &P, &r0, &j0, &b, &n0);
             const CUtensorMap* my = P ? &map_y1 : &map_y0;
             const CUtensorMap* mm = P ? &map_m1 : &map_m0;
-            if (p.has_mask && et == 0) {
-                ptx::bulk_wait_read<1>();
-                ptx::mbar_arrive_expect_tx(&mbar[ob], FT_OUT);
-                ptx::tma_load_4d(mm, &mbar[ob], obuf + ob * FT_OUT, n0, j0, r0, b);
-            }
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
 #pragma unroll 1
@@ -385,10 +401,23 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                 if (et == 0) {
                     ptx::tma_store_4d(my, buf, c0, j0, r0, b);
                     ptx::bulk_commit();
-                    if (p.has_mask && ch + 1 < BN / 64) {
-                        ptx::bulk_wait_read<1>();
-                        ptx::mbar_arrive_expect_tx(&mbar[ob ^ 1], FT_OUT);
-                        ptx::tma_load_4d(mm, &mbar[ob ^ 1], obuf + (ob ^ 1) * FT_OUT, c0 + 64, j0, r0, b);
+                    if (p.has_mask) {
+                        if (ch + 1 < BN / 64) {
+                            ptx::bulk_wait_read<1>();
+                            ptx::mbar_arrive_expect_tx(&mbar[ob ^ 1], FT_OUT);
+                            ptx::tma_load_4d(mm, &mbar[ob ^ 1], obuf + (ob ^ 1) * FT_OUT, c0 + 64, j0, r0, b);
+                        } else {
+                            const int nt = tile + (PAIR ? gridDim.x / 2 : gridDim.x);
+                            if (nt < (PAIR ? p.pair_tiles : p.total_tiles)) {
+                                int P2, r2, j2, b2, n2;
+                                if (PAIR) ft_decode_pair(p, nt, BN, (int)rank, &P2, &r2, &j2, &b2, &n2);
+                                else ft_decode(p, nt, BN, &P2, &r2, &j2, &b2, &n2);
+                                ptx::bulk_wait_read<1>();
+                                ptx::mbar_arrive_expect_tx(&mbar[ob ^ 1], FT_OUT);
+                                ptx::tma_load_4d(P2 ? &map_m1 : &map_m0, &mbar[ob ^ 1], obuf + (ob ^ 1) * FT_OUT, n2,
+                                                 j2, r2, b2);
+                            }
+                        }
                     }
                 }
                 ob ^= 1;
@@ -483,7 +512,23 @@ FtPlan ft_plan(const Geom& g, int Cin, int Cout) {
     if (Cin % 64) return pl;
     const int A = (FT_RB + 2 * g.n) * FT_JB * 128;
     const int fixed = 2 * FT_OUT + 1024 + 512;
-    // 1) resident weights: one Cout tile (Cout = 64 or 128) whose packed weights leave >= 4 A stages
+    // 1) resident weights: one Cout tile (Cout = 64 or 128), one CTA per tile.  The CTA-pair variant
+    //    (each CTA keeps half of the weights, more room for A stages) measured slower on C5 layer 2
+    //    (fwd 382 vs 230 us) and is kept for experiments (HEXCONV_FWD_TR_RESPAIR).
+    if ((Cout == 64 || Cout == 128) && !getenv("HEXCONV_FWD_TR_NORES") && getenv("HEXCONV_FWD_TR_RESPAIR")) {
+        const int res_bytes = g.T * (Cin / 64) * (Cout / 2) * 128;
+        if (res_bytes + fixed + 4 * A <= FT_SMEM_MAX) {
+            pl.BN = Cout;
+            pl.res = 1;
+            pl.pair = 1;
+            pl.tg = ft_tg(true, g.n, Cout);
+            pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
+            if (pl.stages > 8) pl.stages = 8;
+            pl.smem = res_bytes + pl.stages * A + fixed;
+            pl.ok = true;
+            return pl;
+        }
+    }
     if ((Cout == 64 || Cout == 128) && !getenv("HEXCONV_FWD_TR_NORES")) {
         const int res_bytes = g.T * (Cin / 64) * Cout * 128;
         if (res_bytes + fixed + 4 * A <= FT_SMEM_MAX) {
@@ -587,6 +632,12 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
     } else {
         maps[5] = maps[3];
         maps[6] = maps[4];
+    }
+    if (pl.res && pl.pair) {
+        if (pl.BN == 128) return g.n == 1 ? launch_ft<128, 1, true, true>(maps, p, pl.smem, st)
+                                          : launch_ft<128, 2, true, true>(maps, p, pl.smem, st);
+        return g.n == 1 ? launch_ft<64, 1, true, true>(maps, p, pl.smem, st)
+                        : launch_ft<64, 2, true, true>(maps, p, pl.smem, st);
     }
     if (pl.res) {
         if (pl.BN == 128) return g.n == 1 ? launch_ft<128, 1, true, false>(maps, p, pl.smem, st)
