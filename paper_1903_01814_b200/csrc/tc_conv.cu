@@ -1155,8 +1155,17 @@ __global__ void wgrad_tc_reduce_kernel(const float* __restrict__ part, int chunk
     const int64_t q = idx / Cin;
     const int co = (int)(q % Cout);
     const int t = (int)(q / Cout);
-    float s = 0.f;
-    for (int c = 0; c < chunks; ++c) s += part[(int64_t)c * total + idx];
+    // eight independent partial sums (chunk c -> sum c mod 8) keep eight loads in flight per thread;
+    // combined in a fixed tree order: deterministic
+    float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int c = 0;
+    for (; c + 8 <= chunks; c += 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s8[j] += part[(int64_t)(c + j) * total + idx];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (c + j < chunks) s8[j] += part[(int64_t)(c + j) * total + idx];
+    const float s = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
     float* d = dw + ((int64_t)co * Cin + ci) * T + t;
     *d = accumulate ? *d + s : s;
 }
