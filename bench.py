@@ -322,6 +322,7 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the config 2-4 measurements")
+    ap.add_argument("--no-graph", action="store_true", help="e2e leg without CUDA-graph replay")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -434,12 +435,19 @@ def main():
     except Exception:
         pass
 
-    # ---- end-to-end through the public API with host buffers
+    # ---- end-to-end through the public API with host buffers: each step copies its batch from pinned
+    # host memory into the model's input buffers, runs the step (one CUDA-graph replay of
+    # HexCNN.graphed_step on one GPU; eager under data parallelism) and reads the loss back
     pin_x = [torch.from_numpy(a.astype(np.float32)).to(torch.bfloat16).pin_memory() for a in xs_np]
     pin_y = [torch.from_numpy(a).pin_memory() for a in ys_np]
     xd = torch.empty_like(xs[0])
     yd = torch.empty_like(ys[0])
     loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+    graph = None
+    if world == 1 and not args.no_graph:
+        xd.copy_(xs[0])
+        yd.copy_(ys[0])
+        graph, gloss = model.graphed_step(xd, yd)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -447,7 +455,11 @@ def main():
     for i in range(args.steps):
         xd.copy_(pin_x[i % NB], non_blocking=True)
         yd.copy_(pin_y[i % NB], non_blocking=True)
-        loss = model.step(xd, yd)
+        if graph is not None:
+            graph.replay()
+            loss = gloss
+        else:
+            loss = model.step(xd, yd)
         loss_h.copy_(loss, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     e1.record()
@@ -483,7 +495,8 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": WORKLOAD, "global_batch": B * world, "per_gpu_batch": B, "grid": "96x96",
                        "parallelism": f"dp{world}", "l2": "working set > L2 (activations ~2.5 GB/step)"},
-            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
+                    "cuda_graph": graph is not None},
             "roofline": {"bound": "tensor", "kernel": "tc_conv_fwd_kernel / tc_conv_fwd2_kernel (tcgen05 "
                                                       "implicit-GEMM hex conv; fwd + bwd-data of layers 2-6)",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",

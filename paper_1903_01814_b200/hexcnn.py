@@ -268,6 +268,24 @@ class HexCNN:
                                          self.lr, self.mu, 1.0 / self.world, _p(self.params_bf16), stream), "sgd")
         return self.loss
 
+    def graphed_step(self, x, labels):
+        """Capture one training step on the static buffers (x, labels) in a CUDA graph and return
+        (graph, loss): graph.replay() runs the whole step (every kernel of every layer, head and SGD)
+        as one launch, without per-call host dispatch; refill x / labels in place between replays.
+        Single process only (the NCCL gradient allreduce of world > 1 stays eager).  The warm-up
+        call performs one real step."""
+        if self.world > 1:
+            raise RuntimeError("graphed_step: data-parallel steps run eagerly")
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.step(x, labels)  # first-call work (function attributes, allocator) outside the capture
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            loss = self.step(x, labels)
+        return graph, loss
+
     # ------------------------------------------------------------------ accounting
     def pool_bytes(self, l, kind):
         """Algorithmic HBM bytes of one pool call after layer l (read inputs + write outputs once)."""

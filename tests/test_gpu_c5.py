@@ -137,3 +137,23 @@ def test_c5_paths(run):
             a = ctypes.c_int32()
             A.check(A.lib().hex_conv2d_algo(ctypes.byref(m.desc[l]), pass_id, ctypes.byref(a)), "algo")
             assert a.value == (0 if l == 0 else 1), (l, pass_id)
+
+
+def test_graphed_step_matches_eager():
+    # HexCNN.graphed_step (bench.py's e2e leg): a CUDA-graph replay of the step gives bit-identical
+    # parameters to the eager step (same kernels, deterministic reductions)
+    import synth
+    from paper_1903_01814_b200.hexcnn import HexCNN
+    B = 8
+    x = torch.from_numpy(np.ascontiguousarray(synth.shower_images(B, 96, 96, 47, 11).transpose(0, 2, 3, 1))
+                         ).cuda().to(torch.bfloat16)
+    y = torch.from_numpy(synth.labels(B, 12)).cuda()
+    a, b = HexCNN(batch=B, seed=3), HexCNN(batch=B, seed=3)
+    a.step(x, y)
+    la = a.step(x, y).clone()
+    g, lb = b.graphed_step(x, y)   # one real (warm-up) step
+    g.replay()                     # the second step
+    torch.cuda.synchronize()
+    assert torch.equal(a.params, b.params)
+    assert torch.equal(a.mom, b.mom)
+    assert la.item() == lb.item()
