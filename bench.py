@@ -497,8 +497,8 @@ def main():
                        "parallelism": f"dp{world}", "l2": "working set > L2 (activations ~2.5 GB/step)"},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
                     "cuda_graph": graph is not None},
-            "roofline": {"bound": "tensor", "kernel": "tc_conv_fwd_kernel / tc_conv_fwd2_kernel (tcgen05 "
-                                                      "implicit-GEMM hex conv; fwd + bwd-data of layers 2-6)",
+            "roofline": {"bound": "tensor", "kernel": "tc_fwd_tr_kernel (layers 2-4) / tc_conv_fwd2_kernel (layers "
+                                                      "5-6): tcgen05 implicit-GEMM hex conv, fwd + bwd-data",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": traffic,
                          "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",

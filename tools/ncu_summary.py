@@ -27,6 +27,8 @@ def main():
             continue
         unit = r.get("Metric Unit", "")
         v = float(r["Metric Value"].replace(",", ""))
+        if v != v:  # nan: a launch ncu could not time (e.g. cut off at process exit)
+            continue
         scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}.get(unit, 1.0)
         rows.append((short(r["Kernel Name"]), v * scale))
     agg = defaultdict(lambda: [0, 0.0])
