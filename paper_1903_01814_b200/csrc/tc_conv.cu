@@ -1146,38 +1146,40 @@ tc_conv_wgrad2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_c
 
 // dw[co][ci][t] (+)= sum_chunk part[chunk][t][co][ci]   (fixed chunk order)
 __global__ void wgrad_tc_reduce_kernel(const float* __restrict__ part, int chunks, int T, int Cout, int Cin,
-                                       float* __restrict__ dw, int accumulate) {
+                                       float* __restrict__ dw, const float* __restrict__ db_part,
+                                       float* __restrict__ dbias, int accumulate) {
+    // threads [0, T*Cout*Cin) reduce dw, the next Cout threads dbias (one launch for both)
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t total = (int64_t)T * Cout * Cin;
-    if (idx >= total) return;
-    // idx enumerates (t, co, ci) with ci fastest (coalesced partial reads)
-    const int ci = (int)(idx % Cin);
-    const int64_t q = idx / Cin;
-    const int co = (int)(q % Cout);
-    const int t = (int)(q / Cout);
+    const bool is_db = idx >= total;
+    if (is_db && (dbias == nullptr || idx >= total + Cout)) return;
+    const float* src = is_db ? db_part : part;
+    const int64_t stride = is_db ? Cout : total;
+    const int64_t off = is_db ? idx - total : idx;
     // eight independent partial sums (chunk c -> sum c mod 8) keep eight loads in flight per thread;
     // combined in a fixed tree order: deterministic
     float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     int c = 0;
     for (; c + 8 <= chunks; c += 8)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s8[j] += part[(int64_t)(c + j) * total + idx];
+        for (int j = 0; j < 8; ++j) s8[j] += src[(int64_t)(c + j) * stride + off];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-        if (c + j < chunks) s8[j] += part[(int64_t)(c + j) * total + idx];
+        if (c + j < chunks) s8[j] += src[(int64_t)(c + j) * stride + off];
     const float s = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+    if (is_db) {
+        dbias[off] = accumulate ? dbias[off] + s : s;
+        return;
+    }
+    // idx enumerates (t, co, ci) with ci fastest (coalesced partial reads)
+    const int ci = (int)(idx % Cin);
+    const int64_t q = idx / Cin;
+    const int co = (int)(q % Cout);
+    const int t = (int)(q / Cout);
     float* d = dw + ((int64_t)co * Cin + ci) * T + t;
     *d = accumulate ? *d + s : s;
 }
 
-__global__ void dbias_reduce_kernel(const float* __restrict__ part, int chunks, int Cout, float* __restrict__ db,
-                                    int accumulate) {
-    const int co = blockIdx.x * blockDim.x + threadIdx.x;
-    if (co >= Cout) return;
-    float s = 0.f;
-    for (int c = 0; c < chunks; ++c) s += part[(int64_t)c * Cout + co];
-    db[co] = accumulate ? db[co] + s : s;
-}
 
 struct WgPlan {
     int RB, JB, BB, rt, bt, jt0, jt1, tiles0, ptiles;
@@ -1254,14 +1256,9 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
         const hex_status_t s = tc_wgrad_tr(a, ws, ws_bytes, &chunks, &db_part, st);
         if (s != HEX_OK) return s;
         const int64_t total = (int64_t)g.T * a.Cout * a.Cin;
-        wgrad_tc_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const float*)ws, chunks, g.T, a.Cout, a.Cin,
-                                                                     a.dw, a.accumulate);
+        wgrad_tc_reduce_kernel<<<ceil_div(total + a.Cout, 256), 256, 0, st>>>(
+            (const float*)ws, chunks, g.T, a.Cout, a.Cin, a.dw, db_part, a.dbias, a.accumulate);
         count_launch();
-        if (a.dbias) {
-            dbias_reduce_kernel<<<ceil_div(a.Cout, 256), 256, 0, st>>>(db_part, chunks, a.Cout, a.dbias,
-                                                                       a.accumulate);
-            count_launch();
-        }
         return last_launch_status();
     }
     const WgPlan w = wg_plan(g, a.Cin, a.Cout);
@@ -1305,14 +1302,9 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
     }
     count_launch();
     const int64_t total = (int64_t)g.T * a.Cout * a.Cin;
-    wgrad_tc_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const float*)ws, w.chunks, g.T, a.Cout, a.Cin,
-                                                                 a.dw, a.accumulate);
+    wgrad_tc_reduce_kernel<<<ceil_div(total + a.Cout, 256), 256, 0, st>>>(
+        (const float*)ws, w.chunks, g.T, a.Cout, a.Cin, a.dw, p.db_part, a.dbias, a.accumulate);
     count_launch();
-    if (a.dbias) {
-        dbias_reduce_kernel<<<ceil_div(a.Cout, 256), 256, 0, st>>>(p.db_part, w.chunks, a.Cout, a.dbias,
-                                                                   a.accumulate);
-        count_launch();
-    }
     return last_launch_status();
 }
 
