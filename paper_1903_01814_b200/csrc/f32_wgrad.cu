@@ -10,7 +10,8 @@
 // channels; it walks each pixel column of a staged band top to bottom, keeping
 // the column's 2n+1 tap values in a register sliding window (one new shared
 // load per pixel) while the 8 dy values of the pixel arrive as two broadcast
-// 16-byte shared loads: 8 x (2n+1) FFMAs per ~3 shared loads.  Blocks are
+// 16-byte shared loads: 8 x (2n+1) FFMAs per ~3 shared loads.  dbias is a
+// separate plane-sum pass (f32_dbias_partial_kernel).  Blocks are
 // persistent over image bands; each thread's accumulators are its own outputs,
 // written once per block as partials and summed over blocks in a fixed order
 // (deterministic).
@@ -49,17 +50,13 @@ f32_wgrad_kernel(const float* __restrict__ x, const float* __restrict__ dy, floa
     const int ci = rem / L, dcs = rem - ci * L;     // kernel column slot dc = dcs - N
     const int dc = dcs - N;
     const int len = L - (dc < 0 ? -dc : dc);
-    const bool do_db = ci == 0 && dc == 0;
     const int nthreads = blockDim.x;
 
     float acc[FW_CO][L];
-    float accb[FW_CO];
 #pragma unroll
-    for (int j = 0; j < FW_CO; ++j) {
-        accb[j] = 0.f;
+    for (int j = 0; j < FW_CO; ++j)
 #pragma unroll
         for (int k = 0; k < L; ++k) acc[j][k] = 0.f;
-    }
 
     const int nb = (H + FW_RB - 1) / FW_RB;
     const int64_t HW = (int64_t)H * W;
@@ -95,12 +92,13 @@ f32_wgrad_kernel(const float* __restrict__ x, const float* __restrict__ dy, floa
             const int top = -N + (((dc < 0 ? -dc : dc) + p) >> 1);
             // staged row of image row r0 + rl + top + k is rl + top + k + N
             const float* col = xc0 + (c + dc + N) * RBp + top + N;
-            float win[L];
+            // the column's FW_RB + L - 1 staged values; with the row loop fully unrolled the sliding
+            // window is pure register renaming (no moves)
+            float colv[FW_RB + L - 1];
 #pragma unroll
-            for (int k = 0; k < L - 1; ++k) win[k] = col[k];
-#pragma unroll 2
+            for (int k = 0; k < FW_RB + L - 1; ++k) colv[k] = col[k];
+#pragma unroll
             for (int rl = 0; rl < FW_RB; ++rl) {
-                win[L - 1] = col[rl + L - 1];
                 const int q = rl * W + c;
                 const float* dq = ds + q * COT;
                 const float4 g0 = *reinterpret_cast<const float4*>(dq + ((((2 * cs) ^ q) & (COT / 4 - 1)) << 2));
@@ -109,12 +107,7 @@ f32_wgrad_kernel(const float* __restrict__ x, const float* __restrict__ dy, floa
 #pragma unroll
                 for (int j = 0; j < FW_CO; ++j)
 #pragma unroll
-                    for (int k = 0; k < L; ++k) acc[j][k] = fmaf(g[j], win[k], acc[j][k]);
-                if (do_db)
-#pragma unroll
-                    for (int j = 0; j < FW_CO; ++j) accb[j] += g[j];
-#pragma unroll
-                for (int k = 0; k < L - 1; ++k) win[k] = win[k + 1];
+                    for (int k = 0; k < L; ++k) acc[j][k] = fmaf(g[j], colv[rl + k], acc[j][k]);
             }
         }
     }
@@ -130,8 +123,36 @@ f32_wgrad_kernel(const float* __restrict__ x, const float* __restrict__ dy, floa
 #pragma unroll
         for (int k = 0; k < L; ++k)
             if (k < len) pp[k] = acc[j][k];
-        if (do_db) db_part[(int64_t)blk * Cout + co] = accb[j];
     }
+    (void)db_part;
+}
+
+// dbias partials: block (blk, co) sums the dy planes of channel co of images blk, blk + nblk, ...
+// (float4 loads, fixed-order block reduction) -> db_part[blk][co], reduced with the dW partials.
+__global__ void __launch_bounds__(256)
+f32_dbias_partial_kernel(const float* __restrict__ dy, float* __restrict__ db_part, int B, int Cout, int HW,
+                         int nblk) {
+    __shared__ float red[256];
+    const int blk = blockIdx.x, co = blockIdx.y;
+    float s = 0.f;
+    for (int b = blk; b < B; b += nblk) {
+        const float* pl = dy + ((int64_t)b * Cout + co) * HW;
+        if ((HW & 3) == 0 && ((uintptr_t)pl & 15) == 0) {
+            for (int i = threadIdx.x; i < (HW >> 2); i += blockDim.x) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(pl) + i);
+                s += (v.x + v.y) + (v.z + v.w);
+            }
+        } else {
+            for (int i = threadIdx.x; i < HW; i += blockDim.x) s += __ldg(pl + i);
+        }
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) db_part[(int64_t)blk * Cout + co] = red[0];
 }
 
 // dw[co][ci][t] (+)= sum_blk part[blk][co][ci][t]; dbias likewise (fixed block order)
@@ -218,6 +239,10 @@ hex_status_t f32_wgrad(const float* x, const float* dy, float* dw, float* dbias,
                                                               p.COT);
     }
     count_launch();
+    if (dbias) {
+        f32_dbias_partial_kernel<<<dim3(p.blocks, Cout), 256, 0, st>>>(dy, db_part, g.B, Cout, g.H * g.W, p.blocks);
+        count_launch();
+    }
     // the partials of different co tiles were written by different grid.y blocks into the same
     // part[blk] slab (disjoint co ranges), so the reduction runs over grid.x blocks only
     const int64_t outs = n_w + (dbias ? Cout : 0);
