@@ -64,27 +64,36 @@ f32_wgrad_kernel(const float* __restrict__ x, const float* __restrict__ dy, floa
         const int b = band / nb, r0 = (band - b * nb) * FW_RB;
         const int rows = min(FW_RB, H - r0);
         __syncthreads();
-        // stage x rows r0-N .. r0+FW_RB-1+N (zero outside), column-major per channel
+        // stage x rows r0-N .. r0+FW_RB-1+N (zero outside), column-major per channel: 4-byte cp.async
+        // (zero fill off the grid), all in flight at once instead of one load round trip per element
+        const uint32_t xs_s = (uint32_t)__cvta_generic_to_shared(xs);
         for (int i = threadIdx.x; i < Cin * RBp * Wp; i += nthreads) {
             const int c_ = i / (RBp * Wp);
             const int q = i - c_ * RBp * Wp;
             const int rr = q / Wp, cc = q - rr * Wp;  // row-major walk of global memory (coalesced)
             const int r = r0 - N + rr, c = cc - N;
-            float v = 0.f;
-            if (r >= 0 && r < H && c >= 0 && c < W) v = __ldg(x + ((int64_t)b * Cin + c_) * HW + (int64_t)r * W + c);
-            xs[c_ * xs_ci + cc * RBp + rr] = v;
+            const bool ok = r >= 0 && r < H && c >= 0 && c < W;
+            const float* src = x + ((int64_t)b * Cin + c_) * HW + (ok ? (int64_t)r * W + c : 0);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(xs_s + 4u * (c_ * xs_ci + cc * RBp + rr)),
+                         "l"(src), "r"(ok ? 4 : 0)
+                         : "memory");
         }
         // stage dy rows r0 .. r0+rows-1 transposed to [pixel][co] (rows beyond the image: 0).  The
         // 16-byte chunks of a pixel row are XOR-swizzled by the pixel index so that consecutive pixels
         // of one channel land in different banks (fewer store conflicts than a plain transpose).
+        const uint32_t ds_s = (uint32_t)__cvta_generic_to_shared(ds);
         for (int i = threadIdx.x; i < COT * FW_RB * W; i += nthreads) {
             const int co = i / (FW_RB * W);
             const int q = i - co * FW_RB * W;  // pixel within the band (row-major)
             const int rl = q / W;
-            float v = 0.f;
-            if (rl < rows && co0 + co < Cout) v = __ldg(dy + ((int64_t)b * Cout + co0 + co) * HW + (int64_t)r0 * W + q);
-            ds[q * COT + ((((co >> 2) ^ q) & (COT / 4 - 1)) << 2) + (co & 3)] = v;
+            const bool ok = rl < rows && co0 + co < Cout;
+            const float* src = dy + ((int64_t)b * Cout + (ok ? co0 + co : 0)) * HW + (ok ? (int64_t)r0 * W + q : 0);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
+                             ds_s + 4u * (q * COT + ((((co >> 2) ^ q) & (COT / 4 - 1)) << 2) + (co & 3))),
+                         "l"(src), "r"(ok ? 4 : 0)
+                         : "memory");
         }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
         const float* xc0 = xs + ci * xs_ci;
         for (int c = 0; c < W; ++c) {
