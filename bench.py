@@ -413,6 +413,8 @@ def main():
                 add("tc_conv_wgrad (tcgen05, layers 2-6)", dt, fl, "TFLOP/s")
             else:
                 add("tc_conv_fwd (tcgen05 fwd + bwd-data, layers 2-6)", dt, fl, "TFLOP/s")
+        elif kind == "fwd_pool":  # fused conv + ReLU + max pool: the conv's algorithmic FLOPs (no halo recompute)
+            add("tc_conv_maxpool (fused conv+ReLU+maxpool, tcgen05)", dt, per_layer[l][0] * B, "TFLOP/s")
         else:
             add("pool (max n1 s2 fwd + bwd)", dt, model.pool_bytes(l, kind), "GB/s")
     peaks, peak_src = load_peaks()

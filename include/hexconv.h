@@ -157,6 +157,22 @@ HEX_API hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* desc, const 
                                    float* dw, float* dbias, int32_t accumulate,
                                    void* ws, size_t ws_bytes, hex_stream_t stream);
 
+/* Fused forward + ReLU + max pool (PAPER.md:144-151 then 202-205):
+ *   y_pool = maxpool_{n=1, stride 2}( relu?( conv(x, w) + bias ) )
+ * with the pool's lattice, window, tie-break and argmax exactly as hex_pool2d_fwd
+ * (desc->parity, A8/A9) on the conv output grid, bit-identical to
+ * hex_conv2d_fwd followed by hex_pool2d_fwd, but the conv output is never
+ * written to memory.  desc: stride 1, bf16, NHWC.  y_pool: bf16 NHWC
+ * [B][Ho][Wo][Cout], argmax_tap: uint8 [B][Ho][Wo][Cout] (not NULL), with
+ * (Ho, Wo) = hex_output_shape(H, W, 2, parity).  ws as for pass 0.
+ * HEX_ERR_UNSUPPORTED when no fused kernel covers the shape (the caller then
+ * runs the two passes); hex_conv2d_fwd_maxpool_supported answers up front. */
+HEX_API int32_t hex_conv2d_fwd_maxpool_supported(const hex_conv2d_desc_t* desc);
+HEX_API hex_status_t hex_conv2d_fwd_maxpool(const hex_conv2d_desc_t* desc, const void* x, const void* w,
+                                            const float* bias, int32_t fuse_relu, void* y_pool,
+                                            uint8_t* argmax_tap, void* ws, size_t ws_bytes,
+                                            hex_stream_t stream);
+
 /* Which kernel family a call with this descriptor runs: *algo (host) = 0 for
  * the CUDA-core stencil path, 1 for the tcgen05 tensor-core path.
  * pass: 0 fwd, 1 bwd_data, 2 bwd_weight. */

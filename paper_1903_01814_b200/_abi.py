@@ -74,6 +74,8 @@ _SIGS = {
     "hex_conv2d_workspace_size": (_i32, [_CDP, _i32, _szp]),
     "hex_conv2d_algo": (_i32, [_CDP, _i32, _i32p]),
     "hex_conv2d_fwd": (_i32, [_CDP, _vp, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
+    "hex_conv2d_fwd_maxpool_supported": (_i32, [_CDP]),
+    "hex_conv2d_fwd_maxpool": (_i32, [_CDP, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp]),
     "hex_conv2d_bwd_data": (_i32, [_CDP, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "hex_conv2d_bwd_weight": (_i32, [_CDP, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
     "hex_pool2d_fwd": (_i32, [_PDP, _vp, _vp, _vp, _vp]),

@@ -208,6 +208,36 @@ hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* d, const void* x, const voi
     return direct_conv_fwd(a, s);
 }
 
+int32_t hex_conv2d_fwd_maxpool_supported(const hex_conv2d_desc_t* d) {
+    Geom g;
+    if (conv_geom(d, &g) != HEX_OK) return 0;
+    return use_tc_fwd(d, g) && tc_conv_maxpool_supported(g, d->in_channels, d->out_channels) ? 1 : 0;
+}
+
+hex_status_t hex_conv2d_fwd_maxpool(const hex_conv2d_desc_t* d, const void* x, const void* w, const float* bias,
+                                    int32_t fuse_relu, void* y_pool, uint8_t* argmax, void* ws, size_t ws_bytes,
+                                    hex_stream_t stream) {
+    Geom g;
+    hex_status_t st = conv_geom(d, &g);
+    if (st != HEX_OK) return st;
+    if (!x || !w || !y_pool || !argmax) return HEX_ERR_INVALID_ARG;
+    if (!use_tc_fwd(d, g) || !tc_conv_maxpool_supported(g, d->in_channels, d->out_channels))
+        return HEX_ERR_UNSUPPORTED;
+    if (!aligned16(x) || !aligned16(y_pool) || !aligned16(w) || ((uintptr_t)argmax & 7) ||
+        (bias && !aligned16(bias)))
+        return HEX_ERR_ALIGNMENT;
+    const size_t need = packed_weight_bytes(d, g);
+    if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    void* wp = align_up(ws, 1024);
+    st = tc_pack_weights(w, wp, d->out_channels, d->in_channels, g.T, 0, s);
+    if (st != HEX_OK) return st;
+    TcConvArgs a{};
+    a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
+    a.x = x; a.wpack = wp; a.bias = bias; a.y = nullptr; a.relu_y = nullptr; a.relu = fuse_relu;
+    return tc_conv_maxpool(a, y_pool, argmax, s);
+}
+
 hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* d, const void* dy, const void* w, const void* relu_y,
                                  void* dx, void* ws, size_t ws_bytes, hex_stream_t stream) {
     Geom g;

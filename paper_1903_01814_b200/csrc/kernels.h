@@ -59,6 +59,9 @@ struct TcConvArgs {
 bool tc_conv_supported(const Geom& g, int Cin, int Cout);
 bool tc_fwd_tr_supported(const Geom& g, int Cin, int Cout);  // tap-reuse forward (tc_fwd_tr.cu)
 hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st);
+// fused maxpool_{n=1,s=2}(relu(conv(x) + bias)) (tc_fwd_tr.cu); the conv output is not materialised
+bool tc_conv_maxpool_supported(const Geom& g, int Cin, int Cout);
+hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax, cudaStream_t st);
 hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st);
 hex_status_t tc_pack_weights(const void* w, void* wpack, int Cout, int Cin, int T, int transpose_reverse,
                              cudaStream_t st);

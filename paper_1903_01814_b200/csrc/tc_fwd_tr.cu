@@ -443,6 +443,240 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
     }
 }
 
+// ------------------------------------------------------------------ fused conv -> ReLU -> max pool
+// maxpool_{n=1,s=2}(relu(conv(x) + bias)) without writing the conv output.
+// A CTA owns a REGION of the conv-output grid: rows [r0, r0+16) with r0 = 14 i - 1, columns
+// [14k-1, 14k+15), computed as two 16 x 8 tap-reuse tiles -- view 0 sub-columns [7k, 7k+8) and
+// view 1 sub-columns [7k-1, 7k+7) -- into two TMEM accumulators.  It owns the pool windows whose
+// centre column is 2C with C in [7k, 7k+7) and whose centre row lies in [14i, 14i+14): exactly the
+// windows whose 7 taps (rows cr-1..cr+1, columns 2C-1..2C+1) lie inside the region.  Regions therefore overlap by 2 rows and one sub-column (~30 % more MMA work) instead of
+// exchanging halos.  The epilogue writes the region's ReLU'd bf16 conv outputs (one 64-channel chunk
+// at a time) to shared memory and reduces the owned windows from there: first strict maximum in
+// canonical tap order (A9), value = the bf16 conv output at that tap, bit-identical to the
+// unfused conv + pool.  The conv output itself never reaches HBM.
+constexpr int FP_REGION = 2 * 128 * 128;  // two views x 128 pixels x 64 channels bf16 (32 KB)
+
+struct FpParams {
+    int B, H, W, Cin, Cout, T, parity, Ho, Wo;
+    int nr, nc, regions, kchunks, stages, relu;
+    const float* bias;
+    uint16_t* y;   // pooled bf16 NHWC [B][Ho][Wo][Cout]
+    uint8_t* am;   // argmax tap [B][Ho][Wo][Cout]
+};
+
+template <int BN, int N>
+__global__ void __launch_bounds__(FT_THREADS, 1)
+tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
+                       const __grid_constant__ CUtensorMap map_w, const __grid_constant__ FpParams p) {
+    constexpr int TG = 2 * N + 1;
+    using SL = StageList<N, TG>;
+    constexpr int A_BYTES = (FT_RB + 2 * N) * FT_JB * 128;
+    constexpr int W_TILE = BN * 128;
+    constexpr int TMEM_COLS = 4 * BN;  // 2 slots x 2 views
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned
+    const int res_bytes = p.T * p.kchunks * W_TILE;
+    uint8_t* resw = base;
+    uint8_t* ring = base + res_bytes;
+    uint8_t* region = ring + p.stages * A_BYTES;
+    uint64_t* full = (uint64_t*)(region + FP_REGION);
+    uint64_t* empty = full + p.stages;
+    uint64_t* tfull = empty + p.stages;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* bres = tempty + 2;
+    uint32_t* tmem_slot = (uint32_t*)(bres + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], FT_EPI / 32);
+        }
+        ptx::mbar_init(bres, 1);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&map_x0);
+        ptx::prefetch_tmap(&map_x1);
+        ptx::prefetch_tmap(&map_w);
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            ptx::mbar_arrive_expect_tx(bres, (uint32_t)res_bytes);
+            for (int t = 0; t < p.T; ++t)
+                for (int kc = 0; kc < p.kchunks; ++kc)
+                    ptx::tma_load_4d(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0, 0, kc, t);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int reg = blockIdx.x; reg < p.regions; reg += gridDim.x) {
+                const int k = reg % p.nc, i = (reg / p.nc) % p.nr, b = reg / (p.nc * p.nr);
+                const int r0 = 14 * i - 1;
+                for (int v = 0; v < 2; ++v) {
+                    const int P = v, j0 = 7 * k - v;
+                    const int pc = (P + p.parity) & 1;
+                    for (int kc = 0; kc < p.kchunks; ++kc) {
+#pragma unroll 1
+                        for (int s = 0; s < SL::count(); ++s) {
+                            const int dc = SL::dc_of(s);
+                            const int Pv = (P + dc) & 1;
+                            const int jsh = (P + dc - Pv) / 2;
+                            const int top = -N + (((dc < 0 ? -dc : dc) + pc) >> 1);
+                            ptx::mbar_wait(&empty[stage], phase ^ 1);
+                            uint8_t* sa = ring + stage * A_BYTES;
+                            ptx::mbar_arrive_expect_tx(&full[stage], A_BYTES);
+                            ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top, b, kc);
+                            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint64_t a_ring = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
+            const uint64_t res_desc = ptx::smem_desc_sw128(ptx::smem_u32(resw), 16, 1024);
+            int stage = 0;
+            uint32_t phase = 0;
+            int slot = 0;
+            uint32_t sphase = 0;
+            ptx::mbar_wait(bres, 0);
+            for (int reg = blockIdx.x; reg < p.regions; reg += gridDim.x) {
+                ptx::mbar_wait(&tempty[slot], sphase ^ 1);
+                ptx::tc_fence_after();
+                for (int v = 0; v < 2; ++v) {
+                    const uint32_t d = tmem_base + (slot * 2 + v) * BN;
+                    for (int kc = 0; kc < p.kchunks; ++kc)
+                        issue_stages_from<BN, N, TG, true, false, 0>(d, a_ring, a_ring, res_desc, full, empty, stage,
+                                                                     phase, p.stages, A_BYTES >> 4, A_BYTES >> 4, kc,
+                                                                     p.kchunks, kc == 0 ? 0u : 1u);
+                }
+                ptx::mma_commit(&tfull[slot]);
+                slot ^= 1;
+                if (slot == 0) sphase ^= 1;
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
+        const int row = q * 32 + lane;  // tile pixel m = 8 * (region row) + sub-column
+        const int et = threadIdx.x - 64;
+        const int pcen = p.parity & 1;  // centre column parity of every window (centres in even columns)
+        const int top1 = -1 + ((1 + pcen) >> 1);  // first row offset of the dc = +-1 taps
+        int slot = 0;
+        uint32_t sphase = 0;
+        for (int reg = blockIdx.x; reg < p.regions; reg += gridDim.x) {
+            const int k = reg % p.nc, i = (reg / p.nc) % p.nr, b = reg / (p.nc * p.nr);
+            const int r0 = 14 * i - 1;
+            ptx::mbar_wait(&tfull[slot], sphase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 64; ++ch) {
+                ptx::named_bar(1, FT_EPI);  // previous chunk's window reads are done
+                // conv outputs of both views -> bias, ReLU, bf16 -> region buffer
+                // [view][pixel m][64 ch], 16-byte chunk i of row m at i ^ (m & 7) (conflict-free rows)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    uint32_t vals[32];
+                    ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (slot * 2 + v) * BN + ch * 64 + h * 32,
+                                   vals);
+                    ptx::tmem_ld_wait();
+                    uint8_t* rowp = region + v * (128 * 128) + row * 128;
+#pragma unroll
+                    for (int ii = 0; ii < 4; ++ii) {
+                        const int ci8 = 4 * h + ii;
+                        float f[8];
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) f[kk] = __uint_as_float(vals[8 * ii + kk]);
+                        if (p.bias) {
+                            const int c0 = ch * 64 + 8 * ci8;
+                            const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + c0));
+                            const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 4));
+                            f[0] += b0.x; f[1] += b0.y; f[2] += b0.z; f[3] += b0.w;
+                            f[4] += b1.x; f[5] += b1.y; f[6] += b1.z; f[7] += b1.w;
+                        }
+                        if (p.relu) {
+#pragma unroll
+                            for (int kk = 0; kk < 8; ++kk) f[kk] = fmaxf(f[kk], 0.f);
+                        }
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            __nv_bfloat162 hv = __floats2bfloat162_rn(f[2 * kk], f[2 * kk + 1]);
+                            pk[kk] = *reinterpret_cast<uint32_t*>(&hv);
+                        }
+                        *reinterpret_cast<uint4*>(rowp + ((ci8 ^ (row & 7)) << 4)) =
+                            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    }
+                }
+                if (ch + 1 == BN / 64) {  // TMEM of this slot fully read: the MMA may refill it
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty[slot]);
+                }
+                ptx::named_bar(1, FT_EPI);
+                // owned windows: 7 centre columns x 7 centre rows, 8 channels per thread
+                for (int w = et; w < 49 * 8; w += FT_EPI) {
+                    const int wi = w >> 3, cg = w & 7;
+                    const int wc = wi % 7, wr = wi / 7;
+                    const int C = 7 * k + wc;
+                    if (C >= p.Wo) continue;
+                    const int rho = C & 1;  // rho(C) = floor((2C + parity) / 2) mod 2
+                    const int R = 7 * i + wr;  // owned centre rows 2R + rho in [14 i, 14 i + 14)
+                    const int cr = 2 * R + rho;
+                    if (R >= p.Ho) continue;
+                    uint32_t best[4] = {0u, 0u, 0u, 0u}, ix[4] = {0u, 0u, 0u, 0u};
+                    bool any = false;
+#pragma unroll
+                    for (int t = 0; t < 7; ++t) {
+                        // canonical taps: 0,1 column 2C-1 (view 1, local sub-column wc); 2,3,4 column 2C
+                        // (view 0, wc); 5,6 column 2C+1 (view 1, wc + 1)
+                        const int v = (t < 2 || t > 4) ? 1 : 0;
+                        const int col = t < 2 ? 2 * C - 1 : (t > 4 ? 2 * C + 1 : 2 * C);
+                        const int sc = t > 4 ? wc + 1 : wc;
+                        const int rr = t < 2 ? cr + top1 + t : (t > 4 ? cr + top1 + (t - 5) : cr - 1 + (t - 2));
+                        if (col < 0 || col >= p.W || rr < 0 || rr >= p.H) continue;
+                        const int m = (rr - r0) * 8 + sc;
+                        const uint4 q4 = *reinterpret_cast<const uint4*>(region + v * (128 * 128) + m * 128 +
+                                                                          ((cg ^ (m & 7)) << 4));
+                        const uint32_t wv[4] = {q4.x, q4.y, q4.z, q4.w};
+                        const uint32_t tt = (uint32_t)t * 0x0101u;
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            if (!any) {
+                                best[kk] = wv[kk];
+                                ix[kk] = tt;
+                            } else {
+                                const unsigned mk = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&wv[kk]),
+                                                                *reinterpret_cast<const __nv_bfloat162*>(&best[kk]));
+                                best[kk] = (wv[kk] & mk) | (best[kk] & ~mk);
+                                const uint32_t bm = __byte_perm(mk, 0u, 0x4420);
+                                ix[kk] = (tt & bm) | (ix[kk] & ~bm);
+                            }
+                        }
+                        any = true;
+                    }
+                    const int64_t o = (((int64_t)b * p.Ho + R) * p.Wo + C) * p.Cout + ch * 64 + cg * 8;
+                    *reinterpret_cast<uint4*>(p.y + o) = make_uint4(best[0], best[1], best[2], best[3]);
+                    *reinterpret_cast<uint2*>(p.am + o) = make_uint2(ix[0] | (ix[1] << 16), ix[2] | (ix[3] << 16));
+                }
+            }
+            slot ^= 1;
+            if (slot == 0) sphase ^= 1;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 ft_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -651,6 +885,68 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
                                       : launch_ft<128, 2, false, true>(maps, p, pl.smem, st);
     return g.n == 1 ? launch_ft<64, 1, false, true>(maps, p, pl.smem, st)
                     : launch_ft<64, 2, false, true>(maps, p, pl.smem, st);
+}
+
+// ------------------------------------------------------------------ fused conv + max pool host side
+namespace {
+struct FpPlan {
+    int stages, smem, nr, nc, Ho, Wo;
+    bool ok;
+};
+FpPlan fp_plan(const Geom& g, int Cin, int Cout) {
+    FpPlan pl{};
+    if (g.s != 1 || (g.n != 1 && g.n != 2) || Cin % 64 || (Cout != 64 && Cout != 128) || g.W < 2) return pl;
+    int po;
+    if (!out_shape(g.H, g.W, 2, g.parity, &pl.Ho, &pl.Wo, &po)) return pl;
+    const int A = (FT_RB + 2 * g.n) * FT_JB * 128;
+    const int res_bytes = g.T * (Cin / 64) * Cout * 128;
+    const int fixed = FP_REGION + 1024 + 512;
+    pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
+    if (pl.stages > 8) pl.stages = 8;
+    if (pl.stages < 3) return pl;
+    pl.smem = res_bytes + pl.stages * A + fixed;
+    const int cr_max = 2 * (pl.Ho - 1) + 1;
+    pl.nr = (cr_max + 1 + 13) / 14;
+    pl.nc = (pl.Wo + 6) / 7;
+    pl.ok = true;
+    return pl;
+}
+}  // namespace
+
+bool tc_conv_maxpool_supported(const Geom& g, int Cin, int Cout) {
+    if (getenv("HEXCONV_NO_FUSED_POOL") || !ft_encode()) return false;
+    return fp_plan(g, Cin, Cout).ok;
+}
+
+hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax, cudaStream_t st) {
+    const Geom& g = a.g;
+    const FpPlan pl = fp_plan(g, a.Cin, a.Cout);
+    if (!pl.ok) return HEX_ERR_UNSUPPORTED;
+    FpParams p{};
+    p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
+    p.Ho = pl.Ho; p.Wo = pl.Wo; p.nr = pl.nr; p.nc = pl.nc; p.regions = g.B * pl.nr * pl.nc;
+    p.kchunks = a.Cin / 64; p.stages = pl.stages; p.relu = a.relu; p.bias = a.bias;
+    p.y = (uint16_t*)y_pool; p.am = argmax;
+    CUtensorMap mx0, mx1, mw;
+    if (!ft_view5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, FT_RB + 2 * g.n)) return HEX_ERR_CUDA;
+    if (!ft_view5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, FT_RB + 2 * g.n)) return HEX_ERR_CUDA;
+    if (!ft_wmap(&mw, a.wpack, g.T, a.Cout, a.Cin, a.Cout)) return HEX_ERR_CUDA;
+    const int grid = p.regions < num_sms() ? p.regions : num_sms();
+#define HEX_FP(BN_, N_)                                                                                       \
+    {                                                                                                         \
+        auto kern = tc_conv_maxpool_kernel<BN_, N_>;                                                          \
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem) != cudaSuccess) \
+            return HEX_ERR_CUDA;                                                                              \
+        kern<<<grid, FT_THREADS, pl.smem, st>>>(mx0, mx1, mw, p);                                             \
+    }
+    if (a.Cout == 128) {
+        if (g.n == 1) HEX_FP(128, 1) else HEX_FP(128, 2)
+    } else {
+        if (g.n == 1) HEX_FP(64, 1) else HEX_FP(64, 2)
+    }
+#undef HEX_FP
+    count_launch();
+    return last_launch_status();
 }
 
 }  // namespace hexconv

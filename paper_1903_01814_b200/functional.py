@@ -105,6 +105,28 @@ def conv2d_fwd(x, w, bias=None, n: int = 1, stride: int = 1, parity: int = 0, re
     return out
 
 
+def conv2d_fwd_maxpool(x, w, bias=None, n: int = 1, parity: int = 0, relu: bool = True, layout: str = "NHWC"):
+    """(y, argmax) = hex max pool (n = 1, stride 2) of relu?(hexconv(x, w) + bias), fused: the conv
+    output is never materialised (bf16 NHWC, stride 1).  Bit-identical to conv2d_fwd followed by
+    pool2d_fwd; raises HexError(HEX_ERR_UNSUPPORTED) where no fused kernel applies."""
+    _check_cuda(x, w, bias)
+    B, Cin, H, W = _dims(x, layout)
+    Cout = w.shape[0]
+    d = conv_desc(B, Cin, Cout, H, W, n, 1, parity, x.dtype, layout)
+    Ho, Wo, _ = A.output_shape(H, W, 2, parity)
+    y = torch.empty(_shape(layout, B, Cout, Ho, Wo), dtype=x.dtype, device=x.device)
+    am = torch.empty(_shape(layout, B, Cout, Ho, Wo), dtype=torch.uint8, device=x.device)
+    ws, nb = _workspace(d, 0, x.device)
+    A.check(A.lib().hex_conv2d_fwd_maxpool(ctypes.byref(d), _ptr(x), _ptr(w), _ptr(bias), int(relu), _ptr(y),
+                                           _ptr(am), _ptr(ws), nb, _stream()), "hex_conv2d_fwd_maxpool")
+    return y, am
+
+
+def conv2d_fwd_maxpool_supported(B, Cin, Cout, H, W, n, parity=0, dtype=torch.bfloat16, layout="NHWC") -> bool:
+    d = conv_desc(B, Cin, Cout, H, W, n, 1, parity, dtype, layout)
+    return bool(A.lib().hex_conv2d_fwd_maxpool_supported(ctypes.byref(d)))
+
+
 def conv2d_bwd_data(dy, w, in_hw, n: int = 1, stride: int = 1, parity: int = 0, layout: str = "NCHW",
                     relu_y=None, out=None):
     """dx = adjoint of conv2d_fwd applied to dy; optionally masked by relu_y > 0."""

@@ -136,6 +136,7 @@ class HexCNN:
 
     def _alloc(self):
         B, dev, bf = self.B, self.dev, torch.bfloat16
+        L_ = A.lib()
         self.act = []       # conv outputs (post-ReLU), NHWC
         self.pooled = {}    # pool outputs
         self.argmax = {}
@@ -162,6 +163,11 @@ class HexCNN:
                 self.pooled[l] = torch.empty(B, ho, wo, co, dtype=bf, device=dev)
                 self.argmax[l] = torch.empty(B, ho, wo, co, dtype=torch.uint8, device=dev)
                 self.dpool[l] = torch.empty(B, ho, wo, co, dtype=bf, device=dev)
+        import os
+        # fused conv + ReLU + max pool (hex_conv2d_fwd_maxpool): measured no faster than the two calls on
+        # C5 layer 2 (its halo recompute costs ~36 % more MMA work), so opt-in via HEXCNN_FUSED_POOL=1
+        self.fused_pool = {l: bool(L_.hex_conv2d_fwd_maxpool_supported(ctypes.byref(self.desc[l])))
+                           and bool(os.environ.get("HEXCNN_FUSED_POOL")) for l in self.pool_geo}
         self.pdesc = {l: A.PoolDesc(B, self.channels[l + 1], *self.pool_geo[l][:2], 1, 2, 0, _BF16, _NHWC,
                                     A.POOL_MAX) for l in self.pool_geo}
         C = self.channels[-1]
@@ -195,6 +201,15 @@ class HexCNN:
         for l in range(self.L):
             xin = self.layer_input(l, x)
             ws = self.ws[l][0]
+            if l in self.pool_geo and self.fused_pool[l]:
+                # conv -> ReLU -> max pool in one kernel: act[l] is never written (the backward needs
+                # only the pooled tensor and the argmax, see backward())
+                e0 = self._tic()
+                A.check(L.hex_conv2d_fwd_maxpool(ctypes.byref(self.desc[l]), _p(xin), _p(self.weight(l)),
+                                                 _p(self.bias(l)), 1, _p(self.pooled[l]), _p(self.argmax[l]),
+                                                 _p(ws), self.ws_sizes[l][0], stream), f"conv{l + 1} fwd+pool")
+                self._toc("fwd_pool", l, e0)
+                continue
             e0 = self._tic()
             A.check(L.hex_conv2d_fwd(ctypes.byref(self.desc[l]), _p(xin), _p(self.weight(l)), _p(self.bias(l)), 1,
                                      _p(self.act[l]), _p(ws), self.ws_sizes[l][0], stream), f"conv{l + 1} fwd")

@@ -118,3 +118,42 @@ def test_tc_tap_reuse_wgrad_channel_tiles(F, oracle):
     # CTA-pair forward with an odd number of 128-pixel tiles (the last pair's second tile is empty)
     case(F, oracle, 1, 128, 128, 16, 17, 1, 0, 9)
     case(F, oracle, 1, 256, 256, 16, 17, 2, 1, 10)
+
+
+@pytest.mark.parametrize("n", [1])
+@pytest.mark.parametrize("pi", [0, 1])
+def test_fused_conv_relu_maxpool(F, oracle, n, pi):
+    # hex_conv2d_fwd_maxpool: bit-identical to the unfused conv + ReLU + pool, and the
+    # pool of the GPU's own conv output matches the oracle pool bit-exactly (values and argmax taps)
+    import synth
+    # shapes on which the unfused forward also runs the tap-reuse kernel (same fp32 summation order)
+    for (B, Cin, Cout, H, W) in [(2, 64, 128, 30, 31), (1, 128, 64, 32, 32), (3, 64, 64, 16, 16)]:
+        T = oracle.num_taps(n)
+        x = synth.round_bf16(synth.normal((B, Cin, H, W), 70 + H))
+        w = synth.round_bf16(synth.normal((Cout, Cin, T), 71 + H, 1.0 / np.sqrt(Cin * T)))
+        b = synth.round_f32(synth.normal((Cout,), 72 + H, 0.2))
+        xd = nhwc(x)
+        wd = torch.from_numpy(w.astype(np.float32)).to(torch.bfloat16).cuda()
+        bd = torch.from_numpy(b.astype(np.float32)).cuda()
+        assert F.conv2d_fwd_maxpool_supported(B, Cin, Cout, H, W, n, pi)
+        yp, am = F.conv2d_fwd_maxpool(xd, wd, bd, n=n, parity=pi)
+        yc = F.conv2d_fwd(xd, wd, bd, n=n, parity=pi, relu=True, layout="NHWC")
+        yp2, am2 = F.pool2d_fwd(yc, 1, 2, pi, "max", "NHWC")
+        torch.cuda.synchronize()
+        assert torch.equal(yp.view(torch.int16), yp2.view(torch.int16)), (n, pi, H, W)
+        assert torch.equal(am, am2), (n, pi, H, W)
+        pr, amr = oracle.pool2d_fwd(back(yc), n=1, s=2, pi=pi, mode="max")
+        assert np.array_equal(back(yp), pr)
+        assert np.array_equal(am.permute(0, 3, 1, 2).cpu().numpy(), amr)
+
+
+def test_fused_conv_maxpool_unsupported_shape(F):
+    # n = 2 weights do not stay resident next to the fused kernel's buffers: the call reports
+    # HEX_ERR_UNSUPPORTED (8) and the caller runs conv + pool separately
+    from paper_1903_01814_b200._abi import HexError
+    assert not F.conv2d_fwd_maxpool_supported(2, 64, 128, 30, 31, 2, 0)
+    x = torch.zeros(2, 30, 31, 64, device="cuda", dtype=torch.bfloat16)
+    w = torch.zeros(128, 64, 19, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(HexError) as e:
+        F.conv2d_fwd_maxpool(x, w, None, n=2)
+    assert e.value.status == 8

@@ -26,6 +26,8 @@ def main():
             F.conv2d_bwd_data(g, w, (H, W), n=n, layout="NHWC")
         elif op == "wgrad":
             F.conv2d_bwd_weight(x, g, n=n, layout="NHWC")
+        elif op == "convpool":
+            F.conv2d_fwd_maxpool(x, w, None, n=n)
         elif op == "poolf":
             F.pool2d_fwd(x, 1, 2, 0, "max", "NHWC")
         elif op == "l1fwd":

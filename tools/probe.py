@@ -102,6 +102,16 @@ def conv_layer(B, Ci, Co, H, W, n, dtype=torch.bfloat16, layout="NHWC", label=""
     return res
 
 
+def fused_layer(B, Ci, Co, H, W, n, label=""):
+    x = torch.randn(B, H, W, Ci, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(Co, Ci, F.num_taps(n), device="cuda") / (Ci * F.num_taps(n)) ** 0.5).to(torch.bfloat16)
+    if not F.conv2d_fwd_maxpool_supported(B, Ci, Co, H, W, n):
+        return
+    ms = timeit(lambda: F.conv2d_fwd_maxpool(x, w, None, n=n))
+    flops = 2.0 * B * valid_taps(H, W, n) * Ci * Co
+    print(f"{label:10s} fused conv+relu+maxpool {ms*1e3:9.1f} us  {flops / ms / 1e9:8.1f} TFLOP/s (conv FLOPs)")
+
+
 def pool_layer(B, C, H, W, n, s, mode, dtype=torch.bfloat16, layout="NHWC", label=""):
     x = torch.randn(B, H, W, C, device="cuda").to(dtype) if layout == "NHWC" else \
         torch.randn(B, C, H, W, device="cuda").to(dtype)
@@ -128,6 +138,7 @@ def main():
         conv_layer(256, 1, 64, 96, 96, 2, label="C5 L1")
         conv_layer(256, 64, 128, 96, 96, 1, label="C5 L2")
         pool_layer(256, 128, 96, 96, 1, 2, "max", label="C5 P1")
+        fused_layer(256, 64, 128, 96, 96, 1, label="C5 L2+P1")
         conv_layer(256, 128, 128, 48, 48, 2, label="C5 L3")
         conv_layer(256, 128, 256, 48, 48, 1, label="C5 L4")
         pool_layer(256, 256, 48, 48, 1, 2, "max", label="C5 P2")
