@@ -571,7 +571,14 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
         uint32_t sphase = 0;
         for (int reg = blockIdx.x; reg < p.regions; reg += gridDim.x) {
             const int k = reg % p.nc, i = (reg / p.nc) % p.nr, b = reg / (p.nc * p.nr);
-            const int r0 = 14 * i - 1;
+            // this thread's pixel (local row row/8, sub-column row%8) in both views: pixels outside the
+            // image hold -inf in the region buffer, so windows need no per-tap bounds test (a window's
+            // centre is always inside, and the first strict maximum never selects an out-of-image tap)
+            const int img_r = 14 * i - 1 + (row >> 3);
+            const bool rin = img_r >= 0 && img_r < p.H;
+            const int j0v = 7 * k + (row & 7);  // view-0 sub-column; view 1 is one to the left
+            const bool out0 = !rin || 2 * j0v >= p.W;
+            const bool out1 = !rin || j0v == 0 || 2 * (j0v - 1) + 1 >= p.W;
             ptx::mbar_wait(&tfull[slot], sphase);
             ptx::tc_fence_after();
 #pragma unroll 1
@@ -585,6 +592,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
                     ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (slot * 2 + v) * BN + ch * 64 + h * 32,
                                    vals);
                     ptx::tmem_ld_wait();
+                    const bool outside = v ? out1 : out0;
                     uint8_t* rowp = region + v * (128 * 128) + row * 128;
 #pragma unroll
                     for (int ii = 0; ii < 4; ++ii) {
@@ -607,7 +615,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             __nv_bfloat162 hv = __floats2bfloat162_rn(f[2 * kk], f[2 * kk + 1]);
-                            pk[kk] = *reinterpret_cast<uint32_t*>(&hv);
+                            pk[kk] = outside ? 0xFF80FF80u : *reinterpret_cast<uint32_t*>(&hv);
                         }
                         *reinterpret_cast<uint4*>(rowp + ((ci8 ^ (row & 7)) << 4)) =
                             make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -624,45 +632,48 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
                     const int wi = w >> 3, cg = w & 7;
                     const int wc = wi % 7, wr = wi / 7;
                     const int C = 7 * k + wc;
-                    if (C >= p.Wo) continue;
-                    const int rho = C & 1;  // rho(C) = floor((2C + parity) / 2) mod 2
                     const int R = 7 * i + wr;  // owned centre rows 2R + rho in [14 i, 14 i + 14)
-                    const int cr = 2 * R + rho;
-                    if (R >= p.Ho) continue;
-                    uint32_t best[4] = {0u, 0u, 0u, 0u}, ix[4] = {0u, 0u, 0u, 0u};
-                    bool any = false;
+                    if (C >= p.Wo || R >= p.Ho) continue;
+                    // local centre row cr - r0 with cr = 2R + rho(C), rho(C) = C mod 2, r0 = 14 i - 1
+                    const int lr = 2 * wr + (C & 1) + 1;
+                    // canonical taps: 0,1 column 2C-1 (view 1, local sub-column wc); 2,3,4 column 2C
+                    // (view 0, wc); 5,6 column 2C+1 (view 1, wc + 1).  Row stride 1024 B; the swizzle
+                    // chunk depends only on the sub-column.
+                    const uint8_t* pl = region + 16384 + (lr + top1) * 1024 + wc * 128 + ((cg ^ wc) << 4);
+                    const uint8_t* pc = region + lr * 1024 + wc * 128 + ((cg ^ wc) << 4);
+                    const uint8_t* pr = region + 16384 + (lr + top1) * 1024 + (wc + 1) * 128 + ((cg ^ (wc + 1)) << 4);
+                    uint4 tv[7];
+                    tv[0] = *reinterpret_cast<const uint4*>(pl);
+                    tv[1] = *reinterpret_cast<const uint4*>(pl + 1024);
+                    tv[2] = *reinterpret_cast<const uint4*>(pc - 1024);
+                    tv[3] = *reinterpret_cast<const uint4*>(pc);
+                    tv[4] = *reinterpret_cast<const uint4*>(pc + 1024);
+                    tv[5] = *reinterpret_cast<const uint4*>(pr);
+                    tv[6] = *reinterpret_cast<const uint4*>(pr + 1024);
+                    uint32_t best[4], ix[4];
 #pragma unroll
-                    for (int t = 0; t < 7; ++t) {
-                        // canonical taps: 0,1 column 2C-1 (view 1, local sub-column wc); 2,3,4 column 2C
-                        // (view 0, wc); 5,6 column 2C+1 (view 1, wc + 1)
-                        const int v = (t < 2 || t > 4) ? 1 : 0;
-                        const int col = t < 2 ? 2 * C - 1 : (t > 4 ? 2 * C + 1 : 2 * C);
-                        const int sc = t > 4 ? wc + 1 : wc;
-                        const int rr = t < 2 ? cr + top1 + t : (t > 4 ? cr + top1 + (t - 5) : cr - 1 + (t - 2));
-                        if (col < 0 || col >= p.W || rr < 0 || rr >= p.H) continue;
-                        const int m = (rr - r0) * 8 + sc;
-                        const uint4 q4 = *reinterpret_cast<const uint4*>(region + v * (128 * 128) + m * 128 +
-                                                                          ((cg ^ (m & 7)) << 4));
-                        const uint32_t wv[4] = {q4.x, q4.y, q4.z, q4.w};
-                        const uint32_t tt = (uint32_t)t * 0x0101u;
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&tv[0]);
+                        __nv_bfloat162 mx = *reinterpret_cast<const __nv_bfloat162*>(w0 + kk);
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            if (!any) {
-                                best[kk] = wv[kk];
-                                ix[kk] = tt;
-                            } else {
-                                const unsigned mk = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&wv[kk]),
-                                                                *reinterpret_cast<const __nv_bfloat162*>(&best[kk]));
-                                best[kk] = (wv[kk] & mk) | (best[kk] & ~mk);
-                                const uint32_t bm = __byte_perm(mk, 0u, 0x4420);
-                                ix[kk] = (tt & bm) | (ix[kk] & ~bm);
-                            }
+                        for (int t = 1; t < 7; ++t)
+                            mx = __hmax2(mx, *reinterpret_cast<const __nv_bfloat162*>(
+                                                 reinterpret_cast<const uint32_t*>(&tv[t]) + kk));
+                        // first tap equal to the maximum == first strict maximum in canonical order
+                        best[kk] = reinterpret_cast<const uint32_t*>(&tv[6])[kk];
+                        ix[kk] = 6u * 0x00010001u;
+#pragma unroll
+                        for (int t = 5; t >= 0; --t) {
+                            const uint32_t wv = reinterpret_cast<const uint32_t*>(&tv[t])[kk];
+                            const uint32_t mk = __heq2_mask(*reinterpret_cast<const __nv_bfloat162*>(&wv), mx);
+                            best[kk] = (wv & mk) | (best[kk] & ~mk);
+                            ix[kk] = ((uint32_t)t * 0x00010001u & mk) | (ix[kk] & ~mk);
                         }
-                        any = true;
                     }
                     const int64_t o = (((int64_t)b * p.Ho + R) * p.Wo + C) * p.Cout + ch * 64 + cg * 8;
                     *reinterpret_cast<uint4*>(p.y + o) = make_uint4(best[0], best[1], best[2], best[3]);
-                    *reinterpret_cast<uint2*>(p.am + o) = make_uint2(ix[0] | (ix[1] << 16), ix[2] | (ix[3] << 16));
+                    *reinterpret_cast<uint2*>(p.am + o) =
+                        make_uint2(__byte_perm(ix[0], ix[1], 0x6420), __byte_perm(ix[2], ix[3], 0x6420));
                 }
             }
             slot ^= 1;

@@ -164,10 +164,10 @@ class HexCNN:
                 self.argmax[l] = torch.empty(B, ho, wo, co, dtype=torch.uint8, device=dev)
                 self.dpool[l] = torch.empty(B, ho, wo, co, dtype=bf, device=dev)
         import os
-        # fused conv + ReLU + max pool (hex_conv2d_fwd_maxpool): measured no faster than the two calls on
-        # C5 layer 2 (its halo recompute costs ~36 % more MMA work), so opt-in via HEXCNN_FUSED_POOL=1
+        # fused conv + ReLU + max pool (hex_conv2d_fwd_maxpool) where supported; HEXCNN_NO_FUSED_POOL=1
+        # restores the separate conv and pool calls
         self.fused_pool = {l: bool(L_.hex_conv2d_fwd_maxpool_supported(ctypes.byref(self.desc[l])))
-                           and bool(os.environ.get("HEXCNN_FUSED_POOL")) for l in self.pool_geo}
+                           and not os.environ.get("HEXCNN_NO_FUSED_POOL") for l in self.pool_geo}
         self.pdesc = {l: A.PoolDesc(B, self.channels[l + 1], *self.pool_geo[l][:2], 1, 2, 0, _BF16, _NHWC,
                                     A.POOL_MAX) for l in self.pool_geo}
         C = self.channels[-1]
