@@ -375,6 +375,11 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                         f[0] += b0.x; f[1] += b0.y; f[2] += b0.z; f[3] += b0.w;
                         f[4] += b1.x; f[5] += b1.y; f[6] += b1.z; f[7] += b1.w;
                     }
+                    if (p.relu && !p.has_mask) {  // ReLU inside the conversion (bit-identical to fmaxf + cvt)
+                        *slot = make_uint4(ptx::pack_bf16x2_relu(f[0], f[1]), ptx::pack_bf16x2_relu(f[2], f[3]),
+                                           ptx::pack_bf16x2_relu(f[4], f[5]), ptx::pack_bf16x2_relu(f[6], f[7]));
+                        continue;
+                    }
                     if (p.relu) {
 #pragma unroll
                         for (int k = 0; k < 8; ++k) f[k] = fmaxf(f[k], 0.f);
@@ -445,41 +450,136 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
 
 // ------------------------------------------------------------------ fused conv -> ReLU -> max pool
 // maxpool_{n=1,s=2}(relu(conv(x) + bias)) without writing the conv output.
-// A CTA owns a REGION of the conv-output grid: rows [r0, r0+16) with r0 = 14 i - 1, columns
-// [14k-1, 14k+15), computed as two 16 x 8 tap-reuse tiles -- view 0 sub-columns [7k, 7k+8) and
-// view 1 sub-columns [7k-1, 7k+7) -- into two TMEM accumulators.  It owns the pool windows whose
-// centre column is 2C with C in [7k, 7k+7) and whose centre row lies in [14i, 14i+14): exactly the
-// windows whose 7 taps (rows cr-1..cr+1, columns 2C-1..2C+1) lie inside the region.  Regions therefore overlap by 2 rows and one sub-column (~30 % more MMA work) instead of
-// exchanging halos.  The epilogue writes the region's ReLU'd bf16 conv outputs (one 64-channel chunk
-// at a time) to shared memory and reduces the owned windows from there: first strict maximum in
-// canonical tap order (A9), value = the bf16 conv output at that tap, bit-identical to the
-// unfused conv + pool.  The conv output itself never reaches HBM.
-constexpr int FP_REGION = 2 * 128 * 128;  // two views x 128 pixels x 64 channels bf16 (32 KB)
+// Column geometry: window centre column 2C is view-0 sub-column C; its side columns 2C -+ 1 are view-1
+// sub-columns C-1 and C.  A column STRIP k computes view-0 sub-columns [7k, 7k+8) and view-1 sub-columns
+// [7k-1, 7k+7) (two 16 x 8 tap-reuse tiles, two TMEM accumulators) and owns window columns [7k, 7k+7).
+// Rows: a strip walks down the image in tiles of 16 conv rows (r0 = 16 t) and carries the last two rows
+// of each tile (bf16) in shared memory, so tile t owns the windows with centre row cr in [r0-1, r0+14]
+// (+ r0+15 on the last tile) and no row is computed twice.  Strips are dealt round-robin to the
+// persistent CTAs in whole rounds; the strips left over after the last whole round are cut into
+// independent REGIONS (r0 = 14 i - 1, centre rows [14 i, 14 i + 14), halo rows recomputed) so the tail
+// spreads over all CTAs.
+// Epilogue, warp-specialised per 32-channel chunk: 8 CONVERTER warps (one per TMEM lane quadrant and
+// view) drain the accumulators (bias, ReLU, bf16; pixels outside the image become -inf) into one of two
+// region buffers (rows r0-2 .. r0+16), 8 WINDOW warps reduce the owned windows from the other buffer:
+// first maximum in canonical tap order (A9), value = the bf16 conv output of that tap --
+// bit-identical to the unfused conv + pool.  Named barriers FULL/EMPTY per buffer.  The conv output
+// never reaches HBM.
+constexpr int FP_ROWS = FT_RB + 3;               // region rows: 2 carried + 16 tile + 1 (-inf)
+constexpr int FP_PIX = 64;                       // bytes per pixel per chunk (32 channels bf16)
+constexpr int FP_VIEW = FP_ROWS * FT_JB * FP_PIX;  // one view of one chunk (9.5 KB)
+constexpr int FP_BUF = 2 * FP_VIEW;                // both views
+constexpr int FP_CARRY = 2 * 2 * FT_JB * FP_PIX;   // carried rows of one chunk: 2 views x 2 rows (2 KB)
+constexpr int FP_EPI = 512;                      // 8 converter + 8 window warps
+constexpr int FP_THREADS = 64 + FP_EPI;
+constexpr int FP_BAR_FULL = 2, FP_BAR_EMPTY = 4;  // named barrier ids (+ buffer index)
+
+// byte offset of 16-byte channel group i (0..3) of pixel (region row r, sub-column sc): conflict-free
+// for 8 consecutive pixels of one group and for 2 adjacent sub-columns x 4 groups
+__device__ __forceinline__ int fp_off(int r, int sc, int i) {
+    return r * (FT_JB * FP_PIX) + sc * FP_PIX + ((i ^ ((sc >> 1) & 3)) << 4);
+}
 
 struct FpParams {
     int B, H, W, Cin, Cout, T, parity, Ho, Wo;
-    int nr, nc, regions, kchunks, stages, relu;
+    int nr, nc, kchunks, stages, relu;
+    int ntr;           // tiles per strip = ceil(H / 16)
+    int full_rounds;   // strips per CTA in strip mode
+    int left_regions;  // regions cut from the strips after full_rounds * gridDim.x
+    int debug;         // HEXCONV_FP_DEBUG: 1 = no epilogue work, 2 = no MMAs (timing experiments)
     const float* bias;
     uint16_t* y;   // pooled bf16 NHWC [B][Ho][Wo][Cout]
     uint8_t* am;   // argmax tap [B][Ho][Wo][Cout]
 };
 
+struct FpTile {
+    int b, k, r0;
+    bool strip, first, last;
+};
+
+// the seq-th tile of this CTA; false past the end
+__device__ __forceinline__ bool fp_tile(const FpParams& p, int seq, FpTile& tl) {
+    const int ns = p.full_rounds * p.ntr;
+    if (seq < ns) {
+        const int j = seq / p.ntr, t = seq - j * p.ntr;
+        const int strip = blockIdx.x + j * gridDim.x;
+        tl.b = strip / p.nc;
+        tl.k = strip - tl.b * p.nc;
+        tl.r0 = FT_RB * t;
+        tl.strip = true;
+        tl.first = t == 0;
+        tl.last = t == p.ntr - 1;
+        return true;
+    }
+    const int rg = blockIdx.x + (seq - ns) * gridDim.x;
+    if (rg >= p.left_regions) return false;
+    const int strip = p.full_rounds * gridDim.x + rg / p.nr;
+    const int i = rg % p.nr;
+    tl.b = strip / p.nc;
+    tl.k = strip - tl.b * p.nc;
+    tl.r0 = 14 * i - 1;
+    tl.strip = tl.first = tl.last = false;
+    return true;
+}
+
+// n = 1 MMA sequence of one tile pair (view-0 tile -> accumulator d0, view-1 tile -> d1) from four
+// 19-row boxes (top row r0 - 1) that each serve every column group reading them, in an order that keeps
+// both accumulators in the canonical column order dc = -1, 0, +1 (same fp32 summation as the unfused
+// forward):
+//   box 0 = view 0 at sub-column 7k-1: view-1 dc = -1 (taps 0,1)
+//   box 1 = view 1 at 7k-1:            view-0 dc = -1 (taps 0,1) and view-1 dc = 0 (taps 2..4)
+//   box 2 = view 0 at 7k:              view-0 dc =  0 (taps 2..4) and view-1 dc = +1 (taps 5,6)
+//   box 3 = view 1 at 7k:              view-0 dc = +1 (taps 5,6)
+// A side column of view P starts pc_P = (P + parity) mod 2 rows below the box top.
+template <int BN>
+__device__ __forceinline__ void fp_issue_n1(uint32_t d0, uint32_t d1, uint64_t a_ring, uint64_t res_desc,
+                                            uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
+                                            int nstages, uint32_t stage16, int kc, int kchunks, uint32_t first,
+                                            uint32_t pc0) {
+    const uint64_t o0 = (uint64_t)(pc0 * 64), o1 = (uint64_t)((pc0 ^ 1u) * 64);  // 1024-byte rows
+    const int bs = kchunks * BN * 8;
+    const uint64_t w0 = res_desc + (uint64_t)(kc * (BN * 8));  // tap t at w0 + t * bs
+#pragma unroll
+    for (int bx = 0; bx < 4; ++bx) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint64_t ad = a_ring + (uint64_t)stage * stage16;
+        if (bx == 0) {
+            issue_stage<BN, 2, true>(d1, ad + o1, w0, bs, first);
+        } else if (bx == 1) {
+            issue_stage<BN, 2, true>(d0, ad + o0, w0, bs, first);
+            issue_stage<BN, 3, true>(d1, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
+        } else if (bx == 2) {
+            issue_stage<BN, 3, true>(d0, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
+            issue_stage<BN, 2, true>(d1, ad + o1, w0 + (uint64_t)(5 * bs), bs, 1u);
+        } else {
+            issue_stage<BN, 2, true>(d0, ad + o0, w0 + (uint64_t)(5 * bs), bs, 1u);
+        }
+        ptx::mma_commit(&empty[stage]);
+        if (++stage == nstages) { stage = 0; phase ^= 1; }
+    }
+}
+
 template <int BN, int N>
-__global__ void __launch_bounds__(FT_THREADS, 1)
+__global__ void __launch_bounds__(FP_THREADS, 1)
 tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                        const __grid_constant__ CUtensorMap map_w, const __grid_constant__ FpParams p) {
     constexpr int TG = 2 * N + 1;
     using SL = StageList<N, TG>;
-    constexpr int A_BYTES = (FT_RB + 2 * N) * FT_JB * 128;
+    constexpr int A_BYTES = (FT_RB + 2 * N + (N == 1 ? 1 : 0)) * FT_JB * 128;  // n = 1: shared 19-row boxes
     constexpr int W_TILE = BN * 128;
     constexpr int TMEM_COLS = 4 * BN;  // 2 slots x 2 views
+    constexpr int NCH = BN / 32;       // 32-channel chunks per tile
+    constexpr uint32_t NEG_INF2 = 0xFF80FF80u;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned
     const int res_bytes = p.T * p.kchunks * W_TILE;
     uint8_t* resw = base;
     uint8_t* ring = base + res_bytes;
-    uint8_t* region = ring + p.stages * A_BYTES;
-    uint64_t* full = (uint64_t*)(region + FP_REGION);
+    uint8_t* region = ring + p.stages * A_BYTES;  // [buffer][view][row][sub-column][64 B]
+    uint8_t* carry = region + 2 * FP_BUF;         // [chunk][view][2 rows][sub-column][64 B]
+    float* sbias = (float*)(carry + NCH * FP_CARRY);  // [BN]
+    uint64_t* full = (uint64_t*)(sbias + BN);
     uint64_t* empty = full + p.stages;
     uint64_t* tfull = empty + p.stages;
     uint64_t* tempty = tfull + 2;
@@ -491,7 +591,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
         for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], FT_EPI / 32);
+            ptx::mbar_init(&tempty[a], 8);  // the converter warps
         }
         ptx::mbar_init(bres, 1);
         ptx::fence_barrier_init();
@@ -500,6 +600,15 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
         ptx::prefetch_tmap(&map_w);
     }
     if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    if (threadIdx.x >= 64) {  // region row 18 (r0 + 16) is only read on a strip's last tile: below the image
+        const int e = threadIdx.x - 64;
+        if (p.bias && e < BN) sbias[e] = p.bias[e];
+        if (e < 2 * 2 * FT_JB * 4) {
+            const int bf = e >> 6, v = (e >> 5) & 1, sc = (e >> 2) & 7, c16 = e & 3;
+            *reinterpret_cast<uint4*>(region + bf * FP_BUF + v * FP_VIEW + fp_off(18, sc, c16)) =
+                make_uint4(NEG_INF2, NEG_INF2, NEG_INF2, NEG_INF2);
+        }
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -513,11 +622,23 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
                     ptx::tma_load_4d(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0, 0, kc, t);
             int stage = 0;
             uint32_t phase = 0;
-            for (int reg = blockIdx.x; reg < p.regions; reg += gridDim.x) {
-                const int k = reg % p.nc, i = (reg / p.nc) % p.nr, b = reg / (p.nc * p.nr);
-                const int r0 = 14 * i - 1;
+            FpTile tl;
+            for (int seq = 0; fp_tile(p, seq, tl); ++seq) {
+                if constexpr (N == 1) {
+                    for (int kc = 0; kc < p.kchunks; ++kc)
+#pragma unroll
+                        for (int bx = 0; bx < 4; ++bx) {
+                            ptx::mbar_wait(&empty[stage], phase ^ 1);
+                            uint8_t* sa = ring + stage * A_BYTES;
+                            ptx::mbar_arrive_expect_tx(&full[stage], A_BYTES);
+                            ptx::tma_load_5d((bx & 1) ? &map_x1 : &map_x0, &full[stage], sa, 0,
+                                             7 * tl.k - (bx < 2 ? 1 : 0), tl.r0 - 1, tl.b, kc);
+                            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                        }
+                    continue;
+                }
                 for (int v = 0; v < 2; ++v) {
-                    const int P = v, j0 = 7 * k - v;
+                    const int P = v, j0 = 7 * tl.k - v;
                     const int pc = (P + p.parity) & 1;
                     for (int kc = 0; kc < p.kchunks; ++kc) {
 #pragma unroll 1
@@ -529,7 +650,8 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
                             ptx::mbar_wait(&empty[stage], phase ^ 1);
                             uint8_t* sa = ring + stage * A_BYTES;
                             ptx::mbar_arrive_expect_tx(&full[stage], A_BYTES);
-                            ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top, b, kc);
+                            ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, tl.r0 + top,
+                                             tl.b, kc);
                             if (++stage == p.stages) { stage = 0; phase ^= 1; }
                         }
                     }
@@ -545,139 +667,202 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
             int slot = 0;
             uint32_t sphase = 0;
             ptx::mbar_wait(bres, 0);
-            for (int reg = blockIdx.x; reg < p.regions; reg += gridDim.x) {
+            FpTile tl;
+            for (int seq = 0; fp_tile(p, seq, tl); ++seq) {
                 ptx::mbar_wait(&tempty[slot], sphase ^ 1);
                 ptx::tc_fence_after();
-                for (int v = 0; v < 2; ++v) {
-                    const uint32_t d = tmem_base + (slot * 2 + v) * BN;
+                if (p.debug == 2) {
+                    for (int u = 0; u < (N == 1 ? 4 : 2 * SL::count()) * p.kchunks; ++u) {
+                        ptx::mbar_wait(&full[stage], phase);
+                        ptx::mbar_arrive(&empty[stage]);
+                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    }
+                    ptx::mbar_arrive(&tfull[slot]);
+                    slot ^= 1;
+                    if (slot == 0) sphase ^= 1;
+                    continue;
+                }
+                if constexpr (N == 1) {
                     for (int kc = 0; kc < p.kchunks; ++kc)
-                        issue_stages_from<BN, N, TG, true, false, 0>(d, a_ring, a_ring, res_desc, full, empty, stage,
-                                                                     phase, p.stages, A_BYTES >> 4, A_BYTES >> 4, kc,
-                                                                     p.kchunks, kc == 0 ? 0u : 1u);
+                        fp_issue_n1<BN>(tmem_base + (slot * 2) * BN, tmem_base + (slot * 2 + 1) * BN, a_ring, res_desc,
+                                        full, empty, stage, phase, p.stages, A_BYTES >> 4, kc, p.kchunks,
+                                        kc == 0 ? 0u : 1u, (uint32_t)(p.parity & 1));
+                } else {
+                    for (int v = 0; v < 2; ++v) {
+                        const uint32_t d = tmem_base + (slot * 2 + v) * BN;
+                        for (int kc = 0; kc < p.kchunks; ++kc)
+                            issue_stages_from<BN, N, TG, true, false, 0>(d, a_ring, a_ring, res_desc, full, empty,
+                                                                         stage, phase, p.stages, A_BYTES >> 4,
+                                                                         A_BYTES >> 4, kc, p.kchunks,
+                                                                         kc == 0 ? 0u : 1u);
+                    }
                 }
                 ptx::mma_commit(&tfull[slot]);
                 slot ^= 1;
                 if (slot == 0) sphase ^= 1;
             }
         }
-    } else {
+    } else if (warp < 10) {
+        // ---- converter warps: TMEM lane quadrant q (pixels 32 q .. 32 q + 31), view cv
         const int q = warp & 3;
-        const int h = (warp - 2) >> 2;
-        const int row = q * 32 + lane;  // tile pixel m = 8 * (region row) + sub-column
-        const int et = threadIdx.x - 64;
-        const int pcen = p.parity & 1;  // centre column parity of every window (centres in even columns)
-        const int top1 = -1 + ((1 + pcen) >> 1);  // first row offset of the dc = +-1 taps
+        const int cv = (warp - 2) >> 2;
+        const int row = q * 32 + lane;  // tile pixel m = 8 * (tile row) + sub-column
+        const int et = threadIdx.x - 64;  // 0..255
+        // carried 16-byte group of this thread (et < 128): view kv, carried row kr, sub-column ks, group ki
+        const int kv = (et >> 6) & 1, kr = (et >> 5) & 1, ks = (et >> 2) & 7, ki = et & 3;
+        const int koff = kv * FP_VIEW + fp_off(kr, ks, ki);
+        const int kcar = kv * 1024 + kr * 512 + ks * FP_PIX + ki * 16;
+        int soff[4];  // this pixel's 16-byte groups in a region buffer (region rows 2..17)
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) soff[ii] = cv * FP_VIEW + fp_off(2 + (row >> 3), row & 7, ii);
         int slot = 0;
         uint32_t sphase = 0;
-        for (int reg = blockIdx.x; reg < p.regions; reg += gridDim.x) {
-            const int k = reg % p.nc, i = (reg / p.nc) % p.nr, b = reg / (p.nc * p.nr);
-            // this thread's pixel (local row row/8, sub-column row%8) in both views: pixels outside the
-            // image hold -inf in the region buffer, so windows need no per-tap bounds test (a window's
-            // centre is always inside, and the first strict maximum never selects an out-of-image tap)
-            const int img_r = 14 * i - 1 + (row >> 3);
-            const bool rin = img_r >= 0 && img_r < p.H;
-            const int j0v = 7 * k + (row & 7);  // view-0 sub-column; view 1 is one to the left
-            const bool out0 = !rin || 2 * j0v >= p.W;
-            const bool out1 = !rin || j0v == 0 || 2 * (j0v - 1) + 1 >= p.W;
+        int g = 0;  // chunk counter (buffer g & 1)
+        FpTile tl;
+        for (int seq = 0; fp_tile(p, seq, tl); ++seq) {
+            const int img_r = tl.r0 + (row >> 3);
+            const int jv = 7 * tl.k - cv + (row & 7);  // sub-column of this pixel in view cv
+            const bool outside = img_r < 0 || img_r >= p.H || jv < 0 || 2 * jv + cv >= p.W;
             ptx::mbar_wait(&tfull[slot], sphase);
             ptx::tc_fence_after();
+            if (p.debug == 1) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[slot]);
+                slot ^= 1;
+                if (slot == 0) sphase ^= 1;
+                continue;
+            }
 #pragma unroll 1
-            for (int ch = 0; ch < BN / 64; ++ch) {
-                ptx::named_bar(1, FT_EPI);  // previous chunk's window reads are done
-                // conv outputs of both views -> bias, ReLU, bf16 -> region buffer
-                // [view][pixel m][64 ch], 16-byte chunk i of row m at i ^ (m & 7) (conflict-free rows)
+            for (int c = 0; c < NCH; ++c, ++g) {
+                const int bf = g & 1;
+                if (g >= 2) ptx::named_bar(FP_BAR_EMPTY + bf, 512);  // window warps are done with it
+                uint8_t* rb = region + bf * FP_BUF;
+                uint32_t vals[32];
+                ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (slot * 2 + cv) * BN + c * 32, vals);
+                ptx::tmem_ld_wait();
+                if (outside) {
 #pragma unroll
-                for (int v = 0; v < 2; ++v) {
-                    uint32_t vals[32];
-                    ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (slot * 2 + v) * BN + ch * 64 + h * 32,
-                                   vals);
-                    ptx::tmem_ld_wait();
-                    const bool outside = v ? out1 : out0;
-                    uint8_t* rowp = region + v * (128 * 128) + row * 128;
+                    for (int ii = 0; ii < 4; ++ii)
+                        *reinterpret_cast<uint4*>(rb + soff[ii]) = make_uint4(NEG_INF2, NEG_INF2, NEG_INF2, NEG_INF2);
+                } else {
 #pragma unroll
                     for (int ii = 0; ii < 4; ++ii) {
-                        const int ci8 = 4 * h + ii;
                         float f[8];
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk) f[kk] = __uint_as_float(vals[8 * ii + kk]);
-                        if (p.bias) {
-                            const int c0 = ch * 64 + 8 * ci8;
-                            const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + c0));
-                            const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 4));
+                        if (p.bias) {  // bias staged in shared memory (broadcast reads)
+                            const float4 b0 = *reinterpret_cast<const float4*>(sbias + c * 32 + 8 * ii);
+                            const float4 b1 = *reinterpret_cast<const float4*>(sbias + c * 32 + 8 * ii + 4);
                             f[0] += b0.x; f[1] += b0.y; f[2] += b0.z; f[3] += b0.w;
                             f[4] += b1.x; f[5] += b1.y; f[6] += b1.z; f[7] += b1.w;
                         }
+                        uint32_t pk[4];
                         if (p.relu) {
 #pragma unroll
-                            for (int kk = 0; kk < 8; ++kk) f[kk] = fmaxf(f[kk], 0.f);
-                        }
-                        uint32_t pk[4];
+                            for (int kk = 0; kk < 4; ++kk) pk[kk] = ptx::pack_bf16x2_relu(f[2 * kk], f[2 * kk + 1]);
+                        } else {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            __nv_bfloat162 hv = __floats2bfloat162_rn(f[2 * kk], f[2 * kk + 1]);
-                            pk[kk] = outside ? 0xFF80FF80u : *reinterpret_cast<uint32_t*>(&hv);
+                            for (int kk = 0; kk < 4; ++kk) {
+                                __nv_bfloat162 hv = __floats2bfloat162_rn(f[2 * kk], f[2 * kk + 1]);
+                                pk[kk] = *reinterpret_cast<uint32_t*>(&hv);
+                            }
                         }
-                        *reinterpret_cast<uint4*>(rowp + ((ci8 ^ (row & 7)) << 4)) =
-                            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        *reinterpret_cast<uint4*>(rb + soff[ii]) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                     }
                 }
-                if (ch + 1 == BN / 64) {  // TMEM of this slot fully read: the MMA may refill it
+                // rows r0-2, r0-1: carried from the previous tile of the strip (above the image: -inf)
+                if (tl.strip && et < 128)
+                    *reinterpret_cast<uint4*>(rb + koff) =
+                        tl.first ? make_uint4(NEG_INF2, NEG_INF2, NEG_INF2, NEG_INF2)
+                                 : *reinterpret_cast<const uint4*>(carry + c * FP_CARRY + kcar);
+                if (c + 1 == NCH) {  // TMEM slot fully read: the MMA may refill it
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&tempty[slot]);
                 }
-                ptx::named_bar(1, FT_EPI);
-                // owned windows: 7 centre columns x 7 centre rows, 8 channels per thread
-                for (int w = et; w < 49 * 8; w += FT_EPI) {
-                    const int wi = w >> 3, cg = w & 7;
-                    const int wc = wi % 7, wr = wi / 7;
-                    const int C = 7 * k + wc;
-                    const int R = 7 * i + wr;  // owned centre rows 2R + rho in [14 i, 14 i + 14)
-                    if (C >= p.Wo || R >= p.Ho) continue;
-                    // local centre row cr - r0 with cr = 2R + rho(C), rho(C) = C mod 2, r0 = 14 i - 1
-                    const int lr = 2 * wr + (C & 1) + 1;
-                    // canonical taps: 0,1 column 2C-1 (view 1, local sub-column wc); 2,3,4 column 2C
-                    // (view 0, wc); 5,6 column 2C+1 (view 1, wc + 1).  Row stride 1024 B; the swizzle
-                    // chunk depends only on the sub-column.
-                    const uint8_t* pl = region + 16384 + (lr + top1) * 1024 + wc * 128 + ((cg ^ wc) << 4);
-                    const uint8_t* pc = region + lr * 1024 + wc * 128 + ((cg ^ wc) << 4);
-                    const uint8_t* pr = region + 16384 + (lr + top1) * 1024 + (wc + 1) * 128 + ((cg ^ (wc + 1)) << 4);
+                ptx::named_bar_arrive(FP_BAR_FULL + bf, 512);
+            }
+            slot ^= 1;
+            if (slot == 0) sphase ^= 1;
+        }
+        for (int r = g < 2 ? 0 : g - 2; r < g; ++r) ptx::named_bar(FP_BAR_EMPTY + (r & 1), 512);  // drain
+    } else {
+        // ---- window warps: one (window, 8-channel group) item per thread and chunk
+        const int et = threadIdx.x - 64 - 256;  // 0..255
+        const bool relu = p.relu != 0;
+        const int pcen = p.parity & 1;  // centre column parity of every window (centres in even columns)
+        const int top1 = -1 + ((1 + pcen) >> 1);  // first row offset of the dc = +-1 taps
+        const int cg = et & 3, wi = et >> 2;
+        const int wc = wi % 7, ws = wi / 7;
+        const int kv = (et >> 6) & 1, kr = (et >> 5) & 1, ks = (et >> 2) & 7, ki = et & 3;
+        const int soff = kv * FP_VIEW + fp_off(16 + kr, ks, ki);
+        const int kcar = kv * 1024 + kr * 512 + ks * FP_PIX + ki * 16;
+        int g = 0;
+        FpTile tl;
+        for (int seq = 0; p.debug != 1 && fp_tile(p, seq, tl); ++seq) {
+            const int C = 7 * tl.k + wc;
+            const int rho = C & 1;  // centre row of window (R, C): cr = 2R + rho
+            // owned centre rows [lo, hi]
+            const int lo = tl.strip ? tl.r0 - 1 : tl.r0 + 1;
+            const int hi = tl.strip ? (tl.r0 + FT_RB >= p.H ? tl.r0 + 15 : tl.r0 + 14) : tl.r0 + 14;
+            const int R = (lo - rho + 3) / 2 - 1 + ws;  // ceil((lo - rho) / 2) + ws, lo - rho >= -2
+            const int cr = 2 * R + rho;
+            const bool valid = ws < (tl.strip ? 9 : 7) && C < p.Wo && R >= 0 && R < p.Ho && cr <= hi;
+            const int lr = cr - tl.r0 + 2;  // region row of the centre
+            // canonical taps: 0,1 column 2C-1 (view 1, local sub-column wc); 2,3,4 column 2C (view 0, wc);
+            // 5,6 column 2C+1 (view 1, wc + 1)
+            const int ol0 = FP_VIEW + fp_off(lr + top1, wc, cg), ol1 = FP_VIEW + fp_off(lr + top1 + 1, wc, cg);
+            const int oc0 = fp_off(lr - 1, wc, cg), oc1 = fp_off(lr, wc, cg), oc2 = fp_off(lr + 1, wc, cg);
+            const int or0 = FP_VIEW + fp_off(lr + top1, wc + 1, cg);
+            const int or1 = FP_VIEW + fp_off(lr + top1 + 1, wc + 1, cg);
+            const int64_t obase = (((int64_t)tl.b * p.Ho + R) * p.Wo + C) * p.Cout + cg * 8;
+#pragma unroll 1
+            for (int c = 0; c < NCH; ++c, ++g) {
+                const int bf = g & 1;
+                ptx::named_bar(FP_BAR_FULL + bf, 512);
+                const uint8_t* rb = region + bf * FP_BUF;
+                if (tl.strip && !tl.last && et < 128)  // rows r0+14, r0+15 carry into the next tile
+                    *reinterpret_cast<uint4*>(carry + c * FP_CARRY + kcar) =
+                        *reinterpret_cast<const uint4*>(rb + soff);
+                if (valid) {
                     uint4 tv[7];
-                    tv[0] = *reinterpret_cast<const uint4*>(pl);
-                    tv[1] = *reinterpret_cast<const uint4*>(pl + 1024);
-                    tv[2] = *reinterpret_cast<const uint4*>(pc - 1024);
-                    tv[3] = *reinterpret_cast<const uint4*>(pc);
-                    tv[4] = *reinterpret_cast<const uint4*>(pc + 1024);
-                    tv[5] = *reinterpret_cast<const uint4*>(pr);
-                    tv[6] = *reinterpret_cast<const uint4*>(pr + 1024);
+                    tv[0] = *reinterpret_cast<const uint4*>(rb + ol0);
+                    tv[1] = *reinterpret_cast<const uint4*>(rb + ol1);
+                    tv[2] = *reinterpret_cast<const uint4*>(rb + oc0);
+                    tv[3] = *reinterpret_cast<const uint4*>(rb + oc1);
+                    tv[4] = *reinterpret_cast<const uint4*>(rb + oc2);
+                    tv[5] = *reinterpret_cast<const uint4*>(rb + or0);
+                    tv[6] = *reinterpret_cast<const uint4*>(rb + or1);
                     uint32_t best[4], ix[4];
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&tv[0]);
-                        __nv_bfloat162 mx = *reinterpret_cast<const __nv_bfloat162*>(w0 + kk);
+                        __nv_bfloat162 mx = *reinterpret_cast<const __nv_bfloat162*>(
+                            reinterpret_cast<const uint32_t*>(&tv[0]) + kk);
 #pragma unroll
                         for (int t = 1; t < 7; ++t)
                             mx = __hmax2(mx, *reinterpret_cast<const __nv_bfloat162*>(
                                                  reinterpret_cast<const uint32_t*>(&tv[t]) + kk));
-                        // first tap equal to the maximum == first strict maximum in canonical order
-                        best[kk] = reinterpret_cast<const uint32_t*>(&tv[6])[kk];
+                        // first tap equal to the maximum == first strict maximum in canonical order; with
+                        // ReLU no value is -0 (cvt.relu gives +0), so the maximum's bits are that tap's bits
+                        best[kk] = relu ? *reinterpret_cast<const uint32_t*>(&mx)
+                                        : reinterpret_cast<const uint32_t*>(&tv[6])[kk];
                         ix[kk] = 6u * 0x00010001u;
 #pragma unroll
                         for (int t = 5; t >= 0; --t) {
                             const uint32_t wv = reinterpret_cast<const uint32_t*>(&tv[t])[kk];
                             const uint32_t mk = __heq2_mask(*reinterpret_cast<const __nv_bfloat162*>(&wv), mx);
-                            best[kk] = (wv & mk) | (best[kk] & ~mk);
+                            if (!relu) best[kk] = (wv & mk) | (best[kk] & ~mk);
                             ix[kk] = ((uint32_t)t * 0x00010001u & mk) | (ix[kk] & ~mk);
                         }
                     }
-                    const int64_t o = (((int64_t)b * p.Ho + R) * p.Wo + C) * p.Cout + ch * 64 + cg * 8;
+                    const int64_t o = obase + c * 32;
                     *reinterpret_cast<uint4*>(p.y + o) = make_uint4(best[0], best[1], best[2], best[3]);
                     *reinterpret_cast<uint2*>(p.am + o) =
                         make_uint2(__byte_perm(ix[0], ix[1], 0x6420), __byte_perm(ix[2], ix[3], 0x6420));
                 }
+                ptx::named_bar_arrive(FP_BAR_EMPTY + bf, 512);
             }
-            slot ^= 1;
-            if (slot == 0) sphase ^= 1;
         }
     }
     ptx::tc_fence_before();
@@ -909,9 +1094,9 @@ FpPlan fp_plan(const Geom& g, int Cin, int Cout) {
     if (g.s != 1 || (g.n != 1 && g.n != 2) || Cin % 64 || (Cout != 64 && Cout != 128) || g.W < 2) return pl;
     int po;
     if (!out_shape(g.H, g.W, 2, g.parity, &pl.Ho, &pl.Wo, &po)) return pl;
-    const int A = (FT_RB + 2 * g.n) * FT_JB * 128;
+    const int A = (FT_RB + 2 * g.n + (g.n == 1 ? 1 : 0)) * FT_JB * 128;
     const int res_bytes = g.T * (Cin / 64) * Cout * 128;
-    const int fixed = FP_REGION + 1024 + 512;
+    const int fixed = 2 * FP_BUF + (Cout / 32) * FP_CARRY + Cout * 4 + 1024 + 512;
     pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
     if (pl.stages > 8) pl.stages = 8;
     if (pl.stages < 3) return pl;
@@ -935,20 +1120,30 @@ hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax,
     if (!pl.ok) return HEX_ERR_UNSUPPORTED;
     FpParams p{};
     p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
-    p.Ho = pl.Ho; p.Wo = pl.Wo; p.nr = pl.nr; p.nc = pl.nc; p.regions = g.B * pl.nr * pl.nc;
+    p.Ho = pl.Ho; p.Wo = pl.Wo; p.nr = pl.nr; p.nc = pl.nc;
     p.kchunks = a.Cin / 64; p.stages = pl.stages; p.relu = a.relu; p.bias = a.bias;
     p.y = (uint16_t*)y_pool; p.am = argmax;
+    // whole rounds of strips (one per CTA per round), the remaining strips as independent regions
+    const int strips = g.B * pl.nc;
+    p.ntr = (g.H + FT_RB - 1) / FT_RB;
+    const int sms = num_sms();
+    const bool strip_mode = !getenv("HEXCONV_FUSED_POOL_REGIONS");
+    p.debug = getenv("HEXCONV_FP_DEBUG") ? atoi(getenv("HEXCONV_FP_DEBUG")) : 0;
+    int grid = sms;
+    p.full_rounds = strip_mode ? strips / sms : 0;
+    p.left_regions = (strips - p.full_rounds * sms) * pl.nr;
+    if (p.full_rounds == 0 && p.left_regions < grid) grid = p.left_regions;
     CUtensorMap mx0, mx1, mw;
-    if (!ft_view5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, FT_RB + 2 * g.n)) return HEX_ERR_CUDA;
-    if (!ft_view5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, FT_RB + 2 * g.n)) return HEX_ERR_CUDA;
+    const int box_rows = FT_RB + 2 * g.n + (g.n == 1 ? 1 : 0);  // n = 1: 19-row boxes shared by both views
+    if (!ft_view5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, box_rows)) return HEX_ERR_CUDA;
+    if (!ft_view5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, box_rows)) return HEX_ERR_CUDA;
     if (!ft_wmap(&mw, a.wpack, g.T, a.Cout, a.Cin, a.Cout)) return HEX_ERR_CUDA;
-    const int grid = p.regions < num_sms() ? p.regions : num_sms();
 #define HEX_FP(BN_, N_)                                                                                       \
     {                                                                                                         \
         auto kern = tc_conv_maxpool_kernel<BN_, N_>;                                                          \
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem) != cudaSuccess) \
             return HEX_ERR_CUDA;                                                                              \
-        kern<<<grid, FT_THREADS, pl.smem, st>>>(mx0, mx1, mw, p);                                             \
+        kern<<<grid, FP_THREADS, pl.smem, st>>>(mx0, mx1, mw, p);                                             \
     }
     if (a.Cout == 128) {
         if (g.n == 1) HEX_FP(128, 1) else HEX_FP(128, 2)

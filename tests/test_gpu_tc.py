@@ -147,6 +147,31 @@ def test_fused_conv_relu_maxpool(F, oracle, n, pi):
         assert np.array_equal(am.permute(0, 3, 1, 2).cpu().numpy(), amr)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("pi", [0, 1])
+def test_fused_conv_maxpool_strips(F, oracle, pi):
+    # batches with >= one strip per SM run the strip-walking mode (rows carried between tiles) plus the
+    # region-mode tail; ragged bottom (46 rows), a last tile whose bottom window reaches row H (48 rows)
+    import synth
+    for (B, Cin, Cout, H, W) in [(25, 64, 128, 46, 96), (25, 64, 64, 48, 90), (44, 128, 64, 32, 48)]:
+        T = oracle.num_taps(1)
+        g = torch.Generator().manual_seed(900 + H + pi)
+        x = (torch.randn(B, H, W, Cin, generator=g)).to(torch.bfloat16).cuda()
+        w = (torch.randn(Cout, Cin, T, generator=g) / np.sqrt(Cin * T)).to(torch.bfloat16).cuda()
+        b = (0.2 * torch.randn(Cout, generator=g)).cuda()
+        assert F.conv2d_fwd_maxpool_supported(B, Cin, Cout, H, W, 1, pi)
+        yp, am = F.conv2d_fwd_maxpool(x, w, b, n=1, parity=pi)
+        yc = F.conv2d_fwd(x, w, b, n=1, parity=pi, relu=True, layout="NHWC")
+        yp2, am2 = F.pool2d_fwd(yc, 1, 2, pi, "max", "NHWC")
+        torch.cuda.synchronize()
+        assert torch.equal(yp.view(torch.int16), yp2.view(torch.int16)), (pi, B, H, W)
+        assert torch.equal(am, am2), (pi, B, H, W)
+        # the last image (region-mode tail) against the oracle pool of the GPU conv output
+        pr, amr = oracle.pool2d_fwd(back(yc[-1:]), n=1, s=2, pi=pi, mode="max")
+        assert np.array_equal(back(yp[-1:]), pr)
+        assert np.array_equal(am[-1:].permute(0, 3, 1, 2).cpu().numpy(), amr)
+
+
 def test_fused_conv_maxpool_unsupported_shape(F):
     # n = 2 weights do not stay resident next to the fused kernel's buffers: the call reports
     # HEX_ERR_UNSUPPORTED (8) and the caller runs conv + pool separately

@@ -7,6 +7,7 @@
 //        tools/mma_bench.cu -o /tmp/mma_bench -lcuda
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "tc_ptx.cuh"
@@ -148,6 +149,86 @@ __global__ void __launch_bounds__(128, 1) bench_seq(int iters, long long* out) {
     }
 }
 
+// Shared-memory bandwidth contention: thread 0 issues ITERS lean K-major MMAs (M = 128, N) while
+// LW warps stream LDS.128 over a separate 32 KB area until the MMAs are done.
+template <int N, int LW>
+__global__ void __launch_bounds__(64 + 32 * LW, 1) bench_contend(int iters, long long* out, long long* lds_bytes) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t bar;
+    __shared__ uint32_t slot;
+    __shared__ volatile int done;
+    __shared__ unsigned long long nbytes;
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bar, 1);
+        ptx::fence_barrier_init();
+        done = 0;
+        nbytes = 0;
+    }
+    if (warp == 1) ptx::tmem_alloc(&slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        const uint32_t s = ptx::smem_u32(smem);
+        const uint32_t idesc = ptx::idesc_bf16(128, N, 0, 0);
+        const uint64_t ad = ptx::smem_desc_sw128(s, 16, 1024);
+        const uint64_t bd = ptx::smem_desc_sw128(s + 65536, 16, 1024);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ptx::mma_bf16(tmem + ((j * N) & 511), ad, bd, idesc, 1);
+        }
+        ptx::mma_commit(&bar);
+        ptx::mbar_wait(&bar, 0);
+        out[blockIdx.x] = clock64() - t0;
+        done = 1;
+    } else if (warp >= 2) {
+        const uint4* src = reinterpret_cast<const uint4*>(smem + 131072);
+        uint32_t acc = 0;
+        unsigned long long cnt = 0;
+        int i = threadIdx.x & 31;
+        while (!done) {
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const uint4 v = src[(i + u * 32 + (warp - 2) * 512) & 2047];
+                acc ^= v.x ^ v.y ^ v.z ^ v.w;
+            }
+            i += 7;
+            cnt += 16 * 16;
+        }
+        atomicAdd(&nbytes, cnt);
+        if (acc == 0x12345678u) out[0] = 0;  // keep the loads
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) lds_bytes[blockIdx.x] = (long long)nbytes;
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
+template <int N, int LW>
+static void run_contend(long long* d_out, long long* d_lds) {
+    const int smem = 200 * 1024, iters = 16384;
+    cudaFuncSetAttribute(bench_contend<N, LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    bench_contend<N, LW><<<148, 64 + 32 * LW, smem>>>(iters, d_out, d_lds);
+    bench_contend<N, LW><<<148, 64 + 32 * LW, smem>>>(iters, d_out, d_lds);
+    cudaDeviceSynchronize();
+    long long h[148], l[148];
+    cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaMemcpy(l, d_lds, sizeof(l), cudaMemcpyDeviceToHost);
+    double avg = 0, lb = 0;
+    for (int i = 0; i < 148; ++i) { avg += h[i]; lb += l[i]; }
+    avg /= 148;
+    lb /= 148;
+    printf("contend N=%3d lds_warps=%2d  %7.1f cyc/MMA (ideal %5.1f)  LDS %6.1f B/clk  MMA operands %6.1f B/clk\n", N,
+           LW, avg / iters, N / 2.0, lb / avg, (double)iters * (128 + N) * 32 / avg);
+}
+
 template <int N0, int N1, int N2, int N3>
 static void run_seq(const char* name, long long* d_out) {
     const int smem = 200 * 1024, iters = 4096;
@@ -190,6 +271,25 @@ int main() {
     };
     long long* d_out;
     cudaMalloc(&d_out, 148 * sizeof(long long));
+    if (getenv("MMA_CONTEND")) {
+        long long* d_lds;
+        cudaMalloc(&d_lds, 148 * sizeof(long long));
+        run_contend<128, 0>(d_out, d_lds);
+        run_contend<128, 2>(d_out, d_lds);
+        run_contend<128, 4>(d_out, d_lds);
+        run_contend<128, 8>(d_out, d_lds);
+        run_contend<128, 16>(d_out, d_lds);
+        run_contend<256, 0>(d_out, d_lds);
+        run_contend<256, 4>(d_out, d_lds);
+        run_contend<256, 16>(d_out, d_lds);
+        run_contend<64, 0>(d_out, d_lds);
+        run_contend<64, 4>(d_out, d_lds);
+        run_contend<64, 16>(d_out, d_lds);
+        run_contend<32, 0>(d_out, d_lds);
+        run_contend<16, 0>(d_out, d_lds);
+        run_contend<8, 0>(d_out, d_lds);
+        return 0;
+    }
     run_seq<128, 192, 128, 64>("seq n1: 128 192 128 64", d_out);
     run_seq<128, 192, 128, 0>("seq n1: 128 192 128", d_out);
     run_seq<192, 256, 64, 0>("seq n2 g0: 192 256 64", d_out);
