@@ -46,6 +46,7 @@ struct FtParams {
     int rt, jt0, jt1, tiles0, mtiles, n_tiles, total_tiles, kchunks, stages;
     int pair_tiles;  // CTA-pair kernel: (n tile, pair of m tiles) work items
     int relu, has_mask;
+    int debug;  // HEXCONV_FT_DEBUG: 1 = epilogue skipped, 2 = MMAs skipped (timing experiments)
     const float* bias;
 };
 
@@ -304,6 +305,17 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                 ptx::mbar_wait(&tempty[acc], aphase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
+                if (!PAIR && p.debug == 2) {
+                    for (int u = 0; u < p.kchunks * SL::count(); ++u) {
+                        ptx::mbar_wait(&full[stage], phase);
+                        ptx::mbar_arrive(&empty[stage]);
+                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    }
+                    ptx::mbar_arrive(&tfull[acc]);
+                    acc ^= 1;
+                    if (acc == 0) aphase ^= 1;
+                    continue;
+                }
                 for (int kc = 0; kc < p.kchunks; ++kc)
                     issue_stages_from<BN, N, TG, RES, PAIR, 0>(d, a_ring, b_ring, res_desc, full, empty, stage, phase,
                                                                p.stages, stage16, a_bytes16, kc, p.kchunks,
@@ -328,7 +340,7 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
         uint32_t mphase0 = 0, mphase1 = 0;
         // ReLU-backward mask tiles are TMA-loaded one chunk ahead -- across tile boundaries too, so
         // the next tile's first mask chunk is in flight while the current tile's last chunk drains
-        if (p.has_mask && et == 0) {
+        if (p.has_mask && et == 0 && p.debug != 1) {
             const int t0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
             if (t0 < (PAIR ? p.pair_tiles : p.total_tiles)) {
                 int P, r0, j0, b, n0;
@@ -348,7 +360,7 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
 #pragma unroll 1
-            for (int ch = 0; ch < BN / 64; ++ch) {
+            for (int ch = 0; ch < (p.debug == 1 ? 0 : BN / 64); ++ch) {
                 uint8_t* buf = obuf + ob * FT_OUT;
                 const int c0 = n0 + ch * 64;
                 if (p.has_mask) {
@@ -873,6 +885,290 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
     }
 }
 
+// ------------------------------------------------------------------ n = 1 view-pair forward / bwd-data
+// The tap-reuse forward above computes one 16 x 8 tile of ONE parity view per work item, reading three
+// 18-row boxes (one per kernel column), two of which come from the other view at overlapping
+// sub-columns.  Here a work item is the PAIR of tiles (view 0 and view 1) at the same sub-columns
+// [j0, j0+8) and rows [r0, r0+16); four 19-row boxes (top row r0 - 1) serve both tiles:
+//   box 0 = view 1 at j0-1: view-0 dc = -1 (taps 0,1)
+//   box 1 = view 0 at j0:   view-0 dc =  0 (taps 2..4), view-1 dc = -1 (taps 0,1)
+//   box 2 = view 1 at j0:   view-0 dc = +1 (taps 5,6),  view-1 dc =  0 (taps 2..4)
+//   box 3 = view 0 at j0+1: view-1 dc = +1 (taps 5,6)
+// (4 boxes / 76 KB per 2 tiles instead of 6 / 108 KB), each accumulator still summed in the canonical
+// column order.  Resident weights, n = 1, Cout = 64 or 128 (C5 layer-2 bwd-data).
+struct FvParams {
+    int B, H, W, Cin, Cout, parity;
+    int rt, jt, pairs, kchunks, stages, relu, has_mask, debug, prefetch;
+    const float* bias;
+};
+
+template <int BN>
+__device__ __forceinline__ void fv_issue(uint32_t d0, uint32_t d1, uint64_t a_ring, uint64_t res_desc, uint64_t* full,
+                                         uint64_t* empty, int& stage, uint32_t& phase, int nstages, uint32_t stage16,
+                                         int kc, int kchunks, uint32_t first, uint32_t pc0) {
+    const uint64_t o0 = (uint64_t)(pc0 * 64), o1 = (uint64_t)((pc0 ^ 1u) * 64);  // 1024-byte rows
+    const int bs = kchunks * BN * 8;
+    const uint64_t w0 = res_desc + (uint64_t)(kc * (BN * 8));  // tap t at w0 + t * bs
+#pragma unroll
+    for (int bx = 0; bx < 4; ++bx) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint64_t ad = a_ring + (uint64_t)stage * stage16;
+        if (bx == 0) {
+            issue_stage<BN, 2, true>(d0, ad + o0, w0, bs, first);
+        } else if (bx == 1) {
+            issue_stage<BN, 3, true>(d0, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
+            issue_stage<BN, 2, true>(d1, ad + o1, w0, bs, first);
+        } else if (bx == 2) {
+            issue_stage<BN, 2, true>(d0, ad + o0, w0 + (uint64_t)(5 * bs), bs, 1u);
+            issue_stage<BN, 3, true>(d1, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
+        } else {
+            issue_stage<BN, 2, true>(d1, ad + o1, w0 + (uint64_t)(5 * bs), bs, 1u);
+        }
+        ptx::mma_commit(&empty[stage]);
+        if (++stage == nstages) { stage = 0; phase ^= 1; }
+    }
+}
+
+__device__ __forceinline__ void fv_decode(const FvParams& p, int pr, int* r0, int* j0, int* b) {
+    const int ji = pr % p.jt;
+    const int t = pr / p.jt;
+    *r0 = (t % p.rt) * FT_RB;
+    *j0 = ji * FT_JB;
+    *b = t / p.rt;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(FT_THREADS, 1)
+tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
+                    const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
+                    const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
+                    const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ FvParams p) {
+    constexpr int A_BYTES = (FT_RB + 3) * FT_JB * 128;  // 19-row box
+    constexpr int W_TILE = BN * 128;
+    constexpr int TMEM_COLS = 4 * BN;  // 2 slots x 2 views
+    constexpr int UNITS = 2 * (BN / 64);  // (view, 64-channel chunk) epilogue units per pair
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int res_bytes = 7 * p.kchunks * W_TILE;
+    uint8_t* resw = base;
+    uint8_t* ring = base + res_bytes;
+    uint8_t* obuf = ring + p.stages * A_BYTES;
+    uint64_t* full = (uint64_t*)(obuf + 2 * FT_OUT);
+    uint64_t* empty = full + p.stages;
+    uint64_t* tfull = empty + p.stages;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* mbar = tempty + 2;
+    uint64_t* bres = mbar + 2;
+    uint32_t* tmem_slot = (uint32_t*)(bres + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], FT_EPI / 32);
+            ptx::mbar_init(&mbar[a], 1);
+        }
+        ptx::mbar_init(bres, 1);
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&map_x0);
+        ptx::prefetch_tmap(&map_x1);
+        ptx::prefetch_tmap(&map_w);
+        ptx::prefetch_tmap(&map_y0);
+        ptx::prefetch_tmap(&map_y1);
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            ptx::mbar_arrive_expect_tx(bres, (uint32_t)res_bytes);
+            for (int t = 0; t < 7; ++t)
+                for (int kc = 0; kc < p.kchunks; ++kc)
+                    ptx::tma_load_4d(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0, 0, kc, t);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int pr = blockIdx.x; pr < p.pairs; pr += gridDim.x) {
+                int r0, j0, b;
+                if (p.prefetch && pr + gridDim.x < p.pairs) {  // next pair's boxes into L2 (hides DRAM latency)
+                    fv_decode(p, pr + gridDim.x, &r0, &j0, &b);
+                    for (int kc = 0; kc < p.kchunks; ++kc)
+#pragma unroll
+                        for (int bx = 0; bx < 4; ++bx)
+                            ptx::tma_prefetch_5d((bx & 1) ? &map_x0 : &map_x1, 0,
+                                                 j0 + (bx == 0 ? -1 : (bx == 3 ? 1 : 0)), r0 - 1, b, kc);
+                }
+                fv_decode(p, pr, &r0, &j0, &b);
+                for (int kc = 0; kc < p.kchunks; ++kc)
+#pragma unroll
+                    for (int bx = 0; bx < 4; ++bx) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sa = ring + stage * A_BYTES;
+                        if (p.debug == 3) {  // no loads: MMAs on stale shared memory (timing experiment)
+                            ptx::mbar_arrive(&full[stage]);
+                            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                            continue;
+                        }
+                        ptx::mbar_arrive_expect_tx(&full[stage], A_BYTES);
+                        ptx::tma_load_5d((bx & 1) ? &map_x0 : &map_x1, &full[stage], sa, 0,
+                                         j0 + (bx == 0 ? -1 : (bx == 3 ? 1 : 0)), r0 - 1, b, kc);
+                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint64_t a_ring = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
+            const uint64_t res_desc = ptx::smem_desc_sw128(ptx::smem_u32(resw), 16, 1024);
+            int stage = 0;
+            uint32_t phase = 0;
+            int slot = 0;
+            uint32_t sphase = 0;
+            ptx::mbar_wait(bres, 0);
+            for (int pr = blockIdx.x; pr < p.pairs; pr += gridDim.x) {
+                ptx::mbar_wait(&tempty[slot], sphase ^ 1);
+                ptx::tc_fence_after();
+                if (p.debug == 2) {
+                    for (int u = 0; u < 4 * p.kchunks; ++u) {
+                        ptx::mbar_wait(&full[stage], phase);
+                        ptx::mbar_arrive(&empty[stage]);
+                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    }
+                    ptx::mbar_arrive(&tfull[slot]);
+                } else {
+                    for (int kc = 0; kc < p.kchunks; ++kc)
+                        fv_issue<BN>(tmem_base + (slot * 2) * BN, tmem_base + (slot * 2 + 1) * BN, a_ring, res_desc,
+                                     full, empty, stage, phase, p.stages, A_BYTES >> 4, kc, p.kchunks,
+                                     kc == 0 ? 0u : 1u, (uint32_t)(p.parity & 1));
+                    ptx::mma_commit(&tfull[slot]);
+                }
+                slot ^= 1;
+                if (slot == 0) sphase ^= 1;
+            }
+        }
+    } else {
+        // Epilogue (as in tc_fwd_tr_kernel): warps 2..9, TMEM lane quadrant warp % 4, channel half h.
+        // Units (view v, 64-channel chunk ch) of a pair in order; ReLU-backward mask tiles are
+        // TMA-loaded one unit ahead, across pairs too.
+        const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
+        const int row = q * 32 + lane;
+        const int et = threadIdx.x - 64;
+        int slot = 0;
+        uint32_t sphase = 0;
+        int ob = 0;
+        uint32_t mphase0 = 0, mphase1 = 0;
+        if (p.has_mask && et == 0 && p.debug != 1 && (int)blockIdx.x < p.pairs) {
+            int r0, j0, b;
+            fv_decode(p, blockIdx.x, &r0, &j0, &b);
+            ptx::mbar_arrive_expect_tx(&mbar[0], FT_OUT);
+            ptx::tma_load_4d(&map_m0, &mbar[0], obuf, 0, j0, r0, b);
+        }
+        for (int pr = blockIdx.x; pr < p.pairs; pr += gridDim.x) {
+            int r0, j0, b;
+            fv_decode(p, pr, &r0, &j0, &b);
+            ptx::mbar_wait(&tfull[slot], sphase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int u = 0; u < (p.debug == 1 ? 0 : UNITS); ++u) {
+                const int v = u / (BN / 64), ch = u % (BN / 64);
+                uint8_t* buf = obuf + ob * FT_OUT;
+                const int c0 = ch * 64;
+                if (p.has_mask) {
+                    ptx::mbar_wait(&mbar[ob], ob ? mphase1 : mphase0);
+                    if (ob) mphase1 ^= 1; else mphase0 ^= 1;
+                } else {
+                    if (et == 0) ptx::bulk_wait_read<1>();
+                    ptx::named_bar(1, FT_EPI);
+                }
+                uint32_t vals[32];
+                ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (slot * 2 + v) * BN + c0 + h * 32, vals);
+                ptx::tmem_ld_wait();
+                uint8_t* rowp = buf + row * 128;
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    const int i = 4 * h + ii;  // 16-byte unit (8 channels) within the 64-channel chunk
+                    uint4* sl = reinterpret_cast<uint4*>(rowp + ((i ^ (row & 7)) << 4));
+                    float f[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) f[k] = __uint_as_float(vals[8 * ii + k]);
+                    if (p.bias) {
+                        const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i));
+                        const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + 8 * i + 4));
+                        f[0] += b0.x; f[1] += b0.y; f[2] += b0.z; f[3] += b0.w;
+                        f[4] += b1.x; f[5] += b1.y; f[6] += b1.z; f[7] += b1.w;
+                    }
+                    if (p.relu && !p.has_mask) {
+                        *sl = make_uint4(ptx::pack_bf16x2_relu(f[0], f[1]), ptx::pack_bf16x2_relu(f[2], f[3]),
+                                         ptx::pack_bf16x2_relu(f[4], f[5]), ptx::pack_bf16x2_relu(f[6], f[7]));
+                        continue;
+                    }
+                    if (p.relu) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) f[k] = fmaxf(f[k], 0.f);
+                    }
+                    if (p.has_mask) {
+                        const uint4 m4 = *sl;
+                        const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t bits = (k & 1) ? (mw[k >> 1] & 0xffff0000u) : (mw[k >> 1] << 16);
+                            if (!(__uint_as_float(bits) > 0.f)) f[k] = 0.f;
+                        }
+                    }
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        __nv_bfloat162 hv = __floats2bfloat162_rn(f[2 * k], f[2 * k + 1]);
+                        pk[k] = *reinterpret_cast<uint32_t*>(&hv);
+                    }
+                    *sl = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                ptx::fence_proxy_async();
+                ptx::named_bar(1, FT_EPI);
+                if (et == 0) {
+                    ptx::tma_store_4d(v ? &map_y1 : &map_y0, buf, c0, j0, r0, b);
+                    ptx::bulk_commit();
+                    if (p.has_mask) {  // the next unit's mask tile
+                        int nr = r0, nj = j0, nb = b, nu = u + 1;
+                        bool more = true;
+                        if (nu == UNITS) {
+                            nu = 0;
+                            const int np = pr + gridDim.x;
+                            more = np < p.pairs;
+                            if (more) fv_decode(p, np, &nr, &nj, &nb);
+                        }
+                        if (more) {
+                            const int nv = nu / (BN / 64), nch = nu % (BN / 64);
+                            ptx::bulk_wait_read<1>();
+                            ptx::mbar_arrive_expect_tx(&mbar[ob ^ 1], FT_OUT);
+                            ptx::tma_load_4d(nv ? &map_m1 : &map_m0, &mbar[ob ^ 1], obuf + (ob ^ 1) * FT_OUT, nch * 64,
+                                             nj, nr, nb);
+                        }
+                    }
+                }
+                ob ^= 1;
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[slot]);
+            slot ^= 1;
+            if (slot == 0) sphase ^= 1;
+        }
+        if (et == 0) ptx::bulk_wait<0>();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 ft_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1031,8 +1327,67 @@ static hex_status_t launch_ft(const CUtensorMap* maps, const FtParams& p, int sm
     return last_launch_status();
 }
 
+// view-pair plan: n = 1, resident weights, Cout 64 / 128; returns stages (0 = not eligible)
+static int fv_stages(const Geom& g, int Cin, int Cout, int* smem) {
+    if (g.n != 1 || g.s != 1 || Cin % 64 || (Cout != 64 && Cout != 128) || getenv("HEXCONV_NO_FWD_VPAIR")) return 0;
+    const int A = (FT_RB + 3) * FT_JB * 128;
+    const int res_bytes = 7 * (Cin / 64) * Cout * 128;
+    const int fixed = 2 * FT_OUT + 1024 + 512;
+    int stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
+    if (stages > 8) stages = 8;
+    if (stages < 3) return 0;
+    *smem = res_bytes + stages * A + fixed;
+    return stages;
+}
+
+static hex_status_t tc_fwd_vpair(const TcConvArgs& a, int stages, int smem, cudaStream_t st) {
+    const Geom& g = a.g;
+    FvParams p{};
+    p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.parity = g.parity;
+    p.rt = ceil_div(g.H, FT_RB);
+    p.jt = ceil_div((g.W + 1) / 2, FT_JB);  // view 0 has the most sub-columns
+    p.pairs = p.rt * p.jt * g.B;
+    p.kchunks = a.Cin / 64;
+    p.stages = stages;
+    p.relu = a.relu;
+    p.has_mask = a.relu_y != nullptr;
+    p.debug = getenv("HEXCONV_FT_DEBUG") ? atoi(getenv("HEXCONV_FT_DEBUG")) : 0;
+    p.prefetch = getenv("HEXCONV_FV_PREFETCH") ? atoi(getenv("HEXCONV_FV_PREFETCH")) : 0;  // measured no gain
+    p.bias = a.bias;
+    CUtensorMap maps[7];
+    if (!ft_view5(&maps[0], a.x, g.B, g.H, g.W, a.Cin, 0, FT_RB + 3)) return HEX_ERR_CUDA;
+    if (!ft_view5(&maps[1], a.x, g.B, g.H, g.W, a.Cin, 1, FT_RB + 3)) return HEX_ERR_CUDA;
+    if (!ft_wmap(&maps[2], a.wpack, g.T, a.Cout, a.Cin, a.Cout)) return HEX_ERR_CUDA;
+    if (!ft_view4(&maps[3], a.y, g.B, g.H, g.W, a.Cout, 0)) return HEX_ERR_CUDA;
+    if (!ft_view4(&maps[4], a.y, g.B, g.H, g.W, a.Cout, 1)) return HEX_ERR_CUDA;
+    if (a.relu_y) {
+        if (!ft_view4(&maps[5], a.relu_y, g.B, g.H, g.W, a.Cout, 0)) return HEX_ERR_CUDA;
+        if (!ft_view4(&maps[6], a.relu_y, g.B, g.H, g.W, a.Cout, 1)) return HEX_ERR_CUDA;
+    } else {
+        maps[5] = maps[3];
+        maps[6] = maps[4];
+    }
+    const int grid = p.pairs < num_sms() ? p.pairs : num_sms();
+#define HEX_FV(BN_)                                                                                             \
+    {                                                                                                           \
+        auto kern = tc_fwd_vpair_kernel<BN_>;                                                                   \
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)       \
+            return HEX_ERR_CUDA;                                                                                \
+        kern<<<grid, FT_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p); \
+    }
+    if (a.Cout == 128) HEX_FV(128) else HEX_FV(64)
+#undef HEX_FV
+    count_launch();
+    return last_launch_status();
+}
+
 hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
+    {
+        int smem = 0;
+        const int stages = fv_stages(g, a.Cin, a.Cout, &smem);
+        if (stages) return tc_fwd_vpair(a, stages, smem, st);
+    }
     const FtPlan pl = ft_plan(g, a.Cin, a.Cout);
     if (!pl.ok) return HEX_ERR_UNSUPPORTED;
     FtParams p{};
@@ -1049,6 +1404,7 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
     p.stages = pl.stages;
     p.relu = a.relu;
     p.has_mask = a.relu_y != nullptr;
+    p.debug = getenv("HEXCONV_FT_DEBUG") ? atoi(getenv("HEXCONV_FT_DEBUG")) : 0;
     p.bias = a.bias;
     CUtensorMap maps[7];
     if (!ft_view5(&maps[0], a.x, g.B, g.H, g.W, a.Cin, 0, FT_RB + 2 * g.n)) return HEX_ERR_CUDA;

@@ -70,9 +70,10 @@ __global__ void __launch_bounds__(128, 1) bench(Cfg c, int iters, long long* out
         const uint32_t s = ptx::smem_u32(smem);
         const uint32_t idesc = ptx::idesc_bf16(c.M, c.N, c.a_mn, c.b_mn);
         if (c.nmma < 0) {  // lean issue loop: descriptors built once, 8 MMAs per iteration, 8 D tiles
+            // (nmma = -4: all MMAs into ONE accumulator; -5: two accumulators alternating)
             const uint64_t ad = ptx::smem_desc_sw128(s, 16, 1024);
             const uint64_t bd = ptx::smem_desc_sw128(s + 65536, 16, 1024);
-            const uint32_t step = (uint32_t)c.N;
+            const uint32_t step = c.nmma == -4 ? 0u : (c.nmma == -5 ? (uint32_t)(c.N * 4) : (uint32_t)c.N);
             const long long t0 = clock64();
             for (int i = 0; i < iters; i += 8) {
 #pragma unroll
@@ -274,6 +275,28 @@ int main() {
     if (getenv("MMA_CONTEND")) {
         long long* d_lds;
         cudaMalloc(&d_lds, 148 * sizeof(long long));
+        {
+            Cfg extra[] = {
+                {128, 64, 0, 0, 16, 16, 1024, -1, "lean N=64, 8 D tiles"},
+                {128, 64, 0, 0, 16, 16, 1024, -4, "lean N=64, one D"},
+                {128, 64, 0, 0, 16, 16, 1024, -5, "lean N=64, two D alternating"},
+                {128, 128, 0, 0, 16, 16, 1024, -1, "lean N=128, 8 D tiles"},
+                {128, 128, 0, 0, 16, 16, 1024, -4, "lean N=128, one D"},
+                {128, 256, 0, 0, 16, 16, 1024, -4, "lean N=256, one D"},
+            };
+            const int smem = 200 * 1024;
+            cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            for (const Cfg& c : extra) {
+                bench<<<148, 128, smem>>>(c, 8192, d_out);
+                bench<<<148, 128, smem>>>(c, 8192, d_out);
+                cudaDeviceSynchronize();
+                long long h[148];
+                cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+                double avg = 0;
+                for (int i = 0; i < 148; ++i) avg += h[i];
+                printf("%-36s %7.1f cyc/MMA\n", c.name, avg / 148 / 8192);
+            }
+        }
         run_contend<128, 0>(d_out, d_lds);
         run_contend<128, 2>(d_out, d_lds);
         run_contend<128, 4>(d_out, d_lds);
