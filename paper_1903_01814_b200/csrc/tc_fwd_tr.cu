@@ -305,13 +305,15 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                 ptx::mbar_wait(&tempty[acc], aphase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
-                if (!PAIR && p.debug == 2) {
+                if (p.debug == 2) {
                     for (int u = 0; u < p.kchunks * SL::count(); ++u) {
                         ptx::mbar_wait(&full[stage], phase);
                         ptx::mbar_arrive(&empty[stage]);
+                        if (PAIR) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&empty[stage]), 1));
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     }
                     ptx::mbar_arrive(&tfull[acc]);
+                    if (PAIR) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tfull[acc]), 1));
                     acc ^= 1;
                     if (acc == 0) aphase ^= 1;
                     continue;

@@ -22,11 +22,12 @@ struct Cfg {
 __global__ void __launch_bounds__(128, 1) bench(Cfg c, int iters, long long* out) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, bar2;
     __shared__ uint32_t slot;
     const int warp = threadIdx.x / 32;
     if (threadIdx.x == 0) {
         ptx::mbar_init(&bar, 1);
+        ptx::mbar_init(&bar2, 1);
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc(&slot, 512);
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(128, 1) bench(Cfg c, int iters, long long* out
             for (int i = 0; i < iters; i += 8) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) ptx::mma_bf16(tmem + ((j * step) & 511), ad, bd, idesc, 1);
+                if (c.nmma == -6) ptx::mma_commit(&bar2);  // a commit every 8 MMAs (nobody waits)
             }
             ptx::mma_commit(&bar);
             ptx::mbar_wait(&bar, 0);
@@ -212,6 +214,61 @@ __global__ void __launch_bounds__(64 + 32 * LW, 1) bench_contend(int iters, long
     }
 }
 
+// Compile-time commit frequency: EVERY MMAs (M = 128, N, K-major, two D tiles) then one tcgen05.commit.
+template <int N, int EVERY>
+__global__ void __launch_bounds__(128, 1) bench_commit(int iters, long long* out) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t bar, bar2;
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bar, 1);
+        ptx::mbar_init(&bar2, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(&slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        const uint32_t s = ptx::smem_u32(smem);
+        constexpr uint32_t idesc = ptx::idesc_bf16(128, N, 0, 0);
+        const uint64_t ad = ptx::smem_desc_sw128(s, 16, 1024);
+        const uint64_t bd = ptx::smem_desc_sw128(s + 65536, 16, 1024);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; i += EVERY) {
+#pragma unroll
+            for (int j = 0; j < EVERY; ++j) ptx::mma_bf16(tmem + (uint32_t)((j & 1) * 256), ad, bd, idesc, 1);
+            if (EVERY < 1024) ptx::mma_commit(&bar2);
+        }
+        ptx::mma_commit(&bar);
+        ptx::mbar_wait(&bar, 0);
+        out[blockIdx.x] = clock64() - t0;
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
+template <int N, int EVERY>
+static void run_commit(long long* d_out) {
+    const int smem = 200 * 1024, iters = 8192;
+    cudaFuncSetAttribute(bench_commit<N, EVERY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    bench_commit<N, EVERY><<<148, 128, smem>>>(iters, d_out);
+    bench_commit<N, EVERY><<<148, 128, smem>>>(iters, d_out);
+    cudaDeviceSynchronize();
+    long long h[148];
+    cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < 148; ++i) avg += h[i];
+    printf("commit N=%3d every %4d MMAs: %7.1f cyc/MMA\n", N, EVERY, avg / 148 / iters);
+}
+
 template <int N, int LW>
 static void run_contend(long long* d_out, long long* d_lds) {
     const int smem = 200 * 1024, iters = 16384;
@@ -283,6 +340,9 @@ int main() {
                 {128, 128, 0, 0, 16, 16, 1024, -1, "lean N=128, 8 D tiles"},
                 {128, 128, 0, 0, 16, 16, 1024, -4, "lean N=128, one D"},
                 {128, 256, 0, 0, 16, 16, 1024, -4, "lean N=256, one D"},
+                {128, 64, 0, 0, 16, 16, 1024, -6, "lean N=64, commit every 8"},
+                {128, 128, 0, 0, 16, 16, 1024, -6, "lean N=128, commit every 8"},
+                {128, 256, 0, 0, 16, 16, 1024, -1, "lean N=256, 2 D"},
             };
             const int smem = 200 * 1024;
             cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -297,6 +357,19 @@ int main() {
                 printf("%-36s %7.1f cyc/MMA\n", c.name, avg / 148 / 8192);
             }
         }
+        run_commit<64, 1024>(d_out);
+        run_commit<64, 32>(d_out);
+        run_commit<64, 16>(d_out);
+        run_commit<64, 8>(d_out);
+        run_commit<64, 4>(d_out);
+        run_commit<64, 2>(d_out);
+        run_commit<128, 1024>(d_out);
+        run_commit<128, 8>(d_out);
+        run_commit<128, 4>(d_out);
+        run_commit<128, 2>(d_out);
+        run_commit<256, 1024>(d_out);
+        run_commit<256, 4>(d_out);
+        run_commit<256, 2>(d_out);
         run_contend<128, 0>(d_out, d_lds);
         run_contend<128, 2>(d_out, d_lds);
         run_contend<128, 4>(d_out, d_lds);
