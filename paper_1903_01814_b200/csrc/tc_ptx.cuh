@@ -164,8 +164,11 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
     return r;
 }
+// Remote (peer-CTA) arrive with the default .release.cta semantics: the hand-offs it signals (TMEM
+// drained after tcgen05.wait::ld + tcgen05.fence::before_thread_sync) need no cluster-scope release;
+// .release.cluster compiles to MEMBAR.ALL.GPU + ERRBAR and made the CTA-pair epilogues ~2x slower.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load executed by both CTAs of a pair; the transaction bytes land on the
 // leader (even) CTA's barrier (peer bit cleared).
