@@ -76,7 +76,7 @@ typedef enum {
 typedef enum { HEX_F32 = 0, HEX_BF16 = 1 } hex_dtype_t;
 typedef enum { HEX_NCHW = 0, HEX_NHWC = 1 } hex_layout_t;
 typedef enum { HEX_PARITY_ODD_LOW = 0, HEX_PARITY_EVEN_LOW = 1 } hex_parity_t;
-typedef enum { HEX_POOL_MAX = 0, HEX_POOL_AVG = 1 } hex_pool_mode_t;
+typedef enum { HEX_POOL_MAX = 0, HEX_POOL_AVG = 1, HEX_POOL_AVG_PAD = 2 } hex_pool_mode_t;
 
 #define HEX_MAX_N 7   /* largest supported kernel size (T = 169) */
 
@@ -185,7 +185,10 @@ HEX_API hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* desc, int32_t pass
  * HEX_POOL_MAX: y = x at the first strict maximum over the in-grid
  * neighbourhood in canonical tap order (A8, A9); argmax_tap
  * (uint8 [B,C,Ho,Wo] in desc layout, may be NULL) receives that tap index.
- * HEX_POOL_AVG: y = in-grid sum / in-grid count (A8). */
+ * HEX_POOL_AVG: y = in-grid sum / in-grid count (A8).
+ * HEX_POOL_AVG_PAD: y = in-grid sum / T(n) -- off-grid cells count as zeros (the
+ *   include-pad alternative to A8; torch's count_include_pad analogue).
+ *   Backward spreads dy / T(n) over the in-grid cells. */
 HEX_API hex_status_t hex_pool2d_fwd(const hex_pool2d_desc_t* desc, const void* x, void* y,
                             uint8_t* argmax_tap, hex_stream_t stream);
 

@@ -175,14 +175,18 @@ def conv2d_bwd(x, w, dy, n: int = 1, s: int = 1, pi: int = 0, need=("dx", "dw", 
     return dx, dw, db
 
 
+_POOL_MODES = {"max": 0, "avg": 1, "avg_pad": 2}
+
+
 def pool2d_fwd(x, n: int = 1, s: int = 1, pi: int = 0, mode: str = "max"):
-    """Returns (y, argmax uint8 or None)."""
+    """Returns (y, argmax uint8 or None). mode: "max", "avg" (A8: in-grid count) or "avg_pad"
+    (include-pad: in-grid sum / T(n))."""
     x = _f64(x)
     B, C, H, W = x.shape
     Ho, Wo, _ = out_shape(H, W, s, pi)
     y = np.empty((B, C, Ho, Wo), dtype=np.float64)
     am = np.empty((B, C, Ho, Wo), dtype=np.uint8) if mode == "max" else None
-    st = lib().oracle_pool2d_fwd(B, C, H, W, n, s, pi, 0 if mode == "max" else 1,
+    st = lib().oracle_pool2d_fwd(B, C, H, W, n, s, pi, _POOL_MODES[mode],
                                  _ptr(x), _ptr(y), _ptr(am))
     if st == 2:
         raise ValueError("invalid argument")
@@ -195,7 +199,7 @@ def pool2d_bwd(dy, argmax, H: int, W: int, n: int = 1, s: int = 1, pi: int = 0, 
     B, C, Ho, Wo = dy.shape
     dx = np.empty((B, C, H, W), dtype=np.float64)
     am = None if argmax is None else np.ascontiguousarray(argmax, dtype=np.uint8)
-    st = lib().oracle_pool2d_bwd(B, C, H, W, n, s, pi, 0 if mode == "max" else 1,
+    st = lib().oracle_pool2d_bwd(B, C, H, W, n, s, pi, _POOL_MODES[mode],
                                  _ptr(dy), _ptr(am), _ptr(dx))
     assert st == 0
     return dx

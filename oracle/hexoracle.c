@@ -318,10 +318,12 @@ int oracle_conv2d_bwd(int B, int Ci, int Co, int H, int W, int n, int s, int pi,
 /* mode 0 = max: max over in-grid neighbours (A8), ties -> first in       */
 /* canonical order (A9); argmax is the tap index.                          */
 /* mode 1 = avg: in-grid sum / in-grid count (A8).                         */
+/* mode 2 = include-pad avg: in-grid sum / T(n), i.e. off-grid cells are   */
+/*          zeros in the average (the alternative reading of A8, f4).      */
 /* ------------------------------------------------------------------ */
 int oracle_pool2d_fwd(int B, int Cc, int H, int W, int n, int s, int pi, int mode,
                       const double* x, double* y, uint8_t* argmax) {
-    if (n < 1 || (mode != 0 && mode != 1)) return 2;
+    if (n < 1 || mode < 0 || mode > 2) return 2;
     int Ho, Wo, T;
     int32_t* map = build_map(H, W, n, s, pi, &Ho, &Wo, &T);
     if (!map) return 1;
@@ -351,7 +353,7 @@ int oracle_pool2d_fwd(int B, int Cc, int H, int W, int n, int s, int pi, int mod
                         acc += xp[m];
                         ++cnt;
                     }
-                    y[oi] = acc / (double)cnt;
+                    y[oi] = acc / (double)(mode == 2 ? T : cnt);
                 }
             }
     free(map);
@@ -359,10 +361,10 @@ int oracle_pool2d_fwd(int B, int Cc, int H, int W, int n, int s, int pi, int mod
 }
 
 /* Pool backward: max routes dy to the argmax cell; avg spreads dy/count
- * over the in-grid neighbourhood (adjoint of the forward). */
+ * (include-pad: dy/T) over the in-grid neighbourhood (adjoint of the forward). */
 int oracle_pool2d_bwd(int B, int Cc, int H, int W, int n, int s, int pi, int mode,
                       const double* dy, const uint8_t* argmax, double* dx) {
-    if (n < 1 || (mode != 0 && mode != 1)) return 2;
+    if (n < 1 || mode < 0 || mode > 2) return 2;
     int Ho, Wo, T;
     int32_t* map = build_map(H, W, n, s, pi, &Ho, &Wo, &T);
     if (!map) return 1;
@@ -381,6 +383,7 @@ int oracle_pool2d_bwd(int B, int Cc, int H, int W, int n, int s, int pi, int mod
                 } else {
                     int cnt = 0;
                     for (int t = 0; t < T; ++t) if (map[o * T + t] >= 0) ++cnt;
+                    if (mode == 2) cnt = T;
                     for (int t = 0; t < T; ++t) {
                         int32_t m = map[o * T + t];
                         if (m >= 0) dxp[m] += g / (double)cnt;

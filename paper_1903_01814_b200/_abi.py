@@ -29,7 +29,7 @@ STATUS_NAMES = {
 }
 F32, BF16 = 0, 1
 NCHW, NHWC = 0, 1
-POOL_MAX, POOL_AVG = 0, 1
+POOL_MAX, POOL_AVG, POOL_AVG_PAD = 0, 1, 2
 MAX_N = 7
 
 

@@ -312,7 +312,7 @@ static hex_status_t pool_geom(const hex_pool2d_desc_t* d, Geom* g) {
                                    d->parity, d->dtype, d->layout);
     if (st != HEX_OK) return st;
     if (d->kernel_size < 1) return HEX_ERR_INVALID_ARG;
-    if (d->mode != HEX_POOL_MAX && d->mode != HEX_POOL_AVG) return HEX_ERR_INVALID_ARG;
+    if (d->mode != HEX_POOL_MAX && d->mode != HEX_POOL_AVG && d->mode != HEX_POOL_AVG_PAD) return HEX_ERR_INVALID_ARG;
     g->B = d->batch; g->H = d->height; g->W = d->width;
     g->n = d->kernel_size; g->s = d->stride; g->parity = d->parity; g->T = hex_taps(d->kernel_size);
     if (g->T > 255) return HEX_ERR_UNSUPPORTED;  // argmax is a uint8 tap index

@@ -70,7 +70,7 @@ __global__ void pool_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, uint
         y[yo] = braw;
         if (am) am[yo] = (uint8_t)best;
     } else {
-        y[yo] = from_f32<T>(sum / (float)cnt);
+        y[yo] = from_f32<T>(sum / (float)(mode == HEX_POOL_AVG_PAD ? g.T : cnt));
     }
 }
 
@@ -190,7 +190,7 @@ __global__ void pool_bwd_kernel(const T* __restrict__ dy, const uint8_t* __restr
                 if (am[yo] == t) acc += to_f32(dy[yo]);
             } else {
                 const int orow = rho + s * Rq;
-                acc += to_f32(dy[yo]) / (float)in_grid_count(g, orow, oc);
+                acc += to_f32(dy[yo]) / (float)(mode == HEX_POOL_AVG_PAD ? g.T : in_grid_count(g, orow, oc));
             }
         }
     }
@@ -839,7 +839,16 @@ static bool dispatch_wide(const PoolArgs& a, cudaStream_t st, bool fwd) {
 }
 
 hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
-    if (use_spec(a) && dispatch_wide(a, st, true)) {
+    if (a.mode == HEX_POOL_AVG_PAD) {  // include-pad average: the generic kernel only
+        const int64_t total = (int64_t)a.g.B * a.C * a.g.Ho * a.g.Wo;
+        const int cf = a.layout == HEX_NHWC;
+        if (a.dtype == HEX_F32)
+            pool_fwd_kernel<float><<<ceil_div(total, 256), 256, 0, st>>>(
+                (const float*)a.x, (float*)a.y, nullptr, a.g, a.C, a.sx, a.sy, a.mode, cf);
+        else
+            pool_fwd_kernel<__nv_bfloat16><<<ceil_div(total, 256), 256, 0, st>>>(
+                (const __nv_bfloat16*)a.x, (__nv_bfloat16*)a.y, nullptr, a.g, a.C, a.sx, a.sy, a.mode, cf);
+    } else if (use_spec(a) && dispatch_wide(a, st, true)) {
     } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_fwd<1, 1>(a, st); else launch_spec_fwd<1, 2>(a, st); }
         else { if (a.g.s == 1) launch_spec_fwd<2, 1>(a, st); else launch_spec_fwd<2, 2>(a, st); }
@@ -866,7 +875,16 @@ hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
 hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
     // The 8-channel gather measured faster than the wide variant for the backward
     // (round 1: 519 vs 577 us on config-5 pool 1); HEXCONV_POOL_WIDE_BWD selects it.
-    if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC") &&
+    if (a.mode == HEX_POOL_AVG_PAD) {
+        const int64_t total = (int64_t)a.g.B * a.C * a.g.H * a.g.W;
+        const int cf = a.layout == HEX_NHWC;
+        if (a.dtype == HEX_F32)
+            pool_bwd_kernel<float><<<ceil_div(total, 256), 256, 0, st>>>(
+                (const float*)a.dy, nullptr, (float*)a.dx, a.g, a.C, a.sx, a.sy, a.mode, cf);
+        else
+            pool_bwd_kernel<__nv_bfloat16><<<ceil_div(total, 256), 256, 0, st>>>(
+                (const __nv_bfloat16*)a.dy, nullptr, (__nv_bfloat16*)a.dx, a.g, a.C, a.sx, a.sy, a.mode, cf);
+    } else if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC") &&
         !getenv("HEXCONV_POOL_PIXEL_BWD")) {
         const int C8 = a.C / 8;
         dim3 grid(ceil_div((int64_t)a.g.Wo * C8, 256), (a.g.H + 1) / 2, a.g.B);

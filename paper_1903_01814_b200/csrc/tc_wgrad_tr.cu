@@ -387,7 +387,8 @@ bool tc_wgrad_tr_supported(const Geom& g, int Cin, int Cout) {
     if (g.B > 65535) return false;
     const double fill_c = (double)((g.W + 1) / 2) / (ceil_div((g.W + 1) / 2, TR_JB) * TR_JB);
     const double fill_r = (double)g.H / (ceil_div(g.H, tr_rb()) * tr_rb());
-    if (fill_c * fill_r < 0.85) return false;
+    const double min_fill = getenv("HEXCONV_WG_TR_MINFILL") ? atof(getenv("HEXCONV_WG_TR_MINFILL")) : 0.85;
+    if (fill_c * fill_r < min_fill) return false;
     if (tr_smem_bytes(g.n, tr_rb(), 2) > TR_SMEM_MAX) return false;
     return tr_encode() != nullptr;
 }

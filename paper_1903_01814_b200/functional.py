@@ -174,9 +174,12 @@ def gather_map(H: int, W: int, n: int, stride: int = 1, parity: int = 0, device=
 
 
 # ------------------------------------------------------------------ pooling
+_POOL_MODES = {"max": A.POOL_MAX, "avg": A.POOL_AVG, "avg_pad": A.POOL_AVG_PAD}
+
+
 def pool_desc(B, C, H, W, n, stride, parity, dtype, layout, mode) -> A.PoolDesc:
-    return A.PoolDesc(B, C, H, W, n, stride, parity, _DTYPES[dtype], _LAYOUTS[layout],
-                      A.POOL_MAX if mode == "max" else A.POOL_AVG)
+    """mode: "max", "avg" (in-grid count, A8) or "avg_pad" (include-pad: divide by T(n))."""
+    return A.PoolDesc(B, C, H, W, n, stride, parity, _DTYPES[dtype], _LAYOUTS[layout], _POOL_MODES[mode])
 
 
 def pool2d_fwd(x, n: int = 1, stride: int = 1, parity: int = 0, mode: str = "max", layout: str = "NCHW",
@@ -254,5 +257,5 @@ def hex_max_pool2d(x, n=1, stride=1, parity=0, layout="NCHW"):
     return HexPool2dFn.apply(x, n, stride, parity, "max", layout)
 
 
-def hex_avg_pool2d(x, n=1, stride=1, parity=0, layout="NCHW"):
-    return HexPool2dFn.apply(x, n, stride, parity, "avg", layout)
+def hex_avg_pool2d(x, n=1, stride=1, parity=0, layout="NCHW", count_include_pad=False):
+    return HexPool2dFn.apply(x, n, stride, parity, "avg_pad" if count_include_pad else "avg", layout)

@@ -177,7 +177,7 @@ def _pool_case(F, oracle, pi, n, s, H, W, B, C, dtype, layout, mode, seed, data=
     assert rel(to_np(dx, layout), dxr) <= tol, ("pool bwd", mode, pi, n, s, H, W)
 
 
-@pytest.mark.parametrize("mode", ["max", "avg"])
+@pytest.mark.parametrize("mode", ["max", "avg", "avg_pad"])
 @pytest.mark.parametrize("pi", [0, 1])
 def test_pool_envelope(F, oracle, mode, pi):
     for n in (1, 2, 3):
@@ -186,7 +186,7 @@ def test_pool_envelope(F, oracle, mode, pi):
                 _pool_case(F, oracle, pi, n, s, H, W, 2, 3, torch.float32, "NCHW", mode, 200 + k)
 
 
-@pytest.mark.parametrize("mode", ["max", "avg"])
+@pytest.mark.parametrize("mode", ["max", "avg", "avg_pad"])
 def test_pool_bf16_nhwc_vectorised(F, oracle, mode):
     for pi, n, s in [(0, 1, 2), (1, 1, 1), (0, 2, 3), (1, 2, 2)]:
         for C in (8, 16, 3, 32, 96):

@@ -394,6 +394,8 @@ def torch_hexpool(x, n, s, pi, mode):
         u = u[:, :, mask]
         if mode == "max":
             outs.append(u.max(dim=2).values)
+        elif mode == "avg_pad":  # zero padding counted: divide by the number of taps
+            outs.append(u.sum(2) / len(offs))
         else:
             ones = F.pad(torch.ones(1, 1, H, W, dtype=x.dtype), (n, n, n, n))
             cnt = F.unfold(ones, 2 * n + 1).view(1, 1, -1, H, W)[:, :, mask].sum(2)
@@ -407,7 +409,7 @@ def torch_hexpool(x, n, s, pi, mode):
 
 
 @pytest.mark.parametrize("pi", [0, 1])
-@pytest.mark.parametrize("mode", ["max", "avg"])
+@pytest.mark.parametrize("mode", ["max", "avg", "avg_pad"])
 def test_p8_pool_equals_unfold(oracle, mode, pi):
     for n in (1, 2):
         for s in (1, 2, 3):
@@ -596,9 +598,27 @@ def test_p17_pool_pins(oracle):
             assert y[0, 0, r, c] == max(rr for (rr, cc) in phys_neigh(5, 5, r, c, 1))
 
 
+def test_p17_include_pad_avg(oracle):
+    # include-pad average (f4): all-ones input gives in-grid count / T(n) -- the in-grid count of
+    # every window read off the gather map, T(n) the closed form 3n(n+1)+1 (P1); interior = 1
+    for n, s, pi in [(1, 1, 0), (2, 1, 1), (1, 2, 0), (2, 3, 1)]:
+        y, _ = oracle.pool2d_fwd(np.ones((1, 1, 9, 10)), n=n, s=s, pi=pi, mode="avg_pad")
+        m = oracle.gather_map(9, 10, n, s, pi)
+        T = 3 * n * (n + 1) + 1
+        np.testing.assert_allclose(y[0, 0], (m >= 0).sum(-1) / T, rtol=0, atol=1e-15)
+        assert y.max() == 1.0
+    # = in-grid average x in-grid count / T on random data
+    xn = rand((2, 3, 11, 12), 120)
+    for n, s in [(1, 1), (2, 2)]:
+        ya, _ = oracle.pool2d_fwd(xn, n=n, s=s, mode="avg")
+        yp, _ = oracle.pool2d_fwd(xn, n=n, s=s, mode="avg_pad")
+        cnt = (oracle.gather_map(11, 12, n, s) >= 0).sum(-1)
+        np.testing.assert_allclose(yp, ya * cnt / (3 * n * (n + 1) + 1), rtol=1e-14, atol=1e-15)
+
+
 def test_p17_pool_bwd_fd(oracle):
     rng = np.random.default_rng(110)
-    for mode in ("max", "avg"):
+    for mode in ("max", "avg", "avg_pad"):
         for n, s in [(1, 1), (1, 2), (2, 2)]:
             x = rng.standard_normal((1, 2, 7, 8))
             y, am = oracle.pool2d_fwd(x, n=n, s=s, mode=mode)
