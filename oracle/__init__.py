@@ -55,6 +55,9 @@ def lib():
         L.oracle_conv2d_fwd.argtypes = [ctypes.c_int] * 8 + [ctypes.c_void_p] * 4
         L.oracle_conv2d_bwd.argtypes = [ctypes.c_int] * 8 + [ctypes.c_void_p] * 6
         L.oracle_pool2d_fwd.argtypes = [ctypes.c_int] * 8 + [ctypes.c_void_p] * 3
+        L.oracle_conv3d_out_depth.argtypes = [ctypes.c_int] * 3
+        L.oracle_conv3d_fwd.argtypes = [ctypes.c_int] * 11 + [ctypes.c_void_p] * 4
+        L.oracle_conv3d_bwd.argtypes = [ctypes.c_int] * 11 + [ctypes.c_void_p] * 6
         L.oracle_pool2d_bwd.argtypes = [ctypes.c_int] * 8 + [ctypes.c_void_p] * 3
         L.oracle_conv2d_bwd_weight_at.argtypes = [ctypes.c_int] * 6 + [
             ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
@@ -170,6 +173,53 @@ def conv2d_bwd(x, w, dy, n: int = 1, s: int = 1, pi: int = 0, need=("dx", "dw", 
     dw = np.empty_like(w) if "dw" in need else None
     db = np.empty((Co,), dtype=np.float64) if "db" in need else None
     st = lib().oracle_conv2d_bwd(B, Ci, Co, H, W, n, s, pi, _ptr(x), _ptr(w), _ptr(dy),
+                                 _ptr(dx), _ptr(dw), _ptr(db))
+    assert st == 0
+    return dx, dw, db
+
+
+def conv3d_out_depth(D: int, kd: int, sd: int) -> int:
+    """Do = (D-1)/sd + 1 (depth centres 0, sd, 2sd, ...; kd odd), hexoracle.c."""
+    Do = lib().oracle_conv3d_out_depth(D, kd, sd)
+    if Do < 0:
+        raise ValueError("kernel depth must be odd and >= 1, depth stride >= 1")
+    return Do
+
+
+def conv3d_fwd(x, w, bias=None, n: int = 1, s: int = 1, sd: int = 1, pi: int = 0) -> np.ndarray:
+    """3-D hex conv: x [B,Ci,D,H,W], w [Co,Ci,kd,T] -> y [B,Co,Do,Ho,Wo] (fp64)."""
+    x = _f64(x)
+    w = _f64(w)
+    B, Ci, D, H, W = x.shape
+    Co, Ci2, kd, T = w.shape
+    if Ci2 != Ci:
+        raise ValueError("channel mismatch")
+    if T != num_taps(n):
+        raise ValueError("weight tap count does not match kernel size")
+    Do = conv3d_out_depth(D, kd, sd)
+    Ho, Wo, _ = out_shape(H, W, s, pi)
+    b = None if bias is None else _f64(bias)
+    y = np.empty((B, Co, Do, Ho, Wo), dtype=np.float64)
+    st = lib().oracle_conv3d_fwd(B, Ci, Co, D, H, W, n, kd, s, sd, pi, _ptr(x), _ptr(w), _ptr(b), _ptr(y))
+    assert st == 0
+    return y
+
+
+def conv3d_bwd(x, w, dy, n: int = 1, s: int = 1, sd: int = 1, pi: int = 0, need=("dx", "dw", "db")):
+    """(dx, dw, dbias): the literal adjoint of conv3d_fwd."""
+    x = _f64(x)
+    w = _f64(w)
+    dy = _f64(dy)
+    B, Ci, D, H, W = x.shape
+    Co, _, kd, _ = w.shape
+    Do = conv3d_out_depth(D, kd, sd)
+    Ho, Wo, _ = out_shape(H, W, s, pi)
+    if dy.shape != (B, Co, Do, Ho, Wo):
+        raise ValueError("shape mismatch")
+    dx = np.empty_like(x) if "dx" in need else None
+    dw = np.empty_like(w) if "dw" in need else None
+    db = np.empty((Co,), dtype=np.float64) if "db" in need else None
+    st = lib().oracle_conv3d_bwd(B, Ci, Co, D, H, W, n, kd, s, sd, pi, _ptr(x), _ptr(w), _ptr(dy),
                                  _ptr(dx), _ptr(dw), _ptr(db))
     assert st == 0
     return dx, dw, db

@@ -395,6 +395,124 @@ int oracle_pool2d_bwd(int B, int Cc, int H, int W, int n, int s, int pi, int mod
     return 0;
 }
 
+/* ------------------------------------------------------------------ */
+/* 3-D hexagonal convolution (Sec. 2 "Software          */
+/* Functionalities": "hexagonal layout in the x-y-plane while data points */
+/* along the z-axis are assumed to be equidistant").     */
+/* The kernel is a hexagonal kernel of size n in every one of kd depth    */
+/* slices, with independent weights w[co][ci][kz][t] (t canonical, A2);   */
+/* kd odd, the depth window centred on the output slice (kz = dz +        */
+/* (kd-1)/2), zero padding in depth (A4 along z); depth stride sd takes   */
+/* centres 0, sd, 2sd, ... (Do = (D-1)/sd + 1); in-plane lattice as the   */
+/* 2-D convolution (A5, A6).  Layout x[b][ci][z][r][c].                   */
+/* y[b][co][zo][R][C] = bias[co] + sum_ci sum_kz sum_t                    */
+/*                      w[co][ci][kz][t] * x[b][ci][sd*zo+kz-(kd-1)/2][nb_t] */
+/* ------------------------------------------------------------------ */
+int oracle_conv3d_out_depth(int D, int kd, int sd) {
+    if (D < 1 || kd < 1 || (kd & 1) == 0 || sd < 1) return -1;
+    return (D - 1) / sd + 1;
+}
+
+int oracle_conv3d_fwd(int B, int Ci, int Co, int D, int H, int W, int n, int kd, int s, int sd, int pi,
+                      const double* x, const double* w, const double* bias, double* y) {
+    const int Do = oracle_conv3d_out_depth(D, kd, sd);
+    if (Do < 0) return 2;
+    int Ho, Wo, T;
+    int32_t* map = build_map(H, W, n, s, pi, &Ho, &Wo, &T);
+    if (!map) return 1;
+    const int64_t HW = (int64_t)H * W, HWo = (int64_t)Ho * Wo;
+    const int pd = (kd - 1) / 2;
+    #pragma omp parallel for collapse(2) schedule(static)
+    for (int b = 0; b < B; ++b)
+        for (int co = 0; co < Co; ++co)
+            for (int zo = 0; zo < Do; ++zo)
+                for (int64_t o = 0; o < HWo; ++o) {
+                    double acc = 0.0;
+                    for (int ci = 0; ci < Ci; ++ci)
+                        for (int kz = 0; kz < kd; ++kz) {
+                            const int z = sd * zo + kz - pd;
+                            if (z < 0 || z >= D) continue;
+                            const double* xs = x + (((int64_t)b * Ci + ci) * D + z) * HW;
+                            const double* ws = w + (((int64_t)co * Ci + ci) * kd + kz) * T;
+                            for (int t = 0; t < T; ++t) {
+                                const int32_t m = map[o * T + t];
+                                if (m >= 0) acc += ws[t] * xs[m];
+                            }
+                        }
+                    y[(((int64_t)b * Co + co) * Do + zo) * HWo + o] = (bias ? bias[co] : 0.0) + acc;
+                }
+    free(map);
+    return 0;
+}
+
+/* Backward of the 3-D convolution: the literal adjoint (scatter over every
+ * (output, depth tap, tap) that touched an in-grid, in-depth input cell). */
+int oracle_conv3d_bwd(int B, int Ci, int Co, int D, int H, int W, int n, int kd, int s, int sd, int pi,
+                      const double* x, const double* w, const double* dy,
+                      double* dx, double* dw, double* dbias) {
+    const int Do = oracle_conv3d_out_depth(D, kd, sd);
+    if (Do < 0) return 2;
+    int Ho, Wo, T;
+    int32_t* map = build_map(H, W, n, s, pi, &Ho, &Wo, &T);
+    if (!map) return 1;
+    const int64_t HW = (int64_t)H * W, HWo = (int64_t)Ho * Wo;
+    const int pd = (kd - 1) / 2;
+    if (dx) {
+        #pragma omp parallel for collapse(2) schedule(static)
+        for (int b = 0; b < B; ++b)
+            for (int ci = 0; ci < Ci; ++ci) {
+                double* dxp = dx + ((int64_t)b * Ci + ci) * D * HW;
+                for (int64_t i = 0; i < (int64_t)D * HW; ++i) dxp[i] = 0.0;
+                for (int co = 0; co < Co; ++co)
+                    for (int zo = 0; zo < Do; ++zo)
+                        for (int kz = 0; kz < kd; ++kz) {
+                            const int z = sd * zo + kz - pd;
+                            if (z < 0 || z >= D) continue;
+                            const double* ws = w + (((int64_t)co * Ci + ci) * kd + kz) * T;
+                            for (int64_t o = 0; o < HWo; ++o) {
+                                const double g = dy[(((int64_t)b * Co + co) * Do + zo) * HWo + o];
+                                for (int t = 0; t < T; ++t) {
+                                    const int32_t m = map[o * T + t];
+                                    if (m >= 0) dxp[(int64_t)z * HW + m] += ws[t] * g;
+                                }
+                            }
+                        }
+            }
+    }
+    if (dw) {
+        #pragma omp parallel for collapse(2) schedule(static)
+        for (int co = 0; co < Co; ++co)
+            for (int ci = 0; ci < Ci; ++ci)
+                for (int kz = 0; kz < kd; ++kz) {
+                    double* dwp = dw + (((int64_t)co * Ci + ci) * kd + kz) * T;
+                    for (int t = 0; t < T; ++t) dwp[t] = 0.0;
+                    for (int b = 0; b < B; ++b)
+                        for (int zo = 0; zo < Do; ++zo) {
+                            const int z = sd * zo + kz - pd;
+                            if (z < 0 || z >= D) continue;
+                            const double* xs = x + (((int64_t)b * Ci + ci) * D + z) * HW;
+                            for (int64_t o = 0; o < HWo; ++o) {
+                                const double g = dy[(((int64_t)b * Co + co) * Do + zo) * HWo + o];
+                                for (int t = 0; t < T; ++t) {
+                                    const int32_t m = map[o * T + t];
+                                    if (m >= 0) dwp[t] += g * xs[m];
+                                }
+                            }
+                        }
+                }
+    }
+    if (dbias) {
+        for (int co = 0; co < Co; ++co) {
+            double acc = 0.0;
+            for (int b = 0; b < B; ++b)
+                for (int64_t i = 0; i < (int64_t)Do * HWo; ++i) acc += dy[((int64_t)b * Co + co) * Do * HWo + i];
+            dbias[co] = acc;
+        }
+    }
+    free(map);
+    return 0;
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     extern int omp_get_max_threads(void);
