@@ -178,6 +178,51 @@ HEX_API hex_status_t hex_conv2d_fwd_maxpool(const hex_conv2d_desc_t* desc, const
  * pass: 0 fwd, 1 bwd_data, 2 bwd_weight. */
 HEX_API hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* desc, int32_t pass, int32_t* algo);
 
+/* ---------------------------------------------------------------- 3-D convolution */
+
+/* 3-D hexagonal convolution (Sec. 2 "Software Functionalities":
+ * "the input data is expected to have a hexagonal layout in the x-y-plane while
+ * data points along the z-axis are assumed to be equidistant").
+ * Kernel: the hexagonal kernel of size n in each of kd (odd) depth slices with
+ * independent weights w[Cout][Cin][kd][T(n)] (canonical taps, A2),
+ * centred in depth; zero padding in depth; output depth slices are the centres
+ * 0, sd, 2sd, ... (Do = (D-1)/sd + 1); the in-plane lattice is the 2-D one.
+ *   y[b][co][zo][R][C] = bias[co] + sum_ci sum_kz sum_t w[co][ci][kz][t] *
+ *                        x[b][ci][sd*zo + kz - (kd-1)/2][centre(R,C) + off_t]
+ * layout HEX_NCHW means NCDHW, HEX_NHWC means NDHWC (channels innermost).
+ * Implementation: the kd depth taps become input channels of one 2-D
+ * convolution over B*Do images (x' = depth-unfolded input, Cin' = kd*Cin, ordered
+ * (kz, ci)), so every 2-D path applies -- the tcgen05 kernels for bf16 NHWC
+ * with Cin'/Cout multiples of 64.  The workspace holds x' (or dx'), the
+ * reordered weights and the 2-D call's own workspace.
+ * Errors: as the 2-D calls, plus HEX_ERR_INVALID_ARG for even / non-positive
+ * kernel_depth or depth_stride < 1, HEX_ERR_SHAPE for depth < 1. */
+typedef struct {
+    int32_t batch, in_channels, out_channels, depth, height, width;
+    int32_t kernel_size;  /* in-plane n >= 0                       */
+    int32_t kernel_depth; /* kd >= 1, odd                          */
+    int32_t stride;       /* in-plane s >= 1                       */
+    int32_t depth_stride; /* sd >= 1                               */
+    int32_t parity, dtype, layout;
+} hex_conv3d_desc_t;
+
+/* *Do, *Ho, *Wo (host) of the output volume. */
+HEX_API hex_status_t hex_conv3d_output_shape(const hex_conv3d_desc_t* desc, int32_t* Do, int32_t* Ho, int32_t* Wo);
+/* Workspace bytes of pass 0 = fwd, 1 = bwd_data, 2 = bwd_weight. */
+HEX_API hex_status_t hex_conv3d_workspace_size(const hex_conv3d_desc_t* desc, int32_t pass, size_t* bytes);
+/* y [B,Cout,Do,Ho,Wo] (desc layout) = conv3d(x) (+ bias, optional fused ReLU). */
+HEX_API hex_status_t hex_conv3d_fwd(const hex_conv3d_desc_t* desc, const void* x, const void* w, const float* bias,
+                                    int32_t fuse_relu, void* y, void* ws, size_t ws_bytes, hex_stream_t stream);
+/* dx [B,Cin,D,H,W] = adjoint of the forward applied to dy (overwritten; depth taps
+ * summed in ascending kz, deterministic). */
+HEX_API hex_status_t hex_conv3d_bwd_data(const hex_conv3d_desc_t* desc, const void* dy, const void* w, void* dx,
+                                         void* ws, size_t ws_bytes, hex_stream_t stream);
+/* dw (fp32 [Cout][Cin][kd][T]) and dbias (fp32 [Cout], NULL ok); accumulate != 0
+ * adds to them. */
+HEX_API hex_status_t hex_conv3d_bwd_weight(const hex_conv3d_desc_t* desc, const void* x, const void* dy, float* dw,
+                                           float* dbias, int32_t accumulate, void* ws, size_t ws_bytes,
+                                           hex_stream_t stream);
+
 /* ---------------------------------------------------------------- pooling */
 
 /* Pooling (the sub-convolutions are replaced by pooling

@@ -47,6 +47,12 @@ class ConvDesc(ctypes.Structure):
         "kernel_size", "stride", "parity", "dtype", "layout")]
 
 
+class Conv3dDesc(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int32) for f in (
+        "batch", "in_channels", "out_channels", "depth", "height", "width",
+        "kernel_size", "kernel_depth", "stride", "depth_stride", "parity", "dtype", "layout")]
+
+
 class PoolDesc(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int32) for f in (
         "batch", "channels", "height", "width", "kernel_size", "stride",
@@ -62,6 +68,7 @@ _i32p = ctypes.POINTER(ctypes.c_int32)
 _szp = ctypes.POINTER(ctypes.c_size_t)
 _CDP = ctypes.POINTER(ConvDesc)
 _PDP = ctypes.POINTER(PoolDesc)
+_C3P = ctypes.POINTER(Conv3dDesc)
 
 _SIGS = {
     "hex_num_taps": (_i32, [_i32]),
@@ -78,6 +85,11 @@ _SIGS = {
     "hex_conv2d_fwd_maxpool": (_i32, [_CDP, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp]),
     "hex_conv2d_bwd_data": (_i32, [_CDP, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "hex_conv2d_bwd_weight": (_i32, [_CDP, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
+    "hex_conv3d_output_shape": (_i32, [_C3P, _i32p, _i32p, _i32p]),
+    "hex_conv3d_workspace_size": (_i32, [_C3P, _i32, _szp]),
+    "hex_conv3d_fwd": (_i32, [_C3P, _vp, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
+    "hex_conv3d_bwd_data": (_i32, [_C3P, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "hex_conv3d_bwd_weight": (_i32, [_C3P, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
     "hex_pool2d_fwd": (_i32, [_PDP, _vp, _vp, _vp, _vp]),
     "hex_pool2d_bwd": (_i32, [_PDP, _vp, _vp, _vp, _vp]),
     "hex_head_workspace_size": (_sz, [_i32, _i32, _i32]),

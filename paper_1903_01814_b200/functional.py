@@ -164,6 +164,124 @@ def conv2d_bwd_weight(x, dy, n: int = 1, stride: int = 1, parity: int = 0, layou
     return dw, (dbias if with_bias else None)
 
 
+# ------------------------------------------------------------------ 3-D convolution
+_LAYOUTS3 = {"NCDHW": A.NCHW, "NDHWC": A.NHWC}
+
+
+def _dims3(x, layout):
+    if layout == "NCDHW":
+        B, C, D, H, W = x.shape
+    elif layout == "NDHWC":
+        B, D, H, W, C = x.shape
+    else:
+        raise ValueError(f"unknown 3-D layout {layout}")
+    return B, C, D, H, W
+
+
+def _shape3(layout, B, C, D, H, W):
+    return (B, C, D, H, W) if layout == "NCDHW" else (B, D, H, W, C)
+
+
+def conv3d_desc(B, Cin, Cout, D, H, W, n, kd, stride, depth_stride, parity, dtype, layout) -> A.Conv3dDesc:
+    return A.Conv3dDesc(B, Cin, Cout, D, H, W, n, kd, stride, depth_stride, parity, _DTYPES[dtype], _LAYOUTS3[layout])
+
+
+def conv3d_output_shape(desc):
+    Do, Ho, Wo = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    A.check(A.lib().hex_conv3d_output_shape(ctypes.byref(desc), ctypes.byref(Do), ctypes.byref(Ho),
+                                            ctypes.byref(Wo)), "hex_conv3d_output_shape")
+    return Do.value, Ho.value, Wo.value
+
+
+def _workspace3(desc, pass_id, device):
+    nbytes = ctypes.c_size_t()
+    A.check(A.lib().hex_conv3d_workspace_size(ctypes.byref(desc), pass_id, ctypes.byref(nbytes)),
+            "hex_conv3d_workspace_size")
+    return torch.empty(max(nbytes.value, 1), dtype=torch.uint8, device=device), nbytes.value
+
+
+def conv3d_fwd(x, w, bias=None, n: int = 1, stride: int = 1, depth_stride: int = 1, parity: int = 0,
+               relu: bool = False, layout: str = "NCDHW", out=None):
+    """3-D hex conv: w [Cout, Cin, kd, T]; y = conv3d(x, w) + bias (ReLU optional)."""
+    _check_cuda(x, w, bias, out)
+    B, Cin, D, H, W = _dims3(x, layout)
+    Cout, Ci2, kd, T = w.shape
+    if Ci2 != Cin:
+        raise ValueError("channel mismatch")
+    if T != A.num_taps(n):
+        raise ValueError("weight tap count does not match kernel size")
+    if w.dtype != x.dtype:
+        raise ValueError("x and w must share a dtype")
+    d = conv3d_desc(B, Cin, Cout, D, H, W, n, kd, stride, depth_stride, parity, x.dtype, layout)
+    Do, Ho, Wo = conv3d_output_shape(d)
+    if out is None:
+        out = torch.empty(_shape3(layout, B, Cout, Do, Ho, Wo), dtype=x.dtype, device=x.device)
+    ws, nb = _workspace3(d, 0, x.device)
+    A.check(A.lib().hex_conv3d_fwd(ctypes.byref(d), _ptr(x), _ptr(w), _ptr(bias), int(relu), _ptr(out),
+                                   _ptr(ws), nb, _stream()), "hex_conv3d_fwd")
+    return out
+
+
+def conv3d_bwd_data(dy, w, in_dhw, n: int = 1, stride: int = 1, depth_stride: int = 1, parity: int = 0,
+                    layout: str = "NCDHW", out=None):
+    _check_cuda(dy, w, out)
+    B, Cout = _dims3(dy, layout)[:2]
+    Co2, Cin, kd, T = w.shape
+    D, H, W = in_dhw
+    if Co2 != Cout:
+        raise ValueError("channel mismatch")
+    d = conv3d_desc(B, Cin, Cout, D, H, W, n, kd, stride, depth_stride, parity, dy.dtype, layout)
+    if out is None:
+        out = torch.empty(_shape3(layout, B, Cin, D, H, W), dtype=dy.dtype, device=dy.device)
+    ws, nb = _workspace3(d, 1, dy.device)
+    A.check(A.lib().hex_conv3d_bwd_data(ctypes.byref(d), _ptr(dy), _ptr(w), _ptr(out), _ptr(ws), nb, _stream()),
+            "hex_conv3d_bwd_data")
+    return out
+
+
+def conv3d_bwd_weight(x, dy, kd: int, n: int = 1, stride: int = 1, depth_stride: int = 1, parity: int = 0,
+                      layout: str = "NCDHW", with_bias: bool = True, dw=None, dbias=None, accumulate: bool = False):
+    """(dw fp32 [Cout, Cin, kd, T], dbias fp32 [Cout] or None)."""
+    _check_cuda(x, dy, dw, dbias)
+    B, Cin, D, H, W = _dims3(x, layout)
+    Cout = _dims3(dy, layout)[1]
+    T = A.num_taps(n)
+    d = conv3d_desc(B, Cin, Cout, D, H, W, n, kd, stride, depth_stride, parity, x.dtype, layout)
+    if dw is None:
+        dw = torch.empty((Cout, Cin, kd, T), dtype=torch.float32, device=x.device)
+    if with_bias and dbias is None:
+        dbias = torch.empty((Cout,), dtype=torch.float32, device=x.device)
+    ws, nb = _workspace3(d, 2, x.device)
+    A.check(A.lib().hex_conv3d_bwd_weight(ctypes.byref(d), _ptr(x), _ptr(dy), _ptr(dw),
+                                          _ptr(dbias if with_bias else None), int(accumulate), _ptr(ws), nb,
+                                          _stream()), "hex_conv3d_bwd_weight")
+    return dw, (dbias if with_bias else None)
+
+
+class HexConv3dFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, bias, n, stride, depth_stride, parity, layout):
+        ctx.save_for_backward(x, w)
+        ctx.cfg = (n, stride, depth_stride, parity, layout, bias is not None)
+        return conv3d_fwd(x, w, bias, n, stride, depth_stride, parity, False, layout)
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, w = ctx.saved_tensors
+        n, stride, depth_stride, parity, layout, has_bias = ctx.cfg
+        gy = gy.contiguous()
+        B, Cin, D, H, W = _dims3(x, layout)
+        dx = conv3d_bwd_data(gy, w, (D, H, W), n, stride, depth_stride, parity, layout) \
+            if ctx.needs_input_grad[0] else None
+        dw, db = conv3d_bwd_weight(x, gy, w.shape[2], n, stride, depth_stride, parity, layout, with_bias=has_bias)
+        return dx, dw.to(w.dtype), db, None, None, None, None, None
+
+
+def hex_conv3d(x, w, bias=None, n=1, stride=1, depth_stride=1, parity=0, layout="NCDHW"):
+    """Autograd 3-D hex convolution (hexagonal x-y, equidistant z)."""
+    return HexConv3dFn.apply(x, w, bias, n, stride, depth_stride, parity, layout)
+
+
 def gather_map(H: int, W: int, n: int, stride: int = 1, parity: int = 0, device="cuda"):
     Ho, Wo, _ = A.output_shape(H, W, stride, parity)
     T = A.num_taps(n)
