@@ -309,6 +309,27 @@ def secondary_measurements(dev, peak_tf, peak_gbs):
         if f:
             c2[name]["tflops"] = f / (ms / 1e3) / 1e12
     out["c2_16to32_48x48_f32"] = c2
+    del x, y, gy
+
+    # ---- f2: 3-D hex conv (hex x-y, equidistant z), bf16 NDHWC, tcgen05 via depth unfold.
+    # Synthetic shape (no paper workload): 16 volumes x 16 slices x 64x64, 64 -> 128 channels, n = 1, kd = 3.
+    B, D, H, W, C, Co, kd, n = 16, 16, 64, 64, 64, 128, 3, 1
+    T = F.num_taps(n)
+    x = torch.randn(B, D, H, W, C, device=dev).to(torch.bfloat16)
+    g = torch.randn(B, D, H, W, Co, device=dev).to(torch.bfloat16)
+    w = (torch.randn(Co, C, kd, T, device=dev) / (C * kd * T) ** 0.5).to(torch.bfloat16)
+    # valid work: in-grid taps x in-range depth taps (kd*D - 2 boundary slices for kd = 3, sd = 1)
+    fl = 2.0 * B * vt(H, W, n) * (kd * D - 2) * C * Co
+    c3d = {}
+    for name, fn in (("fwd", lambda: F.conv3d_fwd(x, w, None, n=n, layout="NDHWC")),
+                     ("dgrad", lambda: F.conv3d_bwd_data(g, w, (D, H, W), n=n, layout="NDHWC")),
+                     ("wgrad", lambda: F.conv3d_bwd_weight(x, g, kd, n=n, layout="NDHWC"))):
+        ms = _events_ms(fn, 5)
+        tf = fl / (ms / 1e3) / 1e12
+        c3d[name] = {"us": ms * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak_tf}
+    c3d["note"] = ("depth taps unfolded into channels (x' = 3x the input, HBM-bound copy) then one 2-D "
+                   "tcgen05 conv over B*D images; FLOPs count in-range depth taps only")
+    out["conv3d_64to128_16x64x64_kd3_bf16"] = c3d
     return out
 
 
