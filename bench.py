@@ -327,8 +327,9 @@ def secondary_measurements(dev, peak_tf, peak_gbs):
         ms = _events_ms(fn, 5)
         tf = fl / (ms / 1e3) / 1e12
         c3d[name] = {"us": ms * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak_tf}
-    c3d["note"] = ("depth taps unfolded into channels (x' = 3x the input, HBM-bound copy) then one 2-D "
-                   "tcgen05 conv over B*D images; FLOPs count in-range depth taps only")
+    c3d["note"] = ("fwd / dgrad: depth taps inside the K loop of the tcgen05 tap-reuse kernel (out-of-volume "
+                   "slices are zero-fill boxes); wgrad: depth taps unfolded into channels then one 2-D tcgen05 "
+                   "wgrad over B*D images; FLOPs count in-range depth taps only")
     out["conv3d_64to128_16x64x64_kd3_bf16"] = c3d
     return out
 

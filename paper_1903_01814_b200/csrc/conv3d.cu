@@ -13,10 +13,12 @@
 // multiples of 64, and the CUDA-core kernels everything else.  The unfold and
 // fold are HBM-bound gathers (16-byte vectors for NDHWC when Cin % 8 == 0).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "geometry.cuh"
 #include "kernels.h"
 
 namespace hexconv {
@@ -161,6 +163,23 @@ __global__ void swap_mid_kernel(const T* __restrict__ src, T* __restrict__ dst, 
     }
 }
 
+// tcgen05 path weights: tr = 0: wp[kz*T + t][co][ci] = w[co][ci][kz][t];
+// tr = 1 (bwd-data as a forward): wp[kz*T + t][ci][co] = w[co][ci][kd-1-kz][T-1-t]
+__global__ void pack3d_kernel(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wp, int Co, int Ci,
+                              int kd, int Tn, int tr) {
+    const int64_t total = (int64_t)Co * Ci * kd * Tn;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(i % Tn);
+        int64_t q = i / Tn;
+        const int kz = (int)(q % kd);
+        q /= kd;
+        const int ci = (int)(q % Ci);
+        const int co = (int)(q / Ci);
+        if (!tr) wp[(((int64_t)kz * Tn + t) * Co + co) * Ci + ci] = w[i];
+        else wp[(((int64_t)(kd - 1 - kz) * Tn + (Tn - 1 - t)) * Ci + ci) * Co + co] = w[i];
+    }
+}
+
 inline int grid_for(int64_t total) {
     const int64_t b = (total + 255) / 256;
     return (int)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
@@ -230,6 +249,18 @@ size_t out_vol_bytes(const hex_conv3d_desc_t* d, const C3& g) {
     return (size_t)g.B * g.Do * g.Co * Ho * Wo * elt(d->dtype);
 }
 
+// the depth-in-K-loop tcgen05 path: bf16 NDHWC, in-plane stride 1, channels multiples of 64
+bool c3_tc_ok(const hex_conv3d_desc_t* d, int Cin, int Cout, int Dout, Geom* g) {
+    if (d->dtype != HEX_BF16 || d->layout != HEX_NHWC || d->stride != 1 || Cin % 64 || Cout % 64) return false;
+    g->B = d->batch; g->H = d->height; g->W = d->width;
+    g->n = d->kernel_size; g->s = 1; g->parity = d->parity; g->T = hex_num_taps(d->kernel_size);
+    int32_t po;
+    if (hex_output_shape(g->H, g->W, 1, g->parity, &g->Ho, &g->Wo, &po) != HEX_OK) return false;
+    return tc_conv3d_supported(*g, Cin, Cout, Dout);
+}
+
+bool a16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
 hex_status_t wperm(const void* w, void* wu, const C3& g, int Tn, int dtype, cudaStream_t st) {
     const int64_t total = (int64_t)g.Co * g.Ci * g.kd * Tn;
     if (dtype == HEX_F32)
@@ -289,6 +320,20 @@ hex_status_t hex_conv3d_fwd(const hex_conv3d_desc_t* d, const void* x, const voi
     cudaStream_t s = (cudaStream_t)stream;
     const int Tn = hex_num_taps(d->kernel_size);
     uint8_t* p = (uint8_t*)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
+    Geom tg;
+    if (c3_tc_ok(d, g.Ci, g.Co, g.Do, &tg) && a16(x) && a16(y) && a16(w) && (!bias || a16(bias)) &&
+        !getenv("HEXCONV_CONV3D_UNFOLD")) {
+        // depth taps in the K loop of the tcgen05 tap-reuse kernel: no unfolded copy
+        const int64_t total = (int64_t)g.Co * g.Ci * g.kd * Tn;
+        pack3d_kernel<<<grid_for(total), 256, 0, s>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)p, g.Co, g.Ci, g.kd,
+                                                       Tn, 0);
+        count_launch();
+        if ((st = last_launch_status()) != HEX_OK) return st;
+        TcConvArgs a{};
+        a.g = tg; a.Cin = g.Ci; a.Cout = g.Co;
+        a.x = x; a.wpack = p; a.bias = bias; a.y = y; a.relu_y = nullptr; a.relu = fuse_relu;
+        return tc_conv3d_fwd(a, g.D, g.Do, g.sd, g.kd, s);
+    }
     void* xu = p;
     p += up1k((size_t)d2.batch * d2.in_channels * d->height * d->width * elt(d->dtype));
     void* wu = p;
@@ -319,6 +364,21 @@ hex_status_t hex_conv3d_bwd_data(const hex_conv3d_desc_t* d, const void* dy, con
     cudaStream_t s = (cudaStream_t)stream;
     const int Tn = hex_num_taps(d->kernel_size);
     uint8_t* p = (uint8_t*)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
+    Geom tg;
+    if (g.sd == 1 && c3_tc_ok(d, g.Co, g.Ci, g.D, &tg) && a16(dy) && a16(dx) && a16(w) &&
+        !getenv("HEXCONV_CONV3D_UNFOLD")) {
+        // stride 1: dx = the forward of dy with depth- and tap-reversed, channel-transposed weights
+        // (the 3-D form of DESIGN.md P18), depth taps in the K loop
+        const int64_t total = (int64_t)g.Co * g.Ci * g.kd * Tn;
+        pack3d_kernel<<<grid_for(total), 256, 0, s>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)p, g.Co, g.Ci, g.kd,
+                                                       Tn, 1);
+        count_launch();
+        if ((st = last_launch_status()) != HEX_OK) return st;
+        TcConvArgs a{};
+        a.g = tg; a.Cin = g.Co; a.Cout = g.Ci;
+        a.x = dy; a.wpack = p; a.bias = nullptr; a.y = dx; a.relu_y = nullptr; a.relu = 0;
+        return tc_conv3d_fwd(a, g.D, g.D, 1, g.kd, s);
+    }
     void* dxu = p;
     p += up1k((size_t)d2.batch * d2.in_channels * d->height * d->width * elt(d->dtype));
     void* wu = p;

@@ -47,6 +47,10 @@ struct FtParams {
     int pair_tiles;  // CTA-pair kernel: (n tile, pair of m tiles) work items
     int relu, has_mask;
     int debug;  // HEXCONV_FT_DEBUG: 1 = epilogue skipped, 2 = MMAs skipped (timing experiments)
+    // 3-D convolution: tile image index b is an OUTPUT slice b = vol * Do + zo; depth
+    // tap kz reads input image vol * D + sd * zo + kz - pd (a fully out-of-bounds box -- zeros -- when
+    // that slice is outside the volume), weight taps kz * T + t.  2-D: kd = D = Do = sd = 1, pd = 0.
+    int kd, D, Do, sd, pd;
     const float* bias;
 };
 
@@ -258,7 +262,13 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                 if (PAIR) ft_decode_pair(p, tile, BN, (int)rank, &P, &r0, &j0, &b, &n0);
                 else ft_decode(p, tile, BN, &P, &r0, &j0, &b, &n0);
                 const int pc = (P + p.parity) & 1;  // centre column parity
+                const int vol = b / p.Do, zo = b - vol * p.Do;
+                for (int kz = 0; kz < p.kd; ++kz)
                 for (int kc = 0; kc < p.kchunks; ++kc) {
+                    const int z = p.sd * zo + kz - p.pd;
+                    const bool zin = z >= 0 && z < p.D;
+                    const int img = vol * p.D + (zin ? z : 0);
+                    const int roff = zin ? 0 : p.H + 64;  // outside the volume: the box is all zero fill
 #pragma unroll 1
                     for (int s = 0; s < SL::count(); ++s) {
                         const int dc = SL::dc_of(s), g0 = SL::g0_of(s), cnt = SL::cnt_of(s), tb = SL::tb_of(s);
@@ -270,19 +280,20 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                         const uint32_t bytes = RES ? A_BYTES : A_BYTES + cnt * W_TILE;
                         if constexpr (PAIR) {  // both CTAs' bytes land on the leader's barrier
                             if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * bytes);
-                            ptx::tma_load_5d_2sm(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top, b,
-                                                 kc);
+                            ptx::tma_load_5d_2sm(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh,
+                                                 r0 + top + roff, img, kc);
                             if constexpr (!RES)
                                 for (int i = 0; i < cnt; ++i)
                                     ptx::tma_load_4d_2sm(&map_w, &full[stage], sa + A_BYTES + i * W_TILE, 0,
-                                                         n0 + (int)rank * (BN / 2), kc, tb + g0 + i);
+                                                         n0 + (int)rank * (BN / 2), kc, kz * p.T + tb + g0 + i);
                         } else {
                             ptx::mbar_arrive_expect_tx(&full[stage], bytes);
-                            ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top, b, kc);
+                            ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], sa, 0, j0 + jsh, r0 + top + roff,
+                                             img, kc);
                             if constexpr (!RES)
                                 for (int i = 0; i < cnt; ++i)
                                     ptx::tma_load_4d(&map_w, &full[stage], sa + A_BYTES + i * W_TILE, 0, n0, kc,
-                                                     tb + g0 + i);
+                                                     kz * p.T + tb + g0 + i);
                         }
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     }
@@ -306,7 +317,7 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
                 if (p.debug == 2) {
-                    for (int u = 0; u < p.kchunks * SL::count(); ++u) {
+                    for (int u = 0; u < p.kd * p.kchunks * SL::count(); ++u) {
                         ptx::mbar_wait(&full[stage], phase);
                         ptx::mbar_arrive(&empty[stage]);
                         if (PAIR) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&empty[stage]), 1));
@@ -318,10 +329,11 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                     if (acc == 0) aphase ^= 1;
                     continue;
                 }
-                for (int kc = 0; kc < p.kchunks; ++kc)
-                    issue_stages_from<BN, N, TG, RES, PAIR, 0>(d, a_ring, b_ring, res_desc, full, empty, stage, phase,
-                                                               p.stages, stage16, a_bytes16, kc, p.kchunks,
-                                                               kc == 0 ? 0u : 1u);
+                for (int kz = 0; kz < p.kd; ++kz)
+                    for (int kc = 0; kc < p.kchunks; ++kc)
+                        issue_stages_from<BN, N, TG, RES, PAIR, 0>(d, a_ring, b_ring, res_desc, full, empty, stage,
+                                                                   phase, p.stages, stage16, a_bytes16, kc,
+                                                                   p.kchunks, (kz | kc) == 0 ? 0u : 1u);
                 if constexpr (PAIR) ptx::mma_commit_2sm(&tfull[acc]);
                 else ptx::mma_commit(&tfull[acc]);
                 acc ^= 1;
@@ -1235,7 +1247,7 @@ struct FtPlan {
 // many as keep >= 3 stages in shared memory
 constexpr int ft_tg(bool res, int n, int BN) { return res ? 2 * n + 1 : (BN == 256 ? 2 : (n == 1 ? 3 : 5)); }
 
-FtPlan ft_plan(const Geom& g, int Cin, int Cout) {
+FtPlan ft_plan(const Geom& g, int Cin, int Cout, bool allow_res = true) {
     FtPlan pl{};
     if (Cin % 64) return pl;
     const int A = (FT_RB + 2 * g.n) * FT_JB * 128;
@@ -1243,7 +1255,8 @@ FtPlan ft_plan(const Geom& g, int Cin, int Cout) {
     // 1) resident weights: one Cout tile (Cout = 64 or 128), one CTA per tile.  The CTA-pair variant
     //    (each CTA keeps half of the weights, more room for A stages) measured slower on C5 layer 2
     //    (fwd 382 vs 230 us) and is kept for experiments (HEXCONV_FWD_TR_RESPAIR).
-    if ((Cout == 64 || Cout == 128) && !getenv("HEXCONV_FWD_TR_NORES") && getenv("HEXCONV_FWD_TR_RESPAIR")) {
+    if (allow_res && (Cout == 64 || Cout == 128) && !getenv("HEXCONV_FWD_TR_NORES") &&
+        getenv("HEXCONV_FWD_TR_RESPAIR")) {
         const int res_bytes = g.T * (Cin / 64) * (Cout / 2) * 128;
         if (res_bytes + fixed + 4 * A <= FT_SMEM_MAX) {
             pl.BN = Cout;
@@ -1257,7 +1270,7 @@ FtPlan ft_plan(const Geom& g, int Cin, int Cout) {
             return pl;
         }
     }
-    if ((Cout == 64 || Cout == 128) && !getenv("HEXCONV_FWD_TR_NORES")) {
+    if (allow_res && (Cout == 64 || Cout == 128) && !getenv("HEXCONV_FWD_TR_NORES")) {
         const int res_bytes = g.T * (Cin / 64) * Cout * 128;
         if (res_bytes + fixed + 4 * A <= FT_SMEM_MAX) {
             pl.BN = Cout;
@@ -1407,6 +1420,8 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
     p.relu = a.relu;
     p.has_mask = a.relu_y != nullptr;
     p.debug = getenv("HEXCONV_FT_DEBUG") ? atoi(getenv("HEXCONV_FT_DEBUG")) : 0;
+    p.kd = p.D = p.Do = p.sd = 1;
+    p.pd = 0;
     p.bias = a.bias;
     CUtensorMap maps[7];
     if (!ft_view5(&maps[0], a.x, g.B, g.H, g.W, a.Cin, 0, FT_RB + 2 * g.n)) return HEX_ERR_CUDA;
@@ -1439,6 +1454,62 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
                                       : launch_ft<128, 2, false, true>(maps, p, pl.smem, st);
     return g.n == 1 ? launch_ft<64, 1, false, true>(maps, p, pl.smem, st)
                     : launch_ft<64, 2, false, true>(maps, p, pl.smem, st);
+}
+
+// ------------------------------------------------------------------ 3-D convolution
+// a.g: per-slice 2-D geometry with g.B = number of VOLUMES; x bf16 NDHWC [B][D][H][W][Cin], y NDHWC
+// [B][Do][Ho][Wo][Cout] (s = 1), a.wpack bf16 [kd*T][Cout][Cin] (depth-major taps).  The depth taps run
+// inside the K loop of the streamed CTA-pair tap-reuse kernel (no unfold copy).
+bool tc_conv3d_supported(const Geom& g, int Cin, int Cout, int Do) {
+    if (getenv("HEXCONV_NO_CONV3D_TC")) return false;
+    Geom go = g;
+    go.B = g.B * Do;
+    if (go.B > 65535 || !tc_fwd_tr_supported(go, Cin, Cout)) return false;
+    return ft_plan(go, Cin, Cout, false).ok;
+}
+
+hex_status_t tc_conv3d_fwd(const TcConvArgs& a, int D, int Do, int sd, int kd, cudaStream_t st) {
+    Geom go = a.g;
+    go.B = a.g.B * Do;  // output images
+    const FtPlan pl = ft_plan(go, a.Cin, a.Cout, false);
+    if (!pl.ok || !pl.pair || pl.res) return HEX_ERR_UNSUPPORTED;
+    FtParams p{};
+    p.B = go.B; p.H = go.H; p.W = go.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = go.T; p.parity = go.parity;
+    p.rt = ceil_div(go.H, FT_RB);
+    p.jt0 = ceil_div((go.W + 1) / 2, FT_JB);
+    p.jt1 = ceil_div(go.W / 2, FT_JB);
+    p.tiles0 = p.rt * p.jt0 * go.B;
+    p.mtiles = p.tiles0 + p.rt * p.jt1 * go.B;
+    p.n_tiles = a.Cout / pl.BN;
+    p.total_tiles = p.mtiles * p.n_tiles;
+    p.pair_tiles = ceil_div(p.mtiles, 2) * p.n_tiles;
+    p.kchunks = a.Cin / 64;
+    p.stages = pl.stages;
+    p.relu = a.relu;
+    p.has_mask = a.relu_y != nullptr;
+    p.debug = 0;
+    p.kd = kd; p.D = D; p.Do = Do; p.sd = sd; p.pd = (kd - 1) / 2;
+    p.bias = a.bias;
+    const int Bin = a.g.B * D;  // input images
+    CUtensorMap maps[7];
+    if (!ft_view5(&maps[0], a.x, Bin, go.H, go.W, a.Cin, 0, FT_RB + 2 * go.n)) return HEX_ERR_CUDA;
+    if (!ft_view5(&maps[1], a.x, Bin, go.H, go.W, a.Cin, 1, FT_RB + 2 * go.n)) return HEX_ERR_CUDA;
+    if (!ft_wmap(&maps[2], a.wpack, kd * go.T, a.Cout, a.Cin, pl.BN / 2)) return HEX_ERR_CUDA;
+    if (!ft_view4(&maps[3], a.y, go.B, go.H, go.W, a.Cout, 0)) return HEX_ERR_CUDA;
+    if (!ft_view4(&maps[4], a.y, go.B, go.H, go.W, a.Cout, 1)) return HEX_ERR_CUDA;
+    if (a.relu_y) {
+        if (!ft_view4(&maps[5], a.relu_y, go.B, go.H, go.W, a.Cout, 0)) return HEX_ERR_CUDA;
+        if (!ft_view4(&maps[6], a.relu_y, go.B, go.H, go.W, a.Cout, 1)) return HEX_ERR_CUDA;
+    } else {
+        maps[5] = maps[3];
+        maps[6] = maps[4];
+    }
+    if (pl.BN == 256) return go.n == 1 ? launch_ft<256, 1, false, true>(maps, p, pl.smem, st)
+                                       : launch_ft<256, 2, false, true>(maps, p, pl.smem, st);
+    if (pl.BN == 128) return go.n == 1 ? launch_ft<128, 1, false, true>(maps, p, pl.smem, st)
+                                       : launch_ft<128, 2, false, true>(maps, p, pl.smem, st);
+    return go.n == 1 ? launch_ft<64, 1, false, true>(maps, p, pl.smem, st)
+                     : launch_ft<64, 2, false, true>(maps, p, pl.smem, st);
 }
 
 // ------------------------------------------------------------------ fused conv + max pool host side

@@ -2,8 +2,9 @@
 (hex_conv3d_fwd / _bwd_data / _bwd_weight) against the fp64 oracle (oracle.conv3d_*).
 
 Bars as tests/test_gpu_parity.py: fp32 normwise <= 1e-5, bf16 (inputs rounded on both sides, fp32
-accumulation) <= 2e-2.  The bf16 NDHWC cases with Cin' = kd*Cin and Cout multiples of 64 run the
-tcgen05 kernels (the 2-D algo query on the unfolded descriptor says which).
+accumulation) <= 2e-2.  bf16 NDHWC with in-plane stride 1 and channels multiples of 64 runs the
+depth taps inside the K loop of the tcgen05 tap-reuse kernel (forward; backward-data for depth stride 1);
+HEXCONV_CONV3D_UNFOLD=1 selects the unfold + 2-D path, which the weight gradient always takes.
 """
 import numpy as np
 import pytest
@@ -93,6 +94,16 @@ def test_conv3d_bf16_tensor_cores(F, oracle):
     d = F.conv3d_desc(2, 64, 64, 5, 16, 16, 1, 3, 1, 1, 0, torch.bfloat16, "NDHWC")
     assert F.conv_algo(2 * 5, 3 * 64, 64, 16, 16, 1, 1, 0, torch.bfloat16, "NHWC") == "tcgen05"
     assert F.conv3d_output_shape(d) == (5, 16, 16)
+
+
+def test_conv3d_bf16_unfold_path_agrees(F, oracle, monkeypatch):
+    # the depth-in-K-loop tcgen05 path (default) and the unfold + 2-D path both meet the bar
+    for k, (Ci, Co, D, n, kd, sd, pi) in enumerate([(64, 128, 7, 1, 3, 1, 1), (128, 64, 3, 1, 5, 1, 0),
+                                                      (64, 64, 9, 2, 3, 2, 1)]):
+        case(F, oracle, 1, Ci, Co, D, 20, 18, n, kd, 1, sd, pi, torch.bfloat16, "NDHWC", 300 + k)
+        monkeypatch.setenv("HEXCONV_CONV3D_UNFOLD", "1")
+        case(F, oracle, 1, Ci, Co, D, 20, 18, n, kd, 1, sd, pi, torch.bfloat16, "NDHWC", 300 + k)
+        monkeypatch.delenv("HEXCONV_CONV3D_UNFOLD")
 
 
 def test_conv3d_autograd_and_errors(F, oracle):
