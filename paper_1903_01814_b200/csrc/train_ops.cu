@@ -9,7 +9,7 @@ namespace hexconv {
 // Per-sample block: global average pool (8 channels per thread, HW split over
 // thread slices, fixed-order smem reduction), logits, softmax cross-entropy,
 // dlogits.  gap[b][C], dlog[b][K], loss_b[b].
-constexpr int HEAD_THREADS = 256;
+constexpr int HEAD_THREADS = 1024;  // C = 256: 32 pixel slices x 32 channel groups per image
 
 __global__ void __launch_bounds__(HEAD_THREADS)
 head_sample_kernel(const uint4* __restrict__ feat, const float* __restrict__ wl, const float* __restrict__ bl,
@@ -23,6 +23,7 @@ head_sample_kernel(const uint4* __restrict__ feat, const float* __restrict__ wl,
     const int c8 = tid % C8, sl = tid / C8;
     if (sl < slices && tid < slices * C8) {
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
         for (int i = sl; i < HW; i += slices) {
             const uint4 v4 = feat[((int64_t)b * HW + i) * C8 + c8];
             const __nv_bfloat16* v = reinterpret_cast<const __nv_bfloat16*>(&v4);
