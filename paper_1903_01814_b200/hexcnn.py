@@ -20,6 +20,7 @@ the pooled value.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 
 import numpy as np
@@ -74,6 +75,8 @@ class HexCNN:
         self.world = dist.get_world_size(process_group) if (dist.is_available() and dist.is_initialized()) else 1
         self.L = len(ns)
         self.timer = None  # optional list: (kind, layer, start_event, end_event) around conv calls
+        self._side = None if (os.environ.get("HEXCNN_SERIAL_BWD") or not torch.cuda.is_available()) \
+            else torch.cuda.Stream(device=device)
         self._layout()
         self._init_params(seed)
         self._alloc()
@@ -232,16 +235,26 @@ class HexCNN:
                                    _p(self.head_ws), self.head_ws_bytes, stream), "head")
         if hooks:
             hooks(self.L)
+        # The weight gradient of layer l and the backward-data chain (dgrad l, pool bwd, ...) are independent:
+        # weight gradients run on a side stream so each persistent kernel's tail overlaps the other chain
+        # (HEXCNN_SERIAL_BWD=1: one stream).  The side stream joins the main one before the optimizer.
+        main = torch.cuda.current_stream()
+        side = self._side if self._side is not None else main
+        side_h = ctypes.c_void_p(side.cuda_stream) if side is not main else stream
         for l in reversed(range(self.L)):
             wo, wn, bo, bn = self.seg[l]
             xin = self.layer_input(l, x)
             dy = self.dact[l]
-            e0 = self._tic()
-            A.check(L.hex_conv2d_bwd_weight(ctypes.byref(self.desc[l]), _p(xin), _p(dy), _p(g[wo:]), _p(g[bo:]), 0,
-                                            _p(self.ws[l][2]), self.ws_sizes[l][2], stream), f"conv{l + 1} wgrad")
-            self._toc("wgrad", l, e0)
-            if hooks:
-                hooks(l)
+            if side is not main:
+                side.wait_stream(main)  # dy of layer l is complete
+            with torch.cuda.stream(side):
+                e0 = self._tic()
+                A.check(L.hex_conv2d_bwd_weight(ctypes.byref(self.desc[l]), _p(xin), _p(dy), _p(g[wo:]), _p(g[bo:]),
+                                                0, _p(self.ws[l][2]), self.ws_sizes[l][2], side_h),
+                        f"conv{l + 1} wgrad")
+                self._toc("wgrad", l, e0)
+                if hooks:
+                    hooks(l)  # the allreduce of layer l's bucket is ordered after it (current stream = side)
             if l == 0:
                 break
             prev = l - 1
@@ -261,6 +274,8 @@ class HexCNN:
                                               _p(self.act[prev]), _p(self.dact[prev]), _p(self.ws[l][1]),
                                               self.ws_sizes[l][1], stream), f"conv{l + 1} dgrad")
                 self._toc("dgrad", l, e0)
+        if side is not main:
+            main.wait_stream(side)
 
     def _segment(self, l):
         if l == self.L:
