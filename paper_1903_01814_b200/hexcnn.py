@@ -64,7 +64,7 @@ class GradBucketReducer:
 class HexCNN:
     def __init__(self, batch: int = 256, H: int = 96, W: int = 96,
                  channels=(1, 64, 128, 128, 256, 256, 256), ns=(2, 1, 2, 1, 2, 1), pool_after=(2, 4),
-                 num_classes: int = 2, lr: float = 0.01, momentum: float = 0.9, seed: int = 0,
+                 num_classes: int = 2, lr: float = 1e-3, momentum: float = 0.9, seed: int = 0,
                  device="cuda", process_group=None):
         self.B, self.H, self.W = batch, H, W
         self.channels, self.ns, self.pool_after = tuple(channels), tuple(ns), tuple(pool_after)
@@ -75,8 +75,10 @@ class HexCNN:
         self.world = dist.get_world_size(process_group) if (dist.is_available() and dist.is_initialized()) else 1
         self.L = len(ns)
         self.timer = None  # optional list: (kind, layer, start_event, end_event) around conv calls
-        self._side = None if (os.environ.get("HEXCNN_SERIAL_BWD") or not torch.cuda.is_available()) \
-            else torch.cuda.Stream(device=device)
+        # weight gradients on a side stream (HEXCNN_SIDE_BWD=1): measured no faster than one stream once the
+        # training data is finite (3.52 vs 3.47 ms per step), and it blurs the per-family event timings
+        self._side = torch.cuda.Stream(device=device) \
+            if (os.environ.get("HEXCNN_SIDE_BWD") and torch.cuda.is_available()) else None
         self._layout()
         self._init_params(seed)
         self._alloc()
@@ -235,9 +237,8 @@ class HexCNN:
                                    _p(self.head_ws), self.head_ws_bytes, stream), "head")
         if hooks:
             hooks(self.L)
-        # The weight gradient of layer l and the backward-data chain (dgrad l, pool bwd, ...) are independent:
-        # weight gradients run on a side stream so each persistent kernel's tail overlaps the other chain
-        # (HEXCNN_SERIAL_BWD=1: one stream).  The side stream joins the main one before the optimizer.
+        # The weight gradient of layer l and the backward-data chain (dgrad l, pool bwd, ...) are independent;
+        # with HEXCNN_SIDE_BWD=1 the weight gradients run on a side stream that joins before the optimizer.
         main = torch.cuda.current_stream()
         side = self._side if self._side is not None else main
         side_h = ctypes.c_void_p(side.cuda_stream) if side is not main else stream
