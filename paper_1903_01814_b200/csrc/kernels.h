@@ -40,6 +40,9 @@ struct PoolArgs {
     void* dx;
 };
 hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st);
+// bf16 NHWC max pool n = 1, s = 2, C % 64 == 0: TMA-staged bands (pool_tma.cu)
+bool pool_tma_fwd_supported(const PoolArgs& a);
+hex_status_t pool_tma_fwd(const PoolArgs& a, cudaStream_t st);
 // NCHW plane-staged pools (plane_kernels.cu); return false when the shape is not covered
 bool pool_plane_fwd(const PoolArgs& a, cudaStream_t st);
 bool pool_plane_bwd(const PoolArgs& a, cudaStream_t st);

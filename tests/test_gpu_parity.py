@@ -193,6 +193,24 @@ def test_pool_bf16_nhwc_vectorised(F, oracle, mode):
             _pool_case(F, oracle, pi, n, s, 12, 13, 2, C, torch.bfloat16, "NHWC", mode, 300 + C)
 
 
+@pytest.mark.parametrize("pi", [0, 1])
+def test_maxpool_tma_band_kernel(F, oracle, pi, monkeypatch):
+    # bf16 NHWC, C % 64 == 0, n = 1, s = 2: the TMA-staged band kernel (pool_tma.cu); bit-exact values
+    # and argmax vs the oracle, and identical to the stencil kernel (HEXCONV_NO_POOL_TMA=1)
+    for k, (B, C, H, W) in enumerate([(3, 64, 17, 65), (2, 128, 48, 96), (1, 192, 5, 64), (2, 64, 30, 96),
+                                       (1, 64, 2, 70), (1, 256, 3, 64), (2, 128, 96, 96)]):
+        x = rnd((B, C, H, W), 700 + k, torch.bfloat16)
+        xd = to_dev(x, torch.bfloat16, "NHWC")
+        y, am = F.pool2d_fwd(xd, n=1, stride=2, parity=pi, mode="max", layout="NHWC")
+        yref, amref = oracle.pool2d_fwd(x, n=1, s=2, pi=pi, mode="max")
+        assert np.array_equal(to_np(y, "NHWC"), yref), (pi, B, C, H, W)
+        assert np.array_equal(am.permute(0, 3, 1, 2).cpu().numpy(), amref), (pi, B, C, H, W)
+        monkeypatch.setenv("HEXCONV_NO_POOL_TMA", "1")
+        y2, am2 = F.pool2d_fwd(xd, n=1, stride=2, parity=pi, mode="max", layout="NHWC")
+        monkeypatch.delenv("HEXCONV_NO_POOL_TMA")
+        assert torch.equal(y.view(torch.int16), y2.view(torch.int16)) and torch.equal(am, am2)
+
+
 def test_maxpool_ties_first_in_canonical_order(F, oracle):
     # ReLU-like data with many exact zeros: the first in-grid tap wins
     x = np.maximum(rnd((2, 8, 11, 12), 9, torch.bfloat16), 0)
