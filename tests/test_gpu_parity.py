@@ -198,7 +198,8 @@ def test_maxpool_tma_band_kernel(F, oracle, pi, monkeypatch):
     # bf16 NHWC, C % 64 == 0, n = 1, s = 2: the TMA-staged band kernel (pool_tma.cu); bit-exact values
     # and argmax vs the oracle, and identical to the stencil kernel (HEXCONV_NO_POOL_TMA=1)
     for k, (B, C, H, W) in enumerate([(3, 64, 17, 65), (2, 128, 48, 96), (1, 192, 5, 64), (2, 64, 30, 96),
-                                       (1, 64, 2, 70), (1, 256, 3, 64), (2, 128, 96, 96)]):
+                                       (1, 64, 2, 70), (1, 256, 3, 64), (2, 128, 96, 96), (2, 256, 48, 48),
+                                       (1, 64, 9, 13)]):
         x = rnd((B, C, H, W), 700 + k, torch.bfloat16)
         xd = to_dev(x, torch.bfloat16, "NHWC")
         y, am = F.pool2d_fwd(xd, n=1, stride=2, parity=pi, mode="max", layout="NHWC")
@@ -209,6 +210,12 @@ def test_maxpool_tma_band_kernel(F, oracle, pi, monkeypatch):
         y2, am2 = F.pool2d_fwd(xd, n=1, stride=2, parity=pi, mode="max", layout="NHWC")
         monkeypatch.delenv("HEXCONV_NO_POOL_TMA")
         assert torch.equal(y.view(torch.int16), y2.view(torch.int16)) and torch.equal(am, am2)
+        # backward through the pool of these shapes: oracle within the bf16 bar
+        g = rnd(yref.shape, 800 + k, torch.bfloat16)
+        dx = F.pool2d_bwd(to_dev(g, torch.bfloat16, "NHWC"), am, (H, W), n=1, stride=2, parity=pi, mode="max",
+                          layout="NHWC")
+        dxr = oracle.pool2d_bwd(g, amref, H, W, n=1, s=2, pi=pi, mode="max")
+        assert rel(to_np(dx, "NHWC"), dxr) <= TOL_BF16, (pi, B, C, H, W)
 
 
 def test_maxpool_ties_first_in_canonical_order(F, oracle):
