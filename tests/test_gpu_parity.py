@@ -300,3 +300,33 @@ def test_maxpool_n1s2_closed_form_backward(F, oracle):
         for (H, W) in [(12, 13), (13, 12), (9, 9), (2, 7)]:
             for C in (8, 24):
                 _pool_case(F, oracle, pi, 1, 2, H, W, 2, C, torch.bfloat16, "NHWC", "max", 400 + H + C)
+
+
+@pytest.mark.parametrize("n", [4, 5, 7])
+def test_conv_pool_largest_kernels(F, oracle, n):
+    # the largest kernel sizes the ABI accepts (HEX_MAX_N = 7: T = 169 taps) on grids smaller and
+    # larger than the kernel, strides 1 and 2, both parities; pooling up to the uint8 argmax range
+    for k, (pi, s, H, W) in enumerate([(0, 1, 9, 11), (1, 2, 20, 17), (0, 3, 4, 3)]):
+        _conv_case(F, oracle, pi, n, s, H, W, 1, 2, 3, torch.float32, "NCHW", 900 + 10 * n + k)
+        for mode in ("max", "avg", "avg_pad"):
+            _pool_case(F, oracle, pi, n, s, H, W, 2, 3, torch.float32, "NCHW", mode, 950 + 10 * n + k)
+
+
+def test_degenerate_and_invalid_shapes(F, oracle):
+    from paper_1903_01814_b200._abi import HexError
+    # 1 x 1 grid (every tap off-grid but the centre) and a single column
+    _conv_case(F, oracle, 0, 2, 1, 1, 1, 2, 3, 4, torch.float32, "NCHW", 990)
+    _conv_case(F, oracle, 1, 1, 1, 7, 1, 1, 2, 2, torch.float32, "NCHW", 991)
+    _pool_case(F, oracle, 0, 1, 1, 1, 1, 1, 2, torch.float32, "NCHW", "max", 992)
+    x = torch.zeros(1, 2, 5, 5, device="cuda")
+    w = torch.zeros(3, 2, 7, device="cuda")
+    with pytest.raises(HexError) as e:  # kernel size beyond HEX_MAX_N
+        F.conv2d_fwd(x, torch.zeros(3, 2, 3 * 8 * 9 + 1, device="cuda"), n=8)
+    assert e.value.status == 8  # HEX_ERR_UNSUPPORTED
+    with pytest.raises(HexError) as e:  # empty stride lattice: H = 1 with s = 2 leaves the odd columns empty
+        F.conv2d_fwd(torch.zeros(1, 2, 1, 5, device="cuda"), w, n=1, stride=2)
+    assert e.value.status == 3  # HEX_ERR_EMPTY_LATTICE
+    with pytest.raises(HexError):  # zero batch
+        F.conv2d_fwd(torch.zeros(0, 2, 5, 5, device="cuda"), w, n=1)
+    with pytest.raises(ValueError):  # channel mismatch is caught before the ABI
+        F.conv2d_fwd(x, torch.zeros(3, 4, 7, device="cuda"), n=1)
