@@ -164,6 +164,37 @@ def conv2d_bwd_weight(x, dy, n: int = 1, stride: int = 1, parity: int = 0, layou
     return dw, (dbias if with_bias else None)
 
 
+# ------------------------------------------------------------------ custom kernels
+def tap_axial(n: int):
+    """The T(n) taps of a size-n hexagonal kernel as axial displacements (dq, dr), in the canonical
+    weight order (A2: column-major left to right, top to bottom = lexicographic (dq, dr))."""
+    if n < 0:
+        raise ValueError("kernel size n >= 0")
+    taps = [(dq, dr) for dq in range(-n, n + 1) for dr in range(-n, n + 1)
+            if abs(dq) + abs(dr) + abs(dq + dr) <= 2 * n]
+    assert len(taps) == A.num_taps(n)
+    return taps
+
+
+def custom_kernel(n: int, value, out_channels: int = 1, in_channels: int = 1, dtype=torch.float32, device="cuda"):
+    """A hexagonal kernel with user-defined element values ("structure detecting kernels ... smoothing",
+    PAPER.md:207-210): value(dq, dr) -> float for each axial tap displacement, or a dict {(dq, dr): v}
+    (missing taps are 0).  Returns weights [out_channels, in_channels, T(n)] with every (co, ci) pair
+    set to the same kernel, ready for conv2d_fwd / hex_conv2d."""
+    taps = tap_axial(n)
+    fn = (lambda dq, dr: value.get((dq, dr), 0.0)) if isinstance(value, dict) else value
+    k = torch.tensor([float(fn(dq, dr)) for dq, dr in taps], dtype=torch.float32)
+    return k.view(1, 1, -1).expand(out_channels, in_channels, -1).contiguous().to(device=device, dtype=dtype)
+
+
+def ring_kernel(ring_values, out_channels: int = 1, in_channels: int = 1, dtype=torch.float32, device="cuda"):
+    """A rotationally symmetric kernel of size n = len(ring_values) - 1: the value of a tap is
+    ring_values[d] for hexagonal distance d from the centre (e.g. [1/7] * 2 = 7-cell mean smoothing)."""
+    n = len(ring_values) - 1
+    return custom_kernel(n, lambda dq, dr: ring_values[(abs(dq) + abs(dr) + abs(dq + dr)) // 2], out_channels,
+                         in_channels, dtype, device)
+
+
 # ------------------------------------------------------------------ 3-D convolution (PAPER.md:197-199)
 _LAYOUTS3 = {"NCDHW": A.NCHW, "NDHWC": A.NHWC}
 

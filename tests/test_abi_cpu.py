@@ -114,3 +114,17 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 for pat in ("import oracle", "from oracle", "liboracle", '#include "../../oracle', "oracle/hexoracle.h"):
                     assert pat not in txt, (f, pat)
+
+
+def test_custom_kernel_taps_canonical(oracle):
+    # tap_axial (the custom-kernel helper's tap order) is the oracle's canonical tap list (A2, P1)
+    from paper_1903_01814_b200 import functional as F
+    for n in range(0, 5):
+        assert F.tap_axial(n) == [tuple(t) for t in oracle.tap_list(n)]
+    k = F.ring_kernel([1.0, 0.5, 0.25], device="cpu")
+    assert k.shape == (1, 1, 19)
+    taps = F.tap_axial(2)
+    for t, (a, b) in enumerate(taps):
+        assert k[0, 0, t].item() == [1.0, 0.5, 0.25][(abs(a) + abs(b) + abs(a + b)) // 2]
+    d = F.custom_kernel(1, {(0, 0): 2.0, (1, -1): -1.0}, 2, 3, device="cpu")
+    assert d.shape == (2, 3, 7) and d.sum().item() == 6.0

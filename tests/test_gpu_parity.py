@@ -330,3 +330,19 @@ def test_degenerate_and_invalid_shapes(F, oracle):
         F.conv2d_fwd(torch.zeros(0, 2, 5, 5, device="cuda"), w, n=1)
     with pytest.raises(ValueError):  # channel mismatch is caught before the ABI
         F.conv2d_fwd(x, torch.zeros(3, 4, 7, device="cuda"), n=1)
+
+
+def test_custom_ring_kernel_smoothing(F, oracle):
+    # a user-defined kernel: 7-cell mean smoothing via ring_kernel; the GPU result
+    # equals the oracle convolution with the same weights, and a constant image stays constant inside
+    x = rnd((2, 1, 11, 12), 1200, torch.float32)
+    k = F.ring_kernel([1.0 / 7, 1.0 / 7])
+    y = F.conv2d_fwd(torch.from_numpy(x.astype(np.float32)).cuda(), k, None, n=1)
+    assert rel(to_np(y), oracle.conv2d_fwd(x, k.cpu().numpy().astype(np.float64), None, n=1)) <= TOL_F32
+    yc = F.conv2d_fwd(torch.full((1, 1, 9, 9), 3.5, device="cuda"), k, None, n=1)
+    assert torch.allclose(yc[0, 0, 1:-1, 1:-1], torch.tensor(3.5, device="cuda"), atol=1e-6)
+    # an edge detector from a dict of axial displacements: zero response on a constant image interior
+    e = F.custom_kernel(1, {(0, 0): 6.0, (0, -1): -1.0, (0, 1): -1.0, (1, 0): -1.0, (-1, 0): -1.0,
+                            (1, -1): -1.0, (-1, 1): -1.0})
+    ye = F.conv2d_fwd(torch.full((1, 1, 9, 9), 2.0, device="cuda"), e, None, n=1)
+    assert ye[0, 0, 1:-1, 1:-1].abs().max().item() == 0.0
