@@ -916,35 +916,47 @@ struct FvParams {
     const float* bias;
 };
 
-template <int BN>
+template <int BN, int CNT, bool PAIR>
+__device__ __forceinline__ void fv_group(uint32_t d, uint64_t ad, uint64_t bd, int bs, uint32_t first) {
+    if constexpr (PAIR) issue_stage_pair<BN, CNT>(d, ad, bd, bs, first);
+    else issue_stage<BN, CNT, true>(d, ad, bd, bs, first);
+}
+
+template <int BN, bool PAIR>
 __device__ __forceinline__ void fv_issue(uint32_t d0, uint32_t d1, uint64_t a_ring, uint64_t res_desc, uint64_t* full,
                                          uint64_t* empty, int& stage, uint32_t& phase, int nstages, uint32_t stage16,
                                          int kc, int kchunks, uint32_t first, uint32_t pc0) {
+    constexpr int BROWS = PAIR ? BN / 2 : BN;  // weight rows held per CTA
     const uint64_t o0 = (uint64_t)(pc0 * 64), o1 = (uint64_t)((pc0 ^ 1u) * 64);  // 1024-byte rows
-    const int bs = kchunks * BN * 8;
-    const uint64_t w0 = res_desc + (uint64_t)(kc * (BN * 8));  // tap t at w0 + t * bs
+    const int bs = kchunks * BROWS * 8;
+    const uint64_t w0 = res_desc + (uint64_t)(kc * (BROWS * 8));  // tap t at w0 + t * bs
 #pragma unroll
     for (int bx = 0; bx < 4; ++bx) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         const uint64_t ad = a_ring + (uint64_t)stage * stage16;
         if (bx == 0) {
-            issue_stage<BN, 2, true>(d0, ad + o0, w0, bs, first);
+            fv_group<BN, 2, PAIR>(d0, ad + o0, w0, bs, first);
         } else if (bx == 1) {
-            issue_stage<BN, 3, true>(d0, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
-            issue_stage<BN, 2, true>(d1, ad + o1, w0, bs, first);
+            fv_group<BN, 3, PAIR>(d0, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
+            fv_group<BN, 2, PAIR>(d1, ad + o1, w0, bs, first);
         } else if (bx == 2) {
-            issue_stage<BN, 2, true>(d0, ad + o0, w0 + (uint64_t)(5 * bs), bs, 1u);
-            issue_stage<BN, 3, true>(d1, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
+            fv_group<BN, 2, PAIR>(d0, ad + o0, w0 + (uint64_t)(5 * bs), bs, 1u);
+            fv_group<BN, 3, PAIR>(d1, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
         } else {
-            issue_stage<BN, 2, true>(d1, ad + o1, w0 + (uint64_t)(5 * bs), bs, 1u);
+            fv_group<BN, 2, PAIR>(d1, ad + o1, w0 + (uint64_t)(5 * bs), bs, 1u);
         }
-        ptx::mma_commit(&empty[stage]);
+        if constexpr (PAIR) ptx::mma_commit_2sm(&empty[stage]);
+        else ptx::mma_commit(&empty[stage]);
         if (++stage == nstages) { stage = 0; phase ^= 1; }
     }
 }
 
 __device__ __forceinline__ void fv_decode(const FvParams& p, int pr, int* r0, int* j0, int* b) {
+    if (pr >= p.pairs) {  // CTA-pair tail: a missing unit loads zero fill and stores nothing (rows >= H)
+        *r0 = p.H; *j0 = 0; *b = 0;
+        return;
+    }
     const int ji = pr % p.jt;
     const int t = pr / p.jt;
     *r0 = (t % p.rt) * FT_RB;
@@ -952,14 +964,14 @@ __device__ __forceinline__ void fv_decode(const FvParams& p, int pr, int* r0, in
     *b = t / p.rt;
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 __global__ void __launch_bounds__(FT_THREADS, 1)
 tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                     const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
                     const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
                     const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ FvParams p) {
     constexpr int A_BYTES = (FT_RB + 3) * FT_JB * 128;  // 19-row box
-    constexpr int W_TILE = BN * 128;
+    constexpr int W_TILE = (PAIR ? BN / 2 : BN) * 128;  // one (tap, chunk) weight tile (this CTA's rows)
     constexpr int TMEM_COLS = 4 * BN;  // 2 slots x 2 views
     constexpr int UNITS = 2 * (BN / 64);  // (view, 64-channel chunk) epilogue units per pair
     extern __shared__ uint8_t smem_raw[];
@@ -977,11 +989,13 @@ tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
     uint32_t* tmem_slot = (uint32_t*)(bres + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], FT_EPI / 32);
+            ptx::mbar_init(&tempty[a], (PAIR ? 2 : 1) * FT_EPI / 32);
             ptx::mbar_init(&mbar[a], 1);
         }
         ptx::mbar_init(bres, 1);
@@ -992,50 +1006,56 @@ tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
         ptx::prefetch_tmap(&map_y0);
         ptx::prefetch_tmap(&map_y1);
     }
-    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    if (warp == 1) {
+        if constexpr (PAIR) ptx::tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+        else ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) ptx::cluster_sync();
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(bres, (uint32_t)res_bytes);
-            for (int t = 0; t < 7; ++t)
-                for (int kc = 0; kc < p.kchunks; ++kc)
-                    ptx::tma_load_4d(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0, 0, kc, t);
+            if constexpr (PAIR) {  // each CTA holds its half of every weight tile; bytes land on the leader
+                if (leader) ptx::mbar_arrive_expect_tx(bres, (uint32_t)(2 * res_bytes));
+                for (int t = 0; t < 7; ++t)
+                    for (int kc = 0; kc < p.kchunks; ++kc)
+                        ptx::tma_load_4d_2sm(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0,
+                                             (int)rank * (BN / 2), kc, t);
+            } else {
+                ptx::mbar_arrive_expect_tx(bres, (uint32_t)res_bytes);
+                for (int t = 0; t < 7; ++t)
+                    for (int kc = 0; kc < p.kchunks; ++kc)
+                        ptx::tma_load_4d(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0, 0, kc, t);
+            }
             int stage = 0;
             uint32_t phase = 0;
-            for (int pr = blockIdx.x; pr < p.pairs; pr += gridDim.x) {
+            for (int u = PAIR ? blockIdx.x / 2 : blockIdx.x; u < (PAIR ? (p.pairs + 1) / 2 : p.pairs);
+                 u += PAIR ? gridDim.x / 2 : gridDim.x) {
+                const int pr = PAIR ? 2 * u + (int)rank : u;
                 int r0, j0, b;
-                if (p.prefetch && pr + gridDim.x < p.pairs) {  // next pair's boxes into L2 (hides DRAM latency)
-                    fv_decode(p, pr + gridDim.x, &r0, &j0, &b);
-                    for (int kc = 0; kc < p.kchunks; ++kc)
-#pragma unroll
-                        for (int bx = 0; bx < 4; ++bx)
-                            ptx::tma_prefetch_5d((bx & 1) ? &map_x0 : &map_x1, 0,
-                                                 j0 + (bx == 0 ? -1 : (bx == 3 ? 1 : 0)), r0 - 1, b, kc);
-                }
                 fv_decode(p, pr, &r0, &j0, &b);
                 for (int kc = 0; kc < p.kchunks; ++kc)
 #pragma unroll
                     for (int bx = 0; bx < 4; ++bx) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sa = ring + stage * A_BYTES;
-                        if (p.debug == 3) {  // no loads: MMAs on stale shared memory (timing experiment)
-                            ptx::mbar_arrive(&full[stage]);
-                            if (++stage == p.stages) { stage = 0; phase ^= 1; }
-                            continue;
+                        const int jj = j0 + (bx == 0 ? -1 : (bx == 3 ? 1 : 0));
+                        if constexpr (PAIR) {
+                            if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * A_BYTES);
+                            ptx::tma_load_5d_2sm((bx & 1) ? &map_x0 : &map_x1, &full[stage], sa, 0, jj, r0 - 1, b, kc);
+                        } else {
+                            ptx::mbar_arrive_expect_tx(&full[stage], A_BYTES);
+                            ptx::tma_load_5d((bx & 1) ? &map_x0 : &map_x1, &full[stage], sa, 0, jj, r0 - 1, b, kc);
                         }
-                        ptx::mbar_arrive_expect_tx(&full[stage], A_BYTES);
-                        ptx::tma_load_5d((bx & 1) ? &map_x0 : &map_x1, &full[stage], sa, 0,
-                                         j0 + (bx == 0 ? -1 : (bx == 3 ? 1 : 0)), r0 - 1, b, kc);
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && (!PAIR || leader)) {
             const uint64_t a_ring = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
             const uint64_t res_desc = ptx::smem_desc_sw128(ptx::smem_u32(resw), 16, 1024);
             int stage = 0;
@@ -1043,23 +1063,16 @@ tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
             int slot = 0;
             uint32_t sphase = 0;
             ptx::mbar_wait(bres, 0);
-            for (int pr = blockIdx.x; pr < p.pairs; pr += gridDim.x) {
+            for (int u = PAIR ? blockIdx.x / 2 : blockIdx.x; u < (PAIR ? (p.pairs + 1) / 2 : p.pairs);
+                 u += PAIR ? gridDim.x / 2 : gridDim.x) {
                 ptx::mbar_wait(&tempty[slot], sphase ^ 1);
                 ptx::tc_fence_after();
-                if (p.debug == 2) {
-                    for (int u = 0; u < 4 * p.kchunks; ++u) {
-                        ptx::mbar_wait(&full[stage], phase);
-                        ptx::mbar_arrive(&empty[stage]);
-                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
-                    }
-                    ptx::mbar_arrive(&tfull[slot]);
-                } else {
-                    for (int kc = 0; kc < p.kchunks; ++kc)
-                        fv_issue<BN>(tmem_base + (slot * 2) * BN, tmem_base + (slot * 2 + 1) * BN, a_ring, res_desc,
-                                     full, empty, stage, phase, p.stages, A_BYTES >> 4, kc, p.kchunks,
-                                     kc == 0 ? 0u : 1u, (uint32_t)(p.parity & 1));
-                    ptx::mma_commit(&tfull[slot]);
-                }
+                for (int kc = 0; kc < p.kchunks; ++kc)
+                    fv_issue<BN, PAIR>(tmem_base + (slot * 2) * BN, tmem_base + (slot * 2 + 1) * BN, a_ring, res_desc,
+                                       full, empty, stage, phase, p.stages, A_BYTES >> 4, kc, p.kchunks,
+                                       kc == 0 ? 0u : 1u, (uint32_t)(p.parity & 1));
+                if constexpr (PAIR) ptx::mma_commit_2sm(&tfull[slot]);
+                else ptx::mma_commit(&tfull[slot]);
                 slot ^= 1;
                 if (slot == 0) sphase ^= 1;
             }
@@ -1076,13 +1089,15 @@ tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
         uint32_t sphase = 0;
         int ob = 0;
         uint32_t mphase0 = 0, mphase1 = 0;
-        if (p.has_mask && et == 0 && p.debug != 1 && (int)blockIdx.x < p.pairs) {
+        if (p.has_mask && et == 0 && p.debug != 1 && (int)(PAIR ? blockIdx.x / 2 : blockIdx.x) < (PAIR ? (p.pairs + 1) / 2 : p.pairs)) {
             int r0, j0, b;
-            fv_decode(p, blockIdx.x, &r0, &j0, &b);
+            fv_decode(p, PAIR ? (int)(blockIdx.x / 2) * 2 + (int)rank : (int)blockIdx.x, &r0, &j0, &b);
             ptx::mbar_arrive_expect_tx(&mbar[0], FT_OUT);
             ptx::tma_load_4d(&map_m0, &mbar[0], obuf, 0, j0, r0, b);
         }
-        for (int pr = blockIdx.x; pr < p.pairs; pr += gridDim.x) {
+        for (int wu = PAIR ? blockIdx.x / 2 : blockIdx.x; wu < (PAIR ? (p.pairs + 1) / 2 : p.pairs);
+             wu += PAIR ? gridDim.x / 2 : gridDim.x) {
+            const int pr = PAIR ? 2 * wu + (int)rank : wu;
             int r0, j0, b;
             fv_decode(p, pr, &r0, &j0, &b);
             ptx::mbar_wait(&tfull[slot], sphase);
@@ -1152,9 +1167,9 @@ tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
                         bool more = true;
                         if (nu == UNITS) {
                             nu = 0;
-                            const int np = pr + gridDim.x;
-                            more = np < p.pairs;
-                            if (more) fv_decode(p, np, &nr, &nj, &nb);
+                            const int nw = wu + (PAIR ? gridDim.x / 2 : gridDim.x);
+                            more = nw < (PAIR ? (p.pairs + 1) / 2 : p.pairs);
+                            if (more) fv_decode(p, PAIR ? 2 * nw + (int)rank : nw, &nr, &nj, &nb);
                         }
                         if (more) {
                             const int nv = nu / (BN / 64), nch = nu % (BN / 64);
@@ -1169,7 +1184,10 @@ tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[slot]);
+            if (lane == 0) {
+                if (PAIR) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[slot]), 0));
+                else ptx::mbar_arrive(&tempty[slot]);
+            }
             slot ^= 1;
             if (slot == 0) sphase ^= 1;
         }
@@ -1177,9 +1195,11 @@ tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) ptx::cluster_sync();  // the peer's smem / TMEM must outlive the leader's last MMA
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+        if constexpr (PAIR) ptx::tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+        else ptx::tmem_dealloc(tmem_base, TMEM_COLS);
     }
 }
 
@@ -1342,11 +1362,13 @@ static hex_status_t launch_ft(const CUtensorMap* maps, const FtParams& p, int sm
     return last_launch_status();
 }
 
-// view-pair plan: n = 1, resident weights, Cout 64 / 128; returns stages (0 = not eligible)
-static int fv_stages(const Geom& g, int Cin, int Cout, int* smem) {
+// view-pair plan: n = 1, resident weights, Cout 64 / 128; returns stages (0 = not eligible).  *pair: CTA
+// pairs (M = 256 per MMA, each CTA holding half of every weight tile), HEXCONV_FV_PAIR=1 (experiment)
+static int fv_stages(const Geom& g, int Cin, int Cout, int* smem, bool* pair) {
     if (g.n != 1 || g.s != 1 || Cin % 64 || (Cout != 64 && Cout != 128) || getenv("HEXCONV_NO_FWD_VPAIR")) return 0;
+    *pair = getenv("HEXCONV_FV_PAIR") != nullptr;
     const int A = (FT_RB + 3) * FT_JB * 128;
-    const int res_bytes = 7 * (Cin / 64) * Cout * 128;
+    const int res_bytes = 7 * (Cin / 64) * (*pair ? Cout / 2 : Cout) * 128;
     const int fixed = 2 * FT_OUT + 1024 + 512;
     int stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
     if (stages > 8) stages = 8;
@@ -1355,7 +1377,38 @@ static int fv_stages(const Geom& g, int Cin, int Cout, int* smem) {
     return stages;
 }
 
-static hex_status_t tc_fwd_vpair(const TcConvArgs& a, int stages, int smem, cudaStream_t st) {
+template <int BN, bool PAIR>
+static hex_status_t launch_fv(const CUtensorMap* maps, const FvParams& p, int smem, cudaStream_t st) {
+    auto kern = tc_fwd_vpair_kernel<BN, PAIR>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return HEX_ERR_CUDA;
+    if constexpr (PAIR) {
+        const int units = (p.pairs + 1) / 2;
+        const int clusters = units < num_sms() / 2 ? units : num_sms() / 2;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * clusters);
+        cfg.blockDim = dim3(FT_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p) !=
+            cudaSuccess)
+            return HEX_ERR_CUDA;
+    } else {
+        const int grid = p.pairs < num_sms() ? p.pairs : num_sms();
+        kern<<<grid, FT_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
+    }
+    count_launch();
+    return last_launch_status();
+}
+
+static hex_status_t tc_fwd_vpair(const TcConvArgs& a, int stages, int smem, bool pair, cudaStream_t st) {
     const Geom& g = a.g;
     FvParams p{};
     p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.parity = g.parity;
@@ -1366,13 +1419,13 @@ static hex_status_t tc_fwd_vpair(const TcConvArgs& a, int stages, int smem, cuda
     p.stages = stages;
     p.relu = a.relu;
     p.has_mask = a.relu_y != nullptr;
-    p.debug = getenv("HEXCONV_FT_DEBUG") ? atoi(getenv("HEXCONV_FT_DEBUG")) : 0;
-    p.prefetch = getenv("HEXCONV_FV_PREFETCH") ? atoi(getenv("HEXCONV_FV_PREFETCH")) : 0;  // measured no gain
+    p.debug = 0;
+    p.prefetch = 0;
     p.bias = a.bias;
     CUtensorMap maps[7];
     if (!ft_view5(&maps[0], a.x, g.B, g.H, g.W, a.Cin, 0, FT_RB + 3)) return HEX_ERR_CUDA;
     if (!ft_view5(&maps[1], a.x, g.B, g.H, g.W, a.Cin, 1, FT_RB + 3)) return HEX_ERR_CUDA;
-    if (!ft_wmap(&maps[2], a.wpack, g.T, a.Cout, a.Cin, a.Cout)) return HEX_ERR_CUDA;
+    if (!ft_wmap(&maps[2], a.wpack, g.T, a.Cout, a.Cin, pair ? a.Cout / 2 : a.Cout)) return HEX_ERR_CUDA;
     if (!ft_view4(&maps[3], a.y, g.B, g.H, g.W, a.Cout, 0)) return HEX_ERR_CUDA;
     if (!ft_view4(&maps[4], a.y, g.B, g.H, g.W, a.Cout, 1)) return HEX_ERR_CUDA;
     if (a.relu_y) {
@@ -1382,26 +1435,17 @@ static hex_status_t tc_fwd_vpair(const TcConvArgs& a, int stages, int smem, cuda
         maps[5] = maps[3];
         maps[6] = maps[4];
     }
-    const int grid = p.pairs < num_sms() ? p.pairs : num_sms();
-#define HEX_FV(BN_)                                                                                             \
-    {                                                                                                           \
-        auto kern = tc_fwd_vpair_kernel<BN_>;                                                                   \
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)       \
-            return HEX_ERR_CUDA;                                                                                \
-        kern<<<grid, FT_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p); \
-    }
-    if (a.Cout == 128) HEX_FV(128) else HEX_FV(64)
-#undef HEX_FV
-    count_launch();
-    return last_launch_status();
+    if (pair) return a.Cout == 128 ? launch_fv<128, true>(maps, p, smem, st) : launch_fv<64, true>(maps, p, smem, st);
+    return a.Cout == 128 ? launch_fv<128, false>(maps, p, smem, st) : launch_fv<64, false>(maps, p, smem, st);
 }
 
 hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
     {
         int smem = 0;
-        const int stages = fv_stages(g, a.Cin, a.Cout, &smem);
-        if (stages) return tc_fwd_vpair(a, stages, smem, st);
+        bool pair = false;
+        const int stages = fv_stages(g, a.Cin, a.Cout, &smem, &pair);
+        if (stages) return tc_fwd_vpair(a, stages, smem, pair, st);
     }
     const FtPlan pl = ft_plan(g, a.Cin, a.Cout);
     if (!pl.ok) return HEX_ERR_UNSUPPORTED;
