@@ -49,7 +49,7 @@ hex_status_t conv_geom(const hex_conv2d_desc_t* d, Geom* g) {
 
 // The tensor-core path: bf16, NHWC, stride 1 and channel counts that tile.
 bool use_tc_fwd(const hex_conv2d_desc_t* d, const Geom& g) {
-    return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_conv_supported(g, d->in_channels, d->out_channels);
+    return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_conv_fwd_supported(g, d->in_channels, d->out_channels);
 }
 bool use_tc_bwd_data(const hex_conv2d_desc_t* d, const Geom& g) {
     return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_conv_supported(g, d->out_channels, d->in_channels);

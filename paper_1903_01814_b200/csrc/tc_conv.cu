@@ -78,16 +78,17 @@ static bool make_view_map(CUtensorMap* m, const void* base, int B, int H, int W,
 // The same parity view with the channel axis split into 64-channel chunks as an
 // OUTER dimension: dims {64, H, Wp, B, C/64}, box {64, RB, JB, BB, KC}.  One TMA op
 // then fills KC consecutive canonical SW128 blocks (one per 64-channel chunk).
+// es2 = 2: rows and view sub-columns traversed with element stride 2 (stride-2 forward, tap_box)
 static bool make_view_map5(CUtensorMap* m, const void* base, int B, int H, int W, int C, int P, int RB, int JB,
-                           int BB, int KC) {
+                           int BB, int KC, int es2 = 1) {
     auto enc = get_encode();
     if (!enc) return false;
     const int Wp = (W - P + 1) / 2;
     if (Wp < 1 || C % 64) return false;
     cuuint64_t dims[5] = {64, (cuuint64_t)H, (cuuint64_t)Wp, (cuuint64_t)B, (cuuint64_t)(C / 64)};
     cuuint64_t strides[4] = {(cuuint64_t)W * C * 2, (cuuint64_t)2 * C * 2, (cuuint64_t)H * W * C * 2, 128};
-    cuuint32_t box[5] = {64, (cuuint32_t)RB, (cuuint32_t)JB, (cuuint32_t)BB, (cuuint32_t)KC};
-    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    cuuint32_t box[5] = {64, (cuuint32_t)(RB * es2), (cuuint32_t)(JB * es2), (cuuint32_t)BB, (cuuint32_t)KC};
+    cuuint32_t es[5] = {1, (cuuint32_t)es2, (cuuint32_t)es2, 1, 1};
     void* addr = (void*)((const char*)base + (size_t)P * C * 2);
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, addr, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -147,6 +148,7 @@ static void choose_box(int B, int H, int W, int npix, int* RB, int* JB, int* BB)
 // ------------------------------------------------------------------ forward kernel
 struct TcFwdParams {
     int B, H, W, Cin, Cout, T, parity;
+    int s;  // 1, or 2: output column-parity classes e = C mod 2 read stride-2 input boxes (see tap_box)
     int RB, JB, BB;
     int rt, bt, jt0, jt1;  // tiles along rows, batch, and sub-columns of view 0 / view 1
     int tiles0;            // m tiles of view 0
@@ -195,6 +197,24 @@ __device__ __forceinline__ TileCoord decode_pair_tile(const TcFwdParams& p, int 
     }
     tc = decode_fwd_tile(p, m * p.n_tiles + nt, BN);
     return tc;
+}
+
+// Input box of tap (dc, dr) for an output tile of class P at (r0, j0):
+//   s = 1: output view P = tensor columns P::2; input view (P + dc) mod 2, sub-column j0 + shift, row r0 + dr
+//   s = 2: output class P = columns C = 2C' + P (centre row 2R + P, centre column 4C' + 2P, A5:
+//          rho(C) = C mod 2); the maps traverse rows and view sub-columns with element stride 2, so the
+//          box starts at input view dc mod 2, sub-column 2 j0 + (2P + dc - Pv) / 2, row 2 r0 + P + dr.
+__device__ __forceinline__ void tap_box(const TcFwdParams& p, int P, int r0, int j0, int dc, int dr, int* Pv,
+                                        int* row, int* col) {
+    if (p.s == 1) {
+        *Pv = (P + dc) & 1;
+        *col = j0 + (P + dc - *Pv) / 2;
+        *row = r0 + dr;
+    } else {
+        *Pv = dc & 1;
+        *col = 2 * j0 + (2 * P + dc - *Pv) / 2;
+        *row = 2 * r0 + P + dr;
+    }
 }
 
 // KC = 64-channel chunks per K iteration (one TMA op each for A and B).
@@ -386,17 +406,17 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
                 const TileCoord tc = decode_fwd_tile(p, tile, BN);
-                const int pc = (tc.P + p.parity) & 1;
+                const int pc = p.s == 1 ? (tc.P + p.parity) & 1 : p.parity & 1;  // centre column parity
                 for (int t = 0; t < p.T; ++t) {
                     const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
-                    const int Pv = (tc.P + dc) & 1;
-                    const int jsh = (tc.P + dc - Pv) / 2;
+                    int Pv, row, col;
+                    tap_box(p, tc.P, tc.r0, tc.j0, dc, dr, &Pv, &row, &col);
                     const CUtensorMap* mx = Pv ? &map_x1 : &map_x0;
                     for (int kg = 0; kg < kgroups; ++kg) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sa = smem + stage * STAGE;
                         ptx::mbar_arrive_expect_tx(&full[stage], STAGE);
-                        ptx::tma_load_5d(mx, &full[stage], sa, 0, tc.r0 + dr, tc.j0 + jsh, tc.b0, kg * KC);
+                        ptx::tma_load_5d(mx, &full[stage], sa, 0, row, col, tc.b0, kg * KC);
                         if constexpr (!RESB)
                             ptx::tma_load_4d(&map_w, &full[stage], sa + Cfg::A_BYTES, 0, tc.n0, kg * KC, t);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -518,17 +538,17 @@ tc_conv_fwd2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
             uint32_t phase = 0;
             for (int tile = first; tile < p.pair_tiles; tile += step) {
                 const TileCoord tc = decode_pair_tile(p, tile, BN, rank);
-                const int pc = (tc.P + p.parity) & 1;
+                const int pc = p.s == 1 ? (tc.P + p.parity) & 1 : p.parity & 1;  // centre column parity
                 for (int t = 0; t < p.T; ++t) {
                     const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
-                    const int Pv = (tc.P + dc) & 1;
-                    const int jsh = (tc.P + dc - Pv) / 2;
+                    int Pv, row, col;
+                    tap_box(p, tc.P, tc.r0, tc.j0, dc, dr, &Pv, &row, &col);
                     const CUtensorMap* mx = Pv ? &map_x1 : &map_x0;
                     for (int kg = 0; kg < kgroups; ++kg) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sa = smem + stage * Cfg::STAGE;
                         if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
-                        ptx::tma_load_5d_2sm(mx, &full[stage], sa, 0, tc.r0 + dr, tc.j0 + jsh, tc.b0, kg * KC);
+                        ptx::tma_load_5d_2sm(mx, &full[stage], sa, 0, row, col, tc.b0, kg * KC);
                         ptx::tma_load_4d_2sm(&map_w, &full[stage], sa + Cfg::A_BYTES, 0, tc.n0 + (int)rank * (BN / 2),
                                              kg * KC, t);
                         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
@@ -620,6 +640,16 @@ static int pick_bn(int Cout) {
     return 0;
 }
 
+// forward only: stride 2 runs the same kernels with stride-2 input boxes (tap_box); backward passes of
+// strided layers stay on the CUDA-core kernels
+bool tc_conv_fwd_supported(const Geom& g, int Cin, int Cout) {
+    if (g.s == 1) return tc_conv_supported(g, Cin, Cout);
+    if (g.s != 2 || g.T > TC_MAXT || getenv("HEXCONV_NO_TC_STRIDE2")) return false;
+    if (Cin % TC_BK != 0 || pick_bn(Cout) == 0 || g.Wo < 2) return false;
+    if (getenv("HEXCONV_DISABLE_TC")) return false;
+    return get_encode() != nullptr;
+}
+
 bool tc_conv_supported(const Geom& g, int Cin, int Cout) {
     if (g.s != 1 || g.T > TC_MAXT) return false;
     if (Cin % TC_BK != 0 || pick_bn(Cout) == 0) return false;
@@ -699,11 +729,13 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
     TcFwdParams p{};
     p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
-    choose_box(g.B, g.H, g.W, TC_BM, &p.RB, &p.JB, &p.BB);
-    p.rt = ceil_div(g.H, p.RB);
+    p.s = g.s;
+    const int OH = g.s == 1 ? g.H : g.Ho, OW = g.s == 1 ? g.W : g.Wo;  // output grid (tiles, stores)
+    choose_box(g.B, OH, OW, TC_BM, &p.RB, &p.JB, &p.BB);
+    p.rt = ceil_div(OH, p.RB);
     p.bt = ceil_div(g.B, p.BB);
-    p.jt0 = ceil_div((g.W + 1) / 2, p.JB);
-    p.jt1 = ceil_div(g.W / 2, p.JB);
+    p.jt0 = ceil_div((OW + 1) / 2, p.JB);
+    p.jt1 = ceil_div(OW / 2, p.JB);
     p.tiles0 = p.rt * p.jt0 * p.bt;
     const int BN = pick_bn(a.Cout);
     p.n_tiles = a.Cout / BN;
@@ -729,15 +761,15 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
             p.tap_dr[pc][t] = (int8_t)dr;
         }
     CUtensorMap mx0, mx1, mw;
-    if (!make_view_map5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, p.RB, p.JB, p.BB, KC)) return HEX_ERR_CUDA;
-    if (!make_view_map5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, p.RB, p.JB, p.BB, KC)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, p.RB, p.JB, p.BB, KC, g.s)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, p.RB, p.JB, p.BB, KC, g.s)) return HEX_ERR_CUDA;
     if (!make_weight_map4(&mw, a.wpack, g.T, a.Cout, a.Cin, pair ? BN / 2 : BN, KC)) return HEX_ERR_CUDA;
     CUtensorMap my0, my1, mm0, mm1;
-    if (!make_view_map(&my0, a.y, g.B, g.H, g.W, a.Cout, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
-    if (!make_view_map(&my1, a.y, g.B, g.H, g.W, a.Cout, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
+    if (!make_view_map(&my0, a.y, g.B, OH, OW, a.Cout, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
+    if (!make_view_map(&my1, a.y, g.B, OH, OW, a.Cout, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
     if (a.relu_y) {
-        if (!make_view_map(&mm0, a.relu_y, g.B, g.H, g.W, a.Cout, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
-        if (!make_view_map(&mm1, a.relu_y, g.B, g.H, g.W, a.Cout, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
+        if (!make_view_map(&mm0, a.relu_y, g.B, OH, OW, a.Cout, 0, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
+        if (!make_view_map(&mm1, a.relu_y, g.B, OH, OW, a.Cout, 1, p.RB, p.JB, p.BB)) return HEX_ERR_CUDA;
     } else {
         mm0 = my0;
         mm1 = my1;

@@ -346,3 +346,13 @@ def test_custom_ring_kernel_smoothing(F, oracle):
                             (1, -1): -1.0, (-1, 1): -1.0})
     ye = F.conv2d_fwd(torch.full((1, 1, 9, 9), 2.0, device="cuda"), e, None, n=1)
     assert ye[0, 0, 1:-1, 1:-1].abs().max().item() == 0.0
+
+
+@pytest.mark.parametrize("pi", [0, 1])
+def test_conv_stride2_tensor_core_forward(F, oracle, pi):
+    # bf16 NHWC stride 2: the forward runs the tcgen05 kernel with stride-2 input
+    # boxes per output column-parity class; backward passes of strided layers use the CUDA-core kernels
+    for k, (B, Cin, Cout, H, W, n) in enumerate([(2, 64, 64, 20, 23, 1), (1, 128, 256, 31, 30, 2),
+                                                  (3, 64, 128, 9, 8, 1), (1, 64, 64, 5, 6, 2)]):
+        assert F.conv_algo(B, Cin, Cout, H, W, n, 2, pi, torch.bfloat16, "NHWC", 0) == "tcgen05"
+        _conv_case(F, oracle, pi, n, 2, H, W, B, Cin, Cout, torch.bfloat16, "NHWC", 1300 + k)
