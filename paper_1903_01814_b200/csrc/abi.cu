@@ -67,6 +67,29 @@ bool use_tc_wgrad(const hex_conv2d_desc_t* d, const Geom& g) {
     return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_wgrad_supported(g, d->in_channels, d->out_channels);
 }
 
+// strided layers: the backward passes run the stride-1 tensor-core kernels on dy scattered onto the
+// full grid (strided.cu)
+Geom stride1(const Geom& g) {
+    Geom g1 = g;
+    g1.s = 1;
+    g1.Ho = g.H;
+    g1.Wo = g.W;
+    return g1;
+}
+bool strided_tc_ok(const hex_conv2d_desc_t* d, const Geom& g) {
+    return g.s > 1 && d->dtype == HEX_BF16 && d->layout == HEX_NHWC && d->out_channels % 8 == 0 &&
+           !getenv("HEXCONV_NO_TC_STRIDED_BWD");
+}
+bool use_tc_bwd_data_up(const hex_conv2d_desc_t* d, const Geom& g) {
+    return strided_tc_ok(d, g) && tc_conv_supported(stride1(g), d->out_channels, d->in_channels);
+}
+bool use_tc_wgrad_up(const hex_conv2d_desc_t* d, const Geom& g) {
+    return strided_tc_ok(d, g) && tc_wgrad_supported(stride1(g), d->in_channels, d->out_channels);
+}
+size_t up_bytes(const hex_conv2d_desc_t* d, const Geom& g) {  // + slack for aligning it and what follows
+    return (size_t)g.B * g.H * g.W * d->out_channels * 2 + 2048;
+}
+
 size_t packed_weight_bytes(const hex_conv2d_desc_t* d, const Geom& g) {
     return (size_t)g.T * d->out_channels * d->in_channels * 2 + 1024;
 }
@@ -150,9 +173,15 @@ hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* d, int32_t pass,
     if (st != HEX_OK) return st;
     switch (pass) {
         case 0: *bytes = use_tc_fwd(d, g) ? packed_weight_bytes(d, g) : 0; return HEX_OK;
-        case 1: *bytes = use_tc_bwd_data(d, g) ? packed_weight_bytes(d, g) : 0; return HEX_OK;
+        case 1:
+            *bytes = use_tc_bwd_data(d, g)      ? packed_weight_bytes(d, g)
+                     : use_tc_bwd_data_up(d, g) ? up_bytes(d, g) + packed_weight_bytes(d, g)
+                                                : 0;
+            return HEX_OK;
         case 2:
-            *bytes = use_tc_wgrad(d, g)  ? tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
+            *bytes = use_tc_wgrad(d, g)      ? tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
+                     : use_tc_wgrad_up(d, g) ? up_bytes(d, g) + tc_wgrad_ws_bytes(stride1(g), d->in_channels,
+                                                                                   d->out_channels)
                      : use_smallc(d, g) ? smallc_wgrad_ws_bytes(g, d->out_channels)
                      : use_c1(d, g)     ? c1_wgrad_ws_bytes(g, d->out_channels)
                      : use_f32wg(d, g)  ? f32_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
@@ -169,8 +198,8 @@ hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* d, int32_t pass, int32_t* 
     if (st != HEX_OK) return st;
     switch (pass) {
         case 0: *algo = use_tc_fwd(d, g) ? 1 : 0; return HEX_OK;
-        case 1: *algo = use_tc_bwd_data(d, g) ? 1 : 0; return HEX_OK;
-        case 2: *algo = use_tc_wgrad(d, g) ? 1 : 0; return HEX_OK;
+        case 1: *algo = use_tc_bwd_data(d, g) || use_tc_bwd_data_up(d, g) ? 1 : 0; return HEX_OK;
+        case 2: *algo = use_tc_wgrad(d, g) || use_tc_wgrad_up(d, g) ? 1 : 0; return HEX_OK;
         default: return HEX_ERR_INVALID_ARG;
     }
 }
@@ -259,6 +288,19 @@ hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* d, const void* dy, con
         a.x = dy; a.wpack = wp; a.bias = nullptr; a.y = dx; a.relu_y = relu_y; a.relu = 0;
         return tc_conv_fwd(a, s);
     }
+    if (use_tc_bwd_data_up(d, g)) {  // stride s: the stride-1 bwd-data of dy scattered onto the full grid
+        if (!aligned16(dy) || !aligned16(dx) || !aligned16(w) || (relu_y && !aligned16(relu_y)))
+            return HEX_ERR_ALIGNMENT;
+        if (!ws || ws_bytes < up_bytes(d, g) + packed_weight_bytes(d, g)) return HEX_ERR_WORKSPACE;
+        void* up = align_up(ws, 1024);
+        void* wp = align_up((char*)up + (up_bytes(d, g) - 2048), 1024);
+        if ((st = lattice_upsample(dy, up, g, d->out_channels, s)) != HEX_OK) return st;
+        if ((st = tc_pack_weights(w, wp, d->out_channels, d->in_channels, g.T, 1, s)) != HEX_OK) return st;
+        TcConvArgs a{};
+        a.g = stride1(g); a.Cin = d->out_channels; a.Cout = d->in_channels;
+        a.x = up; a.wpack = wp; a.bias = nullptr; a.y = dx; a.relu_y = relu_y; a.relu = 0;
+        return tc_conv_fwd(a, s);
+    }
     if (tiled_supported(g, d->dtype, d->layout))
         return tiled_conv((const float*)dy, (const float*)w, nullptr, (const float*)relu_y, (float*)dx, g,
                           d->out_channels, d->in_channels, 0, 1, s);
@@ -283,6 +325,19 @@ hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* d, const void* x, co
         a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
         a.x = x; a.dy = dy; a.dw = dw; a.dbias = dbias; a.accumulate = accumulate;
         return tc_conv_wgrad(a, ws, ws_bytes, s);
+    }
+    if (use_tc_wgrad_up(d, g)) {  // stride s: the stride-1 weight gradient against dy on the full grid
+        if (!aligned16(x) || !aligned16(dy)) return HEX_ERR_ALIGNMENT;
+        const Geom g1 = stride1(g);
+        const size_t ub = up_bytes(d, g), need = tc_wgrad_ws_bytes(g1, d->in_channels, d->out_channels);
+        if (!ws || ws_bytes < ub + need) return HEX_ERR_WORKSPACE;
+        void* up = align_up(ws, 1024);
+        char* rest = (char*)align_up((char*)up + (ub - 2048), 1024);
+        if ((st = lattice_upsample(dy, up, g, d->out_channels, s)) != HEX_OK) return st;
+        TcWgradArgs a{};
+        a.g = g1; a.Cin = d->in_channels; a.Cout = d->out_channels;
+        a.x = x; a.dy = up; a.dw = dw; a.dbias = dbias; a.accumulate = accumulate;
+        return tc_conv_wgrad(a, rest, ws_bytes - (size_t)(rest - (char*)ws), s);
     }
     if (use_smallc(d, g)) {
         const size_t need = smallc_wgrad_ws_bytes(g, d->out_channels);

@@ -61,6 +61,8 @@ struct TcConvArgs {
 };
 bool tc_conv_supported(const Geom& g, int Cin, int Cout);
 bool tc_conv_fwd_supported(const Geom& g, int Cin, int Cout);  // also stride 2
+// strided.cu: dy of a stride-s layer scattered onto the full grid (bf16 NHWC, C % 8 == 0)
+hex_status_t lattice_upsample(const void* dy, void* up, const Geom& g, int C, cudaStream_t st);
 bool tc_fwd_tr_supported(const Geom& g, int Cin, int Cout);  // tap-reuse forward (tc_fwd_tr.cu)
 hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st);
 // fused maxpool_{n=1,s=2}(relu(conv(x) + bias)) (tc_fwd_tr.cu); the conv output is not materialised

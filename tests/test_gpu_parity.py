@@ -356,3 +356,14 @@ def test_conv_stride2_tensor_core_forward(F, oracle, pi):
                                                   (3, 64, 128, 9, 8, 1), (1, 64, 64, 5, 6, 2)]):
         assert F.conv_algo(B, Cin, Cout, H, W, n, 2, pi, torch.bfloat16, "NHWC", 0) == "tcgen05"
         _conv_case(F, oracle, pi, n, 2, H, W, B, Cin, Cout, torch.bfloat16, "NHWC", 1300 + k)
+
+
+@pytest.mark.parametrize("s", [2, 3])
+def test_conv_strided_tensor_core_backward(F, oracle, s):
+    # strided backward passes (f4): the stride-1 tcgen05 bwd-data / wgrad on dy scattered onto the full
+    # grid (strided.cu; pin P10: a strided conv is the stride-1 conv sampled at the lattice centres)
+    for k, (B, Cin, Cout, H, W, n, pi) in enumerate([(2, 64, 128, 20, 23, 1, 0), (1, 128, 128, 17, 16, 2, 1),
+                                                      (2, 64, 128, 9, 12, 1, 1)]):
+        assert F.conv_algo(B, Cin, Cout, H, W, n, s, pi, torch.bfloat16, "NHWC", 1) == "tcgen05"
+        assert F.conv_algo(B, Cin, Cout, H, W, n, s, pi, torch.bfloat16, "NHWC", 2) == "tcgen05"
+        _conv_case(F, oracle, pi, n, s, H, W, B, Cin, Cout, torch.bfloat16, "NHWC", 1400 + 10 * s + k)
