@@ -260,12 +260,15 @@ smallc_mma_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict
                 const int c = c0 + g + 8 * h;
                 if (c >= W) continue;
                 uint32_t pk[8];
+                if (relu) {  // ReLU inside the conversion (cvt.rn.relu: negatives and -0 give +0)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    float a = acc[j][2 * h], bb = acc[j][2 * h + 1];
-                    if (relu) { a = fmaxf(a, 0.f); bb = fmaxf(bb, 0.f); }
-                    __nv_bfloat162 hv = __floats2bfloat162_rn(a, bb);
-                    pk[j] = *reinterpret_cast<uint32_t*>(&hv);
+                    for (int j = 0; j < 8; ++j) pk[j] = ptx::pack_bf16x2_relu(acc[j][2 * h], acc[j][2 * h + 1]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        __nv_bfloat162 hv = __floats2bfloat162_rn(acc[j][2 * h], acc[j][2 * h + 1]);
+                        pk[j] = *reinterpret_cast<uint32_t*>(&hv);
+                    }
                 }
                 uint4* dst = reinterpret_cast<uint4*>(y + (((int64_t)b * H + r) * W + c) * Cout + co0);
                 dst[tig] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
