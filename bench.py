@@ -345,7 +345,7 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the config 2-4 measurements")
-    ap.add_argument("--no-graph", action="store_true", help="e2e leg without CUDA-graph replay")
+    ap.add_argument("--no-graph", action="store_true", help="device-timed and e2e legs as eager steps (no CUDA graph)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
