@@ -521,14 +521,22 @@ struct FpParams {
 struct FpTile {
     int b, k, r0;
     bool strip, first, last;
+    bool valid;  // false: a CTA-pair tail slot with no region (loads zero fill, nothing is stored)
 };
 
-// the seq-th tile of this CTA; false past the end
+// the seq-th tile of this CTA; false past the end.  CTA pairs (PAIR): the two CTAs of a cluster walk
+// strips 2u and 2u+1 (regions likewise) in lockstep; both CTAs end together.
+template <bool PAIR>
 __device__ __forceinline__ bool fp_tile(const FpParams& p, int seq, FpTile& tl) {
+    const int cid = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int ncl = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int rank = PAIR ? (int)(blockIdx.x & 1) : 0;
+    const int per = PAIR ? 2 : 1;
     const int ns = p.full_rounds * p.ntr;
+    tl.valid = true;
     if (seq < ns) {
         const int j = seq / p.ntr, t = seq - j * p.ntr;
-        const int strip = blockIdx.x + j * gridDim.x;
+        const int strip = (cid + j * ncl) * per + rank;
         tl.b = strip / p.nc;
         tl.k = strip - tl.b * p.nc;
         tl.r0 = FT_RB * t;
@@ -537,15 +545,27 @@ __device__ __forceinline__ bool fp_tile(const FpParams& p, int seq, FpTile& tl) 
         tl.last = t == p.ntr - 1;
         return true;
     }
-    const int rg = blockIdx.x + (seq - ns) * gridDim.x;
-    if (rg >= p.left_regions) return false;
-    const int strip = p.full_rounds * gridDim.x + rg / p.nr;
+    const int rgu = cid + (seq - ns) * ncl;
+    if (rgu * per >= p.left_regions) return false;
+    int rg = rgu * per + rank;
+    if (rg >= p.left_regions) {  // pair tail: a slot without a region
+        tl.valid = false;
+        rg = p.left_regions - 1;
+    }
+    const int strip = p.full_rounds * ncl * per + rg / p.nr;
     const int i = rg % p.nr;
     tl.b = strip / p.nc;
     tl.k = strip - tl.b * p.nc;
-    tl.r0 = 14 * i - 1;
+    tl.r0 = tl.valid ? 14 * i - 1 : p.H + 64;
     tl.strip = tl.first = tl.last = false;
     return true;
+}
+
+// one tap group of the view-pair MMA sequences: cta_group::1, or ::2 (M = 256 over a CTA pair)
+template <int BN, int CNT, bool PAIR>
+__device__ __forceinline__ void fv_group(uint32_t d, uint64_t ad, uint64_t bd, int bs, uint32_t first) {
+    if constexpr (PAIR) issue_stage_pair<BN, CNT>(d, ad, bd, bs, first);
+    else issue_stage<BN, CNT, true>(d, ad, bd, bs, first);
 }
 
 // n = 1 MMA sequence of one tile pair (view-0 tile -> accumulator d0, view-1 tile -> d1) from four
@@ -557,36 +577,38 @@ __device__ __forceinline__ bool fp_tile(const FpParams& p, int seq, FpTile& tl) 
 //   box 2 = view 0 at 7k:              view-0 dc =  0 (taps 2..4) and view-1 dc = +1 (taps 5,6)
 //   box 3 = view 1 at 7k:              view-0 dc = +1 (taps 5,6)
 // A side column of view P starts pc_P = (P + parity) mod 2 rows below the box top.
-template <int BN>
+template <int BN, bool PAIR>
 __device__ __forceinline__ void fp_issue_n1(uint32_t d0, uint32_t d1, uint64_t a_ring, uint64_t res_desc,
                                             uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
                                             int nstages, uint32_t stage16, int kc, int kchunks, uint32_t first,
                                             uint32_t pc0) {
+    constexpr int BROWS = PAIR ? BN / 2 : BN;  // weight rows held per CTA
     const uint64_t o0 = (uint64_t)(pc0 * 64), o1 = (uint64_t)((pc0 ^ 1u) * 64);  // 1024-byte rows
-    const int bs = kchunks * BN * 8;
-    const uint64_t w0 = res_desc + (uint64_t)(kc * (BN * 8));  // tap t at w0 + t * bs
+    const int bs = kchunks * BROWS * 8;
+    const uint64_t w0 = res_desc + (uint64_t)(kc * (BROWS * 8));  // tap t at w0 + t * bs
 #pragma unroll
     for (int bx = 0; bx < 4; ++bx) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         const uint64_t ad = a_ring + (uint64_t)stage * stage16;
         if (bx == 0) {
-            issue_stage<BN, 2, true>(d1, ad + o1, w0, bs, first);
+            fv_group<BN, 2, PAIR>(d1, ad + o1, w0, bs, first);
         } else if (bx == 1) {
-            issue_stage<BN, 2, true>(d0, ad + o0, w0, bs, first);
-            issue_stage<BN, 3, true>(d1, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
+            fv_group<BN, 2, PAIR>(d0, ad + o0, w0, bs, first);
+            fv_group<BN, 3, PAIR>(d1, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
         } else if (bx == 2) {
-            issue_stage<BN, 3, true>(d0, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
-            issue_stage<BN, 2, true>(d1, ad + o1, w0 + (uint64_t)(5 * bs), bs, 1u);
+            fv_group<BN, 3, PAIR>(d0, ad, w0 + (uint64_t)(2 * bs), bs, 1u);
+            fv_group<BN, 2, PAIR>(d1, ad + o1, w0 + (uint64_t)(5 * bs), bs, 1u);
         } else {
-            issue_stage<BN, 2, true>(d0, ad + o0, w0 + (uint64_t)(5 * bs), bs, 1u);
+            fv_group<BN, 2, PAIR>(d0, ad + o0, w0 + (uint64_t)(5 * bs), bs, 1u);
         }
-        ptx::mma_commit(&empty[stage]);
+        if constexpr (PAIR) ptx::mma_commit_2sm(&empty[stage]);
+        else ptx::mma_commit(&empty[stage]);
         if (++stage == nstages) { stage = 0; phase ^= 1; }
     }
 }
 
-template <int BN, int N>
+template <int BN, int N, bool PAIR>
 __global__ void __launch_bounds__(FP_THREADS, 1)
 tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                        const __grid_constant__ CUtensorMap map_w, const __grid_constant__ FpParams p) {
@@ -597,9 +619,11 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
     constexpr int TMEM_COLS = 4 * BN;  // 2 slots x 2 views
     constexpr int NCH = BN / 32;       // 32-channel chunks per tile
     constexpr uint32_t NEG_INF2 = 0xFF80FF80u;
+    static_assert(!PAIR || N == 1, "CTA pairs: n = 1 only");
+    constexpr int W_CTA = PAIR ? W_TILE / 2 : W_TILE;  // this CTA's rows of one (tap, chunk) weight tile
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned
-    const int res_bytes = p.T * p.kchunks * W_TILE;
+    const int res_bytes = p.T * p.kchunks * W_CTA;
     uint8_t* resw = base;
     uint8_t* ring = base + res_bytes;
     uint8_t* region = ring + p.stages * A_BYTES;  // [buffer][view][row][sub-column][64 B]
@@ -613,11 +637,13 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
     uint32_t* tmem_slot = (uint32_t*)(bres + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < p.stages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 8);  // the converter warps
+            ptx::mbar_init(&tempty[a], PAIR ? 16 : 8);  // the converter warps (of both CTAs of a pair)
         }
         ptx::mbar_init(bres, 1);
         ptx::fence_barrier_init();
@@ -625,7 +651,10 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
         ptx::prefetch_tmap(&map_x1);
         ptx::prefetch_tmap(&map_w);
     }
-    if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    if (warp == 1) {
+        if constexpr (PAIR) ptx::tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+        else ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    }
     if (threadIdx.x >= 64) {  // region row 18 (r0 + 16) is only read on a strip's last tile: below the image
         const int e = threadIdx.x - 64;
         if (p.bias && e < BN) sbias[e] = p.bias[e];
@@ -636,29 +665,44 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
         }
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) ptx::cluster_sync();
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(bres, (uint32_t)res_bytes);
-            for (int t = 0; t < p.T; ++t)
-                for (int kc = 0; kc < p.kchunks; ++kc)
-                    ptx::tma_load_4d(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0, 0, kc, t);
+            if constexpr (PAIR) {  // each CTA holds its half of every weight tile; bytes land on the leader
+                if (leader) ptx::mbar_arrive_expect_tx(bres, (uint32_t)(2 * res_bytes));
+                for (int t = 0; t < p.T; ++t)
+                    for (int kc = 0; kc < p.kchunks; ++kc)
+                        ptx::tma_load_4d_2sm(&map_w, bres, resw + (t * p.kchunks + kc) * W_CTA, 0,
+                                             (int)rank * (BN / 2), kc, t);
+            } else {
+                ptx::mbar_arrive_expect_tx(bres, (uint32_t)res_bytes);
+                for (int t = 0; t < p.T; ++t)
+                    for (int kc = 0; kc < p.kchunks; ++kc)
+                        ptx::tma_load_4d(&map_w, bres, resw + (t * p.kchunks + kc) * W_TILE, 0, 0, kc, t);
+            }
             int stage = 0;
             uint32_t phase = 0;
             FpTile tl;
-            for (int seq = 0; fp_tile(p, seq, tl); ++seq) {
+            for (int seq = 0; fp_tile<PAIR>(p, seq, tl); ++seq) {
                 if constexpr (N == 1) {
                     for (int kc = 0; kc < p.kchunks; ++kc)
 #pragma unroll
                         for (int bx = 0; bx < 4; ++bx) {
                             ptx::mbar_wait(&empty[stage], phase ^ 1);
                             uint8_t* sa = ring + stage * A_BYTES;
-                            ptx::mbar_arrive_expect_tx(&full[stage], A_BYTES);
-                            ptx::tma_load_5d((bx & 1) ? &map_x1 : &map_x0, &full[stage], sa, 0,
-                                             7 * tl.k - (bx < 2 ? 1 : 0), tl.r0 - 1, tl.b, kc);
+                            const CUtensorMap* mx = (bx & 1) ? &map_x1 : &map_x0;
+                            const int jj = 7 * tl.k - (bx < 2 ? 1 : 0);
+                            if constexpr (PAIR) {
+                                if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * A_BYTES);
+                                ptx::tma_load_5d_2sm(mx, &full[stage], sa, 0, jj, tl.r0 - 1, tl.b, kc);
+                            } else {
+                                ptx::mbar_arrive_expect_tx(&full[stage], A_BYTES);
+                                ptx::tma_load_5d(mx, &full[stage], sa, 0, jj, tl.r0 - 1, tl.b, kc);
+                            }
                             if (++stage == p.stages) { stage = 0; phase ^= 1; }
                         }
                     continue;
@@ -685,7 +729,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && (!PAIR || leader)) {
             const uint64_t a_ring = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
             const uint64_t res_desc = ptx::smem_desc_sw128(ptx::smem_u32(resw), 16, 1024);
             int stage = 0;
@@ -694,10 +738,10 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
             uint32_t sphase = 0;
             ptx::mbar_wait(bres, 0);
             FpTile tl;
-            for (int seq = 0; fp_tile(p, seq, tl); ++seq) {
+            for (int seq = 0; fp_tile<PAIR>(p, seq, tl); ++seq) {
                 ptx::mbar_wait(&tempty[slot], sphase ^ 1);
                 ptx::tc_fence_after();
-                if (p.debug == 2) {
+                if (!PAIR && p.debug == 2) {
                     for (int u = 0; u < (N == 1 ? 4 : 2 * SL::count()) * p.kchunks; ++u) {
                         ptx::mbar_wait(&full[stage], phase);
                         ptx::mbar_arrive(&empty[stage]);
@@ -710,9 +754,9 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
                 }
                 if constexpr (N == 1) {
                     for (int kc = 0; kc < p.kchunks; ++kc)
-                        fp_issue_n1<BN>(tmem_base + (slot * 2) * BN, tmem_base + (slot * 2 + 1) * BN, a_ring, res_desc,
-                                        full, empty, stage, phase, p.stages, A_BYTES >> 4, kc, p.kchunks,
-                                        kc == 0 ? 0u : 1u, (uint32_t)(p.parity & 1));
+                        fp_issue_n1<BN, PAIR>(tmem_base + (slot * 2) * BN, tmem_base + (slot * 2 + 1) * BN, a_ring,
+                                              res_desc, full, empty, stage, phase, p.stages, A_BYTES >> 4, kc,
+                                              p.kchunks, kc == 0 ? 0u : 1u, (uint32_t)(p.parity & 1));
                 } else {
                     for (int v = 0; v < 2; ++v) {
                         const uint32_t d = tmem_base + (slot * 2 + v) * BN;
@@ -723,7 +767,8 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
                                                                          kc == 0 ? 0u : 1u);
                     }
                 }
-                ptx::mma_commit(&tfull[slot]);
+                if constexpr (PAIR) ptx::mma_commit_2sm(&tfull[slot]);
+                else ptx::mma_commit(&tfull[slot]);
                 slot ^= 1;
                 if (slot == 0) sphase ^= 1;
             }
@@ -745,13 +790,13 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
         uint32_t sphase = 0;
         int g = 0;  // chunk counter (buffer g & 1)
         FpTile tl;
-        for (int seq = 0; fp_tile(p, seq, tl); ++seq) {
+        for (int seq = 0; fp_tile<PAIR>(p, seq, tl); ++seq) {
             const int img_r = tl.r0 + (row >> 3);
             const int jv = 7 * tl.k - cv + (row & 7);  // sub-column of this pixel in view cv
             const bool outside = img_r < 0 || img_r >= p.H || jv < 0 || 2 * jv + cv >= p.W;
             ptx::mbar_wait(&tfull[slot], sphase);
             ptx::tc_fence_after();
-            if (p.debug == 1) {
+            if (!PAIR && p.debug == 1) {
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&tempty[slot]);
@@ -805,7 +850,10 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
                 if (c + 1 == NCH) {  // TMEM slot fully read: the MMA may refill it
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&tempty[slot]);
+                    if (lane == 0) {
+                        if constexpr (PAIR) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[slot]), 0));
+                        else ptx::mbar_arrive(&tempty[slot]);
+                    }
                 }
                 ptx::named_bar_arrive(FP_BAR_FULL + bf, 512);
             }
@@ -826,7 +874,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
         const int kcar = kv * 1024 + kr * 512 + ks * FP_PIX + ki * 16;
         int g = 0;
         FpTile tl;
-        for (int seq = 0; p.debug != 1 && fp_tile(p, seq, tl); ++seq) {
+        for (int seq = 0; (PAIR || p.debug != 1) && fp_tile<PAIR>(p, seq, tl); ++seq) {
             const int C = 7 * tl.k + wc;
             const int rho = C & 1;  // centre row of window (R, C): cr = 2R + rho
             // owned centre rows [lo, hi]
@@ -893,9 +941,11 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) ptx::cluster_sync();  // the peer's smem / TMEM must outlive the leader's last MMA
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+        if constexpr (PAIR) ptx::tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+        else ptx::tmem_dealloc(tmem_base, TMEM_COLS);
     }
 }
 
@@ -915,12 +965,6 @@ struct FvParams {
     int rt, jt, pairs, kchunks, stages, relu, has_mask, debug, prefetch;
     const float* bias;
 };
-
-template <int BN, int CNT, bool PAIR>
-__device__ __forceinline__ void fv_group(uint32_t d, uint64_t ad, uint64_t bd, int bs, uint32_t first) {
-    if constexpr (PAIR) issue_stage_pair<BN, CNT>(d, ad, bd, bs, first);
-    else issue_stage<BN, CNT, true>(d, ad, bd, bs, first);
-}
 
 template <int BN, bool PAIR>
 __device__ __forceinline__ void fv_issue(uint32_t d0, uint32_t d1, uint64_t a_ring, uint64_t res_desc, uint64_t* full,
@@ -1560,15 +1604,17 @@ hex_status_t tc_conv3d_fwd(const TcConvArgs& a, int D, int Do, int sd, int kd, c
 namespace {
 struct FpPlan {
     int stages, smem, nr, nc, Ho, Wo;
-    bool ok;
+    bool ok, pair;
 };
+// pair: CTA pairs (M = 256 MMAs, each CTA holding half of every weight tile), n = 1, HEXCONV_FP_PAIR=1
 FpPlan fp_plan(const Geom& g, int Cin, int Cout) {
     FpPlan pl{};
+    pl.pair = g.n == 1 && getenv("HEXCONV_FP_PAIR") != nullptr;
     if (g.s != 1 || (g.n != 1 && g.n != 2) || Cin % 64 || (Cout != 64 && Cout != 128) || g.W < 2) return pl;
     int po;
     if (!out_shape(g.H, g.W, 2, g.parity, &pl.Ho, &pl.Wo, &po)) return pl;
     const int A = (FT_RB + 2 * g.n + (g.n == 1 ? 1 : 0)) * FT_JB * 128;
-    const int res_bytes = g.T * (Cin / 64) * Cout * 128;
+    const int res_bytes = g.T * (Cin / 64) * (pl.pair ? Cout / 2 : Cout) * 128;
     const int fixed = 2 * FP_BUF + (Cout / 32) * FP_CARRY + Cout * 4 + 1024 + 512;
     pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
     if (pl.stages > 8) pl.stages = 8;
@@ -1602,26 +1648,46 @@ hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax,
     const int sms = num_sms();
     const bool strip_mode = !getenv("HEXCONV_FUSED_POOL_REGIONS");
     p.debug = getenv("HEXCONV_FP_DEBUG") ? atoi(getenv("HEXCONV_FP_DEBUG")) : 0;
-    int grid = sms;
-    p.full_rounds = strip_mode ? strips / sms : 0;
-    p.left_regions = (strips - p.full_rounds * sms) * pl.nr;
-    if (p.full_rounds == 0 && p.left_regions < grid) grid = p.left_regions;
+    int grid = pl.pair ? sms & ~1 : sms;
+    p.full_rounds = strip_mode ? strips / grid : 0;
+    p.left_regions = (strips - p.full_rounds * grid) * pl.nr;
+    if (p.full_rounds == 0 && p.left_regions < grid) grid = pl.pair ? (p.left_regions + 1) & ~1 : p.left_regions;
     CUtensorMap mx0, mx1, mw;
     const int box_rows = FT_RB + 2 * g.n + (g.n == 1 ? 1 : 0);  // n = 1: 19-row boxes shared by both views
     if (!ft_view5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, box_rows)) return HEX_ERR_CUDA;
     if (!ft_view5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, box_rows)) return HEX_ERR_CUDA;
-    if (!ft_wmap(&mw, a.wpack, g.T, a.Cout, a.Cin, a.Cout)) return HEX_ERR_CUDA;
-#define HEX_FP(BN_, N_)                                                                                       \
+    if (!ft_wmap(&mw, a.wpack, g.T, a.Cout, a.Cin, pl.pair ? a.Cout / 2 : a.Cout)) return HEX_ERR_CUDA;
+#define HEX_FP(BN_, N_, PAIR_)                                                                                \
     {                                                                                                         \
-        auto kern = tc_conv_maxpool_kernel<BN_, N_>;                                                          \
+        auto kern = tc_conv_maxpool_kernel<BN_, N_, PAIR_>;                                                   \
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem) != cudaSuccess) \
             return HEX_ERR_CUDA;                                                                              \
-        kern<<<grid, FP_THREADS, pl.smem, st>>>(mx0, mx1, mw, p);                                             \
+        if (PAIR_) {                                                                                          \
+            cudaLaunchConfig_t cfg{};                                                                         \
+            cfg.gridDim = dim3(grid);                                                                         \
+            cfg.blockDim = dim3(FP_THREADS);                                                                  \
+            cfg.dynamicSmemBytes = pl.smem;                                                                   \
+            cfg.stream = st;                                                                                  \
+            cudaLaunchAttribute attr[1];                                                                      \
+            attr[0].id = cudaLaunchAttributeClusterDimension;                                                 \
+            attr[0].val.clusterDim.x = 2;                                                                     \
+            attr[0].val.clusterDim.y = 1;                                                                     \
+            attr[0].val.clusterDim.z = 1;                                                                     \
+            cfg.attrs = attr;                                                                                 \
+            cfg.numAttrs = 1;                                                                                 \
+            if (cudaLaunchKernelEx(&cfg, kern, mx0, mx1, mw, p) != cudaSuccess) return HEX_ERR_CUDA;          \
+        } else {                                                                                              \
+            kern<<<grid, FP_THREADS, pl.smem, st>>>(mx0, mx1, mw, p);                                         \
+        }                                                                                                     \
     }
     if (a.Cout == 128) {
-        if (g.n == 1) HEX_FP(128, 1) else HEX_FP(128, 2)
+        if (g.n == 1) {
+            if (pl.pair) HEX_FP(128, 1, true) else HEX_FP(128, 1, false)
+        } else HEX_FP(128, 2, false)
     } else {
-        if (g.n == 1) HEX_FP(64, 1) else HEX_FP(64, 2)
+        if (g.n == 1) {
+            if (pl.pair) HEX_FP(64, 1, true) else HEX_FP(64, 1, false)
+        } else HEX_FP(64, 2, false)
     }
 #undef HEX_FP
     count_launch();

@@ -144,6 +144,8 @@ def main():
         pool_layer(256, 256, 48, 48, 1, 2, "max", label="C5 P2")
         conv_layer(256, 256, 256, 24, 24, 2, label="C5 L5")
         conv_layer(256, 256, 256, 24, 24, 1, label="C5 L6")
+    if which == "fused":
+        fused_layer(256, 64, 128, 96, 96, 1, label="C5 L2+P1")
     if which in ("c3", "all"):
         conv_layer(256, 1, 16, 40, 40, 1, torch.float32, "NCHW", label="C3 L1")
         conv_layer(256, 16, 32, 40, 40, 2, torch.float32, "NCHW", label="C3 L2")
