@@ -498,7 +498,7 @@ constexpr int FP_BUF = 2 * FP_VIEW;                // both views
 constexpr int FP_CARRY = 2 * 2 * FT_JB * FP_PIX;   // carried rows of one chunk: 2 views x 2 rows (2 KB)
 constexpr int FP_EPI = 512;                      // 8 converter + 8 window warps
 constexpr int FP_THREADS = 64 + FP_EPI;
-constexpr int FP_BAR_FULL = 2, FP_BAR_EMPTY = 4;  // named barrier ids (+ buffer index)
+constexpr int FP_BAR_FULL = 2, FP_BAR_EMPTY = 6;  // named barrier ids (+ buffer index, up to 4 buffers)
 
 // byte offset of 16-byte channel group i (0..3) of pixel (region row r, sub-column sc): conflict-free
 // for 8 consecutive pixels of one group and for 2 adjacent sub-columns x 4 groups
@@ -513,6 +513,7 @@ struct FpParams {
     int full_rounds;   // strips per CTA in strip mode
     int left_regions;  // regions cut from the strips after full_rounds * gridDim.x
     int debug;         // HEXCONV_FP_DEBUG: 1 = no epilogue work, 2 = no MMAs (timing experiments)
+    int nreg;          // region buffers, 2 or 4 (4: the converters drain a whole tile ahead of the windows)
     const float* bias;
     uint16_t* y;   // pooled bf16 NHWC [B][Ho][Wo][Cout]
     uint8_t* am;   // argmax tap [B][Ho][Wo][Cout]
@@ -627,7 +628,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
     uint8_t* resw = base;
     uint8_t* ring = base + res_bytes;
     uint8_t* region = ring + p.stages * A_BYTES;  // [buffer][view][row][sub-column][64 B]
-    uint8_t* carry = region + 2 * FP_BUF;         // [chunk][view][2 rows][sub-column][64 B]
+    uint8_t* carry = region + p.nreg * FP_BUF;    // [chunk][view][2 rows][sub-column][64 B]
     float* sbias = (float*)(carry + NCH * FP_CARRY);  // [BN]
     uint64_t* full = (uint64_t*)(sbias + BN);
     uint64_t* empty = full + p.stages;
@@ -658,7 +659,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
     if (threadIdx.x >= 64) {  // region row 18 (r0 + 16) is only read on a strip's last tile: below the image
         const int e = threadIdx.x - 64;
         if (p.bias && e < BN) sbias[e] = p.bias[e];
-        if (e < 2 * 2 * FT_JB * 4) {
+        if (e < p.nreg * 2 * FT_JB * 4) {
             const int bf = e >> 6, v = (e >> 5) & 1, sc = (e >> 2) & 7, c16 = e & 3;
             *reinterpret_cast<uint4*>(region + bf * FP_BUF + v * FP_VIEW + fp_off(18, sc, c16)) =
                 make_uint4(NEG_INF2, NEG_INF2, NEG_INF2, NEG_INF2);
@@ -788,7 +789,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
         for (int ii = 0; ii < 4; ++ii) soff[ii] = cv * FP_VIEW + fp_off(2 + (row >> 3), row & 7, ii);
         int slot = 0;
         uint32_t sphase = 0;
-        int g = 0;  // chunk counter (buffer g & 1)
+        int g = 0;  // chunk counter (buffer g % nreg)
         FpTile tl;
         for (int seq = 0; fp_tile<PAIR>(p, seq, tl); ++seq) {
             const int img_r = tl.r0 + (row >> 3);
@@ -806,8 +807,8 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
             }
 #pragma unroll 1
             for (int c = 0; c < NCH; ++c, ++g) {
-                const int bf = g & 1;
-                if (g >= 2) ptx::named_bar(FP_BAR_EMPTY + bf, 512);  // window warps are done with it
+                const int bf = g & (p.nreg - 1);
+                if (g >= p.nreg) ptx::named_bar(FP_BAR_EMPTY + bf, 512);  // window warps are done with it
                 uint8_t* rb = region + bf * FP_BUF;
                 uint32_t vals[32];
                 ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (slot * 2 + cv) * BN + c * 32, vals);
@@ -860,7 +861,8 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
             slot ^= 1;
             if (slot == 0) sphase ^= 1;
         }
-        for (int r = g < 2 ? 0 : g - 2; r < g; ++r) ptx::named_bar(FP_BAR_EMPTY + (r & 1), 512);  // drain
+        for (int r = g < p.nreg ? 0 : g - p.nreg; r < g; ++r)  // drain
+            ptx::named_bar(FP_BAR_EMPTY + (r & (p.nreg - 1)), 512);
     } else {
         // ---- window warps: one (window, 8-channel group) item per thread and chunk
         const int et = threadIdx.x - 64 - 256;  // 0..255
@@ -893,7 +895,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
             const int64_t obase = (((int64_t)tl.b * p.Ho + R) * p.Wo + C) * p.Cout + cg * 8;
 #pragma unroll 1
             for (int c = 0; c < NCH; ++c, ++g) {
-                const int bf = g & 1;
+                const int bf = g & (p.nreg - 1);
                 ptx::named_bar(FP_BAR_FULL + bf, 512);
                 const uint8_t* rb = region + bf * FP_BUF;
                 if (tl.strip && !tl.last && et < 128)  // rows r0+14, r0+15 carry into the next tile
@@ -1603,7 +1605,7 @@ hex_status_t tc_conv3d_fwd(const TcConvArgs& a, int D, int Do, int sd, int kd, c
 // ------------------------------------------------------------------ fused conv + max pool host side
 namespace {
 struct FpPlan {
-    int stages, smem, nr, nc, Ho, Wo;
+    int stages, smem, nr, nc, Ho, Wo, nreg;
     bool ok, pair;
 };
 // pair: CTA pairs (M = 256 MMAs, each CTA holding half of every weight tile), n = 1, HEXCONV_FP_PAIR=1
@@ -1615,10 +1617,16 @@ FpPlan fp_plan(const Geom& g, int Cin, int Cout) {
     if (!out_shape(g.H, g.W, 2, g.parity, &pl.Ho, &pl.Wo, &po)) return pl;
     const int A = (FT_RB + 2 * g.n + (g.n == 1 ? 1 : 0)) * FT_JB * 128;
     const int res_bytes = g.T * (Cin / 64) * (pl.pair ? Cout / 2 : Cout) * 128;
-    const int fixed = 2 * FP_BUF + (Cout / 32) * FP_CARRY + Cout * 4 + 1024 + 512;
-    pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
+    // 4 region buffers when 3 ring stages still fit next to them (HEXCONV_FP_NREG=2 forces 2)
+    const char* nr_env = getenv("HEXCONV_FP_NREG");
+    for (pl.nreg = (nr_env && atoi(nr_env) == 2) ? 2 : 4; pl.nreg >= 2; pl.nreg /= 2) {
+        const int fixed = pl.nreg * FP_BUF + (Cout / 32) * FP_CARRY + Cout * 4 + 1024 + 512;
+        pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
+        if (pl.stages >= 3) break;
+    }
     if (pl.stages > 8) pl.stages = 8;
-    if (pl.stages < 3) return pl;
+    if (pl.nreg < 2 || pl.stages < 3) return pl;
+    const int fixed = pl.nreg * FP_BUF + (Cout / 32) * FP_CARRY + Cout * 4 + 1024 + 512;
     pl.smem = res_bytes + pl.stages * A + fixed;
     const int cr_max = 2 * (pl.Ho - 1) + 1;
     pl.nr = (cr_max + 1 + 13) / 14;
@@ -1640,7 +1648,7 @@ hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax,
     FpParams p{};
     p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
     p.Ho = pl.Ho; p.Wo = pl.Wo; p.nr = pl.nr; p.nc = pl.nc;
-    p.kchunks = a.Cin / 64; p.stages = pl.stages; p.relu = a.relu; p.bias = a.bias;
+    p.kchunks = a.Cin / 64; p.stages = pl.stages; p.relu = a.relu; p.bias = a.bias; p.nreg = pl.nreg;
     p.y = (uint16_t*)y_pool; p.am = argmax;
     // whole rounds of strips (one per CTA per round), the remaining strips as independent regions
     const int strips = g.B * pl.nc;
