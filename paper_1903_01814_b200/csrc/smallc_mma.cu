@@ -42,7 +42,7 @@ namespace hexconv {
 namespace {
 
 constexpr int MM_WARPS = 8;
-constexpr int MM_RB = 16;              // image rows per band
+constexpr int MM_RB = 16;              // image rows per band (maximum; the host picks rb <= MM_RB)
 constexpr int MM_CP = 8;               // zero column pad on each side of a staged row (elements)
 constexpr int MM_WG_STAGES = 3;        // dy tiles in flight per warp (weight gradient)
 constexpr int MM_TILE = 2048;          // one dy tile: 16 pixels x 64 channels x bf16
@@ -149,18 +149,18 @@ __device__ __forceinline__ int fwd_phys(int j, int tig, int e) {
 template <int N>
 __global__ void __launch_bounds__(MM_WARPS * 32, 2)
 smallc_mma_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, const float* __restrict__ bias,
-                      uint16_t* __restrict__ y, int B, int H, int W, int parity, int Cout, int relu, int bulk) {
+                      uint16_t* __restrict__ y, int B, int H, int W, int parity, int Cout, int relu, int bulk, int rb) {
     constexpr int T = 3 * N * (N + 1) + 1;
     constexpr int K16 = N >= 2 ? 1 : 0;  // one k16 step covers taps 0..15
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem + 128);
     const int Wp = band_wp(W);
-    const int band_elems = (MM_RB + 2 * N) * Wp;
+    const int band_elems = (rb + 2 * N) * Wp;
     const int co0 = blockIdx.y * 64;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, tig = lane & 3;
-    const int bands_per_img = (H + MM_RB - 1) / MM_RB;
+    const int bands_per_img = (H + rb - 1) / rb;
     const int nbands = B * bands_per_img;
     const int segs = (W + 15) / 16;
     if (threadIdx.x == 0) {
@@ -210,22 +210,22 @@ smallc_mma_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict
     int band = blockIdx.x, buf = 0;
     uint32_t phases = 0u;  // bit k: parity of the next completion of bars[k]
     if (band < nbands) {
-        const int b = band / bands_per_img, r0 = (band - b * bands_per_img) * MM_RB;
-        stage_band<N>(x + (int64_t)b * H * W, xs, &bars[0], H, W, r0, min(MM_RB, H - r0), bulk);
+        const int b = band / bands_per_img, r0 = (band - b * bands_per_img) * rb;
+        stage_band<N>(x + (int64_t)b * H * W, xs, &bars[0], H, W, r0, min(rb, H - r0), bulk);
     }
     for (; band < nbands; band += gridDim.x, buf ^= 1) {
         const int nb = band + gridDim.x;
         if (nb < nbands) {  // buffer buf^1 was released by the __syncthreads that ended the previous band
-            const int b2 = nb / bands_per_img, r2 = (nb - b2 * bands_per_img) * MM_RB;
+            const int b2 = nb / bands_per_img, r2 = (nb - b2 * bands_per_img) * rb;
             stage_band<N>(x + (int64_t)b2 * H * W, xs + (buf ^ 1) * band_elems, &bars[buf ^ 1], H, W, r2,
-                          min(MM_RB, H - r2), bulk);
+                          min(rb, H - r2), bulk);
         }
         ptx::mbar_wait(&bars[buf], (phases >> buf) & 1u);
         phases ^= 1u << buf;
         __syncthreads();
         const int b = band / bands_per_img;
-        const int r0 = (band - b * bands_per_img) * MM_RB;
-        const int rows = min(MM_RB, H - r0);
+        const int r0 = (band - b * bands_per_img) * rb;
+        const int rows = min(rb, H - r0);
         const uint16_t* xb = xs + buf * band_elems;
         const int items = rows * segs;
         for (int it = warp; it < items; it += MM_WARPS) {
@@ -289,7 +289,7 @@ smallc_mma_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict
 template <int N>
 __global__ void __launch_bounds__(MM_WARPS * 32, 2)
 smallc_mma_wgrad_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ dy, float* __restrict__ part,
-                        int B, int H, int W, int parity, int Cout, int bulk) {
+                        int B, int H, int W, int parity, int Cout, int bulk, int rb) {
     constexpr int T = 3 * N * (N + 1) + 1;
     constexpr int MT = (T + 1 + 15) / 16;  // m-tiles of 16 tap rows (incl. the ones row)
     constexpr int NA = T + 1;
@@ -299,11 +299,11 @@ smallc_mma_wgrad_kernel(const uint16_t* __restrict__ x, const uint16_t* __restri
     uint8_t* dyt = smem + 128;                                           // [warp][ST][16 px][128 B], swizzled
     uint16_t* xs = reinterpret_cast<uint16_t*>(dyt + MM_WARPS * ST * MM_TILE);
     const int Wp = band_wp(W);
-    const int band_elems = (MM_RB + 2 * N) * Wp;
+    const int band_elems = (rb + 2 * N) * Wp;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, tig = lane & 3;
     const int co0 = blockIdx.y * 64;
-    const int bands_per_img = (H + MM_RB - 1) / MM_RB;
+    const int bands_per_img = (H + rb - 1) / rb;
     const int nbands = B * bands_per_img;
     const int segs = (W + 15) / 16;
     if (threadIdx.x == 0) {
@@ -350,13 +350,13 @@ smallc_mma_wgrad_kernel(const uint16_t* __restrict__ x, const uint16_t* __restri
     int band = blockIdx.x, buf = 0;
     uint32_t phases = 0u;  // bit k: parity of the next completion of bars[k]
     if (band < nbands) {
-        const int b = band / bands_per_img, r0 = (band - b * bands_per_img) * MM_RB;
-        stage_band<N>(x + (int64_t)b * H * W, xs, &bars[0], H, W, r0, min(MM_RB, H - r0), bulk);
+        const int b = band / bands_per_img, r0 = (band - b * bands_per_img) * rb;
+        stage_band<N>(x + (int64_t)b * H * W, xs, &bars[0], H, W, r0, min(rb, H - r0), bulk);
     }
     for (; band < nbands; band += gridDim.x, buf ^= 1) {
         const int b = band / bands_per_img;
-        const int r0 = (band - b * bands_per_img) * MM_RB;
-        const int rows = min(MM_RB, H - r0);
+        const int r0 = (band - b * bands_per_img) * rb;
+        const int rows = min(rb, H - r0);
         const int items = rows * segs;
         const uint16_t* dimg = dy + (int64_t)b * H * W * Cout + co0;
         // dy tile of item `it` into ring slot `slot`: 16 pixels x 128 B = 128 16-byte chunks, 4 per lane;
@@ -382,9 +382,9 @@ smallc_mma_wgrad_kernel(const uint16_t* __restrict__ x, const uint16_t* __restri
         for (int s = 0; s < ST - 1; ++s) issue(warp + s * MM_WARPS, s);
         const int nb = band + gridDim.x;
         if (nb < nbands) {  // buffer buf^1 was released by the __syncthreads that ended the previous band
-            const int b2 = nb / bands_per_img, r2 = (nb - b2 * bands_per_img) * MM_RB;
+            const int b2 = nb / bands_per_img, r2 = (nb - b2 * bands_per_img) * rb;
             stage_band<N>(x + (int64_t)b2 * H * W, xs + (buf ^ 1) * band_elems, &bars[buf ^ 1], H, W, r2,
-                          min(MM_RB, H - r2), bulk);
+                          min(rb, H - r2), bulk);
         }
         ptx::mbar_wait(&bars[buf], (phases >> buf) & 1u);
         phases ^= 1u << buf;
@@ -500,8 +500,26 @@ bool smallc_mma_supported(const Geom& g, int Cin, int Cout) {
            wgrad_smem(g) <= 100 * 1024;
 }
 
+// rows per band: the persistent grid's last round should be nearly full (H = 96, B = 256: 16 rows give
+// 1536 bands = 5.2 rounds of 296 blocks, 12 rows 2048 = 6.9 rounds); a band's fixed cost ~ one row
+static int pick_rb(const Geom& g) {
+    const int slots = 2 * num_sms();
+    int best = MM_RB;
+    double best_score = 0.0;
+    for (int rb = MM_RB; rb >= 8; --rb) {
+        const int per = (g.H + rb - 1) / rb;
+        const long bands = (long)g.B * per;
+        const long rounds = (bands + slots - 1) / slots;
+        const double fill = bands < slots ? 1.0 : (double)bands / (double)(rounds * slots);
+        const double score = fill * ((double)g.H / (per * rb)) * rb / (rb + 1.0);
+        if (score > best_score + 1e-9) { best_score = score; best = rb; }
+    }
+    return best;
+}
+
 static int resident_blocks(const Geom& g) {
-    const int nbands = g.B * ((g.H + MM_RB - 1) / MM_RB);
+    const int rb = pick_rb(g);
+    const int nbands = g.B * ((g.H + rb - 1) / rb);
     const int cap = 2 * num_sms();  // 2 blocks of 8 warps per SM (launch bounds)
     return nbands < cap ? nbands : cap;
 }
@@ -516,7 +534,7 @@ static void launch_fwd(const Geom& g, dim3 grid, size_t smem, cudaStream_t st, c
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(smallc_mma_fwd_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     smallc_mma_fwd_kernel<N><<<grid, MM_WARPS * 32, smem, st>>>(x, w, bias, y, g.B, g.H, g.W, g.parity, Cout, relu,
-                                                               bulk);
+                                                               bulk, pick_rb(g));
 }
 
 template <int N>
@@ -524,7 +542,8 @@ static void launch_wgrad(const Geom& g, dim3 grid, size_t smem, cudaStream_t st,
                          float* part, int Cout, int bulk) {
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(smallc_mma_wgrad_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smallc_mma_wgrad_kernel<N><<<grid, MM_WARPS * 32, smem, st>>>(x, dy, part, g.B, g.H, g.W, g.parity, Cout, bulk);
+    smallc_mma_wgrad_kernel<N><<<grid, MM_WARPS * 32, smem, st>>>(x, dy, part, g.B, g.H, g.W, g.parity, Cout, bulk,
+                                                                   pick_rb(g));
 }
 
 hex_status_t smallc_mma_fwd(const void* x, const void* w, const float* bias, void* y, const Geom& g, int Cout,
