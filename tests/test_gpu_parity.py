@@ -280,9 +280,11 @@ def test_single_input_channel_bf16_nhwc(F, oracle):
 def test_single_input_channel_mma_bands(F, oracle, pi, n):
     # the stride-1 Cin = 1 tensor-core kernels (smallc_mma.cu): several 16-row bands with a ragged
     # last band, ragged 16-pixel items (W % 16 != 0), two 64-channel blocks, both parities
-    # (W % 8 == 0 takes the bulk-copy band staging; B * bands > 2 * 148 makes the persistent blocks loop)
+    # (W % 8 == 0 takes the bulk-copy band staging; B * bands > 2 * 148 makes the persistent blocks loop;
+    # the host picks the band height so the last round is nearly full: 10 rows at B = 120 / H = 40, and
+    # at B = 100 / H = 47 10 rows with a ragged 7-row last band)
     for (H, W), Cout, B in [((37, 45), 128, 3), ((16, 16), 64, 2), ((5, 70), 64, 1), ((35, 40), 64, 2),
-                            ((40, 24), 64, 120)]:
+                            ((40, 24), 64, 120), ((47, 24), 64, 100)]:
         _conv_case(F, oracle, pi, n, 1, H, W, B, 1, Cout, torch.bfloat16, "NHWC", 60 + n + H)
 
 
