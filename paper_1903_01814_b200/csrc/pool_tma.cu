@@ -179,7 +179,9 @@ bool pool_tma_fwd_supported(const PoolArgs& a) {
     if (getenv("HEXCONV_NO_POOL_TMA") || !pt_encode()) return false;
     const Geom& g = a.g;
     if (a.dtype != HEX_BF16 || a.layout != HEX_NHWC || a.mode != HEX_POOL_MAX || g.n != 1 || g.s != 2) return false;
-    if (a.C % 64 || g.W < 64 || g.W + 2 > 256 || g.B < 1) return false;
+    const char* wm = getenv("HEXCONV_POOL_TMA_MIN_W");
+    const int min_w = wm ? atoi(wm) : 64;
+    if (a.C % 64 || g.W < min_w || g.W < 2 || g.W + 2 > 256 || g.B < 1) return false;
     if (((uintptr_t)a.x & 15) || ((uintptr_t)a.y & 15) || ((uintptr_t)a.argmax & 7)) return false;
     int nb;
     return pt_band(g.W, &nb) > 0;
