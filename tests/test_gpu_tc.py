@@ -118,6 +118,9 @@ def test_tc_tap_reuse_wgrad_channel_tiles(F, oracle):
     # CTA-pair forward with an odd number of 128-pixel tiles (the last pair's second tile is empty)
     case(F, oracle, 1, 128, 128, 16, 17, 1, 0, 9)
     case(F, oracle, 1, 256, 256, 16, 17, 2, 1, 10)
+    # 2-CTA weight gradient with a short last atom group (24 x 24, n = 1: 28 atoms = 8+8+8+4; the last
+    # group gets half the pixel chunks) -- C5 layer 6
+    case(F, oracle, 2, 256, 256, 24, 24, 1, 0, 11)
 
 
 @pytest.mark.parametrize("n", [1])
