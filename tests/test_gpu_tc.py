@@ -179,6 +179,26 @@ def test_fused_conv_maxpool_strips(F, oracle, pi, pair, monkeypatch):
         assert np.array_equal(am[-1:].permute(0, 3, 1, 2).cpu().numpy(), amr)
 
 
+@pytest.mark.parametrize("pi", [0, 1])
+def test_fused_conv_maxpool_no_relu_ties(F, oracle, pi):
+    # no ReLU and no bias: the window warps take the value of the first tap equal to the maximum
+    # (A9); small-integer inputs make many windows tie (several taps with the same value, zeros)
+    for (B, Cin, Cout, H, W) in [(2, 64, 128, 30, 31), (3, 64, 64, 16, 16)]:
+        g = torch.Generator().manual_seed(950 + H + pi)
+        x = torch.randint(-1, 2, (B, H, W, Cin), generator=g).to(torch.bfloat16).cuda()
+        w = torch.randint(-1, 2, (Cout, Cin, 7), generator=g).to(torch.bfloat16).cuda()
+        yp, am = F.conv2d_fwd_maxpool(x, w, None, n=1, parity=pi, relu=False)
+        yc = F.conv2d_fwd(x, w, None, n=1, parity=pi, relu=False, layout="NHWC")
+        yp2, am2 = F.pool2d_fwd(yc, 1, 2, pi, "max", "NHWC")
+        torch.cuda.synchronize()
+        assert torch.equal(yp.view(torch.int16), yp2.view(torch.int16)), (pi, H, W)
+        assert torch.equal(am, am2), (pi, H, W)
+        pr, amr = oracle.pool2d_fwd(back(yc), n=1, s=2, pi=pi, mode="max")
+        assert np.array_equal(back(yp), pr)
+        assert np.array_equal(am.permute(0, 3, 1, 2).cpu().numpy(), amr)
+        assert (am.float().mean() > 0.5), "expected ties / non-centre maxima"
+
+
 def test_fused_conv_maxpool_unsupported_shape(F):
     # n = 2 weights do not stay resident next to the fused kernel's buffers: the call reports
     # HEX_ERR_UNSUPPORTED (8) and the caller runs conv + pool separately
