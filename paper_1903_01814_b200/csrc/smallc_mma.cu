@@ -361,10 +361,9 @@ smallc_mma_wgrad_kernel(const uint16_t* __restrict__ x, const uint16_t* __restri
         const uint16_t* dimg = dy + (int64_t)b * H * W * Cout + co0;
         // dy tile of item `it` into ring slot `slot`: 16 pixels x 128 B = 128 16-byte chunks, 4 per lane;
         // one commit group per call (possibly empty) keeps the group count uniform
-        auto issue = [&](int it, int slot) {
+        auto issue = [&](int it, int rl, int sg, int slot) {  // item it = rl * segs + sg
             if (it < items) {
-                const int rl = it / segs;
-                const int c0 = (it - rl * segs) * 16;
+                const int c0 = sg * 16;
                 const int r = r0 + rl;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -379,7 +378,10 @@ smallc_mma_wgrad_kernel(const uint16_t* __restrict__ x, const uint16_t* __restri
             cp_async_commit();
         };
 #pragma unroll
-        for (int s = 0; s < ST - 1; ++s) issue(warp + s * MM_WARPS, s);
+        for (int s = 0; s < ST - 1; ++s) {
+            const int it0 = warp + s * MM_WARPS;
+            issue(it0, it0 / segs, it0 % segs, s);
+        }
         const int nb = band + gridDim.x;
         if (nb < nbands) {  // buffer buf^1 was released by the __syncthreads that ended the previous band
             const int b2 = nb / bands_per_img, r2 = (nb - b2 * bands_per_img) * rb;
@@ -391,12 +393,16 @@ smallc_mma_wgrad_kernel(const uint16_t* __restrict__ x, const uint16_t* __restri
         __syncthreads();
         const uint16_t* xb = xs + buf * band_elems;
         int slot = 0;
+        int rl = warp / segs, sg = warp % segs;  // item it = rl * segs + sg, stepped by MM_WARPS
+        const int pit0 = warp + (ST - 1) * MM_WARPS;  // the item prefetched ST - 1 steps ahead
+        int prl = pit0 / segs, psg = pit0 % segs;
         for (int it = warp; it < items; it += MM_WARPS) {
-            issue(it + (ST - 1) * MM_WARPS, (slot + ST - 1) % ST);
+            issue(it + (ST - 1) * MM_WARPS, prl, psg, (slot + ST - 1) % ST);
+            psg += MM_WARPS;
+            while (psg >= segs) { psg -= segs; ++prl; }
             cp_async_wait<ST - 1>();
             __syncwarp();
-            const int rl = it / segs;
-            const int c0 = (it - rl * segs) * 16;
+            const int c0 = sg * 16;
             const uint16_t* base = xb + rl * Wp + c0;
             // A fragments: a0 = {m g: px 2tig, 2tig+1}, a1 = {m g+8: ...}, a2 = {m g: px 2tig+8, +9}, a3 = {m g+8: ...}
             uint32_t a[MT][4];
@@ -404,16 +410,14 @@ smallc_mma_wgrad_kernel(const uint16_t* __restrict__ x, const uint16_t* __restri
             for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
+                    // branch-free (the tap rows differ per lane): load from a valid offset, then select
                     const int oe = offe[mt][h], oo = offo[mt][h];
-                    uint16_t e0, o0, e1, o1;
-                    if (oe == -2) { e0 = o0 = e1 = o1 = 0x3F80; }  // 1.0
-                    else if (oe < 0) { e0 = o0 = e1 = o1 = 0; }
-                    else {
-                        e0 = base[2 * tig + oe];
-                        o0 = base[2 * tig + 1 + oo];
-                        e1 = base[2 * tig + 8 + oe];
-                        o1 = base[2 * tig + 9 + oo];
-                    }
+                    const bool tap = oe >= 0;
+                    const uint16_t cst = oe == -2 ? (uint16_t)0x3F80 : (uint16_t)0;  // 1.0 (dbias row) or 0
+                    const uint16_t* pe_ = base + 2 * tig + (tap ? oe : 0);
+                    const uint16_t* po_ = base + 2 * tig + 1 + (tap ? oo : 0);
+                    const uint16_t e0 = tap ? pe_[0] : cst, e1 = tap ? pe_[8] : cst;
+                    const uint16_t o0 = tap ? po_[0] : cst, o1 = tap ? po_[8] : cst;
                     a[mt][h] = pack2(e0, o0);
                     a[mt][2 + h] = pack2(e1, o1);
                 }
@@ -432,6 +436,8 @@ smallc_mma_wgrad_kernel(const uint16_t* __restrict__ x, const uint16_t* __restri
             }
             __syncwarp();  // slot `slot` is refilled ST - 1 items later
             slot = (slot + 1 == ST) ? 0 : slot + 1;
+            sg += MM_WARPS;
+            while (sg >= segs) { sg -= segs; ++rl; }
         }
         cp_async_wait<0>();  // drain the (empty) tail groups
         __syncthreads();     // everyone is done with buffer `buf` before it is restaged
