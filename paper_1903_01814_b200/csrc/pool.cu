@@ -424,10 +424,10 @@ static void launch_spec_bwd(const PoolArgs& a, cudaStream_t st) {
 // results as the scalar kernels (max: a copy of the selected input; avg and
 // backward: fp32 accumulation in canonical tap order).
 // ---------------------------------------------------------------------------
-template <int N, int S, int V>
+template <int N, int S, int V, bool MAXP>  // MAXP: max pooling (else average), fixed at compile time
 __global__ void __launch_bounds__(256)
 pool_fwd_nhwc_v(const uint4* __restrict__ x, uint4* __restrict__ y, uint2* __restrict__ am, Geom g, int CV,
-                int mode, int lgcv) {
+                int lgcv) {
     // grid: x = (output pixel, channel group) of image b = blockIdx.y
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= g.Ho * g.Wo * CV) return;
@@ -466,7 +466,7 @@ pool_fwd_nhwc_v(const uint4* __restrict__ x, uint4* __restrict__ y, uint2* __res
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                     const int i = 4 * v + kk;
-                    if (mode == HEX_POOL_MAX) {
+                    if constexpr (MAXP) {
                         if (cnt == 0) {
                             best[i] = w[kk];
                             ix[i] = tt;
@@ -487,7 +487,7 @@ pool_fwd_nhwc_v(const uint4* __restrict__ x, uint4* __restrict__ y, uint2* __res
         }
     }
     const size_t yo = ((size_t)b * g.Ho * g.Wo + o) * C8 + cv * V;
-    if (mode == HEX_POOL_MAX) {
+    if constexpr (MAXP) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             y[yo + v] = make_uint4(best[4 * v], best[4 * v + 1], best[4 * v + 2], best[4 * v + 3]);
@@ -810,8 +810,12 @@ template <int N, int S, int V>
 static void launch_v_fwd(const PoolArgs& a, cudaStream_t st) {
     const int CV = a.C / (8 * V);
     dim3 grid(ceil_div((int64_t)a.g.Ho * a.g.Wo * CV, 256), a.g.B);
-    pool_fwd_nhwc_v<N, S, V><<<grid, 256, 0, st>>>((const uint4*)a.x, (uint4*)a.y, (uint2*)a.argmax, a.g, CV, a.mode,
-                                                   ilog2_exact(CV));
+    if (a.mode == HEX_POOL_MAX)
+        pool_fwd_nhwc_v<N, S, V, true><<<grid, 256, 0, st>>>((const uint4*)a.x, (uint4*)a.y, (uint2*)a.argmax, a.g,
+                                                             CV, ilog2_exact(CV));
+    else
+        pool_fwd_nhwc_v<N, S, V, false><<<grid, 256, 0, st>>>((const uint4*)a.x, (uint4*)a.y, (uint2*)a.argmax, a.g,
+                                                              CV, ilog2_exact(CV));
 }
 template <int N, int S, int V>
 static void launch_v_bwd(const PoolArgs& a, cudaStream_t st) {
