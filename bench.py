@@ -335,6 +335,22 @@ def secondary_measurements(dev, peak_tf, peak_gbs):
     return out
 
 
+# ------------------------------------------------------------------ launcher
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """Re-run this script as n ranks under torch.distributed.run (nnodes 1, 127.0.0.1); the ranks see
+    WORLD_SIZE = n and take the normal path.  Returns torchrun's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -345,16 +361,30 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the config 2-4 measurements")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="print each rank's (rank, world) and exit before touching a GPU (launcher test)")
     ap.add_argument("--no-graph", action="store_true", help="device-timed and e2e legs as eager steps (no CUDA graph)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.impl == "reference":
+        # the oracle arm runs on rank 0's host cores only; the other ranks (under torchrun) exit 0
+        run_reference(args, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: start the N ranks here (one per GPU, torchrun on
+        # 127.0.0.1) and pass their exit status through, so a multi-GPU request never quietly becomes a
+        # one-rank line
+        sys.exit(relaunch_under_torchrun(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-
-    if args.impl == "reference":
-        run_reference(args, rank, world)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+    if args.launch_check:
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local}), flush=True)
         return
 
     import numpy as np
@@ -391,16 +421,32 @@ def main():
         model.step(xs[i % NB], ys[i % NB])
     torch.cuda.synchronize()
 
-    # ---- device-resident timed region.  One GPU: the production path, one CUDA-graph replay of the
-    # whole step per batch (HexCNN.graphed_step; the batch is copied device -> device into the graph's
-    # static input buffer, 4.7 MB); data parallel: eager steps (NCCL allreduce per layer bucket).
-    graph_v, xg, yg = None, None, None
-    if world == 1 and not args.no_graph:
-        xg, yg = torch.empty_like(xs[0]), torch.empty_like(ys[0])
-        xg.copy_(xs[0])
-        yg.copy_(ys[0])
-        graph_v, _ = model.graphed_step(xg, yg)
+    def capture(xb, yb):
+        """HexCNN.graphed_step on every rank (the per-layer NCCL allreduces are captured too); if any
+        rank fails to capture, every rank falls back to eager steps so the collectives stay matched."""
+        if args.no_graph:
+            return None, None
+        try:
+            g, loss = model.graphed_step(xb, yb)
+            ok = 1.0
+        except Exception as ex:  # reported in the line as cuda_graph: false
+            print(f"bench.py: CUDA-graph capture failed, eager steps: {ex!r}", file=sys.stderr)
+            g, loss, ok = None, None, 0.0
         torch.cuda.synchronize()
+        if world > 1:
+            t = torch.tensor([ok], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            if t.item() < 1.0:
+                return None, None
+        return g, loss
+
+    # ---- device-resident timed region: each step is one CUDA-graph replay of the whole step
+    # (HexCNN.graphed_step: every kernel, the per-layer NCCL gradient allreduces when N > 1, and SGD;
+    # the batch is copied device -> device into the graph's static input buffer, 4.7 MB)
+    xg, yg = torch.empty_like(xs[0]), torch.empty_like(ys[0])
+    xg.copy_(xs[0])
+    yg.copy_(ys[0])
+    graph_v, _ = capture(xg, yg)
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -488,17 +534,15 @@ def main():
 
     # ---- end-to-end through the public API with host buffers: each step copies its batch from pinned
     # host memory into the model's input buffers, runs the step (one CUDA-graph replay of
-    # HexCNN.graphed_step on one GPU; eager under data parallelism) and reads the loss back
+    # HexCNN.graphed_step) and reads the loss back
     pin_x = [torch.from_numpy(a.astype(np.float32)).to(torch.bfloat16).pin_memory() for a in xs_np]
     pin_y = [torch.from_numpy(a).pin_memory() for a in ys_np]
     xd = torch.empty_like(xs[0])
     yd = torch.empty_like(ys[0])
     loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
-    graph = None
-    if world == 1 and not args.no_graph:
-        xd.copy_(xs[0])
-        yd.copy_(ys[0])
-        graph, gloss = model.graphed_step(xd, yd)
+    xd.copy_(xs[0])
+    yd.copy_(ys[0])
+    graph, gloss = capture(xd, yd)
     # Input pipeline: the H2D copy of batch i+1 (pinned host -> device staging buffer, copy stream)
     # overlaps step i; step i starts with a 4.7 MB device copy staging -> model input.  The loss of
     # step i is copied to pinned host memory and read (host sync on its event) after step i+1 has

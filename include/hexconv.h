@@ -115,6 +115,14 @@ HEX_API hex_status_t hex_output_shape(int32_t H, int32_t W, int32_t stride, int3
  * (dc, drow) pairs in canonical order.  (A2) */
 HEX_API hex_status_t hex_tap_offsets(int32_t n, int32_t centre_col_parity, int32_t* dc_dr);
 
+/* The T(n) taps as axial displacements (dq, dr) in canonical order, i.e. the
+ * element order of a user-defined kernel ("structure detecting kernels",
+ * PAPER.md:207-210; A2: lexicographic (dq, dr) over
+ * |dq|+|dr|+|dq+dr| <= 2n = column-major left->right, top->bottom).
+ * dq_dr: host, 2*T int32.  Errors: HEX_ERR_INVALID_ARG (n < 0, NULL),
+ * HEX_ERR_UNSUPPORTED (n > HEX_MAX_N). */
+HEX_API hex_status_t hex_tap_axial(int32_t n, int32_t* dq_dr);
+
 /* Test hook: device int32 map [Ho][Wo][T], entry = r*W + c of tap t of
  * output (R,C), or -1 when that neighbour lies outside the grid.  Uses
  * desc->height/width/kernel_size/stride/parity only. */
@@ -268,6 +276,13 @@ HEX_API hex_status_t hex_sgd_momentum(int64_t count, float* param, const float* 
                               hex_stream_t stream);
 
 /* Elementwise fp32 -> bf16 (RNE) conversion of count values. */
+/* ReLU backward for callers without a fused mask: dx[i] = y[i] > 0 ? dy[i] : 0
+ * over `count` elements of `dtype` (y = the post-ReLU forward output; dy, y,
+ * dx device, same dtype; dx may alias dy).  Errors: HEX_ERR_SHAPE (count < 0),
+ * HEX_ERR_DTYPE, HEX_ERR_INVALID_ARG (NULL with count > 0). */
+HEX_API hex_status_t hex_relu_bwd(int64_t count, int32_t dtype, const void* dy, const void* y, void* dx,
+                                  hex_stream_t stream);
+
 HEX_API hex_status_t hex_cast_f32_bf16(int64_t count, const float* src, void* dst, hex_stream_t stream);
 
 /* ---------------------------------------------------------------- misc */

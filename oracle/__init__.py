@@ -247,10 +247,18 @@ def pool2d_fwd(x, n: int = 1, s: int = 1, pi: int = 0, mode: str = "max"):
 def pool2d_bwd(dy, argmax, H: int, W: int, n: int = 1, s: int = 1, pi: int = 0, mode: str = "max"):
     dy = _f64(dy)
     B, C, Ho, Wo = dy.shape
+    if (Ho, Wo) != out_shape(H, W, s, pi)[:2]:
+        raise ValueError(f"dy grid {(Ho, Wo)} is not the ({H}, {W}) s={s} lattice {out_shape(H, W, s, pi)[:2]}")
     dx = np.empty((B, C, H, W), dtype=np.float64)
     am = None if argmax is None else np.ascontiguousarray(argmax, dtype=np.uint8)
+    if mode == "max" and (am is None or am.shape != dy.shape):
+        raise ValueError("max-pool backward needs an argmax of dy's shape")
     st = lib().oracle_pool2d_bwd(B, C, H, W, n, s, pi, _POOL_MODES[mode],
                                  _ptr(dy), _ptr(am), _ptr(dx))
+    if st == 3:
+        raise ValueError("argmax names a tap index >= T or an off-grid neighbour")
+    if st == 2:
+        raise ValueError("invalid argument")
     assert st == 0
     return dx
 

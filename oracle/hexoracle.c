@@ -369,6 +369,15 @@ int oracle_pool2d_bwd(int B, int Cc, int H, int W, int n, int s, int pi, int mod
     int32_t* map = build_map(H, W, n, s, pi, &Ho, &Wo, &T);
     if (!map) return 1;
     const int64_t HW = (int64_t)H * W, HWo = (int64_t)Ho * Wo;
+    if (mode == 0) {
+        /* The argmax comes from the implementation under test: validate every entry before routing
+         * (a tap index >= T or one that names an off-grid neighbour is an error, not a write). */
+        if (!argmax) { free(map); return 2; }
+        for (int64_t oi = 0; oi < (int64_t)B * Cc * HWo; ++oi) {
+            const int a = argmax[oi];
+            if (a >= T || map[(oi % HWo) * T + a] < 0) { free(map); return 3; }
+        }
+    }
     #pragma omp parallel for collapse(2) schedule(static)
     for (int b = 0; b < B; ++b)
         for (int c = 0; c < Cc; ++c) {

@@ -77,6 +77,7 @@ _SIGS = {
     "hex_status_string": (ctypes.c_char_p, [_i32]),
     "hex_output_shape": (_i32, [_i32, _i32, _i32, _i32, _i32p, _i32p, _i32p]),
     "hex_tap_offsets": (_i32, [_i32, _i32, _i32p]),
+    "hex_tap_axial": (_i32, [_i32, _i32p]),
     "hex_conv2d_gather_map": (_i32, [_CDP, _vp, _vp]),
     "hex_conv2d_workspace_size": (_i32, [_CDP, _i32, _szp]),
     "hex_conv2d_algo": (_i32, [_CDP, _i32, _i32p]),
@@ -96,6 +97,7 @@ _SIGS = {
     "hex_head_fwd_bwd": (_i32, [_i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "hex_sgd_momentum": (_i32, [_i64, _vp, _vp, _vp, _f32, _f32, _f32, _vp, _vp]),
     "hex_cast_f32_bf16": (_i32, [_i64, _vp, _vp, _vp]),
+    "hex_relu_bwd": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -130,6 +132,14 @@ def tap_offsets(n: int, p: int):
     T = num_taps(n)
     buf = (_i32 * (2 * max(T, 1)))()
     check(_lib.hex_tap_offsets(n, p, buf), "hex_tap_offsets")
+    return [(buf[2 * t], buf[2 * t + 1]) for t in range(T)]
+
+
+def tap_axial(n: int):
+    """The T(n) taps as axial (dq, dr) in canonical order (library geometry)."""
+    T = num_taps(n) if n >= 0 else 0
+    buf = (_i32 * (2 * max(T, 1)))()
+    check(_lib.hex_tap_axial(n, buf), "hex_tap_axial")
     return [(buf[2 * t], buf[2 * t + 1]) for t in range(T)]
 
 

@@ -17,6 +17,7 @@ hex_status_t head_fwd_bwd(int B, int HW, int C, int K, const void* feat, const f
 hex_status_t sgd_momentum(int64_t n, float* p, const float* g, float* m, float lr, float mu, float gs, void* pb,
                           cudaStream_t st);
 hex_status_t cast_f32_bf16(int64_t n, const float* s, void* d, cudaStream_t st);
+hex_status_t relu_bwd(int64_t n, int dtype, const void* dy, const void* y, void* dx, cudaStream_t st);
 }  // namespace hexconv
 
 using namespace hexconv;
@@ -151,6 +152,20 @@ hex_status_t hex_tap_offsets(int32_t n, int32_t p, int32_t* dc_dr) {
     if (n > HEX_MAX_N) return HEX_ERR_UNSUPPORTED;
     const int T = hex_taps(n);
     for (int t = 0; t < T; ++t) tap_offset(n, p, t, &dc_dr[2 * t], &dc_dr[2 * t + 1]);
+    return HEX_OK;
+}
+
+hex_status_t hex_tap_axial(int32_t n, int32_t* dq_dr) {
+    if (n < 0 || !dq_dr) return HEX_ERR_INVALID_ARG;
+    if (n > HEX_MAX_N) return HEX_ERR_UNSUPPORTED;
+    int t = 0;  // lexicographic (dq, dr) over the hexagonal disc |dq| + |dr| + |dq + dr| <= 2n
+    for (int dq = -n; dq <= n; ++dq)
+        for (int dr = -n; dr <= n; ++dr)
+            if (abs(dq) + abs(dr) + abs(dq + dr) <= 2 * n) {
+                dq_dr[2 * t] = dq;
+                dq_dr[2 * t + 1] = dr;
+                ++t;
+            }
     return HEX_OK;
 }
 
@@ -434,6 +449,14 @@ hex_status_t hex_sgd_momentum(int64_t count, float* param, const float* grad, fl
     if (count < 0) return HEX_ERR_SHAPE;
     if (count > 0 && (!param || !grad || !mom)) return HEX_ERR_INVALID_ARG;
     return sgd_momentum(count, param, grad, mom, lr, mu, grad_scale, param_bf16, (cudaStream_t)stream);
+}
+
+hex_status_t hex_relu_bwd(int64_t count, int32_t dtype, const void* dy, const void* y, void* dx,
+                          hex_stream_t stream) {
+    if (count < 0) return HEX_ERR_SHAPE;
+    if (dtype != HEX_F32 && dtype != HEX_BF16) return HEX_ERR_DTYPE;
+    if (count > 0 && (!dy || !y || !dx)) return HEX_ERR_INVALID_ARG;
+    return relu_bwd(count, dtype, dy, y, dx, (cudaStream_t)stream);
 }
 
 hex_status_t hex_cast_f32_bf16(int64_t count, const float* src, void* dst, hex_stream_t stream) {

@@ -198,4 +198,23 @@ hex_status_t cast_f32_bf16(int64_t n, const float* s, void* d, cudaStream_t st) 
     return last_launch_status();
 }
 
+// dx = dy * (y > 0): the ReLU backward for callers whose next op has no fused mask (the autograd
+// wrapper's weight gradient needs the masked dy as an operand).  y is the post-ReLU output.
+template <typename T>
+__global__ void relu_bwd_kernel(int64_t n, const T* __restrict__ dy, const T* __restrict__ y, T* __restrict__ dx) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dx[i] = (float)y[i] > 0.f ? dy[i] : T(0.f);
+}
+
+hex_status_t relu_bwd(int64_t n, int dtype, const void* dy, const void* y, void* dx, cudaStream_t st) {
+    if (n == 0) return HEX_OK;
+    if (dtype == HEX_F32)
+        relu_bwd_kernel<float><<<ceil_div(n, 256), 256, 0, st>>>(n, (const float*)dy, (const float*)y, (float*)dx);
+    else
+        relu_bwd_kernel<__nv_bfloat16><<<ceil_div(n, 256), 256, 0, st>>>(
+            n, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)y, (__nv_bfloat16*)dx);
+    count_launch();
+    return last_launch_status();
+}
+
 }  // namespace hexconv

@@ -37,6 +37,22 @@ def _check_cuda(*ts):
             raise ValueError("hexconv ops take contiguous tensors in the declared layout")
 
 
+def _expect(t, shape, dtype, name):
+    """Validate a tensor against the descriptor before its pointer crosses the C ABI (the library sees
+    only the descriptor, so a wrong shape here would be an out-of-bounds access there)."""
+    if t is None:
+        return
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)} does not match the descriptor's {tuple(shape)}")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+
+
+def _dtype_ok(t):
+    if t.dtype not in _DTYPES:
+        raise ValueError(f"unsupported dtype {t.dtype} (float32 or bfloat16)")
+
+
 def _dims(x, layout):
     if layout == "NCHW":
         B, C, H, W = x.shape
@@ -93,12 +109,13 @@ def conv2d_fwd(x, w, bias=None, n: int = 1, stride: int = 1, parity: int = 0, re
         raise ValueError("weight tap count does not match kernel size")
     if w.dtype != x.dtype:
         raise ValueError("x and w must share a dtype")
-    if bias is not None and bias.dtype != torch.float32:
-        raise ValueError("bias is fp32")
+    _dtype_ok(x)
+    _expect(bias, (Cout,), torch.float32, "bias")
     Ho, Wo, _ = A.output_shape(H, W, stride, parity)
     d = conv_desc(B, Cin, Cout, H, W, n, stride, parity, x.dtype, layout)
     if out is None:
         out = torch.empty(_shape(layout, B, Cout, Ho, Wo), dtype=x.dtype, device=x.device)
+    _expect(out, _shape(layout, B, Cout, Ho, Wo), x.dtype, "out")
     ws, nb = _workspace(d, 0, x.device)
     A.check(A.lib().hex_conv2d_fwd(ctypes.byref(d), _ptr(x), _ptr(w), _ptr(bias), int(relu), _ptr(out),
                                    _ptr(ws), nb, _stream()), "hex_conv2d_fwd")
@@ -111,7 +128,10 @@ def conv2d_fwd_maxpool(x, w, bias=None, n: int = 1, parity: int = 0, relu: bool 
     pool2d_fwd; raises HexError(HEX_ERR_UNSUPPORTED) where no fused kernel applies."""
     _check_cuda(x, w, bias)
     B, Cin, H, W = _dims(x, layout)
+    _dtype_ok(x)
     Cout = w.shape[0]
+    _expect(w, (Cout, Cin, A.num_taps(n)), x.dtype, "w")
+    _expect(bias, (Cout,), torch.float32, "bias")
     d = conv_desc(B, Cin, Cout, H, W, n, 1, parity, x.dtype, layout)
     Ho, Wo, _ = A.output_shape(H, W, 2, parity)
     y = torch.empty(_shape(layout, B, Cout, Ho, Wo), dtype=x.dtype, device=x.device)
@@ -132,13 +152,19 @@ def conv2d_bwd_data(dy, w, in_hw, n: int = 1, stride: int = 1, parity: int = 0, 
     """dx = adjoint of conv2d_fwd applied to dy; optionally masked by relu_y > 0."""
     _check_cuda(dy, w, relu_y, out)
     B, Cout, Ho, Wo = _dims(dy, layout)
+    _dtype_ok(dy)
     Co2, Cin, T = w.shape
     H, W = in_hw
     if Co2 != Cout:
         raise ValueError("channel mismatch")
+    _expect(w, (Cout, Cin, A.num_taps(n)), dy.dtype, "w")
+    Ho_, Wo_, _ = A.output_shape(H, W, stride, parity)
+    _expect(dy, _shape(layout, B, Cout, Ho_, Wo_), dy.dtype, "dy")
+    _expect(relu_y, _shape(layout, B, Cin, H, W), dy.dtype, "relu_y")
     d = conv_desc(B, Cin, Cout, H, W, n, stride, parity, dy.dtype, layout)
     if out is None:
         out = torch.empty(_shape(layout, B, Cin, H, W), dtype=dy.dtype, device=dy.device)
+    _expect(out, _shape(layout, B, Cin, H, W), dy.dtype, "out")
     ws, nb = _workspace(d, 1, dy.device)
     A.check(A.lib().hex_conv2d_bwd_data(ctypes.byref(d), _ptr(dy), _ptr(w), _ptr(relu_y), _ptr(out),
                                         _ptr(ws), nb, _stream()), "hex_conv2d_bwd_data")
@@ -150,13 +176,18 @@ def conv2d_bwd_weight(x, dy, n: int = 1, stride: int = 1, parity: int = 0, layou
     """(dw fp32 [Cout,Cin,T], dbias fp32 [Cout] or None)."""
     _check_cuda(x, dy, dw, dbias)
     B, Cin, H, W = _dims(x, layout)
+    _dtype_ok(x)
     Cout = _dims(dy, layout)[1]
     T = A.num_taps(n)
+    Ho, Wo, _ = A.output_shape(H, W, stride, parity)
+    _expect(dy, _shape(layout, B, Cout, Ho, Wo), x.dtype, "dy")
     d = conv_desc(B, Cin, Cout, H, W, n, stride, parity, x.dtype, layout)
     if dw is None:
         dw = torch.empty((Cout, Cin, T), dtype=torch.float32, device=x.device)
     if with_bias and dbias is None:
         dbias = torch.empty((Cout,), dtype=torch.float32, device=x.device)
+    _expect(dw, (Cout, Cin, T), torch.float32, "dw")
+    _expect(dbias if with_bias else None, (Cout,), torch.float32, "dbias")
     ws, nb = _workspace(d, 2, x.device)
     A.check(A.lib().hex_conv2d_bwd_weight(ctypes.byref(d), _ptr(x), _ptr(dy), _ptr(dw),
                                           _ptr(dbias if with_bias else None), int(accumulate),
@@ -170,10 +201,7 @@ def tap_axial(n: int):
     weight order (A2: column-major left to right, top to bottom = lexicographic (dq, dr))."""
     if n < 0:
         raise ValueError("kernel size n >= 0")
-    taps = [(dq, dr) for dq in range(-n, n + 1) for dr in range(-n, n + 1)
-            if abs(dq) + abs(dr) + abs(dq + dr) <= 2 * n]
-    assert len(taps) == A.num_taps(n)
-    return taps
+    return A.tap_axial(n)
 
 
 def custom_kernel(n: int, value, out_channels: int = 1, in_channels: int = 1, dtype=torch.float32, device="cuda"):
@@ -336,10 +364,12 @@ def pool2d_fwd(x, n: int = 1, stride: int = 1, parity: int = 0, mode: str = "max
     """(y, argmax uint8 or None)."""
     _check_cuda(x, out)
     B, C, H, W = _dims(x, layout)
+    _dtype_ok(x)
     Ho, Wo, _ = A.output_shape(H, W, stride, parity)
     d = pool_desc(B, C, H, W, n, stride, parity, x.dtype, layout, mode)
     if out is None:
         out = torch.empty(_shape(layout, B, C, Ho, Wo), dtype=x.dtype, device=x.device)
+    _expect(out, _shape(layout, B, C, Ho, Wo), x.dtype, "out")
     am = None
     if mode == "max" and need_argmax:
         am = torch.empty(_shape(layout, B, C, Ho, Wo), dtype=torch.uint8, device=x.device)
@@ -351,16 +381,35 @@ def pool2d_bwd(dy, argmax, in_hw, n: int = 1, stride: int = 1, parity: int = 0, 
                layout: str = "NCHW", out=None):
     _check_cuda(dy, argmax, out)
     B, C, Ho, Wo = _dims(dy, layout)
+    _dtype_ok(dy)
     H, W = in_hw
+    Ho_, Wo_, _ = A.output_shape(H, W, stride, parity)
+    _expect(dy, _shape(layout, B, C, Ho_, Wo_), dy.dtype, "dy")
+    if mode == "max":
+        if argmax is None:
+            raise ValueError("max-pool backward needs the forward's argmax")
+        _expect(argmax, _shape(layout, B, C, Ho_, Wo_), torch.uint8, "argmax")
     d = pool_desc(B, C, H, W, n, stride, parity, dy.dtype, layout, mode)
     if out is None:
         out = torch.empty(_shape(layout, B, C, H, W), dtype=dy.dtype, device=dy.device)
+    _expect(out, _shape(layout, B, C, H, W), dy.dtype, "out")
     A.check(A.lib().hex_pool2d_bwd(ctypes.byref(d), _ptr(dy), _ptr(argmax), _ptr(out), _stream()),
             "hex_pool2d_bwd")
     return out
 
 
 # ------------------------------------------------------------------ autograd
+def relu_bwd(dy, y):
+    """dy * (y > 0) in one library kernel (y = the post-ReLU forward output)."""
+    _check_cuda(dy, y)
+    _expect(y, tuple(dy.shape), dy.dtype, "y")
+    _dtype_ok(dy)
+    dx = torch.empty_like(dy)
+    A.check(A.lib().hex_relu_bwd(dy.numel(), _DTYPES[dy.dtype], _ptr(dy), _ptr(y), _ptr(dx), _stream()),
+            "hex_relu_bwd")
+    return dx
+
+
 class HexConv2dFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, bias, n, stride, parity, relu, layout):
@@ -375,7 +424,7 @@ class HexConv2dFn(torch.autograd.Function):
         n, stride, parity, relu, layout, has_bias = ctx.cfg
         gy = gy.contiguous()
         if relu:
-            gy = gy * (y > 0).to(gy.dtype)
+            gy = relu_bwd(gy, y)
         B, Cin, H, W = _dims(x, layout)
         dx = conv2d_bwd_data(gy, w, (H, W), n, stride, parity, layout) if ctx.needs_input_grad[0] else None
         dw, db = conv2d_bwd_weight(x, gy, n, stride, parity, layout, with_bias=has_bias)

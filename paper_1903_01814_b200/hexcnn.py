@@ -65,7 +65,7 @@ class HexCNN:
     def __init__(self, batch: int = 256, H: int = 96, W: int = 96,
                  channels=(1, 64, 128, 128, 256, 256, 256), ns=(2, 1, 2, 1, 2, 1), pool_after=(2, 4),
                  num_classes: int = 2, lr: float = 1e-3, momentum: float = 0.9, seed: int = 0,
-                 device="cuda", process_group=None):
+                 device="cuda", process_group=None, reduce_grads=None):
         self.B, self.H, self.W = batch, H, W
         self.channels, self.ns, self.pool_after = tuple(channels), tuple(ns), tuple(pool_after)
         self.K = num_classes
@@ -73,6 +73,9 @@ class HexCNN:
         self.dev = torch.device(device)
         self.pg = process_group
         self.world = dist.get_world_size(process_group) if (dist.is_available() and dist.is_initialized()) else 1
+        # the per-layer gradient allreduce runs whenever there is more than one rank; reduce_grads=True
+        # forces it at world size 1 too (tests: a one-rank NCCL group captured in a CUDA graph)
+        self.reduce_grads = (self.world > 1) if reduce_grads is None else bool(reduce_grads)
         self.L = len(ns)
         self.timer = None  # optional list: (kind, layer, start_event, end_event) around conv calls
         # weight gradients on a side stream (HEXCNN_SIDE_BWD=1): measured no faster than one stream once the
@@ -289,7 +292,7 @@ class HexCNN:
         Returns the device loss tensor (mean CE of this rank's batch)."""
         stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         self.forward(x, stream)
-        if self.world > 1:
+        if self.reduce_grads:
             red = GradBucketReducer(self.pg)
             self.backward(x, labels, stream, lambda l: red.launch(self._segment(l)))
             red.wait_all()
@@ -301,12 +304,13 @@ class HexCNN:
 
     def graphed_step(self, x, labels):
         """Capture one training step on the static buffers (x, labels) in a CUDA graph and return
-        (graph, loss): graph.replay() runs the whole step (every kernel of every layer, head and SGD)
-        as one launch, without per-call host dispatch; refill x / labels in place between replays.
-        Single process only (the NCCL gradient allreduce of world > 1 stays eager).  The warm-up
-        call performs one real step."""
-        if self.world > 1:
-            raise RuntimeError("graphed_step: data-parallel steps run eagerly")
+        (graph, loss): graph.replay() runs the whole step (every kernel of every layer, head, the
+        per-layer NCCL gradient allreduces when data parallel, and SGD) as one launch, without per-call
+        host dispatch; refill x / labels in place between replays.  The warm-up call performs one real
+        step (it also creates the NCCL communicator before capture).  Data parallel capture needs the
+        NCCL backend (gloo collectives run on the host and cannot be captured)."""
+        if self.reduce_grads and dist.get_backend(self.pg) != "nccl":
+            raise RuntimeError("graphed_step: data-parallel capture needs the NCCL backend")
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):

@@ -128,3 +128,16 @@ def test_custom_kernel_taps_canonical(oracle):
         assert k[0, 0, t].item() == [1.0, 0.5, 0.25][(abs(a) + abs(b) + abs(a + b)) // 2]
     d = F.custom_kernel(1, {(0, 0): 2.0, (1, -1): -1.0}, 2, 3, device="cpu")
     assert d.shape == (2, 3, 7) and d.sum().item() == 6.0
+
+
+def test_bench_launches_n_ranks():
+    # `python bench.py --gpus 2` without a launcher starts two ranks itself (torchrun on 127.0.0.1)
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-check"],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["world"] == 2 for d in lines)

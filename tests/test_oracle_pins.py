@@ -675,3 +675,25 @@ def test_wgrad_point_evaluation_matches_dense(oracle):
             got_b = oracle.conv2d_bwd_weight_at(xb, gg, pts, n=n, s=s, pi=pi, layout=layout)
             ref_b = oracle.conv2d_bwd_weight_at(x_trunc, gg, pts, n=n, s=s, pi=pi, layout=layout)
             np.testing.assert_allclose(got_b, ref_b, atol=1e-12)
+
+
+def test_pool_bwd_rejects_invalid_argmax(oracle):
+    # the max-pool backward routes dy through an argmax produced by the code under test: an index
+    # >= T, or one naming an off-grid neighbour, must fail the check rather than write out of bounds
+    H, W, n, s = 6, 7, 1, 2
+    Ho, Wo, _ = oracle.out_shape(H, W, s)
+    dy = np.ones((1, 1, Ho, Wo))
+    ok = np.zeros((1, 1, Ho, Wo), dtype=np.uint8) + 3          # tap 3 = the centre (always in-grid)
+    oracle.pool2d_bwd(dy, ok, H, W, n=n, s=s)
+    with pytest.raises(ValueError):
+        oracle.pool2d_bwd(dy, ok + 4, H, W, n=n, s=s)            # tap index 7 >= T(1)
+    m = oracle.gather_map(H, W, n, s)
+    t_off = int(np.nonzero(m[0, 0] < 0)[0][0])                  # a corner tap outside the grid
+    bad = ok.copy()
+    bad[0, 0, 0, 0] = t_off
+    with pytest.raises(ValueError):
+        oracle.pool2d_bwd(dy, bad, H, W, n=n, s=s)
+    with pytest.raises(ValueError):
+        oracle.pool2d_bwd(dy, None, H, W, n=n, s=s)
+    with pytest.raises(ValueError):
+        oracle.pool2d_bwd(dy[..., :-1], ok[..., :-1], H, W, n=n, s=s)   # dy not on the lattice
