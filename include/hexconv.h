@@ -140,8 +140,18 @@ HEX_API hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* desc, in
  * then y = max(y, 0) if fuse_relu.
  * x: [B,Cin,H,W] in desc layout/dtype.  w: [Cout][Cin][T] in desc dtype.
  * bias: fp32 [Cout] or NULL.  y: [B,Cout,Ho,Wo] in desc layout/dtype.
- * bf16 + NHWC with Cin, Cout multiples of 16 and s == 1 runs on the
- * tcgen05 tensor-core path; everything else on the CUDA-core stencil path. */
+ *
+ * Kernel selection (internal, channel-count driven; hex_conv2d_algo reports it):
+ *  - tcgen05 tensor cores (bf16, NHWC, n <= 3, W >= 2):
+ *      fwd       s = 1 or 2, Cin % 64 == 0, Cout % 64 == 0;
+ *      bwd_data  s = 1: Cin % 64 == 0, Cout % 64 == 0 (the forward kernel on dy
+ *                with reversed taps / transposed channels);  s > 1: the same
+ *                on dy scattered onto the stride-1 grid (Cout % 64 == 0);
+ *      bwd_weight Cin % 64 == 0, Cout % 128 == 0 (s > 1 via the scattered dy).
+ *  - Cin == 1, bf16 NHWC, Cout % 64 == 0, n <= 2: warp-level mma.sync
+ *    stencil kernels (s = 1) or FFMA stencils (s > 1).
+ *  - everything else (fp32, NCHW, small or odd channel counts, any n <= 7,
+ *    any stride): CUDA-core FFMA kernels, exact fp32 products (no TF32). */
 HEX_API hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* desc, const void* x, const void* w,
                             const float* bias, int32_t fuse_relu, void* y,
                             void* ws, size_t ws_bytes, hex_stream_t stream);
@@ -198,11 +208,13 @@ HEX_API hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* desc, int32_t pass
  *   y[b][co][zo][R][C] = bias[co] + sum_ci sum_kz sum_t w[co][ci][kz][t] *
  *                        x[b][ci][sd*zo + kz - (kd-1)/2][centre(R,C) + off_t]
  * layout HEX_NCHW means NCDHW, HEX_NHWC means NDHWC (channels innermost).
- * Implementation: the kd depth taps become input channels of one 2-D
- * convolution over B*Do images (x' = depth-unfolded input, Cin' = kd*Cin, ordered
- * (kz, ci)), so every 2-D path applies -- the tcgen05 kernels for bf16 NHWC
- * with Cin'/Cout multiples of 64.  The workspace holds x' (or dx'), the
- * reordered weights and the 2-D call's own workspace.
+ * Implementation: bf16 NDHWC with in-plane s = 1 and Cin, Cout multiples of
+ * 64 runs fwd (and bwd_data when sd = 1) on the tcgen05 tap-reuse kernel with
+ * the depth taps inside its K loop (out-of-volume slices are TMA zero fill).
+ * Everything else, and every bwd_weight, unfolds the kd depth taps into input
+ * channels of one 2-D convolution over B*Do images (x' = depth-unfolded input,
+ * Cin' = kd*Cin, ordered (kz, ci)), so every 2-D path applies.  The workspace
+ * holds x' (or dx'), the reordered weights and the 2-D call's own workspace.
  * Errors: as the 2-D calls, plus HEX_ERR_INVALID_ARG for even / non-positive
  * kernel_depth or depth_stride < 1, HEX_ERR_SHAPE for depth < 1. */
 typedef struct {
@@ -289,6 +301,14 @@ HEX_API hex_status_t hex_cast_f32_bf16(int64_t count, const float* src, void* ds
 HEX_API const char* hex_status_string(hex_status_t status);
 /* Library version, e.g. 0x000100 for 0.1.0. */
 HEX_API int32_t hex_version(void);
+
+/* Test hook for A/B tests of kernel selection: the HEXCONV_* switches
+ * (DESIGN.md appendix) are read from the environment once, when the library
+ * is loaded; this overrides one of them (value NULL = unset).  Every switch
+ * selects between kernels that compute the same result.  Not synchronised
+ * with concurrent calls: set switches between calls only.
+ * Errors: HEX_ERR_INVALID_ARG (NULL or unknown name). */
+HEX_API hex_status_t hex_debug_set_switch(const char* name, const char* value);
 /* Number of kernels this library has launched since load (host counter,
  * used by bench.py to report gpu_launches). */
 HEX_API int64_t hex_launch_count(void);

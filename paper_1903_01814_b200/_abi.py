@@ -73,6 +73,7 @@ _C3P = ctypes.POINTER(Conv3dDesc)
 _SIGS = {
     "hex_num_taps": (_i32, [_i32]),
     "hex_version": (_i32, []),
+    "hex_debug_set_switch": (_i32, [ctypes.c_char_p, ctypes.c_char_p]),
     "hex_launch_count": (_i64, []),
     "hex_status_string": (ctypes.c_char_p, [_i32]),
     "hex_output_shape": (_i32, [_i32, _i32, _i32, _i32, _i32p, _i32p, _i32p]),
@@ -141,6 +142,24 @@ def tap_axial(n: int):
     buf = (_i32 * (2 * max(T, 1)))()
     check(_lib.hex_tap_axial(n, buf), "hex_tap_axial")
     return [(buf[2 * t], buf[2 * t + 1]) for t in range(T)]
+
+
+class switch:
+    """Context manager for A/B tests: override one HEXCONV_* kernel-selection switch (read from the
+    environment once at library load) and restore its previous setting on exit."""
+
+    def __init__(self, name: str, value="1"):
+        import os
+        self.name, self.value, self.prev = name, value, os.environ.get(name)
+
+    def __enter__(self):
+        check(_lib.hex_debug_set_switch(self.name.encode(), None if self.value is None else str(self.value).encode()),
+              "hex_debug_set_switch")
+        return self
+
+    def __exit__(self, *exc):
+        check(_lib.hex_debug_set_switch(self.name.encode(), None if self.prev is None else self.prev.encode()),
+              "hex_debug_set_switch")
 
 
 def launch_count() -> int:

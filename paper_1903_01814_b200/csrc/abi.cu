@@ -3,6 +3,9 @@
 // Validation is synchronous and never launches on error.  There is no CPU
 // fallback: every data-touching call runs CUDA kernels.
 #include <mutex>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "geometry.cuh"
@@ -18,6 +21,83 @@ hex_status_t sgd_momentum(int64_t n, float* p, const float* g, float* m, float l
                           cudaStream_t st);
 hex_status_t cast_f32_bf16(int64_t n, const float* s, void* d, cudaStream_t st);
 hex_status_t relu_bwd(int64_t n, int dtype, const void* dy, const void* y, void* dx, cudaStream_t st);
+}  // namespace hexconv
+
+
+// ------------------------------------------------------------------ kernel-selection switches
+// Read from the environment once, when the shared library is loaded (a constructor), so the dispatch path
+// never calls getenv and a CUDA graph captures the same kernel selection as every later call.
+namespace {
+struct SwitchEntry {
+    const char* name;
+    bool set;
+    char text[32];
+};
+SwitchEntry g_switches[] = {
+    {"HEXCONV_CONV3D_UNFOLD", false, ""},
+    {"HEXCONV_DEBUG", false, ""},
+    {"HEXCONV_DISABLE_TC", false, ""},
+    {"HEXCONV_FORCE_2SM", false, ""},
+    {"HEXCONV_FP_DEBUG", false, ""},
+    {"HEXCONV_FP_NREG", false, ""},
+    {"HEXCONV_FT_DEBUG", false, ""},
+    {"HEXCONV_FUSED_POOL_REGIONS", false, ""},
+    {"HEXCONV_FWD_TR_NORES", false, ""},
+    {"HEXCONV_NO_2SM", false, ""},
+    {"HEXCONV_NO_CONV3D_TC", false, ""},
+    {"HEXCONV_NO_F32_WGRAD", false, ""},
+    {"HEXCONV_NO_FUSED_POOL", false, ""},
+    {"HEXCONV_NO_FWD_TR", false, ""},
+    {"HEXCONV_NO_FWD_TR_PAIR", false, ""},
+    {"HEXCONV_NO_FWD_VPAIR", false, ""},
+    {"HEXCONV_NO_PLANE", false, ""},
+    {"HEXCONV_NO_POOL_TMA", false, ""},
+    {"HEXCONV_NO_TC_STRIDE2", false, ""},
+    {"HEXCONV_NO_TC_STRIDED_BWD", false, ""},
+    {"HEXCONV_NO_TILED", false, ""},
+    {"HEXCONV_NO_WG_TR", false, ""},
+    {"HEXCONV_POOL_BWD_V2", false, ""},
+    {"HEXCONV_POOL_GENERIC", false, ""},
+    {"HEXCONV_POOL_PIXEL_BWD", false, ""},
+    {"HEXCONV_POOL_TMA_MIN_W", false, ""},
+    {"HEXCONV_POOL_V", false, ""},
+    {"HEXCONV_POOL_WIDE_BWD", false, ""},
+    {"HEXCONV_SMALLC_FFMA", false, ""},
+    {"HEXCONV_WG_DEBUG", false, ""},
+    {"HEXCONV_WG_TR_MINFILL", false, ""},
+    {"HEXCONV_WG_TR_RB", false, ""}
+};
+constexpr int kNumSwitches = (int)(sizeof(g_switches) / sizeof(g_switches[0]));
+
+void load_switch(SwitchEntry& e, const char* v) {
+    e.set = v != nullptr;
+    snprintf(e.text, sizeof(e.text), "%s", v ? v : "");
+}
+
+__attribute__((constructor)) void read_switches_at_load() {
+    for (int i = 0; i < kNumSwitches; ++i) load_switch(g_switches[i], getenv(g_switches[i].name));
+}
+
+const SwitchEntry* find_switch(const char* name) {
+    for (int i = 0; i < kNumSwitches; ++i)
+        if (strcmp(g_switches[i].name, name) == 0) return &g_switches[i];
+    return nullptr;
+}
+}  // namespace
+
+namespace hexconv {
+bool sw_on(const char* name) {
+    const SwitchEntry* e = find_switch(name);
+    return e && e->set;
+}
+int sw_int(const char* name, int dflt) {
+    const SwitchEntry* e = find_switch(name);
+    return e && e->set ? atoi(e->text) : dflt;
+}
+double sw_double(const char* name, double dflt) {
+    const SwitchEntry* e = find_switch(name);
+    return e && e->set ? atof(e->text) : dflt;
+}
 }  // namespace hexconv
 
 using namespace hexconv;
@@ -79,7 +159,7 @@ Geom stride1(const Geom& g) {
 }
 bool strided_tc_ok(const hex_conv2d_desc_t* d, const Geom& g) {
     return g.s > 1 && d->dtype == HEX_BF16 && d->layout == HEX_NHWC && d->out_channels % 8 == 0 &&
-           !getenv("HEXCONV_NO_TC_STRIDED_BWD");
+           !sw_on("HEXCONV_NO_TC_STRIDED_BWD");
 }
 bool use_tc_bwd_data_up(const hex_conv2d_desc_t* d, const Geom& g) {
     return strided_tc_ok(d, g) && tc_conv_supported(stride1(g), d->out_channels, d->in_channels);
@@ -114,7 +194,17 @@ extern "C" {
 
 int32_t hex_num_taps(int32_t n) { return n < 0 ? -1 : hex_taps(n); }
 
-int32_t hex_version(void) { return 0x000100; }
+int32_t hex_version(void) { return 0x000200; }
+
+hex_status_t hex_debug_set_switch(const char* name, const char* value) {
+    if (!name) return HEX_ERR_INVALID_ARG;
+    for (int i = 0; i < kNumSwitches; ++i)
+        if (strcmp(g_switches[i].name, name) == 0) {
+            load_switch(g_switches[i], value);
+            return HEX_OK;
+        }
+    return HEX_ERR_INVALID_ARG;
+}
 
 int64_t hex_launch_count(void) { return g_launches.load(); }
 

@@ -43,6 +43,22 @@ template <typename T> __device__ __forceinline__ T from_f32(float v);
 template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
 template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
+// Kernel-selection switches: the HEXCONV_* environment
+// variables are read ONCE, when the library is loaded (abi.cu), never on the dispatch path, so a CUDA graph
+// captures the same selection every call sees.  hex_debug_set_switch() overrides one (A/B tests only).
+// Every switch picks between kernels that compute the same result (up to the documented summation order).
+bool sw_on(const char* name);                      // the variable is set
+int sw_int(const char* name, int dflt);            // its integer value, or dflt when unset
+double sw_double(const char* name, double dflt);   // its floating value, or dflt when unset
+
+// Timing-experiment modes that skip loads / MMAs / epilogues (results invalid) exist only in builds
+// compiled with -DHEXCONV_TIMING_DEBUG=1; in the product library HEX_DBG(x) is the constant 0.
+#ifndef HEXCONV_TIMING_DEBUG
+#define HEXCONV_TIMING_DEBUG 0
+#endif
+#define HEX_DBG(x) (HEXCONV_TIMING_DEBUG ? (x) : 0)
+inline int debug_mode(const char* name) { return HEXCONV_TIMING_DEBUG ? sw_int(name, 0) : 0; }
+
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 inline int num_sms() {

@@ -322,7 +322,7 @@ hex_status_t hex_conv3d_fwd(const hex_conv3d_desc_t* d, const void* x, const voi
     uint8_t* p = (uint8_t*)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
     Geom tg;
     if (c3_tc_ok(d, g.Ci, g.Co, g.Do, &tg) && a16(x) && a16(y) && a16(w) && (!bias || a16(bias)) &&
-        !getenv("HEXCONV_CONV3D_UNFOLD")) {
+        !sw_on("HEXCONV_CONV3D_UNFOLD")) {
         // depth taps in the K loop of the tcgen05 tap-reuse kernel: no unfolded copy
         const int64_t total = (int64_t)g.Co * g.Ci * g.kd * Tn;
         pack3d_kernel<<<grid_for(total), 256, 0, s>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)p, g.Co, g.Ci, g.kd,
@@ -366,7 +366,7 @@ hex_status_t hex_conv3d_bwd_data(const hex_conv3d_desc_t* d, const void* dy, con
     uint8_t* p = (uint8_t*)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
     Geom tg;
     if (g.sd == 1 && c3_tc_ok(d, g.Co, g.Ci, g.D, &tg) && a16(dy) && a16(dx) && a16(w) &&
-        !getenv("HEXCONV_CONV3D_UNFOLD")) {
+        !sw_on("HEXCONV_CONV3D_UNFOLD")) {
         // stride 1: dx = the forward of dy with depth- and tap-reversed, channel-transposed weights
         // (the 3-D form of DESIGN.md P18), depth taps in the K loop
         const int64_t total = (int64_t)g.Co * g.Ci * g.kd * Tn;

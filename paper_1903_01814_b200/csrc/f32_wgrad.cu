@@ -217,7 +217,7 @@ static FwPlan fw_plan(const Geom& g, int Cin, int Cout) {
 }
 
 bool f32_wgrad_supported(const Geom& g, int Cin, int Cout, int dtype, int layout) {
-    if (getenv("HEXCONV_NO_F32_WGRAD")) return false;
+    if (sw_on("HEXCONV_NO_F32_WGRAD")) return false;
     if (dtype != HEX_F32 || layout != HEX_NCHW || g.s != 1 || (g.n != 1 && g.n != 2)) return false;
     if (Cout % 8 || Cin < 2) return false;
     const FwPlan p = fw_plan(g, Cin, Cout);

@@ -263,7 +263,7 @@ static void launch_bwd_n1s2(const PoolArgs& a, cudaStream_t st) {
 }
 
 static bool plane_pool_ok(const PoolArgs& a) {
-    if (a.layout != HEX_NCHW || (a.g.n != 1 && a.g.n != 2) || (a.g.s != 1 && a.g.s != 2) || getenv("HEXCONV_NO_PLANE"))
+    if (a.layout != HEX_NCHW || (a.g.n != 1 && a.g.n != 2) || (a.g.s != 1 && a.g.s != 2) || sw_on("HEXCONV_NO_PLANE"))
         return false;
     const int64_t HW = (int64_t)a.g.H * a.g.W;
     return HW <= PL_MAX_ELEMS;
@@ -468,7 +468,7 @@ __global__ void c1_wgrad_reduce_kernel(const float* __restrict__ part, int nbloc
 }
 
 bool c1_conv_supported(const Geom& g, int Cin, int Cout, int dtype, int layout) {
-    if (getenv("HEXCONV_NO_PLANE")) return false;
+    if (sw_on("HEXCONV_NO_PLANE")) return false;
     if (dtype != HEX_F32 || layout != HEX_NCHW || Cin != 1 || g.s != 1 || (g.n != 1 && g.n != 2)) return false;
     if (Cout > PL_THREADS || g.B > 65535 * 8) return false;
     const int64_t band = (int64_t)(C1_RB + 2 * g.n) * (g.W + 2 * g.n);

@@ -799,10 +799,8 @@ static int ilog2_exact(int v) {  // log2(v) if v is a power of two, else -1
 
 static int pick_v(const PoolArgs& a) {
     int v = a.C % 16 == 0 ? 2 : 1;  // 16 channels/thread measured best (occupancy vs index reuse)
-    if (const char* e = getenv("HEXCONV_POOL_V")) {  // development override
-        const int want = atoi(e);
-        if ((want == 1 || want == 2 || want == 4) && a.C % (8 * want) == 0) v = want;
-    }
+    const int want = sw_int("HEXCONV_POOL_V", 0);  // development override
+    if ((want == 1 || want == 2 || want == 4) && a.C % (8 * want) == 0) v = want;
     return v;
 }
 
@@ -890,8 +888,8 @@ hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
         else
             pool_bwd_kernel<__nv_bfloat16><<<ceil_div(total, 256), 256, 0, st>>>(
                 (const __nv_bfloat16*)a.dy, nullptr, (__nv_bfloat16*)a.dx, a.g, a.C, a.sx, a.sy, a.mode, cf);
-    } else if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC") &&
-        !getenv("HEXCONV_POOL_PIXEL_BWD")) {
+    } else if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !sw_on("HEXCONV_POOL_GENERIC") &&
+        !sw_on("HEXCONV_POOL_PIXEL_BWD")) {
         const int C8 = a.C / 8;
         dim3 grid(ceil_div((int64_t)a.g.Wo * C8, 256), (a.g.H + 1) / 2, a.g.B);
         if (a.g.parity & 1)
@@ -900,9 +898,9 @@ hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
         else
             maxpool_bwd_n1s2_blk_kernel<0><<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in,
                                                                  (uint4*)a.dx, a.g, C8, ilog2_exact(C8));
-    } else if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !getenv("HEXCONV_POOL_GENERIC")) {
+    } else if (use_spec(a) && a.mode == HEX_POOL_MAX && a.g.n == 1 && a.g.s == 2 && !sw_on("HEXCONV_POOL_GENERIC")) {
         const int C8 = a.C / 8;
-        const int V = (C8 % 2 == 0 && getenv("HEXCONV_POOL_BWD_V2")) ? 2 : 1;
+        const int V = (C8 % 2 == 0 && sw_on("HEXCONV_POOL_BWD_V2")) ? 2 : 1;
         dim3 grid(ceil_div((int64_t)a.g.W * (C8 / V), 256), a.g.H, a.g.B);
         if (V == 2)
             maxpool_bwd_n1s2_kernel<2><<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in,
@@ -910,7 +908,7 @@ hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st) {
         else
             maxpool_bwd_n1s2_kernel<1><<<grid, 256, 0, st>>>((const uint4*)a.dy, (const uint2*)a.argmax_in,
                                                              (uint4*)a.dx, a.g, C8, ilog2_exact(C8));
-    } else if (use_spec(a) && getenv("HEXCONV_POOL_WIDE_BWD") && dispatch_wide(a, st, false)) {
+    } else if (use_spec(a) && sw_on("HEXCONV_POOL_WIDE_BWD") && dispatch_wide(a, st, false)) {
     } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_bwd<1, 1>(a, st); else launch_spec_bwd<1, 2>(a, st); }
         else { if (a.g.s == 1) launch_spec_bwd<2, 1>(a, st); else launch_spec_bwd<2, 2>(a, st); }

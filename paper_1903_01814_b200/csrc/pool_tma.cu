@@ -176,11 +176,10 @@ int pt_band(int W, int* nbuf) {
 }  // namespace
 
 bool pool_tma_fwd_supported(const PoolArgs& a) {
-    if (getenv("HEXCONV_NO_POOL_TMA") || !pt_encode()) return false;
+    if (sw_on("HEXCONV_NO_POOL_TMA") || !pt_encode()) return false;
     const Geom& g = a.g;
     if (a.dtype != HEX_BF16 || a.layout != HEX_NHWC || a.mode != HEX_POOL_MAX || g.n != 1 || g.s != 2) return false;
-    const char* wm = getenv("HEXCONV_POOL_TMA_MIN_W");
-    const int min_w = wm ? atoi(wm) : 64;
+    const int min_w = sw_int("HEXCONV_POOL_TMA_MIN_W", 64);
     if (a.C % 64 || g.W < min_w || g.W < 2 || g.W + 2 > 256 || g.B < 1) return false;
     if (((uintptr_t)a.x & 15) || ((uintptr_t)a.y & 15) || ((uintptr_t)a.argmax & 7)) return false;
     int nb;
@@ -212,7 +211,7 @@ hex_status_t pool_tma_fwd(const PoolArgs& a, cudaStream_t st) {
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (er != CUDA_SUCCESS) {
-        if (getenv("HEXCONV_DEBUG")) fprintf(stderr, "pool_tma: tensor map encode failed (%d)\n", (int)er);
+        if (sw_on("HEXCONV_DEBUG")) fprintf(stderr, "pool_tma: tensor map encode failed (%d)\n", (int)er);
         return HEX_ERR_CUDA;
     }
     if (cudaFuncSetAttribute(pool_tma_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -220,7 +219,7 @@ hex_status_t pool_tma_fwd(const PoolArgs& a, cudaStream_t st) {
     const int grid = p.units < num_sms() ? p.units : num_sms();
     pool_tma_fwd_kernel<<<grid, PT_THREADS, smem, st>>>(m, p, buf_bytes, (uint32_t)(p.box_rows * p.box_cols * 128));
     count_launch();
-    if (getenv("HEXCONV_DEBUG")) {
+    if (sw_on("HEXCONV_DEBUG")) {
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) fprintf(stderr, "pool_tma: launch failed: %s\n", cudaGetErrorString(e));
         return e == cudaSuccess ? HEX_OK : HEX_ERR_CUDA;

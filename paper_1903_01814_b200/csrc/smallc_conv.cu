@@ -211,7 +211,7 @@ bool smallc_supported(const Geom& g, int Cin, int Cout) {
 // Stride 1 runs on the tensor-core kernels of smallc_mma.cu; the FFMA stencil
 // above remains for stride > 1 (HEXCONV_SMALLC_FFMA=1 forces it, for A/B runs).
 static bool use_mma(const Geom& g, int Cout) {
-    static const bool force_ffma = getenv("HEXCONV_SMALLC_FFMA") != nullptr;
+    static const bool force_ffma = sw_on("HEXCONV_SMALLC_FFMA");
     return !force_ffma && smallc_mma_supported(g, 1, Cout);
 }
 

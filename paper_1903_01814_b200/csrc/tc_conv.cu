@@ -342,32 +342,25 @@ __device__ __forceinline__ void fwd_epilogue(const TcFwdParams& p, const CUtenso
     }
 }
 
-// RESB: the whole packed weight tensor ([T][kgroups][KC][BN][64] bf16, <= RES_MAX bytes) is
-// loaded once per CTA and stays resident in shared memory; the producer then
-// streams only the A operand (one TMA op per K iteration instead of two).
-constexpr int RES_MAX = 131072;
-
-template <int BN, int KC, bool RESB = false>
+template <int BN, int KC>
 __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
 tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                    const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y0,
                    const __grid_constant__ CUtensorMap map_y1, const __grid_constant__ CUtensorMap map_m0,
                    const __grid_constant__ CUtensorMap map_m1, const __grid_constant__ TcFwdParams p) {
     using Cfg = FwdCfg<BN, KC>;
-    constexpr int STAGES = RESB ? 4 : Cfg::STAGES;
-    constexpr int STAGE = RESB ? Cfg::A_BYTES : Cfg::STAGE;
+    constexpr int STAGES = Cfg::STAGES;
+    constexpr int STAGE = Cfg::STAGE;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem_base = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned, shared space
-    uint8_t* resb = smem_base;                         // resident weights (RESB only)
-    uint8_t* smem = smem_base + (RESB ? RES_MAX : 0);  // stage ring
+    uint8_t* smem = smem_base;  // stage ring
     uint8_t* obuf = smem + STAGES * STAGE;
     uint64_t* full = (uint64_t*)(obuf + 2 * Cfg::OUT_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* mbar = tempty + 2;  // mask-tile loads into the two staging buffers
-    uint64_t* bres = mbar + 2;    // resident-weight load
-    uint32_t* tmem_slot = (uint32_t*)(bres + 1);
+    uint32_t* tmem_slot = (uint32_t*)(mbar + 3);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
@@ -377,7 +370,6 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
             ptx::mbar_init(&tempty[a], TC_EPI_THREADS / 32);
             ptx::mbar_init(&mbar[a], 1);
         }
-        ptx::mbar_init(bres, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&map_x0);
         ptx::prefetch_tmap(&map_x1);
@@ -393,15 +385,8 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
     const int kgroups = p.kblocks / KC;
     const int k_iters = p.T * kgroups;
 
-    constexpr int BLK = KC * BN * 128;  // one (tap, K group) weight block
     if (warp == 0) {
         if (lane == 0) {
-            if constexpr (RESB) {
-                ptx::mbar_arrive_expect_tx(bres, (uint32_t)(k_iters * BLK));
-                for (int t = 0; t < p.T; ++t)
-                    for (int kg = 0; kg < kgroups; ++kg)
-                        ptx::tma_load_4d(&map_w, bres, resb + (t * kgroups + kg) * BLK, 0, 0, kg * KC, t);
-            }
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
@@ -417,8 +402,7 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
                         uint8_t* sa = smem + stage * STAGE;
                         ptx::mbar_arrive_expect_tx(&full[stage], STAGE);
                         ptx::tma_load_5d(mx, &full[stage], sa, 0, row, col, tc.b0, kg * KC);
-                        if constexpr (!RESB)
-                            ptx::tma_load_4d(&map_w, &full[stage], sa + Cfg::A_BYTES, 0, tc.n0, kg * KC, t);
+                        ptx::tma_load_4d(&map_w, &full[stage], sa + Cfg::A_BYTES, 0, tc.n0, kg * KC, t);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -431,7 +415,6 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
             uint32_t phase = 0;
             int acc = 0;
             uint32_t aphase = 0;
-            if constexpr (RESB) ptx::mbar_wait(bres, 0);
             for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
                 ptx::mbar_wait(&tempty[acc], aphase ^ 1);
                 ptx::tc_fence_after();
@@ -441,7 +424,7 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
                     ptx::tc_fence_after();
                     const uint32_t a0 = ptx::smem_u32(smem + stage * STAGE);
                     // k iteration it = (tap t, K group kg) with it = t * kgroups + kg
-                    const uint32_t b0 = RESB ? ptx::smem_u32(resb + it * BLK) : a0 + Cfg::A_BYTES;
+                    const uint32_t b0 = a0 + Cfg::A_BYTES;
 #pragma unroll
                     for (int c = 0; c < KC; ++c)
 #pragma unroll
@@ -644,9 +627,9 @@ static int pick_bn(int Cout) {
 // strided layers stay on the CUDA-core kernels
 bool tc_conv_fwd_supported(const Geom& g, int Cin, int Cout) {
     if (g.s == 1) return tc_conv_supported(g, Cin, Cout);
-    if (g.s != 2 || g.T > TC_MAXT || getenv("HEXCONV_NO_TC_STRIDE2")) return false;
+    if (g.s != 2 || g.T > TC_MAXT || sw_on("HEXCONV_NO_TC_STRIDE2")) return false;
     if (Cin % TC_BK != 0 || pick_bn(Cout) == 0 || g.Wo < 2) return false;
-    if (getenv("HEXCONV_DISABLE_TC")) return false;
+    if (sw_on("HEXCONV_DISABLE_TC")) return false;
     return get_encode() != nullptr;
 }
 
@@ -654,7 +637,7 @@ bool tc_conv_supported(const Geom& g, int Cin, int Cout) {
     if (g.s != 1 || g.T > TC_MAXT) return false;
     if (Cin % TC_BK != 0 || pick_bn(Cout) == 0) return false;
     if (g.W < 2) return false;
-    if (getenv("HEXCONV_DISABLE_TC")) return false;
+    if (sw_on("HEXCONV_DISABLE_TC")) return false;
     return get_encode() != nullptr;
 }
 
@@ -672,24 +655,6 @@ static hex_status_t launch_fwd_bn(const CUtensorMap& mx0, const CUtensorMap& mx1
     }
     const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
     tc_conv_fwd_kernel<BN, KC><<<grid, TC_FWD_THREADS, Cfg::SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
-    count_launch();
-    return last_launch_status();
-}
-
-template <int BN>
-static hex_status_t launch_fwd_res(const CUtensorMap& mx0, const CUtensorMap& mx1, const CUtensorMap& mw,
-                                   const CUtensorMap& my0, const CUtensorMap& my1, const CUtensorMap& mm0,
-                                   const CUtensorMap& mm1, const TcFwdParams& p, cudaStream_t st) {
-    constexpr int SMEM = RES_MAX + 4 * FwdCfg<BN, 1>::A_BYTES + 2 * FwdCfg<BN, 1>::OUT_BYTES + 1024 + 256;
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(tc_conv_fwd_kernel<BN, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SMEM) != cudaSuccess)
-            return HEX_ERR_CUDA;
-        attr_set = true;
-    }
-    const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
-    tc_conv_fwd_kernel<BN, 1, true><<<grid, TC_FWD_THREADS, SMEM, st>>>(mx0, mx1, mw, my0, my1, mm0, mm1, p);
     count_launch();
     return last_launch_status();
 }
@@ -719,8 +684,8 @@ static hex_status_t launch_fwd2_bn(const CUtensorMap& mx0, const CUtensorMap& mx
 // CTA pairs (cta_group::2, M = 256) so each SM loads only half the weight tile.
 // HEXCONV_FORCE_2SM / HEXCONV_NO_2SM / HEXCONV_KC override for experiments.
 static bool use_2sm(int BN) {
-    if (getenv("HEXCONV_NO_2SM")) return false;
-    if (getenv("HEXCONV_FORCE_2SM")) return BN >= 128;
+    if (sw_on("HEXCONV_NO_2SM")) return false;
+    if (sw_on("HEXCONV_FORCE_2SM")) return BN >= 128;
     return BN == 256;
 }
 
@@ -741,11 +706,7 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     p.n_tiles = a.Cout / BN;
     p.m_total = p.tiles0 + p.rt * p.jt1 * p.bt;
     const bool pair = use_2sm(BN) && p.m_total >= 2;
-    // resident weights: one n tile whose packed weights fit the resident region
-    const bool resident = !pair && p.n_tiles == 1 && BN <= 128 &&
-                          (size_t)g.T * a.Cout * a.Cin * 2 <= (size_t)RES_MAX && getenv("HEXCONV_RESB");
-    int KC = (a.Cin % 128 == 0 && !(BN == 256 && !pair) && !resident) ? 2 : 1;
-    if (getenv("HEXCONV_KC")) KC = atoi(getenv("HEXCONV_KC")) == 2 && a.Cin % 128 == 0 ? 2 : 1;
+    int KC = (a.Cin % 128 == 0 && !(BN == 256 && !pair)) ? 2 : 1;
     if (BN == 256 && !pair) KC = 1;  // a 1-CTA BN = 256 stage with KC = 2 would not fit twice in smem
     p.total_tiles = p.m_total * p.n_tiles;
     p.pair_tiles = ceil_div(p.m_total, 2) * p.n_tiles;
@@ -779,7 +740,6 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
         if (BN == 256) return KC == 2 ? launch_fwd2_bn<256, 2>(HEX_FWD_ARGS) : launch_fwd2_bn<256, 1>(HEX_FWD_ARGS);
         return KC == 2 ? launch_fwd2_bn<128, 2>(HEX_FWD_ARGS) : launch_fwd2_bn<128, 1>(HEX_FWD_ARGS);
     }
-    if (resident) return BN == 128 ? launch_fwd_res<128>(HEX_FWD_ARGS) : launch_fwd_res<64>(HEX_FWD_ARGS);
     switch (BN) {
         case 256: return launch_fwd_bn<256, 1>(HEX_FWD_ARGS);
         case 128: return KC == 2 ? launch_fwd_bn<128, 2>(HEX_FWD_ARGS) : launch_fwd_bn<128, 1>(HEX_FWD_ARGS);
@@ -891,7 +851,7 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
                 const int pc = (P + p.parity) & 1;
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* s = smem + stage * Cfg::STAGE_BYTES;
-                if (p.dbg == 1) {
+                if (HEX_DBG(p.dbg) == 1) {
                     ptx::mbar_arrive(&full[stage]);
                     if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
                     continue;
@@ -927,7 +887,7 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
                     // MN-major SW128: 8-row K groups 1024 B apart, 64-element MN blocks one box (LBO) apart
                     const uint64_t ad = ptx::smem_desc_sw128(s + k * 2048, Cfg::BOX, 1024);
                     const uint32_t acc = (pt != pt_begin) || (k != 0);
-                    if (p.dbg == 2) continue;
+                    if (HEX_DBG(p.dbg) == 2) continue;
                     ptx::mma_bf16(tmem_base, ad, ptx::smem_desc_sw128(bx + k * 2048, Cfg::BOX, 1024), idesc0, acc);
                     if (n1 > 0)
                         ptx::mma_bf16(tmem_base + 256, ad,
@@ -1220,7 +1180,7 @@ struct WgPlan {
 };
 
 static bool wg_use_pair(int Cin, int Cout) {
-    if (getenv("HEXCONV_NO_2SM")) return false;
+    if (sw_on("HEXCONV_NO_2SM")) return false;
     return Cout % 256 == 0 && Cin % 128 == 0;
 }
 
@@ -1256,7 +1216,7 @@ static WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
 bool tc_wgrad_supported(const Geom& g, int Cin, int Cout) {
     if (g.s != 1 || g.T > TC_MAXT || g.W < 2) return false;
     if (Cout % 128 != 0 || Cin % 64 != 0) return false;
-    if (getenv("HEXCONV_DISABLE_TC")) return false;
+    if (sw_on("HEXCONV_DISABLE_TC")) return false;
     return get_encode() != nullptr;
 }
 
@@ -1303,7 +1263,7 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
     p.chunks = w.chunks; p.tiles_per_chunk = w.tiles_per_chunk;
     p.part = (float*)ws;
     p.db_part = a.dbias ? (float*)ws + (size_t)w.chunks * g.T * a.Cout * a.Cin : nullptr;
-    p.dbg = getenv("HEXCONV_WG_DEBUG") ? atoi(getenv("HEXCONV_WG_DEBUG")) : 0;
+    p.dbg = debug_mode("HEXCONV_WG_DEBUG");
     for (int pc = 0; pc < 2; ++pc)
         for (int t = 0; t < g.T; ++t) {
             int dc, dr;

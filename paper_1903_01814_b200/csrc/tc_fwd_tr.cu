@@ -316,7 +316,7 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
                 ptx::mbar_wait(&tempty[acc], aphase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
-                if (p.debug == 2) {
+                if (HEX_DBG(p.debug) == 2) {
                     for (int u = 0; u < p.kd * p.kchunks * SL::count(); ++u) {
                         ptx::mbar_wait(&full[stage], phase);
                         ptx::mbar_arrive(&empty[stage]);
@@ -354,7 +354,7 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
         uint32_t mphase0 = 0, mphase1 = 0;
         // ReLU-backward mask tiles are TMA-loaded one chunk ahead -- across tile boundaries too, so
         // the next tile's first mask chunk is in flight while the current tile's last chunk drains
-        if (p.has_mask && et == 0 && p.debug != 1) {
+        if (p.has_mask && et == 0 && HEX_DBG(p.debug) != 1) {
             const int t0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
             if (t0 < (PAIR ? p.pair_tiles : p.total_tiles)) {
                 int P, r0, j0, b, n0;
@@ -374,7 +374,7 @@ tc_fwd_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_consta
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
 #pragma unroll 1
-            for (int ch = 0; ch < (p.debug == 1 ? 0 : BN / 64); ++ch) {
+            for (int ch = 0; ch < (HEX_DBG(p.debug) == 1 ? 0 : BN / 64); ++ch) {
                 uint8_t* buf = obuf + ob * FT_OUT;
                 const int c0 = n0 + ch * 64;
                 if (p.has_mask) {
@@ -742,7 +742,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
             for (int seq = 0; fp_tile<PAIR>(p, seq, tl); ++seq) {
                 ptx::mbar_wait(&tempty[slot], sphase ^ 1);
                 ptx::tc_fence_after();
-                if (!PAIR && p.debug == 2) {
+                if (!PAIR && HEX_DBG(p.debug) == 2) {
                     for (int u = 0; u < (N == 1 ? 4 : 2 * SL::count()) * p.kchunks; ++u) {
                         ptx::mbar_wait(&full[stage], phase);
                         ptx::mbar_arrive(&empty[stage]);
@@ -797,7 +797,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
             const bool outside = img_r < 0 || img_r >= p.H || jv < 0 || 2 * jv + cv >= p.W;
             ptx::mbar_wait(&tfull[slot], sphase);
             ptx::tc_fence_after();
-            if (!PAIR && p.debug == 1) {
+            if (!PAIR && HEX_DBG(p.debug) == 1) {
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&tempty[slot]);
@@ -876,7 +876,7 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
         const int kcar = kv * 1024 + kr * 512 + ks * FP_PIX + ki * 16;
         int g = 0;
         FpTile tl;
-        for (int seq = 0; (PAIR || p.debug != 1) && fp_tile<PAIR>(p, seq, tl); ++seq) {
+        for (int seq = 0; (PAIR || HEX_DBG(p.debug) != 1) && fp_tile<PAIR>(p, seq, tl); ++seq) {
             const int C = 7 * tl.k + wc;
             const int rho = C & 1;  // centre row of window (R, C): cr = 2R + rho
             // owned centre rows [lo, hi]
@@ -1135,7 +1135,7 @@ tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
         uint32_t sphase = 0;
         int ob = 0;
         uint32_t mphase0 = 0, mphase1 = 0;
-        if (p.has_mask && et == 0 && p.debug != 1 && (int)(PAIR ? blockIdx.x / 2 : blockIdx.x) < (PAIR ? (p.pairs + 1) / 2 : p.pairs)) {
+        if (p.has_mask && et == 0 && HEX_DBG(p.debug) != 1 && (int)(PAIR ? blockIdx.x / 2 : blockIdx.x) < (PAIR ? (p.pairs + 1) / 2 : p.pairs)) {
             int r0, j0, b;
             fv_decode(p, PAIR ? (int)(blockIdx.x / 2) * 2 + (int)rank : (int)blockIdx.x, &r0, &j0, &b);
             ptx::mbar_arrive_expect_tx(&mbar[0], FT_OUT);
@@ -1149,7 +1149,7 @@ tc_fwd_vpair_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
             ptx::mbar_wait(&tfull[slot], sphase);
             ptx::tc_fence_after();
 #pragma unroll 1
-            for (int u = 0; u < (p.debug == 1 ? 0 : UNITS); ++u) {
+            for (int u = 0; u < (HEX_DBG(p.debug) == 1 ? 0 : UNITS); ++u) {
                 const int v = u / (BN / 64), ch = u % (BN / 64);
                 uint8_t* buf = obuf + ob * FT_OUT;
                 const int c0 = ch * 64;
@@ -1318,25 +1318,9 @@ FtPlan ft_plan(const Geom& g, int Cin, int Cout, bool allow_res = true) {
     if (Cin % 64) return pl;
     const int A = (FT_RB + 2 * g.n) * FT_JB * 128;
     const int fixed = 2 * FT_OUT + 1024 + 512;
-    // 1) resident weights: one Cout tile (Cout = 64 or 128), one CTA per tile.  The CTA-pair variant
-    //    (each CTA keeps half of the weights, more room for A stages) measured slower on C5 layer 2
-    //    (fwd 382 vs 230 us) and is kept for experiments (HEXCONV_FWD_TR_RESPAIR).
-    if (allow_res && (Cout == 64 || Cout == 128) && !getenv("HEXCONV_FWD_TR_NORES") &&
-        getenv("HEXCONV_FWD_TR_RESPAIR")) {
-        const int res_bytes = g.T * (Cin / 64) * (Cout / 2) * 128;
-        if (res_bytes + fixed + 4 * A <= FT_SMEM_MAX) {
-            pl.BN = Cout;
-            pl.res = 1;
-            pl.pair = 1;
-            pl.tg = ft_tg(true, g.n, Cout);
-            pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
-            if (pl.stages > 8) pl.stages = 8;
-            pl.smem = res_bytes + pl.stages * A + fixed;
-            pl.ok = true;
-            return pl;
-        }
-    }
-    if (allow_res && (Cout == 64 || Cout == 128) && !getenv("HEXCONV_FWD_TR_NORES")) {
+    // 1) resident weights: one Cout tile (Cout = 64 or 128), one CTA per tile.  (A CTA-pair variant holding
+    //    half of the weights per CTA measured slower on C5 layer 2, fwd 382 vs 230 us, and was removed.)
+    if (allow_res && (Cout == 64 || Cout == 128) && !sw_on("HEXCONV_FWD_TR_NORES")) {
         const int res_bytes = g.T * (Cin / 64) * Cout * 128;
         if (res_bytes + fixed + 4 * A <= FT_SMEM_MAX) {
             pl.BN = Cout;
@@ -1351,7 +1335,7 @@ FtPlan ft_plan(const Geom& g, int Cin, int Cout, bool allow_res = true) {
     }
     // 2) CTA pairs (M = 256) with streamed weights, each CTA loading half of every weight tile
     pl.BN = Cout % 256 == 0 ? 256 : (Cout % 128 == 0 ? 128 : (Cout % 64 == 0 ? 64 : 0));
-    if (!pl.BN || getenv("HEXCONV_NO_FWD_TR_PAIR")) return pl;
+    if (!pl.BN || sw_on("HEXCONV_NO_FWD_TR_PAIR")) return pl;
     pl.pair = 1;
     pl.tg = ft_tg(false, g.n, pl.BN);
     const int st = A + pl.tg * (pl.BN / 2) * 128;
@@ -1367,7 +1351,7 @@ FtPlan ft_plan(const Geom& g, int Cin, int Cout, bool allow_res = true) {
 // Taken for stride-1 bf16 NHWC layers whose 16 x 8 tiles fill >= 85% of both views (n = 1, 2), with
 // resident weights or as CTA pairs; HEXCONV_NO_FWD_TR disables it.
 bool tc_fwd_tr_supported(const Geom& g, int Cin, int Cout) {
-    if (getenv("HEXCONV_NO_FWD_TR")) return false;
+    if (sw_on("HEXCONV_NO_FWD_TR")) return false;
     if (g.s != 1 || (g.n != 1 && g.n != 2) || g.W < 2 || g.B > 65535) return false;
     const double fill_c = (double)((g.W + 1) / 2) / (ceil_div((g.W + 1) / 2, FT_JB) * FT_JB);
     const double fill_r = (double)g.H / (ceil_div(g.H, FT_RB) * FT_RB);
@@ -1408,11 +1392,11 @@ static hex_status_t launch_ft(const CUtensorMap* maps, const FtParams& p, int sm
     return last_launch_status();
 }
 
-// view-pair plan: n = 1, resident weights, Cout 64 / 128; returns stages (0 = not eligible).  *pair: CTA
-// pairs (M = 256 per MMA, each CTA holding half of every weight tile), HEXCONV_FV_PAIR=1 (experiment)
+// view-pair plan: n = 1, resident weights, Cout 64 / 128; returns stages (0 = not eligible).  *pair is
+// always false: the CTA-pair variant (M = 256 per MMA) measured no faster (291 vs 289 us) and is not built.
 static int fv_stages(const Geom& g, int Cin, int Cout, int* smem, bool* pair) {
-    if (g.n != 1 || g.s != 1 || Cin % 64 || (Cout != 64 && Cout != 128) || getenv("HEXCONV_NO_FWD_VPAIR")) return 0;
-    *pair = getenv("HEXCONV_FV_PAIR") != nullptr;
+    if (g.n != 1 || g.s != 1 || Cin % 64 || (Cout != 64 && Cout != 128) || sw_on("HEXCONV_NO_FWD_VPAIR")) return 0;
+    *pair = false;
     const int A = (FT_RB + 3) * FT_JB * 128;
     const int res_bytes = 7 * (Cin / 64) * (*pair ? Cout / 2 : Cout) * 128;
     const int fixed = 2 * FT_OUT + 1024 + 512;
@@ -1481,7 +1465,6 @@ static hex_status_t tc_fwd_vpair(const TcConvArgs& a, int stages, int smem, bool
         maps[5] = maps[3];
         maps[6] = maps[4];
     }
-    if (pair) return a.Cout == 128 ? launch_fv<128, true>(maps, p, smem, st) : launch_fv<64, true>(maps, p, smem, st);
     return a.Cout == 128 ? launch_fv<128, false>(maps, p, smem, st) : launch_fv<64, false>(maps, p, smem, st);
 }
 
@@ -1509,7 +1492,7 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
     p.stages = pl.stages;
     p.relu = a.relu;
     p.has_mask = a.relu_y != nullptr;
-    p.debug = getenv("HEXCONV_FT_DEBUG") ? atoi(getenv("HEXCONV_FT_DEBUG")) : 0;
+    p.debug = debug_mode("HEXCONV_FT_DEBUG");
     p.kd = p.D = p.Do = p.sd = 1;
     p.pd = 0;
     p.bias = a.bias;
@@ -1525,12 +1508,6 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
     } else {
         maps[5] = maps[3];
         maps[6] = maps[4];
-    }
-    if (pl.res && pl.pair) {
-        if (pl.BN == 128) return g.n == 1 ? launch_ft<128, 1, true, true>(maps, p, pl.smem, st)
-                                          : launch_ft<128, 2, true, true>(maps, p, pl.smem, st);
-        return g.n == 1 ? launch_ft<64, 1, true, true>(maps, p, pl.smem, st)
-                        : launch_ft<64, 2, true, true>(maps, p, pl.smem, st);
     }
     if (pl.res) {
         if (pl.BN == 128) return g.n == 1 ? launch_ft<128, 1, true, false>(maps, p, pl.smem, st)
@@ -1551,7 +1528,7 @@ hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st) {
 // [B][Do][Ho][Wo][Cout] (s = 1), a.wpack bf16 [kd*T][Cout][Cin] (depth-major taps).  The depth taps run
 // inside the K loop of the streamed CTA-pair tap-reuse kernel (no unfold copy).
 bool tc_conv3d_supported(const Geom& g, int Cin, int Cout, int Do) {
-    if (getenv("HEXCONV_NO_CONV3D_TC")) return false;
+    if (sw_on("HEXCONV_NO_CONV3D_TC")) return false;
     Geom go = g;
     go.B = g.B * Do;
     if (go.B > 65535 || !tc_fwd_tr_supported(go, Cin, Cout)) return false;
@@ -1608,18 +1585,18 @@ struct FpPlan {
     int stages, smem, nr, nc, Ho, Wo, nreg;
     bool ok, pair;
 };
-// pair: CTA pairs (M = 256 MMAs, each CTA holding half of every weight tile), n = 1, HEXCONV_FP_PAIR=1
+// pair is always false: the CTA-pair variant (M = 256 MMAs) measured no faster (265.6 vs 263.6 us) and is
+// not built
 FpPlan fp_plan(const Geom& g, int Cin, int Cout) {
     FpPlan pl{};
-    pl.pair = g.n == 1 && getenv("HEXCONV_FP_PAIR") != nullptr;
+    pl.pair = false;
     if (g.s != 1 || (g.n != 1 && g.n != 2) || Cin % 64 || (Cout != 64 && Cout != 128) || g.W < 2) return pl;
     int po;
     if (!out_shape(g.H, g.W, 2, g.parity, &pl.Ho, &pl.Wo, &po)) return pl;
     const int A = (FT_RB + 2 * g.n + (g.n == 1 ? 1 : 0)) * FT_JB * 128;
     const int res_bytes = g.T * (Cin / 64) * (pl.pair ? Cout / 2 : Cout) * 128;
     // 4 region buffers when 3 ring stages still fit next to them (HEXCONV_FP_NREG=2 forces 2)
-    const char* nr_env = getenv("HEXCONV_FP_NREG");
-    for (pl.nreg = (nr_env && atoi(nr_env) == 2) ? 2 : 4; pl.nreg >= 2; pl.nreg /= 2) {
+    for (pl.nreg = sw_int("HEXCONV_FP_NREG", 4) == 2 ? 2 : 4; pl.nreg >= 2; pl.nreg /= 2) {
         const int fixed = pl.nreg * FP_BUF + (Cout / 32) * FP_CARRY + Cout * 4 + 1024 + 512;
         pl.stages = (FT_SMEM_MAX - fixed - res_bytes) / A;
         if (pl.stages >= 3) break;
@@ -1637,7 +1614,7 @@ FpPlan fp_plan(const Geom& g, int Cin, int Cout) {
 }  // namespace
 
 bool tc_conv_maxpool_supported(const Geom& g, int Cin, int Cout) {
-    if (getenv("HEXCONV_NO_FUSED_POOL") || !ft_encode()) return false;
+    if (sw_on("HEXCONV_NO_FUSED_POOL") || !ft_encode()) return false;
     return fp_plan(g, Cin, Cout).ok;
 }
 
@@ -1654,8 +1631,8 @@ hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax,
     const int strips = g.B * pl.nc;
     p.ntr = (g.H + FT_RB - 1) / FT_RB;
     const int sms = num_sms();
-    const bool strip_mode = !getenv("HEXCONV_FUSED_POOL_REGIONS");
-    p.debug = getenv("HEXCONV_FP_DEBUG") ? atoi(getenv("HEXCONV_FP_DEBUG")) : 0;
+    const bool strip_mode = !sw_on("HEXCONV_FUSED_POOL_REGIONS");
+    p.debug = debug_mode("HEXCONV_FP_DEBUG");
     int grid = pl.pair ? sms & ~1 : sms;
     p.full_rounds = strip_mode ? strips / grid : 0;
     p.left_regions = (strips - p.full_rounds * grid) * pl.nr;
@@ -1690,11 +1667,11 @@ hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax,
     }
     if (a.Cout == 128) {
         if (g.n == 1) {
-            if (pl.pair) HEX_FP(128, 1, true) else HEX_FP(128, 1, false)
+            HEX_FP(128, 1, false)
         } else HEX_FP(128, 2, false)
     } else {
         if (g.n == 1) {
-            if (pl.pair) HEX_FP(64, 1, true) else HEX_FP(64, 1, false)
+            HEX_FP(64, 1, false)
         } else HEX_FP(64, 2, false)
     }
 #undef HEX_FP

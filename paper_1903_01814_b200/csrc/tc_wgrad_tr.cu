@@ -125,7 +125,7 @@ __device__ __forceinline__ void mma_loop(const MmaLoopArgs& m) {
         ptx::tc_fence_after();
         const uint64_t soff = (uint64_t)stage * m.stage16;
         const uint64_t ad0 = m.a_desc0 + soff, xd0 = m.x_desc0 + soff;
-        if (m.dbg != 2) {
+        if (HEX_DBG(m.dbg) != 2) {
 #pragma unroll
             for (int k = 0; k < KSTEPS; ++k) {
                 const uint64_t ad = ad0 + (uint64_t)(k * 128);  // 16 pixels = 2048 B
@@ -210,7 +210,7 @@ tc_wgrad_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
                 const int pc = (P + p.parity) & 1;  // centre column parity
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* s = smem + stage * stage_stride;
-                if (p.dbg == 1) {
+                if (HEX_DBG(p.dbg) == 1) {
                     ptx::mbar_arrive(&full[stage]);
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     continue;
@@ -338,7 +338,7 @@ static int tr_stage_stride(int n, int RB) {
 static int tr_smem_bytes(int n, int RB, int stages) { return stages * tr_stage_stride(n, RB) + 2048 + 1024 + 256; }
 // Rows per pixel tile: 16 (fewer, larger stages) by default; HEXCONV_WG_TR_RB=8 for experiments.
 static int tr_rb() {
-    static const int rb = (getenv("HEXCONV_WG_TR_RB") && atoi(getenv("HEXCONV_WG_TR_RB")) == 8) ? 8 : 16;
+    static const int rb = (sw_int("HEXCONV_WG_TR_RB", 16) == 8) ? 8 : 16;
     return rb;
 }
 
@@ -382,12 +382,12 @@ namespace hexconv {
 // Taken when the tiles are well filled (sub-column and row padding waste <= 15%)
 // and the 8-row x boxes divide evenly; HEXCONV_NO_WG_TR disables it.
 bool tc_wgrad_tr_supported(const Geom& g, int Cin, int Cout) {
-    if (getenv("HEXCONV_NO_WG_TR")) return false;
+    if (sw_on("HEXCONV_NO_WG_TR")) return false;
     if (g.s != 1 || (g.n != 1 && g.n != 2) || Cout % 128 || Cin % 64 || g.W < 2) return false;
     if (g.B > 65535) return false;
     const double fill_c = (double)((g.W + 1) / 2) / (ceil_div((g.W + 1) / 2, TR_JB) * TR_JB);
     const double fill_r = (double)g.H / (ceil_div(g.H, tr_rb()) * tr_rb());
-    const double min_fill = getenv("HEXCONV_WG_TR_MINFILL") ? atof(getenv("HEXCONV_WG_TR_MINFILL")) : 0.85;
+    const double min_fill = sw_double("HEXCONV_WG_TR_MINFILL", 0.85);
     if (fill_c * fill_r < min_fill) return false;
     if (tr_smem_bytes(g.n, tr_rb(), 2) > TR_SMEM_MAX) return false;
     return tr_encode() != nullptr;
@@ -413,7 +413,7 @@ hex_status_t tc_wgrad_tr(const TcWgradArgs& a, void* ws, size_t ws_bytes, int* c
         p.ncols[i] = w.ncols[i];
         for (int j = 0; j < TR_MAXCOLS; ++j) p.gcols[i][j] = w.gcols[i][j];
     }
-    p.dbg = getenv("HEXCONV_WG_DEBUG") ? atoi(getenv("HEXCONV_WG_DEBUG")) : 0;
+    p.dbg = debug_mode("HEXCONV_WG_DEBUG");
     p.part = (float*)ws;
     p.db_part = a.dbias ? (float*)ws + (size_t)w.chunks * g.T * a.Cout * a.Cin : nullptr;
     CUtensorMap mx0, mx1, md0, md1;

@@ -137,7 +137,7 @@ tiled_conv_s1_kernel(const float* __restrict__ x, const float* __restrict__ w, c
 }
 
 bool tiled_supported(const Geom& g, int dtype, int layout) {
-    return dtype == HEX_F32 && layout == HEX_NCHW && g.s == 1 && g.n <= 3 && !getenv("HEXCONV_NO_TILED");
+    return dtype == HEX_F32 && layout == HEX_NCHW && g.s == 1 && g.n <= 3 && !sw_on("HEXCONV_NO_TILED");
 }
 
 namespace {

@@ -96,14 +96,14 @@ def test_conv3d_bf16_tensor_cores(F, oracle):
     assert F.conv3d_output_shape(d) == (5, 16, 16)
 
 
-def test_conv3d_bf16_unfold_path_agrees(F, oracle, monkeypatch):
+def test_conv3d_bf16_unfold_path_agrees(F, oracle):
+    from paper_1903_01814_b200 import _abi as A
     # the depth-in-K-loop tcgen05 path (default) and the unfold + 2-D path both meet the bar
     for k, (Ci, Co, D, n, kd, sd, pi) in enumerate([(64, 128, 7, 1, 3, 1, 1), (128, 64, 3, 1, 5, 1, 0),
                                                       (64, 64, 9, 2, 3, 2, 1)]):
         case(F, oracle, 1, Ci, Co, D, 20, 18, n, kd, 1, sd, pi, torch.bfloat16, "NDHWC", 300 + k)
-        monkeypatch.setenv("HEXCONV_CONV3D_UNFOLD", "1")
-        case(F, oracle, 1, Ci, Co, D, 20, 18, n, kd, 1, sd, pi, torch.bfloat16, "NDHWC", 300 + k)
-        monkeypatch.delenv("HEXCONV_CONV3D_UNFOLD")
+        with A.switch("HEXCONV_CONV3D_UNFOLD"):
+            case(F, oracle, 1, Ci, Co, D, 20, 18, n, kd, 1, sd, pi, torch.bfloat16, "NDHWC", 300 + k)
 
 
 def test_conv3d_autograd_and_errors(F, oracle):

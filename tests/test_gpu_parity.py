@@ -194,7 +194,8 @@ def test_pool_bf16_nhwc_vectorised(F, oracle, mode):
 
 
 @pytest.mark.parametrize("pi", [0, 1])
-def test_maxpool_tma_band_kernel(F, oracle, pi, monkeypatch):
+def test_maxpool_tma_band_kernel(F, oracle, pi):
+    from paper_1903_01814_b200 import _abi as A
     # bf16 NHWC, C % 64 == 0, n = 1, s = 2: the TMA-staged band kernel (pool_tma.cu); bit-exact values
     # and argmax vs the oracle, and identical to the stencil kernel (HEXCONV_NO_POOL_TMA=1)
     for k, (B, C, H, W) in enumerate([(3, 64, 17, 65), (2, 128, 48, 96), (1, 192, 5, 64), (2, 64, 30, 96),
@@ -206,9 +207,8 @@ def test_maxpool_tma_band_kernel(F, oracle, pi, monkeypatch):
         yref, amref = oracle.pool2d_fwd(x, n=1, s=2, pi=pi, mode="max")
         assert np.array_equal(to_np(y, "NHWC"), yref), (pi, B, C, H, W)
         assert np.array_equal(am.permute(0, 3, 1, 2).cpu().numpy(), amref), (pi, B, C, H, W)
-        monkeypatch.setenv("HEXCONV_NO_POOL_TMA", "1")
-        y2, am2 = F.pool2d_fwd(xd, n=1, stride=2, parity=pi, mode="max", layout="NHWC")
-        monkeypatch.delenv("HEXCONV_NO_POOL_TMA")
+        with A.switch("HEXCONV_NO_POOL_TMA"):
+            y2, am2 = F.pool2d_fwd(xd, n=1, stride=2, parity=pi, mode="max", layout="NHWC")
         assert torch.equal(y.view(torch.int16), y2.view(torch.int16)) and torch.equal(am, am2)
         # backward through the pool of these shapes: oracle within the bf16 bar
         g = rnd(yref.shape, 800 + k, torch.bfloat16)

@@ -151,15 +151,11 @@ def test_fused_conv_relu_maxpool(F, oracle, n, pi):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("pi", [0, 1])
-def test_fused_conv_maxpool_strips(F, oracle, pi, pair, monkeypatch):
+def test_fused_conv_maxpool_strips(F, oracle, pi):
     # batches with >= one strip per SM run the strip-walking mode (rows carried between tiles) plus the
     # region-mode tail; ragged bottom (46 rows), a last tile whose bottom window reaches row H (48 rows).
-    # pair: the CTA-pair variant (HEXCONV_FP_PAIR, M = 256 MMAs; odd region counts leave empty slots)
     import synth
-    if pair:
-        monkeypatch.setenv("HEXCONV_FP_PAIR", "1")
     for (B, Cin, Cout, H, W) in [(25, 64, 128, 46, 96), (25, 64, 64, 48, 90), (44, 128, 64, 32, 48)]:
         T = oracle.num_taps(1)
         g = torch.Generator().manual_seed(900 + H + pi)
