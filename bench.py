@@ -163,6 +163,18 @@ def oracle_train_sample(n_images: int, seed: int = 0):
     return time.perf_counter() - t0, oracle.max_threads()
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def run_reference(args, rank, world):
     """--impl reference: the fp64 oracle on the host cores (rank 0 only)."""
     if rank != 0:
@@ -184,6 +196,7 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "global_batch": 256 * args.gpus, "l2": "n/a (CPU)"},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"{n_img} image per step through the full C5 fwd+bwd+SGD in fp64 "
                                    f"(bounded sample of the 256-image batch)"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -191,143 +204,262 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-# ------------------------------------------------------------------ secondary configs (BASELINE configs 2-4)
-def _events_ms(fn, iters):
-    import torch
-    fn()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(iters):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / iters
+# ------------------------------------------------------------------ secondary configs (BASELINE configs 1-4)
+def ffma_peak():
+    """Measured FP32 FFMA peak (TFLOP/s) for the CUDA-core conv rooflines: tools/ffma_peak.bin run live when
+    it was built, else the committed profiles/r02/ffma_peak.json; the 'reg' form (three register operands,
+    a convolution's weight x activation FFMA) is the denominator."""
+    exe = os.path.join(ROOT, "tools", "ffma_peak.bin")
+    if os.path.exists(exe):
+        try:
+            out = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+            d = json.loads(out.stdout.strip().splitlines()[-1])
+            d["source"] = "measured live (tools/ffma_peak.bin)"
+            return d
+        except Exception:
+            pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "ffma_peak.json")) as f:
+            d = json.load(f)
+        d["source"] = "profiles/r02/ffma_peak.json (measured on this pool, committed)"
+        return d
+    except Exception:
+        return {"ffma_tflops_reg": 74.4, "source": "derived 148 x 128 x 2 x 1.965 GHz (no measurement)"}
+
+
+class GraphTimer:
+    """Times a sequence of library calls as CUDA-graph replays (no host dispatch inside the timed region):
+    'hot' = replays back to back (inputs L2-resident as in a steady training loop), 'flushed' = median of
+    single replays each preceded by a 256 MB L2-evicting write outside the timed events."""
+
+    def __init__(self, dev):
+        import torch
+        self.torch = torch
+        self.flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def capture(self, fn):
+        torch = self.torch
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()  # first-call work (allocations, function attributes) outside the capture
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g
+
+    def time(self, g, iters=20):
+        torch = self.torch
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        hot = e0.elapsed_time(e1) / iters
+        evs = []
+        for _ in range(iters):
+            self.flush_buf.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        flushed = statistics.median(a.elapsed_time(b) for a, b in evs)
+        return hot, flushed
+
+
+def _pass_entry(hot, flushed, flops, nbytes, ffma, hbm):
+    """One pass: times (us), achieved rates and the fraction of its roofline t_roof / t (flushed timing);
+    t_roof = max(bytes / HBM, FLOPs / FFMA) -- SURVEY.md 8(d) 'Rooflines'."""
+    e = {"us_flushed": flushed * 1e3, "us_hot": hot * 1e3}
+    t_roof = max(nbytes / (hbm * 1e9), (flops or 0.0) / (ffma * 1e12))
+    if flops:
+        e["tflops"] = flops / (flushed * 1e-3) / 1e12
+    e["gbs"] = nbytes / (flushed * 1e-3) / 1e9
+    e["roofline_us"] = t_roof * 1e6
+    e["bound"] = "ffma" if (flops or 0.0) / (ffma * 1e12) > nbytes / (hbm * 1e9) else "hbm"
+    e["frac_of_roofline"] = t_roof / (flushed * 1e-3)
+    e["frac_of_roofline_hot"] = t_roof / (hot * 1e-3)
+    return e
 
 
 def secondary_measurements(dev, peak_tf, peak_gbs):
-    """Device-timed passes of BASELINE configs 2, 3 and 4 (inputs resident; each
-    pass re-launched back to back, so L2 holds what the previous pass left: the C4
-    tensors (268 MB) exceed L2, C2/C3 fit).  Rooflines: tensor peak for C4,
-    FP32 FFMA (148 SMs x 128 lanes x 2 x 1.965 GHz = 74.4 TFLOP/s, derived) for
-    the fp32 convs, HBM for the pools; 'valid taps' FLOPs (in-grid taps only)."""
+    """BASELINE configs 1-4 (and the f2 conv3d shape), each pass captured in a CUDA graph and timed hot and
+    L2-flushed (GraphTimer).  Rooflines: FP32 FFMA (measured, ffma_peak()) for the fp32 convs, HBM for pools
+    and the Cin = 1 layer, the measured bf16 burst peak for the tensor-core convs; FLOPs count in-grid taps
+    only ('valid taps'); bytes = inputs + weights + outputs moved once."""
     import numpy as np
     import torch
 
     import synth
     from paper_1903_01814_b200 import functional as F
-    ffma = 74.4
-    out = {}
+    fp = ffma_peak()
+    ffma = fp["ffma_tflops_reg"]
+    gt = GraphTimer(dev)
+    out = {"ffma_peak": fp}
 
     def vt(H, W, n, s=1):
         return int((F.gather_map(H, W, n, stride=s) >= 0).sum().item())
 
-    # ---- C4: 128 x 256->256, 64x64, bf16, n = 1 and 2: fwd / dgrad / wgrad
-    B, C, H, W = 128, 256, 64, 64
-    x = torch.randn(B, H, W, C, device=dev).to(torch.bfloat16)
-    g = torch.randn(B, H, W, C, device=dev).to(torch.bfloat16)
-    c4 = {}
-    for n in (1, 2):
-        T = F.num_taps(n)
-        w = (torch.randn(C, C, T, device=dev) / (C * T) ** 0.5).to(torch.bfloat16)
-        fl = 2.0 * B * vt(H, W, n) * C * C
-        for name, fn in (("fwd", lambda: F.conv2d_fwd(x, w, None, n=n, layout="NHWC")),
-                         ("dgrad", lambda: F.conv2d_bwd_data(g, w, (H, W), n=n, layout="NHWC")),
-                         ("wgrad", lambda: F.conv2d_bwd_weight(x, g, n=n, layout="NHWC"))):
-            ms = _events_ms(fn, 5)
-            tf = fl / (ms / 1e3) / 1e12
-            c4[f"n{n}_{name}"] = {"us": ms * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak_tf}
-    out["c4_256x256_64x64_bf16"] = c4
-    del x, g
+    # ---- C1: 4 x 1 -> 4, 16 x 16, n = 1, fp32 (BASELINE configs[0]): latency
+    c = synth.CONFIGS["c1"]
+    x1 = torch.from_numpy(synth.normal((4, 1, 16, 16), 0).astype(np.float32)).to(dev)
+    w1 = torch.from_numpy((synth.normal((4, 1, 7), 1) * 0.1).astype(np.float32)).to(dev)
+    b1 = torch.zeros(4, device=dev)
+    y1 = torch.empty(4, 4, 16, 16, device=dev)
+    g = gt.capture(lambda: F.conv2d_fwd(x1, w1, b1, n=1, out=y1))
+    hot, fl = gt.time(g, 50)
+    lat = []
+    for _ in range(200):
+        t0 = time.perf_counter()
+        F.conv2d_fwd(x1, w1, b1, n=1, out=y1)
+        torch.cuda.synchronize()
+        lat.append(time.perf_counter() - t0)
+    out["c1_4x1to4_16x16_f32"] = {
+        "device_us_hot": hot * 1e3, "device_us_flushed": fl * 1e3,
+        "host_call_to_sync_us_median": statistics.median(lat) * 1e6,
+        "note": "launch-latency bound (20 KB, 53 kFLOP); device time = CUDA events around one graph replay of "
+                "the single kernel; host latency = one eager ABI call + cudaDeviceSynchronize"}
 
-    # ---- C3: 256 camera images 40x40, fp32 4-layer net, forward + backward
+    # ---- C2: 32 x 16 -> 32, 48 x 48, n2 s2 conv + max pool n1 s2, fp32, fwd + bwd
+    B, Ci, Co, H, W = 32, 16, 32, 48, 48
+    x = torch.from_numpy(synth.normal((B, Ci, H, W), 0).astype(np.float32)).to(dev)
+    w = torch.from_numpy(synth.kaiming_uniform((Co, Ci, 19), 1).astype(np.float32)).to(dev)
+    Ho, Wo, _ = F.output_shape(H, W, 2)
+    y = torch.empty(B, Co, Ho, Wo, device=dev)
+    F.conv2d_fwd(x, w, None, n=2, stride=2, out=y)
+    gy = torch.from_numpy(synth.normal((B, Co, Ho, Wo), 2).astype(np.float32)).to(dev)
+    pyv, am = F.pool2d_fwd(y, n=1, stride=2, mode="max")
+    gp = torch.randn_like(pyv)
+    dx = torch.empty_like(x)
+    dw = torch.empty(Co, Ci, 19, device=dev)
+    db = torch.empty(Co, device=dev)
+    dyp = torch.empty_like(y)
+    fl_c2 = 2.0 * B * vt(H, W, 2, 2) * Ci * Co
+    xb, yb, wb = x.numel() * 4, y.numel() * 4, w.numel() * 4
+    pb_in, pb_out = y.numel() * 4, pyv.numel() * 4
+    c2 = {}
+    for name, fn, f, nb in (
+            ("conv_fwd", lambda: F.conv2d_fwd(x, w, None, n=2, stride=2, out=y), fl_c2, xb + wb + yb),
+            ("conv_dgrad", lambda: F.conv2d_bwd_data(gy, w, (H, W), n=2, stride=2, out=dx), fl_c2, yb + wb + xb),
+            ("conv_wgrad", lambda: F.conv2d_bwd_weight(x, gy, n=2, stride=2, dw=dw, dbias=db), fl_c2, xb + yb + wb),
+            ("pool_fwd", lambda: F.pool2d_fwd(y, n=1, stride=2, mode="max"), None, pb_in + pb_out + pyv.numel()),
+            ("pool_bwd", lambda: F.pool2d_bwd(gp, am, (Ho, Wo), n=1, stride=2, mode="max", out=dyp), None,
+             pb_out + pyv.numel() + pb_in)):
+        hot, fl = gt.time(gt.capture(fn))
+        c2[name] = _pass_entry(hot, fl, f, nb, ffma, peak_gbs)
+    out["c2_16to32_48x48_f32"] = c2
+
+    # ---- C3: 256 camera images 40 x 40, fp32 4-layer net (conv 1->16 n1, conv 16->32 n2, avg pool n1 s2,
+    # conv 32->64 n1, ReLU), forward + backward, every elementwise step in library kernels
     c = synth.CONFIGS["c3"]
     B, H, W = c["B"], c["H"], c["W"]
+    H2, W2, _ = F.output_shape(H, W, 2)
     x = torch.from_numpy(synth.shower_images(B, H, W, c["R"], 3).astype(np.float32)).to(dev)
     convs = [(1, 16, 1), (16, 32, 2), (32, 64, 1)]
     ws = [torch.from_numpy(synth.kaiming_uniform((co, ci, F.num_taps(n)), 20 + i).astype(np.float32)).to(dev)
           for i, (ci, co, n) in enumerate(convs)]
     bs = [torch.zeros(co, device=dev) for _, co, _ in convs]
-    g4 = torch.randn(B, 64, H // 2, W // 2, device=dev)
-    t = {}
+    t = {k: torch.empty(shape, device=dev) for k, shape in (
+        ("y1", (B, 16, H, W)), ("y2", (B, 32, H, W)), ("p", (B, 32, H2, W2)), ("y4", (B, 64, H2, W2)),
+        ("dy4", (B, 64, H2, W2)), ("dp", (B, 32, H2, W2)), ("dy2u", (B, 32, H, W)), ("dy2", (B, 32, H, W)),
+        ("dy1", (B, 16, H, W)))}
+    g4 = torch.from_numpy(synth.normal((B, 64, H2, W2), 4).astype(np.float32)).to(dev)
+    dws = [(torch.empty(co, ci, F.num_taps(n), device=dev), torch.empty(co, device=dev)) for ci, co, n in convs]
 
-    def c3_pass():
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(12)]
-        ev[0].record()
-        y1 = F.conv2d_fwd(x, ws[0], bs[0], n=1, relu=True); ev[1].record()
-        y2 = F.conv2d_fwd(y1, ws[1], bs[1], n=2, relu=True); ev[2].record()
-        p, _ = F.pool2d_fwd(y2, n=1, stride=2, mode="avg"); ev[3].record()
-        y4 = F.conv2d_fwd(p, ws[2], bs[2], n=1, relu=True); ev[4].record()
-        dy4 = g4 * (y4 > 0)
-        ev[5].record()
-        F.conv2d_bwd_weight(p, dy4, n=1)
-        dp = F.conv2d_bwd_data(dy4, ws[2], (H // 2, W // 2), n=1); ev[6].record()
-        dy2 = F.pool2d_bwd(dp, None, (H, W), n=1, stride=2, mode="avg"); ev[7].record()
-        dy2 = dy2 * (y2 > 0)
-        ev[8].record()
-        F.conv2d_bwd_weight(y1, dy2, n=2)
-        dy1 = F.conv2d_bwd_data(dy2, ws[1], (H, W), n=2, relu_y=y1); ev[9].record()
-        F.conv2d_bwd_weight(x, dy1, n=1); ev[10].record()
-        return ev
+    def relu_bwd(dyv, yv, outv):
+        from paper_1903_01814_b200 import _abi as A_
+        A_.check(A_.lib().hex_relu_bwd(dyv.numel(), A_.F32, F._ptr(dyv), F._ptr(yv), F._ptr(outv), F._stream()),
+                 "relu_bwd")
 
-    c3_pass()
-    torch.cuda.synchronize()
-    tot, parts = [], {}
-    names = [(0, 1, "L1 fwd"), (1, 2, "L2 fwd"), (2, 3, "pool fwd"), (3, 4, "L4 fwd"), (5, 6, "L4 wgrad+dgrad"),
-             (6, 7, "pool bwd"), (8, 9, "L2 wgrad+dgrad"), (9, 10, "L1 wgrad")]
-    for _ in range(5):
-        ev = c3_pass()
-        torch.cuda.synchronize()
-        for a, b, nm in names:
-            parts[nm] = parts.get(nm, 0.0) + ev[a].elapsed_time(ev[b]) / 5
-        tot.append(sum(ev[a].elapsed_time(ev[b]) for a, b, _ in names))
-    ms = float(np.median(tot))
-    vt1, vt2, vt4 = vt(H, W, 1), vt(H, W, 2), vt(H // 2, W // 2, 1)
-    fl = 2.0 * B * (vt1 * 16 * 2 + vt2 * 16 * 32 * 3 + vt4 * 32 * 64 * 3)
+    passes = [
+        ("L1 fwd", lambda: F.conv2d_fwd(x, ws[0], bs[0], n=1, relu=True, out=t["y1"])),
+        ("L2 fwd", lambda: F.conv2d_fwd(t["y1"], ws[1], bs[1], n=2, relu=True, out=t["y2"])),
+        ("pool fwd", lambda: F.pool2d_fwd(t["y2"], n=1, stride=2, mode="avg", out=t["p"])),
+        ("L4 fwd", lambda: F.conv2d_fwd(t["p"], ws[2], bs[2], n=1, relu=True, out=t["y4"])),
+        ("L4 relu bwd", lambda: relu_bwd(g4, t["y4"], t["dy4"])),
+        ("L4 wgrad", lambda: F.conv2d_bwd_weight(t["p"], t["dy4"], n=1, dw=dws[2][0], dbias=dws[2][1])),
+        ("L4 dgrad", lambda: F.conv2d_bwd_data(t["dy4"], ws[2], (H2, W2), n=1, out=t["dp"])),
+        ("pool bwd", lambda: F.pool2d_bwd(t["dp"], None, (H, W), n=1, stride=2, mode="avg", out=t["dy2u"])),
+        ("L2 relu bwd", lambda: relu_bwd(t["dy2u"], t["y2"], t["dy2"])),
+        ("L2 wgrad", lambda: F.conv2d_bwd_weight(t["y1"], t["dy2"], n=2, dw=dws[1][0], dbias=dws[1][1])),
+        ("L2 dgrad", lambda: F.conv2d_bwd_data(t["dy2"], ws[1], (H, W), n=2, relu_y=t["y1"], out=t["dy1"])),
+        ("L1 wgrad", lambda: F.conv2d_bwd_weight(x, t["dy1"], n=1, dw=dws[0][0], dbias=dws[0][1])),
+    ]
+    vt1, vt2, vt4 = vt(H, W, 1), vt(H, W, 2), vt(H2, W2, 1)
+    px, px2 = B * H * W, B * H2 * W2
+    acct = {  # (FLOPs, bytes) per pass
+        "L1 fwd": (2.0 * B * vt1 * 16, px * 4 * (1 + 16)),
+        "L2 fwd": (2.0 * B * vt2 * 16 * 32, px * 4 * (16 + 32)),
+        "pool fwd": (None, px * 32 * 4 + px2 * 32 * 4),
+        "L4 fwd": (2.0 * B * vt4 * 32 * 64, px2 * 4 * (32 + 64)),
+        "L4 relu bwd": (None, px2 * 64 * 4 * 3),
+        "L4 wgrad": (2.0 * B * vt4 * 32 * 64, px2 * 4 * (32 + 64)),
+        "L4 dgrad": (2.0 * B * vt4 * 32 * 64, px2 * 4 * (32 + 64)),
+        "pool bwd": (None, px2 * 32 * 4 + px * 32 * 4),
+        "L2 relu bwd": (None, px * 32 * 4 * 3),
+        "L2 wgrad": (2.0 * B * vt2 * 16 * 32, px * 4 * (16 + 32)),
+        "L2 dgrad": (2.0 * B * vt2 * 16 * 32, px * 4 * (32 + 16 + 16)),
+        "L1 wgrad": (2.0 * B * vt1 * 16, px * 4 * (1 + 16)),
+    }
+    c3p = {}
+    for name, fn in passes:
+        hot, fl = gt.time(gt.capture(fn))
+        c3p[name] = _pass_entry(hot, fl, acct[name][0], acct[name][1], ffma, peak_gbs)
+    step = gt.capture(lambda: [fn() for _, fn in passes])
+    hot, fl = gt.time(step)
+    fl_all = sum(v[0] or 0.0 for v in acct.values())
+    t_roof = sum(max(b_ / (peak_gbs * 1e9), (f_ or 0.0) / (ffma * 1e12)) for f_, b_ in acct.values())
     out["c3_camera_40x40_f32"] = {
-        "images_per_s": B / (ms / 1e3), "ms_per_fwd_bwd": ms, "tflops": fl / (ms / 1e3) / 1e12,
-        "frac_of_ffma_peak": fl / (ms / 1e3) / 1e12 / ffma,
-        "ms_by_step": parts, "note": "elementwise ReLU-mask products between layers (torch) are not timed"}
-    del x
+        "images_per_s": B / (fl * 1e-3), "images_per_s_hot": B / (hot * 1e-3),
+        "ms_per_fwd_bwd_flushed": fl, "ms_per_fwd_bwd_hot": hot, "tflops": fl_all / (fl * 1e-3) / 1e12,
+        "roofline_ms": t_roof * 1e3, "frac_of_roofline": t_roof / (fl * 1e-3), "frac_of_roofline_hot": t_roof / (hot * 1e-3),
+        "passes": c3p,
+        "note": "whole fwd+bwd = one CUDA graph of the 12 library calls; per-pass entries are each pass's own graph "
+                "(flushed = L2 evicted before the pass, hot = back-to-back replays)"}
 
-    # ---- C2: 32 x 16->32, 48x48, n2 s2 conv + max pool n1 s2, fp32, fwd + bwd
-    B, Ci, Co, H, W = 32, 16, 32, 48, 48
-    x = torch.randn(B, Ci, H, W, device=dev)
-    w = torch.from_numpy(synth.kaiming_uniform((Co, Ci, 19), 1).astype(np.float32)).to(dev)
-    y = F.conv2d_fwd(x, w, None, n=2, stride=2)
-    gy = torch.randn_like(y)
-    pyv, am = F.pool2d_fwd(y, n=1, stride=2, mode="max")
-    gp = torch.randn_like(pyv)
-    c2 = {}
-    fl = 2.0 * B * vt(H, W, 2, 2) * Ci * Co
-    for name, fn, f in (("conv_fwd", lambda: F.conv2d_fwd(x, w, None, n=2, stride=2), fl),
-                        ("conv_dgrad", lambda: F.conv2d_bwd_data(gy, w, (H, W), n=2, stride=2), fl),
-                        ("conv_wgrad", lambda: F.conv2d_bwd_weight(x, gy, n=2, stride=2), fl),
-                        ("pool_fwd", lambda: F.pool2d_fwd(y, n=1, stride=2, mode="max"), None),
-                        ("pool_bwd", lambda: F.pool2d_bwd(gp, am, y.shape[-2:], n=1, stride=2, mode="max"), None)):
-        ms = _events_ms(fn, 20)
-        c2[name] = {"us": ms * 1e3}
-        if f:
-            c2[name]["tflops"] = f / (ms / 1e3) / 1e12
-    out["c2_16to32_48x48_f32"] = c2
-    del x, y, gy
+    # ---- C4: 128 x 256 -> 256, 64 x 64, bf16, n = 1 and 2: fwd / dgrad / wgrad (268 MB tensors > L2)
+    B, C, H, W = 128, 256, 64, 64
+    x = torch.randn(B, H, W, C, device=dev).to(torch.bfloat16)
+    gq = torch.randn(B, H, W, C, device=dev).to(torch.bfloat16)
+    yq = torch.empty_like(x)
+    dxq = torch.empty_like(x)
+    c4 = {}
+    for n in (1, 2):
+        T = F.num_taps(n)
+        w = (torch.randn(C, C, T, device=dev) / (C * T) ** 0.5).to(torch.bfloat16)
+        dwq, dbq = torch.empty(C, C, T, device=dev), torch.empty(C, device=dev)
+        fl4 = 2.0 * B * vt(H, W, n) * C * C
+        for name, fn in (("fwd", lambda: F.conv2d_fwd(x, w, None, n=n, layout="NHWC", out=yq)),
+                         ("dgrad", lambda: F.conv2d_bwd_data(gq, w, (H, W), n=n, layout="NHWC", out=dxq)),
+                         ("wgrad", lambda: F.conv2d_bwd_weight(x, gq, n=n, layout="NHWC", dw=dwq, dbias=dbq))):
+            hot, fl = gt.time(gt.capture(fn), 10)
+            tf = fl4 / (fl * 1e-3) / 1e12
+            c4[f"n{n}_{name}"] = {"us_flushed": fl * 1e3, "us_hot": hot * 1e3, "tflops": tf,
+                                  "frac_of_bf16_peak": tf / peak_tf}
+    out["c4_256x256_64x64_bf16"] = c4
+    del x, gq, yq, dxq
 
-    # ---- f2: 3-D hex conv (hex x-y, equidistant z; PAPER.md:197-199), bf16 NDHWC, tcgen05 via depth unfold.
+    # ---- f2: 3-D hex conv (hex x-y, equidistant z; PAPER.md:197-199), bf16 NDHWC.
     # Synthetic shape (no paper workload): 16 volumes x 16 slices x 64x64, 64 -> 128 channels, n = 1, kd = 3.
     B, D, H, W, C, Co, kd, n = 16, 16, 64, 64, 64, 128, 3, 1
     T = F.num_taps(n)
     x = torch.randn(B, D, H, W, C, device=dev).to(torch.bfloat16)
-    g = torch.randn(B, D, H, W, Co, device=dev).to(torch.bfloat16)
+    g3 = torch.randn(B, D, H, W, Co, device=dev).to(torch.bfloat16)
     w = (torch.randn(Co, C, kd, T, device=dev) / (C * kd * T) ** 0.5).to(torch.bfloat16)
-    # valid work: in-grid taps x in-range depth taps (kd*D - 2 boundary slices for kd = 3, sd = 1)
-    fl = 2.0 * B * vt(H, W, n) * (kd * D - 2) * C * Co
+    fl3 = 2.0 * B * vt(H, W, n) * (kd * D - 2) * C * Co
     c3d = {}
     for name, fn in (("fwd", lambda: F.conv3d_fwd(x, w, None, n=n, layout="NDHWC")),
-                     ("dgrad", lambda: F.conv3d_bwd_data(g, w, (D, H, W), n=n, layout="NDHWC")),
-                     ("wgrad", lambda: F.conv3d_bwd_weight(x, g, kd, n=n, layout="NDHWC"))):
-        ms = _events_ms(fn, 5)
-        tf = fl / (ms / 1e3) / 1e12
-        c3d[name] = {"us": ms * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak_tf}
+                     ("dgrad", lambda: F.conv3d_bwd_data(g3, w, (D, H, W), n=n, layout="NDHWC")),
+                     ("wgrad", lambda: F.conv3d_bwd_weight(x, g3, kd, n=n, layout="NDHWC"))):
+        hot, fl = gt.time(gt.capture(fn), 10)
+        tf = fl3 / (fl * 1e-3) / 1e12
+        c3d[name] = {"us_flushed": fl * 1e3, "us_hot": hot * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak_tf}
     c3d["note"] = ("fwd / dgrad: depth taps inside the K loop of the tcgen05 tap-reuse kernel (out-of-volume "
                    "slices are zero-fill boxes); wgrad: depth taps unfolded into channels then one 2-D tcgen05 "
                    "wgrad over B*D images; FLOPs count in-range depth taps only")
@@ -361,6 +493,8 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the config 2-4 measurements")
+    ap.add_argument("--sustain-s", type=float, default=2.5,
+                    help="seconds of back-to-back steps for the sustained (power-capped) rate; 0 = skip")
     ap.add_argument("--launch-check", action="store_true",
                     help="print each rank's (rank, world) and exit before touching a GPU (launcher test)")
     ap.add_argument("--no-graph", action="store_true", help="device-timed and e2e legs as eager steps (no CUDA graph)")
@@ -469,6 +603,34 @@ def main():
     ms = max_over_ranks(ms)
     ms_step = ms / args.steps
     value = world * B * args.steps / (ms / 1e3)
+
+    # ---- sustained rate: the same replayed step looped for >= --sustain-s seconds (power-capped steady
+    # state), reported beside the K-step value against the driver's sustained bf16 figure
+    sustained = None
+    if args.sustain_s > 0:
+        n_s = max(1, int(args.sustain_s / (ms_step / 1e3)))
+        sclk = ClockSampler(local)
+        sclk.start()
+        barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for i in range(n_s):
+            if graph_v is not None:
+                xg.copy_(xs[i % NB], non_blocking=True)
+                yg.copy_(ys[i % NB], non_blocking=True)
+                graph_v.replay()
+            else:
+                model.step(xs[i % NB], ys[i % NB])
+        s1.record()
+        torch.cuda.synchronize()
+        barrier()
+        sc = sclk.stop()
+        s_ms = max_over_ranks(s0.elapsed_time(s1))
+        flops_img_, _ = model.flops_per_image()
+        sustained = {"images_per_s": world * B * n_s / (s_ms / 1e3), "steps": n_s, "seconds": s_ms / 1e3,
+                     "ms_per_step": s_ms / n_s,
+                     "step_tflops_per_gpu": flops_img_ * B * n_s / (s_ms / 1e3) / 1e12, "clocks": sc}
 
     # ---- per kernel family: CUDA events recorded around every conv / pool call (on the stream it is
     # launched on) over K eager steps of the same workload; launches counted by the library
@@ -617,10 +779,15 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
+        threads_all = oracle.max_threads()
         dt, threads = oracle_train_sample(1)
+        oracle.set_threads(1)
+        dt1, _ = oracle_train_sample(1)
+        oracle.set_threads(threads_all)
         cpu = {"value": 1.0 / dt, "unit": "images/s", "cores": threads, "kind": "oracle",
+               "single_thread_value": 1.0 / dt1, "cpu_model": cpu_model(),
                "sample": "1 image through the full C5 fwd+bwd+SGD step in fp64 (bounded sample of the "
-                         "256-image batch)"}
+                         "256-image batch), all host cores and one thread"}
 
     if rank == 0:
         line = {
@@ -628,7 +795,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": WORKLOAD, "global_batch": B * world, "per_gpu_batch": B, "grid": "96x96",
-                       "parallelism": f"dp{world}", "l2": "working set > L2 (activations ~2.5 GB/step)"},
+                       "parallelism": f"dp{world}", "l2": "working set > L2 (activations ~2.5 GB/step)",
+                       "cuda_graph": graph_v is not None},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
                     "loss": loss_info,
                     "cuda_graph": graph is not None},
@@ -644,6 +812,9 @@ def main():
                          "dominant_by_time": dom == tc_name},
             "kernels": kernels,
             "step_tflops": total_tf,
+            "sustained": dict(sustained, bf16_tflops_sustained_peak=peaks.get("bf16_tflops_sustained"),
+                              frac_of_sustained_peak=sustained["step_tflops_per_gpu"] / peaks["bf16_tflops_sustained"]
+                              if peaks.get("bf16_tflops_sustained") else None) if sustained else None,
             "step_share_ms": {k: v / args.steps for k, v in share.items()},
             "secondary_configs": secondary,
             "cpu_baseline": cpu,

@@ -267,6 +267,11 @@ def max_threads() -> int:
     return int(lib().oracle_max_threads())
 
 
+def set_threads(n: int) -> None:
+    """OpenMP thread count of the oracle's loops (bench.py times it on all cores and on one)."""
+    lib().oracle_set_threads(int(n))
+
+
 def _storage(a):
     """(contiguous array, fmt) for float32 arrays or bf16 bit patterns (uint16)."""
     a = np.ascontiguousarray(a)

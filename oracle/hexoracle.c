@@ -522,6 +522,16 @@ int oracle_conv3d_bwd(int B, int Ci, int Co, int D, int H, int W, int n, int kd,
     return 0;
 }
 
+/* Thread count of the OpenMP loops (timing the oracle single-threaded for bench.py's cpu_baseline). */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (n >= 1) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     extern int omp_get_max_threads(void);
