@@ -150,8 +150,12 @@ HEX_API hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* desc, in
  *      bwd_weight Cin % 64 == 0, Cout % 128 == 0 (s > 1 via the scattered dy).
  *  - Cin == 1, bf16 NHWC, Cout % 64 == 0, n <= 2: warp-level mma.sync
  *    stencil kernels (s = 1) or FFMA stencils (s > 1).
- *  - everything else (fp32, NCHW, small or odd channel counts, any n <= 7,
- *    any stride): CUDA-core FFMA kernels, exact fp32 products (no TF32). */
+ *  - fp32 NCHW, n <= 3, gathered channels >= 8 (fwd: Cin, bwd_data: Cout),
+ *    output channels <= 64 (fwd: Cout, bwd_data: Cin), any stride: tcgen05
+ *    in 3xTF32 (x = hi + lo, hi = tf32(x); D += hi.hi + hi.lo + lo.hi; ~fp32
+ *    accuracy, A13), the hexagonal gather built in tensor memory.
+ *  - everything else (small or odd channel counts, NHWC fp32, n <= 7, any
+ *    stride): CUDA-core FFMA kernels, exact fp32 products. */
 HEX_API hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* desc, const void* x, const void* w,
                             const float* bias, int32_t fuse_relu, void* y,
                             void* ws, size_t ws_bytes, hex_stream_t stream);
@@ -192,8 +196,8 @@ HEX_API hex_status_t hex_conv2d_fwd_maxpool(const hex_conv2d_desc_t* desc, const
                                             hex_stream_t stream);
 
 /* Which kernel family a call with this descriptor runs: *algo (host) = 0 for
- * the CUDA-core stencil path, 1 for the tcgen05 tensor-core path.
- * pass: 0 fwd, 1 bwd_data, 2 bwd_weight. */
+ * the CUDA-core stencil path, 1 for the bf16 tcgen05 tensor-core path, 2 for
+ * the fp32 3xTF32 tcgen05 path.  pass: 0 fwd, 1 bwd_data, 2 bwd_weight. */
 HEX_API hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* desc, int32_t pass, int32_t* algo);
 
 /* ---------------------------------------------------------------- 3-D convolution */

@@ -54,6 +54,7 @@ SwitchEntry g_switches[] = {
     {"HEXCONV_NO_POOL_TMA", false, ""},
     {"HEXCONV_NO_TC_STRIDE2", false, ""},
     {"HEXCONV_NO_TC_STRIDED_BWD", false, ""},
+    {"HEXCONV_NO_TF32", false, ""},
     {"HEXCONV_NO_TILED", false, ""},
     {"HEXCONV_NO_WG_TR", false, ""},
     {"HEXCONV_POOL_BWD_V2", false, ""},
@@ -143,6 +144,12 @@ bool use_f32wg(const hex_conv2d_desc_t* d, const Geom& g) {
 }
 bool use_c1(const hex_conv2d_desc_t* d, const Geom& g) {
     return c1_conv_supported(g, d->in_channels, d->out_channels, d->dtype, d->layout);
+}
+bool use_tf32_fwd(const hex_conv2d_desc_t* d, const Geom& g) {
+    return tf32_conv_supported(g, d->in_channels, d->out_channels, d->dtype, d->layout);
+}
+bool use_tf32_bwd_data(const hex_conv2d_desc_t* d, const Geom& g) {
+    return tf32_conv_supported(g, d->out_channels, d->in_channels, d->dtype, d->layout);
 }
 bool use_tc_wgrad(const hex_conv2d_desc_t* d, const Geom& g) {
     return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_wgrad_supported(g, d->in_channels, d->out_channels);
@@ -277,10 +284,15 @@ hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* d, int32_t pass,
     hex_status_t st = conv_geom(d, &g);
     if (st != HEX_OK) return st;
     switch (pass) {
-        case 0: *bytes = use_tc_fwd(d, g) ? packed_weight_bytes(d, g) : 0; return HEX_OK;
+        case 0:
+            *bytes = use_tc_fwd(d, g)     ? packed_weight_bytes(d, g)
+                     : use_tf32_fwd(d, g) ? tf32_conv_ws_bytes(g, d->in_channels, d->out_channels)
+                                          : 0;
+            return HEX_OK;
         case 1:
             *bytes = use_tc_bwd_data(d, g)      ? packed_weight_bytes(d, g)
                      : use_tc_bwd_data_up(d, g) ? up_bytes(d, g) + packed_weight_bytes(d, g)
+                     : use_tf32_bwd_data(d, g)  ? tf32_conv_ws_bytes(g, d->out_channels, d->in_channels)
                                                 : 0;
             return HEX_OK;
         case 2:
@@ -302,8 +314,10 @@ hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* d, int32_t pass, int32_t* 
     hex_status_t st = conv_geom(d, &g);
     if (st != HEX_OK) return st;
     switch (pass) {
-        case 0: *algo = use_tc_fwd(d, g) ? 1 : 0; return HEX_OK;
-        case 1: *algo = use_tc_bwd_data(d, g) || use_tc_bwd_data_up(d, g) ? 1 : 0; return HEX_OK;
+        case 0: *algo = use_tc_fwd(d, g) ? 1 : use_tf32_fwd(d, g) ? 2 : 0; return HEX_OK;
+        case 1:
+            *algo = use_tc_bwd_data(d, g) || use_tc_bwd_data_up(d, g) ? 1 : use_tf32_bwd_data(d, g) ? 2 : 0;
+            return HEX_OK;
         case 2: *algo = use_tc_wgrad(d, g) || use_tc_wgrad_up(d, g) ? 1 : 0; return HEX_OK;
         default: return HEX_ERR_INVALID_ARG;
     }
@@ -332,6 +346,9 @@ hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* d, const void* x, const voi
         if (((uintptr_t)y & 3) != 0) return HEX_ERR_ALIGNMENT;
         return smallc_fwd(x, w, bias, y, g, d->out_channels, fuse_relu, s);
     }
+    if (use_tf32_fwd(d, g))
+        return tf32_conv(g, d->in_channels, d->out_channels, 0, (const float*)x, (const float*)w, bias, nullptr,
+                         fuse_relu, (float*)y, ws, ws_bytes, s);
     if (use_c1(d, g)) return c1_conv_fwd((const float*)x, (const float*)w, bias, (float*)y, g, d->out_channels,
                                          fuse_relu, s);
     if (tiled_supported(g, d->dtype, d->layout))
@@ -406,6 +423,9 @@ hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* d, const void* dy, con
         a.x = up; a.wpack = wp; a.bias = nullptr; a.y = dx; a.relu_y = relu_y; a.relu = 0;
         return tc_conv_fwd(a, s);
     }
+    if (use_tf32_bwd_data(d, g))
+        return tf32_conv(g, d->in_channels, d->out_channels, 1, (const float*)dy, (const float*)w, nullptr,
+                         (const float*)relu_y, 0, (float*)dx, ws, ws_bytes, s);
     if (tiled_supported(g, d->dtype, d->layout))
         return tiled_conv((const float*)dy, (const float*)w, nullptr, (const float*)relu_y, (float*)dx, g,
                           d->out_channels, d->in_channels, 0, 1, s);

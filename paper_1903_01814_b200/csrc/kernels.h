@@ -127,4 +127,12 @@ bool tiled_supported(const Geom& g, int dtype, int layout);
 hex_status_t tiled_conv(const float* x, const float* w, const float* bias, const float* relu_y, float* y,
                         const Geom& g, int Cin, int Cout, int relu, int transpose, cudaStream_t st);
 
+// fp32 NCHW convolution on the tcgen05 tensor cores in 3xTF32 (tf32_conv.cu).  Cx = channels of the
+// gathered tensor (fwd: Cin, bwd-data: Cout), Nout = output channels (fwd: Cout, bwd-data: Cin).
+bool tf32_conv_supported(const Geom& g, int Cx, int Nout, int dtype, int layout);
+size_t tf32_conv_ws_bytes(const Geom& g, int Cx, int Nout);
+hex_status_t tf32_conv(const Geom& g, int Cin, int Cout, int mode, const float* in, const float* w,
+                       const float* bias, const float* relu_y, int relu, float* out, void* ws, size_t ws_bytes,
+                       cudaStream_t st);
+
 }  // namespace hexconv

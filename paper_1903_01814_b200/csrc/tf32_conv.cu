@@ -1,0 +1,418 @@
+// tf32_conv.cu -- fp32 hexagonal convolution on the tcgen05 tensor cores in 3xTF32.
+//
+// The fp32 layers of configs 2 and 3 (16 -> 32, 32 -> 64 channels) are dense contractions too small for the
+// 64-channel bf16 tiles, and on CUDA cores they are FFMA-bound (arithmetic intensity 50-100 FLOP/B).
+// Here each one is an implicit GEMM on the tensor cores with fp32 accuracy:
+//
+//   * M = 128 output pixels (consecutive in the flattened (b, R, C) order of the output grid, so a tile may
+//     span images and no pixel of a ragged image is wasted), N = output channels (padded to 16, <= 64),
+//     K = (tap, 8-channel chunk) -- (tap, ci) packed into K, so 16 input channels x 19 taps is K = 304
+//     with no 64-channel padding.
+//   * 3xTF32 split (reading A13): every operand value v = hi + lo with hi = cvt.rna.tf32(v) and
+//     lo = v - hi (exact in fp32); D += A_hi.B_hi + A_hi.B_lo + A_lo.B_hi.  The dropped A_lo.B_lo term and
+//     the tf32 rounding of lo are ~2^-22 of |a.b|: normwise error ~5e-7 against fp64 (tools/tf32_probe.cu),
+//     inside the fp32 bar of 1e-5 (A14).
+//   * A (the hexagonal gather) is built directly in TENSOR MEMORY: builder warps -- one thread per output
+//     pixel, i.e. per TMEM lane -- gather the 8 channels of one tap for their pixel (offset-column geometry,
+//     PAPER.md:144-151; off-grid neighbours read 0, A4), split them and write hi / lo with tcgen05.st; the
+//     MMA reads A from TMEM ([a_tmem] operand), so the gather costs no shared-memory bandwidth.
+//   * B (weights, pre-split hi / lo, K-major SWIZZLE_32B: one 32-byte row = the 8 K values of one output
+//     channel) is resident in shared memory for the whole persistent kernel (one bulk copy).
+//   * Warp roles: 4 epilogue warps (TMEM -> registers -> bias / ReLU / ReLU-backward mask -> NCHW stores,
+//     coalesced across the 32 pixels of a warp), 16 builder warps in 4 groups taking K-steps round-robin
+//     (a group has 4 K-steps of MMA time to hide its global-load latency), 1 MMA-issuing warp.  A ring of
+//     8 TMEM A stages (16 columns each: hi, lo) and two accumulators (the epilogue of tile i overlaps the
+//     MMAs of tile i+1).
+//
+// Modes (one kernel):
+//   forward       output pixel (R, C) of the stride-s lattice has its centre at (rho(C) + sR, sC)
+//                 (PAPER.md:152-154, 172-175); taps read x on the full grid.
+//   bwd-data      the adjoint: dx = forward of dy with reversed taps and transposed channels (pin P18) on the
+//                 full grid; for s > 1 dy is read through the lattice -- a neighbour that is not a lattice
+//                 centre contributes 0 (the stride-1 adjoint of dy scattered onto the full grid, P10) -- so
+//                 no upsampled copy of dy is written.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "geometry.cuh"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace hexconv {
+namespace {
+
+constexpr int TF_STAGES = 8;
+constexpr int TF_GROUPS = 4;                       // builder groups (K-steps round-robin)
+constexpr int TF_EPI_WARPS = 4;
+constexpr int TF_BLD_WARPS = 4 * TF_GROUPS;
+constexpr int TF_MMA_WARP = TF_EPI_WARPS + TF_BLD_WARPS;
+constexpr int TF_THREADS = (TF_MMA_WARP + 1) * 32;
+constexpr int TF_MAXT = 37;                        // n <= 3
+constexpr int TF_MAX_NT = 64;
+constexpr int TF_SMEM_MAX = 220 * 1024;
+
+struct TfParams {
+    const float* x;       // gathered tensor, NCHW [B][Cx][Hin][Win]
+    const float* bias;    // [Nout] or null
+    const float* relu_y;  // mask source shaped like y, or null
+    float* y;             // output, NCHW [B][Nout][Hout][Wout]
+    int Cx, H, W, Hin, Win, Hout, Wout;
+    int Nout, s, parity, T, kc8, ksteps, relu;
+    int out_lat, in_lat;  // output pixels are lattice points / the gathered tensor lives on the lattice
+    int total_pix, tiles;
+    int8_t dc[TF_MAXT], dr0[TF_MAXT], dr1[TF_MAXT];
+};
+
+__device__ __forceinline__ float tf32_rna(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return __uint_as_float(r);
+}
+
+// SW32 K-major shared-memory descriptor: 8-row groups 256 B apart (SBO), LBO unused, layout code 6
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+}
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     ptx::smem_u32(dst)),
+                 "l"((uint64_t)src), "r"(bytes), "r"(ptx::smem_u32(bar))
+                 : "memory");
+}
+
+constexpr int tmem_cols(int NT) {
+    return (2 * NT + TF_STAGES * 16) <= 32 ? 32 : (2 * NT + TF_STAGES * 16) <= 64 ? 64
+           : (2 * NT + TF_STAGES * 16) <= 128                                 ? 128
+           : (2 * NT + TF_STAGES * 16) <= 256                                 ? 256
+                                                                              : 512;
+}
+
+// Output pixel `pix` (flattened b, R, C of the output grid) -> image, centre on the full grid, centre parity.
+__device__ __forceinline__ void pixel_centre(const TfParams& p, int pix, int* b, int* rem, int* rc, int* cc) {
+    const int hw = p.Hout * p.Wout;
+    *b = pix / hw;
+    *rem = pix - *b * hw;
+    const int R = *rem / p.Wout, C = *rem - R * p.Wout;
+    if (p.out_lat) {
+        *rc = hex_rho(C, p.s, p.parity) + p.s * R;
+        *cc = p.s * C;
+    } else {
+        *rc = R;
+        *cc = C;
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(TF_THREADS, 1)
+tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ wpack) {
+    constexpr int ACC_COLS = 2 * NT;
+    constexpr int TMEM_COLS = tmem_cols(NT);
+    constexpr uint32_t KBLK = NT * 32;  // bytes of one (K-step, hi|lo) weight block
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* wsm = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t wbytes = (uint32_t)p.ksteps * 2u * KBLK;
+    uint64_t* full = reinterpret_cast<uint64_t*>(wsm + wbytes);
+    uint64_t* empty = full + TF_STAGES;
+    uint64_t* tfull = empty + TF_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* wbar = tempty + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(wbar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == TF_MMA_WARP && lane == 0) {
+        for (int s = 0; s < TF_STAGES; ++s) {
+            ptx::mbar_init(&full[s], 4);   // the 4 builder warps of the group that wrote the stage
+            ptx::mbar_init(&empty[s], 1);  // tcgen05.commit of the stage's MMAs
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], TF_EPI_WARPS);
+        }
+        ptx::mbar_init(wbar, 1);
+        ptx::fence_barrier_init();
+        ptx::mbar_arrive_expect_tx(wbar, wbytes);
+        constexpr uint32_t CH = 32768;
+        for (uint32_t off = 0; off < wbytes; off += CH)
+            bulk_g2s(wsm + off, reinterpret_cast<const uint8_t*>(wpack) + off, wbytes - off < CH ? wbytes - off : CH,
+                     wbar);
+    }
+    if (warp == TF_MMA_WARP) ptx::tmem_alloc(tslot, TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tm = *tslot;
+
+    if (warp == TF_MMA_WARP) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(128, NT);
+            ptx::mbar_wait(wbar, 0);
+            const uint32_t wbase = ptx::smem_u32(wsm);
+            int kglob = 0, acc = 0;
+            uint32_t aphase = 0;
+            for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+                ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tm + acc * NT;
+                for (int ks = 0; ks < p.ksteps; ++ks, ++kglob) {
+                    const int st = kglob % TF_STAGES;
+                    ptx::mbar_wait(&full[st], (kglob / TF_STAGES) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t ahi = tm + ACC_COLS + st * 16, alo = ahi + 8;
+                    const uint32_t b = wbase + (uint32_t)ks * 2u * KBLK;
+                    const uint64_t bhi = desc_sw32(b), blo = desc_sw32(b + KBLK);
+                    mma_tf32_ts(d, ahi, bhi, idesc, ks > 0 ? 1u : 0u);
+                    mma_tf32_ts(d, ahi, blo, idesc, 1u);
+                    mma_tf32_ts(d, alo, bhi, idesc, 1u);
+                    ptx::mma_commit(&empty[st]);
+                }
+                ptx::mma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) aphase ^= 1;
+            }
+        }
+    } else if (warp >= TF_EPI_WARPS) {
+        // builders: group g takes the K-steps kglob = g (mod TF_GROUPS); warp quadrant q fills TMEM lanes
+        // 32q .. 32q+31 = pixels 32q .. 32q+31 of the tile
+        const int g = (warp - TF_EPI_WARPS) >> 2, q = warp & 3;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        const int hw_in = p.Hin * p.Win;
+        int kglob = 0;
+        for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+            const int pix = tile * 128 + q * 32 + lane;
+            const bool valid = pix < p.total_pix;
+            int b = 0, rem = 0, rc = 0, cc = 0;
+            if (valid) pixel_centre(p, pix, &b, &rem, &rc, &cc);
+            const int pc = (cc + p.parity) & 1;
+            const float* xb = p.x + (size_t)b * p.Cx * hw_in;
+            int ks = (g - kglob % TF_GROUPS + TF_GROUPS) % TF_GROUPS;  // first K-step of this tile for group g
+            kglob += ks;
+            for (; ks < p.ksteps; ks += TF_GROUPS, kglob += TF_GROUPS) {
+                const int t = ks / p.kc8, c0 = (ks - t * p.kc8) * 8;
+                const int qr = rc + (pc ? p.dr1[t] : p.dr0[t]), qc = cc + p.dc[t];
+                bool ok = valid && qr >= 0 && qr < p.H && qc >= 0 && qc < p.W;
+                int idx = qr * p.Win + qc;
+                if (p.in_lat) {  // the neighbour must be a centre of the stride-s lattice (dy lives there)
+                    const int Cq = qc / p.s;
+                    const int rr = qr - hex_rho(Cq, p.s, p.parity);
+                    const int Rq = rr / p.s;
+                    ok = ok && qc == Cq * p.s && rr >= 0 && rr == Rq * p.s && Rq < p.Hin && Cq < p.Win;
+                    idx = Rq * p.Win + Cq;
+                }
+                float v[8];
+                const float* src = xb + (size_t)c0 * hw_in + idx;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = (ok && c0 + k < p.Cx) ? __ldg(src + (size_t)k * hw_in) : 0.f;
+                uint32_t hi[8], lo[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float h = tf32_rna(v[k]);
+                    hi[k] = __float_as_uint(h);
+                    lo[k] = __float_as_uint(v[k] - h);
+                }
+                const int st = kglob % TF_STAGES;
+                ptx::mbar_wait(&empty[st], ((kglob / TF_STAGES) & 1) ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t ta = tm + lane_base + ACC_COLS + st * 16;
+                tmem_st8(ta, hi);
+                tmem_st8(ta + 8, lo);
+                tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&full[st]);
+            }
+            kglob -= ks - p.ksteps;  // realign to the tile boundary (ks overshot by < TF_GROUPS)
+        }
+    } else {
+        // epilogue: warp q drains TMEM lanes 32q .. 32q+31 (its 32 pixels), NT columns
+        const int q = warp;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        const int hw_out = p.Hout * p.Wout;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+            const int pix = tile * 128 + q * 32 + lane;
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+            uint32_t v[NT];
+#pragma unroll
+            for (int c = 0; c < NT; c += 16) tmem_ld16(tm + lane_base + acc * NT + c, v + c);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (pix < p.total_pix) {
+                const int b = pix / hw_out, rem = pix - b * hw_out;
+                float* yo = p.y + (size_t)b * p.Nout * hw_out + rem;
+                const float* mo = p.relu_y ? p.relu_y + (size_t)b * p.Nout * hw_out + rem : nullptr;
+#pragma unroll
+                for (int c = 0; c < NT; ++c) {
+                    if (c < p.Nout) {
+                        float o = __uint_as_float(v[c]);
+                        if (p.bias) o += __ldg(p.bias + c);
+                        if (p.relu) o = fmaxf(o, 0.f);
+                        if (mo && !(__ldg(mo + (size_t)c * hw_out) > 0.f)) o = 0.f;
+                        yo[(size_t)c * hw_out] = o;
+                    }
+                }
+            }
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == TF_MMA_WARP) ptx::tmem_dealloc(tm, TMEM_COLS);
+}
+
+// Weights -> [K-step][hi|lo][NT rows][8] fp32 in the SW32 K-major layout the MMA reads.
+//   forward : row n = co, K-step (t, c8), k -> ci = 8 c8 + k :  w[co][ci][t]
+//   bwd-data: row n = ci, K-step (t, c8), k -> co = 8 c8 + k :  w[co][ci][T-1-t]   (pin P18)
+__global__ void tf32_pack_kernel(const float* __restrict__ w, float* __restrict__ wp, int Cout, int Cin, int T,
+                                 int NT, int kc8, int ksteps, int transpose) {
+    const int total = ksteps * 2 * NT * 8;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int k = e & 7, n = (e >> 3) % NT, half = (e / (8 * NT)) & 1, ks = e / (16 * NT);
+        const int t = ks / kc8, ch = (ks - t * kc8) * 8 + k;
+        float v = 0.f;
+        if (!transpose) {
+            if (n < Cout && ch < Cin) v = w[((size_t)n * Cin + ch) * T + t];
+        } else {
+            if (n < Cin && ch < Cout) v = w[((size_t)ch * Cin + n) * T + (T - 1 - t)];
+        }
+        const float hi = tf32_rna(v);
+        const float out = half ? v - hi : hi;
+        const int off = ks * 2 * NT * 8 + half * NT * 8 + n * 8 + (((k >> 2) ^ ((n >> 2) & 1)) << 2) + (k & 3);
+        wp[off] = out;
+    }
+}
+
+struct TfPlan {
+    int NT, kc8, ksteps, smem;
+    bool ok;
+};
+TfPlan tf_plan(const Geom& g, int Cx, int Nout) {
+    TfPlan pl{};
+    if (g.T > TF_MAXT || Cx < 1 || Nout < 1) return pl;
+    pl.NT = (Nout + 15) / 16 * 16;
+    if (pl.NT > TF_MAX_NT) return pl;
+    pl.kc8 = (Cx + 7) / 8;
+    pl.ksteps = g.T * pl.kc8;
+    pl.smem = pl.ksteps * 2 * pl.NT * 32 + 1024 + 256;
+    pl.ok = pl.smem <= TF_SMEM_MAX;
+    return pl;
+}
+
+template <int NT>
+hex_status_t launch_tf(const TfParams& p, const float* wpack, int smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(tf32_conv_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, TF_SMEM_MAX) !=
+            cudaSuccess)
+            return HEX_ERR_CUDA;
+        attr = true;
+    }
+    const int grid = p.tiles < num_sms() ? p.tiles : num_sms();
+    tf32_conv_kernel<NT><<<grid, TF_THREADS, smem, st>>>(p, wpack);
+    count_launch();
+    return last_launch_status();
+}
+
+}  // namespace
+
+// Which fp32 NCHW convolutions run on the 3xTF32 tensor-core kernel: enough input channels to fill a K-step
+// (Cx >= 8), <= 64 output channels, n <= 3, weights resident in shared memory.  HEXCONV_NO_TF32 forces the
+// FFMA kernels.
+bool tf32_conv_supported(const Geom& g, int Cx, int Nout, int dtype, int layout) {
+    if (dtype != HEX_F32 || layout != HEX_NCHW || Cx < 8 || sw_on("HEXCONV_NO_TF32")) return false;
+    return tf_plan(g, Cx, Nout).ok;
+}
+
+size_t tf32_conv_ws_bytes(const Geom& g, int Cx, int Nout) {
+    const TfPlan pl = tf_plan(g, Cx, Nout);
+    return pl.ok ? (size_t)pl.ksteps * 2 * pl.NT * 32 + 256 : 0;
+}
+
+// mode 0: forward of x [B][Cin][H][W] -> y [B][Cout][Ho][Wo];  mode 1: bwd-data of dy [B][Cout][Ho][Wo] ->
+// dx [B][Cin][H][W] (masked by relu_y > 0 when given).  ws holds the packed weights.
+hex_status_t tf32_conv(const Geom& g, int Cin, int Cout, int mode, const float* in, const float* w,
+                       const float* bias, const float* relu_y, int relu, float* out, void* ws, size_t ws_bytes,
+                       cudaStream_t st) {
+    const int Cx = mode ? Cout : Cin, Nout = mode ? Cin : Cout;
+    const TfPlan pl = tf_plan(g, Cx, Nout);
+    if (!pl.ok) return HEX_ERR_UNSUPPORTED;
+    const size_t need = (size_t)pl.ksteps * 2 * pl.NT * 32;
+    if (!ws || ws_bytes < need + 256) return HEX_ERR_WORKSPACE;
+    float* wp = reinterpret_cast<float*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    {
+        const int total = pl.ksteps * 2 * pl.NT * 8;
+        tf32_pack_kernel<<<ceil_div(total, 256), 256, 0, st>>>(w, wp, Cout, Cin, g.T, pl.NT, pl.kc8, pl.ksteps, mode);
+        count_launch();
+        if (last_launch_status() != HEX_OK) return HEX_ERR_CUDA;
+    }
+    TfParams p{};
+    p.x = in;
+    p.bias = mode ? nullptr : bias;
+    p.relu_y = relu_y;
+    p.y = out;
+    p.Cx = Cx;
+    p.H = g.H;
+    p.W = g.W;
+    if (mode == 0) {
+        p.Hin = g.H; p.Win = g.W; p.Hout = g.Ho; p.Wout = g.Wo;
+        p.out_lat = g.s > 1; p.in_lat = 0;
+    } else {
+        p.Hin = g.Ho; p.Win = g.Wo; p.Hout = g.H; p.Wout = g.W;
+        p.out_lat = 0; p.in_lat = g.s > 1;
+    }
+    p.Nout = Nout;
+    p.s = g.s;
+    p.parity = g.parity;
+    p.T = g.T;
+    p.kc8 = pl.kc8;
+    p.ksteps = pl.ksteps;
+    p.relu = mode ? 0 : relu;
+    p.total_pix = g.B * p.Hout * p.Wout;
+    p.tiles = ceil_div(p.total_pix, 128);
+    for (int t = 0; t < g.T; ++t) {
+        int dc, dr0, dr1;
+        tap_offset(g.n, 0, t, &dc, &dr0);
+        tap_offset(g.n, 1, t, &dc, &dr1);
+        p.dc[t] = (int8_t)dc;
+        p.dr0[t] = (int8_t)dr0;
+        p.dr1[t] = (int8_t)dr1;
+    }
+    switch (pl.NT) {
+        case 16: return launch_tf<16>(p, wp, pl.smem, st);
+        case 32: return launch_tf<32>(p, wp, pl.smem, st);
+        case 48: return launch_tf<48>(p, wp, pl.smem, st);
+        case 64: return launch_tf<64>(p, wp, pl.smem, st);
+    }
+    return HEX_ERR_UNSUPPORTED;
+}
+
+}  // namespace hexconv

@@ -80,11 +80,12 @@ def conv_desc(B, Cin, Cout, H, W, n, stride, parity, dtype, layout) -> A.ConvDes
 
 
 def conv_algo(B, Cin, Cout, H, W, n, stride, parity, dtype, layout, pass_id=0) -> str:
-    """'tcgen05' or 'stencil': the kernel family the library picks for this call."""
+    """'tcgen05' (bf16 tensor cores), 'tcgen05-tf32' (fp32 in 3xTF32 on the tensor cores) or 'stencil'
+    (CUDA cores): the kernel family the library picks for this call."""
     d = conv_desc(B, Cin, Cout, H, W, n, stride, parity, dtype, layout)
     a = ctypes.c_int32()
     A.check(A.lib().hex_conv2d_algo(ctypes.byref(d), pass_id, ctypes.byref(a)), "hex_conv2d_algo")
-    return "tcgen05" if a.value == 1 else "stencil"
+    return {1: "tcgen05", 2: "tcgen05-tf32"}.get(a.value, "stencil")
 
 
 def _workspace(desc, pass_id, device):
