@@ -19,10 +19,10 @@
 //   * B (weights, pre-split hi / lo, K-major SWIZZLE_32B: one 32-byte row = the 8 K values of one output
 //     channel) is resident in shared memory for the whole persistent kernel (one bulk copy).
 //   * Warp roles: 4 epilogue warps (TMEM -> registers -> bias / ReLU / ReLU-backward mask -> NCHW stores,
-//     coalesced across the 32 pixels of a warp), 16 builder warps in 4 groups taking K-steps round-robin
-//     (a group has 4 K-steps of MMA time to hide its global-load latency), 1 MMA-issuing warp.  A ring of
-//     8 TMEM A stages (16 columns each: hi, lo) and two accumulators (the epilogue of tile i overlaps the
-//     MMAs of tile i+1).
+//     coalesced across the 32 pixels of a warp), 16 builder warps in 4 groups taking taps round-robin
+//     (each thread prefetches the next 8-channel chunk while it splits and stores the current one),
+//     1 MMA-issuing warp.  A ring of 16 TMEM A stages (16 columns each: hi, lo) and two accumulators
+//     (the epilogue of tile i overlaps the MMAs of tile i+1).
 //
 // Modes (one kernel):
 //   forward       output pixel (R, C) of the stride-s lattice has its centre at (rho(C) + sR, sC)
@@ -38,10 +38,30 @@
 #include "kernels.h"
 #include "tc_ptx.cuh"
 
+// Development timing probe (tools/tf32_prof.cu builds this file with -DTF_PROF=1): clock64 accumulators of
+// where the MMA, builder and epilogue threads of CTA 0 spend their cycles.  Compiled out of the library.
+#ifndef TF_PROF
+#define TF_PROF 0
+#endif
+#if TF_PROF
+__device__ long long g_tf_prof[32];
+#define PROF_T0() long long _pt0 = clock64()
+#define PROF_ACC(slot) \
+    do { if (blockIdx.x == 0) g_tf_prof_acc[slot] += clock64() - _pt0; _pt0 = clock64(); } while (0)
+#else
+#define PROF_T0() \
+    do {          \
+    } while (0)
+#define PROF_ACC(slot) \
+    do {               \
+    } while (0)
+#endif
+
 namespace hexconv {
 namespace {
 
-constexpr int TF_STAGES = 8;
+constexpr int TF_KPS = 4;                          // K-steps per A stage (one barrier handshake each)
+constexpr int TF_STAGES = 4;                       // A stages in TMEM (power of two, = TF_GROUPS)
 constexpr int TF_GROUPS = 4;                       // builder groups (K-steps round-robin)
 constexpr int TF_EPI_WARPS = 4;
 constexpr int TF_BLD_WARPS = 4 * TF_GROUPS;
@@ -106,10 +126,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 constexpr int tmem_cols(int NT) {
-    return (2 * NT + TF_STAGES * 16) <= 32 ? 32 : (2 * NT + TF_STAGES * 16) <= 64 ? 64
-           : (2 * NT + TF_STAGES * 16) <= 128                                 ? 128
-           : (2 * NT + TF_STAGES * 16) <= 256                                 ? 256
-                                                                              : 512;
+    return (4 * NT + TF_STAGES * 16 * TF_KPS) <= 256 ? 256 : 512;
 }
 
 // Output pixel `pix` (flattened b, R, C of the output grid) -> image, centre on the full grid, centre parity.
@@ -127,10 +144,11 @@ __device__ __forceinline__ void pixel_centre(const TfParams& p, int pix, int* b,
     }
 }
 
-template <int NT>
+template <int NT, bool IN_LAT, bool FULLCH>
 __global__ void __launch_bounds__(TF_THREADS, 1)
 tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ wpack) {
-    constexpr int ACC_COLS = 2 * NT;
+    constexpr int ACC_COLS = 4 * NT;     // two accumulators of 2 NT columns: [D_hh + D_lh | D_hl]
+    constexpr int STAGE_COLS = 16 * TF_KPS;
     constexpr int TMEM_COLS = tmem_cols(NT);
     constexpr uint32_t KBLK = NT * 32;  // bytes of one (K-step, hi|lo) weight block
     extern __shared__ uint8_t smem_raw[];
@@ -142,8 +160,19 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
     uint64_t* tempty = tfull + 2;
     uint64_t* wbar = tempty + 2;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(wbar + 1);
+    // per K-step gather entry: dc | dr(centre parity 0) << 8 | dr(parity 1) << 16 | chunk << 24
+    uint32_t* ktab = tslot + 4;
+    for (int ks = threadIdx.x; ks < p.ksteps; ks += blockDim.x) {
+        const int t = ks / p.kc8, c8 = ks - t * p.kc8;
+        ktab[ks] = (uint32_t)(uint8_t)p.dc[t] | ((uint32_t)(uint8_t)p.dr0[t] << 8) |
+                   ((uint32_t)(uint8_t)p.dr1[t] << 16) | ((uint32_t)c8 << 24);
+    }
+    const int tstages = (p.ksteps + TF_KPS - 1) / TF_KPS;  // A stages per tile
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if TF_PROF
+    long long g_tf_prof_acc[16] = {0};
+#endif
     if (warp == TF_MMA_WARP && lane == 0) {
         for (int s = 0; s < TF_STAGES; ++s) {
             ptx::mbar_init(&full[s], 4);   // the 4 builder warps of the group that wrote the stage
@@ -169,26 +198,38 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
 
     if (warp == TF_MMA_WARP) {
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_tf32(128, NT);
+            // per K-step: D[0, 2NT) += A_hi . [B_hi ; B_lo]  (one N = 2 NT MMA: hi.hi and hi.lo side by side)
+            //             D[0, NT)  += A_lo . B_hi
+            constexpr uint32_t idesc2 = idesc_tf32(128, 2 * NT), idesc1 = idesc_tf32(128, NT);
             ptx::mbar_wait(wbar, 0);
-            const uint32_t wbase = ptx::smem_u32(wsm);
-            int kglob = 0, acc = 0;
+            const uint64_t bdesc0 = desc_sw32(ptx::smem_u32(wsm));
+            constexpr uint64_t BSTEP = (2 * KBLK) >> 4;  // descriptor address units (16 B)
+            int sglob = 0, acc = 0;
             uint32_t aphase = 0;
             for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
                 ptx::mbar_wait(&tempty[acc], aphase ^ 1);
                 ptx::tc_fence_after();
-                const uint32_t d = tm + acc * NT;
-                for (int ks = 0; ks < p.ksteps; ++ks, ++kglob) {
-                    const int st = kglob % TF_STAGES;
-                    ptx::mbar_wait(&full[st], (kglob / TF_STAGES) & 1);
+                const uint32_t d = tm + acc * 2 * NT;
+                uint64_t bd = bdesc0;
+                int ks = 0;
+                for (int js = 0; js < tstages; ++js, ++sglob) {
+                    const int st = sglob & (TF_STAGES - 1);
+                    PROF_T0();
+                    ptx::mbar_wait(&full[st], (sglob / TF_STAGES) & 1);
+                    PROF_ACC(0);
                     ptx::tc_fence_after();
-                    const uint32_t ahi = tm + ACC_COLS + st * 16, alo = ahi + 8;
-                    const uint32_t b = wbase + (uint32_t)ks * 2u * KBLK;
-                    const uint64_t bhi = desc_sw32(b), blo = desc_sw32(b + KBLK);
-                    mma_tf32_ts(d, ahi, bhi, idesc, ks > 0 ? 1u : 0u);
-                    mma_tf32_ts(d, ahi, blo, idesc, 1u);
-                    mma_tf32_ts(d, alo, bhi, idesc, 1u);
+                    const uint32_t a0 = tm + ACC_COLS + st * STAGE_COLS;
+#pragma unroll
+                    for (int kk = 0; kk < TF_KPS; ++kk) {
+                        if (ks < p.ksteps) {
+                            mma_tf32_ts(d, a0 + 16 * kk, bd, idesc2, ks > 0 ? 1u : 0u);
+                            mma_tf32_ts(d, a0 + 16 * kk + 8, bd, idesc1, 1u);
+                        }
+                        ++ks;
+                        bd += BSTEP;
+                    }
                     ptx::mma_commit(&empty[st]);
+                    PROF_ACC(1);
                 }
                 ptx::mma_commit(&tfull[acc]);
                 acc ^= 1;
@@ -196,59 +237,99 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
             }
         }
     } else if (warp >= TF_EPI_WARPS) {
-        // builders: group g takes the K-steps kglob = g (mod TF_GROUPS); warp quadrant q fills TMEM lanes
-        // 32q .. 32q+31 = pixels 32q .. 32q+31 of the tile
+        // builders: group g fills the A stages sglob = g (mod TF_GROUPS) -- every use of a TMEM stage
+        // (sglob mod TF_STAGES) belongs to the same group, so its empty-barrier parity waits are never more
+        // than one phase ahead.  A stage holds TF_KPS consecutive K-steps of one tile (the last stage of a
+        // tile may hold fewer).  Warp quadrant q fills TMEM lanes 32q .. 32q+31 = pixels 32q .. 32q+31 of the
+        // tile; all 8 * TF_KPS loads of a stage are issued before any is used.
         const int g = (warp - TF_EPI_WARPS) >> 2, q = warp & 3;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const int hw_in = p.Hin * p.Win;
-        int kglob = 0;
-        for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-            const int pix = tile * 128 + q * 32 + lane;
-            const bool valid = pix < p.total_pix;
-            int b = 0, rem = 0, rc = 0, cc = 0;
-            if (valid) pixel_centre(p, pix, &b, &rem, &rc, &cc);
-            const int pc = (cc + p.parity) & 1;
-            const float* xb = p.x + (size_t)b * p.Cx * hw_in;
-            int ks = (g - kglob % TF_GROUPS + TF_GROUPS) % TF_GROUPS;  // first K-step of this tile for group g
-            kglob += ks;
-            for (; ks < p.ksteps; ks += TF_GROUPS, kglob += TF_GROUPS) {
-                const int t = ks / p.kc8, c0 = (ks - t * p.kc8) * 8;
-                const int qr = rc + (pc ? p.dr1[t] : p.dr0[t]), qc = cc + p.dc[t];
-                bool ok = valid && qr >= 0 && qr < p.H && qc >= 0 && qc < p.W;
+        int sglob = g, js = g, tile = blockIdx.x;
+        while (js >= tstages && tile < p.tiles) {
+            js -= tstages;
+            tile += gridDim.x;
+        }
+        int cur_tile = -1, pc = 0, rc = 0, cc = 0;
+        bool valid = false;
+        const float* xb = p.x;
+        for (; tile < p.tiles; sglob += TF_GROUPS) {
+            if (tile != cur_tile) {
+                cur_tile = tile;
+                const int pix = tile * 128 + q * 32 + lane;
+                valid = pix < p.total_pix;
+                int b = 0, rem = 0;
+                rc = cc = 0;
+                if (valid) pixel_centre(p, pix, &b, &rem, &rc, &cc);
+                pc = (cc + p.parity) & 1;
+                xb = p.x + (size_t)b * p.Cx * hw_in;
+            }
+            PROF_T0();
+            const int ks0 = js * TF_KPS;
+            float v[TF_KPS][8];
+#pragma unroll
+            for (int kk = 0; kk < TF_KPS; ++kk) {
+                const int ks = ks0 + kk;
+                const bool in_k = ks < p.ksteps;
+                const uint32_t e = ktab[in_k ? ks : 0];
+                const int dc = (int8_t)(e & 0xFF), dr = (int8_t)((pc ? e >> 16 : e >> 8) & 0xFF);
+                const int c0 = (int)(e >> 24) * 8;
+                const int qr = rc + dr, qc = cc + dc;
+                bool ok = in_k && valid && (unsigned)qr < (unsigned)p.H && (unsigned)qc < (unsigned)p.W;
                 int idx = qr * p.Win + qc;
-                if (p.in_lat) {  // the neighbour must be a centre of the stride-s lattice (dy lives there)
+                if constexpr (IN_LAT) {  // the neighbour must be a centre of the stride-s lattice (dy lives there)
                     const int Cq = qc / p.s;
                     const int rr = qr - hex_rho(Cq, p.s, p.parity);
                     const int Rq = rr / p.s;
                     ok = ok && qc == Cq * p.s && rr >= 0 && rr == Rq * p.s && Rq < p.Hin && Cq < p.Win;
                     idx = Rq * p.Win + Cq;
                 }
-                float v[8];
-                const float* src = xb + (size_t)c0 * hw_in + idx;
+                // unconditional loads from a valid address (the image's first pixel when the neighbour is
+                // off-grid or off-lattice), zeroed afterwards: no predicated loads in the hot loop
+                const float* src = xb + (ok ? idx : 0) + (size_t)c0 * hw_in;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = (ok && c0 + k < p.Cx) ? __ldg(src + (size_t)k * hw_in) : 0.f;
+                for (int k = 0; k < 8; ++k) {
+                    float u;
+                    if constexpr (FULLCH) {
+                        u = __ldg(src);
+                    } else {
+                        u = c0 + k < p.Cx ? __ldg(src) : 0.f;
+                    }
+                    v[kk][k] = ok ? u : 0.f;
+                    src += hw_in;
+                }
+            }
+            PROF_ACC(4);
+            const int st = sglob & (TF_STAGES - 1);
+            ptx::mbar_wait(&empty[st], ((sglob / TF_STAGES) & 1) ^ 1);
+            PROF_ACC(6);
+            ptx::tc_fence_after();
+            const uint32_t ta = tm + lane_base + ACC_COLS + st * STAGE_COLS;
+#pragma unroll
+            for (int kk = 0; kk < TF_KPS; ++kk) {
                 uint32_t hi[8], lo[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const float h = tf32_rna(v[k]);
+                    const float h = tf32_rna(v[kk][k]);
                     hi[k] = __float_as_uint(h);
-                    lo[k] = __float_as_uint(v[k] - h);
+                    lo[k] = __float_as_uint(v[kk][k] - h);
                 }
-                const int st = kglob % TF_STAGES;
-                ptx::mbar_wait(&empty[st], ((kglob / TF_STAGES) & 1) ^ 1);
-                ptx::tc_fence_after();
-                const uint32_t ta = tm + lane_base + ACC_COLS + st * 16;
-                tmem_st8(ta, hi);
-                tmem_st8(ta + 8, lo);
-                tmem_st_wait();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&full[st]);
+                tmem_st8(ta + 16 * kk, hi);
+                tmem_st8(ta + 16 * kk + 8, lo);
             }
-            kglob -= ks - p.ksteps;  // realign to the tile boundary (ks overshot by < TF_GROUPS)
+            tmem_st_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&full[st]);
+            PROF_ACC(7);
+            js += TF_GROUPS;
+            while (js >= tstages && tile < p.tiles) {
+                js -= tstages;
+                tile += gridDim.x;
+            }
         }
     } else {
-        // epilogue: warp q drains TMEM lanes 32q .. 32q+31 (its 32 pixels), NT columns
+        // epilogue: warp q drains TMEM lanes 32q .. 32q+31 (its 32 pixels): out = D[c] + D[NT + c]
         const int q = warp;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const int hw_out = p.Hout * p.Wout;
@@ -256,34 +337,50 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
         uint32_t aphase = 0;
         for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
             const int pix = tile * 128 + q * 32 + lane;
+            PROF_T0();
             ptx::mbar_wait(&tfull[acc], aphase);
+            PROF_ACC(10);
             ptx::tc_fence_after();
-            uint32_t v[NT];
+            const bool vpix = pix < p.total_pix;
+            const int b = pix / hw_out, rem = pix - b * hw_out;
+            float* yo = p.y + (size_t)b * p.Nout * hw_out + rem;
+            const float* mo = p.relu_y ? p.relu_y + (size_t)b * p.Nout * hw_out + rem : nullptr;
+            const uint32_t dbase = tm + lane_base + acc * 2 * NT;
 #pragma unroll
-            for (int c = 0; c < NT; c += 16) tmem_ld16(tm + lane_base + acc * NT + c, v + c);
-            ptx::tmem_ld_wait();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-            if (pix < p.total_pix) {
-                const int b = pix / hw_out, rem = pix - b * hw_out;
-                float* yo = p.y + (size_t)b * p.Nout * hw_out + rem;
-                const float* mo = p.relu_y ? p.relu_y + (size_t)b * p.Nout * hw_out + rem : nullptr;
+            for (int c0 = 0; c0 < NT; c0 += 16) {
+                uint32_t u[16], w[16];
+                tmem_ld16(dbase + c0, u);
+                tmem_ld16(dbase + NT + c0, w);
+                ptx::tmem_ld_wait();
+                if (c0 + 16 >= NT) {  // the accumulator is drained: hand it back to the MMA warp
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                }
+                if (vpix) {
 #pragma unroll
-                for (int c = 0; c < NT; ++c) {
-                    if (c < p.Nout) {
-                        float o = __uint_as_float(v[c]);
-                        if (p.bias) o += __ldg(p.bias + c);
-                        if (p.relu) o = fmaxf(o, 0.f);
-                        if (mo && !(__ldg(mo + (size_t)c * hw_out) > 0.f)) o = 0.f;
-                        yo[(size_t)c * hw_out] = o;
+                    for (int j = 0; j < 16; ++j) {
+                        const int c = c0 + j;
+                        if (c < p.Nout) {
+                            float o = __uint_as_float(u[j]) + __uint_as_float(w[j]);
+                            if (p.bias) o += __ldg(p.bias + c);
+                            if (p.relu) o = fmaxf(o, 0.f);
+                            if (mo && !(__ldg(mo + (size_t)c * hw_out) > 0.f)) o = 0.f;
+                            yo[(size_t)c * hw_out] = o;
+                        }
                     }
                 }
             }
+            PROF_ACC(11);
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
     }
+#if TF_PROF
+    if (blockIdx.x == 0 && lane == 0 && (warp == TF_MMA_WARP || warp == TF_EPI_WARPS || warp == 0))
+        for (int i = 0; i < 16; ++i)
+            if (g_tf_prof_acc[i]) g_tf_prof[i] = g_tf_prof_acc[i];
+#endif
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == TF_MMA_WARP) ptx::tmem_dealloc(tm, TMEM_COLS);
@@ -322,24 +419,31 @@ TfPlan tf_plan(const Geom& g, int Cx, int Nout) {
     if (pl.NT > TF_MAX_NT) return pl;
     pl.kc8 = (Cx + 7) / 8;
     pl.ksteps = g.T * pl.kc8;
-    pl.smem = pl.ksteps * 2 * pl.NT * 32 + 1024 + 256;
+    pl.smem = pl.ksteps * 2 * pl.NT * 32 + 1024 + 256 + 4 * pl.ksteps;
     pl.ok = pl.smem <= TF_SMEM_MAX;
     return pl;
 }
 
-template <int NT>
-hex_status_t launch_tf(const TfParams& p, const float* wpack, int smem, cudaStream_t st) {
+template <int NT, bool IN_LAT, bool FULLCH>
+hex_status_t launch_tf_k(const TfParams& p, const float* wpack, int smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(tf32_conv_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, TF_SMEM_MAX) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(tf32_conv_kernel<NT, IN_LAT, FULLCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TF_SMEM_MAX) != cudaSuccess)
             return HEX_ERR_CUDA;
         attr = true;
     }
     const int grid = p.tiles < num_sms() ? p.tiles : num_sms();
-    tf32_conv_kernel<NT><<<grid, TF_THREADS, smem, st>>>(p, wpack);
+    tf32_conv_kernel<NT, IN_LAT, FULLCH><<<grid, TF_THREADS, smem, st>>>(p, wpack);
     count_launch();
     return last_launch_status();
+}
+
+template <int NT>
+hex_status_t launch_tf(const TfParams& p, const float* wpack, int smem, cudaStream_t st) {
+    const bool full = (p.Cx & 7) == 0;
+    if (p.in_lat) return full ? launch_tf_k<NT, true, true>(p, wpack, smem, st) : launch_tf_k<NT, true, false>(p, wpack, smem, st);
+    return full ? launch_tf_k<NT, false, true>(p, wpack, smem, st) : launch_tf_k<NT, false, false>(p, wpack, smem, st);
 }
 
 }  // namespace
