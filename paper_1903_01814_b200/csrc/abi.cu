@@ -151,6 +151,9 @@ bool use_tf32_fwd(const hex_conv2d_desc_t* d, const Geom& g) {
 bool use_tf32_bwd_data(const hex_conv2d_desc_t* d, const Geom& g) {
     return tf32_conv_supported(g, d->out_channels, d->in_channels, d->dtype, d->layout);
 }
+bool use_tf32_wgrad(const hex_conv2d_desc_t* d, const Geom& g) {
+    return tf32_wgrad_supported(g, d->in_channels, d->out_channels, d->dtype, d->layout);
+}
 bool use_tc_wgrad(const hex_conv2d_desc_t* d, const Geom& g) {
     return d->dtype == HEX_BF16 && d->layout == HEX_NHWC && tc_wgrad_supported(g, d->in_channels, d->out_channels);
 }
@@ -299,6 +302,7 @@ hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* d, int32_t pass,
             *bytes = use_tc_wgrad(d, g)      ? tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
                      : use_tc_wgrad_up(d, g) ? up_bytes(d, g) + tc_wgrad_ws_bytes(stride1(g), d->in_channels,
                                                                                    d->out_channels)
+                     : use_tf32_wgrad(d, g)  ? tf32_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
                      : use_smallc(d, g) ? smallc_wgrad_ws_bytes(g, d->out_channels)
                      : use_c1(d, g)     ? c1_wgrad_ws_bytes(g, d->out_channels)
                      : use_f32wg(d, g)  ? f32_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
@@ -318,7 +322,7 @@ hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* d, int32_t pass, int32_t* 
         case 1:
             *algo = use_tc_bwd_data(d, g) || use_tc_bwd_data_up(d, g) ? 1 : use_tf32_bwd_data(d, g) ? 2 : 0;
             return HEX_OK;
-        case 2: *algo = use_tc_wgrad(d, g) || use_tc_wgrad_up(d, g) ? 1 : 0; return HEX_OK;
+        case 2: *algo = use_tc_wgrad(d, g) || use_tc_wgrad_up(d, g) ? 1 : use_tf32_wgrad(d, g) ? 2 : 0; return HEX_OK;
         default: return HEX_ERR_INVALID_ARG;
     }
 }
@@ -464,6 +468,9 @@ hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* d, const void* x, co
         a.x = x; a.dy = up; a.dw = dw; a.dbias = dbias; a.accumulate = accumulate;
         return tc_conv_wgrad(a, rest, ws_bytes - (size_t)(rest - (char*)ws), s);
     }
+    if (use_tf32_wgrad(d, g))
+        return tf32_wgrad(g, d->in_channels, d->out_channels, (const float*)x, (const float*)dy, dw, dbias,
+                          accumulate, ws, ws_bytes, s);
     if (use_smallc(d, g)) {
         const size_t need = smallc_wgrad_ws_bytes(g, d->out_channels);
         if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;

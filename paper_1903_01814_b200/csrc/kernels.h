@@ -134,5 +134,9 @@ size_t tf32_conv_ws_bytes(const Geom& g, int Cx, int Nout);
 hex_status_t tf32_conv(const Geom& g, int Cin, int Cout, int mode, const float* in, const float* w,
                        const float* bias, const float* relu_y, int relu, float* out, void* ws, size_t ws_bytes,
                        cudaStream_t st);
+bool tf32_wgrad_supported(const Geom& g, int Cin, int Cout, int dtype, int layout);
+size_t tf32_wgrad_ws_bytes(const Geom& g, int Cin, int Cout);
+hex_status_t tf32_wgrad(const Geom& g, int Cin, int Cout, const float* x, const float* dy, float* dw, float* dbias,
+                        int accumulate, void* ws, size_t ws_bytes, cudaStream_t st, int dbg = 0);
 
 }  // namespace hexconv

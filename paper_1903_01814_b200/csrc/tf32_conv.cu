@@ -32,6 +32,9 @@
 //                 centre contributes 0 (the stride-1 adjoint of dy scattered onto the full grid, P10) -- so
 //                 no upsampled copy of dy is written.
 #include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "geometry.cuh"
@@ -517,6 +520,471 @@ hex_status_t tf32_conv(const Geom& g, int Cin, int Cout, int mode, const float* 
         case 64: return launch_tf<64>(p, wp, pl.smem, st);
     }
     return HEX_ERR_UNSUPPORTED;
+}
+
+
+// ====================================================================================================
+// Weight gradient (+ dbias) in 3xTF32:  dW[co][ci][t] = sum_{b,o} dy[b][co][o] * x[b][ci][centre(o) + off_t]
+// (the adjoint of the forward with respect to the weights).
+//
+// GEMM view: M = (t, ci) rows (m = t * Cin + ci, up to 3 M-tiles of 128), N = Cout (padded to 16, <= 64),
+// K = output pixels.  A K-step is 8 consecutive output pixels of one output row (b, R): C0 .. C0+7.
+//   * The x rows an output row needs (all Cin channels, every tap's row, W + 2n columns with zero halo)
+//     are staged as one TMA box per output row ("band", OOB rows / columns zero-filled), double-buffered.
+//     The box's rows x columns are padded so that one channel plane is 4 x odd words: the 32 lanes of a
+//     warp (32 (t, ci) rows) then spread over the banks (16 channels of a plane-multiple-of-16 box sat on
+//     2 banks).
+//   * A builders (one thread per TMEM lane = per (t, ci) row, two groups alternating K-steps) read their
+//     8 values from the band -- two base addresses per K-step (the two column parities of the centres)
+//     plus compile-time offsets -- split them hi / lo and tcgen05.st them.
+//   * The same group's first 2 Cout threads load dy[b][co][R][C0 .. C0+7] (two threads per output
+//     channel, one K-step ahead), split it and write the K-major SW32 hi / lo block to shared memory
+//     (fence.proxy.async before signalling), keeping the dbias partial sums.
+//   * Per K-step and M-tile: D += A_hi . [B_hi ; B_lo] (N = 2 Cout) and D += A_lo . B_hi (N = Cout).
+//   * Split-K: CTA c takes a contiguous range of output rows; it writes its partial dW [co][m] and dbias
+//     to the workspace, and a fixed-order reduction kernel sums the partials (deterministic).
+namespace {
+
+constexpr int WG_G = 2;   // A-builder groups (K-steps alternate)
+constexpr int WG_HL = 4;  // left halo columns of a band (16 bytes: TMA needs the innermost start 16-byte aligned)
+
+struct WgParams {
+    const float* dy;      // [B][Cout][Ho][Wo]
+    float* part;          // [grid][Cout][Mrows] partial dW
+    float* part_b;        // [grid][Cout] partial dbias
+    int Cin, Cout, H, W, Ho, Wo, s, parity, n, T, Mrows;
+    int rows, rows_per_cta, cblk;  // output rows B*Ho, per CTA, K-steps per output row
+    int rmin, NR, BW;              // band: input rows s*R + rmin .. + NR - 1, columns -WG_HL .. BW - WG_HL - 1
+
+    int8_t dc[TF_MAXT], dr0[TF_MAXT], dr1[TF_MAXT];
+    int dbg;  // development probe only (TF_PROF builds): bit 0 no MMA, 1 no tcgen05.st, 2 no TMA, 3 no tcgen05.ld
+};
+#if TF_PROF
+#define WG_SKIP(bit) (p.dbg & (1 << (bit)))
+#else
+#define WG_SKIP(bit) false
+#endif
+
+template <int NT, int MT>
+struct WgCfg {
+    static constexpr int AWARPS = 4 * MT * WG_G;           // A builders
+    static constexpr int TWARP = 4 + AWARPS;               // TMA (x bands)
+    static constexpr int MWARP = TWARP + 1;                // MMA issue
+    static constexpr int THREADS = (MWARP + 1) * 32;
+    static constexpr int ACC = MT * 2 * NT;                // accumulators
+    static constexpr int STAGES = (ACC + 4 * MT * 16 <= 512) ? 4 : 2;
+    static constexpr int TCOLS = (ACC + STAGES * MT * 16) <= 256 ? 256 : 512;
+    static constexpr int BBYTES = 2 * NT * 32;             // one stage's B block (hi | lo)
+};
+
+template <int NT, int MT, int S>
+__global__ void __launch_bounds__(WgCfg<NT, MT>::THREADS, 1)
+tf32_wgrad_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ WgParams p) {
+    using Cfg = WgCfg<NT, MT>;
+    constexpr int STAGES = Cfg::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* bsm = base;                                             // STAGES x B blocks (1024-aligned)
+    float* band = reinterpret_cast<float*>(base + STAGES * Cfg::BBYTES);
+    const int band_elems = (p.Cin * p.NR * p.BW + 31) & ~31;  // buffer pitch: 128-byte aligned TMA destinations
+    uint64_t* bars = reinterpret_cast<uint64_t*>(band + 2 * band_elems);
+    uint64_t* full = bars;               // STAGES
+    uint64_t* empty = full + STAGES;     // STAGES
+    uint64_t* xfull = empty + STAGES;    // 2
+    uint64_t* xempty = xfull + 2;        // 2
+    uint64_t* dfull = xempty + 2;        // 1
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(dfull + 1);
+    float* bpart = reinterpret_cast<float*>(tslot + 4);  // [WG_G][2 NT] dbias partial sums
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if TF_PROF
+    long long g_tf_prof_acc[16] = {0};
+#endif
+    const int row0 = blockIdx.x * p.rows_per_cta;
+    const int row1 = min(p.rows, row0 + p.rows_per_cta);
+    const int nrows = max(0, row1 - row0);
+    const int nk = nrows * p.cblk;  // K-steps of this CTA
+    if (warp == Cfg::MWARP && lane == 0) {
+        for (int st = 0; st < STAGES; ++st) {
+            ptx::mbar_init(&full[st], 4 * MT);  // the owning group's warps (A in TMEM, B in smem)
+            ptx::mbar_init(&empty[st], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&xfull[b], 1);
+            ptx::mbar_init(&xempty[b], Cfg::AWARPS);
+        }
+        ptx::mbar_init(dfull, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == Cfg::MWARP) ptx::tmem_alloc(tslot, Cfg::TCOLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tm = *tslot;
+    const int hwo = p.Ho * p.Wo;
+    (void)hwo;
+
+    if (warp == Cfg::TWARP) {
+        if (lane == 0) {
+            ptx::prefetch_tmap(&map_x);
+            for (int r = 0; r < nrows; ++r) {
+                const int buf = r & 1;
+                ptx::mbar_wait(&xempty[buf], ((r >> 1) & 1) ^ 1);
+                const int row = row0 + r, b = row / p.Ho, R = row - b * p.Ho;
+                ptx::mbar_arrive_expect_tx(&xfull[buf], (uint32_t)(p.Cin * p.NR * p.BW) * 4u);
+                ptx::tma_load_4d(&map_x, &xfull[buf], band + buf * band_elems, -WG_HL, p.s * R + p.rmin, 0, b);
+            }
+        }
+    } else if (warp == Cfg::MWARP) {
+        if (lane == 0) {
+            constexpr uint32_t idesc2 = idesc_tf32(128, 2 * NT), idesc1 = idesc_tf32(128, NT);
+            const uint64_t b0 = desc_sw32(ptx::smem_u32(bsm));
+            for (int kg = 0; kg < nk; ++kg) {
+                const int st = kg % STAGES;
+                PROF_T0();
+                ptx::mbar_wait(&full[st], (kg / STAGES) & 1);
+                PROF_ACC(0);
+                ptx::tc_fence_after();
+                const uint64_t bd = b0 + (uint64_t)((st * Cfg::BBYTES) >> 4);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const uint32_t d = tm + mt * 2 * NT;
+                    const uint32_t a = tm + Cfg::ACC + (st * MT + mt) * 16;
+                    if (WG_SKIP(0)) continue;
+                    mma_tf32_ts(d, a, bd, idesc2, kg > 0 ? 1u : 0u);
+                    mma_tf32_ts(d, a + 8, bd, idesc1, 1u);
+                }
+                ptx::mma_commit(&empty[st]);
+                PROF_ACC(1);
+            }
+            ptx::mma_commit(dfull);
+        }
+    } else if (warp >= 4) {
+        // A builders: warp index within the group -> (M-tile, lane quadrant = warp % 4)
+        const int wi = warp - 4, g = wi / (4 * MT), wg = wi - g * 4 * MT;
+        const int mt = wg >> 2, q = warp & 3;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        const int m = mt * 128 + q * 32 + lane;
+        const bool mvalid = m < p.Mrows;
+        const int t = mvalid ? m / p.Cin : 0, ci = mvalid ? m - t * p.Cin : 0;
+        const int dct = p.dc[t];
+        const int plane = p.NR * p.BW;
+        // B role: thread bi of the group (bi < 2 NT) loads dy[b][co = bi / 2][R][C0 + 4 (bi & 1) .. + 3] of the
+        // group's K-steps, one K-step ahead, splits it and writes its half row of the SW32 hi / lo blocks;
+        // it also sums those dy values for dbias
+        const int bi = wg * 32 + lane, bn = bi >> 1, bh = bi & 1;
+        const bool brole = bi < 2 * NT, bload_ok = brole && bn < p.Cout;
+        const bool vec = (p.Wo & 3) == 0 && ((uintptr_t)p.dy & 15) == 0;
+        float bsum = 0.f;
+        auto bload = [&](int kgx, float* v) {
+            v[0] = v[1] = v[2] = v[3] = 0.f;
+            if (!bload_ok || kgx >= nk) return;
+            const int rx = kgx / p.cblk, C0 = (kgx - rx * p.cblk) * 8 + 4 * bh;
+            const int row = row0 + rx, b = row / p.Ho, R = row - b * p.Ho;
+            const float* src = p.dy + ((size_t)(b * p.Cout + bn) * p.Ho + R) * p.Wo + C0;
+            if (vec && C0 + 4 <= p.Wo) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(src));
+                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[k] = C0 + k < p.Wo ? __ldg(src + k) : 0.f;
+            }
+        };
+        float bnext[4];
+        bload(g, bnext);
+        int kg = 0;
+        for (int r = 0; r < nrows; ++r) {
+            const int buf = r & 1;
+            PROF_T0();
+            ptx::mbar_wait(&xfull[buf], (r >> 1) & 1);
+            PROF_ACC(6);
+            const int row = row0 + r, R = row - (row / p.Ho) * p.Ho;
+            const float* bx = band + buf * band_elems + ci * plane;
+            for (int j = 0; j < p.cblk; ++j, ++kg) {
+                if (kg % WG_G != g) continue;
+                const int C0 = j * 8;
+                const int ss = S ? S : p.s;
+                // the two column parities of the centres: base addresses into the band
+                int bse[2];
+#pragma unroll
+                for (int cp = 0; cp < 2; ++cp) {
+                    const int C = C0 + cp;
+                    const int rc = hex_rho(C, ss, p.parity) + ss * R, cc = ss * C;
+                    const int pc = (cc + p.parity) & 1;
+                    const int srow = rc + (pc ? p.dr1[t] : p.dr0[t]) - (ss * R + p.rmin);
+                    bse[cp] = srow * p.BW + cc + dct + WG_HL - cp * ss;
+                }
+                const int nv = min(8, p.Wo - C0);
+                uint32_t hi[8], lo[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float u = (mvalid && k < nv) ? bx[bse[k & 1] + ss * k] : 0.f;
+                    const float h = tf32_rna(u);
+                    hi[k] = __float_as_uint(h);
+                    lo[k] = __float_as_uint(u - h);
+                }
+                float bv[4] = {bnext[0], bnext[1], bnext[2], bnext[3]};
+                bload(kg + WG_G, bnext);  // this group's next K-step
+                const int st = kg % STAGES;
+                PROF_ACC(7);
+                ptx::mbar_wait(&empty[st], ((kg / STAGES) & 1) ^ 1);
+                PROF_ACC(8);
+                ptx::tc_fence_after();
+                const uint32_t ta = tm + lane_base + Cfg::ACC + (st * MT + mt) * 16;
+                if (!WG_SKIP(1)) {
+                    tmem_st8(ta, hi);
+                    tmem_st8(ta + 8, lo);
+                }
+                if (brole) {
+                    float bhv[4], blv[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        bsum += bv[k];
+                        bhv[k] = tf32_rna(bv[k]);
+                        blv[k] = bv[k] - bhv[k];
+                    }
+                    // SW32 K-major: 16-byte chunk c of row n at n * 32 + ((c ^ ((n >> 2) & 1)) * 16)
+                    uint8_t* blk = bsm + st * Cfg::BBYTES;
+                    const int off = bn * 32 + ((bh ^ ((bn >> 2) & 1)) << 4);
+                    *reinterpret_cast<float4*>(blk + off) = make_float4(bhv[0], bhv[1], bhv[2], bhv[3]);
+                    *reinterpret_cast<float4*>(blk + NT * 32 + off) = make_float4(blv[0], blv[1], blv[2], blv[3]);
+                    ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
+                }
+                if (!WG_SKIP(1)) tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&full[st]);
+                PROF_ACC(9);
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&xempty[buf]);  // done with this row's band
+        }
+        if (brole) bpart[g * 2 * NT + bi] = bsum;
+    } else {
+        // epilogue (warps 0-3): D rows of lane quadrant q -> partial [co][m] = D[c] + D[NT + c]
+        const int q = warp;
+        ptx::mbar_wait(dfull, 0);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int m = mt * 128 + q * 32 + lane;
+            const uint32_t dbase = tm + ((uint32_t)(q * 32) << 16) + mt * 2 * NT;
+#pragma unroll
+            for (int c0 = 0; c0 < NT; c0 += 16) {
+                uint32_t u[16] = {}, w[16] = {};
+                if (!WG_SKIP(3)) {
+                    tmem_ld16(dbase + c0, u);
+                    tmem_ld16(dbase + NT + c0, w);
+                    ptx::tmem_ld_wait();
+                }
+                if (m < p.Mrows) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int co = c0 + j;
+                        if (co < p.Cout)
+                            p.part[((size_t)blockIdx.x * p.Cout + co) * p.Mrows + m] =
+                                nk ? __uint_as_float(u[j]) + __uint_as_float(w[j]) : 0.f;
+                    }
+                }
+            }
+        }
+    }
+#if TF_PROF
+    if (blockIdx.x == 0 && lane == 0 && (warp == Cfg::MWARP || warp == 4))
+        for (int i = 0; i < 16; ++i)
+            if (g_tf_prof_acc[i]) g_tf_prof[16 + i] = g_tf_prof_acc[i];
+#endif
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == Cfg::MWARP) ptx::tmem_dealloc(tm, Cfg::TCOLS);
+    if (warp == 0) {  // dbias partial of this CTA: the B threads' sums in fixed order
+        for (int co = lane; co < p.Cout; co += 32) {
+            float acc = 0.f;
+            for (int gg = 0; gg < WG_G; ++gg) acc += bpart[gg * 2 * NT + 2 * co] + bpart[gg * 2 * NT + 2 * co + 1];
+            p.part_b[(size_t)blockIdx.x * p.Cout + co] = nk ? acc : 0.f;
+        }
+    }
+}
+
+// dw[co][ci][t] (+)= sum_c part[c][co][t * Cin + ci]; dbias[co] (+)= sum_c part_b[c][co]  (fixed order)
+__global__ void tf32_wgrad_reduce_kernel(const float* __restrict__ part, const float* __restrict__ part_b, int nparts,
+                                         int Cout, int Cin, int T, float* __restrict__ dw, float* __restrict__ dbias,
+                                         int accumulate) {
+    const int Mrows = T * Cin;
+    const int total = Cout * Mrows;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total + Cout; e += gridDim.x * blockDim.x) {
+        if (e < total) {
+            const int co = e / Mrows, mm = e - co * Mrows;
+            float acc = 0.f;
+            for (int c = 0; c < nparts; ++c) acc += part[(size_t)c * total + e];
+            const int t = mm / Cin, ci = mm - t * Cin;
+            float* o = dw + ((size_t)co * Cin + ci) * T + t;
+            *o = accumulate ? *o + acc : acc;
+        } else if (dbias) {
+            const int co = e - total;
+            float acc = 0.f;
+            for (int c = 0; c < nparts; ++c) acc += part_b[(size_t)c * Cout + co];
+            dbias[co] = accumulate ? dbias[co] + acc : acc;
+        }
+    }
+}
+
+struct WgPlan {
+    int NT, MT, grid, rows_per_cta, cblk, rmin, NR, BW, smem;
+    bool ok;
+};
+WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
+    WgPlan pl{};
+    if (g.T > TF_MAXT || Cin < 1 || Cout < 1 || g.n > 3) return pl;
+    pl.NT = (Cout + 15) / 16 * 16;
+    const int Mrows = g.T * Cin;
+    pl.MT = (Mrows + 127) / 128;
+    if (pl.NT > TF_MAX_NT || pl.MT > 3) return pl;
+    // band rows: s*R + min/max over the two centre-column parities of (rho(C) + dr)
+    int mn = 1 << 20, mx = -(1 << 20);
+    for (int cp = 0; cp < 2; ++cp) {
+        const int rho = hex_rho(cp, g.s, g.parity), pc = (g.s * cp + g.parity) & 1;
+        for (int t = 0; t < g.T; ++t) {
+            int dc, dr;
+            tap_offset(g.n, pc, t, &dc, &dr);
+            mn = std::min(mn, rho + dr);
+            mx = std::max(mx, rho + dr);
+        }
+    }
+    pl.rmin = mn;
+    // box rows x columns (columns a multiple of 4: 16-byte TMA rows) padded until one channel plane is
+    // 4 x odd words (bank spread of the 32 (t, ci) lanes of a warp)
+    pl.NR = mx - mn + 1;
+    pl.BW = (g.W + WG_HL + g.n + 3) / 4 * 4;
+    for (int tries = 0; tries < 16 && ((pl.NR * pl.BW) % 8) != 4; ++tries) {
+        if (tries & 1) ++pl.NR; else pl.BW += 4;
+    }
+    if (pl.BW > 256 || pl.NR > 256 || Cin > 256) return pl;
+    pl.cblk = (g.Wo + 7) / 8;
+    const int rows = g.B * g.Ho;
+    pl.grid = std::min(rows, num_sms());
+    pl.rows_per_cta = (rows + pl.grid - 1) / pl.grid;
+    pl.grid = (rows + pl.rows_per_cta - 1) / pl.rows_per_cta;
+    const int stages = (pl.MT * 2 * pl.NT + 4 * pl.MT * 16 <= 512) ? 4 : 2;
+    pl.smem = 1024 + stages * 2 * pl.NT * 32 + 2 * ((Cin * pl.NR * pl.BW + 31) & ~31) * 4 + 256 + WG_G * 2 * pl.NT * 4;
+    pl.ok = pl.smem <= TF_SMEM_MAX && (g.W * 4) % 16 == 0;  // TMA: 16-byte multiple row pitch of x
+    return pl;
+}
+
+template <int NT, int MT, int S>
+hex_status_t launch_wg_k(const CUtensorMap& mx, const WgParams& p, int grid, int smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(tf32_wgrad_kernel<NT, MT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TF_SMEM_MAX) != cudaSuccess)
+            return HEX_ERR_CUDA;
+        attr = true;
+    }
+    tf32_wgrad_kernel<NT, MT, S><<<grid, WgCfg<NT, MT>::THREADS, smem, st>>>(mx, p);
+    count_launch();
+    return last_launch_status();
+}
+
+template <int NT, int MT>
+hex_status_t launch_wg_s(const CUtensorMap& mx, const WgParams& p, int grid, int smem, cudaStream_t st) {
+    if (p.s == 1) return launch_wg_k<NT, MT, 1>(mx, p, grid, smem, st);
+    if (p.s == 2) return launch_wg_k<NT, MT, 2>(mx, p, grid, smem, st);
+    return launch_wg_k<NT, MT, 0>(mx, p, grid, smem, st);
+}
+
+template <int NT>
+hex_status_t launch_wg_m(const CUtensorMap& mx, const WgParams& p, int MT, int grid, int smem, cudaStream_t st) {
+    switch (MT) {
+        case 1: return launch_wg_s<NT, 1>(mx, p, grid, smem, st);
+        case 2: return launch_wg_s<NT, 2>(mx, p, grid, smem, st);
+        case 3: return launch_wg_s<NT, 3>(mx, p, grid, smem, st);
+    }
+    return HEX_ERR_UNSUPPORTED;
+}
+
+}  // namespace
+
+bool tf32_wgrad_supported(const Geom& g, int Cin, int Cout, int dtype, int layout) {
+    if (dtype != HEX_F32 || layout != HEX_NCHW || Cin < 8 || sw_on("HEXCONV_NO_TF32")) return false;
+    return wg_plan(g, Cin, Cout).ok;
+}
+
+size_t tf32_wgrad_ws_bytes(const Geom& g, int Cin, int Cout) {
+    const WgPlan pl = wg_plan(g, Cin, Cout);
+    if (!pl.ok) return 0;
+    return (size_t)pl.grid * Cout * (g.T * Cin + 1) * sizeof(float) + 512;
+}
+
+hex_status_t tf32_wgrad(const Geom& g, int Cin, int Cout, const float* x, const float* dy, float* dw, float* dbias,
+                        int accumulate, void* ws, size_t ws_bytes, cudaStream_t st, int dbg) {
+    const WgPlan pl = wg_plan(g, Cin, Cout);
+    if (!pl.ok) return HEX_ERR_UNSUPPORTED;
+    const size_t need = (size_t)pl.grid * Cout * (g.T * Cin + 1) * sizeof(float) + 512;
+    if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
+    float* part = reinterpret_cast<float*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    float* part_b = part + (size_t)pl.grid * Cout * g.T * Cin;
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            enc = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
+    }
+    if (!enc) return HEX_ERR_CUDA;
+    if ((uintptr_t)x & 15) return HEX_ERR_ALIGNMENT;  // TMA global address
+    CUtensorMap mx;
+    cuuint64_t dims[4] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)Cin, (cuuint64_t)g.B};
+    cuuint64_t strides[3] = {(cuuint64_t)g.W * 4, (cuuint64_t)g.H * g.W * 4, (cuuint64_t)Cin * g.H * g.W * 4};
+    cuuint32_t box[4] = {(cuuint32_t)pl.BW, (cuuint32_t)pl.NR, (cuuint32_t)Cin, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return HEX_ERR_CUDA;
+    WgParams p{};
+    p.dbg = dbg;
+    p.dy = dy;
+    p.part = part;
+    p.part_b = part_b;
+    p.Cin = Cin;
+    p.Cout = Cout;
+    p.H = g.H;
+    p.W = g.W;
+    p.Ho = g.Ho;
+    p.Wo = g.Wo;
+    p.s = g.s;
+    p.parity = g.parity;
+    p.n = g.n;
+    p.T = g.T;
+    p.Mrows = g.T * Cin;
+    p.rows = g.B * g.Ho;
+    p.rows_per_cta = pl.rows_per_cta;
+    p.cblk = pl.cblk;
+    p.rmin = pl.rmin;
+    p.NR = pl.NR;
+    p.BW = pl.BW;
+    for (int t = 0; t < g.T; ++t) {
+        int dc, dr0, dr1;
+        tap_offset(g.n, 0, t, &dc, &dr0);
+        tap_offset(g.n, 1, t, &dc, &dr1);
+        p.dc[t] = (int8_t)dc;
+        p.dr0[t] = (int8_t)dr0;
+        p.dr1[t] = (int8_t)dr1;
+    }
+    hex_status_t r = HEX_ERR_UNSUPPORTED;
+    switch (pl.NT) {
+        case 16: r = launch_wg_m<16>(mx, p, pl.MT, pl.grid, pl.smem, st); break;
+        case 32: r = launch_wg_m<32>(mx, p, pl.MT, pl.grid, pl.smem, st); break;
+        case 48: r = launch_wg_m<48>(mx, p, pl.MT, pl.grid, pl.smem, st); break;
+        case 64: r = launch_wg_m<64>(mx, p, pl.MT, pl.grid, pl.smem, st); break;
+    }
+    if (r != HEX_OK) return r;
+    const int total = Cout * g.T * Cin + Cout;
+    tf32_wgrad_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(part, part_b, pl.grid, Cout, Cin, g.T, dw, dbias,
+                                                                  accumulate);
+    count_launch();
+    return last_launch_status();
 }
 
 }  // namespace hexconv

@@ -34,15 +34,16 @@ def np64(t):
 
 
 CASES = [  # B, Cin, Cout, H, W, n, s, parity
-    (2, 16, 32, 11, 13, 2, 1, 0),
+    (2, 16, 32, 11, 12, 2, 1, 0),
     (3, 16, 32, 12, 12, 1, 1, 1),
-    (2, 13, 5, 9, 14, 2, 1, 0),      # Cin not a multiple of 8, Cout < 16
-    (1, 32, 64, 20, 20, 1, 1, 0),    # config-3 layer-4 shape (one image)
-    (2, 8, 16, 7, 6, 3, 1, 1),       # n = 3
-    (4, 16, 32, 12, 13, 2, 2, 0),    # config-2 shape family, stride 2
-    (3, 16, 24, 11, 12, 2, 2, 1),
-    (2, 9, 16, 13, 11, 1, 3, 0),     # stride 3
-    (5, 8, 48, 5, 7, 1, 1, 0),       # tiles spanning several small images
+    (2, 13, 5, 9, 16, 2, 1, 0),      # Cin not a multiple of 8, Cout < 16
+    (1, 32, 64, 20, 20, 1, 1, 0),    # config-3 layer-4 shape (one image; 20 columns = 8 + 8 + 4)
+    (2, 8, 16, 7, 8, 3, 1, 1),       # n = 3
+    (4, 16, 32, 12, 12, 2, 2, 0),    # config-2 shape family, stride 2
+    (3, 16, 24, 11, 16, 2, 2, 1),
+    (2, 9, 16, 13, 12, 1, 3, 0),     # stride 3
+    (5, 8, 48, 5, 8, 1, 1, 0),       # tiles spanning several small images
+    (2, 16, 32, 11, 13, 2, 1, 1),    # odd width: the weight gradient takes the FFMA kernel
 ]
 
 
@@ -70,6 +71,15 @@ def test_tf32_conv_fwd_bwd_data(F, oracle, case):
     assert rel(np64(dx), dxr) <= TOL, "dgrad"
     dxm = F.conv2d_bwd_data(gd, wd, (H, W), n=n, stride=s, parity=pi, relu_y=xd)
     assert rel(np64(dxm), dxr * (x > 0)) <= TOL, "dgrad masked"
+    if (W * 4) % 16 == 0:  # the TMA-staged weight-gradient kernel needs 16-byte row pitch
+        assert F.conv_algo(B, Ci, Co, H, W, n, s, pi, torch.float32, "NCHW", 2) == "tcgen05-tf32"
+    _, dwr, dbr = oracle.conv2d_bwd(x, w, g, n=n, s=s, pi=pi, need=("dw", "db"))
+    dw, db = F.conv2d_bwd_weight(xd, gd, n=n, stride=s, parity=pi)
+    assert rel(np64(dw), dwr) <= TOL, "wgrad"
+    assert rel(np64(db), dbr) <= TOL, "dbias"
+    dw2, db2 = F.conv2d_bwd_weight(xd, gd, n=n, stride=s, parity=pi, dw=dw.clone(), dbias=db.clone(),
+                                   accumulate=True)
+    assert rel(np64(dw2), 2 * dwr) <= TOL and rel(np64(db2), 2 * dbr) <= TOL, "wgrad accumulate"
 
 
 def test_tf32_matches_ffma_path(F):
