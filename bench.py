@@ -385,8 +385,8 @@ def secondary_measurements(dev, peak_tf, peak_gbs):
         ("L4 relu bwd", lambda: relu_bwd(g4, t["y4"], t["dy4"])),
         ("L4 wgrad", lambda: F.conv2d_bwd_weight(t["p"], t["dy4"], n=1, dw=dws[2][0], dbias=dws[2][1])),
         ("L4 dgrad", lambda: F.conv2d_bwd_data(t["dy4"], ws[2], (H2, W2), n=1, out=t["dp"])),
-        ("pool bwd", lambda: F.pool2d_bwd(t["dp"], None, (H, W), n=1, stride=2, mode="avg", out=t["dy2u"])),
-        ("L2 relu bwd", lambda: relu_bwd(t["dy2u"], t["y2"], t["dy2"])),
+        ("pool bwd + L2 relu bwd", lambda: F.pool2d_bwd(t["dp"], None, (H, W), n=1, stride=2, mode="avg",
+                                                         out=t["dy2"], relu_y=t["y2"])),
         ("L2 wgrad", lambda: F.conv2d_bwd_weight(t["y1"], t["dy2"], n=2, dw=dws[1][0], dbias=dws[1][1])),
         ("L2 dgrad", lambda: F.conv2d_bwd_data(t["dy2"], ws[1], (H, W), n=2, relu_y=t["y1"], out=t["dy1"])),
         ("L1 wgrad", lambda: F.conv2d_bwd_weight(x, t["dy1"], n=1, dw=dws[0][0], dbias=dws[0][1])),
@@ -401,8 +401,7 @@ def secondary_measurements(dev, peak_tf, peak_gbs):
         "L4 relu bwd": (None, px2 * 64 * 4 * 3),
         "L4 wgrad": (2.0 * B * vt4 * 32 * 64, px2 * 4 * (32 + 64)),
         "L4 dgrad": (2.0 * B * vt4 * 32 * 64, px2 * 4 * (32 + 64)),
-        "pool bwd": (None, px2 * 32 * 4 + px * 32 * 4),
-        "L2 relu bwd": (None, px * 32 * 4 * 3),
+        "pool bwd + L2 relu bwd": (None, px2 * 32 * 4 + px * 32 * 4 * 2),
         "L2 wgrad": (2.0 * B * vt2 * 16 * 32, px * 4 * (16 + 32)),
         "L2 dgrad": (2.0 * B * vt2 * 16 * 32, px * 4 * (32 + 16 + 16)),
         "L1 wgrad": (2.0 * B * vt1 * 16, px * 4 * (1 + 16)),
@@ -420,7 +419,7 @@ def secondary_measurements(dev, peak_tf, peak_gbs):
         "ms_per_fwd_bwd_flushed": fl, "ms_per_fwd_bwd_hot": hot, "tflops": fl_all / (fl * 1e-3) / 1e12,
         "roofline_ms": t_roof * 1e3, "frac_of_roofline": t_roof / (fl * 1e-3), "frac_of_roofline_hot": t_roof / (hot * 1e-3),
         "passes": c3p,
-        "note": "whole fwd+bwd = one CUDA graph of the 12 library calls; per-pass entries are each pass's own graph "
+        "note": "whole fwd+bwd = one CUDA graph of the 11 library calls; per-pass entries are each pass's own graph "
                 "(flushed = L2 evicted before the pass, hot = back-to-back replays)"}
 
     # ---- C4: 128 x 256 -> 256, 64 x 64, bf16, n = 1 and 2: fwd / dgrad / wgrad (268 MB tensors > L2)

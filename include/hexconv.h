@@ -271,6 +271,15 @@ HEX_API hex_status_t hex_pool2d_bwd(const hex_pool2d_desc_t* desc, const void* d
  * Used by the data-parallel training step (BASELINE config 5).  Not part of
  * the paper's method; plain elementwise / reduction kernels. */
 
+/* Pool backward with the ReLU backward of the pooled layer fused:
+ *   dx = hex_pool2d_bwd(dy, argmax) * (relu_y > 0)
+ * relu_y: the pool's forward input (the post-ReLU activation), shaped like dx.
+ * Same arguments, layouts and errors as hex_pool2d_bwd; relu_y must not be
+ * NULL.  NCHW n = 1, stride 2 runs one kernel; other shapes run the pool
+ * backward and then the elementwise mask (hex_relu_bwd). */
+HEX_API hex_status_t hex_pool2d_bwd_relu(const hex_pool2d_desc_t* desc, const void* dy, const uint8_t* argmax_tap,
+                                         const void* relu_y, void* dx, hex_stream_t stream);
+
 /* Head of the C5 network, forward + backward in one launch:
  * feat bf16 NHWC [B][HW][C] (ReLU output) -> global average pool -> logits
  * [B][K] = gap @ wl^T + bl (wl fp32 [K][C], bl fp32 [K]) -> mean softmax

@@ -94,6 +94,7 @@ _SIGS = {
     "hex_conv3d_bwd_weight": (_i32, [_C3P, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
     "hex_pool2d_fwd": (_i32, [_PDP, _vp, _vp, _vp, _vp]),
     "hex_pool2d_bwd": (_i32, [_PDP, _vp, _vp, _vp, _vp]),
+    "hex_pool2d_bwd_relu": (_i32, [_PDP, _vp, _vp, _vp, _vp, _vp]),
     "hex_head_workspace_size": (_sz, [_i32, _i32, _i32]),
     "hex_head_fwd_bwd": (_i32, [_i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "hex_sgd_momentum": (_i32, [_i64, _vp, _vp, _vp, _f32, _f32, _f32, _vp, _vp]),

@@ -545,6 +545,27 @@ hex_status_t hex_pool2d_bwd(const hex_pool2d_desc_t* d, const void* dy, const ui
     return pool_bwd(a, (cudaStream_t)stream);
 }
 
+hex_status_t hex_pool2d_bwd_relu(const hex_pool2d_desc_t* d, const void* dy, const uint8_t* argmax_tap,
+                                 const void* relu_y, void* dx, hex_stream_t stream) {
+    Geom g;
+    hex_status_t st = pool_geom(d, &g);
+    if (st != HEX_OK) return st;
+    if (!dy || !dx || !relu_y) return HEX_ERR_INVALID_ARG;
+    if (d->mode == HEX_POOL_MAX && !argmax_tap) return HEX_ERR_INVALID_ARG;
+    PoolArgs a = make_pool(d, g);
+    if (d->dtype == HEX_BF16 && d->layout == HEX_NHWC && d->channels % 8 == 0) {
+        if (!aligned16(dy) || !aligned16(dx) || (argmax_tap && ((uintptr_t)argmax_tap & 7))) return HEX_ERR_ALIGNMENT;
+    }
+    a.dy = dy; a.argmax_in = argmax_tap; a.dx = dx;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (pool_plane_bwd_n1s2(a, relu_y, s)) {  // mask fused
+        count_launch();
+        return last_launch_status();
+    }
+    if ((st = pool_bwd(a, s)) != HEX_OK) return st;
+    return relu_bwd((int64_t)g.B * d->channels * g.H * g.W, d->dtype, dx, relu_y, dx, s);
+}
+
 size_t hex_head_workspace_size(int32_t B, int32_t K, int32_t C) {
     if (B < 1 || K < 1 || C < 1) return 0;
     return head_ws_bytes(B, K, C);

@@ -47,6 +47,12 @@ hex_status_t pool_tma_fwd(const PoolArgs& a, cudaStream_t st);
 bool pool_plane_fwd(const PoolArgs& a, cudaStream_t st);
 bool pool_plane_bwd(const PoolArgs& a, cudaStream_t st);
 hex_status_t pool_bwd(const PoolArgs& a, cudaStream_t st);
+// NCHW n = 1, stride 2 max / avg pool forward (pool_nchw.cu)
+bool pool_n1s2_nchw_supported(const PoolArgs& a);
+hex_status_t pool_n1s2_nchw_fwd(const PoolArgs& a, cudaStream_t st);
+// NCHW n = 1, stride 2 backward with the ReLU backward fused (dx *= relu_y > 0; relu_y may be null);
+// false when the shape is not covered (plane_kernels.cu)
+bool pool_plane_bwd_n1s2(const PoolArgs& a, const void* relu_y, cudaStream_t st);
 
 // tcgen05 implicit-GEMM path (bf16 NHWC, stride 1).
 struct TcConvArgs {

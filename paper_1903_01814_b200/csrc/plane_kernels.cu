@@ -176,9 +176,10 @@ pool_bwd_plane_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am, 
 // memory (neighbouring threads read neighbouring windows: coalesced, L1 reuse).
 // max: routed where the stored argmax equals the tap; avg: dy / in-grid count.
 // ---------------------------------------------------------------------------
-template <typename T, int P, int RHO, bool MAX>
+template <typename T, int P, int RHO, bool MAX, bool MASK>
 __device__ __forceinline__ void pool_bwd_blk_nchw(const T* __restrict__ dyp, const uint8_t* __restrict__ amp,
-                                                  T* __restrict__ dxp, const Geom& g, int Rp, int C) {
+                                                  const T* __restrict__ mp, T* __restrict__ dxp, const Geom& g,
+                                                  int Rp, int C) {
     float v[2][3];
     int a[2][3];
 #pragma unroll
@@ -218,48 +219,53 @@ __device__ __forceinline__ void pool_bwd_blk_nchw(const T* __restrict__ dyp, con
                 const float d = v[cd.dC][cd.dR + 1];
                 if (!MAX || a[cd.dC][cd.dR + 1] == cd.tap) acc += d;
             }
+            if (MASK && !(to_f32(__ldg(mp + r * g.W + c)) > 0.f)) acc = 0.f;
             dxp[r * g.W + c] = from_f32<T>(acc);
         }
     }
 }
 
-template <typename T, int P, bool MAX>
+template <typename T, int P, bool MAX, bool MASK>
 __global__ void __launch_bounds__(PL_THREADS)
-pool_bwd_n1s2_nchw_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am, T* __restrict__ dx, Geom g,
-                          int64_t planes) {
+pool_bwd_n1s2_nchw_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am, const T* __restrict__ relu_y,
+                          T* __restrict__ dx, Geom g) {
+    // grid: (block tiles of one plane, planes); thread = one 2x2 input block (even C first, then odd C)
     const int nC = g.Wo, nR = (g.H + 1) / 2;
     const int half = (nC + 1) >> 1;  // block columns: even C first, then odd C (rho warp-uniform)
-    const int64_t per_plane = (int64_t)nR * nC;
-    const int64_t total = planes * per_plane;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t pl = i / per_plane;
-        const int rem = (int)(i - pl * per_plane);
-        const int Rp = rem / nC, ci = rem - Rp * nC;
-        const int C = ci < half ? 2 * ci : 2 * (ci - half) + 1;
-        const T* dyp = dy + pl * g.Ho * g.Wo;
-        const uint8_t* amp = MAX ? am + pl * g.Ho * g.Wo : nullptr;
-        T* dxp = dx + pl * g.H * g.W;
-        if (C & 1) pool_bwd_blk_nchw<T, P, 1, MAX>(dyp, amp, dxp, g, Rp, C);
-        else pool_bwd_blk_nchw<T, P, 0, MAX>(dyp, amp, dxp, g, Rp, C);
-    }
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nR * nC) return;
+    const int64_t pl = blockIdx.y;
+    const int Rp = i / nC, ci = i - Rp * nC;
+    const int C = ci < half ? 2 * ci : 2 * (ci - half) + 1;
+    const T* dyp = dy + pl * g.Ho * g.Wo;
+    const uint8_t* amp = MAX ? am + pl * g.Ho * g.Wo : nullptr;
+    const T* mp = MASK ? relu_y + pl * g.H * g.W : nullptr;
+    T* dxp = dx + pl * g.H * g.W;
+    if (C & 1) pool_bwd_blk_nchw<T, P, 1, MAX, MASK>(dyp, amp, mp, dxp, g, Rp, C);
+    else pool_bwd_blk_nchw<T, P, 0, MAX, MASK>(dyp, amp, mp, dxp, g, Rp, C);
 }
 
 template <typename T>
-static void launch_bwd_n1s2(const PoolArgs& a, cudaStream_t st) {
+static bool launch_bwd_n1s2(const PoolArgs& a, const void* relu_y, cudaStream_t st) {
     const int64_t planes = (int64_t)a.g.B * a.C;
-    const int64_t total = planes * ((a.g.H + 1) / 2) * a.g.Wo;
-    int blocks = (int)((total + PL_THREADS - 1) / PL_THREADS);
-    if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+    if (planes > 65535) return false;
+    const int per_plane = ((a.g.H + 1) / 2) * a.g.Wo;
+    dim3 grid(ceil_div(per_plane, PL_THREADS), (unsigned)planes);
     const bool mx = a.mode == HEX_POOL_MAX;
     const T* dy = (const T*)a.dy;
+    const T* m = (const T*)relu_y;
     T* dx = (T*)a.dx;
+#define HEX_BW(PP, MX, MK) \
+    pool_bwd_n1s2_nchw_kernel<T, PP, MX, MK><<<grid, PL_THREADS, 0, st>>>(dy, MX ? a.argmax_in : nullptr, m, dx, a.g)
     if (a.g.parity & 1) {
-        if (mx) pool_bwd_n1s2_nchw_kernel<T, 1, true><<<blocks, PL_THREADS, 0, st>>>(dy, a.argmax_in, dx, a.g, planes);
-        else pool_bwd_n1s2_nchw_kernel<T, 1, false><<<blocks, PL_THREADS, 0, st>>>(dy, nullptr, dx, a.g, planes);
+        if (mx) { if (m) HEX_BW(1, true, true); else HEX_BW(1, true, false); }
+        else { if (m) HEX_BW(1, false, true); else HEX_BW(1, false, false); }
     } else {
-        if (mx) pool_bwd_n1s2_nchw_kernel<T, 0, true><<<blocks, PL_THREADS, 0, st>>>(dy, a.argmax_in, dx, a.g, planes);
-        else pool_bwd_n1s2_nchw_kernel<T, 0, false><<<blocks, PL_THREADS, 0, st>>>(dy, nullptr, dx, a.g, planes);
+        if (mx) { if (m) HEX_BW(0, true, true); else HEX_BW(0, true, false); }
+        else { if (m) HEX_BW(0, false, true); else HEX_BW(0, false, false); }
     }
+#undef HEX_BW
+    return true;
 }
 
 static bool plane_pool_ok(const PoolArgs& a) {
@@ -312,13 +318,16 @@ bool pool_plane_fwd(const PoolArgs& a, cudaStream_t st) {
     return true;
 }
 
+bool pool_plane_bwd_n1s2(const PoolArgs& a, const void* relu_y, cudaStream_t st) {
+    if (a.layout != HEX_NCHW || a.g.n != 1 || a.g.s != 2 || a.mode == HEX_POOL_AVG_PAD ||
+        !(a.g.parity == 0 || a.g.parity == 1) || sw_on("HEXCONV_NO_PLANE"))
+        return false;
+    return a.dtype == HEX_F32 ? launch_bwd_n1s2<float>(a, relu_y, st) : launch_bwd_n1s2<__nv_bfloat16>(a, relu_y, st);
+}
+
 bool pool_plane_bwd(const PoolArgs& a, cudaStream_t st) {
     if (!plane_pool_ok(a)) return false;
-    if (a.g.n == 1 && a.g.s == 2 && (a.g.parity == 0 || a.g.parity == 1)) {
-        if (a.dtype == HEX_F32) launch_bwd_n1s2<float>(a, st);
-        else launch_bwd_n1s2<__nv_bfloat16>(a, st);
-        return true;
-    }
+    if (pool_plane_bwd_n1s2(a, nullptr, st)) return true;
     if (a.dtype == HEX_F32) dispatch_plane<float>(a, st, false);
     else dispatch_plane<__nv_bfloat16>(a, st, false);
     return true;

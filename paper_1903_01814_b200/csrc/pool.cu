@@ -852,6 +852,8 @@ hex_status_t pool_fwd(const PoolArgs& a, cudaStream_t st) {
                 (const __nv_bfloat16*)a.x, (__nv_bfloat16*)a.y, nullptr, a.g, a.C, a.sx, a.sy, a.mode, cf);
     } else if (pool_tma_fwd_supported(a)) {
         return pool_tma_fwd(a, st);
+    } else if (pool_n1s2_nchw_supported(a)) {
+        return pool_n1s2_nchw_fwd(a, st);
     } else if (use_spec(a) && dispatch_wide(a, st, true)) {
     } else if (use_spec(a)) {
         if (a.g.n == 1) { if (a.g.s == 1) launch_spec_fwd<1, 1>(a, st); else launch_spec_fwd<1, 2>(a, st); }

@@ -206,9 +206,22 @@ __global__ void relu_bwd_kernel(int64_t n, const T* __restrict__ dy, const T* __
     if (i < n) dx[i] = (float)y[i] > 0.f ? dy[i] : T(0.f);
 }
 
+__global__ void relu_bwd_f32x4_kernel(int64_t n4, const float4* __restrict__ dy, const float4* __restrict__ y,
+                                      float4* __restrict__ dx) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 g = __ldg(dy + i), v = __ldg(y + i);
+        dx[i] = make_float4(v.x > 0.f ? g.x : 0.f, v.y > 0.f ? g.y : 0.f, v.z > 0.f ? g.z : 0.f, v.w > 0.f ? g.w : 0.f);
+    }
+}
+
 hex_status_t relu_bwd(int64_t n, int dtype, const void* dy, const void* y, void* dx, cudaStream_t st) {
     if (n == 0) return HEX_OK;
-    if (dtype == HEX_F32)
+    if (dtype == HEX_F32 && (n & 3) == 0 && (((uintptr_t)dy | (uintptr_t)y | (uintptr_t)dx) & 15) == 0) {
+        const int64_t n4 = n >> 2;
+        int blocks = ceil_div(n4, 256);
+        if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+        relu_bwd_f32x4_kernel<<<blocks, 256, 0, st>>>(n4, (const float4*)dy, (const float4*)y, (float4*)dx);
+    } else if (dtype == HEX_F32)
         relu_bwd_kernel<float><<<ceil_div(n, 256), 256, 0, st>>>(n, (const float*)dy, (const float*)y, (float*)dx);
     else
         relu_bwd_kernel<__nv_bfloat16><<<ceil_div(n, 256), 256, 0, st>>>(

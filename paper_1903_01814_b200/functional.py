@@ -379,8 +379,10 @@ def pool2d_fwd(x, n: int = 1, stride: int = 1, parity: int = 0, mode: str = "max
 
 
 def pool2d_bwd(dy, argmax, in_hw, n: int = 1, stride: int = 1, parity: int = 0, mode: str = "max",
-               layout: str = "NCHW", out=None):
-    _check_cuda(dy, argmax, out)
+               layout: str = "NCHW", out=None, relu_y=None):
+    """dx of the pool; with relu_y (the pool's post-ReLU input) the ReLU backward is
+    fused: dx *= (relu_y > 0)."""
+    _check_cuda(dy, argmax, out, relu_y)
     B, C, Ho, Wo = _dims(dy, layout)
     _dtype_ok(dy)
     H, W = in_hw
@@ -394,6 +396,11 @@ def pool2d_bwd(dy, argmax, in_hw, n: int = 1, stride: int = 1, parity: int = 0, 
     if out is None:
         out = torch.empty(_shape(layout, B, C, H, W), dtype=dy.dtype, device=dy.device)
     _expect(out, _shape(layout, B, C, H, W), dy.dtype, "out")
+    if relu_y is not None:
+        _expect(relu_y, _shape(layout, B, C, H, W), dy.dtype, "relu_y")
+        A.check(A.lib().hex_pool2d_bwd_relu(ctypes.byref(d), _ptr(dy), _ptr(argmax), _ptr(relu_y), _ptr(out),
+                                            _stream()), "hex_pool2d_bwd_relu")
+        return out
     A.check(A.lib().hex_pool2d_bwd(ctypes.byref(d), _ptr(dy), _ptr(argmax), _ptr(out), _stream()),
             "hex_pool2d_bwd")
     return out

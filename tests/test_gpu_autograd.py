@@ -139,3 +139,25 @@ def test_wrappers_reject_mismatched_shapes(F):
         F.pool2d_bwd(y, am[..., :-1].contiguous(), (8, 9), n=1, stride=2)
     with pytest.raises(ValueError):
         F.pool2d_bwd(y, None, (8, 9), n=1, stride=2, mode="max")
+
+
+@pytest.mark.parametrize("mode", ["max", "avg"])
+@pytest.mark.parametrize("pi", [0, 1])
+@pytest.mark.parametrize("layout,dtype", [("NCHW", torch.float32), ("NHWC", torch.bfloat16)])
+def test_pool_bwd_fused_relu_mask(F, oracle, mode, pi, layout, dtype):
+    # hex_pool2d_bwd_relu: dx = pool_bwd(dy) * (relu_y > 0) (fused for NCHW n = 1 s = 2, two passes otherwise)
+    import synth
+    B, C, H, W = 2, 16, 13, 12
+    x = synth.round_bf16(synth.normal((B, C, H, W), 14)) if dtype == torch.bfloat16 else \
+        synth.round_f32(synth.normal((B, C, H, W), 14))
+    Ho, Wo, _ = F.output_shape(H, W, 2, pi)
+    g = synth.round_bf16(synth.normal((B, C, Ho, Wo), 15)) if dtype == torch.bfloat16 else \
+        synth.round_f32(synth.normal((B, C, Ho, Wo), 15))
+    to = (lambda a: dev(a, dtype).permute(0, 2, 3, 1).contiguous()) if layout == "NHWC" else (lambda a: dev(a, dtype))
+    back = (lambda t: np64(t).transpose(0, 3, 1, 2)) if layout == "NHWC" else np64
+    xd = to(x)
+    y, am = F.pool2d_fwd(xd, n=1, stride=2, parity=pi, mode=mode, layout=layout)
+    _, amr = oracle.pool2d_fwd(x, n=1, s=2, pi=pi, mode=mode)
+    dx = F.pool2d_bwd(to(g), am, (H, W), n=1, stride=2, parity=pi, mode=mode, layout=layout, relu_y=xd)
+    ref = oracle.pool2d_bwd(g, amr, H, W, n=1, s=2, pi=pi, mode=mode) * (x > 0)
+    assert rel(back(dx), ref) <= (1e-5 if dtype == torch.float32 else 2e-2)
