@@ -527,7 +527,7 @@ hex_status_t tf32_conv(const Geom& g, int Cin, int Cout, int mode, const float* 
 // Weight gradient (+ dbias) in 3xTF32:  dW[co][ci][t] = sum_{b,o} dy[b][co][o] * x[b][ci][centre(o) + off_t]
 // (the adjoint of the forward with respect to the weights).
 //
-// GEMM view: M = (t, ci) rows (m = t * Cin + ci, up to 3 M-tiles of 128), N = Cout (padded to 16, <= 64),
+// GEMM view: M = (ci, t) rows (m = ci * T + t, up to 3 M-tiles of 128), N = Cout (padded to 16, <= 64),
 // K = output pixels.  A K-step is 8 consecutive output pixels of one output row (b, R): C0 .. C0+7.
 //   * The x rows an output row needs (all Cin channels, every tap's row, W + 2n columns with zero halo)
 //     are staged as one TMA box per output row ("band", OOB rows / columns zero-filled), double-buffered.
@@ -660,104 +660,124 @@ tf32_wgrad_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_consta
             ptx::mma_commit(dfull);
         }
     } else if (warp >= 4) {
-        // A builders: warp index within the group -> (M-tile, lane quadrant = warp % 4)
+        // A builders: warp index within the group -> (M-tile, lane quadrant = warp % 4).  Row m = ci * T + t
+        // (channel-major: the 32 lanes of a warp are mostly the taps of one channel, whose band addresses
+        // differ by the tap offsets -- spread over the banks -- instead of 16 channel planes 4 x odd words
+        // apart).
         const int wi = warp - 4, g = wi / (4 * MT), wg = wi - g * 4 * MT;
         const int mt = wg >> 2, q = warp & 3;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const int m = mt * 128 + q * 32 + lane;
         const bool mvalid = m < p.Mrows;
-        const int t = mvalid ? m / p.Cin : 0, ci = mvalid ? m - t * p.Cin : 0;
-        const int dct = p.dc[t];
-        const int plane = p.NR * p.BW;
+        const int ci = mvalid ? m / p.T : 0, t = mvalid ? m - ci * p.T : 0;
+        const int ss = S ? S : p.s;
+        // band offsets of this row's 8 values, per centre-column parity cp of C = C0 + cp (C0 is a multiple of
+        // 8 and rho has period 2, so they do not depend on C0 beyond the + ss * C0 column shift):
+        //   value k of a K-step sits at  off[k & 1] + ss * (C0 + k)
+        int off[2];
+#pragma unroll
+        for (int cp = 0; cp < 2; ++cp) {
+            const int pc = (ss * cp + p.parity) & 1;
+            const int srow = hex_rho(cp, ss, p.parity) + (pc ? p.dr1[t] : p.dr0[t]) - p.rmin;
+            off[cp] = ci * p.NR * p.BW + srow * p.BW + p.dc[t] + WG_HL;
+        }
         // B role: thread bi of the group (bi < 2 NT) loads dy[b][co = bi / 2][R][C0 + 4 (bi & 1) .. + 3] of the
         // group's K-steps, one K-step ahead, splits it and writes its half row of the SW32 hi / lo blocks;
         // it also sums those dy values for dbias
         const int bi = wg * 32 + lane, bn = bi >> 1, bh = bi & 1;
         const bool brole = bi < 2 * NT, bload_ok = brole && bn < p.Cout;
         const bool vec = (p.Wo & 3) == 0 && ((uintptr_t)p.dy & 15) == 0;
+        const int boff = bn * 32 + ((bh ^ ((bn >> 2) & 1)) << 4);  // SW32 chunk of this thread's half row
         float bsum = 0.f;
-        auto bload = [&](int kgx, float* v) {
+        // the group's K-steps kg = g, g + WG_G, ...: (row r, column block j) walked without division
+        int r = 0, j = g;
+        while (j >= p.cblk && r < nrows) { j -= p.cblk; ++r; }
+        auto dy_row = [&](int rr) -> const float* {
+            const int row = row0 + rr, b = row / p.Ho, R = row - b * p.Ho;
+            return p.dy + ((size_t)(b * p.Cout + (bload_ok ? bn : 0)) * p.Ho + R) * p.Wo + 4 * bh;
+        };
+        auto bload = [&](const float* rowp, int C0, float* v) {
             v[0] = v[1] = v[2] = v[3] = 0.f;
-            if (!bload_ok || kgx >= nk) return;
-            const int rx = kgx / p.cblk, C0 = (kgx - rx * p.cblk) * 8 + 4 * bh;
-            const int row = row0 + rx, b = row / p.Ho, R = row - b * p.Ho;
-            const float* src = p.dy + ((size_t)(b * p.Cout + bn) * p.Ho + R) * p.Wo + C0;
-            if (vec && C0 + 4 <= p.Wo) {
+            if (!bload_ok) return;
+            const float* src = rowp + C0;
+            if (vec && C0 + 4 * bh + 4 <= p.Wo) {
                 const float4 a = __ldg(reinterpret_cast<const float4*>(src));
                 v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
             } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) v[k] = C0 + k < p.Wo ? __ldg(src + k) : 0.f;
+                for (int k = 0; k < 4; ++k) v[k] = C0 + 4 * bh + k < p.Wo ? __ldg(src + k) : 0.f;
             }
         };
-        float bnext[4];
-        bload(g, bnext);
-        int kg = 0;
-        for (int r = 0; r < nrows; ++r) {
-            const int buf = r & 1;
+        float bnext[4] = {0.f, 0.f, 0.f, 0.f};
+        if (r < nrows) bload(dy_row(r), j * 8, bnext);
+        int cur_r = -1;
+        const float* bx = band;
+        for (int kg = g; r < nrows; kg += WG_G) {
             PROF_T0();
-            ptx::mbar_wait(&xfull[buf], (r >> 1) & 1);
-            PROF_ACC(6);
-            const int row = row0 + r, R = row - (row / p.Ho) * p.Ho;
-            const float* bx = band + buf * band_elems + ci * plane;
-            for (int j = 0; j < p.cblk; ++j, ++kg) {
-                if (kg % WG_G != g) continue;
-                const int C0 = j * 8;
-                const int ss = S ? S : p.s;
-                // the two column parities of the centres: base addresses into the band
-                int bse[2];
-#pragma unroll
-                for (int cp = 0; cp < 2; ++cp) {
-                    const int C = C0 + cp;
-                    const int rc = hex_rho(C, ss, p.parity) + ss * R, cc = ss * C;
-                    const int pc = (cc + p.parity) & 1;
-                    const int srow = rc + (pc ? p.dr1[t] : p.dr0[t]) - (ss * R + p.rmin);
-                    bse[cp] = srow * p.BW + cc + dct + WG_HL - cp * ss;
+            if (r != cur_r) {  // entering row r: release the bands of the rows passed, wait for row r's
+                // (a row is released only after its band was seen loaded, so an arrival always counts toward
+                // that row's phase of the empty barrier -- also for rows this group had no K-step in)
+                for (int rr = cur_r < 0 ? 0 : cur_r; rr < r; ++rr) {
+                    if (rr > cur_r) ptx::mbar_wait(&xfull[rr & 1], (rr >> 1) & 1);
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&xempty[rr & 1]);
                 }
-                const int nv = min(8, p.Wo - C0);
-                uint32_t hi[8], lo[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const float u = (mvalid && k < nv) ? bx[bse[k & 1] + ss * k] : 0.f;
-                    const float h = tf32_rna(u);
-                    hi[k] = __float_as_uint(h);
-                    lo[k] = __float_as_uint(u - h);
-                }
-                float bv[4] = {bnext[0], bnext[1], bnext[2], bnext[3]};
-                bload(kg + WG_G, bnext);  // this group's next K-step
-                const int st = kg % STAGES;
-                PROF_ACC(7);
-                ptx::mbar_wait(&empty[st], ((kg / STAGES) & 1) ^ 1);
-                PROF_ACC(8);
-                ptx::tc_fence_after();
-                const uint32_t ta = tm + lane_base + Cfg::ACC + (st * MT + mt) * 16;
-                if (!WG_SKIP(1)) {
-                    tmem_st8(ta, hi);
-                    tmem_st8(ta + 8, lo);
-                }
-                if (brole) {
-                    float bhv[4], blv[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        bsum += bv[k];
-                        bhv[k] = tf32_rna(bv[k]);
-                        blv[k] = bv[k] - bhv[k];
-                    }
-                    // SW32 K-major: 16-byte chunk c of row n at n * 32 + ((c ^ ((n >> 2) & 1)) * 16)
-                    uint8_t* blk = bsm + st * Cfg::BBYTES;
-                    const int off = bn * 32 + ((bh ^ ((bn >> 2) & 1)) << 4);
-                    *reinterpret_cast<float4*>(blk + off) = make_float4(bhv[0], bhv[1], bhv[2], bhv[3]);
-                    *reinterpret_cast<float4*>(blk + NT * 32 + off) = make_float4(blv[0], blv[1], blv[2], blv[3]);
-                    ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
-                }
-                if (!WG_SKIP(1)) tmem_st_wait();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&full[st]);
-                PROF_ACC(9);
+                ptx::mbar_wait(&xfull[r & 1], (r >> 1) & 1);
+                PROF_ACC(6);
+                cur_r = r;
+                bx = band + (r & 1) * band_elems;
             }
+            const int C0 = j * 8;
+            const int nv = min(8, p.Wo - C0);
+            uint32_t hi[8], lo[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float u = (mvalid && k < nv) ? bx[off[k & 1] + ss * (C0 + k)] : 0.f;
+                const float h = tf32_rna(u);
+                hi[k] = __float_as_uint(h);
+                lo[k] = __float_as_uint(u - h);
+            }
+            // advance to the group's next K-step and prefetch its dy
+            int nr = r, nj = j + WG_G;
+            while (nj >= p.cblk && nr < nrows) { nj -= p.cblk; ++nr; }
+            float bv[4] = {bnext[0], bnext[1], bnext[2], bnext[3]};
+            if (nr < nrows) bload(dy_row(nr), nj * 8, bnext);
+            const int st = kg % STAGES;
+            PROF_ACC(7);
+            ptx::mbar_wait(&empty[st], ((kg / STAGES) & 1) ^ 1);
+            PROF_ACC(8);
+            ptx::tc_fence_after();
+            const uint32_t ta = tm + lane_base + Cfg::ACC + (st * MT + mt) * 16;
+            if (!WG_SKIP(1)) {
+                tmem_st8(ta, hi);
+                tmem_st8(ta + 8, lo);
+            }
+            if (brole) {
+                float bhv[4], blv[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    bsum += bv[k];
+                    bhv[k] = tf32_rna(bv[k]);
+                    blv[k] = bv[k] - bhv[k];
+                }
+                uint8_t* blk = bsm + st * Cfg::BBYTES;
+                *reinterpret_cast<float4*>(blk + boff) = make_float4(bhv[0], bhv[1], bhv[2], bhv[3]);
+                *reinterpret_cast<float4*>(blk + NT * 32 + boff) = make_float4(blv[0], blv[1], blv[2], blv[3]);
+                ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
+            }
+            if (!WG_SKIP(1)) tmem_st_wait();
+            ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&xempty[buf]);  // done with this row's band
+            if (lane == 0) ptx::mbar_arrive(&full[st]);
+            PROF_ACC(9);
+            r = nr;
+            j = nj;
+        }
+        // release the bands of the remaining rows (including ones this group had no K-step in)
+        for (int rr = cur_r < 0 ? 0 : cur_r; rr < nrows; ++rr) {
+            if (rr > cur_r) ptx::mbar_wait(&xfull[rr & 1], (rr >> 1) & 1);
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&xempty[rr & 1]);
         }
         if (brole) bpart[g * 2 * NT + bi] = bsum;
     } else {
@@ -806,7 +826,7 @@ tf32_wgrad_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_consta
     }
 }
 
-// dw[co][ci][t] (+)= sum_c part[c][co][t * Cin + ci]; dbias[co] (+)= sum_c part_b[c][co]  (fixed order)
+// dw[co][ci][t] (+)= sum_c part[c][co][ci * T + t]; dbias[co] (+)= sum_c part_b[c][co]  (fixed order)
 __global__ void tf32_wgrad_reduce_kernel(const float* __restrict__ part, const float* __restrict__ part_b, int nparts,
                                          int Cout, int Cin, int T, float* __restrict__ dw, float* __restrict__ dbias,
                                          int accumulate) {
@@ -814,16 +834,17 @@ __global__ void tf32_wgrad_reduce_kernel(const float* __restrict__ part, const f
     const int total = Cout * Mrows;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total + Cout; e += gridDim.x * blockDim.x) {
         if (e < total) {
-            const int co = e / Mrows, mm = e - co * Mrows;
-            float acc = 0.f;
-            for (int c = 0; c < nparts; ++c) acc += part[(size_t)c * total + e];
-            const int t = mm / Cin, ci = mm - t * Cin;
-            float* o = dw + ((size_t)co * Cin + ci) * T + t;
+            const int co = e / Mrows, mm = e - co * Mrows;  // mm = ci * T + t: dw's own [ci][t] order
+            float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int c = 0; c < nparts; ++c) s8[c & 7] += part[(size_t)c * total + e];
+            const float acc = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+            float* o = dw + (size_t)co * Mrows + mm;
             *o = accumulate ? *o + acc : acc;
         } else if (dbias) {
             const int co = e - total;
-            float acc = 0.f;
-            for (int c = 0; c < nparts; ++c) acc += part_b[(size_t)c * Cout + co];
+            float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int c = 0; c < nparts; ++c) s8[c & 7] += part_b[(size_t)c * Cout + co];
+            const float acc = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
             dbias[co] = accumulate ? dbias[co] + acc : acc;
         }
     }
