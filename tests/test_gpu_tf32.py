@@ -104,3 +104,4 @@ def test_tf32_deterministic(F):
     a = F.conv2d_fwd(x, w, None, n=1)
     b = F.conv2d_fwd(x, w, None, n=1)
     assert torch.equal(a, b)
+

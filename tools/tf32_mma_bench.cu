@@ -38,6 +38,28 @@ __global__ void bench(long long* cycles, int iters) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tm = tslot;
+    if (MODE == 5 && tid >= 32) {  // warps 1-3: continuous tcgen05.st traffic to other TMEM columns
+        const int w = tid / 32;
+        uint32_t v[8] = {1, 2, 3, 4, 5, 6, 7, 8};
+        for (int it = 0; it < iters * 4; ++it) {
+            const uint32_t ta = tm + ((uint32_t)(w * 32) << 16) + 320 + (it & 7) * 16;
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(v[0]),
+                         "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta + 8), "r"(v[0]),
+                         "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+    }
+    if (MODE == 4 && tid == 32) {  // a second issuing warp on its own accumulator (columns 256..)
+        constexpr uint32_t idesc = idesc_tf32(128, N);
+        const uint64_t bd = desc_sw32(smem_u32(bsm));
+        for (int it = 0; it < iters; ++it)
+#pragma unroll
+            for (int a = 0; a < NACC; ++a)
+                asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;}"
+                             ::"r"(tm + 256 + a * N), "r"(tm + 496), "l"(bd), "r"(idesc), "r"(1));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar2)));
+    }
     if (tid == 0) {
         constexpr uint32_t idesc = idesc_tf32(128, N);
         const uint64_t bd = desc_sw32(smem_u32(bsm));
@@ -45,12 +67,12 @@ __global__ void bench(long long* cycles, int iters) {
         const uint32_t a_t = tm + 480;  // A in TMEM columns 480..487 (contents irrelevant for timing)
         long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
-            if constexpr (MODE >= 1) {  // the kernel's per-K-step handshake: wait on a barrier, fence
+            if constexpr (MODE >= 1 && MODE != 4) {  // the kernel's per-K-step handshake: wait on a barrier, fence
                 asm volatile("{.reg .pred P1; W2: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 1; @!P1 bra W2;}" ::"r"(
                     smem_u32(&bar)));
                 asm volatile("tcgen05.fence::after_thread_sync;");
             }
-            if constexpr (MODE == 3) {
+            if constexpr (MODE == 3 || MODE == 5) {
                 constexpr uint32_t id2 = idesc_tf32(128, 2 * N), id1 = idesc_tf32(128, N);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
@@ -62,7 +84,7 @@ __global__ void bench(long long* cycles, int iters) {
                 }
             }
 #pragma unroll
-            for (int a = 0; a < (MODE == 3 ? 0 : NACC); ++a) {
+            for (int a = 0; a < (MODE == 3 || MODE == 5 ? 0 : NACC); ++a) {
                 const uint32_t d = tm + a * N;
                 if constexpr (A_TMEM)
                     asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;}"
@@ -71,7 +93,7 @@ __global__ void bench(long long* cycles, int iters) {
                     asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;}"
                                  ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(1));
             }
-            if constexpr (MODE >= 2)  // commit to a second barrier every iteration
+            if constexpr (MODE >= 2 && MODE != 4)  // commit to a second barrier every iteration
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                     smem_u32(&bar2)));
         }
@@ -107,5 +129,7 @@ int main() {
     run<32, 1, false>(); run<32, 4, false>(); run<64, 4, false>(); run<16, 8, false>();
     run<32, 3, true, 1>(); run<32, 3, true, 2>(); run<64, 3, true, 2>(); run<32, 6, true, 2>();
     run<32, 8, true, 3>(); run<16, 8, true, 3>(); run<64, 8, true, 3>();
+    run<32, 2, true, 4>(); run<64, 2, true, 4>(); run<16, 2, true, 4>();
+    run<32, 8, true, 5>(); run<64, 8, true, 5>();
     return 0;
 }
