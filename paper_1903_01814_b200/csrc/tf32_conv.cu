@@ -74,16 +74,30 @@ constexpr int TF_MAXT = 37;                        // n <= 3
 constexpr int TF_MAX_NT = 64;
 constexpr int TF_SMEM_MAX = 220 * 1024;
 
+constexpr int TF_MAXCLS = 18;   // 2 s^2 phase classes, s <= 3
+constexpr int TF_MAXKL = 2048;  // K-step list entries over all classes
+struct TfClass {
+    int cr, ccl;          // r mod s, c mod 2s of the class's pixels
+    int nr, nc;           // its rows / columns per image
+    int tile0, k0, kn;    // first tile, first K-step list entry, K-steps
+};
+
 struct TfParams {
     const float* x;       // gathered tensor, NCHW [B][Cx][Hin][Win]
     const float* bias;    // [Nout] or null
     const float* relu_y;  // mask source shaped like y, or null
     float* y;             // output, NCHW [B][Nout][Hout][Wout]
-    int Cx, H, W, Hin, Win, Hout, Wout;
+    int B, Cx, H, W, Hin, Win, Hout, Wout;
     int Nout, s, parity, T, kc8, ksteps, relu;
     int out_lat, in_lat;  // output pixels are lattice points / the gathered tensor lives on the lattice
     int total_pix, tiles;
     int8_t dc[TF_MAXT], dr0[TF_MAXT], dr1[TF_MAXT];
+    // strided bwd-data (in_lat): the output pixels are split into the 2 s^2 phase classes (r mod s, c mod 2s);
+    // within a class the taps whose neighbour is a lattice centre are the same for every pixel, so a tile
+    // (one class) runs only those K-steps -- s^2 times fewer MMAs than gathering every tap
+    int ncls;
+    TfClass cls[TF_MAXCLS];
+    uint16_t klist[TF_MAXKL];  // per class, its K-steps: tap | chunk << 8
 };
 
 __device__ __forceinline__ float tf32_rna(float v) {
@@ -163,14 +177,64 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
     uint64_t* tempty = tfull + 2;
     uint64_t* wbar = tempty + 2;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(wbar + 1);
-    // per K-step gather entry: dc | dr(centre parity 0) << 8 | dr(parity 1) << 16 | chunk << 24
+    // per K-step gather entry: dc | dr(centre parity 0) << 8 | dr(parity 1) << 16 | chunk << 24, and (phase
+    // classes) the K-step's weight block t * kc8 + chunk
     uint32_t* ktab = tslot + 4;
-    for (int ks = threadIdx.x; ks < p.ksteps; ks += blockDim.x) {
-        const int t = ks / p.kc8, c8 = ks - t * p.kc8;
-        ktab[ks] = (uint32_t)(uint8_t)p.dc[t] | ((uint32_t)(uint8_t)p.dr0[t] << 8) |
-                   ((uint32_t)(uint8_t)p.dr1[t] << 16) | ((uint32_t)c8 << 24);
+    const int nkt = IN_LAT ? p.cls[p.ncls - 1].k0 + p.cls[p.ncls - 1].kn : p.ksteps;
+    uint16_t* wtab = reinterpret_cast<uint16_t*>(ktab + nkt);
+    for (int i = threadIdx.x; i < nkt; i += blockDim.x) {
+        int t, c8;
+        if (IN_LAT) {
+            t = p.klist[i] & 0xFF;
+            c8 = p.klist[i] >> 8;
+        } else {
+            t = i / p.kc8;
+            c8 = i - t * p.kc8;
+        }
+        ktab[i] = (uint32_t)(uint8_t)p.dc[t] | ((uint32_t)(uint8_t)p.dr0[t] << 8) |
+                  ((uint32_t)(uint8_t)p.dr1[t] << 16) | ((uint32_t)c8 << 24);
+        wtab[i] = (uint16_t)(t * p.kc8 + c8);
     }
-    const int tstages = (p.ksteps + TF_KPS - 1) / TF_KPS;  // A stages per tile
+    // tile -> (K-step list offset, K-steps, A stages); one class of output pixels per tile (IN_LAT)
+    auto tile_class = [&](int tile) -> int {
+        int c = 0;
+        if (IN_LAT)
+            while (c + 1 < p.ncls && tile >= p.cls[c + 1].tile0) ++c;
+        return c;
+    };
+    auto tile_k = [&](int tile, int* k0, int* kn) {
+        if (IN_LAT) {
+            const TfClass& cl = p.cls[tile_class(tile)];
+            *k0 = cl.k0;
+            *kn = cl.kn;
+        } else {
+            *k0 = 0;
+            *kn = p.ksteps;
+        }
+    };
+    auto tile_stages = [&](int tile) {
+        int k0, kn;
+        tile_k(tile, &k0, &kn);
+        return (kn + TF_KPS - 1) / TF_KPS;
+    };
+    // output pixel of TMEM lane `row` of `tile`: image b, offset rem in the output plane, centre (rc, cc)
+    auto tile_pixel = [&](int tile, int row, int* b, int* rem, int* rc, int* cc) -> bool {
+        if (!IN_LAT) {
+            const int pix = tile * 128 + row;
+            if (pix >= p.total_pix) return false;
+            pixel_centre(p, pix, b, rem, rc, cc);
+            return true;
+        }
+        const TfClass& cl = p.cls[tile_class(tile)];
+        const int idx = (tile - cl.tile0) * 128 + row, per = cl.nr * cl.nc;
+        if (idx >= p.B * per) return false;
+        *b = idx / per;
+        const int r2 = idx - *b * per, i = r2 / cl.nc, j = r2 - i * cl.nc;
+        *rc = cl.cr + p.s * i;
+        *cc = cl.ccl + 2 * p.s * j;
+        *rem = *rc * p.Wout + *cc;
+        return true;
+    };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #if TF_PROF
@@ -213,9 +277,12 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
                 ptx::mbar_wait(&tempty[acc], aphase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tm + acc * 2 * NT;
+                int k0, kn;
+                tile_k(tile, &k0, &kn);
+                const int tst = (kn + TF_KPS - 1) / TF_KPS;
                 uint64_t bd = bdesc0;
                 int ks = 0;
-                for (int js = 0; js < tstages; ++js, ++sglob) {
+                for (int js = 0; js < tst; ++js, ++sglob) {
                     const int st = sglob & (TF_STAGES - 1);
                     PROF_T0();
                     ptx::mbar_wait(&full[st], (sglob / TF_STAGES) & 1);
@@ -224,7 +291,8 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
                     const uint32_t a0 = tm + ACC_COLS + st * STAGE_COLS;
 #pragma unroll
                     for (int kk = 0; kk < TF_KPS; ++kk) {
-                        if (ks < p.ksteps) {
+                        if (ks < kn) {
+                            if (IN_LAT) bd = bdesc0 + (uint64_t)wtab[k0 + ks] * BSTEP;
                             mma_tf32_ts(d, a0 + 16 * kk, bd, idesc2, ks > 0 ? 1u : 0u);
                             mma_tf32_ts(d, a0 + 16 * kk + 8, bd, idesc1, 1u);
                         }
@@ -249,23 +317,23 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const int hw_in = p.Hin * p.Win;
         int sglob = g, js = g, tile = blockIdx.x;
-        while (js >= tstages && tile < p.tiles) {
-            js -= tstages;
+        while (tile < p.tiles && js >= tile_stages(tile)) {
+            js -= tile_stages(tile);
             tile += gridDim.x;
         }
-        int cur_tile = -1, pc = 0, rc = 0, cc = 0;
+        int cur_tile = -1, pc = 0, rc = 0, cc = 0, k0 = 0, kn = 0;
         bool valid = false;
         const float* xb = p.x;
         for (; tile < p.tiles; sglob += TF_GROUPS) {
             if (tile != cur_tile) {
                 cur_tile = tile;
-                const int pix = tile * 128 + q * 32 + lane;
-                valid = pix < p.total_pix;
                 int b = 0, rem = 0;
                 rc = cc = 0;
-                if (valid) pixel_centre(p, pix, &b, &rem, &rc, &cc);
+                valid = tile_pixel(tile, q * 32 + lane, &b, &rem, &rc, &cc);
+                if (!valid) b = 0;
                 pc = (cc + p.parity) & 1;
                 xb = p.x + (size_t)b * p.Cx * hw_in;
+                tile_k(tile, &k0, &kn);
             }
             PROF_T0();
             const int ks0 = js * TF_KPS;
@@ -273,8 +341,8 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
 #pragma unroll
             for (int kk = 0; kk < TF_KPS; ++kk) {
                 const int ks = ks0 + kk;
-                const bool in_k = ks < p.ksteps;
-                const uint32_t e = ktab[in_k ? ks : 0];
+                const bool in_k = ks < kn;
+                const uint32_t e = ktab[k0 + (in_k ? ks : 0)];
                 const int dc = (int8_t)(e & 0xFF), dr = (int8_t)((pc ? e >> 16 : e >> 8) & 0xFF);
                 const int c0 = (int)(e >> 24) * 8;
                 const int qr = rc + dr, qc = cc + dc;
@@ -326,8 +394,8 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
             if (lane == 0) ptx::mbar_arrive(&full[st]);
             PROF_ACC(7);
             js += TF_GROUPS;
-            while (js >= tstages && tile < p.tiles) {
-                js -= tstages;
+            while (tile < p.tiles && js >= tile_stages(tile)) {
+                js -= tile_stages(tile);
                 tile += gridDim.x;
             }
         }
@@ -339,13 +407,12 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
         int acc = 0;
         uint32_t aphase = 0;
         for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-            const int pix = tile * 128 + q * 32 + lane;
             PROF_T0();
             ptx::mbar_wait(&tfull[acc], aphase);
             PROF_ACC(10);
             ptx::tc_fence_after();
-            const bool vpix = pix < p.total_pix;
-            const int b = pix / hw_out, rem = pix - b * hw_out;
+            int b = 0, rem = 0, rcx, ccx;
+            const bool vpix = tile_pixel(tile, q * 32 + lane, &b, &rem, &rcx, &ccx);
             float* yo = p.y + (size_t)b * p.Nout * hw_out + rem;
             const float* mo = p.relu_y ? p.relu_y + (size_t)b * p.Nout * hw_out + rem : nullptr;
             const uint32_t dbase = tm + lane_base + acc * 2 * NT;
@@ -503,6 +570,7 @@ hex_status_t tf32_conv(const Geom& g, int Cin, int Cout, int mode, const float* 
     p.kc8 = pl.kc8;
     p.ksteps = pl.ksteps;
     p.relu = mode ? 0 : relu;
+    p.B = g.B;
     p.total_pix = g.B * p.Hout * p.Wout;
     p.tiles = ceil_div(p.total_pix, 128);
     for (int t = 0; t < g.T; ++t) {
@@ -513,11 +581,54 @@ hex_status_t tf32_conv(const Geom& g, int Cin, int Cout, int mode, const float* 
         p.dr0[t] = (int8_t)dr0;
         p.dr1[t] = (int8_t)dr1;
     }
+    int smem = pl.smem;
+    if (p.in_lat) {
+        // phase classes (r mod s, c mod 2s): the taps whose neighbour q = y + off_t(y) is a lattice centre
+        // depend only on the class (q's column parity mod s, its rho(C) (period 2 in C) and its row mod s);
+        // decided on a representative pixel far from the borders (the borders are checked per pixel)
+        const int s = g.s;
+        int nk = 0, tile0 = 0;
+        p.ncls = 0;
+        for (int cr = 0; cr < s; ++cr)
+            for (int ccl = 0; ccl < 2 * s; ++ccl) {
+                const int nr = cr < g.H ? (g.H - cr + s - 1) / s : 0, nc = ccl < g.W ? (g.W - ccl + 2 * s - 1) / (2 * s) : 0;
+                if (nr * nc == 0) continue;
+                TfClass& cl = p.cls[p.ncls++];
+                cl.cr = cr;
+                cl.ccl = ccl;
+                cl.nr = nr;
+                cl.nc = nc;
+                cl.tile0 = tile0;
+                cl.k0 = nk;
+                const int r_rep = cr + 8 * s, c_rep = ccl + 16 * s, pc = (c_rep + g.parity) & 1;
+                for (int t = 0; t < g.T; ++t) {
+                    const int qc = c_rep + p.dc[t], qr = r_rep + (pc ? p.dr1[t] : p.dr0[t]);
+                    if (qc % s) continue;
+                    if ((qr - hex_rho(qc / s, s, g.parity)) % s) continue;
+                    for (int c8 = 0; c8 < pl.kc8; ++c8) {
+                        if (nk >= TF_MAXKL) return HEX_ERR_UNSUPPORTED;
+                        p.klist[nk++] = (uint16_t)(t | (c8 << 8));
+                    }
+                }
+                cl.kn = nk - cl.k0;
+                if (cl.kn == 0) {  // no tap reaches a lattice centre: the class's dx is all zero, but it still
+                    p.klist[nk++] = (uint16_t)0;  // needs one (zero-contributing) K-step to write its tile
+                    cl.kn = 1;
+                }
+                tile0 += ceil_div((int64_t)g.B * nr * nc, 128);
+            }
+        p.tiles = tile0;
+        smem += 6 * nk + 16;
+        if (smem > TF_SMEM_MAX) return HEX_ERR_UNSUPPORTED;
+    } else {
+        p.ncls = 0;
+        smem += 2 * pl.ksteps + 16;
+    }
     switch (pl.NT) {
-        case 16: return launch_tf<16>(p, wp, pl.smem, st);
-        case 32: return launch_tf<32>(p, wp, pl.smem, st);
-        case 48: return launch_tf<48>(p, wp, pl.smem, st);
-        case 64: return launch_tf<64>(p, wp, pl.smem, st);
+        case 16: return launch_tf<16>(p, wp, smem, st);
+        case 32: return launch_tf<32>(p, wp, smem, st);
+        case 48: return launch_tf<48>(p, wp, smem, st);
+        case 64: return launch_tf<64>(p, wp, smem, st);
     }
     return HEX_ERR_UNSUPPORTED;
 }

@@ -38,6 +38,14 @@ __global__ void bench(long long* cycles, int iters) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tm = tslot;
+    if (MODE == 6 && tid >= 32) {  // other warps: dependent FMA chains (issue-slot competition)
+        float a = tid * 1e-3f, b = 1.0001f;
+        for (int it = 0; it < iters * 64; ++it) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) a = fmaf(a, b, 0.5f);
+        }
+        if (a == 1.2345f) cycles[blockIdx.x + 1000] = 1;
+    }
     if (MODE == 5 && tid >= 32) {  // warps 1-3: continuous tcgen05.st traffic to other TMEM columns
         const int w = tid / 32;
         uint32_t v[8] = {1, 2, 3, 4, 5, 6, 7, 8};
@@ -72,7 +80,7 @@ __global__ void bench(long long* cycles, int iters) {
                     smem_u32(&bar)));
                 asm volatile("tcgen05.fence::after_thread_sync;");
             }
-            if constexpr (MODE == 3 || MODE == 5) {
+            if constexpr (MODE == 3 || MODE == 5 || MODE == 6) {
                 constexpr uint32_t id2 = idesc_tf32(128, 2 * N), id1 = idesc_tf32(128, N);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
@@ -84,7 +92,7 @@ __global__ void bench(long long* cycles, int iters) {
                 }
             }
 #pragma unroll
-            for (int a = 0; a < (MODE == 3 || MODE == 5 ? 0 : NACC); ++a) {
+            for (int a = 0; a < (MODE == 3 || MODE == 5 || MODE == 6 ? 0 : NACC); ++a) {
                 const uint32_t d = tm + a * N;
                 if constexpr (A_TMEM)
                     asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;}"
@@ -122,6 +130,20 @@ void run() {
     cudaFree(c);
 }
 
+template <int N>
+void run6() {  // mode 6 with 24 competing warps (768 threads)
+    long long* c;
+    cudaMallocManaged(&c, 2000 * sizeof(long long));
+    const int iters = 2048 / 8;
+    bench<N, 8, true, 6><<<148, 768>>>(c, iters);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long mx = 0;
+    for (int i = 0; i < 148; ++i) mx = c[i] > mx ? c[i] : mx;
+    printf("{\"N\": %d, \"mode\": 6, \"competing_warps\": 23, \"cycles_per_mma\": %.1f, \"status\": \"%s\"}\n", N,
+           (double)mx / (iters * 8), cudaGetErrorString(e));
+    cudaFree(c);
+}
+
 int main() {
     run<16, 1, true>(); run<32, 1, true>(); run<64, 1, true>(); run<128, 1, true>(); run<256, 1, true>();
     run<16, 4, true>(); run<32, 4, true>(); run<64, 4, true>(); run<128, 2, true>();
@@ -131,5 +153,6 @@ int main() {
     run<32, 8, true, 3>(); run<16, 8, true, 3>(); run<64, 8, true, 3>();
     run<32, 2, true, 4>(); run<64, 2, true, 4>(); run<16, 2, true, 4>();
     run<32, 8, true, 5>(); run<64, 8, true, 5>();
+    run6<32>();
     return 0;
 }
