@@ -455,18 +455,25 @@ c1_wgrad_kernel(const float* __restrict__ x, const float* __restrict__ dy, float
     }
 }
 
-__global__ void c1_wgrad_reduce_kernel(const float* __restrict__ part, int nblocks, int Cout, int NA,
-                                       float* __restrict__ dw, float* __restrict__ dbias, int accumulate) {
-    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int o = gid >> 3, sub = gid & 7;
-    const int total = Cout * NA;
+// One block per output (dw[co][t] or dbias[co]): thread k sums partials k, k + 256, ... and the block
+// combines the 256 sums in a fixed shared-memory tree (deterministic).
+constexpr int C1R_THREADS = 256;
+__global__ void __launch_bounds__(C1R_THREADS)
+c1_wgrad_reduce_kernel(const float* __restrict__ part, int nblocks, int Cout, int NA, float* __restrict__ dw,
+                       float* __restrict__ dbias, int accumulate) {
+    __shared__ float red[C1R_THREADS];
+    const int o = blockIdx.x, total = Cout * NA;
     float s = 0.f;
-    if (o < total)
-        for (int k = sub; k < nblocks; k += 8) s += part[(int64_t)k * total + o];
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    if (o >= total || sub != 0) return;
+#pragma unroll 4
+    for (int k = threadIdx.x; k < nblocks; k += C1R_THREADS) s += part[(int64_t)k * total + o];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int h = C1R_THREADS / 2; h > 0; h >>= 1) {
+        if ((int)threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    s = red[0];
     const int co = o / NA, t = o - co * NA;
     if (t == NA - 1) {
         if (dbias) dbias[co] = accumulate ? dbias[co] + s : s;
@@ -530,8 +537,7 @@ hex_status_t c1_conv_wgrad(const float* x, const float* dy, float* dw, float* db
     }
     count_launch();
     const int NA = g.T + 1;
-    c1_wgrad_reduce_kernel<<<ceil_div((int64_t)Cout * NA * 8, 256), 256, 0, st>>>(part, nb, Cout, NA, dw, dbias,
-                                                                                  accumulate);
+    c1_wgrad_reduce_kernel<<<Cout * NA, C1R_THREADS, 0, st>>>(part, nb, Cout, NA, dw, dbias, accumulate);
     count_launch();
     return last_launch_status();
 }

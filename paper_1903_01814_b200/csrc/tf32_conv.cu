@@ -941,23 +941,28 @@ tf32_wgrad_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_consta
 __global__ void tf32_wgrad_reduce_kernel(const float* __restrict__ part, const float* __restrict__ part_b, int nparts,
                                          int Cout, int Cin, int T, float* __restrict__ dw, float* __restrict__ dbias,
                                          int accumulate) {
+    // 8 lanes per output: lane l sums the partials c = l (mod 8), then a fixed shuffle tree (deterministic)
     const int Mrows = T * Cin;
     const int total = Cout * Mrows;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total + Cout; e += gridDim.x * blockDim.x) {
-        if (e < total) {
-            const int co = e / Mrows, mm = e - co * Mrows;  // mm = ci * T + t: dw's own [ci][t] order
-            float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            for (int c = 0; c < nparts; ++c) s8[c & 7] += part[(size_t)c * total + e];
-            const float acc = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
-            float* o = dw + (size_t)co * Mrows + mm;
-            *o = accumulate ? *o + acc : acc;
-        } else if (dbias) {
-            const int co = e - total;
-            float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            for (int c = 0; c < nparts; ++c) s8[c & 7] += part_b[(size_t)c * Cout + co];
-            const float acc = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
-            dbias[co] = accumulate ? dbias[co] + acc : acc;
-        }
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int e = gid >> 3, l = gid & 7;
+    const bool is_db = e >= total;
+    const float* src = is_db ? part_b : part;
+    const int stride = is_db ? Cout : total, off = is_db ? e - total : e;
+    float s = 0.f;
+    if (e < total + Cout) {
+#pragma unroll 4
+        for (int c = l; c < nparts; c += 8) s += src[(size_t)c * stride + off];
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (l != 0 || e >= total + Cout) return;
+    if (!is_db) {
+        float* o = dw + (size_t)e;  // e = co * Mrows + ci * T + t: dw's own [co][ci][t] order
+        *o = accumulate ? *o + s : s;
+    } else if (dbias) {
+        dbias[off] = accumulate ? dbias[off] + s : s;
     }
 }
 
@@ -1113,8 +1118,8 @@ hex_status_t tf32_wgrad(const Geom& g, int Cin, int Cout, const float* x, const 
     }
     if (r != HEX_OK) return r;
     const int total = Cout * g.T * Cin + Cout;
-    tf32_wgrad_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(part, part_b, pl.grid, Cout, Cin, g.T, dw, dbias,
-                                                                  accumulate);
+    tf32_wgrad_reduce_kernel<<<ceil_div((int64_t)total * 8, 256), 256, 0, st>>>(part, part_b, pl.grid, Cout, Cin, g.T,
+                                                                               dw, dbias, accumulate);
     count_launch();
     return last_launch_status();
 }

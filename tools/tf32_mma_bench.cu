@@ -72,6 +72,8 @@ __global__ void bench(long long* cycles, int iters) {
         constexpr uint32_t idesc = idesc_tf32(128, N);
         const uint64_t bd = desc_sw32(smem_u32(bsm));
         const uint64_t ad = desc_sw32(smem_u32(asm_));
+        extern __shared__ __align__(1024) uint8_t dyn[];
+        const uint64_t bdyn = desc_sw32(smem_u32(dyn));
         const uint32_t a_t = tm + 480;  // A in TMEM columns 480..487 (contents irrelevant for timing)
         long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
@@ -80,11 +82,12 @@ __global__ void bench(long long* cycles, int iters) {
                     smem_u32(&bar)));
                 asm volatile("tcgen05.fence::after_thread_sync;");
             }
-            if constexpr (MODE == 3 || MODE == 5 || MODE == 6) {
+            if constexpr (MODE == 3 || MODE == 5 || MODE == 6 || MODE == 7) {
                 constexpr uint32_t id2 = idesc_tf32(128, 2 * N), id1 = idesc_tf32(128, N);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    const uint64_t bk = bd + (uint64_t)((kk & 1) * (2 * N * 32 >> 4));
+                    const uint64_t bk = MODE == 7 ? bdyn + (uint64_t)(((it * 4 + kk) % 24) * (2 * N * 32 >> 4))
+                                                  : bd + (uint64_t)((kk & 1) * (2 * N * 32 >> 4));
                     asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;}"
                                  ::"r"(tm), "r"(tm + 256 + 16 * kk), "l"(bk), "r"(id2), "r"(1));
                     asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;}"
@@ -92,7 +95,7 @@ __global__ void bench(long long* cycles, int iters) {
                 }
             }
 #pragma unroll
-            for (int a = 0; a < (MODE == 3 || MODE == 5 || MODE == 6 ? 0 : NACC); ++a) {
+            for (int a = 0; a < (MODE == 3 || MODE == 5 || MODE == 6 || MODE == 7 ? 0 : NACC); ++a) {
                 const uint32_t d = tm + a * N;
                 if constexpr (A_TMEM)
                     asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;}"
@@ -144,6 +147,22 @@ void run6() {  // mode 6 with 24 competing warps (768 threads)
     cudaFree(c);
 }
 
+template <int N>
+void run7() {  // mode 7: B blocks of successive K-steps from a 24-block region (as the conv kernel's resident weights)
+    long long* c;
+    cudaMallocManaged(&c, 2000 * sizeof(long long));
+    const int iters = 2048 / 8;
+    const int smem = 24 * 2 * N * 32 + 1024;
+    cudaFuncSetAttribute(bench<N, 8, true, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    bench<N, 8, true, 7><<<148, 128, smem>>>(c, iters);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long mx = 0;
+    for (int i = 0; i < 148; ++i) mx = c[i] > mx ? c[i] : mx;
+    printf("{\"N\": %d, \"mode\": 7, \"cycles_per_mma\": %.1f, \"status\": \"%s\"}\n", N,
+           (double)mx / (iters * 8), cudaGetErrorString(e));
+    cudaFree(c);
+}
+
 int main() {
     run<16, 1, true>(); run<32, 1, true>(); run<64, 1, true>(); run<128, 1, true>(); run<256, 1, true>();
     run<16, 4, true>(); run<32, 4, true>(); run<64, 4, true>(); run<128, 2, true>();
@@ -154,5 +173,6 @@ int main() {
     run<32, 2, true, 4>(); run<64, 2, true, 4>(); run<16, 2, true, 4>();
     run<32, 8, true, 5>(); run<64, 8, true, 5>();
     run6<32>();
+    run7<32>(); run7<64>(); run7<16>();
     return 0;
 }
