@@ -1172,61 +1172,13 @@ __global__ void wgrad_tc_reduce_kernel(const float* __restrict__ part, int chunk
     *d = accumulate ? *d + s : s;
 }
 
-// The same reduction for Cin % 32 == 0, transposed through shared memory: block (co, 32-channel group)
-// reads part[c][t][co][ci0 .. ci0+31] (coalesced over ci) for every tap, and writes dw[co][ci0 .. ci0+31][t]
-// as one contiguous run of 32 T floats (the strided [co][ci][t] stores of the kernel above wrote one 4-byte
-// value per 32-byte sector).  Same per-element summation order.  Blocks past Cout * Cin / 32 do dbias.
-constexpr int WR_THREADS = 256;
-__global__ void __launch_bounds__(WR_THREADS)
-wgrad_tc_reduce_t_kernel(const float* __restrict__ part, int chunks, int T, int Cout, int Cin,
-                         float* __restrict__ dw, const float* __restrict__ db_part, float* __restrict__ dbias,
-                         int accumulate) {
-    extern __shared__ float tile[];  // [32][T + 1]
-    const int groups = Cin >> 5;
-    const int64_t total = (int64_t)T * Cout * Cin;
-    if ((int)blockIdx.x >= Cout * groups) {  // dbias
-        const int co = (blockIdx.x - Cout * groups) * WR_THREADS + threadIdx.x;
-        if (!dbias || co >= Cout) return;
-        float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int c = 0; c < chunks; ++c) s8[c & 7] += db_part[(int64_t)c * Cout + co];
-        const float s = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
-        dbias[co] = accumulate ? dbias[co] + s : s;
-        return;
-    }
-    const int co = blockIdx.x / groups, ci0 = (blockIdx.x - co * groups) * 32;
-    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    for (int t = wp; t < T; t += WR_THREADS / 32) {
-        const int64_t off = ((int64_t)t * Cout + co) * Cin + ci0 + lane;
-        float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        int c = 0;
-        for (; c + 8 <= chunks; c += 8)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) s8[j] += part[(int64_t)(c + j) * total + off];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (c + j < chunks) s8[j] += part[(int64_t)(c + j) * total + off];
-        tile[lane * (T + 1) + t] = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
-    }
-    __syncthreads();
-    float* d = dw + ((int64_t)co * Cin + ci0) * T;
-    for (int i = threadIdx.x; i < 32 * T; i += WR_THREADS) {
-        const int j = i / T, t = i - j * T;
-        const float s = tile[j * (T + 1) + t];
-        d[i] = accumulate ? d[i] + s : s;
-    }
-}
-
+// (A variant transposing through shared memory -- block (co, 32 channels) writing dw[co][ci0..ci0+31][t]
+// contiguously -- measured slower in the C5 step: 21.5 vs 15.4 us per launch.)
 static hex_status_t wgrad_reduce(const float* part, int chunks, int T, int Cout, int Cin, float* dw,
                                  const float* db_part, float* dbias, int accumulate, cudaStream_t st) {
-    if (Cin % 32 == 0) {
-        const int blocks = Cout * (Cin / 32) + ceil_div(Cout, WR_THREADS);
-        wgrad_tc_reduce_t_kernel<<<blocks, WR_THREADS, 32 * (T + 1) * sizeof(float), st>>>(
-            part, chunks, T, Cout, Cin, dw, db_part, dbias, accumulate);
-    } else {
-        const int64_t total = (int64_t)T * Cout * Cin;
-        wgrad_tc_reduce_kernel<<<ceil_div(total + Cout, 256), 256, 0, st>>>(part, chunks, T, Cout, Cin, dw, db_part,
-                                                                          dbias, accumulate);
-    }
+    const int64_t total = (int64_t)T * Cout * Cin;
+    wgrad_tc_reduce_kernel<<<ceil_div(total + Cout, 256), 256, 0, st>>>(part, chunks, T, Cout, Cin, dw, db_part, dbias,
+                                                                      accumulate);
     count_launch();
     return last_launch_status();
 }
