@@ -688,7 +688,7 @@ def main():
     total_tf = flops_img * B / (ms_step / 1e3) / 1e12
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "tc_conv_fwd_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02", "tc_fwd_traffic.json")) as f:
             traffic = json.load(f).get("bytes_per_launch")
     except Exception:
         pass

@@ -179,7 +179,7 @@ pool_bwd_plane_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ am, 
 template <typename T, int P, int RHO, bool MAX, bool MASK>
 __device__ __forceinline__ void pool_bwd_blk_nchw(const T* __restrict__ dyp, const uint8_t* __restrict__ amp,
                                                   const T* __restrict__ mp, T* __restrict__ dxp, const Geom& g,
-                                                  int Rp, int C) {
+                                                  int Rp, int C, float* VOUT = nullptr) {
     float v[2][3];
     int a[2][3];
 #pragma unroll
@@ -197,20 +197,20 @@ __device__ __forceinline__ void pool_bwd_blk_nchw(const T* __restrict__ dyp, con
                         a[dC][dR + 1] = amp[o];
                     } else {
                         const int rho = Cw & 1;  // = hex_rho(Cw, 2, parity) for parity in {0, 1}
-                        d = d / (float)window_count(1, g.H, g.W, g.parity, rho + 2 * Rw, 2 * Cw);
+                        const int rc = rho + 2 * Rw, cc = 2 * Cw;
+                        // interior windows (the usual case) have all 7 taps in the grid
+                        const bool interior = rc >= 1 && rc + 1 < g.H && cc >= 1 && cc + 1 < g.W;
+                        d = d / (float)(interior ? 7 : window_count(1, g.H, g.W, g.parity, rc, cc));
                     }
                     v[dC][dR + 1] = d;
                 }
             }
         }
+    float out[2][2];
 #pragma unroll
-    for (int pr = 0; pr < 2; ++pr) {
-        const int r = 2 * Rp + pr;
-        if (r >= g.H) continue;
+    for (int pr = 0; pr < 2; ++pr)
 #pragma unroll
         for (int pc = 0; pc < 2; ++pc) {
-            const int c = 2 * C + pc;
-            if (c >= g.W) continue;
             float acc = 0.f;
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
@@ -219,9 +219,60 @@ __device__ __forceinline__ void pool_bwd_blk_nchw(const T* __restrict__ dyp, con
                 const float d = v[cd.dC][cd.dR + 1];
                 if (!MAX || a[cd.dC][cd.dR + 1] == cd.tap) acc += d;
             }
+            out[pr][pc] = acc;
+        }
+    if (VOUT) {
+#pragma unroll
+        for (int pr = 0; pr < 2; ++pr)
+#pragma unroll
+            for (int pc = 0; pc < 2; ++pc) VOUT[pr * 2 + pc] = out[pr][pc];
+        return;
+    }
+#pragma unroll
+    for (int pr = 0; pr < 2; ++pr) {
+        const int r = 2 * Rp + pr;
+        if (r >= g.H) continue;
+#pragma unroll
+        for (int pc = 0; pc < 2; ++pc) {
+            const int c = 2 * C + pc;
+            if (c >= g.W) continue;
+            float acc = out[pr][pc];
             if (MASK && !(to_f32(__ldg(mp + r * g.W + c)) > 0.f)) acc = 0.f;
             dxp[r * g.W + c] = from_f32<T>(acc);
         }
+    }
+}
+
+// fp32, W % 4 == 0: one thread per pair of 2x2 blocks (window columns C = 2k, 2k + 1 -> input columns
+// 4k .. 4k + 3): two float4 stores (and mask loads) per thread instead of four strided scalars
+template <int P, bool MAX, bool MASK>
+__global__ void __launch_bounds__(PL_THREADS)
+pool_bwd_n1s2_nchw_v4_kernel(const float* __restrict__ dy, const uint8_t* __restrict__ am,
+                             const float* __restrict__ relu_y, float* __restrict__ dx, Geom g) {
+    const int nk = g.W >> 2, nR = (g.H + 1) / 2;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nR * nk) return;
+    const int64_t pl = blockIdx.y;
+    const int Rp = i / nk, k = i - Rp * nk;
+    const float* dyp = dy + pl * g.Ho * g.Wo;
+    const uint8_t* amp = MAX ? am + pl * g.Ho * g.Wo : nullptr;
+    float e[4], o[4];
+    pool_bwd_blk_nchw<float, P, 0, MAX, false>(dyp, amp, nullptr, nullptr, g, Rp, 2 * k, e);
+    pool_bwd_blk_nchw<float, P, 1, MAX, false>(dyp, amp, nullptr, nullptr, g, Rp, 2 * k + 1, o);
+#pragma unroll
+    for (int pr = 0; pr < 2; ++pr) {
+        const int r = 2 * Rp + pr;
+        if (r >= g.H) break;
+        const int64_t off = (pl * g.H + r) * g.W + 4 * k;
+        float4 val = make_float4(e[2 * pr], e[2 * pr + 1], o[2 * pr], o[2 * pr + 1]);
+        if (MASK) {
+            const float4 m = __ldg(reinterpret_cast<const float4*>(relu_y + off));
+            val.x = m.x > 0.f ? val.x : 0.f;
+            val.y = m.y > 0.f ? val.y : 0.f;
+            val.z = m.z > 0.f ? val.z : 0.f;
+            val.w = m.w > 0.f ? val.w : 0.f;
+        }
+        *reinterpret_cast<float4*>(dx + off) = val;
     }
 }
 
@@ -249,6 +300,26 @@ template <typename T>
 static bool launch_bwd_n1s2(const PoolArgs& a, const void* relu_y, cudaStream_t st) {
     const int64_t planes = (int64_t)a.g.B * a.C;
     if (planes > 65535) return false;
+    if (sizeof(T) == 4 && (a.g.W & 3) == 0 && a.g.Wo * 2 == a.g.W &&
+        (((uintptr_t)a.dx | (uintptr_t)relu_y) & 15) == 0) {  // vectorised pair-of-blocks kernel
+        const int per_plane = ((a.g.H + 1) / 2) * (a.g.W / 4);
+        dim3 grid(ceil_div(per_plane, PL_THREADS), (unsigned)planes);
+        const float* dy = (const float*)a.dy;
+        const float* m = (const float*)relu_y;
+        float* dx = (float*)a.dx;
+        const bool mx = a.mode == HEX_POOL_MAX;
+#define HEX_BW4(PP, MX, MK) \
+    pool_bwd_n1s2_nchw_v4_kernel<PP, MX, MK><<<grid, PL_THREADS, 0, st>>>(dy, MX ? a.argmax_in : nullptr, m, dx, a.g)
+        if (a.g.parity & 1) {
+            if (mx) { if (m) HEX_BW4(1, true, true); else HEX_BW4(1, true, false); }
+            else { if (m) HEX_BW4(1, false, true); else HEX_BW4(1, false, false); }
+        } else {
+            if (mx) { if (m) HEX_BW4(0, true, true); else HEX_BW4(0, true, false); }
+            else { if (m) HEX_BW4(0, false, true); else HEX_BW4(0, false, false); }
+        }
+#undef HEX_BW4
+        return true;
+    }
     const int per_plane = ((a.g.H + 1) / 2) * a.g.Wo;
     dim3 grid(ceil_div(per_plane, PL_THREADS), (unsigned)planes);
     const bool mx = a.mode == HEX_POOL_MAX;
