@@ -60,6 +60,22 @@ def test_tap_offsets_bit_exact(abi, oracle):
             assert abi.tap_offsets(n, p) == oracle.tap_offsets(n, p)
 
 
+def test_tap_axial_bit_exact(abi, oracle):
+    # custom-kernel element order (reading A2): the library's axial tap list is the oracle's
+    for n in range(0, abi.MAX_N + 1):
+        assert abi.tap_axial(n) == oracle.tap_list(n)
+    with pytest.raises(abi.HexError):
+        abi.tap_axial(-1)
+
+
+def test_switch_hook_rejects_unknown_names(abi):
+    L = abi.lib()
+    assert L.hex_debug_set_switch(b"HEXCONV_NOT_A_SWITCH", b"1") == 1  # HEX_ERR_INVALID_ARG
+    assert L.hex_debug_set_switch(None, None) == 1
+    with abi.switch("HEXCONV_NO_TF32"):
+        pass  # set and restored without touching a GPU
+
+
 def test_output_shape_bit_exact(abi, oracle):
     for pi in (0, 1):
         for s in range(1, 7):
