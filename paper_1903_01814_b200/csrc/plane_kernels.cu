@@ -406,41 +406,82 @@ bool pool_plane_bwd(const PoolArgs& a, cudaStream_t st) {
 
 // ---------------------------------------------------------------------------
 // Single-input-channel fp32 convolution, stride 1 (config 3 layer 1).
-// Forward: blocks of 128 threads own one band of C1_RB rows of one image and
-// COB output channels (weights + bias in registers); the zero-padded band of x
-// is staged in shared memory, each thread computes whole pixels, stores are
-// coalesced along each output channel plane.
+// The layer is small (7 or 19 FMAs per output element) and its tensors live in
+// L2, so both kernels are instruction-bound: the design keeps the per-pixel
+// instruction count near the FMA count.  A block stages one zero-padded band of
+// x (rb rows + an n-row / n-column halo) in shared memory; its 256 threads form
+// two channel groups of 128 threads (warp-uniform), each thread holding its
+// group's COB channels' taps in registers and walking the band's pixels with
+// stride 128 (incremental row / column, no per-pixel division).
+//   forward: per pixel T shared-memory taps, COB x T FMAs, COB coalesced stores
+//            (one per output plane, 128 consecutive pixels per warp group).
+//   weight gradient: persistent blocks over bands; per pixel COB coalesced dy
+//            loads, T taps, COB x (T + 1) FMAs into registers (the + 1 is
+//            dbias); a fixed xor-shuffle tree per warp, the 4 warps of a group
+//            in warp order, then blocks in block order (c1_wgrad_reduce):
+//            deterministic.
 // ---------------------------------------------------------------------------
-constexpr int C1_RB = 8;
-constexpr int C1_THREADS = 128;
+constexpr int C1_THREADS = 256;
+constexpr int C1_TPG = 128;    // threads per channel group (2 groups per block)
+constexpr int C1_MAX_RB = 32;  // rows per forward band (at most)
 
-template <int N, int COB>
-__global__ void __launch_bounds__(C1_THREADS)
+template <int N>
+struct C1Cfg {
+    static constexpr int T = 3 * N * (N + 1) + 1;
+    static constexpr int COB = N == 1 ? 8 : 4;  // channels per group (registers: COB x T weights / sums)
+};
+
+// zero-padded band [(rows + 2N) x (W + 2N)] of image b, rows r0 - N .. r0 + rows + N - 1
+template <int N>
+__device__ __forceinline__ void c1_stage(const float* __restrict__ x, float* xs, int b, int r0, int rows, int H,
+                                         int W) {
+    const int Wp = W + 2 * N, nr = rows + 2 * N;
+    const float* xb = x + (int64_t)b * H * W;
+    for (int rr = threadIdx.x / 32; rr < nr; rr += C1_THREADS / 32) {  // one warp per staged row
+        const int r = r0 - N + rr;
+        const bool rok = r >= 0 && r < H;
+        for (int cc = threadIdx.x % 32; cc < Wp; cc += 32) {
+            const int c = cc - N;
+            xs[rr * Wp + cc] = (rok && c >= 0 && c < W) ? __ldg(xb + (int64_t)r * W + c) : 0.f;
+        }
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(C1_THREADS, 2)
 c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
-              float* __restrict__ y, int B, int H, int W, int parity, int Cout, int relu) {
-    constexpr int T = 3 * N * (N + 1) + 1;
-    extern __shared__ float xs[];  // [(C1_RB + 2N) x (W + 2N)]
+              float* __restrict__ y, int B, int H, int W, int parity, int Cout, int relu, int rb) {
+    constexpr int T = C1Cfg<N>::T, COB = C1Cfg<N>::COB;
+    extern __shared__ float xs[];  // [(rb + 2N) x (W + 2N)]
+    __shared__ float wsh[2 * COB * T + 2 * COB];
     const int Wp = W + 2 * N;
-    const int nb = (H + C1_RB - 1) / C1_RB;
-    const int b = blockIdx.x / nb, r0 = (blockIdx.x - b * nb) * C1_RB;
-    const int rows = min(C1_RB, H - r0);
-    const int co0 = blockIdx.y * COB;
+    const int nb = (H + rb - 1) / rb;
+    const int b = blockIdx.x / nb, r0 = (blockIdx.x - b * nb) * rb;
+    const int rows = min(rb, H - r0);
+    const int grp = threadIdx.x / C1_TPG, tg = threadIdx.x % C1_TPG;
+    const int cb = blockIdx.y * 2 * COB;  // first channel of the block
+    for (int i = threadIdx.x; i < 2 * COB * T; i += C1_THREADS)
+        wsh[i] = cb + i / T < Cout ? __ldg(w + (int64_t)cb * T + i) : 0.f;
+    if (threadIdx.x < 2 * COB)
+        wsh[2 * COB * T + threadIdx.x] = (bias && cb + (int)threadIdx.x < Cout) ? __ldg(bias + cb + threadIdx.x) : 0.f;
+    c1_stage<N>(x, xs, b, r0, rows, H, W);
+    __syncthreads();
+    const int co0 = cb + grp * COB;
+    if (co0 >= Cout) return;
+    const int nco = min(COB, Cout - co0);
     float wr[T][COB], br[COB];
 #pragma unroll
     for (int j = 0; j < COB; ++j) {
-        const bool ok = co0 + j < Cout;
-        br[j] = (bias && ok) ? __ldg(bias + co0 + j) : 0.f;
+        br[j] = wsh[2 * COB * T + grp * COB + j];
 #pragma unroll
-        for (int t = 0; t < T; ++t) wr[t][j] = ok ? __ldg(w + (int64_t)(co0 + j) * T + t) : 0.f;
+        for (int t = 0; t < T; ++t) wr[t][j] = wsh[(grp * COB + j) * T + t];
     }
-    for (int i = threadIdx.x; i < (rows + 2 * N) * Wp; i += blockDim.x) {
-        const int rr = i / Wp, cc = i - rr * Wp;
-        const int r = r0 - N + rr, c = cc - N;
-        xs[i] = (r >= 0 && r < H && c >= 0 && c < W) ? __ldg(x + ((int64_t)b * H + r) * W + c) : 0.f;
-    }
-    __syncthreads();
-    for (int q = threadIdx.x; q < rows * W; q += blockDim.x) {
-        const int rl = q / W, c = q - rl * W;
+    const int64_t plane = (int64_t)H * W;
+    float* yb = y + ((int64_t)b * Cout + co0) * plane + (int64_t)r0 * W;
+    const int npx = rows * W;
+    int rl = tg / W, c = tg - rl * W;
+    const int dq = C1_TPG / W, dcc = C1_TPG - dq * W;
+    for (int q = tg; q < npx; q += C1_TPG) {
         const int p = (c + parity) & 1;
         float acc[COB];
 #pragma unroll
@@ -450,79 +491,111 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w, const fl
 #pragma unroll
         for (int dc = -N; dc <= N; ++dc) {
             const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
-            const int top = tap_top(N, dc, p);
+            const float* xcol = xc + dc + tap_top(N, dc, p) * Wp;
 #pragma unroll
             for (int k = 0; k < len; ++k, ++t) {
-                const float v = xc[(top + k) * Wp + dc];
+                const float v = xcol[k * Wp];
 #pragma unroll
                 for (int j = 0; j < COB; ++j) acc[j] = fmaf(v, wr[t][j], acc[j]);
             }
         }
-        float* yp = y + (((int64_t)b * Cout + co0) * H + r0 + rl) * W + c;
+        if (nco == COB) {
 #pragma unroll
-        for (int j = 0; j < COB; ++j)
-            if (co0 + j < Cout) yp[(int64_t)j * H * W] = relu ? fmaxf(acc[j], 0.f) : acc[j];
+            for (int j = 0; j < COB; ++j) yb[j * plane + q] = relu ? fmaxf(acc[j], 0.f) : acc[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < COB; ++j)
+                if (j < nco) yb[j * plane + q] = relu ? fmaxf(acc[j], 0.f) : acc[j];
+        }
+        rl += dq;
+        c += dcc;
+        if (c >= W) { c -= W; ++rl; }
     }
 }
 
-// Weight gradient: persistent blocks over (image, band); thread = (output channel,
-// pixel slice): per pixel one coalesced dy load and T shared-memory taps.  Fixed-
-// order reductions: slices of a block in slice order, then blocks in block order
-// (8 lanes per output, fixed shuffle tree).  part[block][co][T + 1].
 template <int N>
-__global__ void __launch_bounds__(PL_THREADS)
+__global__ void __launch_bounds__(C1_THREADS, 2)
 c1_wgrad_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ part, int B, int H,
-                int W, int parity, int Cout, int slices) {
-    constexpr int T = 3 * N * (N + 1) + 1;
+                int W, int parity, int Cout, int rb) {
+    constexpr int T = C1Cfg<N>::T, COB = C1Cfg<N>::COB, NA = T + 1;
     extern __shared__ float sm[];
     const int Wp = W + 2 * N;
-    float* xs = sm;                                   // [(C1_RB + 2N) x Wp]
-    float* red = xs + (C1_RB + 2 * N) * Wp;           // [Cout][slices][T + 1]
-    const int co = threadIdx.x / slices, sl = threadIdx.x - co * slices;
-    const bool active = co < Cout;
-    const int nb = (H + C1_RB - 1) / C1_RB;
-    float acc[T + 1];
+    float* xs = sm;                       // [(rb + 2N) x Wp]
+    float* red = xs + (rb + 2 * N) * Wp;  // [8 warps][COB * NA]
+    const int grp = threadIdx.x / C1_TPG, tg = threadIdx.x % C1_TPG;
+    const int co0 = blockIdx.y * 2 * COB + grp * COB;
+    const int nco = max(0, min(COB, Cout - co0));
+    const int nb = (H + rb - 1) / rb;
+    const int64_t plane = (int64_t)H * W;
+    const int dq = C1_TPG / W, dcc = C1_TPG - dq * W;
+    float acc[COB][NA];
 #pragma unroll
-    for (int t = 0; t <= T; ++t) acc[t] = 0.f;
+    for (int j = 0; j < COB; ++j)
+#pragma unroll
+        for (int t = 0; t < NA; ++t) acc[j][t] = 0.f;
     for (int band = blockIdx.x; band < B * nb; band += gridDim.x) {
-        const int b = band / nb, r0 = (band - b * nb) * C1_RB;
-        const int rows = min(C1_RB, H - r0);
+        const int b = band / nb, r0 = (band - b * nb) * rb;
+        const int rows = min(rb, H - r0);
         __syncthreads();
-        for (int i = threadIdx.x; i < (rows + 2 * N) * Wp; i += blockDim.x) {
-            const int rr = i / Wp, cc = i - rr * Wp;
-            const int r = r0 - N + rr, c = cc - N;
-            xs[i] = (r >= 0 && r < H && c >= 0 && c < W) ? __ldg(x + ((int64_t)b * H + r) * W + c) : 0.f;
-        }
+        c1_stage<N>(x, xs, b, r0, rows, H, W);
         __syncthreads();
-        if (!active) continue;
-        const float* dyp = dy + (((int64_t)b * Cout + co) * H + r0) * W;
-#pragma unroll 4
-        for (int q = sl; q < rows * W; q += slices) {
-            const int rl = q / W, c = q - rl * W;
+        if (nco == 0) continue;
+        const float* dyb = dy + ((int64_t)b * Cout + co0) * plane + (int64_t)r0 * W;
+        const int npx = rows * W;
+        int rl = tg / W, c = tg - rl * W;
+#pragma unroll 2
+        for (int q = tg; q < npx; q += C1_TPG) {
             const int p = (c + parity) & 1;
-            const float g = __ldg(dyp + q);
+            float g[COB];
+#pragma unroll
+            for (int j = 0; j < COB; ++j) g[j] = j < nco ? __ldg(dyb + j * plane + q) : 0.f;
             const float* xc = xs + (rl + N) * Wp + (c + N);
             int t = 0;
 #pragma unroll
             for (int dc = -N; dc <= N; ++dc) {
                 const int len = 2 * N + 1 - (dc < 0 ? -dc : dc);
-                const int top = tap_top(N, dc, p);
+                const float* xcol = xc + dc + tap_top(N, dc, p) * Wp;
 #pragma unroll
-                for (int k = 0; k < len; ++k, ++t) acc[t] = fmaf(g, xc[(top + k) * Wp + dc], acc[t]);
+                for (int k = 0; k < len; ++k, ++t) {
+                    const float v = xcol[k * Wp];
+#pragma unroll
+                    for (int j = 0; j < COB; ++j) acc[j][t] = fmaf(g[j], v, acc[j][t]);
+                }
             }
-            acc[T] += g;
+#pragma unroll
+            for (int j = 0; j < COB; ++j) acc[j][T] += g[j];
+            rl += dq;
+            c += dcc;
+            if (c >= W) { c -= W; ++rl; }
         }
     }
-    __syncthreads();
-    if (active)
+    // fixed xor-shuffle tree within the warp, then the group's 4 warps in warp order
 #pragma unroll
-        for (int t = 0; t <= T; ++t) red[(co * slices + sl) * (T + 1) + t] = acc[t];
+    for (int j = 0; j < COB; ++j)
+#pragma unroll
+        for (int t = 0; t < NA; ++t) {
+            float v = acc[j][t];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            acc[j][t] = v;
+        }
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     __syncthreads();
-    for (int i = threadIdx.x; i < Cout * (T + 1); i += blockDim.x) {
-        const int c = i / (T + 1), t = i - c * (T + 1);
+    if (lane == 0)
+#pragma unroll
+        for (int j = 0; j < COB; ++j)
+#pragma unroll
+            for (int t = 0; t < NA; ++t) red[warp * COB * NA + j * NA + t] = acc[j][t];
+    __syncthreads();
+    constexpr int WPG = C1_TPG / 32;  // warps per group
+    for (int i = threadIdx.x; i < 2 * COB * NA; i += C1_THREADS) {
+        const int gi = i / (COB * NA), e = i - gi * (COB * NA);
+        const int co = blockIdx.y * 2 * COB + gi * COB + e / NA;
+        if (co >= Cout) continue;
         float s = 0.f;
-        for (int k = 0; k < slices; ++k) s += red[(c * slices + k) * (T + 1) + t];
-        part[(int64_t)blockIdx.x * Cout * (T + 1) + i] = s;
+#pragma unroll
+        for (int k = 0; k < WPG; ++k) s += red[(gi * WPG + k) * COB * NA + e];
+        part[((int64_t)blockIdx.x * Cout + co) * NA + (e % NA)] = s;
     }
 }
 
@@ -554,38 +627,54 @@ c1_wgrad_reduce_kernel(const float* __restrict__ part, int nblocks, int Cout, in
     }
 }
 
+static int c1_cgy(const Geom& g, int Cout) { return ceil_div(Cout, 2 * (g.n == 1 ? C1Cfg<1>::COB : C1Cfg<2>::COB)); }
+
+// forward rows per band: about two blocks per SM slot where the batch allows
+static int c1_rows(const Geom& g, int cgy) {
+    const int64_t slots = (int64_t)num_sms() * 2;
+    int nb = (int)((2 * slots + (int64_t)g.B * cgy - 1) / ((int64_t)g.B * cgy));
+    if (nb < 1) nb = 1;
+    if (nb > g.H) nb = g.H;
+    int rb = (g.H + nb - 1) / nb;
+    if (rb < 4 && g.H >= 4) rb = 4;
+    return rb < C1_MAX_RB ? rb : C1_MAX_RB;
+}
+
+static int c1_band_rows(const Geom& g) { return g.H < 16 ? g.H : 16; }  // weight gradient
+
 bool c1_conv_supported(const Geom& g, int Cin, int Cout, int dtype, int layout) {
     if (sw_on("HEXCONV_NO_PLANE")) return false;
     if (dtype != HEX_F32 || layout != HEX_NCHW || Cin != 1 || g.s != 1 || (g.n != 1 && g.n != 2)) return false;
-    if (Cout > PL_THREADS || g.B > 65535 * 8) return false;
-    const int64_t band = (int64_t)(C1_RB + 2 * g.n) * (g.W + 2 * g.n);
-    return band * 4 + (int64_t)PL_THREADS * (g.T + 1) * 4 <= 200 * 1024;
+    if (g.B > 65535 * 8 || Cout > 65535) return false;
+    const int64_t band = (int64_t)(C1_MAX_RB + 2 * g.n) * (g.W + 2 * g.n);  // the tallest band
+    return band * 4 + 8 * 8 * 20 * 4 <= 200 * 1024;
 }
 
-static int c1_wgrad_blocks(const Geom& g) {
-    const int64_t bands = (int64_t)g.B * ((g.H + C1_RB - 1) / C1_RB);
-    const int64_t cap = (int64_t)num_sms() * 8;
-    return (int)(bands < cap ? bands : cap);
+static int c1_wgrad_blocks(const Geom& g, int Cout) {
+    const int64_t bands = (int64_t)g.B * ((g.H + c1_band_rows(g) - 1) / c1_band_rows(g));
+    const int64_t cap = (int64_t)num_sms() * 2 / c1_cgy(g, Cout);
+    const int64_t nb = bands < cap ? bands : cap;
+    return (int)(nb > 0 ? nb : 1);
 }
 
-size_t c1_wgrad_ws_bytes(const Geom& g, int Cout) { return (size_t)c1_wgrad_blocks(g) * Cout * (g.T + 1) * 4; }
+size_t c1_wgrad_ws_bytes(const Geom& g, int Cout) {
+    return (size_t)c1_wgrad_blocks(g, Cout) * Cout * (g.T + 1) * 4;
+}
 
 hex_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, float* y, const Geom& g, int Cout,
                          int relu, cudaStream_t st) {
-    const size_t smem = (size_t)(C1_RB + 2 * g.n) * (g.W + 2 * g.n) * 4;
-    const int nb = (g.H + C1_RB - 1) / C1_RB;
+    const int cgy = c1_cgy(g, Cout);
+    const int rb = c1_rows(g, cgy);
+    const size_t smem = (size_t)(rb + 2 * g.n) * (g.W + 2 * g.n) * 4;
+    dim3 grid(g.B * ceil_div(g.H, rb), cgy);
     if (g.n == 1) {
-        constexpr int COB = 8;
-        dim3 grid(g.B * nb, ceil_div(Cout, COB));
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(c1_fwd_kernel<1, COB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        c1_fwd_kernel<1, COB><<<grid, C1_THREADS, smem, st>>>(x, w, bias, y, g.B, g.H, g.W, g.parity, Cout, relu);
+        if (smem > 40 * 1024)
+            cudaFuncSetAttribute(c1_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        c1_fwd_kernel<1><<<grid, C1_THREADS, smem, st>>>(x, w, bias, y, g.B, g.H, g.W, g.parity, Cout, relu, rb);
     } else {
-        constexpr int COB = 4;
-        dim3 grid(g.B * nb, ceil_div(Cout, COB));
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(c1_fwd_kernel<2, COB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        c1_fwd_kernel<2, COB><<<grid, C1_THREADS, smem, st>>>(x, w, bias, y, g.B, g.H, g.W, g.parity, Cout, relu);
+        if (smem > 40 * 1024)
+            cudaFuncSetAttribute(c1_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        c1_fwd_kernel<2><<<grid, C1_THREADS, smem, st>>>(x, w, bias, y, g.B, g.H, g.W, g.parity, Cout, relu, rb);
     }
     count_launch();
     return last_launch_status();
@@ -593,18 +682,20 @@ hex_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, floa
 
 hex_status_t c1_conv_wgrad(const float* x, const float* dy, float* dw, float* dbias, int accumulate, const Geom& g,
                            int Cout, void* ws, cudaStream_t st) {
-    const int nb = c1_wgrad_blocks(g);
-    const int slices = PL_THREADS / Cout;
-    const size_t smem = ((size_t)(C1_RB + 2 * g.n) * (g.W + 2 * g.n) + (size_t)PL_THREADS * (g.T + 1)) * 4;
+    const int nb = c1_wgrad_blocks(g, Cout);
+    const int rb = c1_band_rows(g);
+    const int COB = g.n == 1 ? C1Cfg<1>::COB : C1Cfg<2>::COB;
+    const size_t smem = ((size_t)(rb + 2 * g.n) * (g.W + 2 * g.n) + (size_t)8 * COB * (g.T + 1)) * 4;
     float* part = (float*)ws;
+    dim3 grid(nb, c1_cgy(g, Cout));
     if (g.n == 1) {
-        if (smem > 48 * 1024)
+        if (smem > 40 * 1024)
             cudaFuncSetAttribute(c1_wgrad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        c1_wgrad_kernel<1><<<nb, PL_THREADS, smem, st>>>(x, dy, part, g.B, g.H, g.W, g.parity, Cout, slices);
+        c1_wgrad_kernel<1><<<grid, C1_THREADS, smem, st>>>(x, dy, part, g.B, g.H, g.W, g.parity, Cout, rb);
     } else {
-        if (smem > 48 * 1024)
+        if (smem > 40 * 1024)
             cudaFuncSetAttribute(c1_wgrad_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        c1_wgrad_kernel<2><<<nb, PL_THREADS, smem, st>>>(x, dy, part, g.B, g.H, g.W, g.parity, Cout, slices);
+        c1_wgrad_kernel<2><<<grid, C1_THREADS, smem, st>>>(x, dy, part, g.B, g.H, g.W, g.parity, Cout, rb);
     }
     count_launch();
     const int NA = g.T + 1;

@@ -227,6 +227,17 @@ def test_maxpool_ties_first_in_canonical_order(F, oracle):
         _pool_case(F, oracle, 0, 1, 1, 11, 12, 2, 8, torch.bfloat16, layout, "max", 0, data=x)
 
 
+@pytest.mark.parametrize("pi", [0, 1])
+def test_pool_n1s2_nchw_f32_pairs(F, oracle, pi):
+    # the fp32 NCHW n = 1, s = 2 output-pair forward (W % 4 == 0, float4 row loads; pool_nchw.cu) and its
+    # backward: top / bottom / left edges, odd and even H, ReLU-like data with exact-zero ties (first
+    # in-grid tap wins), several planes
+    for k, (H, W) in enumerate([(11, 12), (12, 8), (2, 4), (40, 40), (9, 48)]):
+        x = np.maximum(rnd((2, 3, H, W), 30 + k, torch.float32), 0)
+        for mode in ("max", "avg"):
+            _pool_case(F, oracle, pi, 1, 2, H, W, 2, 3, torch.float32, "NCHW", mode, 40 + k, data=x)
+
+
 # ------------------------------------------------------------------ BASELINE configs 1 and 2 at full size
 def test_config1_full(F, oracle):
     import synth
@@ -286,6 +297,16 @@ def test_single_input_channel_mma_bands(F, oracle, pi, n):
     for (H, W), Cout, B in [((37, 45), 128, 3), ((16, 16), 64, 2), ((5, 70), 64, 1), ((35, 40), 64, 2),
                             ((40, 24), 64, 120), ((47, 24), 64, 100)]:
         _conv_case(F, oracle, pi, n, 1, H, W, B, 1, Cout, torch.bfloat16, "NHWC", 60 + n + H)
+
+
+@pytest.mark.parametrize("pi,n", [(0, 1), (1, 1), (0, 2), (1, 2)])
+def test_single_input_channel_f32_bands(F, oracle, pi, n):
+    # the fp32 NCHW Cin = 1 kernels (config 3 layer 1, plane_kernels.cu c1_*): several bands per image with
+    # a ragged last band, channel groups of 8 (n = 1) / 4 (n = 2) with a ragged and an empty group
+    # (Cout = 20), rows wider than a 128-thread group (W = 150), more bands than persistent
+    # weight-gradient blocks (B = 300), both parities
+    for (B, H, W, Cout) in [(3, 37, 45, 16), (2, 40, 40, 20), (1, 5, 150, 8), (300, 9, 7, 8)]:
+        _conv_case(F, oracle, pi, n, 1, H, W, B, 1, Cout, torch.float32, "NCHW", 700 + H + Cout)
 
 
 @pytest.mark.parametrize("pi,n", [(0, 1), (1, 1), (0, 2), (1, 2)])

@@ -1,0 +1,50 @@
+"""CUDA-graph timing (hot / L2-flushed, bench.py's GraphTimer) of the small config-3 / config-5 ops one at a
+time -- the quick check used while tuning them.
+
+    python tools/small_ops.py [op ...]     (default: all)
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from bench import GraphTimer  # noqa: E402
+from paper_1903_01814_b200 import functional as F  # noqa: E402
+
+
+def c3_ops():
+    B, H, W = 256, 40, 40
+    H2, W2, _ = F.output_shape(H, W, 2)
+    x = torch.from_numpy(synth.shower_images(B, H, W, 12, 3).astype(np.float32)).cuda()
+    w1 = torch.from_numpy(synth.kaiming_uniform((16, 1, 7), 20).astype(np.float32)).cuda()
+    b1 = torch.zeros(16, device="cuda")
+    y1 = torch.empty(B, 16, H, W, device="cuda")
+    g1 = torch.randn(B, 16, H, W, device="cuda")
+    y2 = torch.randn(B, 32, H, W, device="cuda")
+    p = torch.empty(B, 32, H2, W2, device="cuda")
+    dp = torch.randn(B, 32, H2, W2, device="cuda")
+    dy2 = torch.empty(B, 32, H, W, device="cuda")
+    dw = torch.empty(16, 1, 7, device="cuda")
+    return {
+        "c3_l1_fwd": lambda: F.conv2d_fwd(x, w1, b1, n=1, relu=True, out=y1),
+        "c3_l1_wgrad": lambda: F.conv2d_bwd_weight(x, g1, n=1, dw=dw),
+        "c3_pool_fwd_avg": lambda: F.pool2d_fwd(y2, n=1, stride=2, mode="avg", out=p),
+        "c3_pool_bwd_relu": lambda: F.pool2d_bwd(dp, None, (H, W), n=1, stride=2, mode="avg", out=dy2, relu_y=y2),
+    }
+
+
+def main():
+    ops = c3_ops()
+    sel = sys.argv[1:] or list(ops)
+    gt = GraphTimer("cuda")
+    for name in sel:
+        g = gt.capture(ops[name])
+        hot, fl = gt.time(g, 50)
+        print(f"{name:22s} hot {hot * 1e3:8.2f} us   flushed {fl * 1e3:8.2f} us")
+
+
+if __name__ == "__main__":
+    main()
