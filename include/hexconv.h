@@ -138,7 +138,8 @@ HEX_API hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* desc, in
  * A4 zero contribution of off-grid neighbours):
  *   y[b,co,R,C] = bias[co] + sum_ci sum_t w[co,ci,t] * x[b,ci, centre(R,C)+off_t]
  * then y = max(y, 0) if fuse_relu.
- * x: [B,Cin,H,W] in desc layout/dtype.  w: [Cout][Cin][T] in desc dtype.
+ * x: [B,Cin,H,W] in desc layout/dtype.  w: [Cout][Cin][T] in desc dtype (NULL on
+ * the tensor-core path: weights prepacked in ws by hex_conv2d_pack_weights).
  * bias: fp32 [Cout] or NULL.  y: [B,Cout,Ho,Wo] in desc layout/dtype.
  *
  * Kernel selection (internal, channel-count driven; hex_conv2d_algo reports it):
@@ -165,7 +166,8 @@ HEX_API hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* desc, const void* x
  * dy: [B,Cout,Ho,Wo]; dx: [B,Cin,H,W] (overwritten).
  * relu_y (optional, may be NULL): a tensor shaped like dx (the ReLU output
  * that was this layer's input); when given, dx is multiplied by (relu_y > 0)
- * -- the fused ReLU backward of the previous layer. */
+ * -- the fused ReLU backward of the previous layer.  w as for the forward
+ * (NULL: prepacked, pass 1, on the stride-1 tensor-core path). */
 HEX_API hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* desc, const void* dy, const void* w,
                                  const void* relu_y, void* dx,
                                  void* ws, size_t ws_bytes, hex_stream_t stream);
@@ -194,6 +196,28 @@ HEX_API hex_status_t hex_conv2d_fwd_maxpool(const hex_conv2d_desc_t* desc, const
                                             const float* bias, int32_t fuse_relu, void* y_pool,
                                             uint8_t* argmax_tap, void* ws, size_t ws_bytes,
                                             hex_stream_t stream);
+
+/* Weight packing hoisted out of the calls (the config-5 training step: the
+ * weights change once per step, and each layer's fwd and bwd_data would pack
+ * them again).  The bf16 tensor-core paths read the weights as per-tap K-major
+ * tiles that hex_conv2d_fwd / hex_conv2d_fwd_maxpool / hex_conv2d_bwd_data
+ * otherwise write into the front of their workspace on every call.  This call
+ * does that packing for `count` (<= 16) layers in ONE kernel launch: for layer i,
+ * descs[i] (host array), passes[i] = 0 (fwd and fwd_maxpool layout) or 1
+ * (bwd_data, stride 1: transposed channels, reversed taps), w[i] the device
+ * weights [Cout][Cin][T] (bf16, 16-byte aligned), ws[i] / ws_bytes[i] that
+ * pass's workspace (hex_conv2d_workspace_size); w, ws, ws_bytes are host arrays
+ * of device pointers / sizes.  A later fwd / fwd_maxpool / bwd_data call with
+ * w == NULL and the same workspace uses the packed weights as they stand (the
+ * caller repacks after changing w).  w == NULL is accepted on those tensor-core
+ * paths only; elsewhere it is HEX_ERR_INVALID_ARG.
+ * Errors: HEX_ERR_INVALID_ARG (count outside 0..16, NULL arrays / entries, pass
+ * not 0/1), HEX_ERR_UNSUPPORTED (a descriptor whose pass does not take the
+ * tensor-core path: check hex_conv2d_algo), HEX_ERR_WORKSPACE, HEX_ERR_ALIGNMENT,
+ * descriptor errors as hex_conv2d_fwd. */
+HEX_API hex_status_t hex_conv2d_pack_weights(int32_t count, const hex_conv2d_desc_t* descs,
+                                             const int32_t* passes, const void* const* w, void* const* ws,
+                                             const size_t* ws_bytes, hex_stream_t stream);
 
 /* Which kernel family a call with this descriptor runs: *algo (host) = 0 for
  * the CUDA-core stencil path, 1 for the bf16 tcgen05 tensor-core path, 2 for

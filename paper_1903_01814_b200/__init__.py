@@ -7,6 +7,7 @@ is the thin Python binding.  Importing it without the built library raises:
 there is no CPU fallback.
 """
 from . import _abi  # noqa: F401  (raises ImportError if libhexconv.so is missing)
+from . import nn  # noqa: F401  (torch.nn modules: HexConv2d, HexConv3d, HexMaxPool2d, HexAvgPool2d)
 from .functional import (  # noqa: F401
     conv2d_bwd_data,
     conv2d_bwd_weight,

@@ -87,6 +87,7 @@ _SIGS = {
     "hex_conv2d_fwd_maxpool": (_i32, [_CDP, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp]),
     "hex_conv2d_bwd_data": (_i32, [_CDP, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "hex_conv2d_bwd_weight": (_i32, [_CDP, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
+    "hex_conv2d_pack_weights": (_i32, [_i32, _CDP, _i32p, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _szp, _vp]),
     "hex_conv3d_output_shape": (_i32, [_C3P, _i32p, _i32p, _i32p]),
     "hex_conv3d_workspace_size": (_i32, [_C3P, _i32, _szp]),
     "hex_conv3d_fwd": (_i32, [_C3P, _vp, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
@@ -143,6 +144,24 @@ def tap_axial(n: int):
     buf = (_i32 * (2 * max(T, 1)))()
     check(_lib.hex_tap_axial(n, buf), "hex_tap_axial")
     return [(buf[2 * t], buf[2 * t + 1]) for t in range(T)]
+
+
+class PackArgs:
+    """Marshalled argument arrays of hex_conv2d_pack_weights for a fixed set of (desc, pass, weight pointer,
+    workspace pointer, workspace bytes) entries -- built once, then `run(stream)` is one library call."""
+
+    def __init__(self, entries):
+        n = len(entries)
+        self.n = n
+        self.descs = (ConvDesc * max(n, 1))(*[e[0] for e in entries])
+        self.passes = (_i32 * max(n, 1))(*[e[1] for e in entries])
+        self.w = (_vp * max(n, 1))(*[e[2] for e in entries])
+        self.ws = (_vp * max(n, 1))(*[e[3] for e in entries])
+        self.ws_bytes = (_sz * max(n, 1))(*[e[4] for e in entries])
+
+    def run(self, stream):
+        check(lib().hex_conv2d_pack_weights(self.n, self.descs, self.passes, self.w, self.ws, self.ws_bytes, stream),
+              "hex_conv2d_pack_weights")
 
 
 class switch:

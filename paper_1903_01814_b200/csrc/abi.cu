@@ -332,20 +332,21 @@ hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* d, const void* x, const voi
     Geom g;
     hex_status_t st = conv_geom(d, &g);
     if (st != HEX_OK) return st;
-    if (!x || !w || !y) return HEX_ERR_INVALID_ARG;
+    if (!x || !y) return HEX_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     if (use_tc_fwd(d, g)) {
-        if (!aligned16(x) || !aligned16(y) || !aligned16(w) || (bias && !aligned16(bias))) return HEX_ERR_ALIGNMENT;
+        if (!aligned16(x) || !aligned16(y) || (w && !aligned16(w)) || (bias && !aligned16(bias)))
+            return HEX_ERR_ALIGNMENT;
         const size_t need = packed_weight_bytes(d, g);
         if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
         void* wp = align_up(ws, 1024);
-        st = tc_pack_weights(w, wp, d->out_channels, d->in_channels, g.T, 0, s);
-        if (st != HEX_OK) return st;
+        if (w && (st = tc_pack_weights(w, wp, d->out_channels, d->in_channels, g.T, 0, s)) != HEX_OK) return st;
         TcConvArgs a{};
         a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
         a.x = x; a.wpack = wp; a.bias = bias; a.y = y; a.relu_y = nullptr; a.relu = fuse_relu;
         return tc_conv_fwd(a, s);
     }
+    if (!w) return HEX_ERR_INVALID_ARG;  // w == NULL (prepacked) only on the tensor-core path
     if (use_smallc(d, g)) {
         if (((uintptr_t)y & 3) != 0) return HEX_ERR_ALIGNMENT;
         return smallc_fwd(x, w, bias, y, g, d->out_channels, fuse_relu, s);
@@ -375,18 +376,17 @@ hex_status_t hex_conv2d_fwd_maxpool(const hex_conv2d_desc_t* d, const void* x, c
     Geom g;
     hex_status_t st = conv_geom(d, &g);
     if (st != HEX_OK) return st;
-    if (!x || !w || !y_pool || !argmax) return HEX_ERR_INVALID_ARG;
+    if (!x || !y_pool || !argmax) return HEX_ERR_INVALID_ARG;
     if (!use_tc_fwd(d, g) || !tc_conv_maxpool_supported(g, d->in_channels, d->out_channels))
         return HEX_ERR_UNSUPPORTED;
-    if (!aligned16(x) || !aligned16(y_pool) || !aligned16(w) || ((uintptr_t)argmax & 7) ||
+    if (!aligned16(x) || !aligned16(y_pool) || (w && !aligned16(w)) || ((uintptr_t)argmax & 7) ||
         (bias && !aligned16(bias)))
         return HEX_ERR_ALIGNMENT;
     const size_t need = packed_weight_bytes(d, g);
     if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
     cudaStream_t s = (cudaStream_t)stream;
     void* wp = align_up(ws, 1024);
-    st = tc_pack_weights(w, wp, d->out_channels, d->in_channels, g.T, 0, s);
-    if (st != HEX_OK) return st;
+    if (w && (st = tc_pack_weights(w, wp, d->out_channels, d->in_channels, g.T, 0, s)) != HEX_OK) return st;
     TcConvArgs a{};
     a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
     a.x = x; a.wpack = wp; a.bias = bias; a.y = nullptr; a.relu_y = nullptr; a.relu = fuse_relu;
@@ -398,22 +398,22 @@ hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* d, const void* dy, con
     Geom g;
     hex_status_t st = conv_geom(d, &g);
     if (st != HEX_OK) return st;
-    if (!dy || !w || !dx) return HEX_ERR_INVALID_ARG;
+    if (!dy || !dx) return HEX_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     if (use_tc_bwd_data(d, g)) {
-        if (!aligned16(dy) || !aligned16(dx) || !aligned16(w) || (relu_y && !aligned16(relu_y)))
+        if (!aligned16(dy) || !aligned16(dx) || (w && !aligned16(w)) || (relu_y && !aligned16(relu_y)))
             return HEX_ERR_ALIGNMENT;
         const size_t need = packed_weight_bytes(d, g);
         if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
         void* wp = align_up(ws, 1024);
         // stride 1: dx = fwd conv of dy with W'[ci][co][t] = W[co][ci][T-1-t] (P18)
-        st = tc_pack_weights(w, wp, d->out_channels, d->in_channels, g.T, 1, s);
-        if (st != HEX_OK) return st;
+        if (w && (st = tc_pack_weights(w, wp, d->out_channels, d->in_channels, g.T, 1, s)) != HEX_OK) return st;
         TcConvArgs a{};
         a.g = g; a.Cin = d->out_channels; a.Cout = d->in_channels;
         a.x = dy; a.wpack = wp; a.bias = nullptr; a.y = dx; a.relu_y = relu_y; a.relu = 0;
         return tc_conv_fwd(a, s);
     }
+    if (!w) return HEX_ERR_INVALID_ARG;  // w == NULL (prepacked) only on the stride-1 tensor-core path
     if (use_tc_bwd_data_up(d, g)) {  // stride s: the stride-1 bwd-data of dy scattered onto the full grid
         if (!aligned16(dy) || !aligned16(dx) || !aligned16(w) || (relu_y && !aligned16(relu_y)))
             return HEX_ERR_ALIGNMENT;
@@ -436,6 +436,35 @@ hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* d, const void* dy, con
     DirectConvArgs a = make_direct(d, g);
     a.dy = dy; a.w = w; a.relu_y = relu_y; a.dx = dx;
     return direct_conv_bwd_data(a, s);
+}
+
+hex_status_t hex_conv2d_pack_weights(int32_t count, const hex_conv2d_desc_t* descs, const int32_t* passes,
+                                     const void* const* w, void* const* ws, const size_t* ws_bytes,
+                                     hex_stream_t stream) {
+    if (count < 0 || count > HEX_PACK_MAX) return HEX_ERR_INVALID_ARG;
+    if (count == 0) return HEX_OK;
+    if (!descs || !passes || !w || !ws || !ws_bytes) return HEX_ERR_INVALID_ARG;
+    PackSegs segs{};
+    int64_t begin = 0;
+    for (int i = 0; i < count; ++i) {
+        const hex_conv2d_desc_t* d = &descs[i];
+        Geom g;
+        const hex_status_t st = conv_geom(d, &g);
+        if (st != HEX_OK) return st;
+        if (!w[i] || !ws[i]) return HEX_ERR_INVALID_ARG;
+        if (passes[i] != 0 && passes[i] != 1) return HEX_ERR_INVALID_ARG;
+        if (!(passes[i] == 0 ? use_tc_fwd(d, g) : use_tc_bwd_data(d, g))) return HEX_ERR_UNSUPPORTED;
+        if (ws_bytes[i] < packed_weight_bytes(d, g)) return HEX_ERR_WORKSPACE;
+        if (!aligned16(w[i])) return HEX_ERR_ALIGNMENT;
+        PackSeg& sg = segs.seg[i];
+        sg.begin = begin;
+        sg.Cout = d->out_channels; sg.Cin = d->in_channels; sg.T = g.T; sg.tr = passes[i];
+        sg.w = w[i];
+        sg.wpack = align_up(ws[i], 1024);
+        begin += (int64_t)g.T * sg.Cout * sg.Cin;
+    }
+    segs.count = count;
+    return tc_pack_weights_multi(segs, (cudaStream_t)stream);
 }
 
 hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* d, const void* x, const void* dy, float* dw,

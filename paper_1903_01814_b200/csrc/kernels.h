@@ -79,6 +79,18 @@ hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax,
 hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st);
 hex_status_t tc_pack_weights(const void* w, void* wpack, int Cout, int Cin, int T, int transpose_reverse,
                              cudaStream_t st);
+struct PackSeg {  // one layer / pass of a batched weight packing
+    int64_t begin;  // first flat element index of this segment
+    int Cout, Cin, T, tr;
+    const void* w;
+    void* wpack;
+};
+constexpr int HEX_PACK_MAX = 16;
+struct PackSegs {
+    int count;
+    PackSeg seg[HEX_PACK_MAX];
+};
+hex_status_t tc_pack_weights_multi(const PackSegs& segs, cudaStream_t st);
 
 struct TcWgradArgs {
     Geom g;

@@ -607,6 +607,42 @@ __global__ void pack_weights_kernel(const __nv_bfloat16* __restrict__ w, __nv_bf
     }
 }
 
+// several layers / passes in one launch (hex_conv2d_pack_weights): thread idx belongs to the segment whose
+// [begin, begin + T*Cout*Cin) range holds it
+__global__ void pack_weights_multi_kernel(const PackSegs segs) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int k = 0;
+    while (k + 1 < segs.count && idx >= segs.seg[k + 1].begin) ++k;
+    const PackSeg& sg = segs.seg[k];
+    const int64_t i = idx - sg.begin;
+    const int64_t total = (int64_t)sg.T * sg.Cout * sg.Cin;
+    if (i < 0 || i >= total) return;
+    const __nv_bfloat16* w = (const __nv_bfloat16*)sg.w;
+    __nv_bfloat16* wp = (__nv_bfloat16*)sg.wpack;
+    if (!sg.tr) {
+        const int ci = (int)(i % sg.Cin);
+        const int64_t q = i / sg.Cin;
+        const int co = (int)(q % sg.Cout);
+        const int t = (int)(q / sg.Cout);
+        wp[i] = w[((int64_t)co * sg.Cin + ci) * sg.T + t];
+    } else {
+        const int co = (int)(i % sg.Cout);
+        const int64_t q = i / sg.Cout;
+        const int ci = (int)(q % sg.Cin);
+        const int t = (int)(q / sg.Cin);
+        wp[i] = w[((int64_t)co * sg.Cin + ci) * sg.T + (sg.T - 1 - t)];
+    }
+}
+
+hex_status_t tc_pack_weights_multi(const PackSegs& segs, cudaStream_t st) {
+    if (segs.count <= 0) return HEX_OK;
+    const PackSeg& last = segs.seg[segs.count - 1];
+    const int64_t total = last.begin + (int64_t)last.T * last.Cout * last.Cin;
+    pack_weights_multi_kernel<<<ceil_div(total, 256), 256, 0, st>>>(segs);
+    count_launch();
+    return last_launch_status();
+}
+
 hex_status_t tc_pack_weights(const void* w, void* wpack, int Cout, int Cin, int T, int tr, cudaStream_t st) {
     const int64_t total = (int64_t)T * Cout * Cin;
     pack_weights_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)wpack, Cout,

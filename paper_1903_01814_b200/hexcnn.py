@@ -171,13 +171,29 @@ class HexCNN:
                 self.pooled[l] = torch.empty(B, ho, wo, co, dtype=bf, device=dev)
                 self.argmax[l] = torch.empty(B, ho, wo, co, dtype=torch.uint8, device=dev)
                 self.dpool[l] = torch.empty(B, ho, wo, co, dtype=bf, device=dev)
-        import os
         # fused conv + ReLU + max pool (hex_conv2d_fwd_maxpool) where supported; HEXCNN_NO_FUSED_POOL=1
         # restores the separate conv and pool calls
         self.fused_pool = {l: bool(L_.hex_conv2d_fwd_maxpool_supported(ctypes.byref(self.desc[l])))
                            and not os.environ.get("HEXCNN_NO_FUSED_POOL") for l in self.pool_geo}
         self.pdesc = {l: A.PoolDesc(B, self.channels[l + 1], *self.pool_geo[l][:2], 1, 2, 0, _BF16, _NHWC,
                                     A.POOL_MAX) for l in self.pool_geo}
+        # tensor-core layers read their weights pre-packed (hex_conv2d_pack_weights: every layer's fwd and
+        # bwd-data packing in one launch per step instead of one per call); HEXCNN_NO_PREPACK=1 packs per call
+        entries = []
+        self.packed = set()  # (layer, pass)
+        if not os.environ.get("HEXCNN_NO_PREPACK"):
+            for l in range(self.L):
+                for pass_id in (0, 1):
+                    if pass_id == 1 and l == 0:
+                        continue  # no bwd-data into the network input
+                    algo = ctypes.c_int32()
+                    A.check(L_.hex_conv2d_algo(ctypes.byref(self.desc[l]), pass_id, ctypes.byref(algo)), "algo")
+                    if algo.value != 1 or self.desc[l].stride != 1:
+                        continue
+                    entries.append((self.desc[l], pass_id, self.weight(l).data_ptr(), self.ws[l][pass_id].data_ptr(),
+                                    self.ws_sizes[l][pass_id]))
+                    self.packed.add((l, pass_id))
+        self.pack_args = A.PackArgs(entries) if entries else None
         C = self.channels[-1]
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
         hw = self.feat_hw[0] * self.feat_hw[1]
@@ -204,8 +220,14 @@ class HexCNN:
             e.record()
             self.timer.append((kind, l, e0, e))
 
+    def _w(self, l, pass_id):
+        """Weight pointer of a conv call: None (NULL) where the packed copy in the pass workspace is current."""
+        return None if (l, pass_id) in self.packed else _p(self.weight(l))
+
     def forward(self, x, stream):
         L = A.lib()
+        if self.pack_args is not None:
+            self.pack_args.run(stream)
         for l in range(self.L):
             xin = self.layer_input(l, x)
             ws = self.ws[l][0]
@@ -213,13 +235,13 @@ class HexCNN:
                 # conv -> ReLU -> max pool in one kernel: act[l] is never written (the backward needs
                 # only the pooled tensor and the argmax, see backward())
                 e0 = self._tic()
-                A.check(L.hex_conv2d_fwd_maxpool(ctypes.byref(self.desc[l]), _p(xin), _p(self.weight(l)),
+                A.check(L.hex_conv2d_fwd_maxpool(ctypes.byref(self.desc[l]), _p(xin), self._w(l, 0),
                                                  _p(self.bias(l)), 1, _p(self.pooled[l]), _p(self.argmax[l]),
                                                  _p(ws), self.ws_sizes[l][0], stream), f"conv{l + 1} fwd+pool")
                 self._toc("fwd_pool", l, e0)
                 continue
             e0 = self._tic()
-            A.check(L.hex_conv2d_fwd(ctypes.byref(self.desc[l]), _p(xin), _p(self.weight(l)), _p(self.bias(l)), 1,
+            A.check(L.hex_conv2d_fwd(ctypes.byref(self.desc[l]), _p(xin), self._w(l, 0), _p(self.bias(l)), 1,
                                      _p(self.act[l]), _p(ws), self.ws_sizes[l][0], stream), f"conv{l + 1} fwd")
             self._toc("fwd", l, e0)
             if l in self.pool_geo:
@@ -265,7 +287,7 @@ class HexCNN:
             e0 = self._tic()
             if prev in self.pool_geo:
                 # dgrad into the pooled tensor, masked by pooled > 0 (== ReLU mask at the argmax cell)
-                A.check(L.hex_conv2d_bwd_data(ctypes.byref(self.desc[l]), _p(dy), _p(self.weight(l)),
+                A.check(L.hex_conv2d_bwd_data(ctypes.byref(self.desc[l]), _p(dy), self._w(l, 1),
                                               _p(self.pooled[prev]), _p(self.dpool[prev]), _p(self.ws[l][1]),
                                               self.ws_sizes[l][1], stream), f"conv{l + 1} dgrad")
                 self._toc("dgrad", l, e0)
@@ -274,7 +296,7 @@ class HexCNN:
                                          _p(self.argmax[prev]), _p(self.dact[prev]), stream), f"pool{prev + 1} bwd")
                 self._toc("pool_bwd", prev, e0)
             else:
-                A.check(L.hex_conv2d_bwd_data(ctypes.byref(self.desc[l]), _p(dy), _p(self.weight(l)),
+                A.check(L.hex_conv2d_bwd_data(ctypes.byref(self.desc[l]), _p(dy), self._w(l, 1),
                                               _p(self.act[prev]), _p(self.dact[prev]), _p(self.ws[l][1]),
                                               self.ws_sizes[l][1], stream), f"conv{l + 1} dgrad")
                 self._toc("dgrad", l, e0)

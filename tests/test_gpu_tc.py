@@ -205,3 +205,82 @@ def test_fused_conv_maxpool_unsupported_shape(F):
     with pytest.raises(HexError) as e:
         F.conv2d_fwd_maxpool(x, w, None, n=2)
     assert e.value.status == 8
+
+
+@pytest.mark.parametrize("pi", [0, 1])
+def test_pack_weights_prepacked_calls_bit_identical(F, pi):
+    # hex_conv2d_pack_weights packs several layers / passes in ONE launch; fwd, fwd_maxpool and bwd_data
+    # called with w = NULL on those workspaces are bit-identical to the calls that pack per call
+    import ctypes
+    from paper_1903_01814_b200 import _abi as A
+    from paper_1903_01814_b200.functional import _workspace, conv_desc
+    L = A.lib()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    p = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())
+    g = torch.Generator().manual_seed(31 + pi)
+    layers = [(2, 64, 128, 12, 13, 2), (2, 128, 64, 14, 16, 1)]
+    tens, entries = [], []
+    for (B, Ci, Co, H, W, n) in layers:
+        T = A.num_taps(n)
+        d = conv_desc(B, Ci, Co, H, W, n, 1, pi, torch.bfloat16, "NHWC")
+        x = torch.randn(B, H, W, Ci, generator=g).to(torch.bfloat16).cuda()
+        dy = torch.randn(B, H, W, Co, generator=g).to(torch.bfloat16).cuda()
+        w = (torch.randn(Co, Ci, T, generator=g) / np.sqrt(Ci * T)).to(torch.bfloat16).cuda()
+        b = (0.1 * torch.randn(Co, generator=g)).cuda()
+        ws = [_workspace(d, k, "cuda") for k in (0, 1)]
+        tens.append((d, x, dy, w, b, ws))
+        for k in (0, 1):
+            entries.append((d, k, w.data_ptr(), ws[k][0].data_ptr(), ws[k][1]))
+
+    def run(prepacked):
+        outs = []
+        for (d, x, dy, w, b, ws) in tens:
+            wa = None if prepacked else p(w)
+            B, H, W, Ci = x.shape
+            Co = dy.shape[-1]
+            y = torch.empty(B, H, W, Co, dtype=torch.bfloat16, device="cuda")
+            A.check(L.hex_conv2d_fwd(ctypes.byref(d), p(x), wa, p(b), 1, p(y), p(ws[0][0]), ws[0][1], st), "fwd")
+            dx = torch.empty_like(x)
+            A.check(L.hex_conv2d_bwd_data(ctypes.byref(d), p(dy), wa, p(x), p(dx), p(ws[1][0]), ws[1][1], st), "dgrad")
+            outs += [y, dx]
+            if L.hex_conv2d_fwd_maxpool_supported(ctypes.byref(d)):
+                Ho, Wo, _ = A.output_shape(H, W, 2, pi)
+                yp = torch.empty(B, Ho, Wo, Co, dtype=torch.bfloat16, device="cuda")
+                am = torch.empty(B, Ho, Wo, Co, dtype=torch.uint8, device="cuda")
+                A.check(L.hex_conv2d_fwd_maxpool(ctypes.byref(d), p(x), wa, p(b), 1, p(yp), p(am), p(ws[0][0]),
+                                                 ws[0][1], st), "fwd_maxpool")
+                outs += [yp, am]
+        return outs
+
+    ref = run(False)
+    for (d, x, dy, w, b, ws) in tens:
+        for k in (0, 1):
+            ws[k][0].zero_()
+    n0 = A.launch_count()
+    A.PackArgs(entries).run(st)
+    assert A.launch_count() - n0 == 1  # one launch for every layer and pass
+    got = run(True)
+    torch.cuda.synchronize()
+    assert len(got) == len(ref) and len(ref) >= 5
+    for a, r in zip(got, ref):
+        assert torch.equal(a.view(torch.uint8), r.view(torch.uint8))
+
+
+def test_pack_weights_rejects(F):
+    import ctypes
+    from paper_1903_01814_b200 import _abi as A
+    from paper_1903_01814_b200.functional import _workspace, conv_desc
+    L = A.lib()
+    d32 = conv_desc(2, 16, 32, 8, 8, 1, 1, 0, torch.float32, "NCHW")
+    w = torch.zeros(32, 16, 7, device="cuda")
+    ws, nb = _workspace(d32, 0, "cuda")
+    ws = ws if ws is not None else torch.zeros(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(A.HexError) as e:  # not a bf16 tensor-core pass
+        A.PackArgs([(d32, 0, w.data_ptr(), ws.data_ptr(), max(nb, 16))]).run(None)
+    assert e.value.status == 8
+    x = torch.zeros(2, 16, 8, 8, device="cuda")
+    y = torch.zeros(2, 32, 8, 8, device="cuda")
+    st = L.hex_conv2d_fwd(ctypes.byref(d32), ctypes.c_void_p(x.data_ptr()), None, None, 0,
+                          ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(ws.data_ptr()), nb, None)
+    assert st == 1  # w == NULL off the tensor-core path
+    assert L.hex_conv2d_pack_weights(17, None, None, None, None, None, None) == 1
