@@ -192,6 +192,15 @@ HEX_API hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* desc, const 
  * HEX_ERR_UNSUPPORTED when no fused kernel covers the shape (the caller then
  * runs the two passes); hex_conv2d_fwd_maxpool_supported answers up front. */
 HEX_API int32_t hex_conv2d_fwd_maxpool_supported(const hex_conv2d_desc_t* desc);
+/* The same fused kernel for either pooling mode ("hex max/avg pool in one epilogue"):
+ * mode HEX_POOL_MAX as hex_conv2d_fwd_maxpool, HEX_POOL_AVG the in-grid average (A8) of the bf16
+ * conv outputs -- fp32 sum in canonical tap order times 1/count, RNE, bit-identical to hex_conv2d_fwd
+ * followed by hex_pool2d_fwd(HEX_POOL_AVG) -- with argmax_tap ignored (may be NULL).
+ * HEX_POOL_AVG_PAD has no fused kernel: HEX_ERR_UNSUPPORTED (as for unsupported shapes). */
+HEX_API int32_t hex_conv2d_fwd_pool_supported(const hex_conv2d_desc_t* desc, int32_t mode);
+HEX_API hex_status_t hex_conv2d_fwd_pool(const hex_conv2d_desc_t* desc, int32_t mode, const void* x,
+                                         const void* w, const float* bias, int32_t fuse_relu, void* y_pool,
+                                         uint8_t* argmax_tap, void* ws, size_t ws_bytes, hex_stream_t stream);
 HEX_API hex_status_t hex_conv2d_fwd_maxpool(const hex_conv2d_desc_t* desc, const void* x, const void* w,
                                             const float* bias, int32_t fuse_relu, void* y_pool,
                                             uint8_t* argmax_tap, void* ws, size_t ws_bytes,

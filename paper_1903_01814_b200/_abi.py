@@ -85,6 +85,8 @@ _SIGS = {
     "hex_conv2d_fwd": (_i32, [_CDP, _vp, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
     "hex_conv2d_fwd_maxpool_supported": (_i32, [_CDP]),
     "hex_conv2d_fwd_maxpool": (_i32, [_CDP, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "hex_conv2d_fwd_pool_supported": (_i32, [_CDP, _i32]),
+    "hex_conv2d_fwd_pool": (_i32, [_CDP, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp]),
     "hex_conv2d_bwd_data": (_i32, [_CDP, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "hex_conv2d_bwd_weight": (_i32, [_CDP, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
     "hex_conv2d_pack_weights": (_i32, [_i32, _CDP, _i32p, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _szp, _vp]),

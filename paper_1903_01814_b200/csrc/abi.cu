@@ -364,23 +364,24 @@ hex_status_t hex_conv2d_fwd(const hex_conv2d_desc_t* d, const void* x, const voi
     return direct_conv_fwd(a, s);
 }
 
-int32_t hex_conv2d_fwd_maxpool_supported(const hex_conv2d_desc_t* d) {
+int32_t hex_conv2d_fwd_pool_supported(const hex_conv2d_desc_t* d, int32_t mode) {
     Geom g;
     if (conv_geom(d, &g) != HEX_OK) return 0;
-    return use_tc_fwd(d, g) && tc_conv_maxpool_supported(g, d->in_channels, d->out_channels) ? 1 : 0;
+    return use_tc_fwd(d, g) && tc_conv_pool_supported(g, d->in_channels, d->out_channels, mode) ? 1 : 0;
 }
 
-hex_status_t hex_conv2d_fwd_maxpool(const hex_conv2d_desc_t* d, const void* x, const void* w, const float* bias,
-                                    int32_t fuse_relu, void* y_pool, uint8_t* argmax, void* ws, size_t ws_bytes,
-                                    hex_stream_t stream) {
+hex_status_t hex_conv2d_fwd_pool(const hex_conv2d_desc_t* d, int32_t mode, const void* x, const void* w,
+                                 const float* bias, int32_t fuse_relu, void* y_pool, uint8_t* argmax, void* ws,
+                                 size_t ws_bytes, hex_stream_t stream) {
     Geom g;
     hex_status_t st = conv_geom(d, &g);
     if (st != HEX_OK) return st;
-    if (!x || !y_pool || !argmax) return HEX_ERR_INVALID_ARG;
-    if (!use_tc_fwd(d, g) || !tc_conv_maxpool_supported(g, d->in_channels, d->out_channels))
+    if (mode != HEX_POOL_MAX && mode != HEX_POOL_AVG && mode != HEX_POOL_AVG_PAD) return HEX_ERR_INVALID_ARG;
+    if (!x || !y_pool || (mode == HEX_POOL_MAX && !argmax)) return HEX_ERR_INVALID_ARG;
+    if (!use_tc_fwd(d, g) || !tc_conv_pool_supported(g, d->in_channels, d->out_channels, mode))
         return HEX_ERR_UNSUPPORTED;
-    if (!aligned16(x) || !aligned16(y_pool) || (w && !aligned16(w)) || ((uintptr_t)argmax & 7) ||
-        (bias && !aligned16(bias)))
+    if (!aligned16(x) || !aligned16(y_pool) || (w && !aligned16(w)) ||
+        (mode == HEX_POOL_MAX && ((uintptr_t)argmax & 7)) || (bias && !aligned16(bias)))
         return HEX_ERR_ALIGNMENT;
     const size_t need = packed_weight_bytes(d, g);
     if (!ws || ws_bytes < need) return HEX_ERR_WORKSPACE;
@@ -390,7 +391,17 @@ hex_status_t hex_conv2d_fwd_maxpool(const hex_conv2d_desc_t* d, const void* x, c
     TcConvArgs a{};
     a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
     a.x = x; a.wpack = wp; a.bias = bias; a.y = nullptr; a.relu_y = nullptr; a.relu = fuse_relu;
-    return tc_conv_maxpool(a, y_pool, argmax, s);
+    return tc_conv_pool(a, mode, y_pool, mode == HEX_POOL_MAX ? argmax : nullptr, s);
+}
+
+int32_t hex_conv2d_fwd_maxpool_supported(const hex_conv2d_desc_t* d) {
+    return hex_conv2d_fwd_pool_supported(d, HEX_POOL_MAX);
+}
+
+hex_status_t hex_conv2d_fwd_maxpool(const hex_conv2d_desc_t* d, const void* x, const void* w, const float* bias,
+                                    int32_t fuse_relu, void* y_pool, uint8_t* argmax, void* ws, size_t ws_bytes,
+                                    hex_stream_t stream) {
+    return hex_conv2d_fwd_pool(d, HEX_POOL_MAX, x, w, bias, fuse_relu, y_pool, argmax, ws, ws_bytes, stream);
 }
 
 hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* d, const void* dy, const void* w, const void* relu_y,

@@ -72,10 +72,10 @@ hex_status_t lattice_upsample(const void* dy, void* up, const Geom& g, int C, cu
 bool tc_fwd_tr_supported(const Geom& g, int Cin, int Cout);  // tap-reuse forward (tc_fwd_tr.cu)
 hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st);
 // fused maxpool_{n=1,s=2}(relu(conv(x) + bias)) (tc_fwd_tr.cu); the conv output is not materialised
-bool tc_conv_maxpool_supported(const Geom& g, int Cin, int Cout);
+bool tc_conv_pool_supported(const Geom& g, int Cin, int Cout, int mode);  // fused conv + ReLU + pool (max / avg)
 bool tc_conv3d_supported(const Geom& g, int Cin, int Cout, int Do);
 hex_status_t tc_conv3d_fwd(const TcConvArgs& a, int D, int Do, int sd, int kd, cudaStream_t st);
-hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax, cudaStream_t st);
+hex_status_t tc_conv_pool(const TcConvArgs& a, int mode, void* y_pool, uint8_t* argmax, cudaStream_t st);
 hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st);
 hex_status_t tc_pack_weights(const void* w, void* wpack, int Cout, int Cin, int T, int transpose_reverse,
                              cudaStream_t st);

@@ -609,7 +609,7 @@ __device__ __forceinline__ void fp_issue_n1(uint32_t d0, uint32_t d1, uint64_t a
     }
 }
 
-template <int BN, int N, bool PAIR>
+template <int BN, int N, bool PAIR, bool AVG>
 __global__ void __launch_bounds__(FP_THREADS, 1)
 tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_constant__ CUtensorMap map_x1,
                        const __grid_constant__ CUtensorMap map_w, const __grid_constant__ FpParams p) {
@@ -901,7 +901,39 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
                 if (tl.strip && !tl.last && et < 128)  // rows r0+14, r0+15 carry into the next tile
                     *reinterpret_cast<uint4*>(carry + c * FP_CARRY + kcar) =
                         *reinterpret_cast<const uint4*>(rb + soff);
-                if (valid) {
+                if (valid && AVG) {
+                    // average over the in-grid taps (A8): fp32 sum in canonical tap order from 0, times
+                    // 1/count, RNE -- the operations of the unfused NHWC average pool on the bf16 conv output
+                    const int c2 = 2 * C;
+                    const bool cl = c2 >= 1, cm = true, crt = c2 + 1 < p.W;
+                    const int rs0 = cr + top1, rs1 = cr + top1 + 1;
+                    const bool ok[7] = {cl && rs0 >= 0 && rs0 < p.H, cl && rs1 >= 0 && rs1 < p.H,
+                                        cm && cr - 1 >= 0, cm, cm && cr + 1 < p.H,
+                                        crt && rs0 >= 0 && rs0 < p.H, crt && rs1 >= 0 && rs1 < p.H};
+                    const int offs[7] = {ol0, ol1, oc0, oc1, oc2, or0, or1};
+                    float sum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                    int cnt = 0;
+#pragma unroll
+                    for (int t = 0; t < 7; ++t) {
+                        if (!ok[t]) continue;
+                        const uint4 q = *reinterpret_cast<const uint4*>(rb + offs[t]);
+                        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            sum[2 * kk] += __uint_as_float(w4[kk] << 16);
+                            sum[2 * kk + 1] += __uint_as_float(w4[kk] & 0xffff0000u);
+                        }
+                        ++cnt;
+                    }
+                    const float inv = 1.f / (float)cnt;
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        __nv_bfloat162 h = __floats2bfloat162_rn(sum[2 * kk] * inv, sum[2 * kk + 1] * inv);
+                        pk[kk] = *reinterpret_cast<uint32_t*>(&h);
+                    }
+                    *reinterpret_cast<uint4*>(p.y + obase + c * 32) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                } else if (valid) {
                     uint4 tv[7];
                     tv[0] = *reinterpret_cast<const uint4*>(rb + ol0);
                     tv[1] = *reinterpret_cast<const uint4*>(rb + ol1);
@@ -1613,15 +1645,16 @@ FpPlan fp_plan(const Geom& g, int Cin, int Cout) {
 }
 }  // namespace
 
-bool tc_conv_maxpool_supported(const Geom& g, int Cin, int Cout) {
+bool tc_conv_pool_supported(const Geom& g, int Cin, int Cout, int mode) {
     if (sw_on("HEXCONV_NO_FUSED_POOL") || !ft_encode()) return false;
+    if (mode != HEX_POOL_MAX && mode != HEX_POOL_AVG) return false;
     return fp_plan(g, Cin, Cout).ok;
 }
 
-hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax, cudaStream_t st) {
+hex_status_t tc_conv_pool(const TcConvArgs& a, int mode, void* y_pool, uint8_t* argmax, cudaStream_t st) {
     const Geom& g = a.g;
     const FpPlan pl = fp_plan(g, a.Cin, a.Cout);
-    if (!pl.ok) return HEX_ERR_UNSUPPORTED;
+    if (!pl.ok || (mode != HEX_POOL_MAX && mode != HEX_POOL_AVG)) return HEX_ERR_UNSUPPORTED;
     FpParams p{};
     p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
     p.Ho = pl.Ho; p.Wo = pl.Wo; p.nr = pl.nr; p.nc = pl.nc;
@@ -1644,7 +1677,8 @@ hex_status_t tc_conv_maxpool(const TcConvArgs& a, void* y_pool, uint8_t* argmax,
     if (!ft_wmap(&mw, a.wpack, g.T, a.Cout, a.Cin, pl.pair ? a.Cout / 2 : a.Cout)) return HEX_ERR_CUDA;
 #define HEX_FP(BN_, N_, PAIR_)                                                                                \
     {                                                                                                         \
-        auto kern = tc_conv_maxpool_kernel<BN_, N_, PAIR_>;                                                   \
+        auto kern = mode == HEX_POOL_AVG ? tc_conv_maxpool_kernel<BN_, N_, PAIR_, true>                      \
+                                         : tc_conv_maxpool_kernel<BN_, N_, PAIR_, false>;                     \
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem) != cudaSuccess) \
             return HEX_ERR_CUDA;                                                                              \
         if (PAIR_) {                                                                                          \

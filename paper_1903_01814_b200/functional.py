@@ -143,6 +143,31 @@ def conv2d_fwd_maxpool(x, w, bias=None, n: int = 1, parity: int = 0, relu: bool 
     return y, am
 
 
+def conv2d_fwd_avgpool(x, w, bias=None, n: int = 1, parity: int = 0, relu: bool = True, layout: str = "NHWC"):
+    """y = hex average pool (n = 1, stride 2, in-grid count) of relu?(hexconv(x, w) + bias), fused
+    (hex_conv2d_fwd_pool, HEX_POOL_AVG); bit-identical to conv2d_fwd followed by pool2d_fwd(mode="avg")."""
+    _check_cuda(x, w, bias)
+    B, Cin, H, W = _dims(x, layout)
+    _dtype_ok(x)
+    Cout = w.shape[0]
+    _expect(w, (Cout, Cin, A.num_taps(n)), x.dtype, "w")
+    _expect(bias, (Cout,), torch.float32, "bias")
+    d = conv_desc(B, Cin, Cout, H, W, n, 1, parity, x.dtype, layout)
+    Ho, Wo, _ = A.output_shape(H, W, 2, parity)
+    y = torch.empty(_shape(layout, B, Cout, Ho, Wo), dtype=x.dtype, device=x.device)
+    ws, nb = _workspace(d, 0, x.device)
+    A.check(A.lib().hex_conv2d_fwd_pool(ctypes.byref(d), A.POOL_AVG, _ptr(x), _ptr(w), _ptr(bias), int(relu),
+                                        _ptr(y), None, _ptr(ws), nb, _stream()), "hex_conv2d_fwd_pool")
+    return y
+
+
+def conv2d_fwd_pool_supported(B, Cin, Cout, H, W, n, parity=0, mode="max", dtype=torch.bfloat16,
+                              layout="NHWC") -> bool:
+    d = conv_desc(B, Cin, Cout, H, W, n, 1, parity, dtype, layout)
+    m = {"max": A.POOL_MAX, "avg": A.POOL_AVG, "avg_pad": A.POOL_AVG_PAD}[mode]
+    return bool(A.lib().hex_conv2d_fwd_pool_supported(ctypes.byref(d), m))
+
+
 def conv2d_fwd_maxpool_supported(B, Cin, Cout, H, W, n, parity=0, dtype=torch.bfloat16, layout="NHWC") -> bool:
     d = conv_desc(B, Cin, Cout, H, W, n, 1, parity, dtype, layout)
     return bool(A.lib().hex_conv2d_fwd_maxpool_supported(ctypes.byref(d)))

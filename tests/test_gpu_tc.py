@@ -284,3 +284,26 @@ def test_pack_weights_rejects(F):
                           ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(ws.data_ptr()), nb, None)
     assert st == 1  # w == NULL off the tensor-core path
     assert L.hex_conv2d_pack_weights(17, None, None, None, None, None, None) == 1
+
+
+@pytest.mark.parametrize("pi", [0, 1])
+def test_fused_conv_relu_avgpool(F, oracle, pi):
+    # hex_conv2d_fwd_pool(HEX_POOL_AVG) (max/avg pool in the conv epilogue): bit-identical to
+    # the unfused conv + ReLU + average pool in strip mode (B = 25: whole rounds of strips) and region mode
+    # (B = 2), ragged bottoms and edges (in-grid counts 3..7), and within the bf16 tolerance of the oracle
+    # pool of the GPU conv output
+    for (B, Cin, Cout, H, W, relu) in [(2, 64, 128, 30, 31, True), (25, 64, 64, 46, 90, True),
+                                       (3, 128, 64, 16, 16, False)]:
+        g = torch.Generator().manual_seed(980 + H + pi)
+        x = torch.randn(B, H, W, Cin, generator=g).to(torch.bfloat16).cuda()
+        w = (torch.randn(Cout, Cin, 7, generator=g) / np.sqrt(Cin * 7)).to(torch.bfloat16).cuda()
+        b = (0.2 * torch.randn(Cout, generator=g)).cuda()
+        assert F.conv2d_fwd_pool_supported(B, Cin, Cout, H, W, 1, pi, mode="avg")
+        ya = F.conv2d_fwd_avgpool(x, w, b, n=1, parity=pi, relu=relu)
+        yc = F.conv2d_fwd(x, w, b, n=1, parity=pi, relu=relu, layout="NHWC")
+        ya2, _ = F.pool2d_fwd(yc, 1, 2, pi, "avg", "NHWC")
+        torch.cuda.synchronize()
+        assert torch.equal(ya.view(torch.int16), ya2.view(torch.int16)), (pi, B, H, W)
+        pr, _ = oracle.pool2d_fwd(back(yc[-1:]), n=1, s=2, pi=pi, mode="avg")
+        assert rel(back(ya[-1:]), pr) <= 1e-2
+    assert not F.conv2d_fwd_pool_supported(2, 64, 64, 16, 16, 1, pi, mode="avg_pad")

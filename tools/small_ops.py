@@ -36,8 +36,25 @@ def c3_ops():
     }
 
 
+def c5_ops():
+    B, H, W, Ci, Co = 256, 96, 96, 64, 128
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(B, H, W, Ci, generator=g).to(torch.bfloat16).cuda()
+    w = (torch.randn(Co, Ci, 7, generator=g) / 21.0).to(torch.bfloat16).cuda()
+    b = torch.zeros(Co, device="cuda")
+    y = torch.empty(B, H, W, Co, dtype=torch.bfloat16, device="cuda")
+    return {
+        "c5_l2_fwd_maxpool": lambda: F.conv2d_fwd_maxpool(x, w, b, n=1),
+        "c5_l2_fwd_avgpool": lambda: F.conv2d_fwd_avgpool(x, w, b, n=1),
+        "c5_l2_fwd_then_avgpool": lambda: (F.conv2d_fwd(x, w, b, n=1, relu=True, layout="NHWC", out=y),
+                                           F.pool2d_fwd(y, 1, 2, 0, "avg", "NHWC")),
+    }
+
+
 def main():
     ops = c3_ops()
+    if any(a.startswith("c5") for a in sys.argv[1:]):
+        ops.update(c5_ops())
     sel = sys.argv[1:] or list(ops)
     gt = GraphTimer("cuda")
     for name in sel:
