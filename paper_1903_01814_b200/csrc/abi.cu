@@ -468,11 +468,11 @@ hex_status_t hex_conv2d_pack_weights(int32_t count, const hex_conv2d_desc_t* des
         if (ws_bytes[i] < packed_weight_bytes(d, g)) return HEX_ERR_WORKSPACE;
         if (!aligned16(w[i])) return HEX_ERR_ALIGNMENT;
         PackSeg& sg = segs.seg[i];
-        sg.begin = begin;
+        sg.row0 = begin;
         sg.Cout = d->out_channels; sg.Cin = d->in_channels; sg.T = g.T; sg.tr = passes[i];
         sg.w = w[i];
         sg.wpack = align_up(ws[i], 1024);
-        begin += (int64_t)g.T * sg.Cout * sg.Cin;
+        begin += sg.tr ? sg.Cin : sg.Cout;
     }
     segs.count = count;
     return tc_pack_weights_multi(segs, (cudaStream_t)stream);

@@ -80,7 +80,7 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st);
 hex_status_t tc_pack_weights(const void* w, void* wpack, int Cout, int Cin, int T, int transpose_reverse,
                              cudaStream_t st);
 struct PackSeg {  // one layer / pass of a batched weight packing
-    int64_t begin;  // first flat element index of this segment
+    int64_t row0;  // first block (row) of this segment: rows are co (forward layout) or ci (transposed)
     int Cout, Cin, T, tr;
     const void* w;
     void* wpack;

@@ -607,38 +607,79 @@ __global__ void pack_weights_kernel(const __nv_bfloat16* __restrict__ w, __nv_bf
     }
 }
 
-// several layers / passes in one launch (hex_conv2d_pack_weights): thread idx belongs to the segment whose
-// [begin, begin + T*Cout*Cin) range holds it
-__global__ void pack_weights_multi_kernel(const PackSegs segs) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// several layers / passes in one launch (hex_conv2d_pack_weights).  One block per ROW: (segment, co) for the
+// forward layout, (segment, ci) for the transposed one.  The block stages its contiguous (fwd) or
+// T-element-run (bwd) slice of w in shared memory, then writes whole contiguous output runs (coalesced
+// both ways); index division by float reciprocal with an exact correction (operands < 2^24).
+__device__ __forceinline__ int pk_div(int n, int d, float inv) {
+    int q = (int)((float)n * inv);
+    const int r = n - q * d;
+    if (r < 0) --q;
+    else if (r >= d) ++q;
+    return q;
+}
+
+constexpr int PK_THREADS = 256;
+
+__global__ void __launch_bounds__(PK_THREADS) pack_weights_multi_kernel(const PackSegs segs) {
+    extern __shared__ __align__(16) __nv_bfloat16 srow[];  // one row: Cin * T (fwd) or Cout * T (bwd) elements
     int k = 0;
-    while (k + 1 < segs.count && idx >= segs.seg[k + 1].begin) ++k;
+    while (k + 1 < segs.count && (int64_t)blockIdx.x >= segs.seg[k + 1].row0) ++k;
     const PackSeg& sg = segs.seg[k];
-    const int64_t i = idx - sg.begin;
-    const int64_t total = (int64_t)sg.T * sg.Cout * sg.Cin;
-    if (i < 0 || i >= total) return;
+    const int row = (int)(blockIdx.x - sg.row0);
     const __nv_bfloat16* w = (const __nv_bfloat16*)sg.w;
     __nv_bfloat16* wp = (__nv_bfloat16*)sg.wpack;
-    if (!sg.tr) {
-        const int ci = (int)(i % sg.Cin);
-        const int64_t q = i / sg.Cin;
-        const int co = (int)(q % sg.Cout);
-        const int t = (int)(q / sg.Cout);
-        wp[i] = w[((int64_t)co * sg.Cin + ci) * sg.T + t];
-    } else {
-        const int co = (int)(i % sg.Cout);
-        const int64_t q = i / sg.Cout;
-        const int ci = (int)(q % sg.Cin);
-        const int t = (int)(q / sg.Cin);
-        wp[i] = w[((int64_t)co * sg.Cin + ci) * sg.T + (sg.T - 1 - t)];
+    const int T = sg.T, Cin = sg.Cin, Cout = sg.Cout;
+    const float invT = 1.f / (float)T;
+    if (!sg.tr) {  // wp[t][co][ci] = w[co][ci][t], row = co
+        const int n = Cin * T;
+        const __nv_bfloat16* src = w + (int64_t)row * n;
+        if ((n & 7) == 0 && ((uintptr_t)src & 15) == 0) {  // 16-byte copies
+#pragma unroll 4
+            for (int i = threadIdx.x; i < n / 8; i += PK_THREADS)
+                reinterpret_cast<uint4*>(srow)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+        } else {
+#pragma unroll 8
+            for (int i = threadIdx.x; i < n; i += PK_THREADS) srow[i] = src[i];
+        }
+        __syncthreads();
+        const float invC = 1.f / (float)Cin;
+        for (int i = threadIdx.x; i < n; i += PK_THREADS) {
+            const int t = pk_div(i, Cin, invC), ci = i - t * Cin;
+            wp[((int64_t)t * Cout + row) * Cin + ci] = srow[ci * T + t];
+        }
+    } else {  // wp[t][ci][co] = w[co][ci][T-1-t], row = ci
+        const int n = Cout * T;
+#pragma unroll 8
+        for (int i = threadIdx.x; i < n; i += PK_THREADS) {  // runs of T elements, 8 loads in flight
+            const int co = pk_div(i, T, invT), t = i - co * T;
+            srow[i] = w[((int64_t)co * Cin + row) * T + t];
+        }
+        __syncthreads();
+        const float invC = 1.f / (float)Cout;
+        for (int i = threadIdx.x; i < n; i += PK_THREADS) {
+            const int t = pk_div(i, Cout, invC), co = i - t * Cout;
+            wp[((int64_t)t * Cin + row) * Cout + co] = srow[co * T + (T - 1 - t)];
+        }
     }
 }
 
 hex_status_t tc_pack_weights_multi(const PackSegs& segs, cudaStream_t st) {
     if (segs.count <= 0) return HEX_OK;
     const PackSeg& last = segs.seg[segs.count - 1];
-    const int64_t total = last.begin + (int64_t)last.T * last.Cout * last.Cin;
-    pack_weights_multi_kernel<<<ceil_div(total, 256), 256, 0, st>>>(segs);
+    const int64_t rows = last.row0 + (last.tr ? last.Cin : last.Cout);
+    int64_t smax = 0;
+    for (int i = 0; i < segs.count; ++i) {
+        const int64_t e = (int64_t)segs.seg[i].T * (segs.seg[i].tr ? segs.seg[i].Cout : segs.seg[i].Cin);
+        if (e > smax) smax = e;
+    }
+    const size_t smem = (size_t)smax * sizeof(__nv_bfloat16);
+    if (smem > 200 * 1024) return HEX_ERR_UNSUPPORTED;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(pack_weights_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+        return HEX_ERR_CUDA;
+    pack_weights_multi_kernel<<<(unsigned)rows, PK_THREADS, smem, st>>>(segs);
     count_launch();
     return last_launch_status();
 }

@@ -9,7 +9,8 @@ namespace hexconv {
 // Per-sample block: global average pool (8 channels per thread, HW split over
 // thread slices, fixed-order smem reduction), logits, softmax cross-entropy,
 // dlogits.  gap[b][C], dlog[b][K], loss_b[b].
-constexpr int HEAD_THREADS = 1024;  // C = 256: 32 pixel slices x 32 channel groups per image
+constexpr int HEAD_THREADS = 512;  // C = 256: 16 pixel slices x 32 channel groups per image; 2 blocks per SM
+constexpr int HEAD_BATCH = 9;      // loads in flight per thread (C5: 576 pixels / 16 slices = 4 batches)
 
 __global__ void __launch_bounds__(HEAD_THREADS)
 head_sample_kernel(const uint4* __restrict__ feat, const float* __restrict__ wl, const float* __restrict__ bl,
@@ -23,9 +24,22 @@ head_sample_kernel(const uint4* __restrict__ feat, const float* __restrict__ wl,
     const int c8 = tid % C8, sl = tid / C8;
     if (sl < slices && tid < slices * C8) {
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 4
-        for (int i = sl; i < HW; i += slices) {
-            const uint4 v4 = feat[((int64_t)b * HW + i) * C8 + c8];
+        // batches of HEAD_BATCH independent 16-byte loads in flight per thread (latency-bound otherwise: one
+        // block per image, a few loads per thread); the sums stay in pixel order
+        int i = sl;
+        for (; i + (HEAD_BATCH - 1) * slices < HW; i += HEAD_BATCH * slices) {
+            uint4 q[HEAD_BATCH];
+#pragma unroll
+            for (int u = 0; u < HEAD_BATCH; ++u) q[u] = __ldg(feat + ((int64_t)b * HW + i + u * slices) * C8 + c8);
+#pragma unroll
+            for (int u = 0; u < HEAD_BATCH; ++u) {
+                const __nv_bfloat16* v = reinterpret_cast<const __nv_bfloat16*>(&q[u]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(v[j]);
+            }
+        }
+        for (; i < HW; i += slices) {
+            const uint4 v4 = __ldg(feat + ((int64_t)b * HW + i) * C8 + c8);
             const __nv_bfloat16* v = reinterpret_cast<const __nv_bfloat16*>(&v4);
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(v[j]);

@@ -46,6 +46,7 @@ def c5_ops():
     return {
         "c5_l2_fwd_maxpool": lambda: F.conv2d_fwd_maxpool(x, w, b, n=1),
         "c5_l2_fwd_avgpool": lambda: F.conv2d_fwd_avgpool(x, w, b, n=1),
+        "c5_l2_fwd_maxpool_nobias": lambda: F.conv2d_fwd_maxpool(x, w, None, n=1),
         "c5_l2_fwd_then_avgpool": lambda: (F.conv2d_fwd(x, w, b, n=1, relu=True, layout="NHWC", out=y),
                                            F.pool2d_fwd(y, 1, 2, 0, "avg", "NHWC")),
     }
