@@ -121,6 +121,23 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
         : "memory");
 }
+// warp-uniform issue: the whole warp runs the loop (descriptors stay in uniform registers) and one elected
+// lane issues the MMA / commit
+__device__ __forceinline__ void mma_tf32_ts_elect(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                                  uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            ptx::smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
                  "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
@@ -264,48 +281,50 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
     const uint32_t tm = *tslot;
 
     if (warp == TF_MMA_WARP) {
-        if (lane == 0) {
-            // per K-step: D[0, 2NT) += A_hi . [B_hi ; B_lo]  (one N = 2 NT MMA: hi.hi and hi.lo side by side)
-            //             D[0, NT)  += A_lo . B_hi
-            constexpr uint32_t idesc2 = idesc_tf32(128, 2 * NT), idesc1 = idesc_tf32(128, NT);
-            ptx::mbar_wait(wbar, 0);
-            const uint64_t bdesc0 = desc_sw32(ptx::smem_u32(wsm));
-            constexpr uint64_t BSTEP = (2 * KBLK) >> 4;  // descriptor address units (16 B)
-            int sglob = 0, acc = 0;
-            uint32_t aphase = 0;
-            for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-                ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+        // per K-step: D[0, 2NT) += A_hi . [B_hi ; B_lo]  (one N = 2 NT MMA: hi.hi and hi.lo side by side)
+        //             D[0, NT)  += A_lo . B_hi
+        // The whole warp runs this loop (its values stay warp-uniform) and an elected lane issues.  A tile's
+        // last stage always issues TF_KPS K-steps: the builders write zeros into the A columns of K-steps
+        // past the tile's count, and those K-steps read weight block 0 (finite), so they add exact zeros --
+        // no per-MMA bounds test in the issue stream.
+        constexpr uint32_t idesc2 = idesc_tf32(128, 2 * NT), idesc1 = idesc_tf32(128, NT);
+        ptx::mbar_wait(wbar, 0);
+        const uint64_t bdesc0 = desc_sw32(ptx::smem_u32(wsm));
+        constexpr uint64_t BSTEP = (2 * KBLK) >> 4;  // descriptor address units (16 B)
+        int sglob = 0, acc = 0;
+        uint32_t aphase = 0;
+        for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+            ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d = tm + acc * 2 * NT;
+            int k0, kn;
+            tile_k(tile, &k0, &kn);
+            const int tst = (kn + TF_KPS - 1) / TF_KPS;
+            uint64_t bd = bdesc0;
+            for (int js = 0; js < tst; ++js, ++sglob) {
+                const int st = sglob & (TF_STAGES - 1);
+                PROF_T0();
+                ptx::mbar_wait(&full[st], (sglob / TF_STAGES) & 1);
+                PROF_ACC(0);
                 ptx::tc_fence_after();
-                const uint32_t d = tm + acc * 2 * NT;
-                int k0, kn;
-                tile_k(tile, &k0, &kn);
-                const int tst = (kn + TF_KPS - 1) / TF_KPS;
-                uint64_t bd = bdesc0;
-                int ks = 0;
-                for (int js = 0; js < tst; ++js, ++sglob) {
-                    const int st = sglob & (TF_STAGES - 1);
-                    PROF_T0();
-                    ptx::mbar_wait(&full[st], (sglob / TF_STAGES) & 1);
-                    PROF_ACC(0);
-                    ptx::tc_fence_after();
-                    const uint32_t a0 = tm + ACC_COLS + st * STAGE_COLS;
+                const uint32_t a0 = tm + ACC_COLS + st * STAGE_COLS;
+                const bool last = js + 1 == tst;
 #pragma unroll
-                    for (int kk = 0; kk < TF_KPS; ++kk) {
-                        if (ks < kn) {
-                            if (IN_LAT) bd = bdesc0 + (uint64_t)wtab[k0 + ks] * BSTEP;
-                            mma_tf32_ts(d, a0 + 16 * kk, bd, idesc2, ks > 0 ? 1u : 0u);
-                            mma_tf32_ts(d, a0 + 16 * kk + 8, bd, idesc1, 1u);
-                        }
-                        ++ks;
-                        bd += BSTEP;
-                    }
-                    ptx::mma_commit(&empty[st]);
-                    PROF_ACC(1);
+                for (int kk = 0; kk < TF_KPS; ++kk) {
+                    const int ks = js * TF_KPS + kk;
+                    uint64_t b = bd + (uint64_t)kk * BSTEP;
+                    if (IN_LAT) b = bdesc0 + (uint64_t)wtab[k0 + (ks < kn ? ks : 0)] * BSTEP;
+                    else if (last && ks >= kn) b = bdesc0;
+                    mma_tf32_ts_elect(d, a0 + 16 * kk, b, idesc2, (js | kk) ? 1u : 0u);
+                    mma_tf32_ts_elect(d, a0 + 16 * kk + 8, b, idesc1, 1u);
                 }
-                ptx::mma_commit(&tfull[acc]);
-                acc ^= 1;
-                if (acc == 0) aphase ^= 1;
+                bd += (uint64_t)TF_KPS * BSTEP;
+                mma_commit_elect(&empty[st]);
+                PROF_ACC(1);
             }
+            mma_commit_elect(&tfull[acc]);
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
         }
     } else if (warp >= TF_EPI_WARPS) {
         // builders: group g fills the A stages sglob = g (mod TF_GROUPS) -- every use of a TMEM stage
