@@ -114,13 +114,6 @@ __device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
-        : "memory");
-}
 // warp-uniform issue: the whole warp runs the loop (descriptors stay in uniform registers) and one elected
 // lane issues the MMA / commit
 __device__ __forceinline__ void mma_tf32_ts_elect(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
@@ -766,29 +759,28 @@ tf32_wgrad_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_consta
             }
         }
     } else if (warp == Cfg::MWARP) {
-        if (lane == 0) {
-            constexpr uint32_t idesc2 = idesc_tf32(128, 2 * NT), idesc1 = idesc_tf32(128, NT);
-            const uint64_t b0 = desc_sw32(ptx::smem_u32(bsm));
-            for (int kg = 0; kg < nk; ++kg) {
-                const int st = kg % STAGES;
-                PROF_T0();
-                ptx::mbar_wait(&full[st], (kg / STAGES) & 1);
-                PROF_ACC(0);
-                ptx::tc_fence_after();
-                const uint64_t bd = b0 + (uint64_t)((st * Cfg::BBYTES) >> 4);
+        // the whole warp runs the issue loop (warp-uniform values), one elected lane issues
+        constexpr uint32_t idesc2 = idesc_tf32(128, 2 * NT), idesc1 = idesc_tf32(128, NT);
+        const uint64_t b0 = desc_sw32(ptx::smem_u32(bsm));
+        for (int kg = 0; kg < nk; ++kg) {
+            const int st = kg % STAGES;
+            PROF_T0();
+            ptx::mbar_wait(&full[st], (kg / STAGES) & 1);
+            PROF_ACC(0);
+            ptx::tc_fence_after();
+            const uint64_t bd = b0 + (uint64_t)((st * Cfg::BBYTES) >> 4);
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) {
-                    const uint32_t d = tm + mt * 2 * NT;
-                    const uint32_t a = tm + Cfg::ACC + (st * MT + mt) * 16;
-                    if (WG_SKIP(0)) continue;
-                    mma_tf32_ts(d, a, bd, idesc2, kg > 0 ? 1u : 0u);
-                    mma_tf32_ts(d, a + 8, bd, idesc1, 1u);
-                }
-                ptx::mma_commit(&empty[st]);
-                PROF_ACC(1);
+            for (int mt = 0; mt < MT; ++mt) {
+                const uint32_t d = tm + mt * 2 * NT;
+                const uint32_t a = tm + Cfg::ACC + (st * MT + mt) * 16;
+                if (WG_SKIP(0)) continue;
+                mma_tf32_ts_elect(d, a, bd, idesc2, kg > 0 ? 1u : 0u);
+                mma_tf32_ts_elect(d, a + 8, bd, idesc1, 1u);
             }
-            ptx::mma_commit(dfull);
+            mma_commit_elect(&empty[st]);
+            PROF_ACC(1);
         }
+        mma_commit_elect(dfull);
     } else if (warp >= 4) {
         // A builders: warp index within the group -> (M-tile, lane quadrant = warp % 4).  Row m = ci * T + t
         // (channel-major: the 32 lanes of a warp are mostly the taps of one channel, whose band addresses

@@ -28,7 +28,23 @@ def c3_ops():
     dp = torch.randn(B, 32, H2, W2, device="cuda")
     dy2 = torch.empty(B, 32, H, W, device="cuda")
     dw = torch.empty(16, 1, 7, device="cuda")
+    x16 = torch.randn(B, 16, H, W, device="cuda")
+    w2 = torch.randn(32, 16, 19, device="cuda") * 0.05
+    g32 = torch.randn(B, 32, H, W, device="cuda")
+    p32 = torch.randn(B, 32, H2, W2, device="cuda")
+    w4 = torch.randn(64, 32, 7, device="cuda") * 0.05
+    g64 = torch.randn(B, 64, H2, W2, device="cuda")
+    o = {k: torch.empty(sh, device="cuda") for k, sh in (("y2", (B, 32, H, W)), ("dx16", (B, 16, H, W)),
+                                                          ("y4", (B, 64, H2, W2)), ("dp", (B, 32, H2, W2)))}
+    dw2 = torch.empty(32, 16, 19, device="cuda")
+    dw4 = torch.empty(64, 32, 7, device="cuda")
     return {
+        "c3_l2_fwd": lambda: F.conv2d_fwd(x16, w2, None, n=2, out=o["y2"]),
+        "c3_l2_dgrad": lambda: F.conv2d_bwd_data(g32, w2, (H, W), n=2, out=o["dx16"]),
+        "c3_l2_wgrad": lambda: F.conv2d_bwd_weight(x16, g32, n=2, dw=dw2),
+        "c3_l4_fwd": lambda: F.conv2d_fwd(p32, w4, None, n=1, out=o["y4"]),
+        "c3_l4_dgrad": lambda: F.conv2d_bwd_data(g64, w4, (H2, W2), n=1, out=o["dp"]),
+        "c3_l4_wgrad": lambda: F.conv2d_bwd_weight(p32, g64, n=1, dw=dw4),
         "c3_l1_fwd": lambda: F.conv2d_fwd(x, w1, b1, n=1, relu=True, out=y1),
         "c3_l1_wgrad": lambda: F.conv2d_bwd_weight(x, g1, n=1, dw=dw),
         "c3_pool_fwd_avg": lambda: F.pool2d_fwd(y2, n=1, stride=2, mode="avg", out=p),
