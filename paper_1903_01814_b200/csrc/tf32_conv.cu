@@ -69,7 +69,7 @@ constexpr int TF_GROUPS = 4;                       // builder groups (K-steps ro
 constexpr int TF_EPI_WARPS = 4;
 constexpr int TF_BLD_WARPS = 4 * TF_GROUPS;
 constexpr int TF_MMA_WARP = TF_EPI_WARPS + TF_BLD_WARPS;
-constexpr int TF_THREADS = (TF_MMA_WARP + 1) * 32;
+constexpr int tf_threads(int iss) { return (TF_MMA_WARP + iss) * 32; }  // iss MMA-issuing warps
 constexpr int TF_MAXT = 37;                        // n <= 3
 constexpr int TF_MAX_NT = 64;
 constexpr int TF_SMEM_MAX = 220 * 1024;
@@ -88,6 +88,7 @@ struct TfParams {
     const float* relu_y;  // mask source shaped like y, or null
     float* y;             // output, NCHW [B][Nout][Hout][Wout]
     int B, Cx, H, W, Hin, Win, Hout, Wout;
+    int64_t plane_bytes;  // Hin * Win * 4: the stride between channel planes of x
     int Nout, s, parity, T, kc8, ksteps, relu;
     int out_lat, in_lat;  // output pixels are lattice points / the gathered tensor lives on the lattice
     int total_pix, tiles;
@@ -152,9 +153,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
-constexpr int tmem_cols(int NT) {
-    return (4 * NT + TF_STAGES * 16 * TF_KPS) <= 256 ? 256 : 512;
+constexpr int tmem_cols(int NT, int iss) {
+    return (4 * NT * iss + TF_STAGES * 16 * TF_KPS) <= 256 ? 256 : 512;
 }
+// two MMA-issuing warps (each takes half of every stage's K-steps into its own accumulator pair) where the
+// accumulators still fit next to the A stages: the MMA front end (~45-75 cycles per tcgen05.mma for N <= 64)
+// is per issuing thread
+constexpr int tf_issuers(int NT) { return 4 * NT * 2 + TF_STAGES * 16 * TF_KPS <= 512 ? 2 : 1; }
 
 // Output pixel `pix` (flattened b, R, C of the output grid) -> image, centre on the full grid, centre parity.
 __device__ __forceinline__ void pixel_centre(const TfParams& p, int pix, int* b, int* rem, int* rc, int* cc) {
@@ -172,11 +177,13 @@ __device__ __forceinline__ void pixel_centre(const TfParams& p, int pix, int* b,
 }
 
 template <int NT, bool IN_LAT, bool FULLCH>
-__global__ void __launch_bounds__(TF_THREADS, 1)
+__global__ void __launch_bounds__(tf_threads(tf_issuers(NT)), 1)
 tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ wpack) {
-    constexpr int ACC_COLS = 4 * NT;     // two accumulators of 2 NT columns: [D_hh + D_lh | D_hl]
+    constexpr int ISS = tf_issuers(NT);
+    constexpr int ACC_COLS = 4 * NT * ISS;  // per slot and issuer an accumulator of 2 NT columns: [D_hh + D_lh | D_hl]
     constexpr int STAGE_COLS = 16 * TF_KPS;
-    constexpr int TMEM_COLS = tmem_cols(NT);
+    constexpr int TMEM_COLS = tmem_cols(NT, ISS);
+    static_assert(TF_KPS % ISS == 0, "issuers split a stage's K-steps evenly");
     constexpr uint32_t KBLK = NT * 32;  // bytes of one (K-step, hi|lo) weight block
     extern __shared__ uint8_t smem_raw[];
     uint8_t* wsm = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -253,10 +260,10 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
     if (warp == TF_MMA_WARP && lane == 0) {
         for (int s = 0; s < TF_STAGES; ++s) {
             ptx::mbar_init(&full[s], 4);   // the 4 builder warps of the group that wrote the stage
-            ptx::mbar_init(&empty[s], 1);  // tcgen05.commit of the stage's MMAs
+            ptx::mbar_init(&empty[s], ISS);  // tcgen05.commit of the stage's MMAs (each issuer)
         }
         for (int a = 0; a < 2; ++a) {
-            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tfull[a], ISS);
             ptx::mbar_init(&tempty[a], TF_EPI_WARPS);
         }
         ptx::mbar_init(wbar, 1);
@@ -273,14 +280,17 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
     ptx::tc_fence_after();
     const uint32_t tm = *tslot;
 
-    if (warp == TF_MMA_WARP) {
+    if (warp >= TF_MMA_WARP) {
         // per K-step: D[0, 2NT) += A_hi . [B_hi ; B_lo]  (one N = 2 NT MMA: hi.hi and hi.lo side by side)
         //             D[0, NT)  += A_lo . B_hi
         // The whole warp runs this loop (its values stay warp-uniform) and an elected lane issues.  A tile's
         // last stage always issues TF_KPS K-steps: the builders write zeros into the A columns of K-steps
         // past the tile's count, and those K-steps read weight block 0 (finite), so they add exact zeros --
         // no per-MMA bounds test in the issue stream.
+        // Issuer i (warp TF_MMA_WARP + i) takes K-steps kk = i, i + ISS, ... of every stage into its own
+        // accumulator (slot acc, issuer i); the epilogue adds the issuers' accumulators.
         constexpr uint32_t idesc2 = idesc_tf32(128, 2 * NT), idesc1 = idesc_tf32(128, NT);
+        const int iss = warp - TF_MMA_WARP;
         ptx::mbar_wait(wbar, 0);
         const uint64_t bdesc0 = desc_sw32(ptx::smem_u32(wsm));
         constexpr uint64_t BSTEP = (2 * KBLK) >> 4;  // descriptor address units (16 B)
@@ -289,7 +299,7 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
         for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
             ptx::mbar_wait(&tempty[acc], aphase ^ 1);
             ptx::tc_fence_after();
-            const uint32_t d = tm + acc * 2 * NT;
+            const uint32_t d = tm + (acc * ISS + iss) * 2 * NT;
             int k0, kn;
             tile_k(tile, &k0, &kn);
             const int tst = (kn + TF_KPS - 1) / TF_KPS;
@@ -303,12 +313,13 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
                 const uint32_t a0 = tm + ACC_COLS + st * STAGE_COLS;
                 const bool last = js + 1 == tst;
 #pragma unroll
-                for (int kk = 0; kk < TF_KPS; ++kk) {
+                for (int k2 = 0; k2 < TF_KPS / ISS; ++k2) {
+                    const int kk = k2 * ISS + iss;
                     const int ks = js * TF_KPS + kk;
                     uint64_t b = bd + (uint64_t)kk * BSTEP;
                     if (IN_LAT) b = bdesc0 + (uint64_t)wtab[k0 + (ks < kn ? ks : 0)] * BSTEP;
                     else if (last && ks >= kn) b = bdesc0;
-                    mma_tf32_ts_elect(d, a0 + 16 * kk, b, idesc2, (js | kk) ? 1u : 0u);
+                    mma_tf32_ts_elect(d, a0 + 16 * kk, b, idesc2, (js | k2) ? 1u : 0u);
                     mma_tf32_ts_elect(d, a0 + 16 * kk + 8, b, idesc1, 1u);
                 }
                 bd += (uint64_t)TF_KPS * BSTEP;
@@ -369,17 +380,19 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
                 }
                 // unconditional loads from a valid address (the image's first pixel when the neighbour is
                 // off-grid or off-lattice), zeroed afterwards: no predicated loads in the hot loop
-                const float* src = xb + (ok ? idx : 0) + (size_t)c0 * hw_in;
+                // channel k of the chunk is k plane strides (p.plane_bytes, a kernel parameter) past the first:
+                // the 8 offsets are warp-uniform, so each load is one LDG [base + uniform offset]
+                const char* src = reinterpret_cast<const char*>(xb + (ok ? idx : 0) + c0 * hw_in);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
+                    const float* sk = reinterpret_cast<const float*>(src + (int64_t)k * p.plane_bytes);
                     float u;
                     if constexpr (FULLCH) {
-                        u = __ldg(src);
+                        u = __ldg(sk);
                     } else {
-                        u = c0 + k < p.Cx ? __ldg(src) : 0.f;
+                        u = c0 + k < p.Cx ? __ldg(sk) : 0.f;
                     }
                     v[kk][k] = ok ? u : 0.f;
-                    src += hw_in;
                 }
             }
             PROF_ACC(4);
@@ -427,12 +440,24 @@ tf32_conv_kernel(const __grid_constant__ TfParams p, const float* __restrict__ w
             const bool vpix = tile_pixel(tile, q * 32 + lane, &b, &rem, &rcx, &ccx);
             float* yo = p.y + (size_t)b * p.Nout * hw_out + rem;
             const float* mo = p.relu_y ? p.relu_y + (size_t)b * p.Nout * hw_out + rem : nullptr;
-            const uint32_t dbase = tm + lane_base + acc * 2 * NT;
+            const uint32_t dbase = tm + lane_base + acc * ISS * 2 * NT;
 #pragma unroll
             for (int c0 = 0; c0 < NT; c0 += 16) {
                 uint32_t u[16], w[16];
                 tmem_ld16(dbase + c0, u);
                 tmem_ld16(dbase + NT + c0, w);
+                if constexpr (ISS == 2) {
+                    uint32_t u2[16], w2[16];
+                    tmem_ld16(dbase + 2 * NT + c0, u2);
+                    tmem_ld16(dbase + 3 * NT + c0, w2);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {  // fixed order: (hh + lh + hl of issuer 0) + (... of issuer 1)
+                        u[j] = __float_as_uint((__uint_as_float(u[j]) + __uint_as_float(w[j])) +
+                                               (__uint_as_float(u2[j]) + __uint_as_float(w2[j])));
+                        w[j] = 0u;
+                    }
+                }
                 ptx::tmem_ld_wait();
                 if (c0 + 16 >= NT) {  // the accumulator is drained: hand it back to the MMA warp
                     ptx::tc_fence_before();
@@ -516,7 +541,7 @@ hex_status_t launch_tf_k(const TfParams& p, const float* wpack, int smem, cudaSt
         attr = true;
     }
     const int grid = p.tiles < num_sms() ? p.tiles : num_sms();
-    tf32_conv_kernel<NT, IN_LAT, FULLCH><<<grid, TF_THREADS, smem, st>>>(p, wpack);
+    tf32_conv_kernel<NT, IN_LAT, FULLCH><<<grid, tf_threads(tf_issuers(NT)), smem, st>>>(p, wpack);
     count_launch();
     return last_launch_status();
 }
@@ -575,6 +600,7 @@ hex_status_t tf32_conv(const Geom& g, int Cin, int Cout, int mode, const float* 
         p.Hin = g.Ho; p.Win = g.Wo; p.Hout = g.H; p.Wout = g.W;
         p.out_lat = 0; p.in_lat = g.s > 1;
     }
+    p.plane_bytes = (int64_t)p.Hin * p.Win * 4;
     p.Nout = Nout;
     p.s = g.s;
     p.parity = g.parity;
