@@ -81,7 +81,7 @@ __device__ __forceinline__ void reduce7(const float* v, const bool* ok, float* o
             ++cnt;
         }
     }
-    *out = MAX ? best : sum / (float)cnt;
+    *out = MAX ? best : sum * (cnt == 7 ? 1.f / 7.f : 1.f / (float)cnt);  // (A8, <= 1 ulp from sum / cnt)
     *idx = bt;
 }
 
