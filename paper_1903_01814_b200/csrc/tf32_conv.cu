@@ -101,10 +101,12 @@ struct TfParams {
     uint16_t klist[TF_MAXKL];  // per class, its K-steps: tap | chunk << 8
 };
 
+// tf32 rounding to nearest, ties away from zero (= cvt.rna.tf32.f32 for every non-NaN input, Inf kept): add
+// half an ulp of the 10-bit mantissa to the magnitude bits and clear the 13 dropped bits -- two integer ops
+// where sm_100 compiles cvt.rna.tf32 to a five-instruction sequence with an Inf / NaN test (the builders'
+// split of every gathered value is on the hot path).  NaN payloads may become Inf (A10: NaN undefined).
 __device__ __forceinline__ float tf32_rna(float v) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-    return __uint_as_float(r);
+    return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xffffe000u);
 }
 
 // SW32 K-major shared-memory descriptor: 8-row groups 256 B apart (SBO), LBO unused, layout code 6
