@@ -460,8 +460,8 @@ def secondary_measurements(dev, peak_tf, peak_gbs):
         tf = fl3 / (fl * 1e-3) / 1e12
         c3d[name] = {"us_flushed": fl * 1e3, "us_hot": hot * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak_tf}
     c3d["note"] = ("fwd / dgrad: depth taps inside the K loop of the tcgen05 tap-reuse kernel (out-of-volume "
-                   "slices are zero-fill boxes); wgrad: depth taps unfolded into channels then one 2-D tcgen05 "
-                   "wgrad over B*D images; FLOPs count in-range depth taps only")
+                   "slices are zero-fill boxes); wgrad: depth taps as channel-chunk units of the tcgen05 tap-reuse "
+                   "weight gradient (no unfolded copy); FLOPs count in-range depth taps only")
     out["conv3d_64to128_16x64x64_kd3_bf16"] = c3d
     return out
 

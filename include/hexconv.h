@@ -247,11 +247,13 @@ HEX_API hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* desc, int32_t pass
  * layout HEX_NCHW means NCDHW, HEX_NHWC means NDHWC (channels innermost).
  * Implementation: bf16 NDHWC with in-plane s = 1 and Cin, Cout multiples of
  * 64 runs fwd (and bwd_data when sd = 1) on the tcgen05 tap-reuse kernel with
- * the depth taps inside its K loop (out-of-volume slices are TMA zero fill).
- * Everything else, and every bwd_weight, unfolds the kd depth taps into input
- * channels of one 2-D convolution over B*Do images (x' = depth-unfolded input,
- * Cin' = kd*Cin, ordered (kz, ci)), so every 2-D path applies.  The workspace
- * holds x' (or dx'), the reordered weights and the 2-D call's own workspace.
+ * the depth taps inside its K loop (out-of-volume slices are TMA zero fill),
+ * and bwd_weight (Cout a multiple of 128, well-filled tiles) on the tcgen05
+ * tap-reuse weight gradient with the depth taps as its channel-chunk units.
+ * Everything else unfolds the kd depth taps into input channels of one 2-D
+ * convolution over B*Do images (x' = depth-unfolded input, Cin' = kd*Cin,
+ * ordered (kz, ci)), so every 2-D path applies.  The workspace holds x' (or
+ * dx'), the reordered weights and the 2-D call's own workspace.
  * Errors: as the 2-D calls, plus HEX_ERR_INVALID_ARG for even / non-positive
  * kernel_depth or depth_stride < 1, HEX_ERR_SHAPE for depth < 1. */
 typedef struct {

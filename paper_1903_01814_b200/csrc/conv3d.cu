@@ -423,6 +423,25 @@ hex_status_t hex_conv3d_bwd_weight(const hex_conv3d_desc_t* d, const void* x, co
     p += up1k((size_t)g.Co * g.Ci * g.kd * Tn * sizeof(float));
     float* dbu = (float*)p;  // fresh dbias, added by dwperm_kernel when accumulating
     p += up1k((size_t)g.Co * sizeof(float));
+    Geom tg;
+    if (c3_tc_ok(d, g.Ci, g.Co, g.Do, &tg) && g.Co % 128 == 0 && a16(x) && a16(dy) &&
+        !sw_on("HEXCONV_CONV3D_UNFOLD")) {
+        tg.B = g.B * g.Do;  // output slices
+        if (tc_wgrad_tr_supported(tg, g.Ci * g.kd, g.Co)) {
+            // depth taps in the units of the tcgen05 tap-reuse weight gradient: no unfolded copy of x; the
+            // partials come out in the unfolded (kz, ci) channel order, permuted by dwperm below
+            TcWgradArgs a{};
+            a.g = tg; a.Cin = g.Ci; a.Cout = g.Co; a.x = x; a.dy = dy; a.dw = dwu; a.dbias = dbias ? dbu : nullptr;
+            a.accumulate = 0;
+            const TrDepth dz{g.kd, g.D, g.Do, g.sd};
+            st = tc_conv3d_wgrad(a, dz, p, ws_bytes - (size_t)(p - (uint8_t*)ws), s);
+            if (st != HEX_OK) return st;
+            const int64_t total = (int64_t)g.Co * g.Ci * g.kd * Tn;
+            dwperm_kernel<<<grid_for(total), 256, 0, s>>>(dwu, dw, g.Co, g.Ci, g.kd, Tn, accumulate, dbu, dbias);
+            count_launch();
+            return last_launch_status();
+        }
+    }
     const void* dy2 = dy;
     if (d->layout != HEX_NHWC) {
         const int64_t HWo = (int64_t)(out_vol_bytes(d, g) / elt(d->dtype)) / ((int64_t)g.B * g.Do * g.Co);

@@ -106,9 +106,15 @@ size_t tc_wgrad_ws_bytes(const Geom& g, int Cin, int Cout);
 hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);
 // tap-reuse variant (tc_wgrad_tr.cu); writes split-K partials, reduced by tc_conv_wgrad
 bool tc_wgrad_tr_supported(const Geom& g, int Cin, int Cout);
-size_t tc_wgrad_tr_ws_bytes(const Geom& g, int Cin, int Cout);
+struct TrDepth {  // 3-D weight gradient: depth taps folded into the units' channel chunks
+    int kd, D, Do, sd;
+};
+size_t tc_wgrad_tr_ws_bytes(const Geom& g, int Cin, int Cout, int kd = 1);
 hex_status_t tc_wgrad_tr(const TcWgradArgs& a, void* ws, size_t ws_bytes, int* chunks_out, float** db_part_out,
-                         cudaStream_t st);
+                         cudaStream_t st, const TrDepth* dz = nullptr);
+// 3-D (conv3d.cu): x bf16 NDHWC [B*D][H][W][Cin], dy [B*Do][H][W][Cout] (a.g.B = B * Do), dw fp32
+// [Cout][kd * Cin][T] in (kz, ci) channel order (permuted by the caller), dbias fresh
+hex_status_t tc_conv3d_wgrad(const TcWgradArgs& a, const TrDepth& dz, void* ws, size_t ws_bytes, cudaStream_t st);
 
 // single-input-channel bf16 NHWC stencil (config 5 layer 1)
 bool smallc_supported(const Geom& g, int Cin, int Cout);

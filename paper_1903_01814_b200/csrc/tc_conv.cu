@@ -1327,6 +1327,15 @@ static hex_status_t launch_wgrad_pix(const CUtensorMap& mx0, const CUtensorMap& 
     return HEX_OK;
 }
 
+hex_status_t tc_conv3d_wgrad(const TcWgradArgs& a, const TrDepth& dz, void* ws, size_t ws_bytes, cudaStream_t st) {
+    int chunks = 0;
+    float* db_part = nullptr;
+    const hex_status_t s = tc_wgrad_tr(a, ws, ws_bytes, &chunks, &db_part, st, &dz);
+    if (s != HEX_OK) return s;
+    return wgrad_reduce((const float*)ws, chunks, a.g.T, a.Cout, dz.kd * a.Cin, a.dw, db_part, a.dbias, a.accumulate,
+                        st);
+}
+
 hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
     const Geom& g = a.g;
     if (tc_wgrad_tr_supported(g, a.Cin, a.Cout)) {  // tap-reuse kernel (tc_wgrad_tr.cu)

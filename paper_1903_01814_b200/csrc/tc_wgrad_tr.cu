@@ -51,6 +51,11 @@ struct TrParams {
     int stages, xrows;                 // pipeline depth; x box rows = RB + 2n
     int gcols[4][TR_MAXCOLS];          // kernel columns dc of each group (unused slots: 99)
     int ncols[4];
+    // 3-D: pixel tile image b is an OUTPUT slice b = vol * Do + zo (dy image); the units'
+    // channel chunk kc runs over (depth tap kz, 64-channel chunk of x) = kz * kchunks_x + kcx, reading x image
+    // vol * D + sd * zo + kz - pd (all zero fill outside the volume), and the partials are laid out with
+    // Cin = kd * Cin_x channels ordered (kz, ci).  2-D: kd = D = Do = sd = 1, pd = 0, kchunks_x = kchunks.
+    int kd, D, Do, sd, pd, kchunks_x;
     float* part;     // [chunks][T][Cout][Cin]
     float* db_part;  // [chunks][Cout] or NULL
     int dbg;         // development (HEXCONV_WG_DEBUG): 1 = no TMA loads, 2 = no MMAs (results invalid)
@@ -218,13 +223,19 @@ tc_wgrad_tr_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
                 ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
                 // dy: both 64-channel chunks of the Cout tile in one op
                 ptx::tma_load_5d(P ? &map_dy1 : &map_dy0, &full[stage], s, 0, j0, r0, b, co0 / 64);
+                const int kz = kc / p.kchunks_x, kcx = kc - kz * p.kchunks_x;
+                const int vol = b / p.Do, zo = b - vol * p.Do;
+                const int z = p.sd * zo + kz - p.pd;
+                const bool zin = z >= 0 && z < p.D;
+                const int ximg = vol * p.D + (zin ? z : 0);
+                const int roff = zin ? 0 : p.H + 64;  // outside the volume: the x boxes are all zero fill
                 for (int c = 0; c < ncol; ++c) {
                     const int dc = p.gcols[grp][c];
                     const int Pv = (P + dc) & 1;
                     const int jsh = (P + dc - Pv) / 2;
                     const int top = -p.n + (((dc < 0 ? -dc : dc) + pc) >> 1);
                     ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], s + 2 * DY_BOX + c * xbox, 0, j0 + jsh,
-                                     r0 + top, b, kc);
+                                     r0 + top + roff, ximg, kcx);
                 }
                 if (++stage == p.stages) { stage = 0; phase ^= 1; }
             }
@@ -342,7 +353,7 @@ static int tr_rb() {
     return rb;
 }
 
-static TrPlan tr_plan(const Geom& g, int Cin, int Cout) {
+static TrPlan tr_plan(const Geom& g, int Cin, int Cout, int kd = 1) {
     TrPlan w{};
     w.RB = tr_rb();
     w.rt = ceil_div(g.H, w.RB);
@@ -350,7 +361,7 @@ static TrPlan tr_plan(const Geom& g, int Cin, int Cout) {
     w.jt1 = ceil_div(g.W / 2, TR_JB);
     w.tiles0 = w.rt * w.jt0 * g.B;
     w.ptiles = w.tiles0 + w.rt * w.jt1 * g.B;
-    w.kchunks = Cin / 64;
+    w.kchunks = kd * (Cin / 64);  // (depth tap, channel chunk) units
     w.co_tiles = Cout / 128;
     for (auto& r : w.gcols)
         for (int& c : r) c = 99;
@@ -393,19 +404,27 @@ bool tc_wgrad_tr_supported(const Geom& g, int Cin, int Cout) {
     return tr_encode() != nullptr;
 }
 
-size_t tc_wgrad_tr_ws_bytes(const Geom& g, int Cin, int Cout) {
-    const TrPlan w = tr_plan(g, Cin, Cout);
-    return (size_t)w.chunks * g.T * Cout * Cin * sizeof(float) + (size_t)w.chunks * Cout * sizeof(float) + 256;
+size_t tc_wgrad_tr_ws_bytes(const Geom& g, int Cin, int Cout, int kd) {
+    const TrPlan w = tr_plan(g, Cin, Cout, kd);
+    return (size_t)w.chunks * g.T * Cout * kd * Cin * sizeof(float) + (size_t)w.chunks * Cout * sizeof(float) + 256;
 }
 
 hex_status_t tc_wgrad_tr(const TcWgradArgs& a, void* ws, size_t ws_bytes, int* chunks_out, float** db_part_out,
-                         cudaStream_t st) {
-    const Geom& g = a.g;
-    const TrPlan w = tr_plan(g, a.Cin, a.Cout);
-    if (ws_bytes < tc_wgrad_tr_ws_bytes(g, a.Cin, a.Cout)) return HEX_ERR_WORKSPACE;
+                         cudaStream_t st, const TrDepth* dz) {
+    const Geom& g = a.g;  // 3-D: g.B = B * Do output slices
+    const int kd = dz ? dz->kd : 1;
+    const TrPlan w = tr_plan(g, a.Cin, a.Cout, kd);
+    if (ws_bytes < tc_wgrad_tr_ws_bytes(g, a.Cin, a.Cout, kd)) return HEX_ERR_WORKSPACE;
     TrParams p{};
     p.RB = w.RB;
-    p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.n = g.n; p.parity = g.parity;
+    p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = kd * a.Cin; p.Cout = a.Cout; p.T = g.T; p.n = g.n; p.parity = g.parity;
+    p.kd = kd;
+    p.D = dz ? dz->D : 1;
+    p.Do = dz ? dz->Do : 1;
+    p.sd = dz ? dz->sd : 1;
+    p.pd = (kd - 1) / 2;
+    p.kchunks_x = a.Cin / 64;
+    const int Bx = dz ? (g.B / p.Do) * p.D : g.B;  // x images
     p.rt = w.rt; p.jt0 = w.jt0; p.jt1 = w.jt1; p.tiles0 = w.tiles0; p.ptiles = w.ptiles;
     p.kchunks = w.kchunks; p.groups = w.groups; p.co_tiles = w.co_tiles; p.chunks = w.chunks;
     p.tiles_per_chunk = w.tiles_per_chunk; p.stages = w.stages; p.xrows = w.RB + 2 * g.n;
@@ -415,10 +434,10 @@ hex_status_t tc_wgrad_tr(const TcWgradArgs& a, void* ws, size_t ws_bytes, int* c
     }
     p.dbg = debug_mode("HEXCONV_WG_DEBUG");
     p.part = (float*)ws;
-    p.db_part = a.dbias ? (float*)ws + (size_t)w.chunks * g.T * a.Cout * a.Cin : nullptr;
+    p.db_part = a.dbias ? (float*)ws + (size_t)w.chunks * g.T * a.Cout * p.Cin : nullptr;
     CUtensorMap mx0, mx1, md0, md1;
-    if (!make_rowmajor_view(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, p.xrows, 1)) return HEX_ERR_CUDA;
-    if (!make_rowmajor_view(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, p.xrows, 1)) return HEX_ERR_CUDA;
+    if (!make_rowmajor_view(&mx0, a.x, Bx, g.H, g.W, a.Cin, 0, p.xrows, 1)) return HEX_ERR_CUDA;
+    if (!make_rowmajor_view(&mx1, a.x, Bx, g.H, g.W, a.Cin, 1, p.xrows, 1)) return HEX_ERR_CUDA;
     if (!make_rowmajor_view(&md0, a.dy, g.B, g.H, g.W, a.Cout, 0, w.RB, 2)) return HEX_ERR_CUDA;
     if (!make_rowmajor_view(&md1, a.dy, g.B, g.H, g.W, a.Cout, 1, w.RB, 2)) return HEX_ERR_CUDA;
     const int smem = tr_smem_bytes(g.n, w.RB, w.stages);

@@ -118,3 +118,25 @@ def test_conv3d_autograd_and_errors(F, oracle):
     with pytest.raises(HexError) as e:  # even kernel depth
         F.conv3d_fwd(x.detach(), torch.zeros(3, 2, 2, 7, device="cuda"), n=1)
     assert e.value.status == 1
+
+
+def test_conv3d_bf16_wgrad_depth_units(F, oracle):
+    # bf16 NDHWC weight gradient with the depth taps folded into the tcgen05 tap-reuse kernel's channel-chunk
+    # units (no unfolded copy of x): one wgrad launch + reduce + permute instead of unfold + the 2-D call;
+    # depth strides 1 and 2, a kernel deeper than the volume (kd = 5, D = 3: zero-fill slices), n = 1 and 2
+    from paper_1903_01814_b200 import _abi as A
+    for k, (B, Ci, Co, D, n, kd, sd, pi) in enumerate([(2, 64, 128, 5, 1, 3, 1, 0), (1, 64, 128, 6, 2, 3, 2, 1),
+                                                        (2, 128, 128, 3, 1, 5, 1, 1)]):
+        case(F, oracle, B, Ci, Co, D, 16, 16, n, kd, 1, sd, pi, torch.bfloat16, "NDHWC", 400 + k)
+        x = torch.randn(B, D, 16, 16, Ci, device="cuda").to(torch.bfloat16)
+        Do = (D - 1) // sd + 1
+        g = torch.randn(B, Do, 16, 16, Co, device="cuda").to(torch.bfloat16)
+        n0 = A.launch_count()
+        dw, db = F.conv3d_bwd_weight(x, g, kd, n=n, depth_stride=sd, parity=pi, layout="NDHWC")
+        direct = A.launch_count() - n0
+        with A.switch("HEXCONV_CONV3D_UNFOLD"):
+            n0 = A.launch_count()
+            dw2, db2 = F.conv3d_bwd_weight(x, g, kd, n=n, depth_stride=sd, parity=pi, layout="NDHWC")
+            unfolded = A.launch_count() - n0
+        assert direct == unfolded - 1, (direct, unfolded)  # no unfold launch
+        assert torch.equal(dw, dw2) and torch.equal(db, db2)  # same partials, same fixed-order reduction

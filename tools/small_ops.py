@@ -68,8 +68,17 @@ def c5_ops():
     }
 
 
+def c3d_ops():
+    B, D, H, W, C, Co, kd, n = 16, 16, 64, 64, 64, 128, 3, 1
+    x = torch.randn(B, D, H, W, C, device="cuda").to(torch.bfloat16)
+    g3 = torch.randn(B, D, H, W, Co, device="cuda").to(torch.bfloat16)
+    return {"c3d_wgrad": lambda: F.conv3d_bwd_weight(x, g3, kd, n=n, layout="NDHWC")}
+
+
 def main():
     ops = c3_ops()
+    if any(a.startswith("c3d") for a in sys.argv[1:]):
+        ops.update(c3d_ops())
     if any(a.startswith("c5") for a in sys.argv[1:]):
         ops.update(c5_ops())
     sel = sys.argv[1:] or list(ops)
