@@ -7,6 +7,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "geometry.cuh"
 #include "kernels.h"
@@ -50,6 +52,7 @@ SwitchEntry g_switches[] = {
     {"HEXCONV_NO_FWD_TR", false, ""},
     {"HEXCONV_NO_FWD_TR_PAIR", false, ""},
     {"HEXCONV_NO_FWD_VPAIR", false, ""},
+    {"HEXCONV_NO_LAT_DGRAD", false, ""},
     {"HEXCONV_NO_PLANE", false, ""},
     {"HEXCONV_NO_POOL_TMA", false, ""},
     {"HEXCONV_NO_TC_STRIDE2", false, ""},
@@ -170,6 +173,10 @@ Geom stride1(const Geom& g) {
 bool strided_tc_ok(const hex_conv2d_desc_t* d, const Geom& g) {
     return g.s > 1 && d->dtype == HEX_BF16 && d->layout == HEX_NHWC && d->out_channels % 8 == 0 &&
            !sw_on("HEXCONV_NO_TC_STRIDED_BWD");
+}
+bool use_lat_dgrad(const hex_conv2d_desc_t* d, const Geom& g) {  // strided bf16 bwd-data by phase classes
+    return g.s > 1 && d->dtype == HEX_BF16 && d->layout == HEX_NHWC && !sw_on("HEXCONV_NO_TC_STRIDED_BWD") &&
+           lat_dgrad_supported(g, d->in_channels, d->out_channels);
 }
 bool use_tc_bwd_data_up(const hex_conv2d_desc_t* d, const Geom& g) {
     return strided_tc_ok(d, g) && tc_conv_supported(stride1(g), d->out_channels, d->in_channels);
@@ -294,7 +301,10 @@ hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* d, int32_t pass,
             return HEX_OK;
         case 1:
             *bytes = use_tc_bwd_data(d, g)      ? packed_weight_bytes(d, g)
-                     : use_tc_bwd_data_up(d, g) ? up_bytes(d, g) + packed_weight_bytes(d, g)
+                     : use_tc_bwd_data_up(d, g)
+                         ? std::max(up_bytes(d, g) + packed_weight_bytes(d, g),
+                                    use_lat_dgrad(d, g) ? lat_dgrad_ws_bytes(g, d->in_channels, d->out_channels) : 0)
+                     : use_lat_dgrad(d, g)      ? lat_dgrad_ws_bytes(g, d->in_channels, d->out_channels)
                      : use_tf32_bwd_data(d, g)  ? tf32_conv_ws_bytes(g, d->out_channels, d->in_channels)
                                                 : 0;
             return HEX_OK;
@@ -320,7 +330,9 @@ hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* d, int32_t pass, int32_t* 
     switch (pass) {
         case 0: *algo = use_tc_fwd(d, g) ? 1 : use_tf32_fwd(d, g) ? 2 : 0; return HEX_OK;
         case 1:
-            *algo = use_tc_bwd_data(d, g) || use_tc_bwd_data_up(d, g) ? 1 : use_tf32_bwd_data(d, g) ? 2 : 0;
+            *algo = use_tc_bwd_data(d, g) || use_lat_dgrad(d, g) || use_tc_bwd_data_up(d, g) ? 1
+                    : use_tf32_bwd_data(d, g)                                              ? 2
+                                                                                           : 0;
             return HEX_OK;
         case 2: *algo = use_tc_wgrad(d, g) || use_tc_wgrad_up(d, g) ? 1 : use_tf32_wgrad(d, g) ? 2 : 0; return HEX_OK;
         default: return HEX_ERR_INVALID_ARG;
@@ -425,6 +437,10 @@ hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* d, const void* dy, con
         return tc_conv_fwd(a, s);
     }
     if (!w) return HEX_ERR_INVALID_ARG;  // w == NULL (prepacked) only on the stride-1 tensor-core path
+    if (use_lat_dgrad(d, g) && ((uintptr_t)dy & 31) == 0) {  // stride s: phase classes (lat_dgrad.cu)
+        if (!aligned16(dx) || (relu_y && !aligned16(relu_y))) return HEX_ERR_ALIGNMENT;
+        return lat_dgrad(g, d->in_channels, d->out_channels, dy, w, relu_y, dx, ws, ws_bytes, s);
+    }
     if (use_tc_bwd_data_up(d, g)) {  // stride s: the stride-1 bwd-data of dy scattered onto the full grid
         if (!aligned16(dy) || !aligned16(dx) || !aligned16(w) || (relu_y && !aligned16(relu_y)))
             return HEX_ERR_ALIGNMENT;

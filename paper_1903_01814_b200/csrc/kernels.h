@@ -72,6 +72,11 @@ hex_status_t lattice_upsample(const void* dy, void* up, const Geom& g, int C, cu
 bool tc_fwd_tr_supported(const Geom& g, int Cin, int Cout);  // tap-reuse forward (tc_fwd_tr.cu)
 hex_status_t tc_fwd_tr(const TcConvArgs& a, cudaStream_t st);
 // fused maxpool_{n=1,s=2}(relu(conv(x) + bias)) (tc_fwd_tr.cu); the conv output is not materialised
+// strided bf16 NHWC backward-data by phase classes on the tensor cores (lat_dgrad.cu)
+bool lat_dgrad_supported(const Geom& g, int Cin, int Cout);
+size_t lat_dgrad_ws_bytes(const Geom& g, int Cin, int Cout);
+hex_status_t lat_dgrad(const Geom& g, int Cin, int Cout, const void* dy, const void* w, const void* relu_y, void* dx,
+                       void* ws, size_t ws_bytes, cudaStream_t st);
 bool tc_conv_pool_supported(const Geom& g, int Cin, int Cout, int mode);  // fused conv + ReLU + pool (max / avg)
 bool tc_conv3d_supported(const Geom& g, int Cin, int Cout, int Do);
 hex_status_t tc_conv3d_fwd(const TcConvArgs& a, int D, int Do, int sd, int kd, cudaStream_t st);

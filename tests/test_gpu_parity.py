@@ -390,3 +390,31 @@ def test_conv_strided_tensor_core_backward(F, oracle, s):
         assert F.conv_algo(B, Cin, Cout, H, W, n, s, pi, torch.bfloat16, "NHWC", 1) == "tcgen05"
         assert F.conv_algo(B, Cin, Cout, H, W, n, s, pi, torch.bfloat16, "NHWC", 2) == "tcgen05"
         _conv_case(F, oracle, pi, n, s, H, W, B, Cin, Cout, torch.bfloat16, "NHWC", 1400 + 10 * s + k)
+
+
+@pytest.mark.parametrize("s", [2, 3])
+@pytest.mark.parametrize("pi", [0, 1])
+def test_strided_bwd_data_phase_classes(F, oracle, s, pi):
+    # strided bf16 NHWC bwd-data by phase classes (lat_dgrad.cu, f4): only the lattice taps are multiplied;
+    # against the oracle (fused ReLU-backward mask included) and against the upsampled route it replaces
+    from paper_1903_01814_b200 import _abi as A
+    import synth
+    for k, (B, Cin, Cout, H, W, n) in enumerate([(2, 64, 128, 21, 22, 1), (1, 128, 64, 17, 19, 2),
+                                                  (2, 256, 48, 12, 13, 3)]):
+        T = oracle.num_taps(n)
+        Ho, Wo, _ = oracle.out_shape(H, W, s, pi)
+        g = synth.round_bf16(synth.normal((B, Cout, Ho, Wo), 1500 + k))
+        w = synth.round_bf16(synth.normal((Cout, Cin, T), 1510 + k, 1.0 / np.sqrt(Cout * T)))
+        m = synth.round_bf16(synth.normal((B, Cin, H, W), 1520 + k))
+        gd, md = to_dev(g, torch.bfloat16, "NHWC"), to_dev(m, torch.bfloat16, "NHWC")
+        wd = torch.from_numpy(w.astype(np.float32)).to(torch.bfloat16).cuda()
+        x0 = np.zeros((B, Cin, H, W))
+        dxr, _, _ = oracle.conv2d_bwd(x0, w, g, n=n, s=s, pi=pi)
+        dx = F.conv2d_bwd_data(gd, wd, (H, W), n=n, stride=s, parity=pi, layout="NHWC")
+        assert rel(to_np(dx, "NHWC"), dxr) <= TOL_BF16, (s, pi, k)
+        dxm = F.conv2d_bwd_data(gd, wd, (H, W), n=n, stride=s, parity=pi, layout="NHWC", relu_y=md)
+        assert rel(to_np(dxm, "NHWC"), dxr * (m > 0)) <= TOL_BF16, (s, pi, k, "mask")
+        if Cout % 8 == 0 and Cin % 64 == 0 and Cout % 64 == 0:
+            with A.switch("HEXCONV_NO_LAT_DGRAD"):
+                dxu = F.conv2d_bwd_data(gd, wd, (H, W), n=n, stride=s, parity=pi, layout="NHWC", relu_y=md)
+            assert rel(to_np(dxm, "NHWC"), to_np(dxu, "NHWC")) <= 1e-2
