@@ -451,13 +451,6 @@ hex_status_t lat_dgrad(const Geom& g, int Cin, int Cout, const void* dy, const v
     const int NT = lat_nt(Cin);
     const int kc16 = Cout / 16;
     uint8_t* wp = reinterpret_cast<uint8_t*>(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
-    {
-        const int64_t total = (int64_t)(Cin / NT) * g.T * kc16 * NT * 16;
-        lat_pack_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)wp, Cout, Cin,
-                                                               g.T, NT, kc16);
-        count_launch();
-        if (last_launch_status() != HEX_OK) return HEX_ERR_CUDA;
-    }
     LdParams p{};
     p.dy = (const uint16_t*)dy;
     p.relu_y = (const uint16_t*)relu_y;
@@ -504,6 +497,13 @@ hex_status_t lat_dgrad(const Geom& g, int Cin, int Cout, const void* dy, const v
     p.tiles = tile0 * p.ntiles;
     const int smem = 1024 + LD_STAGES * LD_KPS * NT * 32 + LD_BLD_WARPS * 4096 + 3 * LD_STAGES * 8 + 32 + 16 + 6 * nk + 16;
     if (smem > LD_SMEM_MAX) return HEX_ERR_UNSUPPORTED;
+    {  // weights packed only once the plan fits (UNSUPPORTED above launches nothing)
+        const int64_t total = (int64_t)(Cin / NT) * g.T * kc16 * NT * 16;
+        lat_pack_kernel<<<ceil_div(total, 256), 256, 0, st>>>((const __nv_bfloat16*)w, (__nv_bfloat16*)wp, Cout, Cin,
+                                                               g.T, NT, kc16);
+        count_launch();
+        if (last_launch_status() != HEX_OK) return HEX_ERR_CUDA;
+    }
     const int grid = p.tiles < num_sms() ? p.tiles : num_sms();
     if (NT == 128) {
         static bool attr = false;
