@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")] + os.environ.get("HEXCONV_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -512,7 +512,8 @@ struct FpParams {
     int ntr;           // tiles per strip = ceil(H / 16)
     int full_rounds;   // strips per CTA in strip mode
     int left_regions;  // regions cut from the strips after full_rounds * gridDim.x
-    int debug;         // HEXCONV_FP_DEBUG: 1 = no epilogue work, 2 = no MMAs (timing experiments)
+    int debug;         // HEXCONV_FP_DEBUG: 1 = no epilogue work, 2 = no MMAs, 3 = window warps idle, 4 = no
+                       // converter stores (timing experiments; -DHEXCONV_TIMING_DEBUG=1 builds only)
     int nreg;          // region buffers, 2 or 4 (4: the converters drain a whole tile ahead of the windows)
     const float* bias;
     uint16_t* y;   // pooled bf16 NHWC [B][Ho][Wo][Cout]
@@ -813,7 +814,8 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
                 uint32_t vals[32];
                 ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (slot * 2 + cv) * BN + c * 32, vals);
                 ptx::tmem_ld_wait();
-                if (outside) {
+                if (HEX_DBG(p.debug) == 4) {  // timing experiment: converters skip their shared-memory stores
+                } else if (outside) {
 #pragma unroll
                     for (int ii = 0; ii < 4; ++ii)
                         *reinterpret_cast<uint4*>(rb + soff[ii]) = make_uint4(NEG_INF2, NEG_INF2, NEG_INF2, NEG_INF2);
@@ -901,7 +903,8 @@ tc_conv_maxpool_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_
                 if (tl.strip && !tl.last && et < 128)  // rows r0+14, r0+15 carry into the next tile
                     *reinterpret_cast<uint4*>(carry + c * FP_CARRY + kcar) =
                         *reinterpret_cast<const uint4*>(rb + soff);
-                if (valid && AVG) {
+                if (HEX_DBG(p.debug) == 3) {  // timing experiment: window warps skip their reads / math
+                } else if (valid && AVG) {
                     // average over the in-grid taps (A8): fp32 sum in canonical tap order from 0, times
                     // 1/count, RNE -- the operations of the unfused NHWC average pool on the bf16 conv output
                     const int c2 = 2 * C;
