@@ -19,10 +19,12 @@
 //   * B (weights, pre-split hi / lo, K-major SWIZZLE_32B: one 32-byte row = the 8 K values of one output
 //     channel) is resident in shared memory for the whole persistent kernel (one bulk copy).
 //   * Warp roles: 4 epilogue warps (TMEM -> registers -> bias / ReLU / ReLU-backward mask -> NCHW stores,
-//     coalesced across the 32 pixels of a warp), 16 builder warps in 4 groups taking taps round-robin
-//     (each thread prefetches the next 8-channel chunk while it splits and stores the current one),
-//     1 MMA-issuing warp.  A ring of 16 TMEM A stages (16 columns each: hi, lo) and two accumulators
-//     (the epilogue of tile i overlaps the MMAs of tile i+1).
+//     coalesced across the 32 pixels of a warp), 16 builder warps in 4 groups taking 4-K-step stages
+//     round-robin (all 32 loads of a stage issued before any is used; the hi / lo split as two integer ops),
+//     and 1 or 2 MMA-issuing warps (2 where the accumulators fit, N <= 32: the tcgen05.mma front end is
+//     per issuing thread) running a warp-uniform loop with elect.sync issue.  A ring of 4 TMEM A stages
+//     (4 K-steps x 16 columns: hi, lo) and two accumulator slots (the epilogue of tile i overlaps the MMAs
+//     of tile i+1).
 //
 // Modes (one kernel):
 //   forward       output pixel (R, C) of the stride-s lattice has its centre at (rho(C) + sR, sC)
