@@ -147,8 +147,8 @@ HEX_API hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* desc, in
  *      fwd       s = 1 or 2, Cin % 64 == 0, Cout % 64 == 0;
  *      bwd_data  s = 1: Cin % 64 == 0, Cout % 64 == 0 (the forward kernel on dy
  *                with reversed taps / transposed channels);  s = 2, 3 with
- *                Cin % 64 == 0, Cout % 16 == 0 and dy 32-byte aligned: phase
- *                classes (only the lattice taps); other s > 1: the s = 1
+ *                Cin % 64 == 0, Cout % 64 == 0: phase classes (only the
+ *                lattice taps, TMA boxes of dy); other s > 1: the s = 1
  *                kernel on dy scattered onto the stride-1 grid (Cout % 64 == 0);
  *      bwd_weight Cin % 64 == 0, Cout % 128 == 0 (s > 1 via the scattered dy).
  *  - Cin == 1, bf16 NHWC, Cout % 64 == 0, n <= 2: warp-level mma.sync

@@ -437,7 +437,7 @@ hex_status_t hex_conv2d_bwd_data(const hex_conv2d_desc_t* d, const void* dy, con
         return tc_conv_fwd(a, s);
     }
     if (!w) return HEX_ERR_INVALID_ARG;  // w == NULL (prepacked) only on the stride-1 tensor-core path
-    if (use_lat_dgrad(d, g) && ((uintptr_t)dy & 31) == 0 && aligned16(dx) && (!relu_y || aligned16(relu_y))) {
+    if (use_lat_dgrad(d, g) && aligned16(dy) && aligned16(dx) && (!relu_y || aligned16(relu_y))) {
         // stride s: phase classes (lat_dgrad.cu); a class list or staging that does not fit falls through
         st = lat_dgrad(g, d->in_channels, d->out_channels, dy, w, relu_y, dx, ws, ws_bytes, s);
         if (st != HEX_ERR_UNSUPPORTED) return st;
