@@ -57,6 +57,7 @@ SwitchEntry g_switches[] = {
     {"HEXCONV_NO_POOL_TMA", false, ""},
     {"HEXCONV_NO_TC_STRIDE2", false, ""},
     {"HEXCONV_NO_TC_STRIDED_BWD", false, ""},
+    {"HEXCONV_NO_TC_WGRAD_S2", false, ""},
     {"HEXCONV_NO_TF32", false, ""},
     {"HEXCONV_NO_TILED", false, ""},
     {"HEXCONV_NO_WG_TR", false, ""},
@@ -180,6 +181,9 @@ bool use_lat_dgrad(const hex_conv2d_desc_t* d, const Geom& g) {  // strided bf16
 }
 bool use_tc_bwd_data_up(const hex_conv2d_desc_t* d, const Geom& g) {
     return strided_tc_ok(d, g) && tc_conv_supported(stride1(g), d->out_channels, d->in_channels);
+}
+bool use_tc_wgrad_s2(const hex_conv2d_desc_t* d, const Geom& g) {  // stride-2 weight gradient on the lattice
+    return strided_tc_ok(d, g) && tc_wgrad_s2_supported(g, d->in_channels, d->out_channels);
 }
 bool use_tc_wgrad_up(const hex_conv2d_desc_t* d, const Geom& g) {
     return strided_tc_ok(d, g) && tc_wgrad_supported(stride1(g), d->in_channels, d->out_channels);
@@ -310,6 +314,7 @@ hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* d, int32_t pass,
             return HEX_OK;
         case 2:
             *bytes = use_tc_wgrad(d, g)      ? tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
+                     : use_tc_wgrad_s2(d, g) ? tc_wgrad_s2_ws_bytes(g, d->in_channels, d->out_channels)
                      : use_tc_wgrad_up(d, g) ? up_bytes(d, g) + tc_wgrad_ws_bytes(stride1(g), d->in_channels,
                                                                                    d->out_channels)
                      : use_tf32_wgrad(d, g)  ? tf32_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
@@ -334,7 +339,11 @@ hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* d, int32_t pass, int32_t* 
                     : use_tf32_bwd_data(d, g)                                              ? 2
                                                                                            : 0;
             return HEX_OK;
-        case 2: *algo = use_tc_wgrad(d, g) || use_tc_wgrad_up(d, g) ? 1 : use_tf32_wgrad(d, g) ? 2 : 0; return HEX_OK;
+        case 2:
+            *algo = use_tc_wgrad(d, g) || use_tc_wgrad_s2(d, g) || use_tc_wgrad_up(d, g) ? 1
+                    : use_tf32_wgrad(d, g)                                             ? 2
+                                                                                       : 0;
+            return HEX_OK;
         default: return HEX_ERR_INVALID_ARG;
     }
 }
@@ -507,6 +516,13 @@ hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* d, const void* x, co
         if (!aligned16(x) || !aligned16(dy)) return HEX_ERR_ALIGNMENT;
         const size_t need = tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels);
         if (need && (!ws || ws_bytes < need)) return HEX_ERR_WORKSPACE;
+        TcWgradArgs a{};
+        a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
+        a.x = x; a.dy = dy; a.dw = dw; a.dbias = dbias; a.accumulate = accumulate;
+        return tc_conv_wgrad(a, ws, ws_bytes, s);
+    }
+    if (use_tc_wgrad_s2(d, g)) {  // stride 2: the lattice walked directly, x boxes with element stride 2
+        if (!aligned16(x) || !aligned16(dy)) return HEX_ERR_ALIGNMENT;
         TcWgradArgs a{};
         a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;
         a.x = x; a.dy = dy; a.dw = dw; a.dbias = dbias; a.accumulate = accumulate;

@@ -856,7 +856,30 @@ struct TcWgParams {
     int dbg;         // development: 1 = skip TMA loads, 2 = skip MMAs (results invalid)
     int8_t tap_dc[2][TC_MAXT];
     int8_t tap_dr[2][TC_MAXT];
+    int s;  // 1, or 2: the pixel tiles walk the stride-2 lattice (dy) and the x maps traverse with element stride 2
 };
+
+// x box of tap (dc, dr) for the pixel tile (P, r0, j0), and the centre-column parity that selects the tap table.
+//   s = 1: tile of parity view P; x view (P + dc) mod 2, sub-column j0 + shift, row r0 + dr (tap reuse as the
+//          forward).
+//   s = 2: tile of lattice view P (output columns C = 2C' + P, centres (P + 2R, 4C' + 2P): rho(C) = C mod 2,
+//          DESIGN.md A5); the x maps traverse rows and view sub-columns with element stride 2, so the box starts
+//          at x view dc mod 2, sub-column 2 j0 + (2P + dc - Pv) / 2, row 2 r0 + P + dr (the forward's tap_box).
+__device__ __forceinline__ int wg_centre_parity(const TcWgParams& p, int P) {
+    return p.s == 1 ? (P + p.parity) & 1 : p.parity & 1;
+}
+__device__ __forceinline__ void wg_xbox(const TcWgParams& p, int P, int r0, int j0, int dc, int dr, int* Pv,
+                                        int* row, int* col) {
+    if (p.s == 1) {
+        *Pv = (P + dc) & 1;
+        *col = j0 + (P + dc - *Pv) / 2;
+        *row = r0 + dr;
+    } else {
+        *Pv = dc & 1;
+        *col = 2 * j0 + (2 * P + dc - *Pv) / 2;
+        *row = 2 * r0 + P + dr;
+    }
+}
 
 __device__ __forceinline__ void decode_ptile(const TcWgParams& p, int m, int* P, int* r0, int* j0, int* b0) {
     int jt;
@@ -925,7 +948,7 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
             for (int pt = pt_begin; pt < pt_end; ++pt) {
                 int P, r0, j0, b0;
                 decode_ptile(p, pt, &P, &r0, &j0, &b0);
-                const int pc = (P + p.parity) & 1;
+                const int pc = wg_centre_parity(p, P);
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* s = smem + stage * Cfg::STAGE_BYTES;
                 if (HEX_DBG(p.dbg) == 1) {
@@ -938,11 +961,10 @@ tc_conv_wgrad_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_co
                 ptx::tma_load_5d(P ? &map_dy1 : &map_dy0, &full[stage], s, 0, r0, j0, b0, co0 / 64);
                 for (int i = 0; i < na; i += p.cpo) {
                     const int t = (a0 + i) / p.kchunks, kc = (a0 + i) - t * p.kchunks;
-                    const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
-                    const int Pv = (P + dc) & 1;
-                    const int jsh = (P + dc - Pv) / 2;
-                    ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], s + (2 + i) * Cfg::BOX, 0, r0 + dr,
-                                     j0 + jsh, b0, kc);
+                    int Pv, row, col;
+                    wg_xbox(p, P, r0, j0, p.tap_dc[pc][t], p.tap_dr[pc][t], &Pv, &row, &col);
+                    ptx::tma_load_5d(Pv ? &map_x1 : &map_x0, &full[stage], s + (2 + i) * Cfg::BOX, 0, row, col, b0,
+                                     kc);
                 }
                 if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
             }
@@ -1106,7 +1128,7 @@ tc_conv_wgrad2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_c
             for (int pt = pt_begin; pt < pt_end; ++pt) {
                 int P, r0, j0, b0;
                 decode_ptile(p, pt, &P, &r0, &j0, &b0);
-                const int pc = (P + p.parity) & 1;
+                const int pc = wg_centre_parity(p, P);
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* s = smem + stage * Cfg::STAGE_BYTES;
                 if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
@@ -1116,11 +1138,10 @@ tc_conv_wgrad2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_c
                     if (q == 0) break;
                     const int a = a0 + 4 * m + (int)rank * (q / 2);
                     const int t = a / p.kchunks, kc = a - t * p.kchunks;
-                    const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
-                    const int Pv = (P + dc) & 1;
-                    const int jsh = (P + dc - Pv) / 2;
-                    ptx::tma_load_5d_2sm(Pv ? &map_x1 : &map_x0, &full[stage], s + (2 + 2 * m) * Cfg::BOX, 0, r0 + dr,
-                                         j0 + jsh, b0, kc);
+                    int Pv, row, col;
+                    wg_xbox(p, P, r0, j0, p.tap_dc[pc][t], p.tap_dr[pc][t], &Pv, &row, &col);
+                    ptx::tma_load_5d_2sm(Pv ? &map_x1 : &map_x0, &full[stage], s + (2 + 2 * m) * Cfg::BOX, 0, row,
+                                         col, b0, kc);
                 }
                 if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
             }
@@ -1336,19 +1357,47 @@ hex_status_t tc_conv3d_wgrad(const TcWgradArgs& a, const TrDepth& dz, void* ws, 
                         st);
 }
 
+// stride 2: the one-box-per-tap weight gradient walks the dy LATTICE directly -- its pixel
+// tiles are tiles of the lattice's column-parity views and every tap's x box is read with element stride 2
+// (wg_xbox) -- instead of the stride-1 kernel on dy scattered onto the full grid (4x the MMAs, mostly zeros)
+static Geom lattice_geom(const Geom& g) {
+    Geom gl = g;
+    gl.H = g.Ho;
+    gl.W = g.Wo;
+    gl.s = 1;
+    return gl;
+}
+
+bool tc_wgrad_s2_supported(const Geom& g, int Cin, int Cout) {
+    if (g.s != 2 || g.T > TC_MAXT || g.Wo < 2 || Cout % 128 != 0 || Cin % 64 != 0) return false;
+    if (sw_on("HEXCONV_DISABLE_TC") || sw_on("HEXCONV_NO_TC_WGRAD_S2")) return false;
+    const WgPlan w = wg_plan(lattice_geom(g), Cin, Cout);
+    if (w.RB * 2 > 256 || w.JB * 2 > 256) return false;
+    return get_encode() != nullptr;
+}
+
+size_t tc_wgrad_s2_ws_bytes(const Geom& g, int Cin, int Cout) {
+    const WgPlan w = wg_plan(lattice_geom(g), Cin, Cout);
+    return (size_t)w.chunks * g.T * Cout * Cin * sizeof(float) + (size_t)w.chunks * Cout * sizeof(float) + 256;
+}
+
 hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
     const Geom& g = a.g;
-    if (tc_wgrad_tr_supported(g, a.Cin, a.Cout)) {  // tap-reuse kernel (tc_wgrad_tr.cu)
+    const bool s2 = g.s == 2;
+    if (!s2 && tc_wgrad_tr_supported(g, a.Cin, a.Cout)) {  // tap-reuse kernel (tc_wgrad_tr.cu)
         int chunks = 0;
         float* db_part = nullptr;
         const hex_status_t s = tc_wgrad_tr(a, ws, ws_bytes, &chunks, &db_part, st);
         if (s != HEX_OK) return s;
         return wgrad_reduce((const float*)ws, chunks, g.T, a.Cout, a.Cin, a.dw, db_part, a.dbias, a.accumulate, st);
     }
-    const WgPlan w = wg_plan(g, a.Cin, a.Cout);
-    if (ws_bytes < tc_wgrad_ws_bytes(g, a.Cin, a.Cout)) return HEX_ERR_WORKSPACE;
+    const Geom gt = s2 ? lattice_geom(g) : g;  // the grid the pixel tiles walk
+    const WgPlan w = wg_plan(gt, a.Cin, a.Cout);
+    if (ws_bytes < (s2 ? tc_wgrad_s2_ws_bytes(g, a.Cin, a.Cout) : tc_wgrad_ws_bytes(g, a.Cin, a.Cout)))
+        return HEX_ERR_WORKSPACE;
     TcWgParams p{};
-    p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
+    p.B = g.B; p.H = gt.H; p.W = gt.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
+    p.s = s2 ? 2 : 1;
     p.RB = w.RB; p.JB = w.JB; p.BB = w.BB; p.rt = w.rt; p.bt = w.bt; p.jt0 = w.jt0; p.jt1 = w.jt1;
     p.tiles0 = w.tiles0; p.ptiles = w.ptiles;
     p.kchunks = w.kchunks; p.cpo = w.cpo; p.n_atoms = w.n_atoms; p.groups = w.groups; p.co_tiles = w.co_tiles;
@@ -1365,10 +1414,11 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
         }
     CUtensorMap mx0, mx1, md0, md1;
     const int xbox = w.pair ? 2 : w.cpo;
-    if (!make_view_map5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, w.RB, w.JB, w.BB, xbox)) return HEX_ERR_CUDA;
-    if (!make_view_map5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, w.RB, w.JB, w.BB, xbox)) return HEX_ERR_CUDA;
-    if (!make_view_map5(&md0, a.dy, g.B, g.H, g.W, a.Cout, 0, w.RB, w.JB, w.BB, 2)) return HEX_ERR_CUDA;
-    if (!make_view_map5(&md1, a.dy, g.B, g.H, g.W, a.Cout, 1, w.RB, w.JB, w.BB, 2)) return HEX_ERR_CUDA;
+    const int es = s2 ? 2 : 1;
+    if (!make_view_map5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, w.RB, w.JB, w.BB, xbox, es)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, w.RB, w.JB, w.BB, xbox, es)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&md0, a.dy, g.B, gt.H, gt.W, a.Cout, 0, w.RB, w.JB, w.BB, 2)) return HEX_ERR_CUDA;
+    if (!make_view_map5(&md1, a.dy, g.B, gt.H, gt.W, a.Cout, 1, w.RB, w.JB, w.BB, 2)) return HEX_ERR_CUDA;
     const int units = w.co_tiles * w.groups * w.chunks;
     if (w.pair) {
         static bool attr2 = false;

@@ -418,3 +418,26 @@ def test_strided_bwd_data_phase_classes(F, oracle, s, pi):
             with A.switch("HEXCONV_NO_LAT_DGRAD"):
                 dxu = F.conv2d_bwd_data(gd, wd, (H, W), n=n, stride=s, parity=pi, layout="NHWC", relu_y=md)
             assert rel(to_np(dxm, "NHWC"), to_np(dxu, "NHWC")) <= 1e-2
+
+
+@pytest.mark.parametrize("pi", [0, 1])
+def test_stride2_wgrad_on_the_lattice(F, oracle, pi):
+    # stride-2 bf16 weight gradient walking the dy lattice directly (x boxes with element stride 2; f4): against
+    # the oracle and bit-identical... within fp32 summation order of the scattered-dy route it replaces
+    from paper_1903_01814_b200 import _abi as A
+    import synth
+    for k, (B, Cin, Cout, H, W, n) in enumerate([(2, 64, 128, 21, 22, 1), (1, 128, 256, 17, 19, 2),
+                                                  (3, 64, 128, 9, 8, 1)]):
+        T = oracle.num_taps(n)
+        Ho, Wo, _ = oracle.out_shape(H, W, 2, pi)
+        x = synth.round_bf16(synth.normal((B, Cin, H, W), 1600 + k))
+        g = synth.round_bf16(synth.normal((B, Cout, Ho, Wo), 1610 + k))
+        xd, gd = to_dev(x, torch.bfloat16, "NHWC"), to_dev(g, torch.bfloat16, "NHWC")
+        assert F.conv_algo(B, Cin, Cout, H, W, n, 2, pi, torch.bfloat16, "NHWC", 2) == "tcgen05"
+        dw, db = F.conv2d_bwd_weight(xd, gd, n=n, stride=2, parity=pi, layout="NHWC")
+        _, dwr, dbr = oracle.conv2d_bwd(x, np.zeros((Cout, Cin, T)), g, n=n, s=2, pi=pi)
+        assert rel(dw.cpu().numpy(), dwr) <= 1e-4, (pi, k)
+        assert rel(db.cpu().numpy(), dbr) <= 1e-4, (pi, k)
+        with A.switch("HEXCONV_NO_TC_WGRAD_S2"):
+            dwu, dbu = F.conv2d_bwd_weight(xd, gd, n=n, stride=2, parity=pi, layout="NHWC")
+        assert rel(dw.cpu().numpy(), dwu.cpu().numpy().astype(np.float64)) <= 1e-5

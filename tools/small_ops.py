@@ -87,6 +87,10 @@ def s2_ops():
         dx = torch.empty(B, H, W, C, device="cuda", dtype=torch.bfloat16)
         out[f"s2_n{n}_dgrad"] = (lambda w=w, g=g, dx=dx, n=n:
                                  F.conv2d_bwd_data(g, w, (H, W), n=n, stride=2, layout="NHWC", out=dx))
+        x = torch.randn(B, H, W, C, device="cuda").to(torch.bfloat16)
+        dw = torch.empty(C, C, T, device="cuda")
+        out[f"s2_n{n}_wgrad"] = (lambda x=x, g=g, dw=dw, n=n:
+                                 F.conv2d_bwd_weight(x, g, n=n, stride=2, layout="NHWC", dw=dw))
     return out
 
 
