@@ -32,8 +32,9 @@
  *    `stream` (a cudaStream_t; NULL = legacy default stream).  A launch
  *    failure returns HEX_ERR_CUDA; device faults surface at the caller's next
  *    synchronisation.
- *  - No device memory is allocated inside a call: scratch space is passed in
- *    `ws` (device) of `ws_bytes`, sized by hex_conv2d_workspace_size().
+ *  - No device memory is allocated inside a call (except the NVLS setup
+ *    calls hex_nvls_open / hex_nvls_map): scratch space is passed in `ws`
+ *    (device) of `ws_bytes`, sized by hex_conv2d_workspace_size().
  *  - Thread-safe and re-entrant.  Results are deterministic (no floating
  *    point atomics): the same inputs give bitwise identical outputs.
  *  - HEX_BF16 tensors use round-to-nearest-even from fp32 accumulators.
@@ -347,6 +348,59 @@ HEX_API hex_status_t hex_relu_bwd(int64_t count, int32_t dtype, const void* dy, 
                                   hex_stream_t stream);
 
 HEX_API hex_status_t hex_cast_f32_bf16(int64_t count, const float* src, void* dst, hex_stream_t stream);
+
+/* ---------------------------------------------------------------- NVLS gradient sum
+ * The data-parallel exchange of the method's training step -- the sum over
+ * ranks of the flat fp32 gradient vector (every rank trains on its own share
+ * of the batch) -- performed inside the NVSwitch: the
+ * gradient vector lives in device memory bound to a CUDA multicast object
+ * spanning one GPU per rank.  Ranks write their local gradients through the
+ * unicast pointer; hex_nvls_allreduce_f32 then replaces a bucket of it, on
+ * every rank, by the sum over ranks (multimem.ld_reduce of a 1/world slice
+ * per rank + multimem.st to all replicas, ordered by multicast counters; see
+ * csrc/nvls.cu).  Every rank ends with bitwise identical sums.
+ *
+ * Setup (collective: every rank calls each step, in order, with a barrier
+ * between the steps; the only calls that allocate device memory):
+ *   1. hex_nvls_open: rank 0 creates the multicast object and, for world > 1,
+ *      exports it as a POSIX file descriptor (*fd_out, host; the caller passes
+ *      it to the other ranks, e.g. SCM_RIGHTS, and closes it); ranks > 0
+ *      import it from fd_in (host; the caller may close it afterwards).  Every
+ *      rank attaches `device`.  data_bytes: the region the caller needs.
+ *   2. barrier (all devices attached)
+ *   3. hex_nvls_map: backs the object with `device` memory, maps it, zeroes
+ *      it; *uc = local pointer, *mc = multicast pointer (device), *map_bytes =
+ *      usable bytes (data_bytes rounded up to 256).
+ *   4. barrier (all counters zero)
+ * hex_nvls_allreduce_f32(h, offset, count, slot, stream): sums elements
+ * [offset, offset+count) of the fp32 region across the ranks, asynchronously
+ * on `stream` after the work already enqueued there; offset % 4 == 0
+ * (HEX_ERR_ALIGNMENT), the bucket must lie in the region (HEX_ERR_SHAPE).
+ * `slot` (0 .. HEX_NVLS_SLOTS-1) names the call site: every rank must issue
+ * the same sequence of (slot, offset, count) calls; concurrent calls must use
+ * different slots.  Graph-capturable (its epoch counters live in device
+ * memory).  A rank that does not arrive within 10 s makes the others trap (a
+ * launch failure at their next synchronisation) instead of hanging.
+ * hex_nvls_supported: *supported = 1 if `device` exists, reports multicast
+ * support and a one-device multicast object can actually be created (a GPU
+ * leased without its NVSwitch fabric reports the attribute but cannot).  hex_nvls_close: synchronises the device, unmaps, frees.
+ * hex_nvls_plan (host only, no GPU needed): the element range [*begin, *end)
+ * that (rank, cta) reduces for a bucket of `count` elements, and the grid
+ * size *grid (cta = -1: grid only).
+ * Errors: HEX_ERR_UNSUPPORTED (no multicast support), HEX_ERR_CUDA (a driver
+ * call failed; the message is printed to stderr), HEX_ERR_INVALID_ARG. */
+#define HEX_NVLS_SLOTS 64
+#define HEX_NVLS_MAX_CTAS 148
+typedef struct hex_nvls hex_nvls_t;
+HEX_API hex_status_t hex_nvls_supported(int32_t device, int32_t* supported);
+HEX_API hex_status_t hex_nvls_open(int32_t world, int32_t rank, int32_t device, size_t data_bytes,
+                                   int32_t fd_in, int32_t* fd_out, hex_nvls_t** out);
+HEX_API hex_status_t hex_nvls_map(hex_nvls_t* h, void** uc, void** mc, size_t* map_bytes);
+HEX_API hex_status_t hex_nvls_allreduce_f32(hex_nvls_t* h, int64_t offset, int64_t count, int32_t slot,
+                                            hex_stream_t stream);
+HEX_API hex_status_t hex_nvls_close(hex_nvls_t* h);
+HEX_API hex_status_t hex_nvls_plan(int64_t count, int32_t world, int32_t rank, int32_t cta, int32_t* grid,
+                                   int64_t* begin, int64_t* end);
 
 /* ---------------------------------------------------------------- misc */
 HEX_API const char* hex_status_string(hex_status_t status);

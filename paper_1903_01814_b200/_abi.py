@@ -103,6 +103,12 @@ _SIGS = {
     "hex_sgd_momentum": (_i32, [_i64, _vp, _vp, _vp, _f32, _f32, _f32, _vp, _vp]),
     "hex_cast_f32_bf16": (_i32, [_i64, _vp, _vp, _vp]),
     "hex_relu_bwd": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp]),
+    "hex_nvls_supported": (_i32, [_i32, _i32p]),
+    "hex_nvls_open": (_i32, [_i32, _i32, _i32, _sz, _i32, _i32p, ctypes.POINTER(_vp)]),
+    "hex_nvls_map": (_i32, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _szp]),
+    "hex_nvls_allreduce_f32": (_i32, [_vp, _i64, _i64, _i32, _vp]),
+    "hex_nvls_close": (_i32, [_vp]),
+    "hex_nvls_plan": (_i32, [_i64, _i32, _i32, _i32, _i32p, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(_lib, _name)

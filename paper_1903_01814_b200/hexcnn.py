@@ -7,7 +7,8 @@ ReLU), hex max-pool n=1 stride 2 after layers 2 and 4, global average pool,
 linear head to 2 logits, softmax cross-entropy.  bf16 NHWC activations,
 fp32 master weights, SGD with momentum 0.9; data parallel over the batch with
 the weight-gradient sum over NCCL (torch.distributed) -- the only exchange
-step of the method.
+step of the method -- or, with nvls=True, inside the
+NVSwitch by the library's multimem kernel (nvls.py, csrc/nvls.cu).
 
 Every tensor operation is a call into libhexconv (include/hexconv.h) on
 buffers allocated once here; torch provides device memory, the stream and
@@ -65,7 +66,7 @@ class HexCNN:
     def __init__(self, batch: int = 256, H: int = 96, W: int = 96,
                  channels=(1, 64, 128, 128, 256, 256, 256), ns=(2, 1, 2, 1, 2, 1), pool_after=(2, 4),
                  num_classes: int = 2, lr: float = 1e-3, momentum: float = 0.9, seed: int = 0,
-                 device="cuda", process_group=None, reduce_grads=None):
+                 device="cuda", process_group=None, reduce_grads=None, nvls=None):
         self.B, self.H, self.W = batch, H, W
         self.channels, self.ns, self.pool_after = tuple(channels), tuple(ns), tuple(pool_after)
         self.K = num_classes
@@ -77,6 +78,10 @@ class HexCNN:
         # forces it at world size 1 too (tests: a one-rank NCCL group captured in a CUDA graph)
         self.reduce_grads = (self.world > 1) if reduce_grads is None else bool(reduce_grads)
         self.L = len(ns)
+        # gradient sum inside the NVSwitch (nvls.py, csrc/nvls.cu) instead of NCCL buckets: HEXCNN_NVLS=1 or
+        # nvls=True; the gradient vector then lives in multicast-bound memory
+        self.nvls = bool(os.environ.get("HEXCNN_NVLS")) if nvls is None else bool(nvls)
+        self._nv = None
         self.timer = None  # optional list: (kind, layer, start_event, end_event) around conv calls
         # weight gradients on a side stream (HEXCNN_SIDE_BWD=1): measured no faster than one stream once the
         # training data is finite (3.52 vs 3.47 ms per step), and it blurs the per-family event timings
@@ -130,6 +135,12 @@ class HexCNN:
         self.params = torch.from_numpy(flat).to(self.dev)
         self.params_bf16 = self.params.to(torch.bfloat16)
         self.grads = torch.zeros_like(self.params)
+        if self.nvls and self.reduce_grads:
+            from .nvls import NvlsBuffer
+            self._nv = NvlsBuffer(4 * self.nparams, self.pg, self.dev)
+            g = self._nv.tensor(self.nparams)
+            g.zero_()
+            self.grads = g
         self.mom = torch.zeros_like(self.params)
 
     def weight(self, l, bf16=True):
@@ -303,18 +314,28 @@ class HexCNN:
         if side is not main:
             main.wait_stream(side)
 
-    def _segment(self, l):
+    def _segment_range(self, l):
         if l == self.L:
-            return self.grads[self.head_w:self.nparams]
+            return self.head_w, self.nparams - self.head_w
         wo, wn, bo, bn = self.seg[l]
-        return self.grads[wo:bo + bn]
+        return wo, bo + bn - wo
+
+    def _segment(self, l):
+        off, n = self._segment_range(l)
+        return self.grads[off:off + n]
+
+    def _nvls_reduce(self, l):
+        off, n = self._segment_range(l)
+        self._nv.allreduce(off, n, slot=l)  # on the current stream, after layer l's weight gradient
 
     def step(self, x, labels):
         """One SGD step on the batch (x: bf16 [B,H,W,1] NHWC, labels: int32 [B]).
         Returns the device loss tensor (mean CE of this rank's batch)."""
         stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         self.forward(x, stream)
-        if self.reduce_grads:
+        if self.reduce_grads and self._nv is not None:
+            self.backward(x, labels, stream, self._nvls_reduce)
+        elif self.reduce_grads:
             red = GradBucketReducer(self.pg)
             self.backward(x, labels, stream, lambda l: red.launch(self._segment(l)))
             red.wait_all()
@@ -327,11 +348,12 @@ class HexCNN:
     def graphed_step(self, x, labels):
         """Capture one training step on the static buffers (x, labels) in a CUDA graph and return
         (graph, loss): graph.replay() runs the whole step (every kernel of every layer, head, the
-        per-layer NCCL gradient allreduces when data parallel, and SGD) as one launch, without per-call
+        per-layer NCCL or NVLS gradient sums when data parallel, and SGD) as one launch, without per-call
         host dispatch; refill x / labels in place between replays.  The warm-up call performs one real
         step (it also creates the NCCL communicator before capture).  Data parallel capture needs the
-        NCCL backend (gloo collectives run on the host and cannot be captured)."""
-        if self.reduce_grads and dist.get_backend(self.pg) != "nccl":
+        NCCL backend (gloo collectives run on the host and cannot be captured) unless the sums run in the
+        NVLS kernel."""
+        if self.reduce_grads and self._nv is None and dist.get_backend(self.pg) != "nccl":
             raise RuntimeError("graphed_step: data-parallel capture needs the NCCL backend")
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())

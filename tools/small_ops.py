@@ -94,8 +94,25 @@ def s2_ops():
     return out
 
 
+def nvls_ops():
+    # NVLS gradient sum of the config-5 gradient vector, one multicast replica (one GPU): the protocol's cost
+    from paper_1903_01814_b200 import nvls
+    from paper_1903_01814_b200.hexcnn import HexCNN
+    m = HexCNN(batch=2)
+    buf = nvls.NvlsBuffer(4 * m.nparams)
+    nvls_ops.keep = buf
+    segs = [m._segment_range(l) for l in range(m.L + 1)]
+
+    def run():
+        for l, (off, n) in enumerate(segs):
+            buf.allreduce(off, n, l)
+    return {"nvls_c5_buckets": run, "nvls_c5_l5": lambda: buf.allreduce(*segs[4], 20)}
+
+
 def main():
     ops = c3_ops()
+    if any(a.startswith("nvls") for a in sys.argv[1:]):
+        ops.update(nvls_ops())
     if any(a.startswith("s2") for a in sys.argv[1:]):
         ops.update(s2_ops())
     if any(a.startswith("c3d") for a in sys.argv[1:]):
