@@ -465,33 +465,37 @@ def secondary_measurements(dev, peak_tf, peak_gbs):
     out["conv3d_64to128_16x64x64_kd3_bf16"] = c3d
     del x, g3
 
-    # ---- f4: stride-2 layer on the tensor cores (forward by stride-2 boxes, bwd-data by phase classes, weight
-    # gradient on the lattice), bf16 NHWC 64 images 96x96 -> 48x48, 128 -> 128, n = 1 and 2.  Synthetic shape;
-    # FLOPs of the in-grid (lattice) taps only.
+    # ---- f4: strided layers on the tensor cores (forward by element-stride-s boxes, bwd-data by phase classes,
+    # weight gradient on the lattice), bf16 NHWC 64 images 96x96 -> 48x48 (s = 2) / 32x32 (s = 3), 128 -> 128,
+    # n = 1 and 2.  Synthetic shape; FLOPs of the in-grid (lattice) taps only.
     B, H, W, C = 64, 96, 96, 128
-    Ho, Wo, _ = F.output_shape(H, W, 2)
     x = torch.randn(B, H, W, C, device=dev).to(torch.bfloat16)
-    g2 = torch.randn(B, Ho, Wo, C, device=dev).to(torch.bfloat16)
-    y2, dx2 = torch.empty_like(g2), torch.empty_like(x)
-    dw2 = {}
-    s2 = {}
-    for n in (1, 2):
-        T = F.num_taps(n)
-        w = (torch.randn(C, C, T, device=dev) / (C * T) ** 0.5).to(torch.bfloat16)
-        dw2[n] = torch.empty(C, C, T, device=dev)
-        fl2 = 2.0 * B * vt(H, W, n, 2) * C * C  # in-grid taps of the lattice outputs
-        for name, fn in (("fwd", lambda w=w: F.conv2d_fwd(x, w, None, n=n, stride=2, layout="NHWC", out=y2)),
-                         ("dgrad", lambda w=w: F.conv2d_bwd_data(g2, w, (H, W), n=n, stride=2, layout="NHWC",
-                                                                 out=dx2)),
-                         ("wgrad", lambda: F.conv2d_bwd_weight(x, g2, n=n, stride=2, layout="NHWC", dw=dw2[n]))):
-            hot, fl = gt.time(gt.capture(fn), 10)
-            tf = fl2 / (fl * 1e-3) / 1e12
-            s2[f"n{n}_{name}"] = {"us_flushed": fl * 1e3, "us_hot": hot * 1e3, "tflops": tf,
-                                  "frac_of_bf16_peak": tf / peak_tf}
-    s2["note"] = ("bf16 NHWC stride 2, tcgen05: forward with stride-2 input boxes, bwd-data by phase classes (TMA boxes "
-                  "of dy parity views), weight gradient on the lattice (element-stride-2 x boxes); FLOPs of the "
-                  "in-grid taps of the lattice outputs")
-    out["stride2_128to128_96x96_bf16"] = s2
+    dx2 = torch.empty_like(x)
+    for s in (2, 3):
+        Ho, Wo, _ = F.output_shape(H, W, s)
+        g2 = torch.randn(B, Ho, Wo, C, device=dev).to(torch.bfloat16)
+        y2 = torch.empty_like(g2)
+        dw2 = {}
+        ent = {}
+        for n in (1, 2):
+            T = F.num_taps(n)
+            w = (torch.randn(C, C, T, device=dev) / (C * T) ** 0.5).to(torch.bfloat16)
+            dw2[n] = torch.empty(C, C, T, device=dev)
+            fl2 = 2.0 * B * vt(H, W, n, s) * C * C  # in-grid taps of the lattice outputs
+            for name, fn in (("fwd", lambda w=w, s=s, n=n, g2=g2, y2=y2:
+                              F.conv2d_fwd(x, w, None, n=n, stride=s, layout="NHWC", out=y2)),
+                             ("dgrad", lambda w=w, s=s, n=n, g2=g2:
+                              F.conv2d_bwd_data(g2, w, (H, W), n=n, stride=s, layout="NHWC", out=dx2)),
+                             ("wgrad", lambda s=s, n=n, g2=g2:
+                              F.conv2d_bwd_weight(x, g2, n=n, stride=s, layout="NHWC", dw=dw2[n]))):
+                hot, fl = gt.time(gt.capture(fn), 10)
+                tf = fl2 / (fl * 1e-3) / 1e12
+                ent[f"n{n}_{name}"] = {"us_flushed": fl * 1e3, "us_hot": hot * 1e3, "tflops": tf,
+                                       "frac_of_bf16_peak": tf / peak_tf}
+        ent["note"] = (f"bf16 NHWC stride {s}, tcgen05: forward with element-stride-{s} input boxes, bwd-data by "
+                       f"phase classes (TMA boxes of dy parity views), weight gradient on the lattice "
+                       f"(element-stride-{s} x boxes); FLOPs of the in-grid taps of the lattice outputs")
+        out[f"stride{s}_128to128_96x96_bf16"] = ent
     return out
 
 

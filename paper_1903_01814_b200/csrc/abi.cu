@@ -55,9 +55,9 @@ SwitchEntry g_switches[] = {
     {"HEXCONV_NO_LAT_DGRAD", false, ""},
     {"HEXCONV_NO_PLANE", false, ""},
     {"HEXCONV_NO_POOL_TMA", false, ""},
-    {"HEXCONV_NO_TC_STRIDE2", false, ""},
+    {"HEXCONV_NO_TC_STRIDED_FWD", false, ""},
     {"HEXCONV_NO_TC_STRIDED_BWD", false, ""},
-    {"HEXCONV_NO_TC_WGRAD_S2", false, ""},
+    {"HEXCONV_NO_TC_WGRAD_LAT", false, ""},
     {"HEXCONV_NO_TF32", false, ""},
     {"HEXCONV_NO_TILED", false, ""},
     {"HEXCONV_NO_WG_TR", false, ""},
@@ -182,8 +182,8 @@ bool use_lat_dgrad(const hex_conv2d_desc_t* d, const Geom& g) {  // strided bf16
 bool use_tc_bwd_data_up(const hex_conv2d_desc_t* d, const Geom& g) {
     return strided_tc_ok(d, g) && tc_conv_supported(stride1(g), d->out_channels, d->in_channels);
 }
-bool use_tc_wgrad_s2(const hex_conv2d_desc_t* d, const Geom& g) {  // stride-2 weight gradient on the lattice
-    return strided_tc_ok(d, g) && tc_wgrad_s2_supported(g, d->in_channels, d->out_channels);
+bool use_tc_wgrad_lat(const hex_conv2d_desc_t* d, const Geom& g) {  // strided (s = 2, 3) weight gradient on the lattice
+    return strided_tc_ok(d, g) && tc_wgrad_lat_supported(g, d->in_channels, d->out_channels);
 }
 bool use_tc_wgrad_up(const hex_conv2d_desc_t* d, const Geom& g) {
     return strided_tc_ok(d, g) && tc_wgrad_supported(stride1(g), d->in_channels, d->out_channels);
@@ -314,7 +314,7 @@ hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* d, int32_t pass,
             return HEX_OK;
         case 2:
             *bytes = use_tc_wgrad(d, g)      ? tc_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
-                     : use_tc_wgrad_s2(d, g) ? tc_wgrad_s2_ws_bytes(g, d->in_channels, d->out_channels)
+                     : use_tc_wgrad_lat(d, g) ? tc_wgrad_lat_ws_bytes(g, d->in_channels, d->out_channels)
                      : use_tc_wgrad_up(d, g) ? up_bytes(d, g) + tc_wgrad_ws_bytes(stride1(g), d->in_channels,
                                                                                    d->out_channels)
                      : use_tf32_wgrad(d, g)  ? tf32_wgrad_ws_bytes(g, d->in_channels, d->out_channels)
@@ -340,7 +340,7 @@ hex_status_t hex_conv2d_algo(const hex_conv2d_desc_t* d, int32_t pass, int32_t* 
                                                                                            : 0;
             return HEX_OK;
         case 2:
-            *algo = use_tc_wgrad(d, g) || use_tc_wgrad_s2(d, g) || use_tc_wgrad_up(d, g) ? 1
+            *algo = use_tc_wgrad(d, g) || use_tc_wgrad_lat(d, g) || use_tc_wgrad_up(d, g) ? 1
                     : use_tf32_wgrad(d, g)                                             ? 2
                                                                                        : 0;
             return HEX_OK;
@@ -521,7 +521,7 @@ hex_status_t hex_conv2d_bwd_weight(const hex_conv2d_desc_t* d, const void* x, co
         a.x = x; a.dy = dy; a.dw = dw; a.dbias = dbias; a.accumulate = accumulate;
         return tc_conv_wgrad(a, ws, ws_bytes, s);
     }
-    if (use_tc_wgrad_s2(d, g)) {  // stride 2: the lattice walked directly, x boxes with element stride 2
+    if (use_tc_wgrad_lat(d, g)) {  // s = 2, 3: the lattice walked directly, x boxes with element stride s
         if (!aligned16(x) || !aligned16(dy)) return HEX_ERR_ALIGNMENT;
         TcWgradArgs a{};
         a.g = g; a.Cin = d->in_channels; a.Cout = d->out_channels;

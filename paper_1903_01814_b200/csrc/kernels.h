@@ -109,8 +109,8 @@ struct TcWgradArgs {
 bool tc_wgrad_supported(const Geom& g, int Cin, int Cout);
 size_t tc_wgrad_ws_bytes(const Geom& g, int Cin, int Cout);
 hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);  // s = 1, or 2 (lattice)
-bool tc_wgrad_s2_supported(const Geom& g, int Cin, int Cout);
-size_t tc_wgrad_s2_ws_bytes(const Geom& g, int Cin, int Cout);
+bool tc_wgrad_lat_supported(const Geom& g, int Cin, int Cout);
+size_t tc_wgrad_lat_ws_bytes(const Geom& g, int Cin, int Cout);
 // tap-reuse variant (tc_wgrad_tr.cu); writes split-K partials, reduced by tc_conv_wgrad
 bool tc_wgrad_tr_supported(const Geom& g, int Cin, int Cout);
 struct TrDepth {  // 3-D weight gradient: depth taps folded into the units' channel chunks

@@ -78,17 +78,18 @@ static bool make_view_map(CUtensorMap* m, const void* base, int B, int H, int W,
 // The same parity view with the channel axis split into 64-channel chunks as an
 // OUTER dimension: dims {64, H, Wp, B, C/64}, box {64, RB, JB, BB, KC}.  One TMA op
 // then fills KC consecutive canonical SW128 blocks (one per 64-channel chunk).
-// es2 = 2: rows and view sub-columns traversed with element stride 2 (stride-2 forward, tap_box)
+// estride = s > 1: rows and view sub-columns traversed with element stride s (strided forward / weight gradient,
+// lattice_box)
 static bool make_view_map5(CUtensorMap* m, const void* base, int B, int H, int W, int C, int P, int RB, int JB,
-                           int BB, int KC, int es2 = 1) {
+                           int BB, int KC, int estride = 1) {
     auto enc = get_encode();
     if (!enc) return false;
     const int Wp = (W - P + 1) / 2;
     if (Wp < 1 || C % 64) return false;
     cuuint64_t dims[5] = {64, (cuuint64_t)H, (cuuint64_t)Wp, (cuuint64_t)B, (cuuint64_t)(C / 64)};
     cuuint64_t strides[4] = {(cuuint64_t)W * C * 2, (cuuint64_t)2 * C * 2, (cuuint64_t)H * W * C * 2, 128};
-    cuuint32_t box[5] = {64, (cuuint32_t)(RB * es2), (cuuint32_t)(JB * es2), (cuuint32_t)BB, (cuuint32_t)KC};
-    cuuint32_t es[5] = {1, (cuuint32_t)es2, (cuuint32_t)es2, 1, 1};
+    cuuint32_t box[5] = {64, (cuuint32_t)(RB * estride), (cuuint32_t)(JB * estride), (cuuint32_t)BB, (cuuint32_t)KC};
+    cuuint32_t es[5] = {1, (cuuint32_t)estride, (cuuint32_t)estride, 1, 1};
     void* addr = (void*)((const char*)base + (size_t)P * C * 2);
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, addr, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -125,12 +126,12 @@ static bool make_weight_map(CUtensorMap* m, const void* base, int T, int N, int 
 }
 
 // Pixel box (RB x JB x BB = npix) minimising the number of tiles over both views.
-static void choose_box(int B, int H, int W, int npix, int* RB, int* JB, int* BB) {
+static void choose_box(int B, int H, int W, int npix, int* RB, int* JB, int* BB, int es = 1) {
     long best = -1;
     for (int rb = 1; rb <= npix; rb *= 2)
         for (int jb = 1; rb * jb <= npix; jb *= 2) {
             const int bb = npix / (rb * jb);
-            if (rb > 256 || jb > 256 || bb > 256) continue;
+            if (rb * es > 256 || jb * es > 256 || bb > 256) continue;  // TMA box extents (element stride es)
             long tiles = 0;
             for (int P = 0; P < 2; ++P) {
                 const int Wp = (W - P + 1) / 2;
@@ -148,7 +149,7 @@ static void choose_box(int B, int H, int W, int npix, int* RB, int* JB, int* BB)
 // ------------------------------------------------------------------ forward kernel
 struct TcFwdParams {
     int B, H, W, Cin, Cout, T, parity;
-    int s;  // 1, or 2: output column-parity classes e = C mod 2 read stride-2 input boxes (see tap_box)
+    int s;  // 1, 2 or 3: output column-parity classes P = C mod 2 read element-stride-s input boxes (lattice_box)
     int RB, JB, BB;
     int rt, bt, jt0, jt1;  // tiles along rows, batch, and sub-columns of view 0 / view 1
     int tiles0;            // m tiles of view 0
@@ -199,22 +200,25 @@ __device__ __forceinline__ TileCoord decode_pair_tile(const TcFwdParams& p, int 
     return tc;
 }
 
-// Input box of tap (dc, dr) for an output tile of class P at (r0, j0):
-//   s = 1: output view P = tensor columns P::2; input view (P + dc) mod 2, sub-column j0 + shift, row r0 + dr
-//   s = 2: output class P = columns C = 2C' + P (centre row 2R + P, centre column 4C' + 2P, A5:
-//          rho(C) = C mod 2); the maps traverse rows and view sub-columns with element stride 2, so the
-//          box starts at input view dc mod 2, sub-column 2 j0 + (2P + dc - Pv) / 2, row 2 r0 + P + dr.
+// Input box of tap (dc, dr) for an output tile of column class P at (r0, j0) of the stride-s lattice:
+// output column C = 2C' + P has its centre at input column sC = 2sC' + sP and row s R + rho_P, where
+// rho(C) = floor((sC + parity) / 2) mod s = floor((sP + parity) / 2) mod s depends only on P (A5).
+// Tap (dc, dr) then reads input column 2sC' + sP + dc: view Pv = (sP + dc) mod 2, sub-column
+// s C' + (sP + dc - Pv) / 2; with the maps traversing rows and view sub-columns with element stride s the
+// box starts at sub-column s j0 + (sP + dc - Pv) / 2, row s r0 + rho_P + dr.  s = 1 is the stride-1 case
+// (output view P = tensor columns P::2, rho = 0); the centre column's parity, which selects the tap table,
+// is (sP + parity) mod 2.
+__device__ __forceinline__ void lattice_box(int s, int parity, int P, int r0, int j0, int dc, int dr, int* Pv,
+                                            int* row, int* col) {
+    const int sp = s * P;
+    *Pv = (sp + dc) & 1;
+    *col = s * j0 + (sp + dc - *Pv) / 2;
+    *row = s * r0 + ((sp + parity) >> 1) % s + dr;
+}
+__device__ __forceinline__ int lattice_centre_parity(int s, int parity, int P) { return (s * P + parity) & 1; }
 __device__ __forceinline__ void tap_box(const TcFwdParams& p, int P, int r0, int j0, int dc, int dr, int* Pv,
                                         int* row, int* col) {
-    if (p.s == 1) {
-        *Pv = (P + dc) & 1;
-        *col = j0 + (P + dc - *Pv) / 2;
-        *row = r0 + dr;
-    } else {
-        *Pv = dc & 1;
-        *col = 2 * j0 + (2 * P + dc - *Pv) / 2;
-        *row = 2 * r0 + P + dr;
-    }
+    lattice_box(p.s, p.parity, P, r0, j0, dc, dr, Pv, row, col);
 }
 
 // KC = 64-channel chunks per K iteration (one TMA op each for A and B).
@@ -391,7 +395,7 @@ tc_conv_fwd_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_cons
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
                 const TileCoord tc = decode_fwd_tile(p, tile, BN);
-                const int pc = p.s == 1 ? (tc.P + p.parity) & 1 : p.parity & 1;  // centre column parity
+                const int pc = lattice_centre_parity(p.s, p.parity, tc.P);  // centre column parity
                 for (int t = 0; t < p.T; ++t) {
                     const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
                     int Pv, row, col;
@@ -521,7 +525,7 @@ tc_conv_fwd2_kernel(const __grid_constant__ CUtensorMap map_x0, const __grid_con
             uint32_t phase = 0;
             for (int tile = first; tile < p.pair_tiles; tile += step) {
                 const TileCoord tc = decode_pair_tile(p, tile, BN, rank);
-                const int pc = p.s == 1 ? (tc.P + p.parity) & 1 : p.parity & 1;  // centre column parity
+                const int pc = lattice_centre_parity(p.s, p.parity, tc.P);  // centre column parity
                 for (int t = 0; t < p.T; ++t) {
                     const int dc = p.tap_dc[pc][t], dr = p.tap_dr[pc][t];
                     int Pv, row, col;
@@ -700,11 +704,11 @@ static int pick_bn(int Cout) {
     return 0;
 }
 
-// forward only: stride 2 runs the same kernels with stride-2 input boxes (tap_box); backward passes of
-// strided layers stay on the CUDA-core kernels
+// strides 2 and 3 run the same kernels with element-stride-s input boxes (lattice_box); the strided
+// backward passes have their own kernels (lat_dgrad.cu, the lattice weight gradient below)
 bool tc_conv_fwd_supported(const Geom& g, int Cin, int Cout) {
     if (g.s == 1) return tc_conv_supported(g, Cin, Cout);
-    if (g.s != 2 || g.T > TC_MAXT || sw_on("HEXCONV_NO_TC_STRIDE2")) return false;
+    if ((g.s != 2 && g.s != 3) || g.T > TC_MAXT || sw_on("HEXCONV_NO_TC_STRIDED_FWD")) return false;
     if (Cin % TC_BK != 0 || pick_bn(Cout) == 0 || g.Wo < 2) return false;
     if (sw_on("HEXCONV_DISABLE_TC")) return false;
     return get_encode() != nullptr;
@@ -773,7 +777,7 @@ hex_status_t tc_conv_fwd(const TcConvArgs& a, cudaStream_t st) {
     p.B = g.B; p.H = g.H; p.W = g.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
     p.s = g.s;
     const int OH = g.s == 1 ? g.H : g.Ho, OW = g.s == 1 ? g.W : g.Wo;  // output grid (tiles, stores)
-    choose_box(g.B, OH, OW, TC_BM, &p.RB, &p.JB, &p.BB);
+    choose_box(g.B, OH, OW, TC_BM, &p.RB, &p.JB, &p.BB, g.s);
     p.rt = ceil_div(OH, p.RB);
     p.bt = ceil_div(g.B, p.BB);
     p.jt0 = ceil_div((OW + 1) / 2, p.JB);
@@ -856,29 +860,18 @@ struct TcWgParams {
     int dbg;         // development: 1 = skip TMA loads, 2 = skip MMAs (results invalid)
     int8_t tap_dc[2][TC_MAXT];
     int8_t tap_dr[2][TC_MAXT];
-    int s;  // 1, or 2: the pixel tiles walk the stride-2 lattice (dy) and the x maps traverse with element stride 2
+    int s;  // 1, 2 or 3: the pixel tiles walk the stride-s lattice (dy), the x maps traverse with element stride s
 };
 
-// x box of tap (dc, dr) for the pixel tile (P, r0, j0), and the centre-column parity that selects the tap table.
-//   s = 1: tile of parity view P; x view (P + dc) mod 2, sub-column j0 + shift, row r0 + dr (tap reuse as the
-//          forward).
-//   s = 2: tile of lattice view P (output columns C = 2C' + P, centres (P + 2R, 4C' + 2P): rho(C) = C mod 2,
-//          DESIGN.md A5); the x maps traverse rows and view sub-columns with element stride 2, so the box starts
-//          at x view dc mod 2, sub-column 2 j0 + (2P + dc - Pv) / 2, row 2 r0 + P + dr (the forward's tap_box).
+// x box of tap (dc, dr) for the pixel tile (P, r0, j0), and the centre-column parity that selects the tap table:
+// the forward's lattice_box.  s = 1: tile of parity view P (tap reuse as the forward); s = 2, 3: tile of lattice
+// view P of dy (output columns C = 2C' + P), x maps traversed with element stride s.
 __device__ __forceinline__ int wg_centre_parity(const TcWgParams& p, int P) {
-    return p.s == 1 ? (P + p.parity) & 1 : p.parity & 1;
+    return lattice_centre_parity(p.s, p.parity, P);
 }
 __device__ __forceinline__ void wg_xbox(const TcWgParams& p, int P, int r0, int j0, int dc, int dr, int* Pv,
                                         int* row, int* col) {
-    if (p.s == 1) {
-        *Pv = (P + dc) & 1;
-        *col = j0 + (P + dc - *Pv) / 2;
-        *row = r0 + dr;
-    } else {
-        *Pv = dc & 1;
-        *col = 2 * j0 + (2 * P + dc - *Pv) / 2;
-        *row = 2 * r0 + P + dr;
-    }
+    lattice_box(p.s, p.parity, P, r0, j0, dc, dr, Pv, row, col);
 }
 
 __device__ __forceinline__ void decode_ptile(const TcWgParams& p, int m, int* P, int* r0, int* j0, int* b0) {
@@ -1357,9 +1350,9 @@ hex_status_t tc_conv3d_wgrad(const TcWgradArgs& a, const TrDepth& dz, void* ws, 
                         st);
 }
 
-// stride 2: the one-box-per-tap weight gradient walks the dy LATTICE directly -- its pixel
-// tiles are tiles of the lattice's column-parity views and every tap's x box is read with element stride 2
-// (wg_xbox) -- instead of the stride-1 kernel on dy scattered onto the full grid (4x the MMAs, mostly zeros)
+// strides 2 and 3: the one-box-per-tap weight gradient walks the dy LATTICE directly -- its
+// pixel tiles are tiles of the lattice's column-parity views and every tap's x box is read with element stride
+// s (wg_xbox) -- instead of the stride-1 kernel on dy scattered onto the full grid (s^2 x the MMAs, mostly zeros)
 static Geom lattice_geom(const Geom& g) {
     Geom gl = g;
     gl.H = g.Ho;
@@ -1368,36 +1361,36 @@ static Geom lattice_geom(const Geom& g) {
     return gl;
 }
 
-bool tc_wgrad_s2_supported(const Geom& g, int Cin, int Cout) {
-    if (g.s != 2 || g.T > TC_MAXT || g.Wo < 2 || Cout % 128 != 0 || Cin % 64 != 0) return false;
-    if (sw_on("HEXCONV_DISABLE_TC") || sw_on("HEXCONV_NO_TC_WGRAD_S2")) return false;
+bool tc_wgrad_lat_supported(const Geom& g, int Cin, int Cout) {
+    if ((g.s != 2 && g.s != 3) || g.T > TC_MAXT || g.Wo < 2 || Cout % 128 != 0 || Cin % 64 != 0) return false;
+    if (sw_on("HEXCONV_DISABLE_TC") || sw_on("HEXCONV_NO_TC_WGRAD_LAT")) return false;
     const WgPlan w = wg_plan(lattice_geom(g), Cin, Cout);
-    if (w.RB * 2 > 256 || w.JB * 2 > 256) return false;
+    if (w.RB * g.s > 256 || w.JB * g.s > 256) return false;
     return get_encode() != nullptr;
 }
 
-size_t tc_wgrad_s2_ws_bytes(const Geom& g, int Cin, int Cout) {
+size_t tc_wgrad_lat_ws_bytes(const Geom& g, int Cin, int Cout) {
     const WgPlan w = wg_plan(lattice_geom(g), Cin, Cout);
     return (size_t)w.chunks * g.T * Cout * Cin * sizeof(float) + (size_t)w.chunks * Cout * sizeof(float) + 256;
 }
 
 hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
     const Geom& g = a.g;
-    const bool s2 = g.s == 2;
-    if (!s2 && tc_wgrad_tr_supported(g, a.Cin, a.Cout)) {  // tap-reuse kernel (tc_wgrad_tr.cu)
+    const bool lat = g.s > 1;
+    if (!lat && tc_wgrad_tr_supported(g, a.Cin, a.Cout)) {  // tap-reuse kernel (tc_wgrad_tr.cu)
         int chunks = 0;
         float* db_part = nullptr;
         const hex_status_t s = tc_wgrad_tr(a, ws, ws_bytes, &chunks, &db_part, st);
         if (s != HEX_OK) return s;
         return wgrad_reduce((const float*)ws, chunks, g.T, a.Cout, a.Cin, a.dw, db_part, a.dbias, a.accumulate, st);
     }
-    const Geom gt = s2 ? lattice_geom(g) : g;  // the grid the pixel tiles walk
+    const Geom gt = lat ? lattice_geom(g) : g;  // the grid the pixel tiles walk
     const WgPlan w = wg_plan(gt, a.Cin, a.Cout);
-    if (ws_bytes < (s2 ? tc_wgrad_s2_ws_bytes(g, a.Cin, a.Cout) : tc_wgrad_ws_bytes(g, a.Cin, a.Cout)))
+    if (ws_bytes < (lat ? tc_wgrad_lat_ws_bytes(g, a.Cin, a.Cout) : tc_wgrad_ws_bytes(g, a.Cin, a.Cout)))
         return HEX_ERR_WORKSPACE;
     TcWgParams p{};
     p.B = g.B; p.H = gt.H; p.W = gt.W; p.Cin = a.Cin; p.Cout = a.Cout; p.T = g.T; p.parity = g.parity;
-    p.s = s2 ? 2 : 1;
+    p.s = g.s;
     p.RB = w.RB; p.JB = w.JB; p.BB = w.BB; p.rt = w.rt; p.bt = w.bt; p.jt0 = w.jt0; p.jt1 = w.jt1;
     p.tiles0 = w.tiles0; p.ptiles = w.ptiles;
     p.kchunks = w.kchunks; p.cpo = w.cpo; p.n_atoms = w.n_atoms; p.groups = w.groups; p.co_tiles = w.co_tiles;
@@ -1414,7 +1407,7 @@ hex_status_t tc_conv_wgrad(const TcWgradArgs& a, void* ws, size_t ws_bytes, cuda
         }
     CUtensorMap mx0, mx1, md0, md1;
     const int xbox = w.pair ? 2 : w.cpo;
-    const int es = s2 ? 2 : 1;
+    const int es = g.s;
     if (!make_view_map5(&mx0, a.x, g.B, g.H, g.W, a.Cin, 0, w.RB, w.JB, w.BB, xbox, es)) return HEX_ERR_CUDA;
     if (!make_view_map5(&mx1, a.x, g.B, g.H, g.W, a.Cin, 1, w.RB, w.JB, w.BB, xbox, es)) return HEX_ERR_CUDA;
     if (!make_view_map5(&md0, a.dy, g.B, gt.H, gt.W, a.Cout, 0, w.RB, w.JB, w.BB, 2)) return HEX_ERR_CUDA;

@@ -371,14 +371,16 @@ def test_custom_ring_kernel_smoothing(F, oracle):
     assert ye[0, 0, 1:-1, 1:-1].abs().max().item() == 0.0
 
 
+@pytest.mark.parametrize("s", [2, 3])
 @pytest.mark.parametrize("pi", [0, 1])
-def test_conv_stride2_tensor_core_forward(F, oracle, pi):
-    # bf16 NHWC stride 2: the forward runs the tcgen05 kernel with stride-2 input
-    # boxes per output column-parity class; backward passes of strided layers use the CUDA-core kernels
+def test_conv_strided_tensor_core_forward(F, oracle, s, pi):
+    # bf16 NHWC stride 2 and 3: the forward runs the tcgen05 kernel with element-stride-s
+    # input boxes per output column-parity class (lattice_box)
     for k, (B, Cin, Cout, H, W, n) in enumerate([(2, 64, 64, 20, 23, 1), (1, 128, 256, 31, 30, 2),
-                                                  (3, 64, 128, 9, 8, 1), (1, 64, 64, 5, 6, 2)]):
-        assert F.conv_algo(B, Cin, Cout, H, W, n, 2, pi, torch.bfloat16, "NHWC", 0) == "tcgen05"
-        _conv_case(F, oracle, pi, n, 2, H, W, B, Cin, Cout, torch.bfloat16, "NHWC", 1300 + k)
+                                                  (3, 64, 128, 9, 8, 1), (1, 64, 64, 5 + 3 * (s - 2), 6, 2),
+                                                  (1, 64, 64, 26, 25, 3)]):
+        assert F.conv_algo(B, Cin, Cout, H, W, n, s, pi, torch.bfloat16, "NHWC", 0) == "tcgen05"
+        _conv_case(F, oracle, pi, n, s, H, W, B, Cin, Cout, torch.bfloat16, "NHWC", 1300 + 10 * s + k)
 
 
 @pytest.mark.parametrize("s", [2, 3])
@@ -420,24 +422,25 @@ def test_strided_bwd_data_phase_classes(F, oracle, s, pi):
             assert rel(to_np(dxm, "NHWC"), to_np(dxu, "NHWC")) <= 1e-2
 
 
+@pytest.mark.parametrize("s", [2, 3])
 @pytest.mark.parametrize("pi", [0, 1])
-def test_stride2_wgrad_on_the_lattice(F, oracle, pi):
-    # stride-2 bf16 weight gradient walking the dy lattice directly (x boxes with element stride 2; f4): against
-    # the oracle and bit-identical... within fp32 summation order of the scattered-dy route it replaces
+def test_strided_wgrad_on_the_lattice(F, oracle, s, pi):
+    # strided (s = 2, 3) bf16 weight gradient walking the dy lattice directly (x boxes with element stride s;
+    # f4): against the oracle, and within fp32 summation order of the scattered-dy route it replaces
     from paper_1903_01814_b200 import _abi as A
     import synth
     for k, (B, Cin, Cout, H, W, n) in enumerate([(2, 64, 128, 21, 22, 1), (1, 128, 256, 17, 19, 2),
-                                                  (3, 64, 128, 9, 8, 1)]):
+                                                  (3, 64, 128, 9, 8, 1), (1, 64, 128, 26, 27, 3)]):
         T = oracle.num_taps(n)
-        Ho, Wo, _ = oracle.out_shape(H, W, 2, pi)
-        x = synth.round_bf16(synth.normal((B, Cin, H, W), 1600 + k))
-        g = synth.round_bf16(synth.normal((B, Cout, Ho, Wo), 1610 + k))
+        Ho, Wo, _ = oracle.out_shape(H, W, s, pi)
+        x = synth.round_bf16(synth.normal((B, Cin, H, W), 1600 + 10 * s + k))
+        g = synth.round_bf16(synth.normal((B, Cout, Ho, Wo), 1610 + 10 * s + k))
         xd, gd = to_dev(x, torch.bfloat16, "NHWC"), to_dev(g, torch.bfloat16, "NHWC")
-        assert F.conv_algo(B, Cin, Cout, H, W, n, 2, pi, torch.bfloat16, "NHWC", 2) == "tcgen05"
-        dw, db = F.conv2d_bwd_weight(xd, gd, n=n, stride=2, parity=pi, layout="NHWC")
-        _, dwr, dbr = oracle.conv2d_bwd(x, np.zeros((Cout, Cin, T)), g, n=n, s=2, pi=pi)
-        assert rel(dw.cpu().numpy(), dwr) <= 1e-4, (pi, k)
-        assert rel(db.cpu().numpy(), dbr) <= 1e-4, (pi, k)
-        with A.switch("HEXCONV_NO_TC_WGRAD_S2"):
-            dwu, dbu = F.conv2d_bwd_weight(xd, gd, n=n, stride=2, parity=pi, layout="NHWC")
+        assert F.conv_algo(B, Cin, Cout, H, W, n, s, pi, torch.bfloat16, "NHWC", 2) == "tcgen05"
+        dw, db = F.conv2d_bwd_weight(xd, gd, n=n, stride=s, parity=pi, layout="NHWC")
+        _, dwr, dbr = oracle.conv2d_bwd(x, np.zeros((Cout, Cin, T)), g, n=n, s=s, pi=pi)
+        assert rel(dw.cpu().numpy(), dwr) <= 1e-4, (s, pi, k)
+        assert rel(db.cpu().numpy(), dbr) <= 1e-4, (s, pi, k)
+        with A.switch("HEXCONV_NO_TC_WGRAD_LAT"):
+            dwu, dbu = F.conv2d_bwd_weight(xd, gd, n=n, stride=s, parity=pi, layout="NHWC")
         assert rel(dw.cpu().numpy(), dwu.cpu().numpy().astype(np.float64)) <= 1e-5

@@ -75,22 +75,25 @@ def c3d_ops():
     return {"c3d_wgrad": lambda: F.conv3d_bwd_weight(x, g3, kd, n=n, layout="NDHWC")}
 
 
-def s2_ops():
-    # strided bf16 layer (f4): 64 images 96x96, 128 -> 128 channels, stride 2
+def s2_ops(s=2):
+    # strided bf16 layer (f4): 64 images 96x96, 128 -> 128 channels, stride s (ops "s2_*" / "s3_*")
     B, C, H, W = 64, 128, 96, 96
-    Ho, Wo, _ = F.output_shape(H, W, 2)
+    Ho, Wo, _ = F.output_shape(H, W, s)
     out = {}
     for n in (1, 2):
         T = F.num_taps(n)
         w = (torch.randn(C, C, T, device="cuda") / (C * T) ** 0.5).to(torch.bfloat16)
         g = torch.randn(B, Ho, Wo, C, device="cuda").to(torch.bfloat16)
         dx = torch.empty(B, H, W, C, device="cuda", dtype=torch.bfloat16)
-        out[f"s2_n{n}_dgrad"] = (lambda w=w, g=g, dx=dx, n=n:
-                                 F.conv2d_bwd_data(g, w, (H, W), n=n, stride=2, layout="NHWC", out=dx))
+        out[f"s{s}_n{n}_dgrad"] = (lambda w=w, g=g, dx=dx, n=n:
+                                 F.conv2d_bwd_data(g, w, (H, W), n=n, stride=s, layout="NHWC", out=dx))
         x = torch.randn(B, H, W, C, device="cuda").to(torch.bfloat16)
+        y = torch.empty(B, Ho, Wo, C, device="cuda", dtype=torch.bfloat16)
+        out[f"s{s}_n{n}_fwd"] = (lambda w=w, x=x, y=y, n=n:
+                                 F.conv2d_fwd(x, w, None, n=n, stride=s, layout="NHWC", out=y))
         dw = torch.empty(C, C, T, device="cuda")
-        out[f"s2_n{n}_wgrad"] = (lambda x=x, g=g, dw=dw, n=n:
-                                 F.conv2d_bwd_weight(x, g, n=n, stride=2, layout="NHWC", dw=dw))
+        out[f"s{s}_n{n}_wgrad"] = (lambda x=x, g=g, dw=dw, n=n:
+                                 F.conv2d_bwd_weight(x, g, n=n, stride=s, layout="NHWC", dw=dw))
     return out
 
 
@@ -114,7 +117,9 @@ def main():
     if any(a.startswith("nvls") for a in sys.argv[1:]):
         ops.update(nvls_ops())
     if any(a.startswith("s2") for a in sys.argv[1:]):
-        ops.update(s2_ops())
+        ops.update(s2_ops(2))
+    if any(a.startswith("s3") for a in sys.argv[1:]):
+        ops.update(s2_ops(3))
     if any(a.startswith("c3d") for a in sys.argv[1:]):
         ops.update(c3d_ops())
     if any(a.startswith("c5") for a in sys.argv[1:]):
