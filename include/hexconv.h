@@ -145,14 +145,16 @@ HEX_API hex_status_t hex_conv2d_workspace_size(const hex_conv2d_desc_t* desc, in
  *
  * Kernel selection (internal, channel-count driven; hex_conv2d_algo reports it):
  *  - tcgen05 tensor cores (bf16, NHWC, n <= 3, W >= 2):
- *      fwd       s = 1 or 2, Cin % 64 == 0, Cout % 64 == 0;
+ *      fwd       s = 1, 2 or 3, Cin % 64 == 0, Cout % 64 == 0 (s > 1:
+ *                element-stride-s input boxes per output column class);
  *      bwd_data  s = 1: Cin % 64 == 0, Cout % 64 == 0 (the forward kernel on dy
  *                with reversed taps / transposed channels);  s = 2, 3 with
  *                Cin % 64 == 0, Cout % 64 == 0: phase classes (only the
  *                lattice taps, TMA boxes of dy); other s > 1: the s = 1
  *                kernel on dy scattered onto the stride-1 grid (Cout % 64 == 0);
- *      bwd_weight Cin % 64 == 0, Cout % 128 == 0 (s = 2: on the lattice, x
- *                boxes with element stride 2; s = 3: via the scattered dy).
+ *      bwd_weight Cin % 64 == 0, Cout % 128 == 0 (s = 2, 3: on the lattice,
+ *                x boxes with element stride s; other s > 1: via the
+ *                scattered dy).
  *  - Cin == 1, bf16 NHWC, Cout % 64 == 0, n <= 2: warp-level mma.sync
  *    stencil kernels (s = 1) or FFMA stencils (s > 1).
  *  - fp32 NCHW, n <= 3, gathered channels >= 8 (fwd: Cin, bwd_data: Cout),
