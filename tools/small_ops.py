@@ -58,14 +58,17 @@ def c5_ops():
     x = torch.randn(B, H, W, Ci, generator=g).to(torch.bfloat16).cuda()
     w = (torch.randn(Co, Ci, 7, generator=g) / 21.0).to(torch.bfloat16).cuda()
     b = torch.zeros(Co, device="cuda")
-    y = torch.empty(B, H, W, Co, dtype=torch.bfloat16, device="cuda")
+    y = torch.randn(B, H, W, Co, generator=g).to(torch.bfloat16).cuda()
+    x2 = torch.empty_like(x)
     return {
         "c5_l2_fwd_maxpool": lambda: F.conv2d_fwd_maxpool(x, w, b, n=1),
         "c5_l2_fwd_avgpool": lambda: F.conv2d_fwd_avgpool(x, w, b, n=1),
         "c5_l2_fwd_maxpool_nobias": lambda: F.conv2d_fwd_maxpool(x, w, None, n=1),
         "c5_l2_fwd_then_avgpool": lambda: (F.conv2d_fwd(x, w, b, n=1, relu=True, layout="NHWC", out=y),
                                            F.pool2d_fwd(y, 1, 2, 0, "avg", "NHWC")),
+        "c5_l2_dgrad": lambda: F.conv2d_bwd_data(y, w, (H, W), n=1, layout="NHWC", relu_y=x, out=x2),
     }
+
 
 
 def c3d_ops():
