@@ -1,5 +1,6 @@
 // tf32_prof.cu -- development timing probe of the 3xTF32 conv kernel: builds csrc/tf32_conv.cu with
-// -DTF_PROF=1 (clock64 accumulators in CTA 0) and runs the config-3 layer-2 forward / bwd-data shapes.
+// -DTF_PROF=1 (clock64 accumulators in CTA 0) and runs the config-3 layer-2 forward / bwd-data shapes
+// (argument "c2": the config-2 stride-2 layer).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -I include \
 //        -DTF_PROF=1 -o tools/tf32_prof.bin tools/tf32_prof.cu -lcuda
 #include <cstdio>
@@ -17,9 +18,11 @@ double sw_double(const char*, double d) { return d; }
 int main(int argc, char** argv) {
     using namespace hexconv;
     const int mode = argc > 1 ? atoi(argv[1]) : 0;
-    const int B = 256, H = 40, W = 40, Cin = 16, Cout = 32, n = 2;
+    const bool c2 = argc > 2 && !strcmp(argv[2], "c2");  // config 2: 32 x 16 -> 32, 48 x 48, n = 2, stride 2
+    const int B = c2 ? 32 : 256, H = c2 ? 48 : 40, W = c2 ? 48 : 40, Cin = 16, Cout = 32, n = 2;
     Geom g{};
-    g.B = B; g.H = H; g.W = W; g.n = n; g.s = 1; g.parity = 0; g.T = hex_taps(n); g.Ho = H; g.Wo = W;
+    g.B = B; g.H = H; g.W = W; g.n = n; g.s = c2 ? 2 : 1; g.parity = 0; g.T = hex_taps(n);
+    g.Ho = c2 ? 24 : H; g.Wo = c2 ? 24 : W;
     float *x, *w, *y, *ws;
     cudaMalloc(&x, (size_t)B * 32 * H * W * 4);
     cudaMalloc(&y, (size_t)B * 32 * H * W * 4);
