@@ -60,6 +60,10 @@ def c5_ops():
     b = torch.zeros(Co, device="cuda")
     y = torch.randn(B, H, W, Co, generator=g).to(torch.bfloat16).cuda()
     x2 = torch.empty_like(x)
+    x1 = torch.randn(B, H, W, 1, generator=g).to(torch.bfloat16).cuda()  # layer 1: 1 -> 64, n = 2
+    w1 = (torch.randn(Ci, 1, 19, generator=g) / 4.4).to(torch.bfloat16).cuda()
+    b1 = torch.zeros(Ci, device="cuda")
+    dw1 = torch.empty(Ci, 1, 19, device="cuda")
     return {
         "c5_l2_fwd_maxpool": lambda: F.conv2d_fwd_maxpool(x, w, b, n=1),
         "c5_l2_fwd_avgpool": lambda: F.conv2d_fwd_avgpool(x, w, b, n=1),
@@ -67,6 +71,8 @@ def c5_ops():
         "c5_l2_fwd_then_avgpool": lambda: (F.conv2d_fwd(x, w, b, n=1, relu=True, layout="NHWC", out=y),
                                            F.pool2d_fwd(y, 1, 2, 0, "avg", "NHWC")),
         "c5_l2_dgrad": lambda: F.conv2d_bwd_data(y, w, (H, W), n=1, layout="NHWC", relu_y=x, out=x2),
+        "c5_l1_fwd": lambda: F.conv2d_fwd(x1, w1, b1, n=2, relu=True, layout="NHWC", out=x2),
+        "c5_l1_wgrad": lambda: F.conv2d_bwd_weight(x1, x, n=2, layout="NHWC", dw=dw1, dbias=b1),
     }
 
 
