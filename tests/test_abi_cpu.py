@@ -157,3 +157,23 @@ def test_bench_launches_n_ranks():
     lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
     assert sorted(d["rank"] for d in lines) == [0, 1]
     assert all(d["world"] == 2 for d in lines)
+
+
+def test_bench_reference_arm_line():
+    # the reference arm (`bench.py --impl reference`: the fp64 oracle on the host cores, a bounded sample of the
+    # config-5 step) prints one JSON line with the contract's keys
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "3"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["n_gpus"] == 1 and d["steps"] == 1 and d["warmup"] == 3
+    for k in ("metric", "value", "unit", "ms_per_step", "higher_is_better", "scaling", "vs_baseline", "dtype",
+              "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["value"] > 0 and d["unit"] == "images/s" and d["dtype"] == "f64"
+    assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert "workload" in d["config"]

@@ -180,3 +180,28 @@ def test_training_loss_stays_finite():
     losses = [float(m.step(xs[i % 2], ys[i % 2]).item()) for i in range(30)]
     assert all(np.isfinite(losses)), losses
     assert abs(np.mean(losses[-5:]) - np.log(2)) < 0.5, losses
+
+
+def test_bench_line_contract():
+    # `python bench.py` (short run, no secondary configs) prints the JSON line the driver parses, with the keys
+    # and value ranges its contract requires
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "3", "--warmup", "3",
+                          "--no-secondary", "--no-cpu-baseline", "--sustain-s", "0"],
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["unit"] == "images/s"
+    assert d["value"] > 1000 and d["ms_per_step"] > 0 and d["higher_is_better"] is True
+    assert d["scaling"] == "weak" and d["data"] == "synthetic" and "workload" in d["config"]
+    r = d["roofline"]
+    assert r["bound"] == "tensor" and r["unit"] == "TFLOP/s" and 0 < r["frac"] <= 1.2
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-6
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    assert d["clocks"]["sm_mhz"] > 0 and "reasons" in d["clocks"]
