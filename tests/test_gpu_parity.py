@@ -378,7 +378,7 @@ def test_conv_strided_tensor_core_forward(F, oracle, s, pi):
     # input boxes per output column-parity class (lattice_box)
     for k, (B, Cin, Cout, H, W, n) in enumerate([(2, 64, 64, 20, 23, 1), (1, 128, 256, 31, 30, 2),
                                                   (3, 64, 128, 9, 8, 1), (1, 64, 64, 5 + 3 * (s - 2), 6, 2),
-                                                  (1, 64, 64, 26, 25, 3)]):
+                                                  (1, 64, 64, 26, 25, 3), (2, 64, 64, 3, 4, 1), (1, 128, 64, 4, 5, 2)]):
         assert F.conv_algo(B, Cin, Cout, H, W, n, s, pi, torch.bfloat16, "NHWC", 0) == "tcgen05"
         _conv_case(F, oracle, pi, n, s, H, W, B, Cin, Cout, torch.bfloat16, "NHWC", 1300 + 10 * s + k)
 
@@ -430,7 +430,8 @@ def test_strided_wgrad_on_the_lattice(F, oracle, s, pi):
     from paper_1903_01814_b200 import _abi as A
     import synth
     for k, (B, Cin, Cout, H, W, n) in enumerate([(2, 64, 128, 21, 22, 1), (1, 128, 256, 17, 19, 2),
-                                                  (3, 64, 128, 9, 8, 1), (1, 64, 128, 26, 27, 3)]):
+                                                  (3, 64, 128, 9, 8, 1), (1, 64, 128, 26, 27, 3),
+                                                  (2, 64, 128, 3, 4, 1), (1, 128, 128, 4, 5, 2)]):
         T = oracle.num_taps(n)
         Ho, Wo, _ = oracle.out_shape(H, W, s, pi)
         x = synth.round_bf16(synth.normal((B, Cin, H, W), 1600 + 10 * s + k))
