@@ -383,6 +383,11 @@ HEX_API hex_status_t hex_cast_f32_bf16(int64_t count, const float* src, void* ds
  * different slots.  Graph-capturable (its epoch counters live in device
  * memory).  A rank that does not arrive within 10 s makes the others trap (a
  * launch failure at their next synchronisation) instead of hanging.
+ * hex_nvls_open_local(device, data_bytes, out): a single-rank region in plain
+ * device memory (no multicast object; then hex_nvls_map as above): the same
+ * kernel protocol with ordinary loads / stores / atomics in place of the
+ * multimem ones -- the gradient "sum" of one rank, for single-GPU use and for
+ * exercising the protocol on GPUs without multicast support.
  * hex_nvls_supported: *supported = 1 if `device` exists, reports multicast
  * support and a one-device multicast object can actually be created (a GPU
  * leased without its NVSwitch fabric reports the attribute but cannot).  hex_nvls_close: synchronises the device, unmaps, frees.
@@ -397,6 +402,7 @@ typedef struct hex_nvls hex_nvls_t;
 HEX_API hex_status_t hex_nvls_supported(int32_t device, int32_t* supported);
 HEX_API hex_status_t hex_nvls_open(int32_t world, int32_t rank, int32_t device, size_t data_bytes,
                                    int32_t fd_in, int32_t* fd_out, hex_nvls_t** out);
+HEX_API hex_status_t hex_nvls_open_local(int32_t device, size_t data_bytes, hex_nvls_t** out);
 HEX_API hex_status_t hex_nvls_map(hex_nvls_t* h, void** uc, void** mc, size_t* map_bytes);
 HEX_API hex_status_t hex_nvls_allreduce_f32(hex_nvls_t* h, int64_t offset, int64_t count, int32_t slot,
                                             hex_stream_t stream);

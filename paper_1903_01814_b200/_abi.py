@@ -105,6 +105,7 @@ _SIGS = {
     "hex_relu_bwd": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp]),
     "hex_nvls_supported": (_i32, [_i32, _i32p]),
     "hex_nvls_open": (_i32, [_i32, _i32, _i32, _sz, _i32, _i32p, ctypes.POINTER(_vp)]),
+    "hex_nvls_open_local": (_i32, [_i32, _sz, ctypes.POINTER(_vp)]),
     "hex_nvls_map": (_i32, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _szp]),
     "hex_nvls_allreduce_f32": (_i32, [_vp, _i64, _i64, _i32, _vp]),
     "hex_nvls_close": (_i32, [_vp]),

@@ -58,10 +58,53 @@ __device__ __forceinline__ unsigned long long nv_now() {
     return t;
 }
 
-// release this CTA's prior writes at system scope, then add 1 to the counter in every replica
+// release this CTA's prior writes at system scope, then add 1 to the counter in every replica (MC) -- or, in
+// the single-rank local mode (a region without a multicast object), to the one local counter
+template <bool MC>
 __device__ __forceinline__ void nv_arrive(uint32_t* mc_counter) {
     asm volatile("fence.acq_rel.sys;" ::: "memory");
-    asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(mc_counter), "r"(1u) : "memory");
+    if constexpr (MC)
+        asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(mc_counter), "r"(1u) : "memory");
+    else
+        asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(mc_counter), "r"(1u) : "memory");
+}
+// the sum over the replicas of 4 / 1 values (MC: in the switch; local mode: the one replica) and its
+// broadcast back to every replica
+template <bool MC>
+__device__ __forceinline__ float4 nv_ld_reduce4(const float* p) {
+    float4 v;
+    if constexpr (MC)
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.sys.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+    return v;
+}
+template <bool MC>
+__device__ __forceinline__ void nv_st4(float* p, float4 v) {
+    if constexpr (MC)
+        asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};"
+                     :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+    else
+        asm volatile("st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};"
+                     :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+template <bool MC>
+__device__ __forceinline__ float nv_ld_reduce1(const float* p) {
+    float v;
+    if constexpr (MC)
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+template <bool MC>
+__device__ __forceinline__ void nv_st1(float* p, float v) {
+    if constexpr (MC)
+        asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+    else
+        asm volatile("st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
 __device__ __forceinline__ void nv_wait(const uint32_t* uc_counter, uint32_t target) {
@@ -82,6 +125,7 @@ __device__ __forceinline__ void nv_wait(const uint32_t* uc_counter, uint32_t tar
 // Sum of one bucket across the ranks; see the file comment.  uc / mc: the bucket's first element in the
 // local and the multicast view; sig_uc / sig_mc: this slot's counters [2][HEX_NVLS_MAX_CTAS] in the two
 // views; epoch: this slot's [HEX_NVLS_MAX_CTAS] local epoch words.
+template <bool MC>
 __global__ void __launch_bounds__(NV_THREADS) nvls_allreduce_f32_kernel(float* __restrict__ mc, int64_t count,
                                                                         uint32_t* sig_uc, uint32_t* sig_mc,
                                                                         uint32_t* epoch, int world, int rank) {
@@ -91,7 +135,7 @@ __global__ void __launch_bounds__(NV_THREADS) nvls_allreduce_f32_kernel(float* _
         const uint32_t e = epoch[c] + 1;
         epoch[c] = e;
         s_epoch = e;
-        nv_arrive(sig_mc + c);
+        nv_arrive<MC>(sig_mc + c);
         nv_wait(sig_uc + c, e * (uint32_t)world);
     }
     __syncthreads();
@@ -101,23 +145,14 @@ __global__ void __launch_bounds__(NV_THREADS) nvls_allreduce_f32_kernel(float* _
     for (int64_t q = qb + threadIdx.x; q < qe; q += blockDim.x) {
         float* p = mc + 4 * q;
         if (4 * q + 4 <= count) {
-            float4 v;
-            asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
-                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
-            asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};"
-                         :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+            nv_st4<MC>(p, nv_ld_reduce4<MC>(p));
         } else {
-            for (int64_t i = 4 * q; i < count; ++i) {
-                float v;
-                asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];"
-                             : "=f"(v) : "l"(mc + i) : "memory");
-                asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc + i), "f"(v) : "memory");
-            }
+            for (int64_t i = 4 * q; i < count; ++i) nv_st1<MC>(mc + i, nv_ld_reduce1<MC>(mc + i));
         }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        nv_arrive(sig_mc + HEX_NVLS_MAX_CTAS + c);
+        nv_arrive<MC>(sig_mc + HEX_NVLS_MAX_CTAS + c);
         nv_wait(sig_uc + HEX_NVLS_MAX_CTAS + c, s_epoch * (uint32_t)world);
     }
 }
@@ -130,6 +165,8 @@ struct hex_nvls {
     size_t map_bytes = 0;    // data + counters, rounded to the multicast granularity
     CUmemGenericAllocationHandle mc = 0, mem = 0;
     bool have_mc = false, have_mem = false, added = false, bound = false;
+    bool local = false;          // single-rank region in plain device memory (hex_nvls_open_local)
+    void* local_mem = nullptr;
     CUdeviceptr uc_va = 0, mc_va = 0;
     bool uc_mapped = false, mc_mapped = false;
     uint32_t* epochs = nullptr;  // local device memory [HEX_NVLS_SLOTS][HEX_NVLS_MAX_CTAS]
@@ -218,6 +255,7 @@ size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 void nv_release(hex_nvls* h) {
     if (h->epochs) cudaFree(h->epochs);
+    if (h->local_mem) cudaFree(h->local_mem);
     if (h->mc_mapped) drv().cuMemUnmap(h->mc_va, h->map_bytes);
     if (h->mc_va) drv().cuMemAddressFree(h->mc_va, h->map_bytes);
     if (h->uc_mapped) drv().cuMemUnmap(h->uc_va, h->map_bytes);
@@ -316,32 +354,56 @@ hex_status_t hex_nvls_open(int32_t world, int32_t rank, int32_t device, size_t d
     return HEX_OK;
 }
 
+hex_status_t hex_nvls_open_local(int32_t device, size_t data_bytes, hex_nvls_t** out) {
+    if (!out || data_bytes == 0) return HEX_ERR_INVALID_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return HEX_ERR_INVALID_ARG;
+    if (cudaSetDevice(device) != cudaSuccess) return HEX_ERR_CUDA;
+    hex_nvls* h = new (std::nothrow) hex_nvls;
+    if (!h) return HEX_ERR_CUDA;
+    h->world = 1;
+    h->rank = 0;
+    h->device = device;
+    h->local = true;
+    h->data_bytes = round_up(data_bytes, 256);
+    h->map_bytes = h->data_bytes + NV_SIG_BYTES;
+    *out = h;
+    return HEX_OK;
+}
+
 hex_status_t hex_nvls_map(hex_nvls_t* h, void** uc, void** mc, size_t* map_bytes) {
     if (!h || !uc || !mc) return HEX_ERR_INVALID_ARG;
     if (h->bound) return HEX_ERR_INVALID_ARG;
     if (cudaSetDevice(h->device) != cudaSuccess) return HEX_ERR_CUDA;
-    CUmemAllocationProp mp;
-    memset(&mp, 0, sizeof(mp));
-    mp.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-    mp.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    mp.location.id = h->device;
-    NV_TRY(drv().cuMemCreate(&h->mem, h->map_bytes, &mp, 0));
-    h->have_mem = true;
-    NV_TRY(drv().cuMulticastBindMem(h->mc, 0, h->mem, 0, h->map_bytes, 0));
-    h->bound = true;
-    CUmemAccessDesc ad;
-    memset(&ad, 0, sizeof(ad));
-    ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    ad.location.id = h->device;
-    ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    NV_TRY(drv().cuMemAddressReserve(&h->uc_va, h->map_bytes, 0, 0, 0));
-    NV_TRY(drv().cuMemMap(h->uc_va, h->map_bytes, 0, h->mem, 0));
-    h->uc_mapped = true;
-    NV_TRY(drv().cuMemSetAccess(h->uc_va, h->map_bytes, &ad, 1));
-    NV_TRY(drv().cuMemAddressReserve(&h->mc_va, h->map_bytes, 0, 0, 0));
-    NV_TRY(drv().cuMemMap(h->mc_va, h->map_bytes, 0, h->mc, 0));
-    h->mc_mapped = true;
-    NV_TRY(drv().cuMemSetAccess(h->mc_va, h->map_bytes, &ad, 1));
+    if (h->local) {  // one replica in plain device memory: both views are the same pointer
+        if (cudaMalloc(&h->local_mem, h->map_bytes) != cudaSuccess) return HEX_ERR_CUDA;
+        h->uc_va = h->mc_va = (CUdeviceptr)h->local_mem;
+        h->bound = true;
+    } else {
+        CUmemAllocationProp mp;
+        memset(&mp, 0, sizeof(mp));
+        mp.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        mp.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        mp.location.id = h->device;
+        NV_TRY(drv().cuMemCreate(&h->mem, h->map_bytes, &mp, 0));
+        h->have_mem = true;
+        NV_TRY(drv().cuMulticastBindMem(h->mc, 0, h->mem, 0, h->map_bytes, 0));
+        h->bound = true;
+        CUmemAccessDesc ad;
+        memset(&ad, 0, sizeof(ad));
+        ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        ad.location.id = h->device;
+        ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        NV_TRY(drv().cuMemAddressReserve(&h->uc_va, h->map_bytes, 0, 0, 0));
+        NV_TRY(drv().cuMemMap(h->uc_va, h->map_bytes, 0, h->mem, 0));
+        h->uc_mapped = true;
+        NV_TRY(drv().cuMemSetAccess(h->uc_va, h->map_bytes, &ad, 1));
+        NV_TRY(drv().cuMemAddressReserve(&h->mc_va, h->map_bytes, 0, 0, 0));
+        NV_TRY(drv().cuMemMap(h->mc_va, h->map_bytes, 0, h->mc, 0));
+        h->mc_mapped = true;
+        NV_TRY(drv().cuMemSetAccess(h->mc_va, h->map_bytes, &ad, 1));
+    }
     // counters and epochs start at 0 on every rank (the caller's barrier after map orders this before any
     // other rank's first arrival)
     if (cudaMemset((void*)h->uc_va, 0, h->map_bytes) != cudaSuccess) return HEX_ERR_CUDA;
@@ -367,9 +429,10 @@ hex_status_t hex_nvls_allreduce_f32(hex_nvls_t* h, int64_t offset, int64_t count
     const int grid = nv_grid((count + 3) / 4);
     uint32_t* sig_uc = (uint32_t*)(h->uc_va + h->data_bytes) + (size_t)slot * 2 * HEX_NVLS_MAX_CTAS;
     uint32_t* sig_mc = (uint32_t*)(h->mc_va + h->data_bytes) + (size_t)slot * 2 * HEX_NVLS_MAX_CTAS;
-    nvls_allreduce_f32_kernel<<<grid, NV_THREADS, 0, (cudaStream_t)stream>>>(
-        (float*)h->mc_va + offset, count, sig_uc, sig_mc, h->epochs + (size_t)slot * HEX_NVLS_MAX_CTAS, h->world,
-        h->rank);
+    auto kern = h->local ? nvls_allreduce_f32_kernel<false> : nvls_allreduce_f32_kernel<true>;
+    kern<<<grid, NV_THREADS, 0, (cudaStream_t)stream>>>((float*)h->mc_va + offset, count, sig_uc, sig_mc,
+                                                        h->epochs + (size_t)slot * HEX_NVLS_MAX_CTAS, h->world,
+                                                        h->rank);
     hexconv::count_launch();
     return hexconv::last_launch_status();
 }

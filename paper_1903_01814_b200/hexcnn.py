@@ -136,8 +136,11 @@ class HexCNN:
         self.params_bf16 = self.params.to(torch.bfloat16)
         self.grads = torch.zeros_like(self.params)
         if self.nvls and self.reduce_grads:
-            from .nvls import NvlsBuffer
-            self._nv = NvlsBuffer(4 * self.nparams, self.pg, self.dev)
+            from . import nvls as nv
+            # one rank on a GPU that cannot create multicast objects: the same kernel on plain memory
+            local = self.world == 1 and not nv.supported(self.dev)
+            self._nv = nv.NvlsBuffer(4 * self.nparams, self.pg, self.dev, local=local)
+            self._nv_side = torch.cuda.Stream(device=self.dev)  # the bucket sums overlap the backward
             g = self._nv.tensor(self.nparams)
             g.zero_()
             self.grads = g
@@ -325,8 +328,14 @@ class HexCNN:
         return self.grads[off:off + n]
 
     def _nvls_reduce(self, l):
+        # layer l's bucket is summed on a side stream as soon as its weight gradient is written (an event on
+        # the current stream), so the sum overlaps the backward of the earlier layers
         off, n = self._segment_range(l)
-        self._nv.allreduce(off, n, slot=l)  # on the current stream, after layer l's weight gradient
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._nv_side.wait_event(ev)
+        with torch.cuda.stream(self._nv_side):
+            self._nv.allreduce(off, n, slot=l)
 
     def step(self, x, labels):
         """One SGD step on the batch (x: bf16 [B,H,W,1] NHWC, labels: int32 [B]).
@@ -335,6 +344,7 @@ class HexCNN:
         self.forward(x, stream)
         if self.reduce_grads and self._nv is not None:
             self.backward(x, labels, stream, self._nvls_reduce)
+            torch.cuda.current_stream().wait_stream(self._nv_side)  # SGD reads the summed gradients
         elif self.reduce_grads:
             red = GradBucketReducer(self.pg)
             self.backward(x, labels, stream, lambda l: red.launch(self._segment(l)))

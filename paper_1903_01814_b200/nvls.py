@@ -20,6 +20,11 @@ import torch.distributed as dist
 from . import _abi as A
 
 
+def _cuda_device(device):
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    return torch.device("cuda", dev.index if dev.index is not None else torch.cuda.current_device())
+
+
 def _dist_on(group):
     return dist.is_available() and dist.is_initialized()
 
@@ -83,17 +88,24 @@ class _CudaArray:
 
 
 class NvlsBuffer:
-    """fp32 region of `nbytes` bound to a multicast object over the ranks of `group` (collective setup)."""
+    """fp32 region of `nbytes` bound to a multicast object over the ranks of `group` (collective setup).
+    local=True (one rank only): plain device memory, the same kernel protocol with ordinary memory operations
+    (hex_nvls_open_local) -- for one GPU, and for GPUs that cannot create multicast objects."""
 
-    def __init__(self, nbytes: int, group=None, device=None):
+    def __init__(self, nbytes: int, group=None, device=None, local: bool = False):
         self.group = group
         self.world, self.rank = world_rank(group)
-        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        dev = _cuda_device(device)
         self.device = dev
+        self.local = bool(local)
         L = A.lib()
         h = ctypes.c_void_p()
         fd_out = ctypes.c_int32(-1)
-        if self.rank == 0:
+        if self.local:
+            if self.world != 1:
+                raise ValueError("NvlsBuffer(local=True) is single-rank")
+            A.check(L.hex_nvls_open_local(dev.index, nbytes, ctypes.byref(h)), "hex_nvls_open_local")
+        elif self.rank == 0:
             A.check(L.hex_nvls_open(self.world, 0, dev.index, nbytes, -1, ctypes.byref(fd_out), ctypes.byref(h)),
                     "hex_nvls_open")
             fd = share_fd(fd_out.value, group)
@@ -132,7 +144,7 @@ class NvlsBuffer:
 
 
 def supported(device=None) -> bool:
-    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    dev = _cuda_device(device)
     s = ctypes.c_int32(0)
     A.check(A.lib().hex_nvls_supported(dev.index, ctypes.byref(s)), "hex_nvls_supported")
     return bool(s.value)

@@ -1,14 +1,15 @@
 """NVLS gradient sum (include/hexconv.h "NVLS gradient sum", csrc/nvls.cu) on one GPU.
 
-The run has one GPU, so the multicast object spans one device: the switch's sum over the replicas is the
-identity and every counter wait completes on this rank's own arrival.  That still executes the whole
-device protocol -- multicast object, bind and both mappings, the multimem.red arrivals, the acquire waits
-with device-resident epochs, multimem.ld_reduce / multimem.st over the rank's slice in vector and scalar
-(ragged tail) form -- so these tests pin: the bucket comes back bitwise unchanged (sum over one rank),
-elements outside the bucket are untouched, repeated and graph-replayed calls keep their epochs in step, and
-a HexCNN step whose gradients go through the NVLS path gives bit-identical parameters to the plain step.
-The sum over several ranks is the hardware's multimem.ld_reduce; the partition that makes each element
-summed exactly once is pinned on CPU (tests/test_nvls_host.py)."""
+The run has one GPU.  Where it can create a multicast object, the object spans that one device; where it
+cannot (this pool's lease, profiles/r02/nvls_probe.txt), the region is the single-rank local mode
+(hex_nvls_open_local: plain device memory, ordinary loads / stores / red in place of the multimem ones).
+Either way the sum over the replicas is the identity and every counter wait completes on this rank's own
+arrival, and the kernel's whole control path runs: the arrivals, the acquire waits with device-resident
+epochs, the per-CTA partition and the vector / scalar (ragged tail) element loop.  Pinned: the bucket comes
+back bitwise unchanged, elements outside the bucket are untouched, repeated and graph-replayed calls keep
+their epochs in step, and a HexCNN step whose gradients go through the NVLS path gives bit-identical
+parameters to the plain step.  The sum over several ranks is the hardware's multimem.ld_reduce; the
+partition that makes each element summed exactly once is pinned on CPU (tests/test_nvls_host.py)."""
 import ctypes
 
 import numpy as np
@@ -18,12 +19,12 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def nv():
+@pytest.fixture(scope="module", params=["multicast", "local"])
+def nv(request):
     from paper_1903_01814_b200 import nvls
-    if not nvls.supported():
+    if request.param == "multicast" and not nvls.supported():
         pytest.skip("device without usable multicast objects (profiles/r02/nvls_probe.txt)")
-    buf = nvls.NvlsBuffer(4 * 3_000_000)
+    buf = nvls.NvlsBuffer(4 * 3_000_000, local=request.param == "local")
     yield buf
     buf.close()
 
@@ -71,9 +72,7 @@ def test_nvls_rejects_bad_buckets(nv):
 
 
 def test_hexcnn_step_through_nvls_is_bit_identical():
-    from paper_1903_01814_b200 import nvls
-    if not nvls.supported():
-        pytest.skip("device without usable multicast objects (profiles/r02/nvls_probe.txt)")
+    # one rank: the multicast region where the GPU can create one, else the local mode (HexCNN picks)
     import synth
     from paper_1903_01814_b200.hexcnn import HexCNN
     B = 8

@@ -111,7 +111,7 @@ def nvls_ops():
     from paper_1903_01814_b200 import nvls
     from paper_1903_01814_b200.hexcnn import HexCNN
     m = HexCNN(batch=2)
-    buf = nvls.NvlsBuffer(4 * m.nparams)
+    buf = nvls.NvlsBuffer(4 * m.nparams, local=not nvls.supported())
     nvls_ops.keep = buf
     segs = [m._segment_range(l) for l in range(m.L + 1)]
 
