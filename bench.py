@@ -54,14 +54,24 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        """Start nvidia-smi sampling every 100 ms and wait (<= 3 s) for its first sample, so that sampling is
+        live when the timed region begins (nvidia-smi takes a few hundred ms to start)."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.first = len(self.lines)
+
+    def mark(self):
+        """Samples from here on belong to the measured region."""
+        self.first = len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -70,6 +80,7 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return None
+        end = len(self.lines)  # samples taken while the measured region ran
         time.sleep(0.15)
         self.proc.terminate()
         try:
@@ -78,7 +89,11 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # the samples taken during the region; a region shorter than the 100 ms sampling period may hold
+        # none: then the first one after it (<= 150 ms later), else the last one before it
+        lines = (self.lines[self.first:end] or self.lines[end:end + 1] or
+                 self.lines[max(0, self.first - 1):self.first])
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -617,6 +632,7 @@ def main():
     clocks.start()
     barrier()
     torch.cuda.synchronize()
+    clocks.mark()
     l0 = _abi.launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_start.record()
@@ -645,6 +661,7 @@ def main():
         sclk.start()
         barrier()
         torch.cuda.synchronize()
+        sclk.mark()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record()
         for i in range(n_s):
