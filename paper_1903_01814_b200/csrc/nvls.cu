@@ -211,6 +211,15 @@ const Drv& drv() {
 
 constexpr size_t NV_SIG_BYTES = (size_t)HEX_NVLS_SLOTS * 2 * HEX_NVLS_MAX_CTAS * sizeof(uint32_t);
 
+// The setup calls work on `device` and leave the caller's current device as it was.
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() { cudaGetDevice(&prev); }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 hex_status_t nv_cu(CUresult r, const char* what) {
     if (r == CUDA_SUCCESS) return HEX_OK;
     const char* s = nullptr;
@@ -287,6 +296,7 @@ hex_status_t hex_nvls_plan(int64_t count, int32_t world, int32_t rank, int32_t c
 }
 
 hex_status_t hex_nvls_supported(int32_t device, int32_t* supported) {
+    DeviceGuard guard;
     if (!supported) return HEX_ERR_INVALID_ARG;
     *supported = 0;
     int n = 0;
@@ -297,6 +307,7 @@ hex_status_t hex_nvls_supported(int32_t device, int32_t* supported) {
 
 hex_status_t hex_nvls_open(int32_t world, int32_t rank, int32_t device, size_t data_bytes, int32_t fd_in,
                            int32_t* fd_out, hex_nvls_t** out) {
+    DeviceGuard guard;
     if (!out || world < 1 || rank < 0 || rank >= world || data_bytes == 0) return HEX_ERR_INVALID_ARG;
     if (rank == 0 && world > 1 && !fd_out) return HEX_ERR_INVALID_ARG;
     if (rank > 0 && fd_in < 0) return HEX_ERR_INVALID_ARG;
@@ -355,6 +366,7 @@ hex_status_t hex_nvls_open(int32_t world, int32_t rank, int32_t device, size_t d
 }
 
 hex_status_t hex_nvls_open_local(int32_t device, size_t data_bytes, hex_nvls_t** out) {
+    DeviceGuard guard;
     if (!out || data_bytes == 0) return HEX_ERR_INVALID_ARG;
     *out = nullptr;
     int n = 0;
@@ -373,6 +385,7 @@ hex_status_t hex_nvls_open_local(int32_t device, size_t data_bytes, hex_nvls_t**
 }
 
 hex_status_t hex_nvls_map(hex_nvls_t* h, void** uc, void** mc, size_t* map_bytes) {
+    DeviceGuard guard;
     if (!h || !uc || !mc) return HEX_ERR_INVALID_ARG;
     if (h->bound) return HEX_ERR_INVALID_ARG;
     if (cudaSetDevice(h->device) != cudaSuccess) return HEX_ERR_CUDA;
@@ -438,6 +451,7 @@ hex_status_t hex_nvls_allreduce_f32(hex_nvls_t* h, int64_t offset, int64_t count
 }
 
 hex_status_t hex_nvls_close(hex_nvls_t* h) {
+    DeviceGuard guard;
     if (!h) return HEX_ERR_INVALID_ARG;
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
