@@ -1304,9 +1304,12 @@ static WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
     w.pair = wg_use_pair(Cin, Cout);
     w.co_tiles = w.pair ? Cout / 256 : Cout / 128;
     const int base_units = w.co_tiles * w.groups;
-    // whole waves: the largest chunk count with base_units * chunks <= 2 x 148 SMs (one CTA per SM,
-    // a pair unit takes two).  A fixed SM count keeps the split-K summation order identical on every B200.
-    int chunks = (w.pair ? 148 : 2 * 148) / base_units;
+    // whole waves: the largest chunk count with base_units * chunks <= 2 x 148 SMs (one CTA per SM, a pair
+    // unit takes two) -- one wave of pair units for n = 1, whose 7-tap units are short enough that a second
+    // wave's extra partials cost more than its balance gains (C5 layer 6: 128 vs 139 us; n = 2 keeps two
+    // waves: layer 5 270 vs 274 us).  A fixed SM count keeps the split-K summation order identical on every
+    // B200.
+    int chunks = (w.pair ? (g.n == 1 ? 74 : 148) : 2 * 148) / base_units;
     if (chunks > w.ptiles) chunks = w.ptiles;
     if (chunks < 1) chunks = 1;
     w.tiles_per_chunk = ceil_div(w.ptiles, chunks);

@@ -77,6 +77,21 @@ def c5_ops():
 
 
 
+def c5_wgrad_ops():
+    # config-5 CTA-pair weight gradients: layer 4 (128 -> 256, n = 1, 48 x 48), 5 (256 -> 256, n = 2, 24 x 24),
+    # 6 (256 -> 256, n = 1, 24 x 24)
+    out = {}
+    for name, (ci, co, hw, n) in {"c5_l4_wgrad": (128, 256, 48, 1), "c5_l5_wgrad": (256, 256, 24, 2),
+                                  "c5_l6_wgrad": (256, 256, 24, 1)}.items():
+        x = torch.randn(256, hw, hw, ci, device="cuda").to(torch.bfloat16)
+        g = torch.randn(256, hw, hw, co, device="cuda").to(torch.bfloat16)
+        dw = torch.empty(co, ci, F.num_taps(n), device="cuda")
+        db = torch.empty(co, device="cuda")
+        out[name] = (lambda x=x, g=g, dw=dw, db=db, n=n:
+                     F.conv2d_bwd_weight(x, g, n=n, layout="NHWC", dw=dw, dbias=db))
+    return out
+
+
 def c3d_ops():
     B, D, H, W, C, Co, kd, n = 16, 16, 64, 64, 64, 128, 3, 1
     x = torch.randn(B, D, H, W, C, device="cuda").to(torch.bfloat16)
@@ -133,6 +148,7 @@ def main():
         ops.update(c3d_ops())
     if any(a.startswith("c5") for a in sys.argv[1:]):
         ops.update(c5_ops())
+        ops.update(c5_wgrad_ops())
     sel = sys.argv[1:] or list(ops)
     gt = GraphTimer("cuda")
     for name in sel:
