@@ -210,6 +210,12 @@ __device__ __forceinline__ TileCoord decode_pair_tile(const TcFwdParams& p, int 
 // is (sP + parity) mod 2.
 __device__ __forceinline__ void lattice_box(int s, int parity, int P, int r0, int j0, int dc, int dr, int* Pv,
                                             int* row, int* col) {
+    if (s == 1) {  // the stride-1 kernels' hot path: no integer division
+        *Pv = (P + dc) & 1;
+        *col = j0 + (P + dc - *Pv) / 2;
+        *row = r0 + dr;
+        return;
+    }
     const int sp = s * P;
     *Pv = (sp + dc) & 1;
     *col = s * j0 + (sp + dc - *Pv) / 2;
@@ -1306,8 +1312,8 @@ static WgPlan wg_plan(const Geom& g, int Cin, int Cout) {
     const int base_units = w.co_tiles * w.groups;
     // whole waves: the largest chunk count with base_units * chunks <= 2 x 148 SMs (one CTA per SM, a pair
     // unit takes two) -- one wave of pair units for n = 1, whose 7-tap units are short enough that a second
-    // wave's extra partials cost more than its balance gains (C5 layer 6: 128 vs 139 us; n = 2 keeps two
-    // waves: layer 5 270 vs 274 us).  A fixed SM count keeps the split-K summation order identical on every
+    // wave's extra partials cost more than its balance gains (C5 layer 6: 124 vs 132 us, A/B in fresh
+    // processes on one box; n = 2 keeps two waves: layer 5 270 vs 274 us).  A fixed SM count keeps the split-K summation order identical on every
     // B200.
     int chunks = (w.pair ? (g.n == 1 ? 74 : 148) : 2 * 148) / base_units;
     if (chunks > w.ptiles) chunks = w.ptiles;

@@ -89,6 +89,10 @@ def c5_wgrad_ops():
         db = torch.empty(co, device="cuda")
         out[name] = (lambda x=x, g=g, dw=dw, db=db, n=n:
                      F.conv2d_bwd_weight(x, g, n=n, layout="NHWC", dw=dw, dbias=db))
+        w = (torch.randn(co, ci, F.num_taps(n), device="cuda") / 40).to(torch.bfloat16)
+        y = torch.empty(256, hw, hw, co, device="cuda", dtype=torch.bfloat16)
+        out[name.replace("wgrad", "fwd")] = (lambda x=x, w=w, y=y, n=n:
+                                             F.conv2d_fwd(x, w, None, n=n, layout="NHWC", out=y))
     return out
 
 
