@@ -81,7 +81,8 @@ def c5_wgrad_ops():
     # config-5 CTA-pair weight gradients: layer 4 (128 -> 256, n = 1, 48 x 48), 5 (256 -> 256, n = 2, 24 x 24),
     # 6 (256 -> 256, n = 1, 24 x 24)
     out = {}
-    for name, (ci, co, hw, n) in {"c5_l4_wgrad": (128, 256, 48, 1), "c5_l5_wgrad": (256, 256, 24, 2),
+    for name, (ci, co, hw, n) in {"c5_l2_wgrad": (64, 128, 96, 1), "c5_l3_wgrad": (128, 128, 48, 2),
+                                  "c5_l4_wgrad": (128, 256, 48, 1), "c5_l5_wgrad": (256, 256, 24, 2),
                                   "c5_l6_wgrad": (256, 256, 24, 1)}.items():
         x = torch.randn(256, hw, hw, ci, device="cuda").to(torch.bfloat16)
         g = torch.randn(256, hw, hw, co, device="cuda").to(torch.bfloat16)
