@@ -52,6 +52,21 @@ def c3_ops():
     }
 
 
+def c2_ops():
+    # config 2: 32 x 16 -> 32, 48 x 48, n = 2, stride 2 (fp32 NCHW)
+    B, H, W = 32, 48, 48
+    Ho, Wo, _ = F.output_shape(H, W, 2)
+    x = torch.randn(B, 16, H, W, device="cuda")
+    w = torch.randn(32, 16, 19, device="cuda") * 0.06
+    g = torch.randn(B, 32, Ho, Wo, device="cuda")
+    y = torch.empty(B, 32, Ho, Wo, device="cuda")
+    dx = torch.empty(B, 16, H, W, device="cuda")
+    dw = torch.empty(32, 16, 19, device="cuda")
+    return {"c2_fwd": lambda: F.conv2d_fwd(x, w, None, n=2, stride=2, out=y),
+            "c2_dgrad": lambda: F.conv2d_bwd_data(g, w, (H, W), n=2, stride=2, out=dx),
+            "c2_wgrad": lambda: F.conv2d_bwd_weight(x, g, n=2, stride=2, dw=dw)}
+
+
 def c5_ops():
     B, H, W, Ci, Co = 256, 96, 96, 64, 128
     g = torch.Generator().manual_seed(0)
@@ -143,6 +158,8 @@ def nvls_ops():
 
 def main():
     ops = c3_ops()
+    if any(a.startswith("c2") for a in sys.argv[1:]):
+        ops.update(c2_ops())
     if any(a.startswith("nvls") for a in sys.argv[1:]):
         ops.update(nvls_ops())
     if any(a.startswith("s2") for a in sys.argv[1:]):
