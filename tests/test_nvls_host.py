@@ -53,6 +53,10 @@ def test_setup_argument_checks_without_gpu():
     assert L.hex_nvls_open(2, 0, 0, 1024, -1, None, ctypes.byref(h)) == 1                  # no fd_out on rank 0
     assert L.hex_nvls_open(2, 1, 0, 1024, -1, None, ctypes.byref(h)) == 1                  # no fd_in on rank 1
     assert L.hex_nvls_open(1, 0, 0, 0, -1, None, ctypes.byref(h)) == 1                     # empty region
+    assert L.hex_nvls_open_local(0, 0, ctypes.byref(h)) == 1                                # empty region
+    assert L.hex_nvls_open_local(0, 1024, None) == 1
+    if not __import__("torch").cuda.is_available():
+        assert L.hex_nvls_open_local(0, 1024, ctypes.byref(h)) == 1                         # no device
     assert L.hex_nvls_allreduce_f32(None, 0, 4, 0, None) == 1
     assert L.hex_nvls_close(None) == 1
     g = ctypes.c_int32()
